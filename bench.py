@@ -1,0 +1,408 @@
+#!/usr/bin/env python
+"""Headline benchmark: DGR training iterations/s at 256^3, 50k Gaussians, 50 views.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+A "step" is one full training iteration (optim.py:350-403 with densify off):
+project -> L1+SSIM+TV loss -> adjoint -> splat adjoint -> Adam -> re-splat.
+Workload (BASELINE.json configs[1]): 256^3 synthetic
+chest phantom, 50,000 Gaussians (init_cloud_fbp sampling of the phantom,
+seed 0, sigma 1.5, box 17^3), fan stand-in for the 512^2-detector scan:
+50 views x 512 detectors per slice, spacing 1.6, rs = rd = 512, 256 slices.
+Under torchrun (N > 1) the volume is z-slab sharded across ranks (strong
+scaling: the same problem on more GPUs); time = max over ranks.
+
+One JSON line on rank 0.  ``--impl reference`` times the reference
+algorithm's CPU implementation (the oracle port, oracle/, all host cores) on
+the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "train iters/s @256³, 50k Gaussians, 50 views; voxelize HBM GB/s vs roofline"
+
+CONFIGS = {
+    "c2": dict(dims=(256, 256, 256), n=50_000, views=50, n_det=512, spacing=1.6, rs=512.0,
+               rd=512.0, variant="fan", phantom="chest",
+               label="C2: 256^3 chest phantom, 50k Gaussians, 50-view fan (512 det/slice, "
+                     "spacing 1.6, rs=rd=512), box 17^3"),
+    "c3": dict(dims=(256, 256, 256), n=50_000, views=25, n_det=512, spacing=1.6, rs=512.0,
+               rd=512.0, variant="fan", phantom="chest",
+               label="C3: 256^3 chest phantom, 50k Gaussians, 25-view fan (512 det/slice)"),
+    "c1": dict(dims=(64, 64, 64), n=10_000, views=25, n_det=96, spacing=1.0, variant="parallel",
+               phantom="shepp", label="C1: 64^3 Shepp-Logan, 10k Gaussians, 25-view parallel"),
+    "c4": dict(dims=(512, 512, 512), n=400_000, views=100, n_det=1024, spacing=1.6, rs=1024.0,
+               rd=1024.0, variant="fan", phantom="chest",
+               label="C4: 512^3 chest phantom, 400k Gaussians, 100-view fan (1024 det/slice)"),
+}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def make_problem(cfg):
+    """Host inputs shared by both arms: truth, geometry, initial cloud."""
+    from paper_2411_04844_b200 import core, optim, phantom
+    w, h, c = cfg["dims"]
+    truth = (phantom.chest_3d(w, h, c) if cfg["phantom"] == "chest"
+             else phantom.shepp_logan_3d(w, h, c))
+    if cfg["variant"] == "fan":
+        geom = core.ScanGeometry.fan(cfg["views"], cfg["n_det"], cfg["spacing"], cfg["rs"],
+                                     cfg["rd"])
+    else:
+        geom = core.ScanGeometry.parallel(cfg["views"], cfg["n_det"], cfg["spacing"])
+    box = core.BoxConfig.for_dims(17, cfg["dims"])
+    cloud = optim.init_cloud_fbp(truth, cfg["n"], seed=0, box=box)
+    return truth, geom, box, cloud
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        time.sleep(0.05)
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[4 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def cpu_reference_iters(cfg, steps, warmup, threads=None):
+    """Time the oracle (the reference algorithm's CPU port) on the workload."""
+    from oracle import oracle as O
+    if threads:
+        O.set_num_threads(threads)
+    truth, geom, box, cloud = make_problem(cfg)
+    og = (O.Geometry.fan(cfg["views"], cfg["n_det"], cfg["spacing"], cfg["rs"], cfg["rd"])
+          if cfg["variant"] == "fan" else O.Geometry.parallel(cfg["views"], cfg["n_det"],
+                                                              cfg["spacing"]))
+    meas = O.project_forward(truth.zyx, og)
+    args = (meas, og, cfg["dims"], box.shape, cloud.mu, cloud.sigma, cloud.intensity, 1000)
+    if warmup:
+        O.train(*args, iters_to_run=warmup)
+    t0 = time.perf_counter()
+    O.train(*args, iters_to_run=steps)
+    dt = time.perf_counter() - t0
+    return steps / dt, dt, O.num_threads()
+
+
+def stage_profile(tr, iters):
+    """Per-stage device time of eager iterations (CUDA events on the launch stream)."""
+    import torch
+    from paper_2411_04844_b200 import device as D
+    from paper_2411_04844_b200 import _lib
+    s = torch.cuda.current_stream()
+    names = ["proj_forward", "loss_fused", "proj_adjoint_tv", "finalize", "fvr_backward", "adam",
+             "fvr_bin", "fvr_forward"]
+    acc = {k: 0.0 for k in names}
+    lw = tr.weights
+    launches = 0
+    for _ in range(iters):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(names) + 1)]
+        l0 = _lib.launch_count()
+        ev[0].record(s)
+        tr.op.forward(tr.vol, tr.pred, tr.halt)
+        ev[1].record(s)
+        tr.loss.fused(tr.pred, tr.meas, tr.lmax, lw.lambda1, lw.lambda2, tr.l1_count,
+                      float(tr.slab.c_global), tr.gpred, tr.sums, tr.halt)
+        ev[2].record(s)
+        lo, hi = tr.comm.halo(tr.vol)
+        tr.op.adjoint(tr.gpred, tr.dl, vol=tr.vol, halo_lo=lo, halo_hi=hi,
+                      lambda_tv=lw.lambda3, tv_count=tr.tv_count, tv_partial=tr.tv_part,
+                      halt=tr.halt)
+        D.reduce_sum(tr.tv_part, tr.sums[2:3])
+        ev[3].record(s)
+        tr.comm.allreduce_sum_(tr.sums)
+        D.call("splatct_iter_finalize", D.ptr(tr.sums), float(lw.lambda1), float(lw.lambda2),
+               float(lw.lambda3), tr.l1_count, tr.ssim_count, tr.tv_count, tr.lr0, tr.lrf,
+               tr.max_iters, D.ptr(tr.step_t), D.ptr(tr.iter_t), D.ptr(tr.trace), tr.trace_cap,
+               D.ptr(tr.adam_s), D.ptr(tr.halt), D.stream_handle())
+        ev[4].record(s)
+        sharded = tr.comm.world > 1
+        tr.fvr.backward(tr.params, tr.dl, tr.grads, None if sharded else tr.accum, tr.halt)
+        if sharded:
+            tr.comm.allreduce_sum_(tr.grads)
+            D.grad_norm_accum(tr.grads, tr.accum, tr.halt)
+        ev[5].record(s)
+        D.adam(tr.params, tr.grads, tr.m1, tr.m2, tr.adam_s, 0.3, tr.sigma_ceiling, tr.halt)
+        ev[6].record(s)
+        tr.fvr.bin(tr.params, tr.halt)
+        ev[7].record(s)
+        tr.fvr.forward(tr.params, tr.vol, tr.halt)
+        ev[8].record(s)
+        torch.cuda.synchronize()
+        launches = _lib.launch_count() - l0
+        for k, nm in enumerate(names):
+            acc[nm] += ev[k].elapsed_time(ev[k + 1])
+    return {k: v / iters for k, v in acc.items()}, launches
+
+
+def run_b200(args, cfg):
+    import torch
+    import torch.distributed as dist
+    from paper_2411_04844_b200 import device as D
+    from paper_2411_04844_b200 import loss as L
+    from paper_2411_04844_b200 import optim, _lib
+    from paper_2411_04844_b200.core import Sinogram
+    from paper_2411_04844_b200.distributed import (SlabComm, init_from_env,
+                                                   run_reconstruction_sharded, slab_bounds)
+    from paper_2411_04844_b200.trainer import NullComm, Trainer
+
+    rank, world = init_from_env("nccl")
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    comm = SlabComm() if world > 1 else NullComm()
+    truth, geom, box, cloud = make_problem(cfg)
+    w, h, c = cfg["dims"]
+    s = slab_bounds(c, world, rank)
+    # measured projections of the phantom (same operator as the model)
+    op = D.projector_for(geom, w, h, 0.5, dev)
+    tslab = np.ascontiguousarray(truth.zyx[s.z0:s.z0 + s.c_local])
+    meas_local = op.forward(D.zyx_to_yxz(tslab, dev))
+    params = D.cloud_to_params(cloud, dev)
+    tr = Trainer(meas_local, geom, cfg["dims"], box, L.LossWeights(), params, max_iters=1000,
+                 slab=s, comm=comm, trace_cap=args.warmup + args.steps + 16)
+    tr.initial_volume()
+    use_graph = world == 1
+    done = 0
+    if use_graph:
+        done = tr.capture()
+    for _ in range(max(args.warmup - done, 0)):
+        tr.step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.start()
+        time.sleep(0.3)
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.steps):
+        tr.step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clocks = sampler.stop() if sampler else None
+    ms_local = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    ms = float(t.item())
+    if tr.halted():
+        raise RuntimeError("non-finite loss during the benchmark")
+    loss_last = float(tr.trace_rows()[-1, 0])
+
+    # per-stage device times (eager, instrumented) + launch count
+    stages, launches = stage_profile(tr, 5)
+    st = torch.tensor([stages[k] for k in sorted(stages)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(st, op=dist.ReduceOp.MAX)
+    stages = {k: float(v) for k, v in zip(sorted(stages), st.tolist())}
+
+    # end-to-end through the public API with host buffers
+    e2e = None
+    if world == 1:
+        meas_host = Sinogram.from_views(meas_local.cpu().numpy())
+        settings = optim.ReconstructionSettings(dims=cfg["dims"], box=box, max_iters=args.steps,
+                                                n_gaussians=cfg["n"], densify_interval=0)
+        optim.run_reconstruction(meas_host, geom, settings, init_cloud=cloud)   # warm
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        vol, cl_out, trace = optim.run_reconstruction(meas_host, geom, settings, init_cloud=cloud)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+    else:
+        meas_host = Sinogram.from_views(
+            np.concatenate([op.forward(D.zyx_to_yxz(np.ascontiguousarray(
+                truth.zyx[b.z0:b.z0 + b.c_local]), dev)).cpu().numpy()
+                for b in [slab_bounds(c, world, r) for r in range(world)]], axis=2))
+        settings = optim.ReconstructionSettings(dims=cfg["dims"], box=box, max_iters=args.steps,
+                                                n_gaussians=cfg["n"], densify_interval=0)
+        dist.barrier()
+        t0 = time.perf_counter()
+        run_reconstruction_sharded(meas_host, geom, settings, cloud, comm=comm)
+        torch.cuda.synchronize()
+        dt_t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        dist.all_reduce(dt_t, op=dist.ReduceOp.MAX)
+        dt = float(dt_t.item())
+    m, n = cfg["views"], cfg["n_det"]
+    sino_b = m * n * c * 4
+    cloud_b = cfg["n"] * 5 * 8
+    e2e = {"value": args.steps / dt, "unit": "iterations/s",
+           "h2d_bytes_per_step": int((sino_b + 3 * cloud_b) / args.steps),
+           "d2h_bytes_per_step": int((w * h * c * 4 + cloud_b + 32 * args.steps) / args.steps),
+           "api": "optim.run_reconstruction" if world == 1 else
+                  "distributed.run_reconstruction_sharded",
+           "includes": "H2D of measured sinogram + cloud, operator lookup, plans, "
+                       "initial splat, K iterations, D2H of volume + cloud + trace"}
+
+    # roofline: algorithmic bytes per launch / measured duration
+    peak, peak_src = load_peaks()
+    N = cfg["n"]
+    cl = s.c_local
+    vol_b = w * h * cl * 4
+    sino_l = m * n * cl * 4
+    nnz = op.nnz
+    alg = {
+        "proj_forward": 8 * nnz + vol_b + sino_l,
+        "proj_adjoint_tv": 8 * nnz + sino_l + 2 * vol_b,
+        "loss_fused": 3 * sino_l,
+        "fvr_forward": 40 * N + vol_b,
+        "fvr_backward": 96 * N + vol_b,
+    }
+
+    def roof(name):
+        a = alg[name] / (stages[name] * 1e-3) / 1e9
+        return {"kernel": name, "bound": "hbm", "achieved": round(a, 1), "peak": peak,
+                "unit": "GB/s", "frac": round(a / peak, 4), "traffic": None,
+                "ms": round(stages[name], 4), "algorithmic_bytes": int(alg[name])}
+
+    dominant = max(alg, key=lambda k: stages[k])
+    fl = np.floor(cloud.mu)
+    hv = np.array(box.half)
+    dimv = np.array(cfg["dims"])
+    span = np.minimum(fl + hv, dimv - 1) - np.maximum(fl - hv, 0) + 1
+    contributions = int(np.prod(np.clip(span, 0, None), axis=1).sum())
+    out = {
+        "metric": METRIC, "value": round(1000.0 / ms, 3), "unit": "iterations/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": cfg["label"], "dims": list(cfg["dims"]), "n_gaussians": N,
+                   "views": m, "detectors_per_slice": n, "geometry": cfg["variant"],
+                   "init": "init_cloud_fbp sampling of the phantom, seed 0",
+                   "densify": "off (densify_interval=0, SURVEY D7)",
+                   "precision": "f32 voxelizer/projector, f64 params/Adam/SSIM statistics",
+                   "cache": "per-iteration working set (A, A^T, volume, sinograms) > 126 MB L2; "
+                            "no flush",
+                   "parallelism": f"zslab{world}", "cuda_graph": use_graph,
+                   "projector_nnz": nnz},
+        "roofline": {**roof(dominant), "peak_source": peak_src},
+        "voxelize": {"fwd": roof("fvr_forward"), "bwd": roof("fvr_backward"),
+                     "contributions_per_iter": contributions,
+                     "fwd_contributions_per_s": contributions / (stages["fvr_forward"] * 1e-3),
+                     "bwd_contributions_per_s": contributions / (stages["fvr_backward"] * 1e-3)},
+        "stages_ms": {k: round(v, 4) for k, v in stages.items()},
+        "e2e": e2e,
+        "gpu_launches": int(launches * args.steps),
+        "clocks": clocks,
+        "last_loss": loss_last,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, dt, cores = cpu_reference_iters(cfg, args.cpu_iters, 0)
+        out["cpu_baseline"] = {"value": round(v, 5), "unit": "iterations/s", "cores": cores,
+                               "kind": "port",
+                               "sample": f"{args.cpu_iters} full training iteration(s) of the "
+                                         f"same workload, oracle/ C+OpenMP port, {dt:.1f} s"}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    steps = max(1, min(args.steps, args.ref_max_steps))
+    warm = min(args.warmup, 1)
+    v, dt, cores = cpu_reference_iters(cfg, steps, warm)
+    out = {"metric": METRIC, "value": round(v, 5), "unit": "iterations/s",
+           "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": steps, "warmup": warm,
+           "ms_per_step": round(1000 * dt / steps, 2), "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "impl": "reference",
+           "config": {"workload": cfg["label"], "dims": list(cfg["dims"]), "n_gaussians": cfg["n"],
+                      "parallelism": f"cpu{cores}"},
+           "cpu_baseline": {"value": round(v, 5), "unit": "iterations/s", "cores": cores,
+                            "kind": "port",
+                            "sample": f"{steps} timed full iteration(s) after {warm} warm-up, "
+                                      "oracle/ C+OpenMP restatement of the reference"},
+           "e2e": {"value": round(v, 5), "unit": "iterations/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--cpu-iters", type=int, default=1)
+    ap.add_argument("--ref-max-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_b200(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,229 @@
+/*
+ * splatct.h -- C ABI of libsplatct.so, the B200 (sm_100a) hot path of DGR
+ * Fast Volume Reconstruction (arXiv 2411.04844).
+ *
+ * Every entry point is extern "C", takes plain device pointers, explicit
+ * sizes and a CUDA stream (as void*), never allocates, never synchronises
+ * (except the two *_count setup calls, which return a size to the host), and
+ * returns 0 on success or a SPLATCT_ERR_* code; splatct_last_error() then
+ * holds a thread-local message.  Validation of domain invariants stays in the
+ * Python layer (as in the reference, fvr.py:123-139).
+ *
+ * Each function names the reference interface it replaces
+ * (paths relative to /root/reference/pkg/src/splatct/).
+ *
+ * Device layouts (chosen for B200):
+ *   params  double[5][n]  rows mu_x, mu_y, mu_z, sigma, intensity
+ *           (GaussianCloud, core.py:211-235; kept in f64 like the reference
+ *           so floor(mu) -- the footprint -- is bit-exact)
+ *   grads   double[5][n]  d_mu_x, d_mu_y, d_mu_z, d_sigma, d_intensity
+ *           (ParamGradients, core.py:278-303)
+ *   volume  float[h][w][c]   "yxz": slice index fastest, i.e. one contiguous
+ *           c-vector per (y, x) pixel column.  The reference's VolumeGrid is
+ *           (c,h,w) x-fastest (core.py:9-11); the Python layer transposes at
+ *           the API edge.
+ *   sinogram float[m][n][p]  identical to the reference (core.py:12-13):
+ *           one contiguous p-vector per (view, detector) ray.
+ */
+#ifndef SPLATCT_H
+#define SPLATCT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPLATCT_OK 0
+#define SPLATCT_ERR_INVALID 1
+#define SPLATCT_ERR_CUDA 2
+
+#define SPLATCT_ABI_VERSION 1
+
+int splatct_abi_version(void);
+const char* splatct_last_error(void);
+/* Number of kernels this library has launched (process lifetime). */
+unsigned long long splatct_launch_count(void);
+
+/* ---------------------------------------------------------------------------
+ * Voxelizer ("FVR"): fvr.reconstruct / fvr.backward (fvr.py:148-167,
+ * 227-273) replacing _kernels.splat_decomposed (_kernels.py:22-78) and
+ * _kernels.splat_backward (_kernels.py:132-205).
+ * Tiles are SPLATCT_TILE^3 voxels; a Gaussian's footprint is
+ * [floor(mu_a)-h_a, floor(mu_a)+h_a] intersect [0, dim_a) (_kernels.py:45-78).
+ * (w, h, c) are the dims of the local volume; z0 is its origin in the global
+ * volume (0 unless the volume is a z-slab of a sharded volume): local voxel
+ * z holds global slice z0 + z, and footprints are clipped to the slab.
+ * ------------------------------------------------------------------------- */
+#define SPLATCT_TILE 16
+
+/* Bytes of the caller-provided voxelizer workspace (bins, sort buffers,
+ * backward partials) for n Gaussians on a (w,h,c) grid with box halves. */
+int splatct_fvr_workspace_bytes(int64_t n, int w, int h, int c, int hx, int hy, int hz,
+                                size_t* bytes);
+
+/* Footprints + radix-sorted (tile, Gaussian) bin lists into ws.  Replaces the
+ * implicit per-Gaussian box loop of _kernels.py:42-78 (no reference
+ * counterpart for tiles).  halt: optional device flag; non-zero skips work. */
+int splatct_fvr_bin(const double* params, int64_t n, int w, int h, int c, int z0, int hx,
+                    int hy, int hz, void* ws, size_t ws_bytes, const int* halt, void* stream);
+
+/* V = sum_i I_i ex_i (x) ey_i (x) ez_i over box intersect volume; one CTA per
+ * tile accumulating in registers/shared memory, each voxel written once
+ * (no memset, no global atomics).  Requires a prior splatct_fvr_bin on the
+ * same params.  Replaces _kernels.splat_decomposed(mu, sigma, intensity,
+ * hx, hy, hz, w, h, c, bufs) (_kernels.py:23) + fvr.py:163-167. */
+int splatct_fvr_forward(const double* params, int64_t n, int w, int h, int c, int z0, int hx,
+                        int hy, int hz, const void* ws, size_t ws_bytes, float* vol_yxz,
+                        const int* halt, void* stream);
+
+/* Per-Gaussian gradients from dL/dV (yxz), fvr.py:227-273: per-tile partial
+ * moments, combined per Gaussian in fixed slot order (deterministic).
+ * grads: double[5][n] (overwritten).  accum: optional double[n]; if non-NULL
+ * accum[i] += |d_mu_i| (fvr.py:266-273).  Requires the bins of
+ * splatct_fvr_bin on the same params.  Replaces _kernels.splat_backward(mu,
+ * sigma, intensity, hx, hy, hz, w, h, c, upstream, d_mu, d_sigma,
+ * d_intensity) (_kernels.py:133-134). */
+int splatct_fvr_backward(const double* params, int64_t n, int w, int h, int c, int z0, int hx,
+                         int hy, int hz, void* ws, size_t ws_bytes, const float* up_yxz,
+                         double* grads, double* accum, const int* halt, void* stream);
+
+/* accum[i] += |(grads[0][i], grads[1][i], grads[2][i])| -- the densification
+ * statistic of fvr.py:266-273, applied after the cross-slab gradient
+ * all-reduce when the volume is sharded. */
+int splatct_grad_norm_accum(const double* grads, int64_t n, double* accum, const int* halt,
+                            void* stream);
+
+/* Copy the bins out for the bit-exact check against the CPU restatement.
+ * fp: int32[n][6] {xlo,xhi,ylo,yhi,zlo,zhi} (empty axis: lo>hi);
+ * tile_start: int32[n_tiles+1]; items: int32[npairs] Gaussian ids, per tile
+ * ascending.  *npairs and *n_tiles are written to host memory (synchronous). */
+int splatct_fvr_export_bins(const void* ws, size_t ws_bytes, int64_t n, int w, int h, int c,
+                            int hx, int hy, int hz, int32_t* fp, int32_t* tile_start,
+                            int32_t* items, int64_t* npairs, int64_t* n_tiles, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Projector: forward_project / back_project (projector.py:59-111) replacing
+ * _kernels.project_forward (_kernels.py:262-303) and project_adjoint
+ * (_kernels.py:306-357).  The per-slice geometry is slice-invariant, so the
+ * ray march (_ray_geometry/_clip_ray, _kernels.py:208-259, in f64) runs once
+ * per geometry and produces the exact sample weights merged per (ray, pixel):
+ * A (ray-major CSR) and its exact transpose A^T (pixel-major CSR).  Each
+ * iteration then applies them to the z-vectors of the yxz volume / sinogram.
+ * cos_t, sin_t: device double[m] (projector.py:50-52, f64 on host).
+ * ------------------------------------------------------------------------- */
+
+/* Scratch bytes for splatct_proj_count (nnz = 0) and splatct_proj_fill
+ * (nnz = the count returned by splatct_proj_count). */
+int splatct_proj_scratch_bytes(int m, int n_det, int w, int h, int64_t nnz, size_t* bytes);
+
+/* Pass 1 (synchronous): a_ptr (device int64[m*n_det+1]) = row offsets of A;
+ * *nnz (host) = number of merged (ray, pixel) weights. */
+int splatct_proj_count(const double* cos_t, const double* sin_t, int m, int n_det,
+                       double spacing, double step, int is_fan, double rs, double rd, int w,
+                       int h, int64_t* a_ptr, void* scratch, size_t scratch_bytes,
+                       int64_t* nnz, void* stream);
+
+/* Pass 2: fills A (a_col = pixel y*w+x, a_val = step * merged bilinear
+ * weight) and A^T (at_ptr int64[w*h+1], at_ray, at_val; rows sorted by ray). */
+int splatct_proj_fill(const double* cos_t, const double* sin_t, int m, int n_det,
+                      double spacing, double step, int is_fan, double rs, double rd, int w,
+                      int h, const int64_t* a_ptr, int32_t* a_col, float* a_val,
+                      int64_t* at_ptr, int32_t* at_ray, float* at_val, void* scratch,
+                      size_t scratch_bytes, void* stream);
+
+/* sino[r][z] = sum_j a_val[j] * vol[a_col[j]][z]  for r < n_rays, z < c. */
+int splatct_proj_forward(const int64_t* a_ptr, const int32_t* a_col, const float* a_val,
+                         int n_rays, const float* vol_yxz, float* sino, int c,
+                         const int* halt, void* stream);
+
+/* out[p][z] = f32( sum_j at_val[j] * gsino[at_ray[j]][z] + lambda_tv * tvgrad(p,z) )
+ * with tvgrad the anisotropic TV subgradient of vol / tv_count
+ * (loss.tv_loss, loss.py:183-207) fused in; tv_partial (optional, double[w*h])
+ * receives per-pixel-column sums of |forward differences| of vol.
+ * halo_lo / halo_hi (optional, float[h*w]) are the neighbouring z-planes
+ * z = -1 and z = c of a z-slab (NULL at the global volume edges); the
+ * forward difference into halo_hi is counted by this slab.
+ * Pass vol = NULL / lambda_tv = 0 for the plain adjoint. */
+int splatct_proj_adjoint(const int64_t* at_ptr, const int32_t* at_ray, const float* at_val,
+                         int w, int h, int c, const float* gsino, const float* vol_yxz,
+                         const float* halo_lo, const float* halo_hi, double lambda_tv,
+                         double tv_count, float* out_yxz, double* tv_partial, const int* halt,
+                         void* stream);
+
+/* Direct ray-marching forward projection (no matrix), same f64 ray setup and
+ * sample enumeration as _kernels.py:262-303; used as a cross-check and for
+ * one-off projections. */
+int splatct_proj_march_forward(const double* cos_t, const double* sin_t, int m, int n_det,
+                               double spacing, double step, int is_fan, double rs, double rd,
+                               int w, int h, int c, const float* vol_yxz, float* sino,
+                               void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Loss: loss.total_loss_detailed (loss.py:210-239): L1 (loss.py:64-74) and
+ * valid-window SSIM (loss.py:77-180) of pred vs ref, both (m,n,p), with the
+ * analytic gradient written as f32 (optim.py:368 quantisation).
+ * ------------------------------------------------------------------------- */
+
+int splatct_loss_workspace_bytes(int m, int n, int p, size_t* bytes);
+
+/* out[0] = max(ref) over all bins (double) -- the SSIM dynamic range L. */
+int splatct_sino_max(const float* x, int64_t count, double* out, void* stream);
+
+/* grad_pred = lambda1*sign(pred-ref)/l1_count - lambda2*dSSIM/dpred/ssim_slices.
+ * sums (device double[2]) receive sum|pred-ref| and sum over local slices of
+ * mean-SSIM.  lmax: global max(ref) (<=0 -> 1).  l1_count and ssim_slices are
+ * GLOBAL counts (they differ from m*n*p under z-slab sharding). */
+int splatct_loss_fused(const float* pred, const float* ref, int m, int n, int p, double lmax,
+                       double lambda1, double lambda2, double l1_count, double ssim_slices,
+                       float* grad_pred, void* ws, size_t ws_bytes, double* sums,
+                       const int* halt, void* stream);
+
+/* out[0] = sum (x-y)^2 over count elements (f64, fixed order); ws holds
+ * SPLATCT_SQDIFF_BLOCKS doubles.  Used for PSNR (metrics.psnr, metrics.py:24-38). */
+#define SPLATCT_SQDIFF_BLOCKS 592
+int splatct_sum_sq_diff(const float* x, const float* y, int64_t count, double* ws, double* out,
+                        void* stream);
+
+/* Sum n doubles in a fixed order into out[0] (deterministic reductions). */
+int splatct_reduce_sum(const double* in, int64_t n, double* out, void* stream);
+
+/* Iteration bookkeeping (optim.py:350-386): from the global sums
+ * {l1_sum, ssim_sum, tv_sum} compute the loss parts
+ * (zero-weight terms -> NaN, loss.py:216-239), write
+ * trace[4*it .. 4*it+3] = {loss, l1, ssim, tv} with it = *iter, set *halt if
+ * the loss is non-finite (optim.py:356), else write the Adam scalars
+ * adam[0..2] = {lr, 1-b1^t, 1-b2^t} for the pre-increment *step
+ * (optim.py:88-90,123-126) and advance *step and *iter. */
+int splatct_iter_finalize(const double* sums, double lambda1, double lambda2, double lambda3,
+                          double l1_count, double ssim_count, double tv_count, double lr0,
+                          double lrf, int64_t max_iters, int64_t* step, int64_t* iter,
+                          double* trace, int64_t trace_cap, double* adam, int* halt,
+                          void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Adam: optim.adam_step (optim.py:109-144): bias-corrected Adam on the
+ * params block with scalars adam = {lr, bc1, bc2} from splatct_iter_finalize
+ * (device), then sigma clamped to [sigma_floor, sigma_ceiling], intensity >= 0.
+ * ------------------------------------------------------------------------- */
+int splatct_adam(double* params, const double* grads, double* m1, double* m2, int64_t n,
+                 const double* adam, double sigma_floor, double sigma_ceiling,
+                 const int* halt, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * FBP initialiser (projector.fbp, projector.py:154-206; out of the iteration
+ * loop): filtered rows (host-filtered or device) are back-projected
+ * pixel-driven, _kernels.backproject_parallel_beam / backproject_fan_beam
+ * (_kernels.py:360-419).  filtered: (m, n, p) like the sinogram; out yxz.
+ * ------------------------------------------------------------------------- */
+int splatct_fbp_filter(const float* sino, int m, int n, int p, const double* kernel,
+                       const double* det_weight, double* filtered, void* stream);
+int splatct_fbp_backproject(const double* filtered, const double* cos_t, const double* sin_t,
+                            int m, int n, int p, int w, int h, double spacing, double dbeta,
+                            int is_fan, double rs, float* out_yxz, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPLATCT_H */

@@ -1,0 +1,87 @@
+// common.cuh -- shared helpers for the splatct sm_100a kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "../../include/splatct.h"
+
+namespace splatct {
+
+// Thread-local last-error message (the C-ABI's only global state).
+void set_error_msg(const char* fmt, ...);
+
+#define SPLATCT_CK(expr)                                                          \
+    do {                                                                          \
+        cudaError_t e_ = (expr);                                                  \
+        if (e_ != cudaSuccess) {                                                  \
+            ::splatct::set_error_msg("%s:%d %s: %s", __FILE__, __LINE__, #expr,   \
+                                     cudaGetErrorString(e_));                     \
+            return SPLATCT_ERR_CUDA;                                              \
+        }                                                                         \
+    } while (0)
+
+// Every kernel launch goes through SPLATCT_LAUNCH_CK, which also counts it
+// (splatct_launch_count(): the evidence for bench.py's gpu_launches).
+void count_launch();
+#define SPLATCT_LAUNCH_CK()            \
+    do {                               \
+        ::splatct::count_launch();     \
+        SPLATCT_CK(cudaGetLastError()); \
+    } while (0)
+
+#define SPLATCT_REQUIRE(cond, ...)                                                \
+    do {                                                                          \
+        if (!(cond)) {                                                            \
+            ::splatct::set_error_msg(__VA_ARGS__);                                \
+            return SPLATCT_ERR_INVALID;                                           \
+        }                                                                         \
+    } while (0)
+
+static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+static inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+// Early-out for kernels inside a training iteration once a non-finite loss
+// has been recorded (mirrors optim.py:356-366 aborting before the update).
+__device__ __forceinline__ bool halted(const int* halt) {
+    return halt != nullptr && *(volatile const int*)halt != 0;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Block-wide sum of a double into lane 0 of warp 0 (deterministic order).
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* sh /* >= NT/32 */) {
+    v = warp_sum(v);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) sh[wid] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (wid == 0) {
+        r = lane < NT / 32 ? sh[lane] : 0.0;
+        r = warp_sum(r);
+    }
+    __syncthreads();
+    return r;
+}
+
+// Device-wide exclusive scan helpers (scan.cu).
+size_t scan_temp_bytes(int64_t n);
+int exclusive_scan_i64(const int64_t* in, int64_t* out, int64_t n, void* temp, cudaStream_t s);
+int exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, void* temp, cudaStream_t s);
+
+// Sum of n doubles in fixed order into out[0] (one CTA).
+int reduce_sum_f64(const double* in, int64_t n, double* out, cudaStream_t s);
+
+}  // namespace splatct

@@ -1,0 +1,568 @@
+// fvr.cu -- Fast Volume Reconstruction on B200: footprints, radix-sorted
+// tile bins, tile-owned forward splat, tile-partial backward + deterministic
+// per-Gaussian combine.
+//
+// Reference semantics (paths under /root/reference/pkg/src/splatct/):
+//   footprint  [floor(mu_a)-h_a, floor(mu_a)+h_a] intersect [0, dim_a)
+//              _kernels.py:45-47,61-78 (true floor, out-of-volume dropped)
+//   forward    V[z,y,x] += I * ez[oz] * ey[oy] * ex[ox]           _kernels.py:51-78
+//              e[k] = exp(-(b - d)^2 / (2 sigma^2)), b = k - h, d = mu - floor(mu)
+//   backward   dI += u g ; dmu += u g I r / sigma^2 ; dsigma += u g I |r|^2 / sigma^3
+//              _kernels.py:132-205 ; accum += |dmu| fvr.py:266-273
+//
+// B200 design:
+//   * volume stored yxz (slice fastest) so a tile's (y,x) column is a
+//     contiguous 64 B segment;
+//   * (tile, Gaussian) pairs emitted per Gaussian in slot order and stably
+//     LSD-radix-sorted by tile id -> per-tile lists in ascending Gaussian id
+//     (bit-exact against the CPU restatement, deterministic sums);
+//   * forward: one CTA per 16^3 tile, each thread owns a (y,x) column of 16
+//     voxels in registers; per-Gaussian separable tables staged in shared
+//     memory; every voxel stored exactly once (no memset, no atomics);
+//   * backward: one CTA per tile, upstream tile staged in shared memory, one
+//     warp per (tile, Gaussian) pair, separable moment contraction
+//     (x in the loop, then y, then z), warp-shuffle reduction, partials
+//     written to the pair's original slot; combine sums slots in fixed order.
+#include "common.cuh"
+
+namespace splatct {
+
+constexpr int TT = SPLATCT_TILE;   // tile edge (16)
+constexpr int SORT_NT = 256;
+constexpr int SORT_IPT = 8;
+constexpr int SORT_CHUNK = SORT_NT * SORT_IPT;
+constexpr int RADIX = 256;
+
+struct FvrLayout {
+    int64_t n;
+    int w, h, c, hx, hy, hz;
+    int ntx, nty, ntz;
+    int64_t nt;
+    int S;            // max tiles per Gaussian (slots)
+    int64_t np;       // n * S
+    int passes;
+    int64_t sort_blocks;
+    size_t o_fp, o_gcount, o_k0, o_v0, o_k1, o_v1, o_tcount, o_tstart, o_hist, o_scan, o_part,
+        total;
+    int final_buf;    // which (k,v) buffer holds the sorted result
+};
+
+static int axis_span(int half, int dim) {
+    int s = (2 * half + TT - 1) / TT + 1;
+    int nta = (dim + TT - 1) / TT;
+    return s < nta ? s : nta;
+}
+
+static FvrLayout make_layout(int64_t n, int w, int h, int c, int hx, int hy, int hz) {
+    FvrLayout L{};
+    L.n = n;
+    L.w = w; L.h = h; L.c = c; L.hx = hx; L.hy = hy; L.hz = hz;
+    L.ntx = (w + TT - 1) / TT;
+    L.nty = (h + TT - 1) / TT;
+    L.ntz = (c + TT - 1) / TT;
+    L.nt = (int64_t)L.ntx * L.nty * L.ntz;
+    L.S = axis_span(hx, w) * axis_span(hy, h) * axis_span(hz, c);
+    L.np = n * L.S;
+    int bits = 0;
+    while (((int64_t)1 << bits) <= L.nt) ++bits;   // keys in [0, nt] (nt = sentinel)
+    L.passes = (bits + 7) / 8;
+    if (L.passes < 1) L.passes = 1;
+    L.sort_blocks = (L.np + SORT_CHUNK - 1) / SORT_CHUNK;
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off += align_up(bytes > 0 ? bytes : 1); return o; };
+    L.o_fp = take(sizeof(int32_t) * 6 * (size_t)n);
+    L.o_gcount = take(sizeof(int32_t) * (size_t)n);
+    L.o_k0 = take(sizeof(uint32_t) * (size_t)L.np);
+    L.o_v0 = take(sizeof(uint32_t) * (size_t)L.np);
+    L.o_k1 = take(sizeof(uint32_t) * (size_t)L.np);
+    L.o_v1 = take(sizeof(uint32_t) * (size_t)L.np);
+    L.o_tcount = take(sizeof(uint32_t) * (size_t)(L.nt + 1));
+    L.o_tstart = take(sizeof(uint32_t) * (size_t)(L.nt + 1));
+    L.o_hist = take(sizeof(uint32_t) * RADIX * (size_t)(L.sort_blocks > 0 ? L.sort_blocks : 1));
+    size_t sc1 = scan_temp_bytes(RADIX * (L.sort_blocks > 0 ? L.sort_blocks : 1));
+    size_t sc2 = scan_temp_bytes(L.nt + 1);
+    L.o_scan = take(sc1 > sc2 ? sc1 : sc2);
+    L.o_part = take(sizeof(float) * 5 * (size_t)L.np);
+    L.total = off;
+    L.final_buf = L.passes % 2;   // pass p reads buf p%2, writes (p+1)%2
+    return L;
+}
+
+template <typename T>
+static inline T* at(void* base, size_t off) {
+    return reinterpret_cast<T*>(reinterpret_cast<char*>(base) + off);
+}
+template <typename T>
+static inline const T* at(const void* base, size_t off) {
+    return reinterpret_cast<const T*>(reinterpret_cast<const char*>(base) + off);
+}
+
+// --------------------------------------------------------------------------
+// footprints + pair emission
+// --------------------------------------------------------------------------
+__global__ void k_footprint(const double* __restrict__ P, int64_t n, int w, int h, int c, int zoff,
+                            int hx, int hy, int hz, int ntx, int nty, int S, uint32_t sentinel,
+                            int32_t* __restrict__ fp, int32_t* __restrict__ gcount,
+                            uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                            uint32_t* __restrict__ tcount, const int* halt) {
+    if (halted(halt)) return;
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int half[3] = {hx, hy, hz};
+    const int dim[3] = {w, h, c};
+    const int org[3] = {0, 0, zoff};
+    int lo[3], hi[3];
+    bool empty = false;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        // local coordinates: global footprint minus the slab origin
+        double f = floor(P[a * n + i]) - org[a];
+        double l = f - half[a], u = f + half[a];
+        if (l < 0.0) l = 0.0;
+        if (u > dim[a] - 1) u = dim[a] - 1;
+        if (!(l <= u)) {   // also catches NaN
+            empty = true;
+            lo[a] = 1; hi[a] = 0;
+        } else {
+            lo[a] = (int)l; hi[a] = (int)u;
+        }
+        fp[6 * i + 2 * a] = lo[a];
+        fp[6 * i + 2 * a + 1] = hi[a];
+    }
+    int cnt = 0;
+    const uint32_t base = (uint32_t)(i * S);
+    if (!empty) {
+        for (int tz = lo[2] / TT; tz <= hi[2] / TT; ++tz)
+            for (int ty = lo[1] / TT; ty <= hi[1] / TT; ++ty)
+                for (int tx = lo[0] / TT; tx <= hi[0] / TT; ++tx) {
+                    uint32_t tid = (uint32_t)((tz * nty + ty) * ntx + tx);
+                    keys[base + cnt] = tid;
+                    vals[base + cnt] = base + cnt;
+                    atomicAdd(&tcount[tid], 1u);
+                    ++cnt;
+                }
+    }
+    for (int s = cnt; s < S; ++s) {
+        keys[base + s] = sentinel;
+        vals[base + s] = base + s;
+    }
+    gcount[i] = cnt;
+}
+
+// --------------------------------------------------------------------------
+// stable LSD radix sort, 8-bit digits
+// --------------------------------------------------------------------------
+__global__ void __launch_bounds__(SORT_NT) k_radix_hist(const uint32_t* __restrict__ keys,
+                                                        int64_t np, int shift, int64_t nblk,
+                                                        uint32_t* __restrict__ hist,
+                                                        const int* halt) {
+    if (halted(halt)) return;
+    __shared__ uint32_t sh[RADIX];
+    sh[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t base = blockIdx.x * (int64_t)SORT_CHUNK;
+#pragma unroll
+    for (int r = 0; r < SORT_IPT; ++r) {
+        int64_t g = base + r * SORT_NT + threadIdx.x;
+        if (g < np) atomicAdd(&sh[(keys[g] >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    hist[(int64_t)threadIdx.x * nblk + blockIdx.x] = sh[threadIdx.x];   // digit-major
+}
+
+__global__ void __launch_bounds__(SORT_NT) k_radix_scatter(
+    const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
+    uint32_t* __restrict__ kout, uint32_t* __restrict__ vout, int64_t np, int shift,
+    int64_t nblk, const uint32_t* __restrict__ hist_scanned, const int* halt) {
+    if (halted(halt)) return;
+    constexpr int NW = SORT_NT / 32;
+    __shared__ uint32_t run[RADIX];
+    __shared__ uint32_t wcnt[NW][RADIX];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    run[threadIdx.x] = hist_scanned[(int64_t)threadIdx.x * nblk + blockIdx.x];
+    const int64_t base = blockIdx.x * (int64_t)SORT_CHUNK;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    for (int r = 0; r < SORT_IPT; ++r) {
+#pragma unroll
+        for (int q = 0; q < NW; ++q) wcnt[q][threadIdx.x] = 0;
+        __syncthreads();
+        const int64_t g = base + r * SORT_NT + threadIdx.x;
+        const bool valid = g < np;
+        uint32_t k = 0, v = 0;
+        uint32_t d = RADIX;   // invalid lanes form their own group
+        if (valid) {
+            k = kin[g];
+            v = vin[g];
+            d = (k >> shift) & 255u;
+        }
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t rank = __popc(peers & lt_mask);
+        const int leader = __ffs(peers) - 1;
+        if (valid && lane == leader) wcnt[wid][d] = __popc(peers);
+        __syncthreads();
+        {   // per-digit exclusive prefix over warps, in warp order
+            uint32_t acc = run[threadIdx.x];
+#pragma unroll
+            for (int q = 0; q < NW; ++q) {
+                uint32_t t = wcnt[q][threadIdx.x];
+                wcnt[q][threadIdx.x] = acc;
+                acc += t;
+            }
+            run[threadIdx.x] = acc;
+        }
+        __syncthreads();
+        if (valid) {
+            uint32_t pos = wcnt[wid][d] + rank;
+            kout[pos] = k;
+            vout[pos] = v;
+        }
+        __syncthreads();
+    }
+}
+
+// --------------------------------------------------------------------------
+// forward: one CTA per tile, thread = (y, x) column of 16 voxels
+// --------------------------------------------------------------------------
+constexpr int FWD_BATCH = 32;
+
+__device__ __forceinline__ float axis_weight(double mu_a, float inv2, int coord, int dim, int half,
+                                             int origin) {
+    // b = coord - floor(mu); r = b - (mu - floor(mu)) evaluated in f64 then
+    // rounded; zero outside the box or the (local) volume.
+    double f = floor(mu_a);
+    double b = (double)(coord + origin) - f;
+    if (coord >= dim || fabs(b) > (double)half) return 0.f;
+    float r = (float)(b - (mu_a - f));
+    return expf(-inv2 * r * r);
+}
+
+__global__ void __launch_bounds__(256) k_fvr_fwd(const double* __restrict__ P, int64_t n, int w,
+                                                 int h, int c, int zoff, int hx, int hy, int hz,
+                                                 int ntx,
+                                                 int nty, int S,
+                                                 const uint32_t* __restrict__ tstart,
+                                                 const uint32_t* __restrict__ svals,
+                                                 float* __restrict__ vol, const int* halt) {
+    if (halted(halt)) return;
+    __shared__ __align__(16) float tab[FWD_BATCH][3][TT];
+    const int t = blockIdx.x;
+    const int txi = t % ntx, tyi = (t / ntx) % nty, tzi = t / (ntx * nty);
+    const int x0 = txi * TT, y0 = tyi * TT, z0 = tzi * TT;
+    const int tx = threadIdx.x & (TT - 1), ty = threadIdx.x / TT;
+    const uint32_t beg = tstart[t], end = tstart[t + 1];
+    float acc[TT];
+#pragma unroll
+    for (int k = 0; k < TT; ++k) acc[k] = 0.f;
+
+    for (uint32_t b0 = beg; b0 < end; b0 += FWD_BATCH) {
+        const int nb = (int)min((uint32_t)FWD_BATCH, end - b0);
+        __syncthreads();
+        for (int e = threadIdx.x; e < nb * 3 * TT; e += blockDim.x) {
+            const int g = e / (3 * TT), q = e % (3 * TT), a = q / TT, l = q % TT;
+            const int64_t gid = svals[b0 + g] / (uint32_t)S;
+            const double s = P[3 * n + gid];
+            const float inv2 = (float)(0.5 / (s * s));
+            float v;
+            if (a == 0) v = axis_weight(P[gid], inv2, x0 + l, w, hx, 0);
+            else if (a == 1) v = axis_weight(P[n + gid], inv2, y0 + l, h, hy, 0) * (float)P[4 * n + gid];
+            else v = axis_weight(P[2 * n + gid], inv2, z0 + l, c, hz, zoff);
+            tab[g][a][l] = v;
+        }
+        __syncthreads();
+        for (int g = 0; g < nb; ++g) {
+            const float cxy = tab[g][1][ty] * tab[g][0][tx];
+            if (cxy != 0.f) {
+                const float4* ez = reinterpret_cast<const float4*>(&tab[g][2][0]);
+#pragma unroll
+                for (int q = 0; q < TT / 4; ++q) {
+                    float4 e4 = ez[q];
+                    acc[4 * q + 0] = fmaf(cxy, e4.x, acc[4 * q + 0]);
+                    acc[4 * q + 1] = fmaf(cxy, e4.y, acc[4 * q + 1]);
+                    acc[4 * q + 2] = fmaf(cxy, e4.z, acc[4 * q + 2]);
+                    acc[4 * q + 3] = fmaf(cxy, e4.w, acc[4 * q + 3]);
+                }
+            }
+        }
+    }
+    const int x = x0 + tx, y = y0 + ty;
+    if (x >= w || y >= h) return;
+    float* col = vol + ((int64_t)y * w + x) * c;
+    if ((c & 3) == 0 && z0 + TT <= c) {
+        float4* dst = reinterpret_cast<float4*>(col + z0);
+#pragma unroll
+        for (int q = 0; q < TT / 4; ++q)
+            dst[q] = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < TT; ++k)
+            if (z0 + k < c) col[z0 + k] = acc[k];
+    }
+}
+
+// --------------------------------------------------------------------------
+// backward: one CTA per tile, one warp per (tile, Gaussian) pair
+// --------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_fvr_bwd(const double* __restrict__ P, int64_t n, int w,
+                                                 int h, int c, int zoff, int hx, int hy, int hz,
+                                                 int ntx,
+                                                 int nty, int S,
+                                                 const uint32_t* __restrict__ tstart,
+                                                 const uint32_t* __restrict__ svals,
+                                                 const float* __restrict__ up,
+                                                 float* __restrict__ part, const int* halt) {
+    if (halted(halt)) return;
+    __shared__ float sup[TT][TT][TT + 1];   // [y][x][z], padded
+    const int t = blockIdx.x;
+    const int txi = t % ntx, tyi = (t / ntx) % nty, tzi = t / (ntx * nty);
+    const int x0 = txi * TT, y0 = tyi * TT, z0 = tzi * TT;
+    const uint32_t beg = tstart[t], end = tstart[t + 1];
+    if (beg == end) return;
+    for (int e = threadIdx.x; e < TT * TT * TT; e += blockDim.x) {
+        const int z = e % TT, x = (e / TT) % TT, y = e / (TT * TT);
+        const int gx = x0 + x, gy = y0 + y, gz = z0 + z;
+        float u = 0.f;
+        if (gx < w && gy < h && gz < c) u = up[((int64_t)gy * w + gx) * c + gz];
+        sup[y][x][z] = u;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int zl = lane & (TT - 1), yh = lane >> 4;
+    for (uint32_t j = beg + wid; j < end; j += blockDim.x / 32) {
+        const uint32_t orig = svals[j];
+        const int64_t gid = orig / (uint32_t)S;
+        const double mx = P[gid], my = P[n + gid], mz = P[2 * n + gid], s = P[3 * n + gid];
+        const float inv2 = (float)(0.5 / (s * s));
+        const double fx = floor(mx), fy = floor(my), fz = floor(mz);
+        // lane l < 16: x-table entry l; lane l >= 16: y-table entry l-16
+        float tabw, tabr;
+        {
+            const bool isx = lane < TT;
+            const int l = lane & (TT - 1);
+            const int coord = (isx ? x0 : y0) + l;
+            const double f = isx ? fx : fy, mu_a = isx ? mx : my;
+            const int dim = isx ? w : h, half = isx ? hx : hy;
+            const double b = (double)coord - f;
+            const float r = (float)(b - (mu_a - f));
+            const bool ok = coord < dim && fabs(b) <= (double)half;
+            tabw = ok ? expf(-inv2 * r * r) : 0.f;
+            tabr = r;
+        }
+        float wz, rz;
+        {
+            const int coord = z0 + zl;
+            const double b = (double)(coord + zoff) - fz;
+            rz = (float)(b - (mz - fz));
+            wz = (coord < c && fabs(b) <= (double)hz) ? expf(-inv2 * rz * rz) : 0.f;
+        }
+        // box intersect tile, tile-local, per axis (uniform across the warp)
+        const int xlo = max((int)(fx - hx) - x0, 0), xhi = min((int)(fx + hx) - x0, TT - 1);
+        const int ylo = max((int)(fy - hy) - y0, 0), yhi = min((int)(fy + hy) - y0, TT - 1);
+        float S0 = 0.f, Sx = 0.f, Sy = 0.f, Sxy2 = 0.f;
+        const int nrows = (yhi - ylo + 2) / 2;
+        for (int k = 0; k < nrows; ++k) {
+            int y = ylo + 2 * k + yh;
+            const bool yok = y <= yhi;
+            y = yok ? y : yhi;
+            const float ey = __shfl_sync(0xffffffffu, tabw, TT + y);
+            const float ry = __shfl_sync(0xffffffffu, tabr, TT + y);
+            float p0 = 0.f, px = 0.f, pxx = 0.f;
+            for (int x = xlo; x <= xhi; ++x) {
+                const float ex = __shfl_sync(0xffffffffu, tabw, x);
+                const float rx = __shfl_sync(0xffffffffu, tabr, x);
+                const float tv = sup[y][x][zl] * ex;
+                const float tr = tv * rx;
+                p0 += tv;
+                px += tr;
+                pxx = fmaf(tr, rx, pxx);
+            }
+            const float wy = yok ? ey : 0.f;
+            S0 = fmaf(wy, p0, S0);
+            Sx = fmaf(wy, px, Sx);
+            Sy = fmaf(wy * ry, p0, Sy);
+            Sxy2 = fmaf(wy, fmaf(ry * ry, p0, pxx), Sxy2);
+        }
+        float T0 = wz * S0, Tx = wz * Sx, Ty = wz * Sy, Tz = wz * rz * S0,
+              T2 = wz * fmaf(rz * rz, S0, Sxy2);
+        T0 = warp_sum(T0);
+        Tx = warp_sum(Tx);
+        Ty = warp_sum(Ty);
+        Tz = warp_sum(Tz);
+        T2 = warp_sum(T2);
+        if (lane == 0) {
+            float* o = part + (size_t)orig * 5;
+            o[0] = T0; o[1] = Tx; o[2] = Ty; o[3] = Tz; o[4] = T2;
+        }
+    }
+}
+
+__global__ void k_fvr_combine(const double* __restrict__ P, int64_t n, int S,
+                              const int32_t* __restrict__ gcount, const float* __restrict__ part,
+                              double* __restrict__ G, double* __restrict__ accum,
+                              const int* halt) {
+    if (halted(halt)) return;
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double s0 = 0, sx = 0, sy = 0, sz = 0, s2 = 0;
+    const int cnt = gcount[i];
+    const float* p = part + (size_t)i * S * 5;
+    for (int k = 0; k < cnt; ++k) {
+        s0 += p[5 * k + 0];
+        sx += p[5 * k + 1];
+        sy += p[5 * k + 2];
+        sz += p[5 * k + 3];
+        s2 += p[5 * k + 4];
+    }
+    const double amp = P[4 * n + i], sg = P[3 * n + i];
+    const double inv_s2 = 1.0 / (sg * sg), inv_s3 = inv_s2 / sg;
+    const double k2 = amp * inv_s2;
+    const double gx = k2 * sx, gy = k2 * sy, gz = k2 * sz;
+    G[i] = gx;
+    G[n + i] = gy;
+    G[2 * n + i] = gz;
+    G[3 * n + i] = amp * inv_s3 * s2;
+    G[4 * n + i] = s0;
+    if (accum) accum[i] += sqrt(gx * gx + gy * gy + gz * gz);
+}
+
+__global__ void k_grad_norm_accum(const double* __restrict__ G, int64_t n,
+                                  double* __restrict__ accum, const int* halt) {
+    if (halted(halt)) return;
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double gx = G[i], gy = G[n + i], gz = G[2 * n + i];
+    accum[i] += sqrt(gx * gx + gy * gy + gz * gz);
+}
+
+__global__ void k_export_items(const uint32_t* __restrict__ svals, int64_t np, int S,
+                               int32_t* __restrict__ items) {
+    int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j < np) items[j] = (int32_t)(svals[j] / (uint32_t)S);
+}
+
+static int check_args(int64_t n, int w, int h, int c, int hx, int hy, int hz, size_t ws_bytes,
+                      const FvrLayout& L) {
+    SPLATCT_REQUIRE(n >= 0 && w > 0 && h > 0 && c > 0, "invalid sizes n=%lld dims=(%d,%d,%d)",
+                    (long long)n, w, h, c);
+    SPLATCT_REQUIRE(hx >= 0 && hy >= 0 && hz >= 0, "negative box half");
+    SPLATCT_REQUIRE(L.np < ((int64_t)1 << 32) - 1, "too many (tile, Gaussian) slots: %lld",
+                    (long long)L.np);
+    SPLATCT_REQUIRE(L.nt < ((int64_t)1 << 31), "too many tiles");
+    SPLATCT_REQUIRE(ws_bytes >= L.total, "workspace too small: %zu < %zu", ws_bytes, L.total);
+    return SPLATCT_OK;
+}
+
+}  // namespace splatct
+
+using namespace splatct;
+
+extern "C" {
+
+int splatct_fvr_workspace_bytes(int64_t n, int w, int h, int c, int hx, int hy, int hz,
+                                size_t* bytes) {
+    FvrLayout L = make_layout(n, w, h, c, hx, hy, hz);
+    *bytes = L.total;
+    return SPLATCT_OK;
+}
+
+int splatct_fvr_bin(const double* params, int64_t n, int w, int h, int c, int z0, int hx,
+                    int hy, int hz, void* ws, size_t ws_bytes, const int* halt, void* stream) {
+    FvrLayout L = make_layout(n, w, h, c, hx, hy, hz);
+    if (int e = check_args(n, w, h, c, hx, hy, hz, ws_bytes, L)) return e;
+    cudaStream_t s = as_stream(stream);
+    uint32_t* tcount = at<uint32_t>(ws, L.o_tcount);
+    SPLATCT_CK(cudaMemsetAsync(tcount, 0, sizeof(uint32_t) * (L.nt + 1), s));
+    if (n > 0) {
+        k_footprint<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
+            params, n, w, h, c, z0, hx, hy, hz, L.ntx, L.nty, L.S, (uint32_t)L.nt,
+            at<int32_t>(ws, L.o_fp), at<int32_t>(ws, L.o_gcount), at<uint32_t>(ws, L.o_k0),
+            at<uint32_t>(ws, L.o_v0), tcount, halt);
+        SPLATCT_LAUNCH_CK();
+        uint32_t* hist = at<uint32_t>(ws, L.o_hist);
+        for (int p = 0; p < L.passes; ++p) {
+            const size_t ki = p % 2 ? L.o_k1 : L.o_k0, vi = p % 2 ? L.o_v1 : L.o_v0;
+            const size_t ko = p % 2 ? L.o_k0 : L.o_k1, vo = p % 2 ? L.o_v0 : L.o_v1;
+            k_radix_hist<<<(unsigned)L.sort_blocks, SORT_NT, 0, s>>>(
+                at<uint32_t>(ws, ki), L.np, 8 * p, L.sort_blocks, hist, halt);
+            SPLATCT_LAUNCH_CK();
+            if (int e = exclusive_scan_u32(hist, hist, RADIX * L.sort_blocks,
+                                           at<void>(ws, L.o_scan), s))
+                return e;
+            k_radix_scatter<<<(unsigned)L.sort_blocks, SORT_NT, 0, s>>>(
+                at<uint32_t>(ws, ki), at<uint32_t>(ws, vi), at<uint32_t>(ws, ko),
+                at<uint32_t>(ws, vo), L.np, 8 * p, L.sort_blocks, hist, halt);
+            SPLATCT_LAUNCH_CK();
+        }
+    }
+    return exclusive_scan_u32(tcount, at<uint32_t>(ws, L.o_tstart), L.nt + 1,
+                              at<void>(ws, L.o_scan), s);
+}
+
+int splatct_fvr_forward(const double* params, int64_t n, int w, int h, int c, int z0, int hx,
+                        int hy, int hz, const void* ws, size_t ws_bytes, float* vol_yxz,
+                        const int* halt, void* stream) {
+    FvrLayout L = make_layout(n, w, h, c, hx, hy, hz);
+    if (int e = check_args(n, w, h, c, hx, hy, hz, ws_bytes, L)) return e;
+    const size_t vo = L.final_buf ? L.o_v1 : L.o_v0;
+    k_fvr_fwd<<<(unsigned)L.nt, 256, 0, as_stream(stream)>>>(
+        params, n, w, h, c, z0, hx, hy, hz, L.ntx, L.nty, L.S, at<uint32_t>(ws, L.o_tstart),
+        at<uint32_t>(ws, vo), vol_yxz, halt);
+    SPLATCT_LAUNCH_CK();
+    return SPLATCT_OK;
+}
+
+int splatct_fvr_backward(const double* params, int64_t n, int w, int h, int c, int z0, int hx,
+                         int hy, int hz, void* ws, size_t ws_bytes, const float* up_yxz,
+                         double* grads, double* accum, const int* halt, void* stream) {
+    FvrLayout L = make_layout(n, w, h, c, hx, hy, hz);
+    if (int e = check_args(n, w, h, c, hx, hy, hz, ws_bytes, L)) return e;
+    if (n == 0) return SPLATCT_OK;
+    cudaStream_t s = as_stream(stream);
+    const size_t vo = L.final_buf ? L.o_v1 : L.o_v0;
+    float* part = at<float>(ws, L.o_part);
+    k_fvr_bwd<<<(unsigned)L.nt, 256, 0, s>>>(params, n, w, h, c, z0, hx, hy, hz, L.ntx, L.nty, L.S,
+                                             at<uint32_t>(ws, L.o_tstart), at<uint32_t>(ws, vo),
+                                             up_yxz, part, halt);
+    SPLATCT_LAUNCH_CK();
+    k_fvr_combine<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
+        params, n, L.S, at<int32_t>(ws, L.o_gcount), part, grads, accum, halt);
+    SPLATCT_LAUNCH_CK();
+    return SPLATCT_OK;
+}
+
+int splatct_grad_norm_accum(const double* grads, int64_t n, double* accum, const int* halt,
+                            void* stream) {
+    if (n <= 0) return SPLATCT_OK;
+    k_grad_norm_accum<<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(grads, n, accum,
+                                                                                 halt);
+    SPLATCT_LAUNCH_CK();
+    return SPLATCT_OK;
+}
+
+int splatct_fvr_export_bins(const void* ws, size_t ws_bytes, int64_t n, int w, int h, int c,
+                            int hx, int hy, int hz, int32_t* fp, int32_t* tile_start,
+                            int32_t* items, int64_t* npairs, int64_t* n_tiles, void* stream) {
+    FvrLayout L = make_layout(n, w, h, c, hx, hy, hz);
+    if (int e = check_args(n, w, h, c, hx, hy, hz, ws_bytes, L)) return e;
+    cudaStream_t s = as_stream(stream);
+    uint32_t total = 0;
+    SPLATCT_CK(cudaMemcpyAsync(&total, at<uint32_t>(ws, L.o_tstart) + L.nt, sizeof(uint32_t),
+                               cudaMemcpyDeviceToHost, s));
+    SPLATCT_CK(cudaStreamSynchronize(s));
+    *npairs = total;
+    *n_tiles = L.nt;
+    if (fp)
+        SPLATCT_CK(cudaMemcpyAsync(fp, at<int32_t>(ws, L.o_fp), sizeof(int32_t) * 6 * n,
+                                   cudaMemcpyDeviceToDevice, s));
+    if (tile_start)
+        SPLATCT_CK(cudaMemcpyAsync(tile_start, at<uint32_t>(ws, L.o_tstart),
+                                   sizeof(int32_t) * (L.nt + 1), cudaMemcpyDeviceToDevice, s));
+    if (items && total > 0) {
+        const size_t vo = L.final_buf ? L.o_v1 : L.o_v0;
+        k_export_items<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(at<uint32_t>(ws, vo),
+                                                                        total, L.S, items);
+        SPLATCT_LAUNCH_CK();
+    }
+    return SPLATCT_OK;
+}
+
+}  // extern "C"

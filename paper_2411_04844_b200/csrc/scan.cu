@@ -1,0 +1,169 @@
+// scan.cu -- device-wide exclusive scans and fixed-order reductions, plus the
+// C-ABI error plumbing.  Used by the voxelizer's radix sort / tile offsets
+// and by the projector's CSR construction.
+#include <atomic>
+
+#include "common.cuh"
+
+namespace splatct {
+
+static thread_local char g_err[1024] = "";
+static std::atomic<unsigned long long> g_launches{0};
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+void set_error_msg(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+constexpr int SCAN_NT = 256;
+constexpr int SCAN_PER_THREAD = 16;
+constexpr int64_t SCAN_CHUNK = SCAN_NT * SCAN_PER_THREAD;
+
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        T u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += u;
+    }
+    return v;
+}
+
+// Exclusive block scan of one value per thread; returns the exclusive prefix
+// and writes the block total to *total.
+template <typename T, int NT>
+__device__ __forceinline__ T block_excl_scan(T v, T* sh, T* total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    T inc = warp_incl_scan(v);
+    if (lane == 31) sh[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        T s = lane < NT / 32 ? sh[lane] : T(0);
+        s = warp_incl_scan(s);
+        if (lane < NT / 32) sh[lane] = s;
+    }
+    __syncthreads();
+    T wprefix = wid > 0 ? sh[wid - 1] : T(0);
+    *total = sh[NT / 32 - 1];
+    __syncthreads();
+    return wprefix + inc - v;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(SCAN_NT) k_chunk_sums(const T* __restrict__ in, int64_t n,
+                                                        T* __restrict__ sums) {
+    __shared__ T sh[SCAN_NT / 32];
+    const int64_t base = blockIdx.x * SCAN_CHUNK;
+    T acc = 0;
+    for (int i = threadIdx.x; i < SCAN_CHUNK; i += SCAN_NT) {
+        int64_t g = base + i;
+        if (g < n) acc += in[g];
+    }
+    T tot;
+    block_excl_scan<T, SCAN_NT>(acc, sh, &tot);
+    if (threadIdx.x == 0) sums[blockIdx.x] = tot;
+}
+
+// One CTA scans the chunk sums (exclusive) in place.
+template <typename T>
+__global__ void __launch_bounds__(1024) k_scan_single(T* __restrict__ a, int64_t n) {
+    __shared__ T sh[32];
+    const int64_t per = (n + 1023) / 1024;
+    const int64_t beg = threadIdx.x * per;
+    const int64_t end = beg + per < n ? beg + per : n;
+    T acc = 0;
+    for (int64_t i = beg; i < end; ++i) acc += a[i];
+    T tot;
+    T off = block_excl_scan<T, 1024>(acc, sh, &tot);
+    for (int64_t i = beg; i < end; ++i) {
+        T v = a[i];
+        a[i] = off;
+        off += v;
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(SCAN_NT) k_chunk_scan(const T* __restrict__ in, T* __restrict__ out,
+                                                        int64_t n, const T* __restrict__ offs) {
+    __shared__ T sh[SCAN_NT / 32];
+    const int64_t base = blockIdx.x * SCAN_CHUNK + (int64_t)threadIdx.x * SCAN_PER_THREAD;
+    T v[SCAN_PER_THREAD];
+    T acc = 0;
+#pragma unroll
+    for (int k = 0; k < SCAN_PER_THREAD; ++k) {
+        int64_t g = base + k;
+        v[k] = g < n ? in[g] : T(0);
+        acc += v[k];
+    }
+    T tot;
+    T off = block_excl_scan<T, SCAN_NT>(acc, sh, &tot) + offs[blockIdx.x];
+#pragma unroll
+    for (int k = 0; k < SCAN_PER_THREAD; ++k) {
+        int64_t g = base + k;
+        if (g < n) out[g] = off;
+        off += v[k];
+    }
+}
+
+size_t scan_temp_bytes(int64_t n) {
+    int64_t nb = (n + SCAN_CHUNK - 1) / SCAN_CHUNK;
+    return align_up((size_t)(nb > 0 ? nb : 1) * sizeof(int64_t));
+}
+
+template <typename T>
+static int exclusive_scan(const T* in, T* out, int64_t n, void* temp, cudaStream_t s) {
+    if (n <= 0) return SPLATCT_OK;
+    int64_t nb = (n + SCAN_CHUNK - 1) / SCAN_CHUNK;
+    T* sums = reinterpret_cast<T*>(temp);
+    k_chunk_sums<T><<<(unsigned)nb, SCAN_NT, 0, s>>>(in, n, sums);
+    SPLATCT_LAUNCH_CK();
+    k_scan_single<T><<<1, 1024, 0, s>>>(sums, nb);
+    SPLATCT_LAUNCH_CK();
+    k_chunk_scan<T><<<(unsigned)nb, SCAN_NT, 0, s>>>(in, out, n, sums);
+    SPLATCT_LAUNCH_CK();
+    return SPLATCT_OK;
+}
+
+int exclusive_scan_i64(const int64_t* in, int64_t* out, int64_t n, void* temp, cudaStream_t s) {
+    return exclusive_scan<int64_t>(in, out, n, temp, s);
+}
+int exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, void* temp,
+                       cudaStream_t s) {
+    return exclusive_scan<uint32_t>(in, out, n, temp, s);
+}
+
+__global__ void __launch_bounds__(1024) k_reduce_sum(const double* __restrict__ in, int64_t n,
+                                                     double* __restrict__ out) {
+    __shared__ double sh[32];
+    double acc = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += 1024) acc += in[i];
+    double r = block_sum<1024>(acc, sh);
+    if (threadIdx.x == 0) out[0] = r;
+}
+
+int reduce_sum_f64(const double* in, int64_t n, double* out, cudaStream_t s) {
+    k_reduce_sum<<<1, 1024, 0, s>>>(in, n, out);
+    SPLATCT_LAUNCH_CK();
+    return SPLATCT_OK;
+}
+
+}  // namespace splatct
+
+extern "C" {
+
+int splatct_abi_version(void) { return SPLATCT_ABI_VERSION; }
+
+const char* splatct_last_error(void) { return splatct::g_err; }
+
+unsigned long long splatct_launch_count(void) { return splatct::g_launches.load(); }
+
+int splatct_reduce_sum(const double* in, int64_t n, double* out, void* stream) {
+    return splatct::reduce_sum_f64(in, n, out, splatct::as_stream(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,307 @@
+"""Device-resident building blocks over the libsplatct C ABI.
+
+PyTorch is used only for device memory, streams and collectives; all
+arithmetic on the hot path runs in the hand-written sm_100a kernels of
+``csrc/`` (called through ``_lib``).  There is no CPU fallback: every class
+here requires a CUDA device and raises otherwise.
+
+Layouts (include/splatct.h):
+  params / grads / Adam moments  float64 [5, N]  (mu_x, mu_y, mu_z, sigma, I)
+  volume                         float32 [h, w, c]  ("yxz", slice fastest)
+  sinogram                       float32 [m, n, p]  (reference layout)
+"""
+
+from __future__ import annotations
+
+import ctypes
+from collections import OrderedDict
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import call, size_query
+from .core import GaussianCloud, ScanGeometry
+
+VP = ctypes.c_void_p
+
+
+def ptr(t) -> VP:
+    return VP(0 if t is None else t.data_ptr())
+
+
+def stream_handle(stream=None) -> VP:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return VP(s.cuda_stream)
+
+
+def require_cuda(device=None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError(
+            "splatct B200 path needs a CUDA device; there is no CPU fallback "
+            "(the CPU restatement in oracle/ is test infrastructure only)")
+    _lib.load()
+    dev = torch.device(device if device is not None else "cuda")
+    if dev.type != "cuda":
+        raise RuntimeError(f"splatct kernels run on CUDA devices only, got {dev}")
+    return dev
+
+
+# ---------------------------------------------------------------------------
+# conversions at the API edge
+# ---------------------------------------------------------------------------
+
+def cloud_to_params(cloud: GaussianCloud, device) -> torch.Tensor:
+    p = np.empty((5, cloud.n), np.float64)
+    p[0:3] = cloud.mu.T
+    p[3] = cloud.sigma
+    p[4] = cloud.intensity
+    return torch.from_numpy(p).to(device)
+
+
+def params_to_cloud(params: torch.Tensor) -> GaussianCloud:
+    p = params.detach().cpu().numpy()
+    return GaussianCloud(np.ascontiguousarray(p[0:3].T), p[3].copy(), p[4].copy())
+
+
+def zyx_to_yxz(arr, device) -> torch.Tensor:
+    """(c, h, w) host array -> (h, w, c) device tensor."""
+    t = torch.as_tensor(np.ascontiguousarray(arr, dtype=np.float32))
+    return t.to(device).permute(1, 2, 0).contiguous()
+
+
+def yxz_to_zyx(t: torch.Tensor) -> np.ndarray:
+    return t.permute(2, 0, 1).contiguous().cpu().numpy()
+
+
+def sino_to_device(views, device) -> torch.Tensor:
+    return torch.as_tensor(np.ascontiguousarray(views, dtype=np.float32)).to(device)
+
+
+# ---------------------------------------------------------------------------
+# voxelizer
+# ---------------------------------------------------------------------------
+
+class FvrPlan:
+    """Workspace + launches for the tiled voxelizer on a (w, h, c) slab at z0.
+
+    fvr.reconstruct / fvr.backward (fvr.py:148-273) on device.
+    """
+
+    def __init__(self, n: int, dims, half, z0: int = 0, device=None):
+        self.device = require_cuda(device)
+        self.n = int(n)
+        self.w, self.h, self.c = (int(v) for v in dims)
+        self.hx, self.hy, self.hz = (int(v) for v in half)
+        self.z0 = int(z0)
+        self.ws_bytes = size_query("splatct_fvr_workspace_bytes", self.n, self.w, self.h, self.c,
+                                   self.hx, self.hy, self.hz)
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
+
+    def _geo(self):
+        return (self.n, self.w, self.h, self.c, self.z0, self.hx, self.hy, self.hz)
+
+    def bin(self, params: torch.Tensor, halt=None) -> None:
+        call("splatct_fvr_bin", ptr(params), *self._geo(), ptr(self.ws), self.ws_bytes,
+             ptr(halt), stream_handle())
+
+    def forward(self, params: torch.Tensor, out: torch.Tensor, halt=None) -> torch.Tensor:
+        call("splatct_fvr_forward", ptr(params), *self._geo(), ptr(self.ws), self.ws_bytes,
+             ptr(out), ptr(halt), stream_handle())
+        return out
+
+    def backward(self, params, upstream, grads, accum=None, halt=None) -> torch.Tensor:
+        call("splatct_fvr_backward", ptr(params), *self._geo(), ptr(self.ws), self.ws_bytes,
+             ptr(upstream), ptr(grads), ptr(accum), ptr(halt), stream_handle())
+        return grads
+
+    def new_volume(self) -> torch.Tensor:
+        return torch.empty((self.h, self.w, self.c), dtype=torch.float32, device=self.device)
+
+    def export_bins(self):
+        """(fp int32 [n,6], tile_start int32 [T+1], items int32 [P]) on the host."""
+        fp = torch.empty((max(self.n, 1), 6), dtype=torch.int32, device=self.device)
+        np_ = ctypes.c_int64(0)
+        nt = ctypes.c_int64(0)
+        call("splatct_fvr_export_bins", ptr(self.ws), self.ws_bytes, self.n, self.w, self.h,
+             self.c, self.hx, self.hy, self.hz, VP(0), VP(0), VP(0), ctypes.byref(np_),
+             ctypes.byref(nt), stream_handle())
+        ts = torch.empty(nt.value + 1, dtype=torch.int32, device=self.device)
+        items = torch.empty(max(np_.value, 1), dtype=torch.int32, device=self.device)
+        call("splatct_fvr_export_bins", ptr(self.ws), self.ws_bytes, self.n, self.w, self.h,
+             self.c, self.hx, self.hy, self.hz, ptr(fp), ptr(ts), ptr(items), ctypes.byref(np_),
+             ctypes.byref(nt), stream_handle())
+        torch.cuda.current_stream().synchronize()
+        return (fp[: self.n].cpu().numpy(), ts.cpu().numpy(),
+                items[: np_.value].cpu().numpy())
+
+
+# ---------------------------------------------------------------------------
+# projector operator
+# ---------------------------------------------------------------------------
+
+class ProjectorOperator:
+    """Exact per-slice projector A and adjoint A^T for one geometry.
+
+    Built once by marching every ray in f64 (the reference's
+    _ray_geometry/_clip_ray sample enumeration, _kernels.py:208-303) and
+    merging sample weights per (ray, pixel); reused every iteration.
+    """
+
+    def __init__(self, geom: ScanGeometry, w: int, h: int, step: float = 0.5, device=None):
+        self.device = require_cuda(device)
+        geom.check_volume((w, h, 1))
+        self.geom = geom
+        self.w, self.h = int(w), int(h)
+        self.m, self.n_det = int(geom.n_views), int(geom.n_detectors)
+        self.step = float(step)
+        self.is_fan = geom.variant == "fan"
+        self.rs = float(geom.source_to_origin) if self.is_fan else 0.0
+        self.rd = float(geom.origin_to_detector) if self.is_fan else 0.0
+        self.spacing = float(geom.detector_spacing)
+        ang = np.asarray(geom.view_angles, np.float64)
+        self.cos_t = torch.from_numpy(np.cos(ang)).to(self.device)
+        self.sin_t = torch.from_numpy(np.sin(ang)).to(self.device)
+        rays = self.m * self.n_det
+        self.n_rays = rays
+        g = self._gargs()
+        sb = size_query("splatct_proj_scratch_bytes", self.m, self.n_det, self.w, self.h, 0)
+        scratch = torch.empty(sb, dtype=torch.uint8, device=self.device)
+        self.a_ptr = torch.empty(rays + 1, dtype=torch.int64, device=self.device)
+        nnz = ctypes.c_int64(0)
+        call("splatct_proj_count", *g, ptr(self.a_ptr), ptr(scratch), sb, ctypes.byref(nnz),
+             stream_handle())
+        self.nnz = int(nnz.value)
+        sb = size_query("splatct_proj_scratch_bytes", self.m, self.n_det, self.w, self.h,
+                        self.nnz)
+        scratch = torch.empty(sb, dtype=torch.uint8, device=self.device)
+        k = max(self.nnz, 1)
+        self.a_col = torch.empty(k, dtype=torch.int32, device=self.device)
+        self.a_val = torch.empty(k, dtype=torch.float32, device=self.device)
+        self.at_ptr = torch.empty(self.w * self.h + 1, dtype=torch.int64, device=self.device)
+        self.at_ray = torch.empty(k, dtype=torch.int32, device=self.device)
+        self.at_val = torch.empty(k, dtype=torch.float32, device=self.device)
+        call("splatct_proj_fill", *g, ptr(self.a_ptr), ptr(self.a_col), ptr(self.a_val),
+             ptr(self.at_ptr), ptr(self.at_ray), ptr(self.at_val), ptr(scratch), sb,
+             stream_handle())
+        del scratch
+
+    def _gargs(self):
+        return (ptr(self.cos_t), ptr(self.sin_t), self.m, self.n_det, self.spacing, self.step,
+                int(self.is_fan), self.rs, self.rd, self.w, self.h)
+
+    @property
+    def matrix_bytes(self) -> int:
+        return 16 * self.nnz + 8 * (self.n_rays + self.w * self.h + 2)
+
+    def forward(self, vol: torch.Tensor, out: torch.Tensor | None = None, halt=None):
+        """vol (h, w, c) -> sinogram (m, n, c)."""
+        c = int(vol.shape[2])
+        if out is None:
+            out = torch.empty((self.m, self.n_det, c), dtype=torch.float32, device=vol.device)
+        call("splatct_proj_forward", ptr(self.a_ptr), ptr(self.a_col), ptr(self.a_val),
+             self.n_rays, ptr(vol), ptr(out), c, ptr(halt), stream_handle())
+        return out
+
+    def adjoint(self, gsino: torch.Tensor, out: torch.Tensor | None = None, vol=None,
+                halo_lo=None, halo_hi=None, lambda_tv: float = 0.0, tv_count: float = 1.0,
+                tv_partial=None, halt=None):
+        """sinogram (m, n, c) -> volume (h, w, c) [+ lambda_tv * TV subgradient of vol]."""
+        c = int(gsino.shape[2])
+        if out is None:
+            out = torch.empty((self.h, self.w, c), dtype=torch.float32, device=gsino.device)
+        call("splatct_proj_adjoint", ptr(self.at_ptr), ptr(self.at_ray), ptr(self.at_val),
+             self.w, self.h, c, ptr(gsino), ptr(vol), ptr(halo_lo), ptr(halo_hi),
+             float(lambda_tv), float(tv_count), ptr(out), ptr(tv_partial), ptr(halt),
+             stream_handle())
+        return out
+
+    def march_forward(self, vol: torch.Tensor) -> torch.Tensor:
+        """Matrix-free ray-marching forward projection (cross-check path)."""
+        c = int(vol.shape[2])
+        out = torch.empty((self.m, self.n_det, c), dtype=torch.float32, device=vol.device)
+        call("splatct_proj_march_forward", *self._gargs()[:9], self.w, self.h, c, ptr(vol),
+             ptr(out), stream_handle())
+        return out
+
+
+_PROJ_CACHE: "OrderedDict[tuple, ProjectorOperator]" = OrderedDict()
+
+
+def projector_for(geom: ScanGeometry, w: int, h: int, step: float = 0.5,
+                  device=None) -> ProjectorOperator:
+    dev = require_cuda(device)
+    key = (geom.key(), int(w), int(h), float(step), str(dev))
+    op = _PROJ_CACHE.get(key)
+    if op is None:
+        op = ProjectorOperator(geom, w, h, step, dev)
+        _PROJ_CACHE[key] = op
+        while len(_PROJ_CACHE) > 4:
+            _PROJ_CACHE.popitem(last=False)
+    else:
+        _PROJ_CACHE.move_to_end(key)
+    return op
+
+
+def tv_operator(w: int, h: int, device=None) -> ProjectorOperator:
+    """An operator with an empty A^T: its adjoint is the TV term alone."""
+    dev = require_cuda(device)
+    op = ProjectorOperator.__new__(ProjectorOperator)
+    op.device = dev
+    op.w, op.h = int(w), int(h)
+    op.at_ptr = torch.zeros(op.w * op.h + 1, dtype=torch.int64, device=dev)
+    op.at_ray = torch.zeros(1, dtype=torch.int32, device=dev)
+    op.at_val = torch.zeros(1, dtype=torch.float32, device=dev)
+    return op
+
+
+# ---------------------------------------------------------------------------
+# loss
+# ---------------------------------------------------------------------------
+
+class LossPlan:
+    """Workspace for the fused L1 + SSIM loss on an (m, n, p) sinogram slab."""
+
+    def __init__(self, m: int, n: int, p: int, device=None):
+        self.device = require_cuda(device)
+        self.m, self.n, self.p = int(m), int(n), int(p)
+        self.ws_bytes = size_query("splatct_loss_workspace_bytes", self.m, self.n, self.p)
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
+        kr, kc = min(11, self.m), min(11, self.n)
+        kr -= 1 - kr % 2
+        kc -= 1 - kc % 2
+        self.valid = (self.m - kr + 1) * (self.n - kc + 1)
+
+    def fused(self, pred, ref, lmax: float, lambda1: float, lambda2: float, l1_count: float,
+              ssim_slices: float, grad_out, sums, halt=None):
+        call("splatct_loss_fused", ptr(pred), ptr(ref), self.m, self.n, self.p, float(lmax),
+             float(lambda1), float(lambda2), float(l1_count), float(ssim_slices), ptr(grad_out),
+             ptr(self.ws), self.ws_bytes, ptr(sums), ptr(halt), stream_handle())
+
+
+def sino_max(x: torch.Tensor) -> float:
+    out = torch.empty(1, dtype=torch.float64, device=x.device)
+    call("splatct_sino_max", ptr(x), int(x.numel()), ptr(out), stream_handle())
+    return float(out.item())
+
+
+def reduce_sum(x: torch.Tensor, out: torch.Tensor) -> None:
+    call("splatct_reduce_sum", ptr(x), int(x.numel()), ptr(out), stream_handle())
+
+
+def sum_sq_diff(x: torch.Tensor, y: torch.Tensor) -> float:
+    ws = torch.empty(_lib.SQDIFF_BLOCKS, dtype=torch.float64, device=x.device)
+    out = torch.empty(1, dtype=torch.float64, device=x.device)
+    call("splatct_sum_sq_diff", ptr(x), ptr(y), int(x.numel()), ptr(ws), ptr(out),
+         stream_handle())
+    return float(out.item())
+
+
+def adam(params, grads, m1, m2, scalars, sigma_floor, sigma_ceiling, halt=None):
+    call("splatct_adam", ptr(params), ptr(grads), ptr(m1), ptr(m2), int(params.shape[1]),
+         ptr(scalars), float(sigma_floor), float(sigma_ceiling), ptr(halt), stream_handle())
+
+
+def grad_norm_accum(grads, accum, halt=None):
+    call("splatct_grad_norm_accum", ptr(grads), int(grads.shape[1]), ptr(accum), ptr(halt),
+         stream_handle())

@@ -1,0 +1,142 @@
+"""z-slab domain decomposition across the GPUs of one node.
+
+For the per-slice parallel/fan geometries, sinogram slice z depends only on
+volume slice z (_kernels.py:273-278), so each rank owns a contiguous z-slab
+of the volume AND the same slices of the sinogram; projector, adjoint, L1
+and SSIM are slab-local.  Exchanges per iteration:
+
+  * all-reduce(sum) of the 3 loss sums (L1, SSIM, TV) -- bookkeeping only;
+  * one xy-plane TV halo with each z-neighbour (the TV subgradient couples
+    adjacent slices, loss.py:195-206);
+  * all-reduce(sum) of the float64 [5, N] partial gradient block (a Gaussian
+    whose box straddles a slab boundary gets contributions from two ranks).
+
+Adam then runs identically on every rank (replicated cloud).  The
+communicator is written against torch.distributed and works for NCCL on
+device tensors and for gloo on CPU tensors (tests/test_distributed.py).
+"""
+
+from __future__ import annotations
+
+import os
+
+import torch
+import torch.distributed as dist
+
+from .trainer import Slab
+
+
+def slab_bounds(c: int, world: int, rank: int) -> Slab:
+    """Contiguous, balanced split of c slices over world ranks."""
+    base, rem = divmod(int(c), int(world))
+    z0 = rank * base + min(rank, rem)
+    cl = base + (1 if rank < rem else 0)
+    return Slab(z0, cl, int(c))
+
+
+class SlabComm:
+    """Collectives of the z-slab decomposition over a torch.distributed group."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self._lo = None
+        self._hi = None
+
+    def allreduce_sum_(self, t: torch.Tensor) -> torch.Tensor:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+        return t
+
+    def allreduce_max_(self, t: torch.Tensor) -> torch.Tensor:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        return t
+
+    def halo(self, vol: torch.Tensor):
+        """Exchange boundary z-planes of a (h, w, c_local) slab.
+
+        Returns (lo, hi): plane z0-1 from rank-1 and plane z0+c_local from
+        rank+1, each a contiguous (h*w,) tensor, or None at the volume edges.
+        """
+        h, w, _ = vol.shape
+        if self._lo is None or self._lo.numel() != h * w or self._lo.device != vol.device:
+            self._lo = torch.empty(h * w, dtype=vol.dtype, device=vol.device)
+            self._hi = torch.empty(h * w, dtype=vol.dtype, device=vol.device)
+            self._send_lo = torch.empty_like(self._lo)
+            self._send_hi = torch.empty_like(self._lo)
+        self._send_lo.copy_(vol[:, :, 0].reshape(-1))
+        self._send_hi.copy_(vol[:, :, -1].reshape(-1))
+        ops = []
+        r, n = self.rank, self.world
+        if r > 0:
+            ops.append(dist.P2POp(dist.isend, self._send_lo, r - 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, self._lo, r - 1, self.group))
+        if r + 1 < n:
+            ops.append(dist.P2POp(dist.isend, self._send_hi, r + 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, self._hi, r + 1, self.group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        return (self._lo if r > 0 else None), (self._hi if r + 1 < n else None)
+
+
+def init_from_env(backend: str = "nccl"):
+    """Initialise torch.distributed from torchrun's env (127.0.0.1 rendezvous)."""
+    if dist.is_available() and not dist.is_initialized() and int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        local = int(os.environ.get("LOCAL_RANK", "0"))
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            dist.init_process_group(backend, device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_rank(), dist.get_world_size()
+    return 0, 1
+
+
+def run_reconstruction_sharded(measured, geom, settings, init_cloud, comm=None,
+                               use_graph: bool = False):
+    """run_reconstruction (optim.py:286-427) over a z-slab-sharded volume.
+
+    Every rank calls this with the same host inputs; rank r keeps slices
+    slab_bounds(c, world, r) of the measured sinogram and the volume.  Densify
+    and the per-iteration truth/val hooks of the single-device API are not
+    supported here.  Returns (VolumeGrid on rank 0 else None, GaussianCloud,
+    trace array [iters, 4] = loss, l1, ssim, tv).
+    """
+    import numpy as np
+
+    from . import device as D
+    from .core import VolumeGrid
+    from .trainer import Trainer
+
+    comm = comm or SlabComm()
+    dims = tuple(int(v) for v in settings.dims)
+    s = slab_bounds(dims[2], comm.world, comm.rank)
+    dev = D.require_cuda()
+    local = np.ascontiguousarray(measured.views[:, :, s.z0:s.z0 + s.c_local])
+    tr = Trainer(D.sino_to_device(local, dev), geom, dims, settings.box, settings.weights,
+                 D.cloud_to_params(init_cloud, dev), lr0=settings.lr_initial,
+                 lrf=settings.lr_final, max_iters=settings.max_iters, slab=s, comm=comm)
+    tr.initial_volume()
+    done = 0
+    if use_graph and settings.max_iters > 0 and comm.world == 1:
+        done = tr.capture()
+    for _ in range(done, settings.max_iters):
+        tr.step()
+    torch.cuda.synchronize()
+    if tr.halted():
+        raise RuntimeError(f"non-finite loss at iteration {tr.iterations_done()}")
+    cmax = -(-dims[2] // comm.world)
+    pad = torch.zeros((tr.h, tr.w, cmax), dtype=torch.float32, device=dev)
+    pad[:, :, : s.c_local] = tr.vol
+    parts = [torch.empty_like(pad) for _ in range(comm.world)] if comm.world > 1 else [pad]
+    if comm.world > 1:
+        dist.all_gather(parts, pad, group=comm.group)
+    vol = None
+    if comm.rank == 0:
+        cols = [parts[r][:, :, : slab_bounds(dims[2], comm.world, r).c_local]
+                for r in range(comm.world)]
+        vol = VolumeGrid.from_zyx(D.yxz_to_zyx(torch.cat(cols, dim=2)))
+    return vol, D.params_to_cloud(tr.params), tr.trace_rows()

@@ -1,0 +1,198 @@
+"""Device-resident training iteration (the body of optim.run_reconstruction).
+
+One iteration in the reference order (optim.py:350-403):
+
+  1. pred  = A vol                         projector.forward_project   (proj.cu)
+  2. L1 + SSIM value and dL/dpred (f32)    loss.l1_loss/ssim_loss     (loss.cu)
+  3. dl_dvol = f32(A^T dL/dpred + l3 dTV)  projector.back_project + loss.tv_loss (proj.cu)
+  4. loss bookkeeping, non-finite guard, Adam scalars (optim.py:356-366, 88-90)
+  5. grads = splat adjoint(dl_dvol)        fvr.backward               (fvr.cu)
+  6. Adam step + clamps                    optim.adam_step            (loss.cu)
+  7. bins + vol = splat(params)            fvr.reconstruct            (fvr.cu)
+
+Everything stays in HBM; no host synchronisation inside an iteration, so a
+single-GPU iteration is captured once as a CUDA graph and replayed.  Under
+z-slab sharding (distributed.py) each rank owns slices [z0, z0+c_local) of
+the volume and the sinogram; the only exchanges are the loss sums and the
+gradient all-reduce plus a one-plane TV halo.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import torch
+
+from . import device as D
+from .core import BoxConfig, ScanGeometry
+
+SIGMA_FLOOR = 0.3
+
+
+@dataclass
+class Slab:
+    """The z-range [z0, z0 + c_local) of a c_global-slice volume owned by a rank."""
+
+    z0: int
+    c_local: int
+    c_global: int
+
+
+class NullComm:
+    """Single-device communicator (no-ops)."""
+
+    rank = 0
+    world = 1
+
+    def allreduce_sum_(self, t):
+        return t
+
+    def allreduce_max_(self, t):
+        return t
+
+    def halo(self, vol):
+        return None, None
+
+
+class Trainer:
+    """The training loop state on one device (one z-slab when sharded)."""
+
+    def __init__(self, measured: torch.Tensor, geom: ScanGeometry, dims, box: BoxConfig,
+                 weights, params: torch.Tensor, *, m1=None, m2=None, step: int = 0,
+                 accum=None, lr0: float = 3e-4, lrf: float = 3e-5, max_iters: int = 1000,
+                 slab: Slab | None = None, comm=None, trace_cap: int | None = None,
+                 step_length: float = 0.5):
+        self.device = D.require_cuda(measured.device)
+        self.geom = geom
+        self.w, self.h, self.c = (int(v) for v in dims)
+        self.box = box
+        self.weights = weights
+        self.slab = slab or Slab(0, self.c, self.c)
+        self.comm = comm or NullComm()
+        self.lr0, self.lrf, self.max_iters = float(lr0), float(lrf), int(max_iters)
+        self.sigma_ceiling = 3.0 * box.extent
+        m, n, cl = (int(v) for v in measured.shape)
+        if cl != self.slab.c_local:
+            raise ValueError(f"measured slab has {cl} slices, slab owns {self.slab.c_local}")
+        self.m, self.n = m, n
+        self.meas = measured
+        dev = self.device
+        self.op = D.projector_for(geom, self.w, self.h, step_length, dev)
+        self.loss = D.LossPlan(m, n, cl, dev)
+        self.pred = torch.empty((m, n, cl), dtype=torch.float32, device=dev)
+        self.gpred = torch.empty_like(self.pred)
+        self.vol = torch.empty((self.h, self.w, cl), dtype=torch.float32, device=dev)
+        self.dl = torch.empty_like(self.vol)
+        self.tv_part = torch.zeros(self.w * self.h, dtype=torch.float64, device=dev)
+        self.sums = torch.zeros(3, dtype=torch.float64, device=dev)
+        self.adam_s = torch.zeros(3, dtype=torch.float64, device=dev)
+        self.step_t = torch.tensor([int(step)], dtype=torch.int64, device=dev)
+        self.iter_t = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.halt = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.trace_cap = int(trace_cap if trace_cap is not None else max_iters)
+        self.trace = torch.full((max(self.trace_cap, 1), 4), math.nan, dtype=torch.float64,
+                                device=dev)
+        lm = torch.tensor([D.sino_max(measured)], dtype=torch.float64, device=dev)
+        self.comm.allreduce_max_(lm)
+        self.lmax = float(lm.item())
+        cg = self.slab.c_global
+        self.l1_count = float(m * n * cg)
+        self.ssim_count = float(self.loss.valid * cg)
+        self.tv_count = float(self.w * self.h * cg)
+        self.graph = None
+        self._set_params(params, m1, m2, accum)
+
+    # -- state ------------------------------------------------------------
+    def _set_params(self, params, m1=None, m2=None, accum=None):
+        dev = self.device
+        self.params = params.to(dev, torch.float64).contiguous()
+        nG = int(self.params.shape[1])
+        self.N = nG
+        self.m1 = (m1.to(dev, torch.float64).contiguous() if m1 is not None
+                   else torch.zeros_like(self.params))
+        self.m2 = (m2.to(dev, torch.float64).contiguous() if m2 is not None
+                   else torch.zeros_like(self.params))
+        self.grads = torch.zeros_like(self.params)
+        self.accum = (accum.to(dev, torch.float64).contiguous() if accum is not None
+                      else torch.zeros(nG, dtype=torch.float64, device=dev))
+        s = self.slab
+        self.fvr = D.FvrPlan(nG, (self.w, self.h, s.c_local), self.box.half, s.z0, dev)
+        self.graph = None
+
+    def resize(self, params, m1, m2, accum=None):
+        """Replace the cloud (densification changes N); drops the captured graph."""
+        self._set_params(params, m1, m2, accum)
+        self.initial_volume()
+
+    # -- iteration ----------------------------------------------------------
+    def initial_volume(self):
+        self.fvr.bin(self.params, self.halt)
+        self.fvr.forward(self.params, self.vol, self.halt)
+
+    def iteration(self):
+        lw = self.weights
+        halt = self.halt
+        self.op.forward(self.vol, self.pred, halt)
+        if lw.lambda1 > 0 or lw.lambda2 > 0:
+            self.loss.fused(self.pred, self.meas, self.lmax, lw.lambda1, lw.lambda2,
+                            self.l1_count, float(self.slab.c_global), self.gpred, self.sums,
+                            halt)
+        else:
+            self.gpred.zero_()
+        if lw.lambda3 > 0:
+            lo, hi = self.comm.halo(self.vol)
+            self.op.adjoint(self.gpred, self.dl, vol=self.vol, halo_lo=lo, halo_hi=hi,
+                            lambda_tv=lw.lambda3, tv_count=self.tv_count,
+                            tv_partial=self.tv_part, halt=halt)
+            D.reduce_sum(self.tv_part, self.sums[2:3])
+        else:
+            self.op.adjoint(self.gpred, self.dl, halt=halt)
+        self.comm.allreduce_sum_(self.sums)
+        D.call("splatct_iter_finalize", D.ptr(self.sums), float(lw.lambda1), float(lw.lambda2),
+               float(lw.lambda3), self.l1_count, self.ssim_count, self.tv_count, self.lr0,
+               self.lrf, self.max_iters, D.ptr(self.step_t), D.ptr(self.iter_t),
+               D.ptr(self.trace), self.trace_cap, D.ptr(self.adam_s), D.ptr(halt),
+               D.stream_handle())
+        sharded = self.comm.world > 1
+        self.fvr.backward(self.params, self.dl, self.grads, None if sharded else self.accum,
+                          halt)
+        if sharded:
+            self.comm.allreduce_sum_(self.grads)
+            D.grad_norm_accum(self.grads, self.accum, halt)
+        D.adam(self.params, self.grads, self.m1, self.m2, self.adam_s, SIGMA_FLOOR,
+               self.sigma_ceiling, halt)
+        self.fvr.bin(self.params, halt)
+        self.fvr.forward(self.params, self.vol, halt)
+
+    def capture(self):
+        """Capture one iteration as a CUDA graph (runs one real iteration first)."""
+        side = torch.cuda.Stream(device=self.device)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            self.iteration()
+        torch.cuda.current_stream().wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.iteration()
+        self.graph = g
+        return 1   # iterations executed
+
+    def step(self):
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self.iteration()
+
+    # -- readback -----------------------------------------------------------
+    def halted(self) -> bool:
+        return bool(self.halt.item())
+
+    def iterations_done(self) -> int:
+        return int(self.iter_t.item())
+
+    def trace_rows(self, upto: int | None = None):
+        k = self.iterations_done() if upto is None else upto
+        if self.halted():
+            k = min(k + 1, self.trace_cap)
+        return self.trace[:k].cpu().numpy()
