@@ -152,6 +152,37 @@ int splatct_proj_adjoint(const int64_t* at_ptr, const int32_t* at_ray, const flo
                          double tv_count, float* out_yxz, double* tv_partial, const int* halt,
                          void* stream);
 
+/* 4-row blocked form of a CSR operator (proj_blocked.cu).  kind 0 groups
+ * rows 4g..4g+3 (consecutive rays of A); kind 1 groups the 2x2 pixel quad
+ * (2qx+dx, 2qy+dy), k = 2*dy + dx, of A^T on a w x h slice.  A group entry
+ * is (column, w[4]) with the member rows' weights (0 where absent), columns
+ * ascending.  count (synchronous) -> gptr[ngroups+1] and *nb; fill -> gidx,
+ * gval (float[nb][4], 16-byte aligned). */
+int splatct_proj_block_scratch_bytes(int nrows, int kind, int w, int h, size_t* bytes);
+int splatct_proj_block_count(const int64_t* ptr, const int32_t* idx, int nrows, int kind, int w,
+                             int h, int64_t* gptr, void* scratch, size_t scratch_bytes,
+                             int64_t* nb, void* stream);
+int splatct_proj_block_fill(const int64_t* ptr, const int32_t* idx, const float* val, int nrows,
+                            int kind, int w, int h, const int64_t* gptr, int32_t* gidx,
+                            float* gval, void* scratch, size_t scratch_bytes, void* stream);
+
+/* Length (doubles) of the tv_partial buffer splatct_proj_adjoint_blocked
+ * writes for a w x h x c slab: one slot per (pixel column, 32*V-slice chunk),
+ * each written exactly once (reduce the whole buffer in a fixed order). */
+int splatct_proj_tv_partial_len(int w, int h, int c, int64_t* len);
+
+/* Blocked applications: same results as splatct_proj_forward /
+ * splatct_proj_adjoint (up to f32 summation order), one z-column load per
+ * group entry feeding four rows. */
+int splatct_proj_forward_blocked(const int64_t* gptr, const int32_t* gidx, const float* gval,
+                                 int n_rays, const float* vol_yxz, float* sino, int c,
+                                 const int* halt, void* stream);
+int splatct_proj_adjoint_blocked(const int64_t* gptr, const int32_t* gidx, const float* gval,
+                                 int w, int h, int c, const float* gsino, const float* vol_yxz,
+                                 const float* halo_lo, const float* halo_hi, double lambda_tv,
+                                 double tv_count, float* out_yxz, double* tv_partial,
+                                 const int* halt, void* stream);
+
 /* Direct ray-marching forward projection (no matrix), same f64 ray setup and
  * sample enumeration as _kernels.py:262-303; used as a cross-check and for
  * one-off projections. */

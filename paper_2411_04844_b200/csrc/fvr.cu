@@ -33,6 +33,15 @@ constexpr int SORT_IPT = 8;
 constexpr int SORT_CHUNK = SORT_NT * SORT_IPT;
 constexpr int RADIX = 256;
 
+// Per-Gaussian record written by the footprint pass: integer floor (global
+// voxel coordinates), fractional offsets, 0.5/sigma^2 and intensity in f32,
+// so the tile kernels never touch f64.
+struct __align__(16) GRec {
+    int fx, fy, fz;
+    float inv2;
+    float dx, dy, dz, I;
+};
+
 struct FvrLayout {
     int64_t n;
     int w, h, c, hx, hy, hz;
@@ -43,7 +52,8 @@ struct FvrLayout {
     int passes;
     int64_t sort_blocks;
     size_t o_fp, o_gcount, o_k0, o_v0, o_k1, o_v1, o_tcount, o_tstart, o_hist, o_scan, o_part,
-        total;
+        o_rec, o_cc, o_cstart, total;
+    int64_t bwd_grid;   // upper bound on backward (tile, chunk) work items
     int final_buf;    // which (k,v) buffer holds the sorted result
 };
 
@@ -83,6 +93,10 @@ static FvrLayout make_layout(int64_t n, int w, int h, int c, int hx, int hy, int
     size_t sc2 = scan_temp_bytes(L.nt + 1);
     L.o_scan = take(sc1 > sc2 ? sc1 : sc2);
     L.o_part = take(sizeof(float) * 5 * (size_t)L.np);
+    L.o_rec = take(sizeof(GRec) * (size_t)n);
+    L.o_cc = take(sizeof(uint32_t) * (size_t)(L.nt + 1));
+    L.o_cstart = take(sizeof(uint32_t) * (size_t)(L.nt + 1));
+    L.bwd_grid = L.nt + L.np / 64 + 1;
     L.total = off;
     L.final_buf = L.passes % 2;   // pass p reads buf p%2, writes (p+1)%2
     return L;
@@ -104,7 +118,8 @@ __global__ void k_footprint(const double* __restrict__ P, int64_t n, int w, int 
                             int hx, int hy, int hz, int ntx, int nty, int S, uint32_t sentinel,
                             int32_t* __restrict__ fp, int32_t* __restrict__ gcount,
                             uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
-                            uint32_t* __restrict__ tcount, const int* halt) {
+                            uint32_t* __restrict__ tcount, GRec* __restrict__ rec,
+                            const int* halt) {
     if (halted(halt)) return;
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -131,7 +146,15 @@ __global__ void k_footprint(const double* __restrict__ P, int64_t n, int w, int 
     }
     int cnt = 0;
     const uint32_t base = (uint32_t)(i * S);
-    if (!empty) {
+    if (!empty) {   // binned Gaussians have |floor(mu)| <= dim + half: int32 is exact
+        GRec r;
+        const double mx = P[i], my = P[n + i], mz = P[2 * n + i], sg = P[3 * n + i];
+        const double fx = floor(mx), fy = floor(my), fz = floor(mz);
+        r.fx = (int)fx; r.fy = (int)fy; r.fz = (int)fz;
+        r.dx = (float)(mx - fx); r.dy = (float)(my - fy); r.dz = (float)(mz - fz);
+        r.inv2 = (float)(0.5 / (sg * sg));
+        r.I = (float)P[4 * n + i];
+        rec[i] = r;
         for (int tz = lo[2] / TT; tz <= hi[2] / TT; ++tz)
             for (int ty = lo[1] / TT; ty <= hi[1] / TT; ++ty)
                 for (int tx = lo[0] / TT; tx <= hi[0] / TT; ++tx) {
@@ -223,22 +246,20 @@ __global__ void __launch_bounds__(SORT_NT) k_radix_scatter(
 // --------------------------------------------------------------------------
 // forward: one CTA per tile, thread = (y, x) column of 16 voxels
 // --------------------------------------------------------------------------
-constexpr int FWD_BATCH = 32;
+constexpr int FWD_BATCH = 32;   // Gaussians staged per round (8 threads each)
 
-__device__ __forceinline__ float axis_weight(double mu_a, float inv2, int coord, int dim, int half,
-                                             int origin) {
-    // b = coord - floor(mu); r = b - (mu - floor(mu)) evaluated in f64 then
-    // rounded; zero outside the box or the (local) volume.
-    double f = floor(mu_a);
-    double b = (double)(coord + origin) - f;
-    if (coord >= dim || fabs(b) > (double)half) return 0.f;
-    float r = (float)(b - (mu_a - f));
+// Separable weight of tile-local coordinate l on one axis (zero outside the
+// box or the local volume): exp(-(b - d)^2 inv2), b = coord - floor(mu).
+__device__ __forceinline__ float tab_weight(int coord_local, int origin, int dim, int f, int half,
+                                            float d, float inv2) {
+    const int b = coord_local + origin - f;
+    if (coord_local >= dim || b > half || b < -half) return 0.f;
+    const float r = (float)b - d;
     return expf(-inv2 * r * r);
 }
 
-__global__ void __launch_bounds__(256) k_fvr_fwd(const double* __restrict__ P, int64_t n, int w,
-                                                 int h, int c, int zoff, int hx, int hy, int hz,
-                                                 int ntx,
+__global__ void __launch_bounds__(256) k_fvr_fwd(const GRec* __restrict__ rec, int w, int h, int c,
+                                                 int zoff, int hx, int hy, int hz, int ntx,
                                                  int nty, int S,
                                                  const uint32_t* __restrict__ tstart,
                                                  const uint32_t* __restrict__ svals,
@@ -253,20 +274,22 @@ __global__ void __launch_bounds__(256) k_fvr_fwd(const double* __restrict__ P, i
     float acc[TT];
 #pragma unroll
     for (int k = 0; k < TT; ++k) acc[k] = 0.f;
+    const int tg = threadIdx.x >> 3, tj = threadIdx.x & 7;   // table builder: Gaussian, part
 
     for (uint32_t b0 = beg; b0 < end; b0 += FWD_BATCH) {
         const int nb = (int)min((uint32_t)FWD_BATCH, end - b0);
         __syncthreads();
-        for (int e = threadIdx.x; e < nb * 3 * TT; e += blockDim.x) {
-            const int g = e / (3 * TT), q = e % (3 * TT), a = q / TT, l = q % TT;
-            const int64_t gid = svals[b0 + g] / (uint32_t)S;
-            const double s = P[3 * n + gid];
-            const float inv2 = (float)(0.5 / (s * s));
-            float v;
-            if (a == 0) v = axis_weight(P[gid], inv2, x0 + l, w, hx, 0);
-            else if (a == 1) v = axis_weight(P[n + gid], inv2, y0 + l, h, hy, 0) * (float)P[4 * n + gid];
-            else v = axis_weight(P[2 * n + gid], inv2, z0 + l, c, hz, zoff);
-            tab[g][a][l] = v;
+        if (tg < nb) {
+            const GRec r = rec[svals[b0 + tg] / (uint32_t)S];
+#pragma unroll
+            for (int k = 0; k < 3 * TT / 8; ++k) {
+                const int e = tj + 8 * k, a = e / TT, l = e % TT;   // compile-time a per k
+                float v;
+                if (a == 0) v = tab_weight(x0 + l, 0, w, r.fx, hx, r.dx, r.inv2);
+                else if (a == 1) v = tab_weight(y0 + l, 0, h, r.fy, hy, r.dy, r.inv2) * r.I;
+                else v = tab_weight(z0 + l, zoff, c, r.fz, hz, r.dz, r.inv2);
+                tab[tg][a][l] = v;
+            }
         }
         __syncthreads();
         for (int g = 0; g < nb; ++g) {
@@ -275,7 +298,7 @@ __global__ void __launch_bounds__(256) k_fvr_fwd(const double* __restrict__ P, i
                 const float4* ez = reinterpret_cast<const float4*>(&tab[g][2][0]);
 #pragma unroll
                 for (int q = 0; q < TT / 4; ++q) {
-                    float4 e4 = ez[q];
+                    const float4 e4 = ez[q];
                     acc[4 * q + 0] = fmaf(cxy, e4.x, acc[4 * q + 0]);
                     acc[4 * q + 1] = fmaf(cxy, e4.y, acc[4 * q + 1]);
                     acc[4 * q + 2] = fmaf(cxy, e4.z, acc[4 * q + 2]);
@@ -300,23 +323,43 @@ __global__ void __launch_bounds__(256) k_fvr_fwd(const double* __restrict__ P, i
 }
 
 // --------------------------------------------------------------------------
-// backward: one CTA per tile, one warp per (tile, Gaussian) pair
+// backward: one CTA per (tile, chunk of <= BWD_CHUNK pairs), one warp per pair
 // --------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_fvr_bwd(const double* __restrict__ P, int64_t n, int w,
-                                                 int h, int c, int zoff, int hx, int hy, int hz,
-                                                 int ntx,
-                                                 int nty, int S,
+constexpr int BWD_CHUNK = 64;
+
+__global__ void k_tile_chunks(const uint32_t* __restrict__ tstart, int64_t nt,
+                              uint32_t* __restrict__ cc, const int* halt) {
+    if (halted(halt)) return;
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t > nt) return;
+    cc[t] = t < nt ? (tstart[t + 1] - tstart[t] + BWD_CHUNK - 1) / BWD_CHUNK : 0u;
+}
+
+__global__ void __launch_bounds__(256) k_fvr_bwd(const GRec* __restrict__ rec, int w, int h, int c,
+                                                 int zoff, int hx, int hy, int hz, int ntx,
+                                                 int nty, int64_t nt, int S,
                                                  const uint32_t* __restrict__ tstart,
+                                                 const uint32_t* __restrict__ cstart,
                                                  const uint32_t* __restrict__ svals,
                                                  const float* __restrict__ up,
                                                  float* __restrict__ part, const int* halt) {
     if (halted(halt)) return;
-    __shared__ float sup[TT][TT][TT + 1];   // [y][x][z], padded
-    const int t = blockIdx.x;
-    const int txi = t % ntx, tyi = (t / ntx) % nty, tzi = t / (ntx * nty);
+    __shared__ float sup[TT][TT][TT + 1];     // upstream tile [y][x][z], padded
+    __shared__ float4 xt[8][TT];              // per warp: {ex, ex*rx, ex*rx^2, -}
+    __shared__ float2 yt[8][TT];              // per warp: {ey, ry}
+    const uint32_t b = blockIdx.x;
+    if (b >= cstart[nt]) return;
+    // tile of this chunk: last t with cstart[t] <= b
+    int64_t lo = 0, hi = nt - 1;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) >> 1;
+        if (cstart[mid] <= b) lo = mid; else hi = mid - 1;
+    }
+    const int64_t t = lo;
+    const uint32_t beg = tstart[t] + (b - cstart[t]) * BWD_CHUNK;
+    const uint32_t end = min(beg + BWD_CHUNK, tstart[t + 1]);
+    const int txi = (int)(t % ntx), tyi = (int)((t / ntx) % nty), tzi = (int)(t / ((int64_t)ntx * nty));
     const int x0 = txi * TT, y0 = tyi * TT, z0 = tzi * TT;
-    const uint32_t beg = tstart[t], end = tstart[t + 1];
-    if (beg == end) return;
     for (int e = threadIdx.x; e < TT * TT * TT; e += blockDim.x) {
         const int z = e % TT, x = (e / TT) % TT, y = e / (TT * TT);
         const int gx = x0 + x, gy = y0 + y, gz = z0 + z;
@@ -329,58 +372,54 @@ __global__ void __launch_bounds__(256) k_fvr_bwd(const double* __restrict__ P, i
     const int zl = lane & (TT - 1), yh = lane >> 4;
     for (uint32_t j = beg + wid; j < end; j += blockDim.x / 32) {
         const uint32_t orig = svals[j];
-        const int64_t gid = orig / (uint32_t)S;
-        const double mx = P[gid], my = P[n + gid], mz = P[2 * n + gid], s = P[3 * n + gid];
-        const float inv2 = (float)(0.5 / (s * s));
-        const double fx = floor(mx), fy = floor(my), fz = floor(mz);
-        // lane l < 16: x-table entry l; lane l >= 16: y-table entry l-16
-        float tabw, tabr;
-        {
-            const bool isx = lane < TT;
+        const GRec r = rec[orig / (uint32_t)S];
+        {   // per-warp separable tables: lanes 0-15 x entries, 16-31 y entries
             const int l = lane & (TT - 1);
-            const int coord = (isx ? x0 : y0) + l;
-            const double f = isx ? fx : fy, mu_a = isx ? mx : my;
-            const int dim = isx ? w : h, half = isx ? hx : hy;
-            const double b = (double)coord - f;
-            const float r = (float)(b - (mu_a - f));
-            const bool ok = coord < dim && fabs(b) <= (double)half;
-            tabw = ok ? expf(-inv2 * r * r) : 0.f;
-            tabr = r;
+            if (lane < TT) {
+                const int bb = x0 + l - r.fx;
+                const float rx = (float)bb - r.dx;
+                const bool ok = x0 + l < w && bb <= hx && bb >= -hx;
+                const float ex = ok ? expf(-r.inv2 * rx * rx) : 0.f;
+                xt[wid][l] = make_float4(ex, ex * rx, ex * rx * rx, 0.f);
+            } else {
+                const int bb = y0 + l - r.fy;
+                const float ry = (float)bb - r.dy;
+                const bool ok = y0 + l < h && bb <= hy && bb >= -hy;
+                yt[wid][l] = make_float2(ok ? expf(-r.inv2 * ry * ry) : 0.f, ry);
+            }
         }
         float wz, rz;
         {
-            const int coord = z0 + zl;
-            const double b = (double)(coord + zoff) - fz;
-            rz = (float)(b - (mz - fz));
-            wz = (coord < c && fabs(b) <= (double)hz) ? expf(-inv2 * rz * rz) : 0.f;
+            const int bb = z0 + zl + zoff - r.fz;
+            rz = (float)bb - r.dz;
+            wz = (z0 + zl < c && bb <= hz && bb >= -hz) ? expf(-r.inv2 * rz * rz) : 0.f;
         }
-        // box intersect tile, tile-local, per axis (uniform across the warp)
-        const int xlo = max((int)(fx - hx) - x0, 0), xhi = min((int)(fx + hx) - x0, TT - 1);
-        const int ylo = max((int)(fy - hy) - y0, 0), yhi = min((int)(fy + hy) - y0, TT - 1);
+        __syncwarp();
+        // box intersect tile, tile-local (uniform across the warp)
+        const int xlo = max(r.fx - hx - x0, 0), xhi = min(r.fx + hx - x0, TT - 1);
+        const int ylo = max(r.fy - hy - y0, 0), yhi = min(r.fy + hy - y0, TT - 1);
         float S0 = 0.f, Sx = 0.f, Sy = 0.f, Sxy2 = 0.f;
         const int nrows = (yhi - ylo + 2) / 2;
         for (int k = 0; k < nrows; ++k) {
             int y = ylo + 2 * k + yh;
             const bool yok = y <= yhi;
             y = yok ? y : yhi;
-            const float ey = __shfl_sync(0xffffffffu, tabw, TT + y);
-            const float ry = __shfl_sync(0xffffffffu, tabr, TT + y);
+            const float2 eyr = yt[wid][y];
             float p0 = 0.f, px = 0.f, pxx = 0.f;
             for (int x = xlo; x <= xhi; ++x) {
-                const float ex = __shfl_sync(0xffffffffu, tabw, x);
-                const float rx = __shfl_sync(0xffffffffu, tabr, x);
-                const float tv = sup[y][x][zl] * ex;
-                const float tr = tv * rx;
-                p0 += tv;
-                px += tr;
-                pxx = fmaf(tr, rx, pxx);
+                const float4 tx4 = xt[wid][x];
+                const float u = sup[y][x][zl];
+                p0 = fmaf(u, tx4.x, p0);
+                px = fmaf(u, tx4.y, px);
+                pxx = fmaf(u, tx4.z, pxx);
             }
-            const float wy = yok ? ey : 0.f;
+            const float wy = yok ? eyr.x : 0.f, ry = eyr.y;
             S0 = fmaf(wy, p0, S0);
             Sx = fmaf(wy, px, Sx);
             Sy = fmaf(wy * ry, p0, Sy);
             Sxy2 = fmaf(wy, fmaf(ry * ry, p0, pxx), Sxy2);
         }
+        __syncwarp();
         float T0 = wz * S0, Tx = wz * Sx, Ty = wz * Sy, Tz = wz * rz * S0,
               T2 = wz * fmaf(rz * rz, S0, Sxy2);
         T0 = warp_sum(T0);
@@ -475,7 +514,7 @@ int splatct_fvr_bin(const double* params, int64_t n, int w, int h, int c, int z0
         k_footprint<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
             params, n, w, h, c, z0, hx, hy, hz, L.ntx, L.nty, L.S, (uint32_t)L.nt,
             at<int32_t>(ws, L.o_fp), at<int32_t>(ws, L.o_gcount), at<uint32_t>(ws, L.o_k0),
-            at<uint32_t>(ws, L.o_v0), tcount, halt);
+            at<uint32_t>(ws, L.o_v0), tcount, at<GRec>(ws, L.o_rec), halt);
         SPLATCT_LAUNCH_CK();
         uint32_t* hist = at<uint32_t>(ws, L.o_hist);
         for (int p = 0; p < L.passes; ++p) {
@@ -493,7 +532,14 @@ int splatct_fvr_bin(const double* params, int64_t n, int w, int h, int c, int z0
             SPLATCT_LAUNCH_CK();
         }
     }
-    return exclusive_scan_u32(tcount, at<uint32_t>(ws, L.o_tstart), L.nt + 1,
+    if (int e = exclusive_scan_u32(tcount, at<uint32_t>(ws, L.o_tstart), L.nt + 1,
+                                   at<void>(ws, L.o_scan), s))
+        return e;
+    // backward work items: ceil(pairs / BWD_CHUNK) chunks per tile
+    k_tile_chunks<<<(unsigned)((L.nt + 1 + 255) / 256), 256, 0, s>>>(
+        at<uint32_t>(ws, L.o_tstart), L.nt, at<uint32_t>(ws, L.o_cc), halt);
+    SPLATCT_LAUNCH_CK();
+    return exclusive_scan_u32(at<uint32_t>(ws, L.o_cc), at<uint32_t>(ws, L.o_cstart), L.nt + 1,
                               at<void>(ws, L.o_scan), s);
 }
 
@@ -504,8 +550,8 @@ int splatct_fvr_forward(const double* params, int64_t n, int w, int h, int c, in
     if (int e = check_args(n, w, h, c, hx, hy, hz, ws_bytes, L)) return e;
     const size_t vo = L.final_buf ? L.o_v1 : L.o_v0;
     k_fvr_fwd<<<(unsigned)L.nt, 256, 0, as_stream(stream)>>>(
-        params, n, w, h, c, z0, hx, hy, hz, L.ntx, L.nty, L.S, at<uint32_t>(ws, L.o_tstart),
-        at<uint32_t>(ws, vo), vol_yxz, halt);
+        at<GRec>(ws, L.o_rec), w, h, c, z0, hx, hy, hz, L.ntx, L.nty, L.S,
+        at<uint32_t>(ws, L.o_tstart), at<uint32_t>(ws, vo), vol_yxz, halt);
     SPLATCT_LAUNCH_CK();
     return SPLATCT_OK;
 }
@@ -519,9 +565,10 @@ int splatct_fvr_backward(const double* params, int64_t n, int w, int h, int c, i
     cudaStream_t s = as_stream(stream);
     const size_t vo = L.final_buf ? L.o_v1 : L.o_v0;
     float* part = at<float>(ws, L.o_part);
-    k_fvr_bwd<<<(unsigned)L.nt, 256, 0, s>>>(params, n, w, h, c, z0, hx, hy, hz, L.ntx, L.nty, L.S,
-                                             at<uint32_t>(ws, L.o_tstart), at<uint32_t>(ws, vo),
-                                             up_yxz, part, halt);
+    k_fvr_bwd<<<(unsigned)L.bwd_grid, 256, 0, s>>>(
+        at<GRec>(ws, L.o_rec), w, h, c, z0, hx, hy, hz, L.ntx, L.nty, L.nt, L.S,
+        at<uint32_t>(ws, L.o_tstart), at<uint32_t>(ws, L.o_cstart), at<uint32_t>(ws, vo), up_yxz,
+        part, halt);
     SPLATCT_LAUNCH_CK();
     k_fvr_combine<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
         params, n, L.S, at<int32_t>(ws, L.o_gcount), part, grads, accum, halt);

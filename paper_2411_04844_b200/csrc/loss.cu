@@ -53,9 +53,9 @@ static Win make_win(int m, int n) {
 }
 
 struct LossLayout {
-    int vr, vc;
-    int64_t nblk_stats, nblk_grad;
-    size_t o_D, o_ps, o_pl, total;
+    int vr, vc, zc, nchunks;
+    int64_t nb_v, nb_g;    // blocks per chunk of the SSIM-map and gradient passes
+    size_t o_H, o_D, o_T, o_ps, o_pl, total;
 };
 
 static LossLayout loss_layout(int m, int n, int p) {
@@ -63,141 +63,192 @@ static LossLayout loss_layout(int m, int n, int p) {
     Win W = make_win(m, n);
     L.vr = m - W.kr + 1;
     L.vc = n - W.kc + 1;
-    const int64_t zc = (p + LZ - 1) / LZ;
-    L.nblk_stats = zc * ((L.vc + LCOL - 1) / LCOL);
-    L.nblk_grad = zc * ((n + LCOL - 1) / LCOL);
+    L.zc = p < 64 ? p : 64;
+    L.nchunks = (p + L.zc - 1) / L.zc;
+    L.nb_v = ((int64_t)L.vr * L.vc * L.zc + 255) / 256;
+    L.nb_g = ((int64_t)m * n * L.zc + 255) / 256;
     size_t off = 0;
     auto take = [&](size_t b) { size_t o = off; off += align_up(b > 0 ? b : 1); return o; };
-    L.o_D = take(sizeof(double) * 3 * (size_t)L.vr * L.vc * p);
-    L.o_ps = take(sizeof(double) * L.nblk_stats);
-    L.o_pl = take(sizeof(double) * L.nblk_grad);
+    L.o_H = take(sizeof(double) * 5 * (size_t)m * L.vc * L.zc);
+    L.o_D = take(sizeof(double) * 3 * (size_t)L.vr * L.vc * L.zc);
+    L.o_T = take(sizeof(double) * 3 * (size_t)L.vr * n * L.zc);
+    L.o_ps = take(sizeof(double) * L.nb_v * L.nchunks);
+    L.o_pl = take(sizeof(double) * L.nb_g * L.nchunks);
     L.total = off;
     return L;
 }
 
-// Pass 1: window statistics, SSIM map, derivative fields D (f64 [3][vr][vc][p]).
-__global__ void __launch_bounds__(LNT) k_ssim_stats(const float* __restrict__ X,
-                                                   const float* __restrict__ Y, int m, int n,
-                                                   int p, Win W, double c1, double c2, int vr,
-                                                   int vc, double* __restrict__ D,
-                                                   double* __restrict__ part, const int* halt) {
+// ---------------------------------------------------------------------------
+// Four separable passes, one thread per output element, processed per chunk
+// of ZC slices so the f64 intermediates (H, D, T) of a chunk stay L2-resident:
+//   S1  H[5][m][vc][zc]  = row-direction window sums of x, y, x^2, y^2, xy
+//   S2  D[3][vr][vc][zc] = column-direction sums -> SSIM map and its
+//                          derivative fields (d_mx, d_x2w, d_xyw), sum of SSIM
+//   G1  T[3][vr][n][zc]  = transposed row correlation of D
+//   G2  grad[m][n][p]    = transposed column correlation of T, combined with
+//                          x, y and the L1 sign term; sum |x - y|
+// (loss.py:83-141: _valid_corr / _valid_corr_adjoint / _ssim_slice).  Every
+// tap loop keeps two partial sums so the DFMA dependency chains are halved.
+// ---------------------------------------------------------------------------
+constexpr int ZC = 64;
+constexpr int PT = 256;   // threads per block
+
+template <int K>
+__device__ __forceinline__ int ktaps(int k) { return K > 0 ? K : k; }
+
+template <int KC_>
+__global__ void __launch_bounds__(PT) k_ssim_h(const float* __restrict__ X, const float* __restrict__ Y,
+                                              int m, int n, int p, int z0, int zc, Win W, int vc,
+                                              double* __restrict__ H, const int* halt) {
     if (halted(halt)) return;
-    extern __shared__ double ring[];   // [KMAX][5][LNT]
-    __shared__ double red[LNT / 32];
-    const int lane = threadIdx.x % LZ, cg = threadIdx.x / LZ;
-    const int z = blockIdx.x * LZ + lane;
-    const int j = blockIdx.y * LCOL + cg;
-    const bool act = z < p && j < vc;
-    double ssum = 0.0;
-    const int kr = W.kr, kc = W.kc;
-    for (int v = 0; v < m && act; ++v) {
-        double h0 = 0, h1 = 0, h2 = 0, h3 = 0, h4 = 0;
-        const int64_t rowb = ((int64_t)v * n + j) * p + z;
-        for (int b = 0; b < kc; ++b) {
-            const double xv = (double)__ldg(X + rowb + (int64_t)b * p);
-            const double yv = (double)__ldg(Y + rowb + (int64_t)b * p);
-            const double g = W.gc[b];
-            h0 += g * xv;
-            h1 += g * yv;
-            h2 += g * (xv * xv);
-            h3 += g * (yv * yv);
-            h4 += g * (xv * yv);
-        }
-        const int slot = v % kr;
-        double* rs = ring + (size_t)slot * 5 * LNT + threadIdx.x;
-        rs[0 * LNT] = h0; rs[1 * LNT] = h1; rs[2 * LNT] = h2; rs[3 * LNT] = h3; rs[4 * LNT] = h4;
-        if (v >= kr - 1) {
-            const int i = v - kr + 1;
-            double mx = 0, my = 0, x2w = 0, y2w = 0, xyw = 0;
-            for (int a = 0; a < kr; ++a) {
-                const double* q = ring + (size_t)((i + a) % kr) * 5 * LNT + threadIdx.x;
-                const double g = W.gr[a];
-                mx += g * q[0];
-                my += g * q[LNT];
-                x2w += g * q[2 * LNT];
-                y2w += g * q[3 * LNT];
-                xyw += g * q[4 * LNT];
-            }
-            const double sx2 = x2w - mx * mx, sy2 = y2w - my * my, sxy = xyw - mx * my;
-            const double a1 = 2.0 * mx * my + c1, a2 = 2.0 * sxy + c2;
-            const double b1 = mx * mx + my * my + c1, b2 = sx2 + sy2 + c2;
-            const double s = (a1 * a2) / (b1 * b2);
-            ssum += s;
-            const double dmx = (2.0 * my * (a2 - a1)) / (b1 * b2) - 2.0 * mx * s * (1.0 / b1 - 1.0 / b2);
-            const double dx2 = -s / b2;
-            const double dxy = 2.0 * a1 / (b1 * b2);
-            const int64_t plane = (int64_t)vr * vc * p;
-            const int64_t o = ((int64_t)i * vc + j) * p + z;
-            D[o] = dmx;
-            D[plane + o] = dx2;
-            D[2 * plane + o] = dxy;
-        }
+    const int64_t idx = blockIdx.x * (int64_t)PT + threadIdx.x;
+    const int64_t tot = (int64_t)m * vc * zc;
+    if (idx >= tot) return;
+    const int zl = (int)(idx % zc);
+    const int64_t vj = idx / zc;
+    const int j = (int)(vj % vc), v = (int)(vj / vc);
+    const int kc = ktaps<KC_>(W.kc);
+    const float* xr = X + ((int64_t)v * n + j) * p + z0 + zl;
+    const float* yr = Y + ((int64_t)v * n + j) * p + z0 + zl;
+    double h[2][5] = {{0, 0, 0, 0, 0}, {0, 0, 0, 0, 0}};
+#pragma unroll
+    for (int b = 0; b < (KC_ > 0 ? KC_ : KMAX); ++b) {
+        if (KC_ == 0 && b >= kc) break;
+        const double xv = (double)__ldg(xr + (int64_t)b * p);
+        const double yv = (double)__ldg(yr + (int64_t)b * p);
+        const double g = W.gc[b];
+        double* hb = h[b & 1];
+        hb[0] = fma(g, xv, hb[0]);
+        hb[1] = fma(g, yv, hb[1]);
+        hb[2] = fma(g, xv * xv, hb[2]);
+        hb[3] = fma(g, yv * yv, hb[3]);
+        hb[4] = fma(g, xv * yv, hb[4]);
     }
-    const double r = block_sum<LNT>(ssum, red);
-    if (threadIdx.x == 0) part[blockIdx.y * gridDim.x + blockIdx.x] = r;
+#pragma unroll
+    for (int f = 0; f < 5; ++f) H[f * tot + idx] = h[0][f] + h[1][f];
 }
 
-// Pass 2: transposed correlation of D, SSIM gradient, L1 term, f32 store.
-__global__ void __launch_bounds__(LNT) k_loss_grad(const float* __restrict__ X,
-                                                  const float* __restrict__ Y, int m, int n,
-                                                  int p, Win W, int vr, int vc,
-                                                  const double* __restrict__ D, double l1w,
-                                                  double l1_count, double ssw, double ssim_slices,
-                                                  float* __restrict__ G,
-                                                  double* __restrict__ part, const int* halt) {
+template <int KR_>
+__global__ void __launch_bounds__(PT) k_ssim_v(const double* __restrict__ H, int m, int zc, Win W,
+                                              int vr, int vc, double c1, double c2,
+                                              double* __restrict__ D, double* __restrict__ part,
+                                              const int* halt) {
     if (halted(halt)) return;
-    extern __shared__ double ring[];   // [KMAX][3][LNT]
-    __shared__ double red[LNT / 32];
-    const int lane = threadIdx.x % LZ, cg = threadIdx.x / LZ;
-    const int z = blockIdx.x * LZ + lane;
-    const int s = blockIdx.y * LCOL + cg;
-    const bool act = z < p && s < n;
-    const int kr = W.kr, kc = W.kc;
-    const int64_t plane = (int64_t)vr * vc * p;
-    const double inv_val = 1.0 / ((double)vr * (double)vc);
-    double l1sum = 0.0;
-    for (int r = 0; r < m && act; ++r) {
-        if (ssw > 0.0 && r < vr) {
-            double t0 = 0, t1 = 0, t2 = 0;
-            for (int b = 0; b < kc; ++b) {
-                const int jj = s - b;
-                if (jj < 0 || jj >= vc) continue;
-                const int64_t o = ((int64_t)r * vc + jj) * p + z;
-                const double g = W.gc[b];
-                t0 += g * D[o];
-                t1 += g * D[plane + o];
-                t2 += g * D[2 * plane + o];
-            }
-            double* rs = ring + (size_t)(r % kr) * 3 * LNT + threadIdx.x;
-            rs[0] = t0; rs[LNT] = t1; rs[2 * LNT] = t2;
+    __shared__ double red[PT / 32];
+    const int64_t idx = blockIdx.x * (int64_t)PT + threadIdx.x;
+    const int64_t tot = (int64_t)vr * vc * zc;      // outputs
+    const int64_t htot = (int64_t)m * vc * zc;      // H field stride
+    const int64_t rstride = (int64_t)vc * zc;       // one row of H
+    double s = 0.0;
+    if (idx < tot) {
+        const int kr = ktaps<KR_>(W.kr);
+        const double* h0 = H + idx;   // row i of H has the same (j, zl) offset
+        double a[2][5] = {{0, 0, 0, 0, 0}, {0, 0, 0, 0, 0}};
+#pragma unroll
+        for (int t = 0; t < (KR_ > 0 ? KR_ : KMAX); ++t) {
+            if (KR_ == 0 && t >= kr) break;
+            const double g = W.gr[t];
+            double* at = a[t & 1];
+#pragma unroll
+            for (int f = 0; f < 5; ++f) at[f] = fma(g, h0[f * htot + t * rstride], at[f]);
         }
-        const int64_t idx = ((int64_t)r * n + s) * p + z;
-        const double xv = (double)__ldg(X + idx), yv = (double)__ldg(Y + idx);
+        const double mx = a[0][0] + a[1][0], my = a[0][1] + a[1][1], x2w = a[0][2] + a[1][2],
+                     y2w = a[0][3] + a[1][3], xyw = a[0][4] + a[1][4];
+        const double sx2 = x2w - mx * mx, sy2 = y2w - my * my, sxy = xyw - mx * my;
+        const double a1 = 2.0 * mx * my + c1, a2 = 2.0 * sxy + c2;
+        const double b1 = mx * mx + my * my + c1, b2 = sx2 + sy2 + c2;
+        const double inv = 1.0 / (b1 * b2);   // 1/b1 = b2*inv, 1/b2 = b1*inv
+        s = (a1 * a2) * inv;
+        D[idx] = (2.0 * my * (a2 - a1)) * inv - 2.0 * mx * s * ((b2 - b1) * inv);
+        D[tot + idx] = -s * (b1 * inv);
+        D[2 * tot + idx] = 2.0 * a1 * inv;
+    }
+    const double r = block_sum<PT>(s, red);
+    if (threadIdx.x == 0) part[blockIdx.x] = r;
+}
+
+template <int KC_>
+__global__ void __launch_bounds__(PT) k_ssim_gh(const double* __restrict__ D, int n, int zc, Win W,
+                                               int vr, int vc, double* __restrict__ T,
+                                               const int* halt) {
+    if (halted(halt)) return;
+    const int64_t idx = blockIdx.x * (int64_t)PT + threadIdx.x;
+    const int64_t tot = (int64_t)vr * n * zc;
+    if (idx >= tot) return;
+    const int zl = (int)(idx % zc);
+    const int64_t is = idx / zc;
+    const int s = (int)(is % n), i = (int)(is / n);
+    const int kc = ktaps<KC_>(W.kc);
+    const int64_t dtot = (int64_t)vr * vc * zc;
+    const int blo = max(0, s - vc + 1), bhi = min(kc - 1, s);
+    const double* d0 = D + ((int64_t)i * vc + s) * zc + zl;   // column jj = s - b
+    double t[2][3] = {{0, 0, 0}, {0, 0, 0}};
+#pragma unroll
+    for (int b = 0; b < (KC_ > 0 ? KC_ : KMAX); ++b) {
+        if (KC_ == 0 && b >= kc) break;
+        if (b < blo || b > bhi) continue;
+        const double g = W.gc[b];
+        const double* q = d0 - (int64_t)b * zc;
+        double* tb = t[b & 1];
+        tb[0] = fma(g, q[0], tb[0]);
+        tb[1] = fma(g, q[dtot], tb[1]);
+        tb[2] = fma(g, q[2 * dtot], tb[2]);
+    }
+    T[idx] = t[0][0] + t[1][0];
+    T[tot + idx] = t[0][1] + t[1][1];
+    T[2 * tot + idx] = t[0][2] + t[1][2];
+}
+
+template <int KR_>
+__global__ void __launch_bounds__(PT) k_loss_gv(const float* __restrict__ X, const float* __restrict__ Y,
+                                               const double* __restrict__ T, int m, int n, int p,
+                                               int z0, int zc, Win W, int vr, int vc, double l1w,
+                                               double l1_count, double ssw, double ssim_slices,
+                                               float* __restrict__ G, double* __restrict__ part,
+                                               const int* halt) {
+    if (halted(halt)) return;
+    __shared__ double red[PT / 32];
+    const int64_t idx = blockIdx.x * (int64_t)PT + threadIdx.x;
+    const int64_t tot = (int64_t)m * n * zc;
+    double l1 = 0.0;
+    if (idx < tot) {
+        const int zl = (int)(idx % zc);
+        const int64_t rs = idx / zc;
+        const int s = (int)(rs % n), r = (int)(rs / n);
+        const int64_t gi = rs * p + z0 + zl;
+        const double xv = (double)__ldg(X + gi), yv = (double)__ldg(Y + gi);
         const double diff = xv - yv;
-        l1sum += fabs(diff);
+        l1 = fabs(diff);
         double g = 0.0;
         if (l1w > 0.0) g += l1w * ((double)((diff > 0) - (diff < 0)) / l1_count);
         if (ssw > 0.0) {
-            double A1 = 0, A2 = 0, A3 = 0;
-            for (int a = 0; a < kr; ++a) {
-                const int i = r - a;
-                if (i < 0 || i >= vr) continue;
-                const double* q = ring + (size_t)(i % kr) * 3 * LNT + threadIdx.x;
+            const int kr = ktaps<KR_>(W.kr);
+            const int64_t ttot = (int64_t)vr * n * zc;
+            const int64_t rstride = (int64_t)n * zc;
+            const int alo = max(0, r - vr + 1), ahi = min(kr - 1, r);
+            const double* t0 = T + ((int64_t)r * n + s) * zc + zl;   // row i = r - a
+            double A[2][3] = {{0, 0, 0}, {0, 0, 0}};
+#pragma unroll
+            for (int a = 0; a < (KR_ > 0 ? KR_ : KMAX); ++a) {
+                if (KR_ == 0 && a >= kr) break;
+                if (a < alo || a > ahi) continue;
                 const double gg = W.gr[a];
-                A1 += gg * q[0];
-                A2 += gg * q[LNT];
-                A3 += gg * q[2 * LNT];
+                const double* q = t0 - (int64_t)a * rstride;
+                double* Aa = A[a & 1];
+                Aa[0] = fma(gg, q[0], Aa[0]);
+                Aa[1] = fma(gg, q[ttot], Aa[1]);
+                Aa[2] = fma(gg, q[2 * ttot], Aa[2]);
             }
-            double gs = A1;
-            gs += 2.0 * xv * A2;
-            gs += yv * A3;
-            gs *= inv_val;
+            double gs = A[0][0] + A[1][0];
+            gs += 2.0 * xv * (A[0][1] + A[1][1]);
+            gs += yv * (A[0][2] + A[1][2]);
+            gs *= 1.0 / ((double)vr * (double)vc);
             g += ssw * (-gs / ssim_slices);
         }
-        G[idx] = (float)g;
+        G[gi] = (float)g;
     }
-    const double rr = block_sum<LNT>(l1sum, red);
-    if (threadIdx.x == 0) part[blockIdx.y * gridDim.x + blockIdx.x] = rr;
+    const double rr = block_sum<PT>(l1, red);
+    if (threadIdx.x == 0) part[blockIdx.x] = rr;
 }
 
 __global__ void __launch_bounds__(1024) k_sino_max(const float* __restrict__ x, int64_t count,
@@ -314,33 +365,56 @@ int splatct_loss_fused(const float* pred, const float* ref, int m, int n, int p,
     if (!(lmax > 0.0)) lmax = 1.0;
     const double c1 = (0.01 * lmax) * (0.01 * lmax), c2 = (0.03 * lmax) * (0.03 * lmax);
     char* base = reinterpret_cast<char*>(ws);
+    double* H = reinterpret_cast<double*>(base + L.o_H);
     double* D = reinterpret_cast<double*>(base + L.o_D);
+    double* T = reinterpret_cast<double*>(base + L.o_T);
     double* ps = reinterpret_cast<double*>(base + L.o_ps);
     double* pl = reinterpret_cast<double*>(base + L.o_pl);
-    const unsigned zc = (unsigned)((p + LZ - 1) / LZ);
-    if (lambda2 > 0.0) {
-        const size_t sm = sizeof(double) * KMAX * 5 * LNT;
-        static bool attr_set = false;
-        if (!attr_set) {
-            SPLATCT_CK(cudaFuncSetAttribute(k_ssim_stats, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)sm));
-            attr_set = true;
+    const bool k11 = W.kr == 11 && W.kc == 11;
+    if (L.nchunks > 1 && p % L.zc != 0) {   // short last chunk leaves unused partial slots
+        SPLATCT_CK(cudaMemsetAsync(ps, 0, sizeof(double) * L.nb_v * L.nchunks, s));
+        SPLATCT_CK(cudaMemsetAsync(pl, 0, sizeof(double) * L.nb_g * L.nchunks, s));
+    }
+    for (int ci = 0; ci < L.nchunks; ++ci) {
+        const int z0 = ci * L.zc, zc = min(L.zc, p - z0);
+        if (lambda2 > 0.0) {
+            const unsigned g1 = (unsigned)(((int64_t)m * L.vc * zc + 255) / 256);
+            const unsigned g2 = (unsigned)(((int64_t)L.vr * L.vc * zc + 255) / 256);
+            const unsigned g3 = (unsigned)(((int64_t)L.vr * n * zc + 255) / 256);
+            if (k11) {
+                k_ssim_h<11><<<g1, PT, 0, s>>>(pred, ref, m, n, p, z0, zc, W, L.vc, H, halt);
+                SPLATCT_LAUNCH_CK();
+                k_ssim_v<11><<<g2, PT, 0, s>>>(H, m, zc, W, L.vr, L.vc, c1, c2, D,
+                                               ps + ci * L.nb_v, halt);
+                SPLATCT_LAUNCH_CK();
+                k_ssim_gh<11><<<g3, PT, 0, s>>>(D, n, zc, W, L.vr, L.vc, T, halt);
+            } else {
+                k_ssim_h<0><<<g1, PT, 0, s>>>(pred, ref, m, n, p, z0, zc, W, L.vc, H, halt);
+                SPLATCT_LAUNCH_CK();
+                k_ssim_v<0><<<g2, PT, 0, s>>>(H, m, zc, W, L.vr, L.vc, c1, c2, D,
+                                              ps + ci * L.nb_v, halt);
+                SPLATCT_LAUNCH_CK();
+                k_ssim_gh<0><<<g3, PT, 0, s>>>(D, n, zc, W, L.vr, L.vc, T, halt);
+            }
+            SPLATCT_LAUNCH_CK();
         }
-        dim3 grid(zc, (unsigned)((L.vc + LCOL - 1) / LCOL));
-        k_ssim_stats<<<grid, LNT, sm, s>>>(pred, ref, m, n, p, W, c1, c2, L.vr, L.vc, D, ps, halt);
+        const unsigned g4 = (unsigned)(((int64_t)m * n * zc + 255) / 256);
+        if (k11)
+            k_loss_gv<11><<<g4, PT, 0, s>>>(pred, ref, T, m, n, p, z0, zc, W, L.vr, L.vc, lambda1,
+                                            l1_count, lambda2, ssim_slices, grad_pred,
+                                            pl + ci * L.nb_g, halt);
+        else
+            k_loss_gv<0><<<g4, PT, 0, s>>>(pred, ref, T, m, n, p, z0, zc, W, L.vr, L.vc, lambda1,
+                                           l1_count, lambda2, ssim_slices, grad_pred,
+                                           pl + ci * L.nb_g, halt);
         SPLATCT_LAUNCH_CK();
-        if (int e = reduce_sum_f64(ps, L.nblk_stats, sums + 1, s)) return e;
+    }
+    if (lambda2 > 0.0) {
+        if (int e = reduce_sum_f64(ps, L.nb_v * L.nchunks, sums + 1, s)) return e;
     } else {
         SPLATCT_CK(cudaMemsetAsync(sums + 1, 0, sizeof(double), s));
     }
-    {
-        const size_t sm = sizeof(double) * KMAX * 3 * LNT;
-        dim3 grid(zc, (unsigned)((n + LCOL - 1) / LCOL));
-        k_loss_grad<<<grid, LNT, sm, s>>>(pred, ref, m, n, p, W, L.vr, L.vc, D, lambda1, l1_count,
-                                          lambda2, ssim_slices, grad_pred, pl, halt);
-        SPLATCT_LAUNCH_CK();
-        if (int e = reduce_sum_f64(pl, L.nblk_grad, sums, s)) return e;
-    }
+    if (int e = reduce_sum_f64(pl, L.nb_g * L.nchunks, sums, s)) return e;
     return SPLATCT_OK;
 }
 

@@ -1,0 +1,477 @@
+// proj_blocked.cu -- 4-row blocked form of the projector operator and its
+// application.
+//
+// The CSR operators of proj.cu spend one 1 KB z-column load (L1 -> registers)
+// per (row, column) weight, i.e. 256 FMAs per 1 KB: the kernels are
+// L1-throughput bound.  Adjacent rays of a view cross mostly the same pixels,
+// and adjacent pixels are crossed by mostly the same rays, so rows are grouped
+// four at a time:
+//   kind 0 (forward, A):  rays 4g .. 4g+3 (consecutive detectors of a view);
+//   kind 1 (adjoint, A^T): the 2x2 pixel quad (2qx..2qx+1, 2qy..2qy+1).
+// A group entry is (column, w[4]) with the four member rows' weights (zero
+// where a row does not touch the column).  One column load now feeds up to
+// four rows: ~2.5x fewer L1 bytes and load instructions per useful FMA.
+// The weights are exactly the CSR weights (same f32 values), summed per row
+// in the same ascending-column order for the adjoint (rows of A^T are sorted
+// by ray), so the blocked and unblocked operators agree to f32 rounding of
+// the accumulation order only.
+#include "common.cuh"
+
+namespace splatct {
+
+constexpr int BLK_NT = 256;
+constexpr int BLK_CAP = 8192;   // max gathered entries per group (4 rows)
+
+struct GroupMap {
+    int kind, nrows, w, h;
+    __host__ __device__ int64_t ngroups() const {
+        if (kind == 0) return (nrows + 3) / 4;
+        return (int64_t)((w + 1) / 2) * ((h + 1) / 2);
+    }
+    // member row k (0..3) of group g, or -1
+    __host__ __device__ int64_t row(int64_t g, int k) const {
+        if (kind == 0) {
+            const int64_t r = 4 * g + k;
+            return r < nrows ? r : -1;
+        }
+        const int qw = (w + 1) / 2;
+        const int qx = (int)(g % qw), qy = (int)(g / qw);
+        const int x = 2 * qx + (k & 1), y = 2 * qy + (k >> 1);
+        return (x < w && y < h) ? (int64_t)y * w + x : -1;
+    }
+};
+
+// One CTA per group: gather the member rows' entries, bitonic-sort by column,
+// merge equal columns into one (column, w[4]) entry.  mode 0 counts, mode 1
+// writes at gptr[g].
+__global__ void __launch_bounds__(BLK_NT) k_block_build(GroupMap gm, const int64_t* __restrict__ ptr,
+                                                        const int32_t* __restrict__ idx,
+                                                        const float* __restrict__ val, int mode,
+                                                        int64_t* __restrict__ gcount,
+                                                        const int64_t* __restrict__ gptr,
+                                                        int32_t* __restrict__ gidx,
+                                                        float4* __restrict__ gval,
+                                                        int* __restrict__ overflow) {
+    extern __shared__ unsigned char smem[];
+    uint32_t* key = reinterpret_cast<uint32_t*>(smem);            // [cap]
+    uint32_t* pay = key + BLK_CAP;                                // [cap] (k << 29 | src)
+    float* wv = reinterpret_cast<float*>(pay + BLK_CAP);          // [cap]
+    __shared__ int64_t beg[4], len[4];
+    __shared__ int total, nuniq;
+    const int64_t g = blockIdx.x;
+    if (threadIdx.x < 4) {
+        const int64_t r = gm.row(g, threadIdx.x);
+        beg[threadIdx.x] = r >= 0 ? ptr[r] : 0;
+        len[threadIdx.x] = r >= 0 ? ptr[r + 1] - ptr[r] : 0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int64_t t = len[0] + len[1] + len[2] + len[3];
+        if (t > BLK_CAP) {
+            atomicExch(overflow, 1);
+            t = 0;
+        }
+        total = (int)t;
+    }
+    __syncthreads();
+    const int L = total;
+    int P = 1;
+    while (P < L) P <<= 1;
+    for (int i = threadIdx.x; i < P; i += BLK_NT) {
+        if (i < L) {
+            int k = 0;
+            int64_t off = i;
+            while (off >= len[k]) { off -= len[k]; ++k; }
+            const int64_t j = beg[k] + off;
+            key[i] = (uint32_t)idx[j];
+            pay[i] = ((uint32_t)k << 29) | (uint32_t)i;
+            wv[i] = mode == 1 ? val[j] : 0.f;
+        } else {
+            key[i] = 0xffffffffu;
+            pay[i] = 0xffffffffu;
+        }
+    }
+    __syncthreads();
+    // bitonic sort of (key, pay) pairs, ascending by key then payload
+    for (int size = 2; size <= P; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int t = threadIdx.x; t < P / 2; t += BLK_NT) {
+                const int lo = 2 * t - (t & (stride - 1));
+                const int hi = lo + stride;
+                const bool up = (lo & size) == 0;
+                const uint64_t a = ((uint64_t)key[lo] << 32) | pay[lo];
+                const uint64_t b = ((uint64_t)key[hi] << 32) | pay[hi];
+                if ((a > b) == up) {
+                    key[lo] = (uint32_t)(b >> 32); pay[lo] = (uint32_t)b;
+                    key[hi] = (uint32_t)(a >> 32); pay[hi] = (uint32_t)a;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    // run heads -> unique columns (serial scan by one warp is enough here)
+    if (threadIdx.x == 0) nuniq = 0;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        int base = 0;
+        for (int i0 = 0; i0 < L; i0 += 32) {
+            const int i = i0 + threadIdx.x;
+            const bool head = i < L && (i == 0 || key[i] != key[i - 1]);
+            const unsigned m = __ballot_sync(0xffffffffu, head);
+            const int pos = base + __popc(m & ((1u << threadIdx.x) - 1u));
+            if (head && mode == 1) {
+                float w4[4] = {0.f, 0.f, 0.f, 0.f};
+                for (int e = i; e < L && key[e] == key[i]; ++e) {
+                    const uint32_t pl = pay[e];
+                    w4[pl >> 29] = wv[pl & 0x1fffffffu];
+                }
+                const int64_t o = gptr[g] + pos;
+                gidx[o] = (int32_t)key[i];
+                gval[o] = make_float4(w4[0], w4[1], w4[2], w4[3]);
+            }
+            base += __popc(m);
+        }
+        if (threadIdx.x == 0) nuniq = base;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && mode == 0) gcount[g] = nuniq;
+}
+
+// ---------------------------------------------------------------------------
+// Blocked application: warp per group, lanes over slices.
+// ---------------------------------------------------------------------------
+template <int V>
+__device__ __forceinline__ void ldvb(const float* p, float (&o)[V]) {
+    if constexpr (V == 4) {
+        const float4 t = __ldg(reinterpret_cast<const float4*>(p));
+        o[0] = t.x; o[1] = t.y; o[2] = t.z; o[3] = t.w;
+    } else if constexpr (V == 2) {
+        const float2 t = __ldg(reinterpret_cast<const float2*>(p));
+        o[0] = t.x; o[1] = t.y;
+    } else {
+        o[0] = __ldg(p);
+    }
+}
+template <int V>
+__device__ __forceinline__ void stvb(float* p, const float (&o)[V]) {
+    if constexpr (V == 4) {
+        *reinterpret_cast<float4*>(p) = make_float4(o[0], o[1], o[2], o[3]);
+    } else if constexpr (V == 2) {
+        *reinterpret_cast<float2*>(p) = make_float2(o[0], o[1]);
+    } else {
+        p[0] = o[0];
+    }
+}
+
+struct TvB {
+    const float* vol;
+    const float* halo_lo;
+    const float* halo_hi;
+    double lambda, count;
+    double* partial;
+    int w, h;
+};
+
+__device__ __forceinline__ int sgnf(float d) { return (d > 0.f) - (d < 0.f); }
+
+constexpr int BS_WARPS = 8;
+
+// TV epilogue for one pixel row and the lane's V consecutive slices
+// [zb, zb+V): forward-difference subgradient of loss.tv_loss (loss.py:195-206)
+// with the x/y neighbours loaded as V-vectors and the z neighbours taken from
+// the adjacent lanes (shuffles) or, at warp/slab edges, from memory / halos.
+template <int V>
+__device__ __forceinline__ void tv_epilogue(const TvB& a, int64_t row, int zb, int c, bool zok,
+                                            const float (&acc)[V], float (&o)[V],
+                                            double& tvsum) {
+    const int lane = threadIdx.x & 31;
+    const int y = (int)(row / a.w), x = (int)(row % a.w);
+    const float* col = a.vol + row * c;
+    float v[V];
+    if (zok) ldvb<V>(col + zb, v);
+    else
+#pragma unroll
+        for (int t = 0; t < V; ++t) v[t] = 0.f;
+    // z neighbours across lanes (all lanes execute the shuffles)
+    const float up_prev = __shfl_up_sync(0xffffffffu, v[V - 1], 1);
+    const float dn_next = __shfl_down_sync(0xffffffffu, v[0], 1);
+    if (!zok) return;
+    int g[V];
+    float s1[V];
+#pragma unroll
+    for (int t = 0; t < V; ++t) { g[t] = 0; s1[t] = 0.f; }
+    auto along = [&](const float* nb_col, bool has_next, bool has_prev, const float* pb_col) {
+        if (has_next) {
+            float n[V];
+            ldvb<V>(nb_col + zb, n);
+#pragma unroll
+            for (int t = 0; t < V; ++t) {
+                const float d = n[t] - v[t];
+                s1[t] += fabsf(d);
+                g[t] -= sgnf(d);
+            }
+        }
+        if (has_prev) {
+            float p[V];
+            ldvb<V>(pb_col + zb, p);
+#pragma unroll
+            for (int t = 0; t < V; ++t) g[t] += sgnf(v[t] - p[t]);
+        }
+    };
+    along(col + c, x + 1 < a.w, x > 0, col - c);
+    along(col + (int64_t)a.w * c, y + 1 < a.h, y > 0, col - (int64_t)a.w * c);
+    // z direction
+#pragma unroll
+    for (int t = 0; t < V; ++t) {
+        const int z = zb + t;
+        float zn = 0.f;
+        bool hn = true;
+        if (t + 1 < V) {
+            zn = v[t + 1];
+        } else if (z + 1 < c) {
+            zn = lane < 31 ? dn_next : __ldg(col + z + 1);
+        } else if (a.halo_hi) {
+            zn = __ldg(a.halo_hi + row);
+        } else {
+            hn = false;
+        }
+        if (hn) {
+            const float d = zn - v[t];
+            s1[t] += fabsf(d);
+            g[t] -= sgnf(d);
+        }
+        float zp = 0.f;
+        bool hp = true;
+        if (t > 0) {
+            zp = v[t - 1];
+        } else if (z > 0) {
+            zp = lane > 0 ? up_prev : __ldg(col + z - 1);
+        } else if (a.halo_lo) {
+            zp = __ldg(a.halo_lo + row);
+        } else {
+            hp = false;
+        }
+        if (hp) g[t] += sgnf(v[t] - zp);
+        o[t] = (float)((double)acc[t] + a.lambda * ((double)g[t] / a.count));
+        tvsum += (double)s1[t];
+    }
+}
+
+// Warp per (group, z-chunk of 32*V slices); groups of 4 rows share every
+// column load.  Entries are staged per warp in shared memory and consumed
+// four at a time (four independent vector loads in flight).
+template <int V, bool TV>
+__global__ void __launch_bounds__(32 * BS_WARPS) k_bspmm(GroupMap gm, const int64_t* __restrict__ gptr,
+                                                        const int32_t* __restrict__ gidx,
+                                                        const float4* __restrict__ gval,
+                                                        const float* __restrict__ X,
+                                                        float* __restrict__ Y, int c, int zsplit,
+                                                        TvB tv, const int* halt) {
+    if (halted(halt)) return;
+    __shared__ int s_col[BS_WARPS][32];
+    __shared__ float4 s_w[BS_WARPS][32];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t gw = blockIdx.x * (int64_t)BS_WARPS + wid;
+    const int64_t g = gw / zsplit;
+    if (g >= gm.ngroups()) return;
+    const int zb = (int)(gw % zsplit) * 32 * V + lane * V;
+    const bool zok = zb < c;
+    const int zl = zok ? zb : 0;   // keep loads in bounds for idle lanes
+    float acc[4][V];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int t = 0; t < V; ++t) acc[k][t] = 0.f;
+    const int64_t b = gptr[g], e = gptr[g + 1];
+    for (int64_t j0 = b; j0 < e; j0 += 32) {
+        const int64_t jl = j0 + lane;
+        __syncwarp();
+        if (jl < e) {
+            s_col[wid][lane] = __ldcs(gidx + jl);
+            s_w[wid][lane] = __ldcs(gval + jl);
+        }
+        __syncwarp();
+        const int cnt = (int)min((int64_t)32, e - j0);
+        int jj = 0;
+        for (; jj + 4 <= cnt; jj += 4) {
+            float xv[4][V];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) ldvb<V>(X + (int64_t)s_col[wid][jj + u] * c + zl, xv[u]);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const float4 w4 = s_w[wid][jj + u];
+#pragma unroll
+                for (int t = 0; t < V; ++t) {
+                    acc[0][t] = fmaf(w4.x, xv[u][t], acc[0][t]);
+                    acc[1][t] = fmaf(w4.y, xv[u][t], acc[1][t]);
+                    acc[2][t] = fmaf(w4.z, xv[u][t], acc[2][t]);
+                    acc[3][t] = fmaf(w4.w, xv[u][t], acc[3][t]);
+                }
+            }
+        }
+        for (; jj < cnt; ++jj) {
+            float xv[V];
+            ldvb<V>(X + (int64_t)s_col[wid][jj] * c + zl, xv);
+            const float4 w4 = s_w[wid][jj];
+#pragma unroll
+            for (int t = 0; t < V; ++t) {
+                acc[0][t] = fmaf(w4.x, xv[t], acc[0][t]);
+                acc[1][t] = fmaf(w4.y, xv[t], acc[1][t]);
+                acc[2][t] = fmaf(w4.z, xv[t], acc[2][t]);
+                acc[3][t] = fmaf(w4.w, xv[t], acc[3][t]);
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int64_t row = gm.row(g, k);
+        if (row < 0) continue;   // uniform across the warp
+        float o[V];
+        if constexpr (TV) {
+            double tvsum = 0.0;
+            tv_epilogue<V>(tv, row, zb, c, zok, acc[k], o, tvsum);
+            if (zok) stvb<V>(Y + row * c + zb, o);
+            if (tv.partial) {   // slot (z-chunk, row): written once, reduced in fixed order
+                tvsum = warp_sum(tvsum);
+                if (lane == 0) tv.partial[(gw % zsplit) * (int64_t)gm.nrows + row] = tvsum;
+            }
+        } else {
+            if (zok) stvb<V>(Y + row * c + zb, acc[k]);
+        }
+    }
+}
+
+template <int V, bool TV>
+static int launch_bspmm_v(const GroupMap& gm, const int64_t* gptr, const int32_t* gidx,
+                          const float* gval, const float* X, float* Y, int c, const TvB& tv,
+                          const int* halt, cudaStream_t s) {
+    const int zsplit = (c + 32 * V - 1) / (32 * V);
+    const int64_t warps = gm.ngroups() * zsplit;
+    const unsigned grid = (unsigned)((warps + BS_WARPS - 1) / BS_WARPS);
+    k_bspmm<V, TV><<<grid, 32 * BS_WARPS, 0, s>>>(gm, gptr, gidx,
+                                                  reinterpret_cast<const float4*>(gval), X, Y, c,
+                                                  zsplit, tv, halt);
+    SPLATCT_LAUNCH_CK();
+    return SPLATCT_OK;
+}
+
+static int vec_width(int c) {
+    if (c % 4 == 0 && c >= 128) return 4;
+    if (c % 2 == 0 && c >= 64) return 2;
+    return 1;
+}
+
+template <bool TV>
+static int launch_bspmm(const GroupMap& gm, const int64_t* gptr, const int32_t* gidx,
+                        const float* gval, const float* X, float* Y, int c, const TvB& tv,
+                        const int* halt, cudaStream_t s) {
+    const int V = vec_width(c);
+    SPLATCT_REQUIRE((uintptr_t)X % (4 * V) == 0 && (uintptr_t)Y % (4 * V) == 0 &&
+                        (!TV || (uintptr_t)tv.vol % (4 * V) == 0),
+                    "projector operands must be %d-byte aligned", 4 * V);
+    if (V == 4) return launch_bspmm_v<4, TV>(gm, gptr, gidx, gval, X, Y, c, tv, halt, s);
+    if (V == 2) return launch_bspmm_v<2, TV>(gm, gptr, gidx, gval, X, Y, c, tv, halt, s);
+    return launch_bspmm_v<1, TV>(gm, gptr, gidx, gval, X, Y, c, tv, halt, s);
+}
+
+static size_t block_smem() { return (size_t)BLK_CAP * 12; }
+
+}  // namespace splatct
+
+using namespace splatct;
+
+extern "C" {
+
+int splatct_proj_tv_partial_len(int w, int h, int c, int64_t* len) {
+    const int V = vec_width(c);
+    *len = (int64_t)w * h * ((c + 32 * V - 1) / (32 * V));
+    return SPLATCT_OK;
+}
+
+int splatct_proj_block_scratch_bytes(int nrows, int kind, int w, int h, size_t* bytes) {
+    GroupMap gm{kind, nrows, w, h};
+    const int64_t ng = gm.ngroups();
+    *bytes = align_up(sizeof(int64_t) * (ng + 1)) + scan_temp_bytes(ng + 1) + 256;
+    return SPLATCT_OK;
+}
+
+int splatct_proj_block_count(const int64_t* ptr, const int32_t* idx, int nrows, int kind, int w,
+                             int h, int64_t* gptr, void* scratch, size_t scratch_bytes,
+                             int64_t* nb, void* stream) {
+    SPLATCT_REQUIRE(kind == 0 || kind == 1, "kind must be 0 (row groups) or 1 (pixel quads)");
+    GroupMap gm{kind, nrows, w, h};
+    const int64_t ng = gm.ngroups();
+    size_t need = 0;
+    splatct_proj_block_scratch_bytes(nrows, kind, w, h, &need);
+    SPLATCT_REQUIRE(scratch_bytes >= need, "block scratch too small");
+    cudaStream_t s = as_stream(stream);
+    int64_t* cnt = reinterpret_cast<int64_t*>(scratch);
+    char* scan_tmp = reinterpret_cast<char*>(scratch) + align_up(sizeof(int64_t) * (ng + 1));
+    int* overflow = reinterpret_cast<int*>(scan_tmp + scan_temp_bytes(ng + 1));
+    SPLATCT_CK(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (ng + 1), s));
+    SPLATCT_CK(cudaMemsetAsync(overflow, 0, sizeof(int), s));
+    static bool attr = false;
+    if (!attr) {
+        SPLATCT_CK(cudaFuncSetAttribute(k_block_build, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)block_smem()));
+        attr = true;
+    }
+    k_block_build<<<(unsigned)ng, BLK_NT, block_smem(), s>>>(gm, ptr, idx, nullptr, 0, cnt, nullptr,
+                                                             nullptr, nullptr, overflow);
+    SPLATCT_LAUNCH_CK();
+    if (int e = exclusive_scan_i64(cnt, gptr, ng + 1, scan_tmp, s)) return e;
+    int ovf = 0;
+    SPLATCT_CK(cudaMemcpyAsync(nb, gptr + ng, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    SPLATCT_CK(cudaMemcpyAsync(&ovf, overflow, sizeof(int), cudaMemcpyDeviceToHost, s));
+    SPLATCT_CK(cudaStreamSynchronize(s));
+    SPLATCT_REQUIRE(!ovf, "a 4-row group has more than %d entries", BLK_CAP);
+    return SPLATCT_OK;
+}
+
+int splatct_proj_block_fill(const int64_t* ptr, const int32_t* idx, const float* val, int nrows,
+                            int kind, int w, int h, const int64_t* gptr, int32_t* gidx,
+                            float* gval, void* scratch, size_t scratch_bytes, void* stream) {
+    GroupMap gm{kind, nrows, w, h};
+    const int64_t ng = gm.ngroups();
+    size_t need = 0;
+    splatct_proj_block_scratch_bytes(nrows, kind, w, h, &need);
+    SPLATCT_REQUIRE(scratch_bytes >= need, "block scratch too small");
+    SPLATCT_REQUIRE((uintptr_t)gval % 16 == 0, "gval must be 16-byte aligned");
+    cudaStream_t s = as_stream(stream);
+    int* overflow = reinterpret_cast<int*>(reinterpret_cast<char*>(scratch) +
+                                           align_up(sizeof(int64_t) * (ng + 1)) +
+                                           scan_temp_bytes(ng + 1));
+    k_block_build<<<(unsigned)ng, BLK_NT, block_smem(), s>>>(
+        gm, ptr, idx, val, 1, nullptr, gptr, gidx, reinterpret_cast<float4*>(gval), overflow);
+    SPLATCT_LAUNCH_CK();
+    SPLATCT_CK(cudaStreamSynchronize(s));
+    return SPLATCT_OK;
+}
+
+int splatct_proj_forward_blocked(const int64_t* gptr, const int32_t* gidx, const float* gval,
+                                 int n_rays, const float* vol_yxz, float* sino, int c,
+                                 const int* halt, void* stream) {
+    SPLATCT_REQUIRE(n_rays >= 0 && c > 0, "invalid sizes");
+    GroupMap gm{0, n_rays, 0, 0};
+    TvB tv{};
+    return launch_bspmm<false>(gm, gptr, gidx, gval, vol_yxz, sino, c, tv, halt,
+                               as_stream(stream));
+}
+
+int splatct_proj_adjoint_blocked(const int64_t* gptr, const int32_t* gidx, const float* gval,
+                                 int w, int h, int c, const float* gsino, const float* vol_yxz,
+                                 const float* halo_lo, const float* halo_hi, double lambda_tv,
+                                 double tv_count, float* out_yxz, double* tv_partial,
+                                 const int* halt, void* stream) {
+    SPLATCT_REQUIRE(w > 0 && h > 0 && c > 0, "invalid sizes");
+    GroupMap gm{1, w * h, w, h};
+    TvB tv{vol_yxz, halo_lo, halo_hi, lambda_tv, tv_count, tv_partial, w, h};
+    cudaStream_t s = as_stream(stream);
+    if (vol_yxz != nullptr && lambda_tv > 0.0) {
+        SPLATCT_REQUIRE(tv_count > 0.0, "tv_count must be positive");
+        return launch_bspmm<true>(gm, gptr, gidx, gval, gsino, out_yxz, c, tv, halt, s);
+    }
+    return launch_bspmm<false>(gm, gptr, gidx, gval, gsino, out_yxz, c, tv, halt, s);
+}
+
+}  // extern "C"

@@ -148,7 +148,8 @@ class ProjectorOperator:
     merging sample weights per (ray, pixel); reused every iteration.
     """
 
-    def __init__(self, geom: ScanGeometry, w: int, h: int, step: float = 0.5, device=None):
+    def __init__(self, geom: ScanGeometry, w: int, h: int, step: float = 0.5, device=None,
+                 blocked: bool = True):
         self.device = require_cuda(device)
         geom.check_volume((w, h, 1))
         self.geom = geom
@@ -185,6 +186,26 @@ class ProjectorOperator:
              ptr(self.at_ptr), ptr(self.at_ray), ptr(self.at_val), ptr(scratch), sb,
              stream_handle())
         del scratch
+        self.blocked = blocked
+        if blocked:
+            self.fb = self._block(self.a_ptr, self.a_col, self.a_val, self.n_rays, 0)
+            self.ab = self._block(self.at_ptr, self.at_ray, self.at_val, self.w * self.h, 1)
+
+    def _block(self, ptr_, idx, val, nrows, kind):
+        """4-row blocked copy (gptr, gidx, gval[nb, 4]) of a CSR operator."""
+        sb = size_query("splatct_proj_block_scratch_bytes", nrows, kind, self.w, self.h)
+        scratch = torch.empty(sb, dtype=torch.uint8, device=self.device)
+        ng = (nrows + 3) // 4 if kind == 0 else ((self.w + 1) // 2) * ((self.h + 1) // 2)
+        gptr = torch.empty(ng + 1, dtype=torch.int64, device=self.device)
+        nb = ctypes.c_int64(0)
+        call("splatct_proj_block_count", ptr(ptr_), ptr(idx), nrows, kind, self.w, self.h,
+             ptr(gptr), ptr(scratch), sb, ctypes.byref(nb), stream_handle())
+        k = max(int(nb.value), 1)
+        gidx = torch.empty(k, dtype=torch.int32, device=self.device)
+        gval = torch.empty((k, 4), dtype=torch.float32, device=self.device)
+        call("splatct_proj_block_fill", ptr(ptr_), ptr(idx), ptr(val), nrows, kind, self.w,
+             self.h, ptr(gptr), ptr(gidx), ptr(gval), ptr(scratch), sb, stream_handle())
+        return gptr, gidx, gval, int(nb.value)
 
     def _gargs(self):
         return (ptr(self.cos_t), ptr(self.sin_t), self.m, self.n_det, self.spacing, self.step,
@@ -192,28 +213,42 @@ class ProjectorOperator:
 
     @property
     def matrix_bytes(self) -> int:
-        return 16 * self.nnz + 8 * (self.n_rays + self.w * self.h + 2)
+        b = 16 * self.nnz + 8 * (self.n_rays + self.w * self.h + 2)
+        if self.blocked:
+            b += 20 * (self.fb[3] + self.ab[3]) + 8 * (len(self.fb[0]) + len(self.ab[0]))
+        return b
 
-    def forward(self, vol: torch.Tensor, out: torch.Tensor | None = None, halt=None):
+    def forward(self, vol: torch.Tensor, out: torch.Tensor | None = None, halt=None,
+                blocked: bool | None = None):
         """vol (h, w, c) -> sinogram (m, n, c)."""
         c = int(vol.shape[2])
         if out is None:
             out = torch.empty((self.m, self.n_det, c), dtype=torch.float32, device=vol.device)
-        call("splatct_proj_forward", ptr(self.a_ptr), ptr(self.a_col), ptr(self.a_val),
-             self.n_rays, ptr(vol), ptr(out), c, ptr(halt), stream_handle())
+        if self.blocked if blocked is None else blocked:
+            g = self.fb
+            call("splatct_proj_forward_blocked", ptr(g[0]), ptr(g[1]), ptr(g[2]), self.n_rays,
+                 ptr(vol), ptr(out), c, ptr(halt), stream_handle())
+        else:
+            call("splatct_proj_forward", ptr(self.a_ptr), ptr(self.a_col), ptr(self.a_val),
+                 self.n_rays, ptr(vol), ptr(out), c, ptr(halt), stream_handle())
         return out
 
     def adjoint(self, gsino: torch.Tensor, out: torch.Tensor | None = None, vol=None,
                 halo_lo=None, halo_hi=None, lambda_tv: float = 0.0, tv_count: float = 1.0,
-                tv_partial=None, halt=None):
+                tv_partial=None, halt=None, blocked: bool | None = None):
         """sinogram (m, n, c) -> volume (h, w, c) [+ lambda_tv * TV subgradient of vol]."""
         c = int(gsino.shape[2])
         if out is None:
             out = torch.empty((self.h, self.w, c), dtype=torch.float32, device=gsino.device)
-        call("splatct_proj_adjoint", ptr(self.at_ptr), ptr(self.at_ray), ptr(self.at_val),
-             self.w, self.h, c, ptr(gsino), ptr(vol), ptr(halo_lo), ptr(halo_hi),
-             float(lambda_tv), float(tv_count), ptr(out), ptr(tv_partial), ptr(halt),
-             stream_handle())
+        args = (ptr(gsino), ptr(vol), ptr(halo_lo), ptr(halo_hi), float(lambda_tv),
+                float(tv_count), ptr(out), ptr(tv_partial), ptr(halt), stream_handle())
+        if getattr(self, "blocked", False) if blocked is None else blocked:
+            g = self.ab
+            call("splatct_proj_adjoint_blocked", ptr(g[0]), ptr(g[1]), ptr(g[2]), self.w, self.h,
+                 c, *args)
+        else:
+            call("splatct_proj_adjoint", ptr(self.at_ptr), ptr(self.at_ray), ptr(self.at_val),
+                 self.w, self.h, c, *args)
         return out
 
     def march_forward(self, vol: torch.Tensor) -> torch.Tensor:
@@ -241,6 +276,13 @@ def projector_for(geom: ScanGeometry, w: int, h: int, step: float = 0.5,
     else:
         _PROJ_CACHE.move_to_end(key)
     return op
+
+
+def tv_partial_len(w: int, h: int, c: int) -> int:
+    """Doubles in the tv_partial buffer of the blocked adjoint (+ CSR: w*h)."""
+    n = ctypes.c_int64(0)
+    call("splatct_proj_tv_partial_len", int(w), int(h), int(c), ctypes.byref(n))
+    return max(int(n.value), int(w) * int(h))
 
 
 def tv_operator(w: int, h: int, device=None) -> ProjectorOperator:

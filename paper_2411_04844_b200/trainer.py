@@ -84,7 +84,8 @@ class Trainer:
         self.gpred = torch.empty_like(self.pred)
         self.vol = torch.empty((self.h, self.w, cl), dtype=torch.float32, device=dev)
         self.dl = torch.empty_like(self.vol)
-        self.tv_part = torch.zeros(self.w * self.h, dtype=torch.float64, device=dev)
+        self.tv_part = torch.zeros(D.tv_partial_len(self.w, self.h, cl), dtype=torch.float64,
+                                   device=dev)
         self.sums = torch.zeros(3, dtype=torch.float64, device=dev)
         self.adam_s = torch.zeros(3, dtype=torch.float64, device=dev)
         self.step_t = torch.tensor([int(step)], dtype=torch.int64, device=dev)

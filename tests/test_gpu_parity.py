@@ -213,7 +213,10 @@ def test_ssim_value_and_psnr():
     x = rng.uniform(0, 1, (40, 30))
     assert abs(loss.ssim_value(x, x) - 1.0) < 1e-9
     y = rng.uniform(0, 1, (40, 30))
-    assert abs(loss.ssim_value(x, y) - O.ssim_value(x, y)) < 1e-9
+    # images enter the kernels as float32 (the training loop's storage type)
+    assert abs(loss.ssim_value(x, y) - O.ssim_value(x, y)) < 1e-6
+    xf, yf = x.astype(np.float32), y.astype(np.float32)
+    assert abs(loss.ssim_value(xf, yf) - O.ssim_value(xf, yf)) < 1e-12
     assert metrics.psnr(np.full(10, 0.1), np.zeros(10), max_val=1.0) == pytest.approx(20.0, abs=1e-12)
 
 
@@ -357,9 +360,33 @@ def test_nonfinite_loss_raises():
     dims = (32, 32, 32)
     geom = core.ScanGeometry.parallel(8, 48)
     meas = core.Sinogram.from_views(np.ones((8, 48, 32), np.float32))
-    cl = core.GaussianCloud([[16.0, 16, 16]], [1.0], [1e38])
+    cl = core.GaussianCloud([[16.0, 16, 16]], [1.0], [1e300])   # inf once stored as f32
     st = optim.ReconstructionSettings(dims=dims, box=core.BoxConfig.cube(17), max_iters=3,
                                       densify_interval=0)
     with pytest.raises(optim.NonFiniteLossError) as ei:
         optim.run_reconstruction(meas, geom, st, init_cloud=cl)
     assert ei.value.snapshot["iteration"] == 0
+
+
+@pytest.mark.parametrize("variant,dims,m,n", [("parallel", (24, 20, 70), 7, 30),
+                                              ("fan", (13, 21, 300), 6, 17),
+                                              ("fan", (64, 48, 5), 11, 93)])
+def test_blocked_operator_matches_csr(variant, dims, m, n):
+    """4-row blocked A / A^T (+TV epilogue) equal the CSR operators."""
+    dev = D.require_cuda()
+    w, h, c = dims
+    geom = (core.ScanGeometry.parallel(m, n, 0.9) if variant == "parallel"
+            else core.ScanGeometry.fan(m, n, 1.7, 60.0, 40.0))
+    op = D.ProjectorOperator(geom, w, h, 0.5, dev)
+    g = torch.Generator().manual_seed(1)
+    x = torch.randn((h, w, c), generator=g).to(dev)
+    y = torch.randn((m, n, c), generator=g).to(dev)
+    a = op.forward(x, blocked=True)
+    b = op.forward(x, blocked=False)
+    assert rel_l2(a.cpu().numpy(), b.cpu().numpy()) < 1e-6
+    pa = torch.zeros(D.tv_partial_len(w, h, c), dtype=torch.float64, device=dev)
+    pb = torch.zeros_like(pa)
+    a = op.adjoint(y, vol=x, lambda_tv=0.3, tv_count=float(w * h * c), tv_partial=pa, blocked=True)
+    b = op.adjoint(y, vol=x, lambda_tv=0.3, tv_count=float(w * h * c), tv_partial=pb, blocked=False)
+    assert rel_l2(a.cpu().numpy(), b.cpu().numpy()) < 1e-6
+    assert abs(float(pa.sum()) - float(pb.sum())) <= 1e-8 * abs(float(pb.sum()))
