@@ -156,15 +156,18 @@ int splatct_proj_adjoint(const int64_t* at_ptr, const int32_t* at_ray, const flo
  * rows 4g..4g+3 (consecutive rays of A); kind 1 groups the 2x2 pixel quad
  * (2qx+dx, 2qy+dy), k = 2*dy + dx, of A^T on a w x h slice.  A group entry
  * is (column, w[4]) with the member rows' weights (0 where absent), columns
- * ascending.  count (synchronous) -> gptr[ngroups+1] and *nb; fill -> gidx,
- * gval (float[nb][4], 16-byte aligned). */
+ * ascending -- or, with order_dir (device float[ngroups][2], the group's ray
+ * direction; kind 0 only), in march order along that direction so concurrent
+ * warps sweep the slice together.  count (synchronous) -> gptr[ngroups+1]
+ * and *nb; fill -> gidx, gval (float[nb][4], 16-byte aligned). */
 int splatct_proj_block_scratch_bytes(int nrows, int kind, int w, int h, size_t* bytes);
 int splatct_proj_block_count(const int64_t* ptr, const int32_t* idx, int nrows, int kind, int w,
-                             int h, int64_t* gptr, void* scratch, size_t scratch_bytes,
-                             int64_t* nb, void* stream);
+                             int h, const float* order_dir, int64_t* gptr, void* scratch,
+                             size_t scratch_bytes, int64_t* nb, void* stream);
 int splatct_proj_block_fill(const int64_t* ptr, const int32_t* idx, const float* val, int nrows,
-                            int kind, int w, int h, const int64_t* gptr, int32_t* gidx,
-                            float* gval, void* scratch, size_t scratch_bytes, void* stream);
+                            int kind, int w, int h, const float* order_dir, const int64_t* gptr,
+                            int32_t* gidx, float* gval, void* scratch, size_t scratch_bytes,
+                            void* stream);
 
 /* Length (doubles) of the tv_partial buffer splatct_proj_adjoint_blocked
  * writes for a w x h x c slab: one slot per (pixel column, 32*V-slice chunk),

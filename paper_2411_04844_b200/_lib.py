@@ -46,10 +46,10 @@ SIGNATURES: dict[str, list] = {
                              c_f64, c_vp, c_vp, c_vp, c_vp],
     "splatct_proj_tv_partial_len": [c_i32, c_i32, c_i32, c_i64p],
     "splatct_proj_block_scratch_bytes": [c_i32, c_i32, c_i32, c_i32, c_szp],
-    "splatct_proj_block_count": [c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_vp, c_vp, c_sz, c_i64p,
-                                 c_vp],
+    "splatct_proj_block_count": [c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp, c_sz,
+                                 c_i64p, c_vp],
     "splatct_proj_block_fill": [c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp,
-                                c_sz, c_vp],
+                                c_vp, c_sz, c_vp],
     "splatct_proj_forward_blocked": [c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_i32, c_vp, c_vp],
     "splatct_proj_adjoint_blocked": [c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp,
                                      c_f64, c_f64, c_vp, c_vp, c_vp, c_vp],

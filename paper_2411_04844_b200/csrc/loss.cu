@@ -55,67 +55,98 @@ static Win make_win(int m, int n) {
 struct LossLayout {
     int vr, vc, zc, nchunks;
     int64_t nb_v, nb_g;    // blocks per chunk of the SSIM-map and gradient passes
-    size_t o_H, o_D, o_T, o_ps, o_pl, total;
+    int64_t nb_s11, nb_g11;   // blocks of the 11x11 row-walking kernels
+    bool k11;
+    size_t o_H, o_D, o_T, o_ps, o_pl, o_D11, total;
 };
+
+constexpr int ZC = 64;    // slices per chunk (one block = 4 columns x ZC slices)
+constexpr int PT = 256;   // threads per block
 
 static LossLayout loss_layout(int m, int n, int p) {
     LossLayout L{};
     Win W = make_win(m, n);
     L.vr = m - W.kr + 1;
     L.vc = n - W.kc + 1;
-    L.zc = p < 64 ? p : 64;
-    L.nchunks = (p + L.zc - 1) / L.zc;
-    L.nb_v = ((int64_t)L.vr * L.vc * L.zc + 255) / 256;
-    L.nb_g = ((int64_t)m * n * L.zc + 255) / 256;
+    L.zc = p < ZC ? p : ZC;
+    L.nchunks = (p + ZC - 1) / ZC;
+    L.nb_v = (int64_t)((L.vr + 3) / 4) * L.vc;
+    L.nb_g = (int64_t)((m + 3) / 4) * n;
     size_t off = 0;
     auto take = [&](size_t b) { size_t o = off; off += align_up(b > 0 ? b : 1); return o; };
-    L.o_H = take(sizeof(double) * 5 * (size_t)m * L.vc * L.zc);
-    L.o_D = take(sizeof(double) * 3 * (size_t)L.vr * L.vc * L.zc);
-    L.o_T = take(sizeof(double) * 3 * (size_t)L.vr * n * L.zc);
-    L.o_ps = take(sizeof(double) * L.nb_v * L.nchunks);
-    L.o_pl = take(sizeof(double) * L.nb_g * L.nchunks);
+    L.k11 = W.kr == 11 && W.kc == 11 && p % 4 == 0;
+    L.nb_s11 = (int64_t)((p + 31) / 32) * ((L.vc + 7) / 8);
+    L.nb_g11 = (int64_t)((p + 31) / 32) * ((n + 7) / 8);
+    if (L.k11) {   // row-walking kernels: full-p D, no H/T
+        L.o_H = L.o_T = 0;
+        L.o_D11 = take(sizeof(double) * 3 * (size_t)L.vr * L.vc * p);
+        L.o_D = L.o_D11;
+        L.o_ps = take(sizeof(double) * L.nb_s11);
+        L.o_pl = take(sizeof(double) * L.nb_g11);
+    } else {
+        L.o_H = take(sizeof(double) * 5 * (size_t)m * L.vc * ZC);
+        L.o_D = take(sizeof(double) * 3 * (size_t)L.vr * L.vc * ZC);
+        L.o_T = take(sizeof(double) * 3 * (size_t)L.vr * n * ZC);
+        L.o_ps = take(sizeof(double) * L.nb_v * L.nchunks);
+        L.o_pl = take(sizeof(double) * L.nb_g * L.nchunks);
+    }
     L.total = off;
     return L;
 }
 
 // ---------------------------------------------------------------------------
-// Four separable passes, one thread per output element, processed per chunk
-// of ZC slices so the f64 intermediates (H, D, T) of a chunk stay L2-resident:
-//   S1  H[5][m][vc][zc]  = row-direction window sums of x, y, x^2, y^2, xy
-//   S2  D[3][vr][vc][zc] = column-direction sums -> SSIM map and its
+// Four separable passes, processed per chunk of ZC = 64 slices so the f64
+// intermediates (H, D, T) of a chunk stay L2-resident:
+//   S1  H[5][m][vc][ZC]  = row-direction window sums of x, y, x^2, y^2, xy
+//   S2  D[3][vr][vc][ZC] = column-direction sums -> SSIM map and its
 //                          derivative fields (d_mx, d_x2w, d_xyw), sum of SSIM
-//   G1  T[3][vr][n][zc]  = transposed row correlation of D
+//   G1  T[3][vr][n][ZC]  = transposed row correlation of D
 //   G2  grad[m][n][p]    = transposed column correlation of T, combined with
 //                          x, y and the L1 sign term; sum |x - y|
-// (loss.py:83-141: _valid_corr / _valid_corr_adjoint / _ssim_slice).  Every
-// tap loop keeps two partial sums so the DFMA dependency chains are halved.
+// (loss.py:83-141: _valid_corr / _valid_corr_adjoint / _ssim_slice).
+// A block computes 4 consecutive outputs along the filtered axis for 64
+// slices; it first stages the 4 + 10 input positions it needs in shared
+// memory (coalesced 256 B rows), so every tap is an immediate-offset LDS and
+// each input value is read from L2 once per block instead of 11 times.
+// Tap loops keep two partial sums (even / odd taps) to halve DFMA chains.
 // ---------------------------------------------------------------------------
-constexpr int ZC = 64;
-constexpr int PT = 256;   // threads per block
+constexpr int OB = 4;            // outputs per block along the filtered axis
+constexpr int SPAN = OB + KMAX - 1;
 
 template <int K>
 __device__ __forceinline__ int ktaps(int k) { return K > 0 ? K : k; }
 
+// S1: block (row v, columns j0..j0+3); stage x, y columns j0..j0+13.
 template <int KC_>
 __global__ void __launch_bounds__(PT) k_ssim_h(const float* __restrict__ X, const float* __restrict__ Y,
                                               int m, int n, int p, int z0, int zc, Win W, int vc,
                                               double* __restrict__ H, const int* halt) {
     if (halted(halt)) return;
-    const int64_t idx = blockIdx.x * (int64_t)PT + threadIdx.x;
-    const int64_t tot = (int64_t)m * vc * zc;
-    if (idx >= tot) return;
-    const int zl = (int)(idx % zc);
-    const int64_t vj = idx / zc;
-    const int j = (int)(vj % vc), v = (int)(vj / vc);
+    __shared__ float sx[SPAN][ZC], sy[SPAN][ZC];
+    const int zl = threadIdx.x & (ZC - 1), o = threadIdx.x / ZC;
+    const int j0 = blockIdx.x * OB, v = blockIdx.y;
     const int kc = ktaps<KC_>(W.kc);
-    const float* xr = X + ((int64_t)v * n + j) * p + z0 + zl;
-    const float* yr = Y + ((int64_t)v * n + j) * p + z0 + zl;
+    const int ncol = min(OB + kc - 1, n - j0);
+    for (int e = threadIdx.x; e < SPAN * ZC; e += PT) {
+        const int cidx = e / ZC, z = e & (ZC - 1);
+        float xv = 0.f, yv = 0.f;
+        if (cidx < ncol && z < zc) {
+            const int64_t gi = ((int64_t)v * n + j0 + cidx) * p + z0 + z;
+            xv = __ldg(X + gi);
+            yv = __ldg(Y + gi);
+        }
+        sx[cidx][z] = xv;
+        sy[cidx][z] = yv;
+    }
+    __syncthreads();
+    const int j = j0 + o;
+    if (zl >= zc || j >= vc) return;
     double h[2][5] = {{0, 0, 0, 0, 0}, {0, 0, 0, 0, 0}};
 #pragma unroll
     for (int b = 0; b < (KC_ > 0 ? KC_ : KMAX); ++b) {
         if (KC_ == 0 && b >= kc) break;
-        const double xv = (double)__ldg(xr + (int64_t)b * p);
-        const double yv = (double)__ldg(yr + (int64_t)b * p);
+        const double xv = (double)sx[o + b][zl];
+        const double yv = (double)sy[o + b][zl];
         const double g = W.gc[b];
         double* hb = h[b & 1];
         hb[0] = fma(g, xv, hb[0]);
@@ -124,25 +155,36 @@ __global__ void __launch_bounds__(PT) k_ssim_h(const float* __restrict__ X, cons
         hb[3] = fma(g, yv * yv, hb[3]);
         hb[4] = fma(g, xv * yv, hb[4]);
     }
+    const int64_t tot = (int64_t)m * vc * ZC;
+    const int64_t idx = ((int64_t)v * vc + j) * ZC + zl;
 #pragma unroll
     for (int f = 0; f < 5; ++f) H[f * tot + idx] = h[0][f] + h[1][f];
 }
 
+// S2: block (rows i0..i0+3, column j); stage H rows i0..i0+13 of column j.
 template <int KR_>
 __global__ void __launch_bounds__(PT) k_ssim_v(const double* __restrict__ H, int m, int zc, Win W,
                                               int vr, int vc, double c1, double c2,
                                               double* __restrict__ D, double* __restrict__ part,
                                               const int* halt) {
     if (halted(halt)) return;
+    __shared__ double sh[5][SPAN][ZC];
     __shared__ double red[PT / 32];
-    const int64_t idx = blockIdx.x * (int64_t)PT + threadIdx.x;
-    const int64_t tot = (int64_t)vr * vc * zc;      // outputs
-    const int64_t htot = (int64_t)m * vc * zc;      // H field stride
-    const int64_t rstride = (int64_t)vc * zc;       // one row of H
+    const int zl = threadIdx.x & (ZC - 1), o = threadIdx.x / ZC;
+    const int i0 = blockIdx.x * OB, j = blockIdx.y;
+    const int kr = ktaps<KR_>(W.kr);
+    const int nrow = min(OB + kr - 1, m - i0);
+    const int64_t htot = (int64_t)m * vc * ZC;
+    for (int e = threadIdx.x; e < SPAN * ZC; e += PT) {
+        const int r = e / ZC, z = e & (ZC - 1);
+        const int64_t hi = ((int64_t)(i0 + r) * vc + j) * ZC + z;
+#pragma unroll
+        for (int f = 0; f < 5; ++f) sh[f][r][z] = (r < nrow && z < zc) ? H[f * htot + hi] : 0.0;
+    }
+    __syncthreads();
+    const int i = i0 + o;
     double s = 0.0;
-    if (idx < tot) {
-        const int kr = ktaps<KR_>(W.kr);
-        const double* h0 = H + idx;   // row i of H has the same (j, zl) offset
+    if (zl < zc && i < vr) {
         double a[2][5] = {{0, 0, 0, 0, 0}, {0, 0, 0, 0, 0}};
 #pragma unroll
         for (int t = 0; t < (KR_ > 0 ? KR_ : KMAX); ++t) {
@@ -150,7 +192,7 @@ __global__ void __launch_bounds__(PT) k_ssim_v(const double* __restrict__ H, int
             const double g = W.gr[t];
             double* at = a[t & 1];
 #pragma unroll
-            for (int f = 0; f < 5; ++f) at[f] = fma(g, h0[f * htot + t * rstride], at[f]);
+            for (int f = 0; f < 5; ++f) at[f] = fma(g, sh[f][o + t][zl], at[f]);
         }
         const double mx = a[0][0] + a[1][0], my = a[0][1] + a[1][1], x2w = a[0][2] + a[1][2],
                      y2w = a[0][3] + a[1][3], xyw = a[0][4] + a[1][4];
@@ -159,46 +201,59 @@ __global__ void __launch_bounds__(PT) k_ssim_v(const double* __restrict__ H, int
         const double b1 = mx * mx + my * my + c1, b2 = sx2 + sy2 + c2;
         const double inv = 1.0 / (b1 * b2);   // 1/b1 = b2*inv, 1/b2 = b1*inv
         s = (a1 * a2) * inv;
+        const int64_t tot = (int64_t)vr * vc * ZC;
+        const int64_t idx = ((int64_t)i * vc + j) * ZC + zl;
         D[idx] = (2.0 * my * (a2 - a1)) * inv - 2.0 * mx * s * ((b2 - b1) * inv);
         D[tot + idx] = -s * (b1 * inv);
         D[2 * tot + idx] = 2.0 * a1 * inv;
     }
     const double r = block_sum<PT>(s, red);
-    if (threadIdx.x == 0) part[blockIdx.x] = r;
+    if (threadIdx.x == 0) part[blockIdx.y * gridDim.x + blockIdx.x] = r;
 }
 
+// G1: block (row i, columns s0..s0+3); stage D columns s0-10..s0+3 of row i
+// (zero outside [0, vc)).  T[i][s] = sum_b gc[b] D[i][s-b].
 template <int KC_>
 __global__ void __launch_bounds__(PT) k_ssim_gh(const double* __restrict__ D, int n, int zc, Win W,
                                                int vr, int vc, double* __restrict__ T,
                                                const int* halt) {
     if (halted(halt)) return;
-    const int64_t idx = blockIdx.x * (int64_t)PT + threadIdx.x;
-    const int64_t tot = (int64_t)vr * n * zc;
-    if (idx >= tot) return;
-    const int zl = (int)(idx % zc);
-    const int64_t is = idx / zc;
-    const int s = (int)(is % n), i = (int)(is / n);
+    __shared__ double sd[3][SPAN][ZC];
+    const int zl = threadIdx.x & (ZC - 1), o = threadIdx.x / ZC;
+    const int s0 = blockIdx.x * OB, i = blockIdx.y;
     const int kc = ktaps<KC_>(W.kc);
-    const int64_t dtot = (int64_t)vr * vc * zc;
-    const int blo = max(0, s - vc + 1), bhi = min(kc - 1, s);
-    const double* d0 = D + ((int64_t)i * vc + s) * zc + zl;   // column jj = s - b
+    const int base = s0 - (kc - 1);   // staged column q holds D column base + q
+    const int64_t dtot = (int64_t)vr * vc * ZC;
+    for (int e = threadIdx.x; e < SPAN * ZC; e += PT) {
+        const int q = e / ZC, z = e & (ZC - 1);
+        const int jj = base + q;
+        const bool ok = q < OB + kc - 1 && jj >= 0 && jj < vc && z < zc;
+        const int64_t di = ((int64_t)i * vc + jj) * ZC + z;
+#pragma unroll
+        for (int f = 0; f < 3; ++f) sd[f][q][z] = ok ? D[f * dtot + di] : 0.0;
+    }
+    __syncthreads();
+    const int s = s0 + o;
+    if (zl >= zc || s >= n) return;
     double t[2][3] = {{0, 0, 0}, {0, 0, 0}};
 #pragma unroll
     for (int b = 0; b < (KC_ > 0 ? KC_ : KMAX); ++b) {
         if (KC_ == 0 && b >= kc) break;
-        if (b < blo || b > bhi) continue;
         const double g = W.gc[b];
-        const double* q = d0 - (int64_t)b * zc;
+        const int q = o + (kc - 1) - b;   // column s - b
         double* tb = t[b & 1];
-        tb[0] = fma(g, q[0], tb[0]);
-        tb[1] = fma(g, q[dtot], tb[1]);
-        tb[2] = fma(g, q[2 * dtot], tb[2]);
+#pragma unroll
+        for (int f = 0; f < 3; ++f) tb[f] = fma(g, sd[f][q][zl], tb[f]);
     }
+    const int64_t tot = (int64_t)vr * n * ZC;
+    const int64_t idx = ((int64_t)i * n + s) * ZC + zl;
     T[idx] = t[0][0] + t[1][0];
     T[tot + idx] = t[0][1] + t[1][1];
     T[2 * tot + idx] = t[0][2] + t[1][2];
 }
 
+// G2: block (rows r0..r0+3, column s); stage T rows r0-10..r0+3 of column s
+// (zero outside [0, vr)).  A_f[r] = sum_a gr[a] T_f[r-a].
 template <int KR_>
 __global__ void __launch_bounds__(PT) k_loss_gv(const float* __restrict__ X, const float* __restrict__ Y,
                                                const double* __restrict__ T, int m, int n, int p,
@@ -207,37 +262,43 @@ __global__ void __launch_bounds__(PT) k_loss_gv(const float* __restrict__ X, con
                                                float* __restrict__ G, double* __restrict__ part,
                                                const int* halt) {
     if (halted(halt)) return;
+    __shared__ double st[3][SPAN][ZC];
     __shared__ double red[PT / 32];
-    const int64_t idx = blockIdx.x * (int64_t)PT + threadIdx.x;
-    const int64_t tot = (int64_t)m * n * zc;
+    const int zl = threadIdx.x & (ZC - 1), o = threadIdx.x / ZC;
+    const int r0 = blockIdx.x * OB, s = blockIdx.y;
+    const int kr = ktaps<KR_>(W.kr);
+    if (ssw > 0.0) {
+        const int base = r0 - (kr - 1);
+        const int64_t ttot = (int64_t)vr * n * ZC;
+        for (int e = threadIdx.x; e < SPAN * ZC; e += PT) {
+            const int q = e / ZC, z = e & (ZC - 1);
+            const int ii = base + q;
+            const bool ok = q < OB + kr - 1 && ii >= 0 && ii < vr && z < zc;
+            const int64_t ti = ((int64_t)ii * n + s) * ZC + z;
+#pragma unroll
+            for (int f = 0; f < 3; ++f) st[f][q][z] = ok ? T[f * ttot + ti] : 0.0;
+        }
+        __syncthreads();
+    }
+    const int r = r0 + o;
     double l1 = 0.0;
-    if (idx < tot) {
-        const int zl = (int)(idx % zc);
-        const int64_t rs = idx / zc;
-        const int s = (int)(rs % n), r = (int)(rs / n);
-        const int64_t gi = rs * p + z0 + zl;
+    if (zl < zc && r < m) {
+        const int64_t gi = ((int64_t)r * n + s) * p + z0 + zl;
         const double xv = (double)__ldg(X + gi), yv = (double)__ldg(Y + gi);
         const double diff = xv - yv;
         l1 = fabs(diff);
         double g = 0.0;
         if (l1w > 0.0) g += l1w * ((double)((diff > 0) - (diff < 0)) / l1_count);
         if (ssw > 0.0) {
-            const int kr = ktaps<KR_>(W.kr);
-            const int64_t ttot = (int64_t)vr * n * zc;
-            const int64_t rstride = (int64_t)n * zc;
-            const int alo = max(0, r - vr + 1), ahi = min(kr - 1, r);
-            const double* t0 = T + ((int64_t)r * n + s) * zc + zl;   // row i = r - a
             double A[2][3] = {{0, 0, 0}, {0, 0, 0}};
 #pragma unroll
             for (int a = 0; a < (KR_ > 0 ? KR_ : KMAX); ++a) {
                 if (KR_ == 0 && a >= kr) break;
-                if (a < alo || a > ahi) continue;
                 const double gg = W.gr[a];
-                const double* q = t0 - (int64_t)a * rstride;
+                const int q = o + (kr - 1) - a;   // row r - a
                 double* Aa = A[a & 1];
-                Aa[0] = fma(gg, q[0], Aa[0]);
-                Aa[1] = fma(gg, q[ttot], Aa[1]);
-                Aa[2] = fma(gg, q[2 * ttot], Aa[2]);
+#pragma unroll
+                for (int f = 0; f < 3; ++f) Aa[f] = fma(gg, st[f][q][zl], Aa[f]);
             }
             double gs = A[0][0] + A[1][0];
             gs += 2.0 * xv * (A[0][1] + A[1][1]);
@@ -248,7 +309,223 @@ __global__ void __launch_bounds__(PT) k_loss_gv(const float* __restrict__ X, con
         G[gi] = (float)g;
     }
     const double rr = block_sum<PT>(l1, red);
-    if (threadIdx.x == 0) part[blockIdx.x] = rr;
+    if (threadIdx.x == 0) part[blockIdx.y * gridDim.x + blockIdx.x] = rr;
+}
+
+// ---------------------------------------------------------------------------
+// 11 x 11 window fast path (the default: every image with >= 11 views and
+// detectors, p % 4 == 0).  A block owns 32 slices x 8 output columns and walks
+// the view axis.  Input rows (18 columns x 32 slices) are gathered with
+// cp.async into a 3-deep shared-memory ring two rows ahead of the compute, and
+// the last 11 rows of horizontal window sums live in REGISTERS: the row loop
+// is unrolled by 11 so every ring slot is a compile-time index.  f64
+// throughout like loss.py:112-141.
+// ---------------------------------------------------------------------------
+constexpr int R_COLS = 8;                 // output columns per block
+constexpr int R_SPAN = R_COLS + 10;       // staged input columns
+constexpr int R_NT = 32 * R_COLS;
+constexpr int R_BUF = 3;                  // staged rows in flight
+
+__device__ __forceinline__ void cp16_zfill(void* smem, const void* gmem, bool valid) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    const int n = valid ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+}
+__device__ __forceinline__ void cp_commit_group() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait_group() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__global__ void __launch_bounds__(R_NT, 1) k_ssim_stats11(const float* __restrict__ X,
+                                                          const float* __restrict__ Y, int m, int n,
+                                                          int p, Win W, double c1, double c2,
+                                                          int vr, int vc, double* __restrict__ D,
+                                                          double* __restrict__ part,
+                                                          const int* halt) {
+    if (halted(halt)) return;
+    __shared__ __align__(16) float sx[R_BUF][R_SPAN][32];
+    __shared__ __align__(16) float sy[R_BUF][R_SPAN][32];
+    __shared__ double red[R_NT / 32];
+    const int lane = threadIdx.x & 31, cl = threadIdx.x >> 5;
+    const int zb = blockIdx.x * 32, j0 = blockIdx.y * R_COLS;
+    const int z = zb + lane, j = j0 + cl;
+    const bool act = z < p && j < vc;
+    const int64_t plane = (int64_t)vr * vc * p;
+    // row v -> buffer v % 3: 18 columns x 8 chunks of 16 B per array
+    auto issue = [&](int v) {
+        if (v < m) {
+            const int buf = v % R_BUF;
+            for (int e = threadIdx.x; e < R_SPAN * 8 * 2; e += R_NT) {
+                const int arr = e / (R_SPAN * 8), rem = e % (R_SPAN * 8);
+                const int col = rem >> 3, q = rem & 7;
+                const bool ok = j0 + col < n && zb + 4 * q < p;
+                const int64_t gi = ok ? ((int64_t)v * n + j0 + col) * p + zb + 4 * q : 0;
+                float* dst = arr ? &sy[buf][col][4 * q] : &sx[buf][col][4 * q];
+                cp16_zfill(dst, (arr ? Y : X) + gi, ok);
+            }
+        }
+        cp_commit_group();
+    };
+    issue(0);
+    issue(1);
+    double ring[11][5];
+    double ssum = 0.0;
+    for (int v0 = 0; v0 < m; v0 += 11) {
+#pragma unroll
+        for (int ph = 0; ph < 11; ++ph) {
+            const int v = v0 + ph;
+            if (v >= m) break;
+            cp_wait_group<1>();   // row v landed (row v+1 may still be in flight)
+            __syncthreads();
+            issue(v + 2);          // into the buffer row v-1 used (all threads are past it)
+            const int buf = v % R_BUF;
+            double h[2][5] = {{0, 0, 0, 0, 0}, {0, 0, 0, 0, 0}};
+#pragma unroll
+            for (int b = 0; b < 11; ++b) {
+                const double xv = (double)sx[buf][cl + b][lane];
+                const double yv = (double)sy[buf][cl + b][lane];
+                const double g = W.gc[b];
+                double* hb = h[b & 1];
+                hb[0] = fma(g, xv, hb[0]);
+                hb[1] = fma(g, yv, hb[1]);
+                hb[2] = fma(g, xv * xv, hb[2]);
+                hb[3] = fma(g, yv * yv, hb[3]);
+                hb[4] = fma(g, xv * yv, hb[4]);
+            }
+#pragma unroll
+            for (int f = 0; f < 5; ++f) ring[ph][f] = h[0][f] + h[1][f];
+            if (v >= 10 && act) {
+                double a[2][5] = {{0, 0, 0, 0, 0}, {0, 0, 0, 0, 0}};
+#pragma unroll
+                for (int t = 0; t < 11; ++t) {   // row v-10+t lives in slot (ph+1+t) % 11
+                    const double g = W.gr[t];
+                    double* at = a[t & 1];
+#pragma unroll
+                    for (int f = 0; f < 5; ++f) at[f] = fma(g, ring[(ph + 1 + t) % 11][f], at[f]);
+                }
+                const double mx = a[0][0] + a[1][0], my = a[0][1] + a[1][1],
+                             x2w = a[0][2] + a[1][2], y2w = a[0][3] + a[1][3],
+                             xyw = a[0][4] + a[1][4];
+                const double sx2 = x2w - mx * mx, sy2 = y2w - my * my, sxy = xyw - mx * my;
+                const double a1 = 2.0 * mx * my + c1, a2 = 2.0 * sxy + c2;
+                const double b1 = mx * mx + my * my + c1, b2 = sx2 + sy2 + c2;
+                const double inv = 1.0 / (b1 * b2);   // 1/b1 = b2*inv, 1/b2 = b1*inv
+                const double s = (a1 * a2) * inv;
+                ssum += s;
+                const int64_t o = ((int64_t)(v - 10) * vc + j) * p + z;
+                D[o] = (2.0 * my * (a2 - a1)) * inv - 2.0 * mx * s * ((b2 - b1) * inv);
+                D[plane + o] = -s * (b1 * inv);
+                D[2 * plane + o] = 2.0 * a1 * inv;
+            }
+        }
+    }
+    cp_wait_group<0>();
+    const double r = block_sum<R_NT>(ssum, red);
+    if (threadIdx.x == 0) part[blockIdx.y * gridDim.x + blockIdx.x] = r;
+}
+
+__global__ void __launch_bounds__(R_NT, 1) k_loss_grad11(const float* __restrict__ X,
+                                                         const float* __restrict__ Y, int m, int n,
+                                                         int p, Win W, int vr, int vc,
+                                                         const double* __restrict__ D, double l1w,
+                                                         double l1_count, double ssw,
+                                                         double ssim_slices, float* __restrict__ G,
+                                                         double* __restrict__ part,
+                                                         const int* halt) {
+    if (halted(halt)) return;
+    // per staged row: D columns s0-10 .. s0+7 (3 fields) and x, y columns s0 .. s0+7
+    __shared__ __align__(16) double sd[R_BUF][3][R_SPAN][32];
+    __shared__ __align__(16) float sxy[R_BUF][2][R_COLS][32];
+    __shared__ double red[R_NT / 32];
+    const int lane = threadIdx.x & 31, cl = threadIdx.x >> 5;
+    const int zb = blockIdx.x * 32, s0 = blockIdx.y * R_COLS;
+    const int z = zb + lane, s = s0 + cl;
+    const bool act = z < p && s < n;
+    const int64_t plane = (int64_t)vr * vc * p;
+    const double inv_val = 1.0 / ((double)vr * (double)vc);
+    const bool ss = ssw > 0.0;
+    auto issue = [&](int r) {
+        if (r < m) {
+            const int buf = r % R_BUF;
+            if (ss && r < vr) {   // D: 3 fields x 18 columns x 16 chunks of 16 B (2 doubles)
+                for (int e = threadIdx.x; e < 3 * R_SPAN * 16; e += R_NT) {
+                    const int f = e / (R_SPAN * 16), rem = e % (R_SPAN * 16);
+                    const int col = rem >> 4, q = rem & 15;
+                    const int jj = s0 - 10 + col;
+                    const bool ok = jj >= 0 && jj < vc && zb + 2 * q < p;
+                    const int64_t gi = ok ? f * plane + ((int64_t)r * vc + jj) * p + zb + 2 * q : 0;
+                    cp16_zfill(&sd[buf][f][col][2 * q], D + gi, ok);
+                }
+            }
+            for (int e = threadIdx.x; e < 2 * R_COLS * 8; e += R_NT) {   // x, y: 8 cols x 8 chunks
+                const int arr = e / (R_COLS * 8), rem = e % (R_COLS * 8);
+                const int col = rem >> 3, q = rem & 7;
+                const bool ok = s0 + col < n && zb + 4 * q < p;
+                const int64_t gi = ok ? ((int64_t)r * n + s0 + col) * p + zb + 4 * q : 0;
+                cp16_zfill(&sxy[buf][arr][col][4 * q], (arr ? Y : X) + gi, ok);
+            }
+        }
+        cp_commit_group();
+    };
+    issue(0);
+    issue(1);
+    double ring[11][3];
+#pragma unroll
+    for (int q = 0; q < 11; ++q) ring[q][0] = ring[q][1] = ring[q][2] = 0.0;
+    double l1sum = 0.0;
+    for (int r0 = 0; r0 < m; r0 += 11) {
+#pragma unroll
+        for (int ph = 0; ph < 11; ++ph) {
+            const int r = r0 + ph;
+            if (r >= m) break;
+            cp_wait_group<1>();
+            __syncthreads();
+            issue(r + 2);
+            const int buf = r % R_BUF;
+            if (ss && r < vr) {
+                double t[2][3] = {{0, 0, 0}, {0, 0, 0}};
+#pragma unroll
+                for (int b = 0; b < 11; ++b) {    // column s - b = staged column cl + 10 - b
+                    const double g = W.gc[b];
+                    double* tb = t[b & 1];
+#pragma unroll
+                    for (int f = 0; f < 3; ++f) tb[f] = fma(g, sd[buf][f][cl + 10 - b][lane], tb[f]);
+                }
+#pragma unroll
+                for (int f = 0; f < 3; ++f) ring[ph][f] = t[0][f] + t[1][f];
+            } else {
+#pragma unroll
+                for (int f = 0; f < 3; ++f) ring[ph][f] = 0.0;   // rows >= vr contribute 0
+            }
+            if (act) {
+                const double xv = (double)sxy[buf][0][cl][lane];
+                const double yv = (double)sxy[buf][1][cl][lane];
+                const double diff = xv - yv;
+                l1sum += fabs(diff);
+                double g = 0.0;
+                if (l1w > 0.0) g += l1w * ((double)((diff > 0) - (diff < 0)) / l1_count);
+                if (ss) {
+                    double A[2][3] = {{0, 0, 0}, {0, 0, 0}};
+#pragma unroll
+                    for (int a = 0; a < 11; ++a) {   // row r - a lives in slot (ph - a) mod 11
+                        if (r - a < 0) break;
+                        const double gg = W.gr[a];
+                        double* Aa = A[a & 1];
+#pragma unroll
+                        for (int f = 0; f < 3; ++f) Aa[f] = fma(gg, ring[(ph - a + 11) % 11][f], Aa[f]);
+                    }
+                    double gs = A[0][0] + A[1][0];
+                    gs += 2.0 * xv * (A[0][1] + A[1][1]);
+                    gs += yv * (A[0][2] + A[1][2]);
+                    gs *= inv_val;
+                    g += ssw * (-gs / ssim_slices);
+                }
+                G[((int64_t)r * n + s) * p + z] = (float)g;
+            }
+        }
+    }
+    cp_wait_group<0>();
+    const double rr = block_sum<R_NT>(l1sum, red);
+    if (threadIdx.x == 0) part[blockIdx.y * gridDim.x + blockIdx.x] = rr;
 }
 
 __global__ void __launch_bounds__(1024) k_sino_max(const float* __restrict__ x, int64_t count,
@@ -370,17 +647,27 @@ int splatct_loss_fused(const float* pred, const float* ref, int m, int n, int p,
     double* T = reinterpret_cast<double*>(base + L.o_T);
     double* ps = reinterpret_cast<double*>(base + L.o_ps);
     double* pl = reinterpret_cast<double*>(base + L.o_pl);
-    const bool k11 = W.kr == 11 && W.kc == 11;
-    if (L.nchunks > 1 && p % L.zc != 0) {   // short last chunk leaves unused partial slots
-        SPLATCT_CK(cudaMemsetAsync(ps, 0, sizeof(double) * L.nb_v * L.nchunks, s));
-        SPLATCT_CK(cudaMemsetAsync(pl, 0, sizeof(double) * L.nb_g * L.nchunks, s));
+    const bool k11 = L.k11;
+    if (k11) {
+        double* D11 = reinterpret_cast<double*>(base + L.o_D11);
+        const dim3 gs((p + 31) / 32, (L.vc + 7) / 8), gg((p + 31) / 32, (n + 7) / 8);
+        if (lambda2 > 0.0) {
+            k_ssim_stats11<<<gs, R_NT, 0, s>>>(pred, ref, m, n, p, W, c1, c2, L.vr, L.vc, D11, ps,
+                                               halt);
+            SPLATCT_LAUNCH_CK();
+            if (int e = reduce_sum_f64(ps, L.nb_s11, sums + 1, s)) return e;
+        } else {
+            SPLATCT_CK(cudaMemsetAsync(sums + 1, 0, sizeof(double), s));
+        }
+        k_loss_grad11<<<gg, R_NT, 0, s>>>(pred, ref, m, n, p, W, L.vr, L.vc, D11, lambda1,
+                                          l1_count, lambda2, ssim_slices, grad_pred, pl, halt);
+        SPLATCT_LAUNCH_CK();
+        return reduce_sum_f64(pl, L.nb_g11, sums, s);
     }
     for (int ci = 0; ci < L.nchunks; ++ci) {
-        const int z0 = ci * L.zc, zc = min(L.zc, p - z0);
+        const int z0 = ci * ZC, zc = min(ZC, p - z0);
         if (lambda2 > 0.0) {
-            const unsigned g1 = (unsigned)(((int64_t)m * L.vc * zc + 255) / 256);
-            const unsigned g2 = (unsigned)(((int64_t)L.vr * L.vc * zc + 255) / 256);
-            const unsigned g3 = (unsigned)(((int64_t)L.vr * n * zc + 255) / 256);
+            const dim3 g1((L.vc + 3) / 4, m), g2((L.vr + 3) / 4, L.vc), g3((n + 3) / 4, L.vr);
             if (k11) {
                 k_ssim_h<11><<<g1, PT, 0, s>>>(pred, ref, m, n, p, z0, zc, W, L.vc, H, halt);
                 SPLATCT_LAUNCH_CK();
@@ -398,7 +685,7 @@ int splatct_loss_fused(const float* pred, const float* ref, int m, int n, int p,
             }
             SPLATCT_LAUNCH_CK();
         }
-        const unsigned g4 = (unsigned)(((int64_t)m * n * zc + 255) / 256);
+        const dim3 g4((m + 3) / 4, n);
         if (k11)
             k_loss_gv<11><<<g4, PT, 0, s>>>(pred, ref, T, m, n, p, z0, zc, W, L.vr, L.vc, lambda1,
                                             l1_count, lambda2, ssim_slices, grad_pred,

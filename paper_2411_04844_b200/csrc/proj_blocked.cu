@@ -46,7 +46,9 @@ struct GroupMap {
 // writes at gptr[g].
 __global__ void __launch_bounds__(BLK_NT) k_block_build(GroupMap gm, const int64_t* __restrict__ ptr,
                                                         const int32_t* __restrict__ idx,
-                                                        const float* __restrict__ val, int mode,
+                                                        const float* __restrict__ val,
+                                                        const float2* __restrict__ order_dir,
+                                                        int mode,
                                                         int64_t* __restrict__ gcount,
                                                         const int64_t* __restrict__ gptr,
                                                         int32_t* __restrict__ gidx,
@@ -77,13 +79,29 @@ __global__ void __launch_bounds__(BLK_NT) k_block_build(GroupMap gm, const int64
     const int L = total;
     int P = 1;
     while (P < L) P <<= 1;
+    // march order: sort by the pixel's position along the group's ray
+    // direction (13-bit quantised, then pixel id), so the warps of a CTA sweep
+    // the slice together and share L1 lines; pixel order otherwise.
+    const bool march = order_dir != nullptr && (int64_t)gm.w * gm.h <= (1 << 19);
+    float2 dir = make_float2(0.f, 0.f);
+    if (march) dir = order_dir[g];
+    const float cx = 0.5f * (gm.w - 1), cy = 0.5f * (gm.h - 1);
+    const float R = 0.5f * sqrtf((float)gm.w * gm.w + (float)gm.h * gm.h) + 1.f;
     for (int i = threadIdx.x; i < P; i += BLK_NT) {
         if (i < L) {
             int k = 0;
             int64_t off = i;
             while (off >= len[k]) { off -= len[k]; ++k; }
             const int64_t j = beg[k] + off;
-            key[i] = (uint32_t)idx[j];
+            const uint32_t pix = (uint32_t)idx[j];
+            if (march) {
+                const float px = (float)(pix % gm.w) - cx, py = (float)(pix / gm.w) - cy;
+                int tq = (int)((px * dir.x + py * dir.y + R) * 4.f);
+                tq = min(max(tq, 0), 8191);
+                key[i] = ((uint32_t)tq << 19) | pix;
+            } else {
+                key[i] = pix;
+            }
             pay[i] = ((uint32_t)k << 29) | (uint32_t)i;
             wv[i] = mode == 1 ? val[j] : 0.f;
         } else {
@@ -126,7 +144,7 @@ __global__ void __launch_bounds__(BLK_NT) k_block_build(GroupMap gm, const int64
                     w4[pl >> 29] = wv[pl & 0x1fffffffu];
                 }
                 const int64_t o = gptr[g] + pos;
-                gidx[o] = (int32_t)key[i];
+                gidx[o] = (int32_t)(march ? (key[i] & 0x7ffffu) : key[i]);
                 gval[o] = make_float4(w4[0], w4[1], w4[2], w4[3]);
             }
             base += __popc(m);
@@ -396,8 +414,8 @@ int splatct_proj_block_scratch_bytes(int nrows, int kind, int w, int h, size_t* 
 }
 
 int splatct_proj_block_count(const int64_t* ptr, const int32_t* idx, int nrows, int kind, int w,
-                             int h, int64_t* gptr, void* scratch, size_t scratch_bytes,
-                             int64_t* nb, void* stream) {
+                             int h, const float* order_dir, int64_t* gptr, void* scratch,
+                             size_t scratch_bytes, int64_t* nb, void* stream) {
     SPLATCT_REQUIRE(kind == 0 || kind == 1, "kind must be 0 (row groups) or 1 (pixel quads)");
     GroupMap gm{kind, nrows, w, h};
     const int64_t ng = gm.ngroups();
@@ -416,8 +434,9 @@ int splatct_proj_block_count(const int64_t* ptr, const int32_t* idx, int nrows, 
                                         (int)block_smem()));
         attr = true;
     }
-    k_block_build<<<(unsigned)ng, BLK_NT, block_smem(), s>>>(gm, ptr, idx, nullptr, 0, cnt, nullptr,
-                                                             nullptr, nullptr, overflow);
+    k_block_build<<<(unsigned)ng, BLK_NT, block_smem(), s>>>(
+        gm, ptr, idx, nullptr, reinterpret_cast<const float2*>(order_dir), 0, cnt, nullptr, nullptr,
+        nullptr, overflow);
     SPLATCT_LAUNCH_CK();
     if (int e = exclusive_scan_i64(cnt, gptr, ng + 1, scan_tmp, s)) return e;
     int ovf = 0;
@@ -429,8 +448,9 @@ int splatct_proj_block_count(const int64_t* ptr, const int32_t* idx, int nrows, 
 }
 
 int splatct_proj_block_fill(const int64_t* ptr, const int32_t* idx, const float* val, int nrows,
-                            int kind, int w, int h, const int64_t* gptr, int32_t* gidx,
-                            float* gval, void* scratch, size_t scratch_bytes, void* stream) {
+                            int kind, int w, int h, const float* order_dir, const int64_t* gptr,
+                            int32_t* gidx, float* gval, void* scratch, size_t scratch_bytes,
+                            void* stream) {
     GroupMap gm{kind, nrows, w, h};
     const int64_t ng = gm.ngroups();
     size_t need = 0;
@@ -442,7 +462,8 @@ int splatct_proj_block_fill(const int64_t* ptr, const int32_t* idx, const float*
                                            align_up(sizeof(int64_t) * (ng + 1)) +
                                            scan_temp_bytes(ng + 1));
     k_block_build<<<(unsigned)ng, BLK_NT, block_smem(), s>>>(
-        gm, ptr, idx, val, 1, nullptr, gptr, gidx, reinterpret_cast<float4*>(gval), overflow);
+        gm, ptr, idx, val, reinterpret_cast<const float2*>(order_dir), 1, nullptr, gptr, gidx,
+        reinterpret_cast<float4*>(gval), overflow);
     SPLATCT_LAUNCH_CK();
     SPLATCT_CK(cudaStreamSynchronize(s));
     return SPLATCT_OK;

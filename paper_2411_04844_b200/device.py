@@ -188,10 +188,28 @@ class ProjectorOperator:
         del scratch
         self.blocked = blocked
         if blocked:
-            self.fb = self._block(self.a_ptr, self.a_col, self.a_val, self.n_rays, 0)
+            self.fb = self._block(self.a_ptr, self.a_col, self.a_val, self.n_rays, 0,
+                                  self._group_dirs())
             self.ab = self._block(self.at_ptr, self.at_ray, self.at_val, self.w * self.h, 1)
 
-    def _block(self, ptr_, idx, val, nrows, kind):
+    def _group_dirs(self) -> torch.Tensor:
+        """Unit direction of the middle ray of each 4-ray group (march-order key)."""
+        ng = (self.n_rays + 3) // 4
+        r = np.minimum(np.arange(ng) * 4 + 2, self.n_rays - 1)
+        v, d = r // self.n_det, r % self.n_det
+        ang = np.asarray(self.geom.view_angles, np.float64)[v]
+        c, s = np.cos(ang), np.sin(ang)
+        if self.is_fan:
+            u = (d - 0.5 * (self.n_det - 1)) * self.spacing
+            dx = (self.rd + self.rs) * c - u * s
+            dy = (self.rd + self.rs) * s + u * c
+            nrm = np.hypot(dx, dy)
+            dx, dy = dx / nrm, dy / nrm
+        else:
+            dx, dy = c, s
+        return torch.from_numpy(np.stack([dx, dy], 1).astype(np.float32)).to(self.device)
+
+    def _block(self, ptr_, idx, val, nrows, kind, order_dir=None):
         """4-row blocked copy (gptr, gidx, gval[nb, 4]) of a CSR operator."""
         sb = size_query("splatct_proj_block_scratch_bytes", nrows, kind, self.w, self.h)
         scratch = torch.empty(sb, dtype=torch.uint8, device=self.device)
@@ -199,12 +217,13 @@ class ProjectorOperator:
         gptr = torch.empty(ng + 1, dtype=torch.int64, device=self.device)
         nb = ctypes.c_int64(0)
         call("splatct_proj_block_count", ptr(ptr_), ptr(idx), nrows, kind, self.w, self.h,
-             ptr(gptr), ptr(scratch), sb, ctypes.byref(nb), stream_handle())
+             ptr(order_dir), ptr(gptr), ptr(scratch), sb, ctypes.byref(nb), stream_handle())
         k = max(int(nb.value), 1)
         gidx = torch.empty(k, dtype=torch.int32, device=self.device)
         gval = torch.empty((k, 4), dtype=torch.float32, device=self.device)
         call("splatct_proj_block_fill", ptr(ptr_), ptr(idx), ptr(val), nrows, kind, self.w,
-             self.h, ptr(gptr), ptr(gidx), ptr(gval), ptr(scratch), sb, stream_handle())
+             self.h, ptr(order_dir), ptr(gptr), ptr(gidx), ptr(gval), ptr(scratch), sb,
+             stream_handle())
         return gptr, gidx, gval, int(nb.value)
 
     def _gargs(self):
