@@ -64,10 +64,16 @@ def params_to_cloud(params: torch.Tensor) -> GaussianCloud:
     return GaussianCloud(np.ascontiguousarray(p[0:3].T), p[3].copy(), p[4].copy())
 
 
+def _host_f32(arr) -> torch.Tensor:
+    a = np.ascontiguousarray(arr, dtype=np.float32)
+    if not a.flags.writeable:   # value objects are frozen; torch wants writable memory
+        a = a.copy()
+    return torch.from_numpy(a)
+
+
 def zyx_to_yxz(arr, device) -> torch.Tensor:
     """(c, h, w) host array -> (h, w, c) device tensor."""
-    t = torch.as_tensor(np.ascontiguousarray(arr, dtype=np.float32))
-    return t.to(device).permute(1, 2, 0).contiguous()
+    return _host_f32(arr).to(device).permute(1, 2, 0).contiguous()
 
 
 def yxz_to_zyx(t: torch.Tensor) -> np.ndarray:
@@ -75,7 +81,7 @@ def yxz_to_zyx(t: torch.Tensor) -> np.ndarray:
 
 
 def sino_to_device(views, device) -> torch.Tensor:
-    return torch.as_tensor(np.ascontiguousarray(views, dtype=np.float32)).to(device)
+    return _host_f32(views).to(device)
 
 
 # ---------------------------------------------------------------------------

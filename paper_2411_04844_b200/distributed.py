@@ -41,16 +41,27 @@ class SlabComm:
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        # gloo has no device-side point-to-point: stage halos through the host
+        # (used to emulate ranks on one GPU in tests; NCCL stays on device)
+        self.host_p2p = dist.get_backend(group) == "gloo"
         self._lo = None
         self._hi = None
+        self._out_dev = None
+
+    def _reduce(self, t: torch.Tensor, op) -> torch.Tensor:
+        if self.host_p2p and t.is_cuda:
+            h = t.cpu()
+            dist.all_reduce(h, op=op, group=self.group)
+            t.copy_(h)
+        else:
+            dist.all_reduce(t, op=op, group=self.group)
+        return t
 
     def allreduce_sum_(self, t: torch.Tensor) -> torch.Tensor:
-        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
-        return t
+        return self._reduce(t, dist.ReduceOp.SUM)
 
     def allreduce_max_(self, t: torch.Tensor) -> torch.Tensor:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
-        return t
+        return self._reduce(t, dist.ReduceOp.MAX)
 
     def halo(self, vol: torch.Tensor):
         """Exchange boundary z-planes of a (h, w, c_local) slab.
@@ -59,11 +70,15 @@ class SlabComm:
         rank+1, each a contiguous (h*w,) tensor, or None at the volume edges.
         """
         h, w, _ = vol.shape
-        if self._lo is None or self._lo.numel() != h * w or self._lo.device != vol.device:
-            self._lo = torch.empty(h * w, dtype=vol.dtype, device=vol.device)
-            self._hi = torch.empty(h * w, dtype=vol.dtype, device=vol.device)
+        buf_dev = torch.device("cpu") if self.host_p2p else vol.device
+        if self._lo is None or self._lo.numel() != h * w or self._out_dev != vol.device:
+            self._out_dev = vol.device
+            self._lo = torch.empty(h * w, dtype=vol.dtype, device=buf_dev)
+            self._hi = torch.empty(h * w, dtype=vol.dtype, device=buf_dev)
             self._send_lo = torch.empty_like(self._lo)
             self._send_hi = torch.empty_like(self._lo)
+            self._lo_dev = torch.empty(h * w, dtype=vol.dtype, device=vol.device)
+            self._hi_dev = torch.empty(h * w, dtype=vol.dtype, device=vol.device)
         self._send_lo.copy_(vol[:, :, 0].reshape(-1))
         self._send_hi.copy_(vol[:, :, -1].reshape(-1))
         ops = []
@@ -77,7 +92,11 @@ class SlabComm:
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
-        return (self._lo if r > 0 else None), (self._hi if r + 1 < n else None)
+        lo, hi = self._lo, self._hi
+        if self.host_p2p and vol.device.type == "cuda":
+            lo = self._lo_dev.copy_(self._lo)
+            hi = self._hi_dev.copy_(self._hi)
+        return (lo if r > 0 else None), (hi if r + 1 < n else None)
 
 
 def init_from_env(backend: str = "nccl"):
@@ -111,7 +130,9 @@ def run_reconstruction_sharded(measured, geom, settings, init_cloud, comm=None,
     from .core import VolumeGrid
     from .trainer import Trainer
 
-    comm = comm or SlabComm()
+    if comm is None:
+        from .trainer import NullComm
+        comm = SlabComm() if dist.is_available() and dist.is_initialized() else NullComm()
     dims = tuple(int(v) for v in settings.dims)
     s = slab_bounds(dims[2], comm.world, comm.rank)
     dev = D.require_cuda()
@@ -133,7 +154,12 @@ def run_reconstruction_sharded(measured, geom, settings, init_cloud, comm=None,
     pad[:, :, : s.c_local] = tr.vol
     parts = [torch.empty_like(pad) for _ in range(comm.world)] if comm.world > 1 else [pad]
     if comm.world > 1:
-        dist.all_gather(parts, pad, group=comm.group)
+        if comm.host_p2p:
+            hp = [torch.empty_like(pad, device="cpu") for _ in range(comm.world)]
+            dist.all_gather(hp, pad.cpu(), group=comm.group)
+            parts = [t.to(dev) for t in hp]
+        else:
+            dist.all_gather(parts, pad, group=comm.group)
     vol = None
     if comm.rank == 0:
         cols = [parts[r][:, :, : slab_bounds(dims[2], comm.world, r).c_local]
