@@ -202,7 +202,8 @@ int splatct_proj_march_forward(const double* cos_t, const double* sin_t, int m, 
 
 int splatct_loss_workspace_bytes(int m, int n, int p, size_t* bytes);
 
-/* out[0] = max(ref) over all bins (double) -- the SSIM dynamic range L. */
+/* out[0] = max(x) over all bins (double) -- the SSIM dynamic range L.
+ * out must hold 1 + SPLATCT_SQDIFF_BLOCKS doubles (the tail is scratch). */
 int splatct_sino_max(const float* x, int64_t count, double* out, void* stream);
 
 /* grad_pred = lambda1*sign(pred-ref)/l1_count - lambda2*dSSIM/dpred/ssim_slices.

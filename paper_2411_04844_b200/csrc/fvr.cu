@@ -38,7 +38,7 @@ constexpr int RADIX = 256;
 // so the tile kernels never touch f64.
 struct __align__(16) GRec {
     int fx, fy, fz;
-    float inv2;
+    float inv2;       // log2(e) / (2 sigma^2)
     float dx, dy, dz, I;
 };
 
@@ -47,12 +47,13 @@ struct FvrLayout {
     int w, h, c, hx, hy, hz;
     int ntx, nty, ntz;
     int64_t nt;
-    int S;            // max tiles per Gaussian (slots)
+    int S;            // slots per Gaussian (power of two >= max tiles per Gaussian)
+    int Sl;           // log2(S)
     int64_t np;       // n * S
     int passes;
     int64_t sort_blocks;
     size_t o_fp, o_gcount, o_k0, o_v0, o_k1, o_v1, o_tcount, o_tstart, o_hist, o_scan, o_part,
-        o_rec, o_cc, o_cstart, total;
+        o_rec, o_cc, o_cstart, o_ctile, total;
     int64_t bwd_grid;   // upper bound on backward (tile, chunk) work items
     int final_buf;    // which (k,v) buffer holds the sorted result
 };
@@ -71,7 +72,12 @@ static FvrLayout make_layout(int64_t n, int w, int h, int c, int hx, int hy, int
     L.nty = (h + TT - 1) / TT;
     L.ntz = (c + TT - 1) / TT;
     L.nt = (int64_t)L.ntx * L.nty * L.ntz;
-    L.S = axis_span(hx, w) * axis_span(hy, h) * axis_span(hz, c);
+    {   // slots per Gaussian, rounded up to a power of two (slot -> Gaussian is a shift)
+        const int s_raw = axis_span(hx, w) * axis_span(hy, h) * axis_span(hz, c);
+        L.Sl = 0;
+        while ((1 << L.Sl) < s_raw) ++L.Sl;
+        L.S = 1 << L.Sl;
+    }
     L.np = n * L.S;
     int bits = 0;
     while (((int64_t)1 << bits) <= L.nt) ++bits;   // keys in [0, nt] (nt = sentinel)
@@ -97,6 +103,7 @@ static FvrLayout make_layout(int64_t n, int w, int h, int c, int hx, int hy, int
     L.o_cc = take(sizeof(uint32_t) * (size_t)(L.nt + 1));
     L.o_cstart = take(sizeof(uint32_t) * (size_t)(L.nt + 1));
     L.bwd_grid = L.nt + L.np / 64 + 1;
+    L.o_ctile = take(sizeof(uint32_t) * (size_t)L.bwd_grid);
     L.total = off;
     L.final_buf = L.passes % 2;   // pass p reads buf p%2, writes (p+1)%2
     return L;
@@ -152,7 +159,7 @@ __global__ void k_footprint(const double* __restrict__ P, int64_t n, int w, int 
         const double fx = floor(mx), fy = floor(my), fz = floor(mz);
         r.fx = (int)fx; r.fy = (int)fy; r.fz = (int)fz;
         r.dx = (float)(mx - fx); r.dy = (float)(my - fy); r.dz = (float)(mz - fz);
-        r.inv2 = (float)(0.5 / (sg * sg));
+        r.inv2 = (float)(0.5 / (sg * sg) * 1.4426950408889634);   // exp(-a) = exp2(-a log2 e)
         r.I = (float)P[4 * n + i];
         rec[i] = r;
         for (int tz = lo[2] / TT; tz <= hi[2] / TT; ++tz)
@@ -255,7 +262,7 @@ __device__ __forceinline__ float tab_weight(int coord_local, int origin, int dim
     const int b = coord_local + origin - f;
     if (coord_local >= dim || b > half || b < -half) return 0.f;
     const float r = (float)b - d;
-    return expf(-inv2 * r * r);
+    return exp2f(-inv2 * r * r);   // inv2 carries log2(e)
 }
 
 __global__ void __launch_bounds__(256) k_fvr_fwd(const GRec* __restrict__ rec, int w, int h, int c,
@@ -280,7 +287,7 @@ __global__ void __launch_bounds__(256) k_fvr_fwd(const GRec* __restrict__ rec, i
         const int nb = (int)min((uint32_t)FWD_BATCH, end - b0);
         __syncthreads();
         if (tg < nb) {
-            const GRec r = rec[svals[b0 + tg] / (uint32_t)S];
+            const GRec r = rec[svals[b0 + tg] >> S];   // S = log2(slots per Gaussian)
 #pragma unroll
             for (int k = 0; k < 3 * TT / 8; ++k) {
                 const int e = tj + 8 * k, a = e / TT, l = e % TT;   // compile-time a per k
@@ -335,27 +342,31 @@ __global__ void k_tile_chunks(const uint32_t* __restrict__ tstart, int64_t nt,
     cc[t] = t < nt ? (tstart[t + 1] - tstart[t] + BWD_CHUNK - 1) / BWD_CHUNK : 0u;
 }
 
+// chunk k of tile t -> ctile[cstart[t] + k] = t (the backward's work list)
+__global__ void k_chunk_tiles(const uint32_t* __restrict__ cstart, int64_t nt,
+                              uint32_t* __restrict__ ctile, const int* halt) {
+    if (halted(halt)) return;
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= nt) return;
+    for (uint32_t k = cstart[t]; k < cstart[t + 1]; ++k) ctile[k] = (uint32_t)t;
+}
+
 __global__ void __launch_bounds__(256) k_fvr_bwd(const GRec* __restrict__ rec, int w, int h, int c,
                                                  int zoff, int hx, int hy, int hz, int ntx,
                                                  int nty, int64_t nt, int S,
                                                  const uint32_t* __restrict__ tstart,
                                                  const uint32_t* __restrict__ cstart,
+                                                 const uint32_t* __restrict__ ctile,
                                                  const uint32_t* __restrict__ svals,
                                                  const float* __restrict__ up,
                                                  float* __restrict__ part, const int* halt) {
     if (halted(halt)) return;
     __shared__ float sup[TT][TT][TT + 1];     // upstream tile [y][x][z], padded
-    __shared__ float4 xt[8][TT];              // per warp: {ex, ex*rx, ex*rx^2, -}
-    __shared__ float2 yt[8][TT];              // per warp: {ey, ry}
+    __shared__ float4 zt[8][TT];              // per warp: {ez, ez*rz, ez*rz^2, -}
+    __shared__ float2 xt[8][TT], yt[8][TT];   // per warp: {e, r}
     const uint32_t b = blockIdx.x;
     if (b >= cstart[nt]) return;
-    // tile of this chunk: last t with cstart[t] <= b
-    int64_t lo = 0, hi = nt - 1;
-    while (lo < hi) {
-        const int64_t mid = (lo + hi + 1) >> 1;
-        if (cstart[mid] <= b) lo = mid; else hi = mid - 1;
-    }
-    const int64_t t = lo;
+    const int64_t t = ctile[b];
     const uint32_t beg = tstart[t] + (b - cstart[t]) * BWD_CHUNK;
     const uint32_t end = min(beg + BWD_CHUNK, tstart[t + 1]);
     const int txi = (int)(t % ntx), tyi = (int)((t / ntx) % nty), tzi = (int)(t / ((int64_t)ntx * nty));
@@ -369,67 +380,69 @@ __global__ void __launch_bounds__(256) k_fvr_bwd(const GRec* __restrict__ rec, i
     }
     __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int zl = lane & (TT - 1), yh = lane >> 4;
     for (uint32_t j = beg + wid; j < end; j += blockDim.x / 32) {
         const uint32_t orig = svals[j];
-        const GRec r = rec[orig / (uint32_t)S];
-        {   // per-warp separable tables: lanes 0-15 x entries, 16-31 y entries
+        const GRec r = rec[orig >> S];   // S = log2(slots per Gaussian)
+        {   // separable tables (zero outside box, tile and local volume)
             const int l = lane & (TT - 1);
             if (lane < TT) {
-                const int bb = x0 + l - r.fx;
-                const float rx = (float)bb - r.dx;
-                const bool ok = x0 + l < w && bb <= hx && bb >= -hx;
-                const float ex = ok ? expf(-r.inv2 * rx * rx) : 0.f;
-                xt[wid][l] = make_float4(ex, ex * rx, ex * rx * rx, 0.f);
+                const int bx = x0 + l - r.fx;
+                const float rx = (float)bx - r.dx;
+                const bool okx = x0 + l < w && bx <= hx && bx >= -hx;
+                xt[wid][l] = make_float2(okx ? exp2f(-r.inv2 * rx * rx) : 0.f, rx);
+                const int bz = z0 + l + zoff - r.fz;
+                const float rz = (float)bz - r.dz;
+                const bool okz = z0 + l < c && bz <= hz && bz >= -hz;
+                const float ez = okz ? exp2f(-r.inv2 * rz * rz) : 0.f;
+                zt[wid][l] = make_float4(ez, ez * rz, ez * rz * rz, 0.f);
             } else {
-                const int bb = y0 + l - r.fy;
-                const float ry = (float)bb - r.dy;
-                const bool ok = y0 + l < h && bb <= hy && bb >= -hy;
-                yt[wid][l] = make_float2(ok ? expf(-r.inv2 * ry * ry) : 0.f, ry);
+                const int by = y0 + l - r.fy;
+                const float ry = (float)by - r.dy;
+                const bool oky = y0 + l < h && by <= hy && by >= -hy;
+                yt[wid][l] = make_float2(oky ? exp2f(-r.inv2 * ry * ry) : 0.f, ry);
             }
         }
-        float wz, rz;
-        {
-            const int bb = z0 + zl + zoff - r.fz;
-            rz = (float)bb - r.dz;
-            wz = (z0 + zl < c && bb <= hz && bb >= -hz) ? expf(-r.inv2 * rz * rz) : 0.f;
-        }
         __syncwarp();
-        // box intersect tile, tile-local (uniform across the warp)
+        // box intersect tile (tile-local, uniform across the warp)
         const int xlo = max(r.fx - hx - x0, 0), xhi = min(r.fx + hx - x0, TT - 1);
         const int ylo = max(r.fy - hy - y0, 0), yhi = min(r.fy + hy - y0, TT - 1);
-        float S0 = 0.f, Sx = 0.f, Sy = 0.f, Sxy2 = 0.f;
-        const int nrows = (yhi - ylo + 2) / 2;
-        for (int k = 0; k < nrows; ++k) {
-            int y = ylo + 2 * k + yh;
-            const bool yok = y <= yhi;
-            y = yok ? y : yhi;
-            const float2 eyr = yt[wid][y];
-            float p0 = 0.f, px = 0.f, pxx = 0.f;
-            for (int x = xlo; x <= xhi; ++x) {
-                const float4 tx4 = xt[wid][x];
-                const float u = sup[y][x][zl];
-                p0 = fmaf(u, tx4.x, p0);
-                px = fmaf(u, tx4.y, px);
-                pxx = fmaf(u, tx4.z, pxx);
+        const int zlo = max(r.fz - hz - zoff - z0, 0), zhi = min(r.fz + hz - zoff - z0, TT - 1);
+        const int lx = xhi - xlo + 1;
+        const int ncols = lx * (yhi - ylo + 1);
+        const uint32_t magic = (65536u + (uint32_t)lx - 1u) / (uint32_t)lx;   // c / lx for c < 256
+        float S0 = 0.f, Sx = 0.f, Sy = 0.f, Sz = 0.f, S2 = 0.f;
+        for (int c0 = 0; c0 < ncols; c0 += 32) {
+            const int cc = c0 + lane;
+            const bool valid = cc < ncols;
+            const int yo = (int)(((uint32_t)(valid ? cc : 0) * magic) >> 16);
+            const int y = ylo + yo, x = xlo + (valid ? cc : 0) - yo * lx;
+            const float* col = &sup[y][x][0];
+            float q0 = 0.f, q1 = 0.f, q2 = 0.f;
+            for (int z = zlo; z <= zhi; ++z) {   // z contraction: u * {ez, ez rz, ez rz^2}
+                const float4 t4 = zt[wid][z];
+                const float u = col[z];
+                q0 = fmaf(u, t4.x, q0);
+                q1 = fmaf(u, t4.y, q1);
+                q2 = fmaf(u, t4.z, q2);
             }
-            const float wy = yok ? eyr.x : 0.f, ry = eyr.y;
-            S0 = fmaf(wy, p0, S0);
-            Sx = fmaf(wy, px, Sx);
-            Sy = fmaf(wy * ry, p0, Sy);
-            Sxy2 = fmaf(wy, fmaf(ry * ry, p0, pxx), Sxy2);
+            const float2 ex = xt[wid][x], ey = yt[wid][y];
+            const float wv = valid ? ex.x * ey.x : 0.f;
+            const float wq = wv * q0;
+            S0 += wq;
+            Sx = fmaf(wq, ex.y, Sx);
+            Sy = fmaf(wq, ey.y, Sy);
+            Sz = fmaf(wv, q1, Sz);
+            S2 = fmaf(wq, fmaf(ex.y, ex.y, ey.y * ey.y), fmaf(wv, q2, S2));
         }
         __syncwarp();
-        float T0 = wz * S0, Tx = wz * Sx, Ty = wz * Sy, Tz = wz * rz * S0,
-              T2 = wz * fmaf(rz * rz, S0, Sxy2);
-        T0 = warp_sum(T0);
-        Tx = warp_sum(Tx);
-        Ty = warp_sum(Ty);
-        Tz = warp_sum(Tz);
-        T2 = warp_sum(T2);
+        S0 = warp_sum(S0);
+        Sx = warp_sum(Sx);
+        Sy = warp_sum(Sy);
+        Sz = warp_sum(Sz);
+        S2 = warp_sum(S2);
         if (lane == 0) {
             float* o = part + (size_t)orig * 5;
-            o[0] = T0; o[1] = Tx; o[2] = Ty; o[3] = Tz; o[4] = T2;
+            o[0] = S0; o[1] = Sx; o[2] = Sy; o[3] = Sz; o[4] = S2;
         }
     }
 }
@@ -475,7 +488,7 @@ __global__ void k_grad_norm_accum(const double* __restrict__ G, int64_t n,
 __global__ void k_export_items(const uint32_t* __restrict__ svals, int64_t np, int S,
                                int32_t* __restrict__ items) {
     int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (j < np) items[j] = (int32_t)(svals[j] / (uint32_t)S);
+    if (j < np) items[j] = (int32_t)(svals[j] >> S);   // S = log2(slots)
 }
 
 static int check_args(int64_t n, int w, int h, int c, int hx, int hy, int hz, size_t ws_bytes,
@@ -539,8 +552,13 @@ int splatct_fvr_bin(const double* params, int64_t n, int w, int h, int c, int z0
     k_tile_chunks<<<(unsigned)((L.nt + 1 + 255) / 256), 256, 0, s>>>(
         at<uint32_t>(ws, L.o_tstart), L.nt, at<uint32_t>(ws, L.o_cc), halt);
     SPLATCT_LAUNCH_CK();
-    return exclusive_scan_u32(at<uint32_t>(ws, L.o_cc), at<uint32_t>(ws, L.o_cstart), L.nt + 1,
-                              at<void>(ws, L.o_scan), s);
+    if (int e = exclusive_scan_u32(at<uint32_t>(ws, L.o_cc), at<uint32_t>(ws, L.o_cstart),
+                                   L.nt + 1, at<void>(ws, L.o_scan), s))
+        return e;
+    k_chunk_tiles<<<(unsigned)((L.nt + 255) / 256), 256, 0, s>>>(
+        at<uint32_t>(ws, L.o_cstart), L.nt, at<uint32_t>(ws, L.o_ctile), halt);
+    SPLATCT_LAUNCH_CK();
+    return SPLATCT_OK;
 }
 
 int splatct_fvr_forward(const double* params, int64_t n, int w, int h, int c, int z0, int hx,
@@ -550,7 +568,7 @@ int splatct_fvr_forward(const double* params, int64_t n, int w, int h, int c, in
     if (int e = check_args(n, w, h, c, hx, hy, hz, ws_bytes, L)) return e;
     const size_t vo = L.final_buf ? L.o_v1 : L.o_v0;
     k_fvr_fwd<<<(unsigned)L.nt, 256, 0, as_stream(stream)>>>(
-        at<GRec>(ws, L.o_rec), w, h, c, z0, hx, hy, hz, L.ntx, L.nty, L.S,
+        at<GRec>(ws, L.o_rec), w, h, c, z0, hx, hy, hz, L.ntx, L.nty, L.Sl,
         at<uint32_t>(ws, L.o_tstart), at<uint32_t>(ws, vo), vol_yxz, halt);
     SPLATCT_LAUNCH_CK();
     return SPLATCT_OK;
@@ -566,8 +584,9 @@ int splatct_fvr_backward(const double* params, int64_t n, int w, int h, int c, i
     const size_t vo = L.final_buf ? L.o_v1 : L.o_v0;
     float* part = at<float>(ws, L.o_part);
     k_fvr_bwd<<<(unsigned)L.bwd_grid, 256, 0, s>>>(
-        at<GRec>(ws, L.o_rec), w, h, c, z0, hx, hy, hz, L.ntx, L.nty, L.nt, L.S,
-        at<uint32_t>(ws, L.o_tstart), at<uint32_t>(ws, L.o_cstart), at<uint32_t>(ws, vo), up_yxz,
+        at<GRec>(ws, L.o_rec), w, h, c, z0, hx, hy, hz, L.ntx, L.nty, L.nt, L.Sl,
+        at<uint32_t>(ws, L.o_tstart), at<uint32_t>(ws, L.o_cstart), at<uint32_t>(ws, L.o_ctile),
+        at<uint32_t>(ws, vo), up_yxz,
         part, halt);
     SPLATCT_LAUNCH_CK();
     k_fvr_combine<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
@@ -606,7 +625,7 @@ int splatct_fvr_export_bins(const void* ws, size_t ws_bytes, int64_t n, int w, i
     if (items && total > 0) {
         const size_t vo = L.final_buf ? L.o_v1 : L.o_v0;
         k_export_items<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(at<uint32_t>(ws, vo),
-                                                                        total, L.S, items);
+                                                                        total, L.Sl, items);
         SPLATCT_LAUNCH_CK();
     }
     return SPLATCT_OK;

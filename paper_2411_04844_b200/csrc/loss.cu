@@ -528,21 +528,39 @@ __global__ void __launch_bounds__(R_NT, 1) k_loss_grad11(const float* __restrict
     if (threadIdx.x == 0) part[blockIdx.y * gridDim.x + blockIdx.x] = rr;
 }
 
-__global__ void __launch_bounds__(1024) k_sino_max(const float* __restrict__ x, int64_t count,
-                                                   double* __restrict__ out) {
-    __shared__ float sh[32];
+// max(x) over count floats: per-block maxima (grid-stride, 16 B loads), then
+// a single-block max.  NaN-free input (the sinogram is validated finite).
+__global__ void __launch_bounds__(256) k_sino_max_part(const float* __restrict__ x, int64_t count,
+                                                       float* __restrict__ part) {
+    __shared__ float sh[8];
     float mv = -INFINITY;
-    for (int64_t i = threadIdx.x; i < count; i += 1024) mv = fmaxf(mv, x[i]);
+    const int64_t n4 = ((uintptr_t)x % 16 == 0) ? count / 4 : 0;
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+    for (int64_t i = blockIdx.x * 256 + threadIdx.x; i < n4; i += (int64_t)gridDim.x * 256) {
+        const float4 v = x4[i];
+        mv = fmaxf(mv, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
+    }
+    for (int64_t i = 4 * n4 + blockIdx.x * 256 + threadIdx.x; i < count;
+         i += (int64_t)gridDim.x * 256)
+        mv = fmaxf(mv, x[i]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mv = fmaxf(mv, __shfl_xor_sync(0xffffffffu, mv, o));
     if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = mv;
     __syncthreads();
     if (threadIdx.x < 32) {
-        mv = sh[threadIdx.x];
+        mv = threadIdx.x < 8 ? sh[threadIdx.x] : -INFINITY;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) mv = fmaxf(mv, __shfl_xor_sync(0xffffffffu, mv, o));
-        if (threadIdx.x == 0) out[0] = (double)mv;
+        if (threadIdx.x == 0) part[blockIdx.x] = mv;
     }
+}
+
+__global__ void k_sino_max_final(const float* __restrict__ part, int n, double* __restrict__ out) {
+    float mv = -INFINITY;
+    for (int i = threadIdx.x; i < n; i += 32) mv = fmaxf(mv, part[i]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mv = fmaxf(mv, __shfl_xor_sync(0xffffffffu, mv, o));
+    if (threadIdx.x == 0) out[0] = (double)mv;
 }
 
 __global__ void __launch_bounds__(256) k_sq_diff(const float* __restrict__ x,
@@ -625,7 +643,13 @@ int splatct_loss_workspace_bytes(int m, int n, int p, size_t* bytes) {
 }
 
 int splatct_sino_max(const float* x, int64_t count, double* out, void* stream) {
-    k_sino_max<<<1, 1024, 0, as_stream(stream)>>>(x, count, out);
+    // out[1 ..] is scratch for the per-block maxima (caller passes
+    // double[1 + SPLATCT_SQDIFF_BLOCKS])
+    cudaStream_t s = as_stream(stream);
+    float* part = reinterpret_cast<float*>(out + 1);
+    k_sino_max_part<<<SPLATCT_SQDIFF_BLOCKS, 256, 0, s>>>(x, count, part);
+    SPLATCT_LAUNCH_CK();
+    k_sino_max_final<<<1, 32, 0, s>>>(part, SPLATCT_SQDIFF_BLOCKS, out);
     SPLATCT_LAUNCH_CK();
     return SPLATCT_OK;
 }

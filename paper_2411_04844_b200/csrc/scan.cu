@@ -115,9 +115,35 @@ size_t scan_temp_bytes(int64_t n) {
     return align_up((size_t)(nb > 0 ? nb : 1) * sizeof(int64_t));
 }
 
+// Whole array in one CTA (n <= SMALL_SCAN): one launch instead of three.
+constexpr int64_t SMALL_SCAN = 1 << 13;
+
+template <typename T>
+__global__ void __launch_bounds__(1024) k_scan_small(const T* __restrict__ in, T* __restrict__ out,
+                                                     int64_t n) {
+    __shared__ T sh[32];
+    const int64_t per = (n + 1023) / 1024;
+    const int64_t beg = threadIdx.x * per;
+    const int64_t end = beg + per < n ? beg + per : n;
+    T acc = 0;
+    for (int64_t i = beg; i < end; ++i) acc += in[i];
+    T tot;
+    T off = block_excl_scan<T, 1024>(acc, sh, &tot);
+    for (int64_t i = beg; i < end; ++i) {
+        const T v = in[i];
+        out[i] = off;
+        off += v;
+    }
+}
+
 template <typename T>
 static int exclusive_scan(const T* in, T* out, int64_t n, void* temp, cudaStream_t s) {
     if (n <= 0) return SPLATCT_OK;
+    if (n <= SMALL_SCAN) {
+        k_scan_small<T><<<1, 1024, 0, s>>>(in, out, n);
+        SPLATCT_LAUNCH_CK();
+        return SPLATCT_OK;
+    }
     int64_t nb = (n + SCAN_CHUNK - 1) / SCAN_CHUNK;
     T* sums = reinterpret_cast<T*>(temp);
     k_chunk_sums<T><<<(unsigned)nb, SCAN_NT, 0, s>>>(in, n, sums);

@@ -60,7 +60,7 @@ def cloud_to_params(cloud: GaussianCloud, device) -> torch.Tensor:
 
 
 def params_to_cloud(params: torch.Tensor) -> GaussianCloud:
-    p = params.detach().cpu().numpy()
+    p = to_host(params.detach())
     return GaussianCloud(np.ascontiguousarray(p[0:3].T), p[3].copy(), p[4].copy())
 
 
@@ -76,8 +76,17 @@ def zyx_to_yxz(arr, device) -> torch.Tensor:
     return _host_f32(arr).to(device).permute(1, 2, 0).contiguous()
 
 
+def to_host(t: torch.Tensor) -> np.ndarray:
+    """Device -> fresh numpy array via a pinned staging buffer (DMA-speed D2H)."""
+    if t.device.type != "cuda":
+        return t.numpy().copy()
+    pinned = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    pinned.copy_(t)
+    return pinned.numpy().copy()
+
+
 def yxz_to_zyx(t: torch.Tensor) -> np.ndarray:
-    return t.permute(2, 0, 1).contiguous().cpu().numpy()
+    return to_host(t.permute(2, 0, 1).contiguous())
 
 
 def sino_to_device(views, device) -> torch.Tensor:
@@ -347,9 +356,9 @@ class LossPlan:
 
 
 def sino_max(x: torch.Tensor) -> float:
-    out = torch.empty(1, dtype=torch.float64, device=x.device)
+    out = torch.empty(1 + _lib.SQDIFF_BLOCKS, dtype=torch.float64, device=x.device)
     call("splatct_sino_max", ptr(x), int(x.numel()), ptr(out), stream_handle())
-    return float(out.item())
+    return float(out[0].item())
 
 
 def reduce_sum(x: torch.Tensor, out: torch.Tensor) -> None:

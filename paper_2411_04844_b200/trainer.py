@@ -121,6 +121,35 @@ class Trainer:
         self.fvr = D.FvrPlan(nG, (self.w, self.h, s.c_local), self.box.half, s.z0, dev)
         self.graph = None
 
+    def reload(self, measured, params, m1=None, m2=None, step: int = 0, accum=None):
+        """Re-initialise the state in place (same shapes and lmax).
+
+        Every buffer keeps its address, so a captured CUDA graph stays valid
+        and the next run replays it without re-capture (optim's trainer cache).
+        """
+        if tuple(measured.shape) != tuple(self.meas.shape) or \
+                tuple(params.shape) != tuple(self.params.shape):
+            raise ValueError("reload needs the same sinogram and cloud shapes")
+        self.meas.copy_(measured)
+        self.params.copy_(params)
+        if m1 is None:
+            self.m1.zero_()
+        else:
+            self.m1.copy_(m1)
+        if m2 is None:
+            self.m2.zero_()
+        else:
+            self.m2.copy_(m2)
+        self.grads.zero_()
+        if accum is None:
+            self.accum.zero_()
+        else:
+            self.accum.copy_(accum)
+        self.step_t.fill_(int(step))
+        self.iter_t.zero_()
+        self.halt.zero_()
+        self.trace.fill_(math.nan)
+
     def resize(self, params, m1, m2, accum=None):
         """Replace the cloud (densification changes N); drops the captured graph."""
         self._set_params(params, m1, m2, accum)

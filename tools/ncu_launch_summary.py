@@ -1,3 +1,4 @@
+"""Summarise an ncu --csv launch list: per-kernel count, device time (us), DRAM MB, instructions."""
 import csv, collections, sys
 rows=list(csv.reader(open(sys.argv[1])))
 hdr=None; data=[]
@@ -10,9 +11,9 @@ for d in data:
     v=float(d['Metric Value'].replace(',',''))
     u=d['Metric Unit']; m=d['Metric Name']
     if m=='gpu__time_duration.sum':
-        v = v/1000 if u=='nsecond' else (v*1000 if u=='msecond' else v)
+        v = v/1000 if u in ('nsecond','ns') else (v*1000 if u in ('msecond','ms') else v)
     if m.startswith('dram'):
-        v = v/1e6 if u=='byte' else (v/1e3 if u=='Kbyte' else (v if u=='Mbyte' else v*1e3))
+        v = v/1e6 if u in ('byte','B') else (v/1e3 if u in ('Kbyte','KB') else (v if u in ('Mbyte','MB') else v*1e3))
     per[d['ID']][m]=v; names[d['ID']]=d['Kernel Name'].split('(')[0][:50]
 agg=collections.defaultdict(lambda:[0,0.0,0.0,0.0])
 for i,mm in per.items():
