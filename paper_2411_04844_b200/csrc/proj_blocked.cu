@@ -193,6 +193,7 @@ struct TvB {
 __device__ __forceinline__ int sgnf(float d) { return (d > 0.f) - (d < 0.f); }
 
 constexpr int BS_WARPS = 8;
+constexpr int UNR = 8;    // z-vector gathers in flight per warp (16 measured no faster)
 
 // TV epilogue for one pixel row and the lane's V consecutive slices
 // [zb, zb+V): forward-difference subgradient of loss.tv_loss (loss.py:195-206)
@@ -279,7 +280,7 @@ __device__ __forceinline__ void tv_epilogue(const TvB& a, int64_t row, int zb, i
 // column load.  Entries are staged per warp in shared memory and consumed
 // four at a time (four independent vector loads in flight).
 template <int V, bool TV>
-__global__ void __launch_bounds__(32 * BS_WARPS) k_bspmm(GroupMap gm, const int64_t* __restrict__ gptr,
+__global__ void __launch_bounds__(32 * BS_WARPS, 3) k_bspmm(GroupMap gm, const int64_t* __restrict__ gptr,
                                                         const int32_t* __restrict__ gidx,
                                                         const float4* __restrict__ gval,
                                                         const float* __restrict__ X,
@@ -301,16 +302,41 @@ __global__ void __launch_bounds__(32 * BS_WARPS) k_bspmm(GroupMap gm, const int6
 #pragma unroll
         for (int t = 0; t < V; ++t) acc[k][t] = 0.f;
     const int64_t b = gptr[g], e = gptr[g + 1];
+    // entries of the next batch are prefetched into registers while the
+    // current batch is consumed from shared memory
+    int nc = 0;
+    float4 nw = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (b + lane < e) {
+        nc = __ldcs(gidx + b + lane);
+        nw = __ldcs(gval + b + lane);
+    }
     for (int64_t j0 = b; j0 < e; j0 += 32) {
-        const int64_t jl = j0 + lane;
         __syncwarp();
-        if (jl < e) {
-            s_col[wid][lane] = __ldcs(gidx + jl);
-            s_w[wid][lane] = __ldcs(gval + jl);
+        s_col[wid][lane] = nc;
+        s_w[wid][lane] = nw;
+        __syncwarp();
+        if (j0 + 32 + lane < e) {
+            nc = __ldcs(gidx + j0 + 32 + lane);
+            nw = __ldcs(gval + j0 + 32 + lane);
         }
-        __syncwarp();
         const int cnt = (int)min((int64_t)32, e - j0);
         int jj = 0;
+        for (; jj + UNR <= cnt; jj += UNR) {   // UNR z-vector gathers in flight
+            float xv[UNR][V];
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) ldvb<V>(X + (int64_t)s_col[wid][jj + u] * c + zl, xv[u]);
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const float4 w4 = s_w[wid][jj + u];
+#pragma unroll
+                for (int t = 0; t < V; ++t) {
+                    acc[0][t] = fmaf(w4.x, xv[u][t], acc[0][t]);
+                    acc[1][t] = fmaf(w4.y, xv[u][t], acc[1][t]);
+                    acc[2][t] = fmaf(w4.z, xv[u][t], acc[2][t]);
+                    acc[3][t] = fmaf(w4.w, xv[u][t], acc[3][t]);
+                }
+            }
+        }
         for (; jj + 4 <= cnt; jj += 4) {
             float xv[4][V];
 #pragma unroll
