@@ -71,11 +71,11 @@ int splatct_fvr_bin(const double* params, int64_t n, int w, int h, int c, int z0
 
 /* V = sum_i I_i ex_i (x) ey_i (x) ez_i over box intersect volume; one CTA per
  * tile accumulating in registers/shared memory, each voxel written once
- * (no memset, no global atomics).  Requires a prior splatct_fvr_bin on the
- * same params.  Replaces _kernels.splat_decomposed(mu, sigma, intensity,
+ * (no memset, no float atomics; persistent CTAs take tiles from a counter in
+ * ws).  Requires a prior splatct_fvr_bin on the same params.  Replaces _kernels.splat_decomposed(mu, sigma, intensity,
  * hx, hy, hz, w, h, c, bufs) (_kernels.py:23) + fvr.py:163-167. */
 int splatct_fvr_forward(const double* params, int64_t n, int w, int h, int c, int z0, int hx,
-                        int hy, int hz, const void* ws, size_t ws_bytes, float* vol_yxz,
+                        int hy, int hz, void* ws, size_t ws_bytes, float* vol_yxz,
                         const int* halt, void* stream);
 
 /* Per-Gaussian gradients from dL/dV (yxz), fvr.py:227-273: per-tile partial

@@ -91,12 +91,10 @@ def load(build_if_missing: bool = True):
         if _lib is not None:
             return _lib
         path = _build.LIB
-        if build_if_missing:
-            try:
-                _build.build()
-            except (RuntimeError, FileNotFoundError, OSError):
-                if not os.path.exists(path):
-                    raise
+        if build_if_missing and _build.nvcc_available():
+            _build.build()   # a failed build raises: never run a stale library
+        elif not os.path.exists(path):
+            raise OSError(f"libsplatct.so missing at {path} and nvcc is not available")
         if not os.path.exists(path):
             raise OSError(f"libsplatct.so not found at {path}; run paper_2411_04844_b200.build")
         L = ctypes.CDLL(path)

@@ -27,6 +27,10 @@ NVCC_FLAGS = [
 ]
 
 
+def nvcc_available() -> bool:
+    return os.path.exists(NVCC)
+
+
 def _stale() -> bool:
     if not os.path.exists(LIB):
         return True

@@ -92,7 +92,7 @@ static FvrLayout make_layout(int64_t n, int w, int h, int c, int hx, int hy, int
     L.o_v0 = take(sizeof(uint32_t) * (size_t)L.np);
     L.o_k1 = take(sizeof(uint32_t) * (size_t)L.np);
     L.o_v1 = take(sizeof(uint32_t) * (size_t)L.np);
-    L.o_tcount = take(sizeof(uint32_t) * (size_t)(L.nt + 1));
+    L.o_tcount = take(sizeof(uint32_t) * 4);   // forward's dynamic tile counter
     L.o_tstart = take(sizeof(uint32_t) * (size_t)(L.nt + 1));
     L.o_hist = take(sizeof(uint32_t) * RADIX * (size_t)(L.sort_blocks > 0 ? L.sort_blocks : 1));
     size_t sc1 = scan_temp_bytes(RADIX * (L.sort_blocks > 0 ? L.sort_blocks : 1));
@@ -125,7 +125,7 @@ __global__ void k_footprint(const double* __restrict__ P, int64_t n, int w, int 
                             int hx, int hy, int hz, int ntx, int nty, int S, uint32_t sentinel,
                             int32_t* __restrict__ fp, int32_t* __restrict__ gcount,
                             uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
-                            uint32_t* __restrict__ tcount, GRec* __restrict__ rec,
+                            GRec* __restrict__ rec,
                             const int* halt) {
     if (halted(halt)) return;
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -168,7 +168,6 @@ __global__ void k_footprint(const double* __restrict__ P, int64_t n, int w, int 
                     uint32_t tid = (uint32_t)((tz * nty + ty) * ntx + tx);
                     keys[base + cnt] = tid;
                     vals[base + cnt] = base + cnt;
-                    atomicAdd(&tcount[tid], 1u);
                     ++cnt;
                 }
     }
@@ -267,20 +266,35 @@ __device__ __forceinline__ float tab_weight(int coord_local, int origin, int dim
 
 __global__ void __launch_bounds__(256) k_fvr_fwd(const GRec* __restrict__ rec, int w, int h, int c,
                                                  int zoff, int hx, int hy, int hz, int ntx,
-                                                 int nty, int S,
+                                                 int nty, int64_t nt, int S,
                                                  const uint32_t* __restrict__ tstart,
                                                  const uint32_t* __restrict__ svals,
-                                                 float* __restrict__ vol, const int* halt) {
+                                                 float* __restrict__ vol,
+                                                 unsigned int* __restrict__ counter,
+                                                 const int* halt) {
     if (halted(halt)) return;
     __shared__ __align__(16) float tab[FWD_BATCH][3][TT];
-    const int t = blockIdx.x;
-    const int txi = t % ntx, tyi = (t / ntx) % nty, tzi = t / (ntx * nty);
-    const int x0 = txi * TT, y0 = tyi * TT, z0 = tzi * TT;
     const int tx = threadIdx.x & (TT - 1), ty = threadIdx.x / TT;
+    __shared__ int64_t s_next;
+    const int ntz = (int)(nt / ((int64_t)ntx * nty));
+    // persistent CTAs fetch tiles dynamically (uneven per-tile cost); tiles are
+    // visited z-fastest so consecutive fetches write adjacent 64 B column
+    // segments (HBM-friendly for the all-zero tiles of sparse volumes)
+    for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_next = (int64_t)atomicAdd(counter, 1u);
+    __syncthreads();
+    const int64_t k = s_next;
+    if (k >= nt) break;
+    const int tzi = (int)(k % ntz);
+    const int64_t rest = k / ntz;
+    const int txi = (int)(rest % ntx), tyi = (int)(rest / ntx);
+    const int64_t t = ((int64_t)tzi * nty + tyi) * ntx + txi;
+    const int x0 = txi * TT, y0 = tyi * TT, z0 = tzi * TT;
     const uint32_t beg = tstart[t], end = tstart[t + 1];
     float acc[TT];
 #pragma unroll
-    for (int k = 0; k < TT; ++k) acc[k] = 0.f;
+    for (int q = 0; q < TT; ++q) acc[q] = 0.f;
     const int tg = threadIdx.x >> 3, tj = threadIdx.x & 7;   // table builder: Gaussian, part
 
     for (uint32_t b0 = beg; b0 < end; b0 += FWD_BATCH) {
@@ -315,17 +329,19 @@ __global__ void __launch_bounds__(256) k_fvr_fwd(const GRec* __restrict__ rec, i
         }
     }
     const int x = x0 + tx, y = y0 + ty;
-    if (x >= w || y >= h) return;
-    float* col = vol + ((int64_t)y * w + x) * c;
-    if ((c & 3) == 0 && z0 + TT <= c) {
-        float4* dst = reinterpret_cast<float4*>(col + z0);
+    if (x < w && y < h) {
+        float* col = vol + ((int64_t)y * w + x) * c;
+        if ((c & 3) == 0 && z0 + TT <= c) {
+            float4* dst = reinterpret_cast<float4*>(col + z0);
 #pragma unroll
-        for (int q = 0; q < TT / 4; ++q)
-            dst[q] = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
-    } else {
+            for (int q = 0; q < TT / 4; ++q)
+                dst[q] = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
+        } else {
 #pragma unroll
-        for (int k = 0; k < TT; ++k)
-            if (z0 + k < c) col[z0 + k] = acc[k];
+            for (int k = 0; k < TT; ++k)
+                if (z0 + k < c) col[z0 + k] = acc[k];
+        }
+    }
     }
 }
 
@@ -333,6 +349,21 @@ __global__ void __launch_bounds__(256) k_fvr_fwd(const GRec* __restrict__ rec, i
 // backward: one CTA per (tile, chunk of <= BWD_CHUNK pairs), one warp per pair
 // --------------------------------------------------------------------------
 constexpr int BWD_CHUNK = 64;
+
+// tstart[t] = lower_bound(sorted keys, t) for t in [0, nt]; keys >= nt are
+// the empty-slot sentinels, so tstart[nt] = number of real pairs.
+__global__ void k_tile_starts(const uint32_t* __restrict__ skeys, int64_t np, int64_t nt,
+                              uint32_t* __restrict__ tstart, const int* halt) {
+    if (halted(halt)) return;
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t > nt) return;
+    int64_t lo = 0, hi = np;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (skeys[mid] < (uint32_t)t) lo = mid + 1; else hi = mid;
+    }
+    tstart[t] = (uint32_t)lo;
+}
 
 __global__ void k_tile_chunks(const uint32_t* __restrict__ tstart, int64_t nt,
                               uint32_t* __restrict__ cc, const int* halt) {
@@ -521,13 +552,11 @@ int splatct_fvr_bin(const double* params, int64_t n, int w, int h, int c, int z0
     FvrLayout L = make_layout(n, w, h, c, hx, hy, hz);
     if (int e = check_args(n, w, h, c, hx, hy, hz, ws_bytes, L)) return e;
     cudaStream_t s = as_stream(stream);
-    uint32_t* tcount = at<uint32_t>(ws, L.o_tcount);
-    SPLATCT_CK(cudaMemsetAsync(tcount, 0, sizeof(uint32_t) * (L.nt + 1), s));
     if (n > 0) {
         k_footprint<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
             params, n, w, h, c, z0, hx, hy, hz, L.ntx, L.nty, L.S, (uint32_t)L.nt,
             at<int32_t>(ws, L.o_fp), at<int32_t>(ws, L.o_gcount), at<uint32_t>(ws, L.o_k0),
-            at<uint32_t>(ws, L.o_v0), tcount, at<GRec>(ws, L.o_rec), halt);
+            at<uint32_t>(ws, L.o_v0), at<GRec>(ws, L.o_rec), halt);
         SPLATCT_LAUNCH_CK();
         uint32_t* hist = at<uint32_t>(ws, L.o_hist);
         for (int p = 0; p < L.passes; ++p) {
@@ -545,9 +574,13 @@ int splatct_fvr_bin(const double* params, int64_t n, int w, int h, int c, int z0
             SPLATCT_LAUNCH_CK();
         }
     }
-    if (int e = exclusive_scan_u32(tcount, at<uint32_t>(ws, L.o_tstart), L.nt + 1,
-                                   at<void>(ws, L.o_scan), s))
-        return e;
+    {   // tile offsets from the sorted keys (sentinels sort last): no atomics
+        const size_t ko = L.final_buf ? L.o_k1 : L.o_k0;
+        k_tile_starts<<<(unsigned)((L.nt + 1 + 255) / 256), 256, 0, s>>>(
+            n > 0 ? at<uint32_t>(ws, ko) : nullptr, n > 0 ? L.np : 0, L.nt,
+            at<uint32_t>(ws, L.o_tstart), halt);
+        SPLATCT_LAUNCH_CK();
+    }
     // backward work items: ceil(pairs / BWD_CHUNK) chunks per tile
     k_tile_chunks<<<(unsigned)((L.nt + 1 + 255) / 256), 256, 0, s>>>(
         at<uint32_t>(ws, L.o_tstart), L.nt, at<uint32_t>(ws, L.o_cc), halt);
@@ -562,14 +595,17 @@ int splatct_fvr_bin(const double* params, int64_t n, int w, int h, int c, int z0
 }
 
 int splatct_fvr_forward(const double* params, int64_t n, int w, int h, int c, int z0, int hx,
-                        int hy, int hz, const void* ws, size_t ws_bytes, float* vol_yxz,
+                        int hy, int hz, void* ws, size_t ws_bytes, float* vol_yxz,
                         const int* halt, void* stream) {
     FvrLayout L = make_layout(n, w, h, c, hx, hy, hz);
     if (int e = check_args(n, w, h, c, hx, hy, hz, ws_bytes, L)) return e;
     const size_t vo = L.final_buf ? L.o_v1 : L.o_v0;
-    k_fvr_fwd<<<(unsigned)L.nt, 256, 0, as_stream(stream)>>>(
-        at<GRec>(ws, L.o_rec), w, h, c, z0, hx, hy, hz, L.ntx, L.nty, L.Sl,
-        at<uint32_t>(ws, L.o_tstart), at<uint32_t>(ws, vo), vol_yxz, halt);
+    const int64_t grid = L.nt < 148 * 8 ? L.nt : 148 * 8;   // persistent over tiles
+    unsigned int* counter = at<uint32_t>(ws, L.o_tcount);
+    SPLATCT_CK(cudaMemsetAsync(counter, 0, sizeof(unsigned int), as_stream(stream)));
+    k_fvr_fwd<<<(unsigned)grid, 256, 0, as_stream(stream)>>>(
+        at<GRec>(ws, L.o_rec), w, h, c, z0, hx, hy, hz, L.ntx, L.nty, L.nt, L.Sl,
+        at<uint32_t>(ws, L.o_tstart), at<uint32_t>(ws, vo), vol_yxz, counter, halt);
     SPLATCT_LAUNCH_CK();
     return SPLATCT_OK;
 }
