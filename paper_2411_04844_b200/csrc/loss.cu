@@ -335,6 +335,12 @@ __device__ __forceinline__ void cp_commit_group() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_wait_group() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
+// Each thread issues (and later converts) the same 16-byte chunks of every
+// staged row, so the f32 landing buffer is private per chunk: only the
+// converted f64 row (read by 11 neighbouring columns) needs a barrier.
+constexpr int S_CHUNKS = 2 * R_SPAN * 8;                  // x, y: 18 columns x 8 chunks
+constexpr int S_SLOTS = (S_CHUNKS + R_NT - 1) / R_NT;      // chunks per thread
+
 __global__ void __launch_bounds__(R_NT, 1) k_ssim_stats11(const float* __restrict__ X,
                                                           const float* __restrict__ Y, int m, int n,
                                                           int p, Win W, double c1, double c2,
@@ -342,28 +348,55 @@ __global__ void __launch_bounds__(R_NT, 1) k_ssim_stats11(const float* __restric
                                                           double* __restrict__ part,
                                                           const int* halt) {
     if (halted(halt)) return;
-    __shared__ __align__(16) float sx[R_BUF][R_SPAN][32];
-    __shared__ __align__(16) float sy[R_BUF][R_SPAN][32];
+    __shared__ __align__(16) float sf[R_BUF][2][R_SPAN][32];    // cp.async landing (f32)
+    __shared__ __align__(16) double sd[2][2][R_SPAN][32];       // converted rows (f64)
     __shared__ double red[R_NT / 32];
     const int lane = threadIdx.x & 31, cl = threadIdx.x >> 5;
     const int zb = blockIdx.x * 32, j0 = blockIdx.y * R_COLS;
     const int z = zb + lane, j = j0 + cl;
     const bool act = z < p && j < vc;
     const int64_t plane = (int64_t)vr * vc * p;
-    // row v -> buffer v % 3: 18 columns x 8 chunks of 16 B per array
+    const int64_t rowstride = (int64_t)n * p;
+    // per-thread chunk table (fixed for every row)
+    int64_t goff[S_SLOTS];
+    int soff[S_SLOTS];
+    bool gok[S_SLOTS], mine[S_SLOTS];
+#pragma unroll
+    for (int k = 0; k < S_SLOTS; ++k) {
+        const int e = threadIdx.x + k * R_NT;
+        mine[k] = e < S_CHUNKS;
+        const int arr = e / (R_SPAN * 8), rem = e % (R_SPAN * 8);
+        const int col = rem >> 3, q = rem & 7;
+        gok[k] = mine[k] && j0 + col < n && zb + 4 * q < p;
+        goff[k] = gok[k] ? (int64_t)(j0 + col) * p + zb + 4 * q : 0;
+        soff[k] = (arr * R_SPAN + col) * 32 + 4 * q;     // within one [2][R_SPAN][32] row
+        if (arr) goff[k] = -goff[k] - 1;                  // sign selects Y
+    }
     auto issue = [&](int v) {
         if (v < m) {
-            const int buf = v % R_BUF;
-            for (int e = threadIdx.x; e < R_SPAN * 8 * 2; e += R_NT) {
-                const int arr = e / (R_SPAN * 8), rem = e % (R_SPAN * 8);
-                const int col = rem >> 3, q = rem & 7;
-                const bool ok = j0 + col < n && zb + 4 * q < p;
-                const int64_t gi = ok ? ((int64_t)v * n + j0 + col) * p + zb + 4 * q : 0;
-                float* dst = arr ? &sy[buf][col][4 * q] : &sx[buf][col][4 * q];
-                cp16_zfill(dst, (arr ? Y : X) + gi, ok);
+            float* buf = &sf[v % R_BUF][0][0][0];
+#pragma unroll
+            for (int k = 0; k < S_SLOTS; ++k) {
+                if (!mine[k]) continue;
+                const bool isy = goff[k] < 0;
+                const int64_t o = isy ? -goff[k] - 1 : goff[k];
+                const float* src = (isy ? Y : X) + (gok[k] ? v * rowstride + o : 0);
+                cp16_zfill(buf + soff[k], src, gok[k]);
             }
         }
         cp_commit_group();
+    };
+    auto convert = [&](int v) {   // own chunks of row v: f32 landing -> f64 row buffer
+        const float* fb = &sf[v % R_BUF][0][0][0];
+        double* db = &sd[v & 1][0][0][0];
+#pragma unroll
+        for (int k = 0; k < S_SLOTS; ++k) {
+            if (!mine[k]) continue;
+            const float4 f = *reinterpret_cast<const float4*>(fb + soff[k]);
+            double2* d2 = reinterpret_cast<double2*>(db + soff[k]);
+            d2[0] = make_double2((double)f.x, (double)f.y);
+            d2[1] = make_double2((double)f.z, (double)f.w);
+        }
     };
     issue(0);
     issue(1);
@@ -374,22 +407,23 @@ __global__ void __launch_bounds__(R_NT, 1) k_ssim_stats11(const float* __restric
         for (int ph = 0; ph < 11; ++ph) {
             const int v = v0 + ph;
             if (v >= m) break;
-            cp_wait_group<1>();   // row v landed (row v+1 may still be in flight)
-            __syncthreads();
-            issue(v + 2);          // into the buffer row v-1 used (all threads are past it)
-            const int buf = v % R_BUF;
+            cp_wait_group<1>();   // my chunks of row v landed (row v+1 may be in flight)
+            convert(v);
+            issue(v + 2);         // my landing slot of row v-1 is free (converted last step)
+            __syncthreads();      // row v (f64) complete; everyone is past row v-2's reads
+            const double* xr = &sd[v & 1][0][cl][lane];
+            const double* yr = &sd[v & 1][1][cl][lane];
             double h[2][5] = {{0, 0, 0, 0, 0}, {0, 0, 0, 0, 0}};
 #pragma unroll
             for (int b = 0; b < 11; ++b) {
-                const double xv = (double)sx[buf][cl + b][lane];
-                const double yv = (double)sy[buf][cl + b][lane];
-                const double g = W.gc[b];
+                const double xv = xr[32 * b], yv = yr[32 * b];
+                const double gx = W.gc[b] * xv, gy = W.gc[b] * yv;
                 double* hb = h[b & 1];
-                hb[0] = fma(g, xv, hb[0]);
-                hb[1] = fma(g, yv, hb[1]);
-                hb[2] = fma(g, xv * xv, hb[2]);
-                hb[3] = fma(g, yv * yv, hb[3]);
-                hb[4] = fma(g, xv * yv, hb[4]);
+                hb[0] += gx;
+                hb[1] += gy;
+                hb[2] = fma(gx, xv, hb[2]);
+                hb[3] = fma(gy, yv, hb[3]);
+                hb[4] = fma(gx, yv, hb[4]);
             }
 #pragma unroll
             for (int f = 0; f < 5; ++f) ring[ph][f] = h[0][f] + h[1][f];
@@ -423,6 +457,10 @@ __global__ void __launch_bounds__(R_NT, 1) k_ssim_stats11(const float* __restric
     if (threadIdx.x == 0) part[blockIdx.y * gridDim.x + blockIdx.x] = r;
 }
 
+constexpr int G_DCHUNKS = 3 * R_SPAN * 16;                   // D: 3 fields x 18 cols x 16
+constexpr int G_DSLOTS = (G_DCHUNKS + R_NT - 1) / R_NT;
+constexpr int G_XCHUNKS = 2 * R_COLS * 8;                    // x, y: 8 cols x 8 chunks
+
 __global__ void __launch_bounds__(R_NT, 1) k_loss_grad11(const float* __restrict__ X,
                                                          const float* __restrict__ Y, int m, int n,
                                                          int p, Win W, int vr, int vc,
@@ -441,28 +479,42 @@ __global__ void __launch_bounds__(R_NT, 1) k_loss_grad11(const float* __restrict
     const int z = zb + lane, s = s0 + cl;
     const bool act = z < p && s < n;
     const int64_t plane = (int64_t)vr * vc * p;
-    const double inv_val = 1.0 / ((double)vr * (double)vc);
     const bool ss = ssw > 0.0;
+    // constant factors of loss.py:64-74 (sign / count) and the SSIM chain rule
+    const double l1f = l1w > 0.0 ? l1w / l1_count : 0.0;
+    const double ssf = ss ? -ssw / (ssim_slices * (double)vr * (double)vc) : 0.0;
+    int64_t dgo[G_DSLOTS];
+    int dso[G_DSLOTS];
+    bool dok[G_DSLOTS], dmine[G_DSLOTS];
+#pragma unroll
+    for (int k = 0; k < G_DSLOTS; ++k) {
+        const int e = threadIdx.x + k * R_NT;
+        dmine[k] = e < G_DCHUNKS;
+        const int f = e / (R_SPAN * 16), rem = e % (R_SPAN * 16);
+        const int col = rem >> 4, q = rem & 15;
+        const int jj = s0 - 10 + col;
+        dok[k] = dmine[k] && jj >= 0 && jj < vc && zb + 2 * q < p;
+        dgo[k] = dok[k] ? f * plane + (int64_t)jj * p + zb + 2 * q : 0;
+        dso[k] = (f * R_SPAN + col) * 32 + 2 * q;
+    }
+    const bool xmine = threadIdx.x < G_XCHUNKS;
+    const int xarr = threadIdx.x / (R_COLS * 8), xrem = threadIdx.x % (R_COLS * 8);
+    const int xcol = xrem >> 3, xq = xrem & 7;
+    const bool xok = xmine && s0 + xcol < n && zb + 4 * xq < p;
+    const int64_t xgo = xok ? (int64_t)(s0 + xcol) * p + zb + 4 * xq : 0;
+    const float* xsrc = xarr ? Y : X;
+    const int64_t drow = (int64_t)vc * p, xrowstride = (int64_t)n * p;
     auto issue = [&](int r) {
         if (r < m) {
             const int buf = r % R_BUF;
-            if (ss && r < vr) {   // D: 3 fields x 18 columns x 16 chunks of 16 B (2 doubles)
-                for (int e = threadIdx.x; e < 3 * R_SPAN * 16; e += R_NT) {
-                    const int f = e / (R_SPAN * 16), rem = e % (R_SPAN * 16);
-                    const int col = rem >> 4, q = rem & 15;
-                    const int jj = s0 - 10 + col;
-                    const bool ok = jj >= 0 && jj < vc && zb + 2 * q < p;
-                    const int64_t gi = ok ? f * plane + ((int64_t)r * vc + jj) * p + zb + 2 * q : 0;
-                    cp16_zfill(&sd[buf][f][col][2 * q], D + gi, ok);
-                }
+            if (ss && r < vr) {
+                double* db = &sd[buf][0][0][0];
+#pragma unroll
+                for (int k = 0; k < G_DSLOTS; ++k)
+                    if (dmine[k]) cp16_zfill(db + dso[k], D + (dok[k] ? r * drow + dgo[k] : 0), dok[k]);
             }
-            for (int e = threadIdx.x; e < 2 * R_COLS * 8; e += R_NT) {   // x, y: 8 cols x 8 chunks
-                const int arr = e / (R_COLS * 8), rem = e % (R_COLS * 8);
-                const int col = rem >> 3, q = rem & 7;
-                const bool ok = s0 + col < n && zb + 4 * q < p;
-                const int64_t gi = ok ? ((int64_t)r * n + s0 + col) * p + zb + 4 * q : 0;
-                cp16_zfill(&sxy[buf][arr][col][4 * q], (arr ? Y : X) + gi, ok);
-            }
+            if (xmine)
+                cp16_zfill(&sxy[buf][xarr][xcol][4 * xq], xsrc + (xok ? r * xrowstride + xgo : 0), xok);
         }
         cp_commit_group();
     };
@@ -501,13 +553,12 @@ __global__ void __launch_bounds__(R_NT, 1) k_loss_grad11(const float* __restrict
                 const double yv = (double)sxy[buf][1][cl][lane];
                 const double diff = xv - yv;
                 l1sum += fabs(diff);
-                double g = 0.0;
-                if (l1w > 0.0) g += l1w * ((double)((diff > 0) - (diff < 0)) / l1_count);
+                double g = l1f * (double)((diff > 0) - (diff < 0));
                 if (ss) {
+                    // row r - a lives in slot (ph - a) mod 11; rows < 0 are the zeroed slots
                     double A[2][3] = {{0, 0, 0}, {0, 0, 0}};
 #pragma unroll
-                    for (int a = 0; a < 11; ++a) {   // row r - a lives in slot (ph - a) mod 11
-                        if (r - a < 0) break;
+                    for (int a = 0; a < 11; ++a) {
                         const double gg = W.gr[a];
                         double* Aa = A[a & 1];
 #pragma unroll
@@ -516,8 +567,7 @@ __global__ void __launch_bounds__(R_NT, 1) k_loss_grad11(const float* __restrict
                     double gs = A[0][0] + A[1][0];
                     gs += 2.0 * xv * (A[0][1] + A[1][1]);
                     gs += yv * (A[0][2] + A[1][2]);
-                    gs *= inv_val;
-                    g += ssw * (-gs / ssim_slices);
+                    g += ssf * gs;
                 }
                 G[((int64_t)r * n + s) * p + z] = (float)g;
             }
