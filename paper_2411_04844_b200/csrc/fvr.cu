@@ -274,6 +274,7 @@ __global__ void __launch_bounds__(256) k_fvr_fwd(const GRec* __restrict__ rec, i
                                                  const int* halt) {
     if (halted(halt)) return;
     __shared__ __align__(16) float tab[FWD_BATCH][3][TT];
+    __shared__ __align__(16) float4 sacc[TT * TT][TT / 4];   // store transpose
     const int tx = threadIdx.x & (TT - 1), ty = threadIdx.x / TT;
     __shared__ int64_t s_next;
     const int ntz = (int)(nt / ((int64_t)ntx * nty));
@@ -328,15 +329,33 @@ __global__ void __launch_bounds__(256) k_fvr_fwd(const GRec* __restrict__ rec, i
             }
         }
     }
-    const int x = x0 + tx, y = y0 + ty;
-    if (x < w && y < h) {
-        float* col = vol + ((int64_t)y * w + x) * c;
-        if ((c & 3) == 0 && z0 + TT <= c) {
-            float4* dst = reinterpret_cast<float4*>(col + z0);
+    // store: the tile's 256 columns x 64 B are written 8 columns per warp
+    // instruction (4 lanes x 16 B per column) instead of 32 scattered
+    // half-sectors; non-empty tiles transpose through shared memory
+    // (XOR-swizzled, conflict-free), empty tiles store zeros directly
+    if ((c & 3) == 0 && z0 + TT <= c) {
+        const bool empty = beg == end;
+        if (!empty) {
 #pragma unroll
             for (int q = 0; q < TT / 4; ++q)
-                dst[q] = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
-        } else {
+                sacc[threadIdx.x][q ^ ((threadIdx.x >> 1) & 3)] =
+                    make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
+            __syncthreads();
+        }
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, ch = lane & 3;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int cid = wid * 32 + i * 8 + (lane >> 2);
+            const int x = x0 + (cid & (TT - 1)), y = y0 + cid / TT;
+            const float4 v = empty ? make_float4(0.f, 0.f, 0.f, 0.f)
+                                   : sacc[cid][ch ^ ((cid >> 1) & 3)];
+            if (x < w && y < h)
+                *reinterpret_cast<float4*>(vol + ((int64_t)y * w + x) * c + z0 + 4 * ch) = v;
+        }
+    } else {
+        const int x = x0 + tx, y = y0 + ty;
+        if (x < w && y < h) {
+            float* col = vol + ((int64_t)y * w + x) * c;
 #pragma unroll
             for (int k = 0; k < TT; ++k)
                 if (z0 + k < c) col[z0 + k] = acc[k];
