@@ -1,6 +1,5 @@
 // fvr.cu -- Fast Volume Reconstruction on B200: footprints, radix-sorted
-// tile bins, tile-owned forward splat, tile-partial backward + deterministic
-// per-Gaussian combine.
+// tile bins, tile-owned forward splat, Gaussian-owned backward.
 //
 // Reference semantics (paths under /root/reference/pkg/src/splatct/):
 //   footprint  [floor(mu_a)-h_a, floor(mu_a)+h_a] intersect [0, dim_a)
@@ -19,10 +18,10 @@
 //   * forward: one CTA per 16^3 tile, each thread owns a (y,x) column of 16
 //     voxels in registers; per-Gaussian separable tables staged in shared
 //     memory; every voxel stored exactly once (no memset, no atomics);
-//   * backward: one CTA per tile, upstream tile staged in shared memory, one
-//     warp per (tile, Gaussian) pair, separable moment contraction
-//     (x in the loop, then y, then z), warp-shuffle reduction, partials
-//     written to the pair's original slot; combine sums slots in fixed order.
+//   * backward: one warp per Gaussian (lanes over z) reading the upstream
+//     straight from L2, separable moment contraction (x inner, y outer, z
+//     per lane), warp-shuffle reduction, f64 chain rule; no atomics, no
+//     partial buffers, deterministic.
 #include "common.cuh"
 
 namespace splatct {
@@ -52,9 +51,8 @@ struct FvrLayout {
     int64_t np;       // n * S
     int passes;
     int64_t sort_blocks;
-    size_t o_fp, o_gcount, o_k0, o_v0, o_k1, o_v1, o_tcount, o_tstart, o_hist, o_scan, o_part,
-        o_rec, o_cc, o_cstart, o_ctile, total;
-    int64_t bwd_grid;   // upper bound on backward (tile, chunk) work items
+    size_t o_fp, o_gcount, o_k0, o_v0, o_k1, o_v1, o_tcount, o_tstart, o_hist, o_scan, o_rec,
+        total;
     int final_buf;    // which (k,v) buffer holds the sorted result
 };
 
@@ -98,12 +96,7 @@ static FvrLayout make_layout(int64_t n, int w, int h, int c, int hx, int hy, int
     size_t sc1 = scan_temp_bytes(RADIX * (L.sort_blocks > 0 ? L.sort_blocks : 1));
     size_t sc2 = scan_temp_bytes(L.nt + 1);
     L.o_scan = take(sc1 > sc2 ? sc1 : sc2);
-    L.o_part = take(sizeof(float) * 5 * (size_t)L.np);
     L.o_rec = take(sizeof(GRec) * (size_t)n);
-    L.o_cc = take(sizeof(uint32_t) * (size_t)(L.nt + 1));
-    L.o_cstart = take(sizeof(uint32_t) * (size_t)(L.nt + 1));
-    L.bwd_grid = L.nt + L.np / 64 + 1;
-    L.o_ctile = take(sizeof(uint32_t) * (size_t)L.bwd_grid);
     L.total = off;
     L.final_buf = L.passes % 2;   // pass p reads buf p%2, writes (p+1)%2
     return L;
@@ -364,11 +357,6 @@ __global__ void __launch_bounds__(256) k_fvr_fwd(const GRec* __restrict__ rec, i
     }
 }
 
-// --------------------------------------------------------------------------
-// backward: one CTA per (tile, chunk of <= BWD_CHUNK pairs), one warp per pair
-// --------------------------------------------------------------------------
-constexpr int BWD_CHUNK = 64;
-
 // tstart[t] = lower_bound(sorted keys, t) for t in [0, nt]; keys >= nt are
 // the empty-slot sentinels, so tstart[nt] = number of real pairs.
 __global__ void k_tile_starts(const uint32_t* __restrict__ skeys, int64_t np, int64_t nt,
@@ -384,146 +372,131 @@ __global__ void k_tile_starts(const uint32_t* __restrict__ skeys, int64_t np, in
     tstart[t] = (uint32_t)lo;
 }
 
-__global__ void k_tile_chunks(const uint32_t* __restrict__ tstart, int64_t nt,
-                              uint32_t* __restrict__ cc, const int* halt) {
-    if (halted(halt)) return;
-    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (t > nt) return;
-    cc[t] = t < nt ? (tstart[t + 1] - tstart[t] + BWD_CHUNK - 1) / BWD_CHUNK : 0u;
-}
+// --------------------------------------------------------------------------
+// backward: one warp per Gaussian, lanes over z, upstream read straight from
+// global memory (the C2 upstream, 64 MB, stays L2-resident between the loss
+// and this kernel).  The box's columns are walked (y outer, x inner) with the
+// separable factors in per-warp shared tables, so per column a lane does one
+// coalesced load and three FMAs:
+//   C_k(y) = sum_x ex rx^k u(y,x,z)           (k = 0, 1, 2)
+//   A0 += ey C0, Ax += ey C1, Ay += ey ry C0, Ar += ey (C2 + ry^2 C0)
+// and the lane-private z factors ez, rz are applied once at the end.  One
+// warp sums a Gaussian's moments in a fixed order: deterministic, with no
+// partial buffer and no combine pass.  Gradient formulas: _kernels.py:132-205.
+// --------------------------------------------------------------------------
+constexpr int BG_WARPS = 8;
+constexpr int BG_XC = 17;   // box columns per register row (default box 17^3)
 
-// chunk k of tile t -> ctile[cstart[t] + k] = t (the backward's work list)
-__global__ void k_chunk_tiles(const uint32_t* __restrict__ cstart, int64_t nt,
-                              uint32_t* __restrict__ ctile, const int* halt) {
+__global__ void __launch_bounds__(32 * BG_WARPS, 2) k_fvr_bwd(const double* __restrict__ P, int64_t n,
+                                                          const int32_t* __restrict__ fp,
+                                                          const GRec* __restrict__ rec, int w,
+                                                          int h, int c, int zoff,
+                                                          const float* __restrict__ up,
+                                                          double* __restrict__ G,
+                                                          double* __restrict__ accum,
+                                                          const int* halt) {
     if (halted(halt)) return;
-    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (t >= nt) return;
-    for (uint32_t k = cstart[t]; k < cstart[t + 1]; ++k) ctile[k] = (uint32_t)t;
-}
-
-__global__ void __launch_bounds__(256) k_fvr_bwd(const GRec* __restrict__ rec, int w, int h, int c,
-                                                 int zoff, int hx, int hy, int hz, int ntx,
-                                                 int nty, int64_t nt, int S,
-                                                 const uint32_t* __restrict__ tstart,
-                                                 const uint32_t* __restrict__ cstart,
-                                                 const uint32_t* __restrict__ ctile,
-                                                 const uint32_t* __restrict__ svals,
-                                                 const float* __restrict__ up,
-                                                 float* __restrict__ part, const int* halt) {
-    if (halted(halt)) return;
-    __shared__ float sup[TT][TT][TT + 1];     // upstream tile [y][x][z], padded
-    __shared__ float4 zt[8][TT];              // per warp: {ez, ez*rz, ez*rz^2, -}
-    __shared__ float2 xt[8][TT], yt[8][TT];   // per warp: {e, r}
-    const uint32_t b = blockIdx.x;
-    if (b >= cstart[nt]) return;
-    const int64_t t = ctile[b];
-    const uint32_t beg = tstart[t] + (b - cstart[t]) * BWD_CHUNK;
-    const uint32_t end = min(beg + BWD_CHUNK, tstart[t + 1]);
-    const int txi = (int)(t % ntx), tyi = (int)((t / ntx) % nty), tzi = (int)(t / ((int64_t)ntx * nty));
-    const int x0 = txi * TT, y0 = tyi * TT, z0 = tzi * TT;
-    for (int e = threadIdx.x; e < TT * TT * TT; e += blockDim.x) {
-        const int z = e % TT, x = (e / TT) % TT, y = e / (TT * TT);
-        const int gx = x0 + x, gy = y0 + y, gz = z0 + z;
-        float u = 0.f;
-        if (gx < w && gy < h && gz < c) u = up[((int64_t)gy * w + gx) * c + gz];
-        sup[y][x][z] = u;
-    }
-    __syncthreads();
+    __shared__ float xt[3][BG_WARPS][32];   // ex, ex rx, ex rx^2
+    __shared__ float2 yt[BG_WARPS][32];   // {ey, ry}
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (uint32_t j = beg + wid; j < end; j += blockDim.x / 32) {
-        const uint32_t orig = svals[j];
-        const GRec r = rec[orig >> S];   // S = log2(slots per Gaussian)
-        {   // separable tables (zero outside box, tile and local volume)
-            const int l = lane & (TT - 1);
-            if (lane < TT) {
-                const int bx = x0 + l - r.fx;
-                const float rx = (float)bx - r.dx;
-                const bool okx = x0 + l < w && bx <= hx && bx >= -hx;
-                xt[wid][l] = make_float2(okx ? exp2f(-r.inv2 * rx * rx) : 0.f, rx);
-                const int bz = z0 + l + zoff - r.fz;
-                const float rz = (float)bz - r.dz;
-                const bool okz = z0 + l < c && bz <= hz && bz >= -hz;
-                const float ez = okz ? exp2f(-r.inv2 * rz * rz) : 0.f;
-                zt[wid][l] = make_float4(ez, ez * rz, ez * rz * rz, 0.f);
-            } else {
-                const int by = y0 + l - r.fy;
-                const float ry = (float)by - r.dy;
-                const bool oky = y0 + l < h && by <= hy && by >= -hy;
-                yt[wid][l] = make_float2(oky ? exp2f(-r.inv2 * ry * ry) : 0.f, ry);
+    const int64_t i = blockIdx.x * (int64_t)BG_WARPS + wid;
+    if (i >= n) return;   // warp-uniform: only warp-level syncs below
+    const int xlo = fp[6 * i], xhi = fp[6 * i + 1], ylo = fp[6 * i + 2], yhi = fp[6 * i + 3];
+    const int zlo = fp[6 * i + 4], zhi = fp[6 * i + 5];
+    float S0 = 0.f, Sx = 0.f, Sy = 0.f, Sz = 0.f, S2 = 0.f;
+    if (xlo <= xhi && ylo <= yhi && zlo <= zhi) {
+        const GRec r = rec[i];
+        for (int zc = zlo; zc <= zhi; zc += 32) {
+            const int z = zc + lane;
+            const bool zok = z <= zhi;
+            const float rz = (float)(z + zoff - r.fz) - r.dz;
+            const float ez = zok ? exp2f(-r.inv2 * rz * rz) : 0.f;
+            const float* ubase = up + (zok ? z : zlo);
+            float A0 = 0.f, Ax = 0.f, Ay = 0.f, Ar = 0.f;
+            for (int yc = ylo; yc <= yhi; yc += 32) {
+                const int ny = min(32, yhi - yc + 1);
+                for (int xc = xlo; xc <= xhi; xc += BG_XC) {
+                    const int nx = min(BG_XC, xhi - xc + 1);
+                    __syncwarp();   // previous chunk's table reads are done
+                    {
+                        const float ry = (float)(yc + lane - r.fy) - r.dy;
+                        yt[wid][lane] = make_float2(lane < ny ? exp2f(-r.inv2 * ry * ry) : 0.f, ry);
+                        const float rx = (float)(xc + lane - r.fx) - r.dx;
+                        const float ex = lane < nx ? exp2f(-r.inv2 * rx * rx) : 0.f;
+                        xt[0][wid][lane] = ex;
+                        xt[1][wid][lane] = ex * rx;
+                        xt[2][wid][lane] = ex * rx * rx;
+                    }
+                    __syncwarp();
+                    // a whole row (<= BG_XC columns) of loads is issued at once and
+                    // the next row is prefetched while this one is consumed.
+                    // Columns beyond nx re-read column nx-1 (valid memory, L1 hit)
+                    // and meet a zero weight, so the loads need no k-predicate.
+                    float wx0[BG_XC], wx1[BG_XC], wx2[BG_XC];
+                    uint32_t coff[BG_XC];
+#pragma unroll
+                    for (int k = 0; k < BG_XC; ++k) {
+                        wx0[k] = xt[0][wid][k];
+                        wx1[k] = xt[1][wid][k];
+                        wx2[k] = xt[2][wid][k];
+                        coff[k] = (uint32_t)min(k, nx - 1) * (uint32_t)c;
+                    }
+                    const float* row = ubase + ((int64_t)yc * w + xc) * c;
+                    const int64_t rstride = (int64_t)w * c;
+                    float ua[BG_XC], ub[BG_XC];
+#define BG_LOAD(U)                                                        \
+    _Pragma("unroll") for (int k = 0; k < BG_XC; ++k) U[k] = zok ? __ldg(row + coff[k]) : 0.f;
+#define BG_CONSUME(U, YI)                                                 \
+    {                                                                     \
+        float C0 = 0.f, C1 = 0.f, C2 = 0.f;                               \
+        _Pragma("unroll") for (int k = 0; k < BG_XC; ++k) {               \
+            C0 = fmaf(wx0[k], U[k], C0);                                  \
+            C1 = fmaf(wx1[k], U[k], C1);                                  \
+            C2 = fmaf(wx2[k], U[k], C2);                                  \
+        }                                                                 \
+        const float2 ey = yt[wid][YI];                                    \
+        A0 = fmaf(ey.x, C0, A0);                                          \
+        Ax = fmaf(ey.x, C1, Ax);                                          \
+        Ay = fmaf(ey.x * ey.y, C0, Ay);                                   \
+        Ar = fmaf(ey.x, fmaf(ey.y * ey.y, C0, C2), Ar);                   \
+    }
+                    BG_LOAD(ua);
+                    for (int yi = 0; yi < ny; yi += 2) {
+                        const bool more = yi + 1 < ny;
+                        if (more) { row += rstride; BG_LOAD(ub); }
+                        BG_CONSUME(ua, yi);
+                        if (!more) break;
+                        if (yi + 2 < ny) { row += rstride; BG_LOAD(ua); }
+                        BG_CONSUME(ub, yi + 1);
+                    }
+#undef BG_LOAD
+#undef BG_CONSUME
+                }
             }
-        }
-        __syncwarp();
-        // box intersect tile (tile-local, uniform across the warp)
-        const int xlo = max(r.fx - hx - x0, 0), xhi = min(r.fx + hx - x0, TT - 1);
-        const int ylo = max(r.fy - hy - y0, 0), yhi = min(r.fy + hy - y0, TT - 1);
-        const int zlo = max(r.fz - hz - zoff - z0, 0), zhi = min(r.fz + hz - zoff - z0, TT - 1);
-        const int lx = xhi - xlo + 1;
-        const int ncols = lx * (yhi - ylo + 1);
-        const uint32_t magic = (65536u + (uint32_t)lx - 1u) / (uint32_t)lx;   // c / lx for c < 256
-        float S0 = 0.f, Sx = 0.f, Sy = 0.f, Sz = 0.f, S2 = 0.f;
-        for (int c0 = 0; c0 < ncols; c0 += 32) {
-            const int cc = c0 + lane;
-            const bool valid = cc < ncols;
-            const int yo = (int)(((uint32_t)(valid ? cc : 0) * magic) >> 16);
-            const int y = ylo + yo, x = xlo + (valid ? cc : 0) - yo * lx;
-            const float* col = &sup[y][x][0];
-            float q0 = 0.f, q1 = 0.f, q2 = 0.f;
-            for (int z = zlo; z <= zhi; ++z) {   // z contraction: u * {ez, ez rz, ez rz^2}
-                const float4 t4 = zt[wid][z];
-                const float u = col[z];
-                q0 = fmaf(u, t4.x, q0);
-                q1 = fmaf(u, t4.y, q1);
-                q2 = fmaf(u, t4.z, q2);
-            }
-            const float2 ex = xt[wid][x], ey = yt[wid][y];
-            const float wv = valid ? ex.x * ey.x : 0.f;
-            const float wq = wv * q0;
-            S0 += wq;
-            Sx = fmaf(wq, ex.y, Sx);
-            Sy = fmaf(wq, ey.y, Sy);
-            Sz = fmaf(wv, q1, Sz);
-            S2 = fmaf(wq, fmaf(ex.y, ex.y, ey.y * ey.y), fmaf(wv, q2, S2));
-        }
-        __syncwarp();
-        S0 = warp_sum(S0);
-        Sx = warp_sum(Sx);
-        Sy = warp_sum(Sy);
-        Sz = warp_sum(Sz);
-        S2 = warp_sum(S2);
-        if (lane == 0) {
-            float* o = part + (size_t)orig * 5;
-            o[0] = S0; o[1] = Sx; o[2] = Sy; o[3] = Sz; o[4] = S2;
+            S0 = fmaf(ez, A0, S0);
+            Sx = fmaf(ez, Ax, Sx);
+            Sy = fmaf(ez, Ay, Sy);
+            Sz = fmaf(ez * rz, A0, Sz);
+            S2 = fmaf(ez, fmaf(rz * rz, A0, Ar), S2);
         }
     }
-}
-
-__global__ void k_fvr_combine(const double* __restrict__ P, int64_t n, int S,
-                              const int32_t* __restrict__ gcount, const float* __restrict__ part,
-                              double* __restrict__ G, double* __restrict__ accum,
-                              const int* halt) {
-    if (halted(halt)) return;
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    double s0 = 0, sx = 0, sy = 0, sz = 0, s2 = 0;
-    const int cnt = gcount[i];
-    const float* p = part + (size_t)i * S * 5;
-    for (int k = 0; k < cnt; ++k) {
-        s0 += p[5 * k + 0];
-        sx += p[5 * k + 1];
-        sy += p[5 * k + 2];
-        sz += p[5 * k + 3];
-        s2 += p[5 * k + 4];
+    S0 = warp_sum(S0);
+    Sx = warp_sum(Sx);
+    Sy = warp_sum(Sy);
+    Sz = warp_sum(Sz);
+    S2 = warp_sum(S2);
+    if (lane == 0) {   // chain rule in f64 (fvr.py:227-273)
+        const double amp = P[4 * n + i], sg = P[3 * n + i];
+        const double inv_s2 = 1.0 / (sg * sg), inv_s3 = inv_s2 / sg;
+        const double k2 = amp * inv_s2;
+        const double gx = k2 * Sx, gy = k2 * Sy, gz = k2 * Sz;
+        G[i] = gx;
+        G[n + i] = gy;
+        G[2 * n + i] = gz;
+        G[3 * n + i] = amp * inv_s3 * S2;
+        G[4 * n + i] = S0;
+        if (accum) accum[i] += sqrt(gx * gx + gy * gy + gz * gz);
     }
-    const double amp = P[4 * n + i], sg = P[3 * n + i];
-    const double inv_s2 = 1.0 / (sg * sg), inv_s3 = inv_s2 / sg;
-    const double k2 = amp * inv_s2;
-    const double gx = k2 * sx, gy = k2 * sy, gz = k2 * sz;
-    G[i] = gx;
-    G[n + i] = gy;
-    G[2 * n + i] = gz;
-    G[3 * n + i] = amp * inv_s3 * s2;
-    G[4 * n + i] = s0;
-    if (accum) accum[i] += sqrt(gx * gx + gy * gy + gz * gz);
 }
 
 __global__ void k_grad_norm_accum(const double* __restrict__ G, int64_t n,
@@ -600,16 +573,6 @@ int splatct_fvr_bin(const double* params, int64_t n, int w, int h, int c, int z0
             at<uint32_t>(ws, L.o_tstart), halt);
         SPLATCT_LAUNCH_CK();
     }
-    // backward work items: ceil(pairs / BWD_CHUNK) chunks per tile
-    k_tile_chunks<<<(unsigned)((L.nt + 1 + 255) / 256), 256, 0, s>>>(
-        at<uint32_t>(ws, L.o_tstart), L.nt, at<uint32_t>(ws, L.o_cc), halt);
-    SPLATCT_LAUNCH_CK();
-    if (int e = exclusive_scan_u32(at<uint32_t>(ws, L.o_cc), at<uint32_t>(ws, L.o_cstart),
-                                   L.nt + 1, at<void>(ws, L.o_scan), s))
-        return e;
-    k_chunk_tiles<<<(unsigned)((L.nt + 255) / 256), 256, 0, s>>>(
-        at<uint32_t>(ws, L.o_cstart), L.nt, at<uint32_t>(ws, L.o_ctile), halt);
-    SPLATCT_LAUNCH_CK();
     return SPLATCT_OK;
 }
 
@@ -636,16 +599,9 @@ int splatct_fvr_backward(const double* params, int64_t n, int w, int h, int c, i
     if (int e = check_args(n, w, h, c, hx, hy, hz, ws_bytes, L)) return e;
     if (n == 0) return SPLATCT_OK;
     cudaStream_t s = as_stream(stream);
-    const size_t vo = L.final_buf ? L.o_v1 : L.o_v0;
-    float* part = at<float>(ws, L.o_part);
-    k_fvr_bwd<<<(unsigned)L.bwd_grid, 256, 0, s>>>(
-        at<GRec>(ws, L.o_rec), w, h, c, z0, hx, hy, hz, L.ntx, L.nty, L.nt, L.Sl,
-        at<uint32_t>(ws, L.o_tstart), at<uint32_t>(ws, L.o_cstart), at<uint32_t>(ws, L.o_ctile),
-        at<uint32_t>(ws, vo), up_yxz,
-        part, halt);
-    SPLATCT_LAUNCH_CK();
-    k_fvr_combine<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
-        params, n, L.S, at<int32_t>(ws, L.o_gcount), part, grads, accum, halt);
+    k_fvr_bwd<<<(unsigned)((n + BG_WARPS - 1) / BG_WARPS), 32 * BG_WARPS, 0, s>>>(
+        params, n, at<int32_t>(ws, L.o_fp), at<GRec>(ws, L.o_rec), w, h, c, z0, up_yxz, grads,
+        accum, halt);
     SPLATCT_LAUNCH_CK();
     return SPLATCT_OK;
 }
