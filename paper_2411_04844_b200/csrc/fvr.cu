@@ -243,9 +243,23 @@ __global__ void __launch_bounds__(SORT_NT) k_radix_scatter(
 }
 
 // --------------------------------------------------------------------------
-// forward: one CTA per tile, thread = (y, x) column of 16 voxels
+// forward: one CTA per 16^3 tile on the tensor cores.
+//
+// Inside a tile the splat is a rank-K sum of separable factors,
+//   V[y][x][z] = sum_k ex_k[x] * (I_k ey_k[y] ez_k[z]),
+// i.e. a GEMM D[x][(y,z)] = A[x][k] B[k][(y,z)] with A = ex (16 x K) and B the
+// per-Gaussian outer product I ey (x) ez (K x 256).  Each warp owns two y rows
+// (N = 32 = 4 n8 tiles) and all 16 x (M = 16) and runs mma.sync m16n8k8 TF32
+// with the 3xTF32 split (a_hi b_hi + a_hi b_lo + a_lo b_hi, fp32 accumulate),
+// which keeps fp32-level accuracy (the volume target is 1e-5 relative L2).
+// The separable tables (I ey, ex, ez; zero outside box, tile and volume) are
+// built 32 Gaussians at a time in shared memory exactly as before; padding
+// rows are zero so partial k8 steps contribute nothing.  Accumulators go
+// through an XOR-swizzled shared-memory tile for coalesced stores.
 // --------------------------------------------------------------------------
 constexpr int FWD_BATCH = 32;   // Gaussians staged per round (8 threads each)
+// per Gaussian row: ex_hi[16] | ex_lo[16] (TF32 split, A operand) | I ey[16] | ez[16] | pad
+constexpr int TAB_STRIDE = 72;  // 72 mod 32 = 8: the four k rows of a fragment hit distinct banks
 
 // Separable weight of tile-local coordinate l on one axis (zero outside the
 // box or the local volume): exp(-(b - d)^2 inv2), b = coord - floor(mu).
@@ -257,85 +271,160 @@ __device__ __forceinline__ float tab_weight(int coord_local, int origin, int dim
     return exp2f(-inv2 * r * r);   // inv2 carries log2(e)
 }
 
-__global__ void __launch_bounds__(256) k_fvr_fwd(const GRec* __restrict__ rec, int w, int h, int c,
+// x = hi + lo with hi a TF32 value (round-half-away on the 13 dropped bits;
+// inputs are finite and >= 0) and lo exact in fp32 (the MMA reads its top 19
+// bits, |lo| <= 2^-11 |x|, so the split keeps ~2^-22 relative accuracy).
+__device__ __forceinline__ void tf32_split(float x, uint32_t& hi, uint32_t& lo) {
+    hi = (__float_as_uint(x) + 0x1000u) & 0xffffe000u;
+    lo = __float_as_uint(x - __uint_as_float(hi));
+}
+
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0,
+                                         uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+        "{%8,%9}, {%0,%1,%2,%3};\n"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__global__ void __launch_bounds__(256, 4) k_fvr_fwd(const GRec* __restrict__ rec, int w, int h, int c,
                                                  int zoff, int hx, int hy, int hz, int ntx,
                                                  int nty, int64_t nt, int S,
                                                  const uint32_t* __restrict__ tstart,
                                                  const uint32_t* __restrict__ svals,
                                                  float* __restrict__ vol,
-                                                 unsigned int* __restrict__ counter,
+                                                 unsigned int* __restrict__ counter, int fetch,
                                                  const int* halt) {
     if (halted(halt)) return;
-    __shared__ __align__(16) float tab[FWD_BATCH][3][TT];
-    __shared__ __align__(16) float4 sacc[TT * TT][TT / 4];   // store transpose
-    const int tx = threadIdx.x & (TT - 1), ty = threadIdx.x / TT;
+    __shared__ __align__(16) float tab[FWD_BATCH * TAB_STRIDE];
+    __shared__ __align__(16) float4 sacc[TT * TT][TT / 4];   // [y*16+x][z/4], swizzled
     __shared__ int64_t s_next;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int g = lane >> 2, t4 = lane & 3;        // mma fragment coordinates
+    const int r0 = 2 * wid;                        // this warp's two tile rows (y)
     const int ntz = (int)(nt / ((int64_t)ntx * nty));
     // persistent CTAs fetch tiles dynamically (uneven per-tile cost); tiles are
     // visited z-fastest so consecutive fetches write adjacent 64 B column
     // segments (HBM-friendly for the all-zero tiles of sparse volumes)
+    // `fetch` consecutive tiles are claimed per counter bump (1 for dense
+    // volumes, up to 32 for sparse ones where most tiles are empty zero-stores)
     for (;;) {
     __syncthreads();
-    if (threadIdx.x == 0) s_next = (int64_t)atomicAdd(counter, 1u);
+    if (threadIdx.x == 0) s_next = (int64_t)atomicAdd(counter, (unsigned)fetch);
     __syncthreads();
-    const int64_t k = s_next;
-    if (k >= nt) break;
-    const int tzi = (int)(k % ntz);
-    const int64_t rest = k / ntz;
-    const int txi = (int)(rest % ntx), tyi = (int)(rest / ntx);
+    const int64_t kc = s_next;
+    if (kc >= nt) break;
+    const int kend = (int)min(kc + fetch, nt);
+    for (int k32 = (int)kc; k32 < kend; ++k32) {   // nt < 2^31 (check_args)
+    const int tzi = k32 % ntz;
+    const int rest = k32 / ntz;
+    const int txi = rest % ntx, tyi = rest / ntx;
     const int64_t t = ((int64_t)tzi * nty + tyi) * ntx + txi;
     const int x0 = txi * TT, y0 = tyi * TT, z0 = tzi * TT;
     const uint32_t beg = tstart[t], end = tstart[t + 1];
-    float acc[TT];
+    const bool empty = beg == end;
+    float acc[4][4];
 #pragma unroll
-    for (int q = 0; q < TT; ++q) acc[q] = 0.f;
+    for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
     const int tg = threadIdx.x >> 3, tj = threadIdx.x & 7;   // table builder: Gaussian, part
 
+    // the next batch's Gaussian records are loaded while this batch's MMAs run
+    GRec rn;
+    if (beg + tg < end) rn = rec[svals[beg + tg] >> S];   // S = log2(slots per Gaussian)
     for (uint32_t b0 = beg; b0 < end; b0 += FWD_BATCH) {
         const int nb = (int)min((uint32_t)FWD_BATCH, end - b0);
+        const int nk = (nb + 7) & ~7;
+        const GRec r = rn;
+        if (b0 + FWD_BATCH + tg < end) rn = rec[svals[b0 + FWD_BATCH + tg] >> S];
         __syncthreads();
-        if (tg < nb) {
-            const GRec r = rec[svals[b0 + tg] >> S];   // S = log2(slots per Gaussian)
+        if (tg < nk) {
+            float* row = tab + tg * TAB_STRIDE;
+            uint32_t* urow = reinterpret_cast<uint32_t*>(row);
+            if (tg < nb) {
 #pragma unroll
-            for (int k = 0; k < 3 * TT / 8; ++k) {
-                const int e = tj + 8 * k, a = e / TT, l = e % TT;   // compile-time a per k
-                float v;
-                if (a == 0) v = tab_weight(x0 + l, 0, w, r.fx, hx, r.dx, r.inv2);
-                else if (a == 1) v = tab_weight(y0 + l, 0, h, r.fy, hy, r.dy, r.inv2) * r.I;
-                else v = tab_weight(z0 + l, zoff, c, r.fz, hz, r.dz, r.inv2);
-                tab[tg][a][l] = v;
-            }
-        }
-        __syncthreads();
-        for (int g = 0; g < nb; ++g) {
-            const float cxy = tab[g][1][ty] * tab[g][0][tx];
-            if (cxy != 0.f) {
-                const float4* ez = reinterpret_cast<const float4*>(&tab[g][2][0]);
-#pragma unroll
-                for (int q = 0; q < TT / 4; ++q) {
-                    const float4 e4 = ez[q];
-                    acc[4 * q + 0] = fmaf(cxy, e4.x, acc[4 * q + 0]);
-                    acc[4 * q + 1] = fmaf(cxy, e4.y, acc[4 * q + 1]);
-                    acc[4 * q + 2] = fmaf(cxy, e4.z, acc[4 * q + 2]);
-                    acc[4 * q + 3] = fmaf(cxy, e4.w, acc[4 * q + 3]);
+                for (int q = 0; q < 3 * TT / 8; ++q) {
+                    const int e = tj + 8 * q, a = e / TT, l = e % TT;   // compile-time a per q
+                    if (a == 0) {
+                        uint32_t hi, lo;
+                        tf32_split(tab_weight(x0 + l, 0, w, r.fx, hx, r.dx, r.inv2), hi, lo);
+                        urow[l] = hi;
+                        urow[TT + l] = lo;
+                    } else if (a == 1) {
+                        row[2 * TT + l] = tab_weight(y0 + l, 0, h, r.fy, hy, r.dy, r.inv2) * r.I;
+                    } else {
+                        row[3 * TT + l] = tab_weight(z0 + l, zoff, c, r.fz, hz, r.dz, r.inv2);
+                    }
                 }
+            } else {
+#pragma unroll
+                for (int q = 0; q < 4 * TT / 8; ++q) row[tj + 8 * q] = 0.f;   // k8 padding
             }
         }
+        __syncthreads();
+        for (int k0 = 0; k0 < nk; k0 += 8) {
+            const float* ra = tab + (k0 + t4) * TAB_STRIDE;       // Gaussian k0 + t
+            const float* rb = tab + (k0 + t4 + 4) * TAB_STRIDE;   // Gaussian k0 + t + 4
+            const uint32_t* ua = reinterpret_cast<const uint32_t*>(ra);
+            const uint32_t* ub = reinterpret_cast<const uint32_t*>(rb);
+            // A[x][k] = ex_k[x], pre-split by the table builder
+            const uint32_t ah[4] = {ua[g], ua[g + 8], ub[g], ub[g + 8]};
+            const uint32_t al[4] = {ua[TT + g], ua[TT + g + 8], ub[TT + g], ub[TT + g + 8]};
+            const float ya0 = ra[2 * TT + r0], ya1 = ra[2 * TT + r0 + 1];
+            const float yb0 = rb[2 * TT + r0], yb1 = rb[2 * TT + r0 + 1];
+            const float za0 = ra[3 * TT + g], za1 = ra[3 * TT + g + 8];
+            const float zb0 = rb[3 * TT + g], zb1 = rb[3 * TT + g + 8];
+            // n-tile j: row r0 + (j >> 1), z = (j & 1) * 8 + n
+            uint32_t bh[4][2], bl[4][2];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float ya = (j >> 1) ? ya1 : ya0, yb = (j >> 1) ? yb1 : yb0;
+                const float za = (j & 1) ? za1 : za0, zb = (j & 1) ? zb1 : zb0;
+                tf32_split(ya * za, bh[j][0], bl[j][0]);   // B[k=t][n=g]
+                tf32_split(yb * zb, bh[j][1], bl[j][1]);   // B[k=t+4][n=g]
+            }
+            // each k8 step accumulates from zero (small terms first) and is
+            // added to the fp32 accumulators with round-to-nearest: the tensor
+            // core's truncating accumulation then only biases one step's
+            // partial sum, not the tile's running total.  The four n-tiles'
+            // chains are interleaved so consecutive HMMAs are independent.
+            float d[4][4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) d[j][0] = d[j][1] = d[j][2] = d[j][3] = 0.f;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) mma_tf32(d[j], al, bh[j][0], bh[j][1]);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) mma_tf32(d[j], ah, bl[j][0], bl[j][1]);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) mma_tf32(d[j], ah, bh[j][0], bh[j][1]);
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc[j][q] += d[j][q];
+        }
+    }
+    if (!empty) {   // accumulators -> swizzled [column][z] tile
+        float* sf = reinterpret_cast<float*>(sacc);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int y = r0 + (j >> 1);
+            const int z = (j & 1) * 8 + 2 * t4;
+            const int q = z >> 2, hf = z & 3;   // float4 chunk, offset 0 or 2
+#pragma unroll
+            for (int hx8 = 0; hx8 < 2; ++hx8) {
+                const int col = y * TT + g + 8 * hx8;
+                float2* dst = reinterpret_cast<float2*>(
+                    sf + (col * 4 + (q ^ ((col >> 1) & 3))) * 4 + hf);
+                *dst = make_float2(acc[j][2 * hx8], acc[j][2 * hx8 + 1]);
+            }
+        }
+        __syncthreads();
     }
     // store: the tile's 256 columns x 64 B are written 8 columns per warp
     // instruction (4 lanes x 16 B per column) instead of 32 scattered
-    // half-sectors; non-empty tiles transpose through shared memory
-    // (XOR-swizzled, conflict-free), empty tiles store zeros directly
+    // half-sectors; empty tiles store zeros directly
     if ((c & 3) == 0 && z0 + TT <= c) {
-        const bool empty = beg == end;
-        if (!empty) {
-#pragma unroll
-            for (int q = 0; q < TT / 4; ++q)
-                sacc[threadIdx.x][q ^ ((threadIdx.x >> 1) & 3)] =
-                    make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
-            __syncthreads();
-        }
-        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, ch = lane & 3;
+        const int ch = lane & 3;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const int cid = wid * 32 + i * 8 + (lane >> 2);
@@ -345,16 +434,24 @@ __global__ void __launch_bounds__(256) k_fvr_fwd(const GRec* __restrict__ rec, i
             if (x < w && y < h)
                 *reinterpret_cast<float4*>(vol + ((int64_t)y * w + x) * c + z0 + 4 * ch) = v;
         }
-    } else {
-        const int x = x0 + tx, y = y0 + ty;
+    } else {   // ragged z tile: one column per thread, scalar stores
+        const int cid = threadIdx.x;
+        const int x = x0 + (cid & (TT - 1)), y = y0 + cid / TT;
         if (x < w && y < h) {
             float* col = vol + ((int64_t)y * w + x) * c;
 #pragma unroll
-            for (int k = 0; k < TT; ++k)
-                if (z0 + k < c) col[z0 + k] = acc[k];
+            for (int q = 0; q < TT / 4; ++q) {
+                const float4 v = empty ? make_float4(0.f, 0.f, 0.f, 0.f)
+                                       : sacc[cid][q ^ ((cid >> 1) & 3)];
+                if (z0 + 4 * q + 0 < c) col[z0 + 4 * q + 0] = v.x;
+                if (z0 + 4 * q + 1 < c) col[z0 + 4 * q + 1] = v.y;
+                if (z0 + 4 * q + 2 < c) col[z0 + 4 * q + 2] = v.z;
+                if (z0 + 4 * q + 3 < c) col[z0 + 4 * q + 3] = v.w;
+            }
         }
     }
-    }
+    }   // tile
+    }   // fetch
 }
 
 // tstart[t] = lower_bound(sorted keys, t) for t in [0, nt]; keys >= nt are
@@ -582,12 +679,14 @@ int splatct_fvr_forward(const double* params, int64_t n, int w, int h, int c, in
     FvrLayout L = make_layout(n, w, h, c, hx, hy, hz);
     if (int e = check_args(n, w, h, c, hx, hy, hz, ws_bytes, L)) return e;
     const size_t vo = L.final_buf ? L.o_v1 : L.o_v0;
-    const int64_t grid = L.nt < 148 * 8 ? L.nt : 148 * 8;   // persistent over tiles
+    const int64_t grid = L.nt < 148 * 4 ? L.nt : 148 * 4;   // persistent: 4 CTAs/SM resident
+    int64_t fetch = L.nt / (8 * grid);                       // >= 8 claims per CTA
+    fetch = fetch < 1 ? 1 : (fetch > 32 ? 32 : fetch);
     unsigned int* counter = at<uint32_t>(ws, L.o_tcount);
     SPLATCT_CK(cudaMemsetAsync(counter, 0, sizeof(unsigned int), as_stream(stream)));
     k_fvr_fwd<<<(unsigned)grid, 256, 0, as_stream(stream)>>>(
         at<GRec>(ws, L.o_rec), w, h, c, z0, hx, hy, hz, L.ntx, L.nty, L.nt, L.Sl,
-        at<uint32_t>(ws, L.o_tstart), at<uint32_t>(ws, vo), vol_yxz, counter, halt);
+        at<uint32_t>(ws, L.o_tstart), at<uint32_t>(ws, vo), vol_yxz, counter, (int)fetch, halt);
     SPLATCT_LAUNCH_CK();
     return SPLATCT_OK;
 }

@@ -251,7 +251,7 @@ def test_fbp_and_init_cloud(traj_golden):
 
 # --------------------------------------------------------------------------- z-slab emulation
 def test_slab_emulation_matches_full():
-    """Voxelizer + TV-fused adjoint on G z-slabs of one device == unsharded."""
+    """Voxelizer + TV-fused adjoint on G z-slabs of one device match unsharded (fp32 rounding)."""
     dev = D.require_cuda()
     dims = (48, 40, 64)
     w, h, c = dims
@@ -279,7 +279,9 @@ def test_slab_emulation_matches_full():
         v = plan.new_volume()
         plan.bin(params)
         plan.forward(params, v)
-        assert torch.equal(v, vfull[:, :, s.z0:s.z0 + s.c_local])
+        # slab tiles group Gaussians into different tensor-core k8 steps than
+        # the full volume's tiles, so sums agree to fp32 rounding, not bitwise
+        assert rel_l2(v.cpu().numpy(), vfull[:, :, s.z0:s.z0 + s.c_local].cpu().numpy()) < 1e-6
         gl = torch.empty_like(gfull)
         plan.backward(params, up[:, :, s.z0:s.z0 + s.c_local].contiguous(), gl)
         gsum += gl
@@ -287,7 +289,7 @@ def test_slab_emulation_matches_full():
         hi = vfull[:, :, s.z0 + s.c_local].contiguous() if s.z0 + s.c_local < c else None
         dl = op.adjoint(gs[:, :, s.z0:s.z0 + s.c_local].contiguous(), vol=v, halo_lo=lo,
                         halo_hi=hi, lambda_tv=0.7, tv_count=float(w * h * c))
-        assert torch.equal(dl, dl_full[:, :, s.z0:s.z0 + s.c_local])
+        assert rel_l2(dl.cpu().numpy(), dl_full[:, :, s.z0:s.z0 + s.c_local].cpu().numpy()) < 1e-6
     assert rel_l2(gsum.cpu().numpy(), gfull.cpu().numpy()) < 1e-6
 
 
