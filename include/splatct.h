@@ -258,6 +258,42 @@ int splatct_fbp_backproject(const double* filtered, const double* cos_t, const d
                             int m, int n, int p, int w, int h, double spacing, double dbeta,
                             int is_fan, double rs, float* out_yxz, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Cone-beam extension (no reference counterpart, parity
+ * unpinned; model in cone.cu / DESIGN.md "Cone beam").  Setup, once per
+ * geometry: splatct_cone_count (per-column sample counts -> rptr[m*nu+1],
+ * 1/L per column; returns the total) and splatct_cone_fill (16-byte samples);
+ * splatct_cone_entry_count / _fill transpose them into per-pixel entry lists
+ * (16 B each, eptr[w*h+1]) for the gather adjoint.  Per iteration:
+ * splatct_cone_forward (vol yxz slab [h][w][c_local] -> sino (m*nu, nv);
+ * zc = (c_global-1)/2 - z0, so slab results are partial projections that sum
+ * to the full one) and splatct_cone_adjoint (exact transpose; gscaled is an
+ * (m*nu*nv) f32 scratch; accumulate != 0 adds into out).
+ * ------------------------------------------------------------------------- */
+int splatct_cone_setup_scratch_bytes(int m, int nu, int w, int h, size_t* bytes);
+int splatct_cone_count(const double* cos_t, const double* sin_t, int m, int nu, double su,
+                       double rs, double rd, int w, int h, double step, int64_t* rptr,
+                       float* inv_len, void* scratch, size_t scratch_bytes, int64_t* nsamples,
+                       void* stream);
+int splatct_cone_fill(const double* cos_t, const double* sin_t, int m, int nu, double su,
+                      double rs, double rd, int w, int h, double step, const int64_t* rptr,
+                      void* samples, void* stream);
+int splatct_cone_entry_count(const void* samples, const int64_t* rptr, int nrays, int w, int h,
+                             int64_t* eptr, void* scratch, size_t scratch_bytes,
+                             int64_t* nentries, void* stream);
+int splatct_cone_entry_scratch_bytes(int64_t nentries, int w, int h, size_t* bytes);
+int splatct_cone_entry_fill(const void* samples, const int64_t* rptr, int nrays, int w, int h,
+                            const int64_t* eptr, int64_t nentries, void* entries, void* scratch,
+                            size_t scratch_bytes, void* stream);
+int splatct_cone_forward(const void* samples, const int64_t* rptr, const float* inv_len,
+                         int nrays, int nv, double sv, double step, int w, int h, int c_local,
+                         double zc, const float* vol_yxz, float* sino, const int* halt,
+                         void* stream);
+int splatct_cone_adjoint(const void* entries, const int64_t* eptr, const float* inv_len,
+                         int nrays, int nv, double sv, double step, int w, int h, int c_local,
+                         double zc, const float* gsino, float* gscaled, float* out_yxz,
+                         int accumulate, const int* halt, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,91 @@
+"""CPU oracle of the cone-beam extension -- TEST INFRASTRUCTURE ONLY.
+
+PARITY UNPINNED: the reference has no cone-beam geometry (SPEC.md:15,249,255
+exclude it).  This module restates the model documented in
+DESIGN.md "Cone beam" / csrc/cone.cu in plain Python + numpy (f64) so the CUDA
+kernels can be checked on small cases.  The xy part is the reference's fan ray
+(_kernels.py:208-259: _clip_ray, _ray_geometry; samples at t0 + (k + 1/2) step,
+n_steps = int((t1 - t0) / step)); detector row v samples z(t) = cz + v t / L
+(L = |P - S|) with trilinear interpolation, zero outside the volume, scaled by
+step * sqrt(1 + (v / L)^2).  It is pinned indirectly by the tests: the centre
+row of an odd-c volume equals the reference-pinned fan projection of slice
+cz, the adjoint passes the dot test, and a ball's chord lengths match.
+Only tests/ import it.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+
+def _clip_ray(px, py, dx, dy, t0, t1, xlo, xhi, ylo, yhi):
+    # _kernels.py:208-229
+    if dx != 0.0:
+        ta, tb = (xlo - px) / dx, (xhi - px) / dx
+        if ta > tb:
+            ta, tb = tb, ta
+        t0, t1 = max(t0, ta), min(t1, tb)
+    elif px < xlo or px > xhi:
+        return 1.0, 0.0
+    if dy != 0.0:
+        ta, tb = (ylo - py) / dy, (yhi - py) / dy
+        if ta > tb:
+            ta, tb = tb, ta
+        t0, t1 = max(t0, ta), min(t1, tb)
+    elif py < ylo or py > yhi:
+        return 1.0, 0.0
+    return t0, t1
+
+
+def column_samples(cos_a, sin_a, u, rs, rd, w, h, step):
+    """Fan ray of detector column u (_kernels.py:232-259) -> samples (x, y, tau), L."""
+    cx, cy = 0.5 * (w - 1), 0.5 * (h - 1)
+    sx, sy = cx - rs * cos_a, cy - rs * sin_a
+    px, py = cx + rd * cos_a - u * sin_a, cy + rd * sin_a + u * cos_a
+    dx, dy = px - sx, py - sy
+    length = math.sqrt(dx * dx + dy * dy)
+    dx, dy = dx / length, dy / length
+    t0, t1 = _clip_ray(sx, sy, dx, dy, 0.0, length, -1.0, float(w), -1.0, float(h))
+    out = []
+    if t1 > t0:
+        for k in range(int((t1 - t0) / step)):
+            t = t0 + (k + 0.5) * step
+            out.append((sx + t * dx, sy + t * dy, t / length))
+    return out, length
+
+
+def _tri(vol_zyx, x, y, z):
+    c, h, w = vol_zyx.shape
+    x0, y0, z0 = math.floor(x), math.floor(y), math.floor(z)
+    fx, fy, fz = x - x0, y - y0, z - z0
+    acc = 0.0
+    for dz, wz in ((0, 1 - fz), (1, fz)):
+        for dyy, wy in ((0, 1 - fy), (1, fy)):
+            for dxx, wx in ((0, 1 - fx), (1, fx)):
+                xi, yi, zi = x0 + dxx, y0 + dyy, z0 + dz
+                if 0 <= xi < w and 0 <= yi < h and 0 <= zi < c:
+                    acc += wx * wy * wz * vol_zyx[zi, yi, xi]
+    return acc
+
+
+def cone_forward(vol_zyx, geom, step=0.5, z0=0, c_global=None):
+    """vol slab (c_local, h, w) -> partial cone projections (m, nu, nv), f64."""
+    vol = np.asarray(vol_zyx, np.float64)
+    cl, h, w = vol.shape
+    cg = cl if c_global is None else int(c_global)
+    zc = 0.5 * (cg - 1) - z0
+    m, nu, nv = geom.n_views, geom.n_detectors, geom.n_rows
+    sv, su = float(geom.row_spacing), float(geom.detector_spacing)
+    rs, rd = float(geom.source_to_origin), float(geom.origin_to_detector)
+    out = np.zeros((m, nu, nv))
+    for a, ang in enumerate(np.asarray(geom.view_angles, np.float64)):
+        ca, sa = math.cos(ang), math.sin(ang)
+        for d in range(nu):
+            u = (d - 0.5 * (nu - 1)) * su
+            samples, length = column_samples(ca, sa, u, rs, rd, w, h, step)
+            for dv in range(nv):
+                v = (dv - 0.5 * (nv - 1)) * sv
+                acc = sum(_tri(vol, x, y, zc + v * tau) for x, y, tau in samples)
+                out[a, d, dv] = acc * step * math.sqrt(1.0 + (v / length) ** 2)
+    return out

@@ -67,6 +67,20 @@ SIGNATURES: dict[str, list] = {
     "splatct_fbp_filter": [c_vp, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp],
     "splatct_fbp_backproject": [c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_i32, c_f64,
                                 c_f64, c_i32, c_f64, c_vp, c_vp],
+    "splatct_cone_setup_scratch_bytes": [c_i32, c_i32, c_i32, c_i32, c_szp],
+    "splatct_cone_count": [c_vp, c_vp, c_i32, c_i32, c_f64, c_f64, c_f64, c_i32, c_i32, c_f64,
+                           c_vp, c_vp, c_vp, c_sz, c_i64p, c_vp],
+    "splatct_cone_fill": [c_vp, c_vp, c_i32, c_i32, c_f64, c_f64, c_f64, c_i32, c_i32, c_f64,
+                          c_vp, c_vp, c_vp],
+    "splatct_cone_entry_count": [c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_vp, c_sz, c_i64p,
+                                 c_vp],
+    "splatct_cone_entry_scratch_bytes": [c_i64, c_i32, c_i32, c_szp],
+    "splatct_cone_entry_fill": [c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_i64, c_vp, c_vp, c_sz,
+                                c_vp],
+    "splatct_cone_forward": [c_vp, c_vp, c_vp, c_i32, c_i32, c_f64, c_f64, c_i32, c_i32, c_i32,
+                             c_f64, c_vp, c_vp, c_vp, c_vp],
+    "splatct_cone_adjoint": [c_vp, c_vp, c_vp, c_i32, c_i32, c_f64, c_f64, c_i32, c_i32, c_i32,
+                             c_f64, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp],
 }
 
 SQDIFF_BLOCKS = 592   # SPLATCT_SQDIFF_BLOCKS

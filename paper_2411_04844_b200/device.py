@@ -253,8 +253,8 @@ class ProjectorOperator:
         return b
 
     def forward(self, vol: torch.Tensor, out: torch.Tensor | None = None, halt=None,
-                blocked: bool | None = None):
-        """vol (h, w, c) -> sinogram (m, n, c)."""
+                blocked: bool | None = None, z0: int = 0):
+        """vol (h, w, c) -> sinogram (m, n, c); per-slice, so a slab's z0 is irrelevant."""
         c = int(vol.shape[2])
         if out is None:
             out = torch.empty((self.m, self.n_det, c), dtype=torch.float32, device=vol.device)
@@ -269,9 +269,10 @@ class ProjectorOperator:
 
     def adjoint(self, gsino: torch.Tensor, out: torch.Tensor | None = None, vol=None,
                 halo_lo=None, halo_hi=None, lambda_tv: float = 0.0, tv_count: float = 1.0,
-                tv_partial=None, halt=None, blocked: bool | None = None):
+                tv_partial=None, halt=None, blocked: bool | None = None, z0: int = 0,
+                c_local: int | None = None):
         """sinogram (m, n, c) -> volume (h, w, c) [+ lambda_tv * TV subgradient of vol]."""
-        c = int(gsino.shape[2])
+        c = int(c_local if c_local is not None else gsino.shape[2])
         if out is None:
             out = torch.empty((self.h, self.w, c), dtype=torch.float32, device=gsino.device)
         args = (ptr(gsino), ptr(vol), ptr(halo_lo), ptr(halo_hi), float(lambda_tv),
@@ -310,6 +311,126 @@ def projector_for(geom: ScanGeometry, w: int, h: int, step: float = 0.5,
     else:
         _PROJ_CACHE.move_to_end(key)
     return op
+
+
+class ConeOperator:
+    """Circular cone-beam projector and its exact adjoint (cone.cu; SURVEY
+    §8(f) N3, parity unpinned).  The per-column xy samples and their
+    per-pixel transpose are built once per geometry; ``z0`` selects the slab
+    of a ``c_global``-slice volume, whose projections are partial line
+    integrals (summed across slabs by the caller).  Sinogram (m, nu, nv)."""
+
+    def __init__(self, geom: ScanGeometry, w: int, h: int, c_global: int, step: float = 0.5,
+                 device=None):
+        if geom.variant != "cone":
+            raise ValueError("ConeOperator needs a cone geometry")
+        self.device = require_cuda(device)
+        geom.check_volume((w, h, c_global))
+        self.geom = geom
+        self.w, self.h, self.c_global = int(w), int(h), int(c_global)
+        self.m, self.n_det, self.nv = int(geom.n_views), int(geom.n_detectors), int(geom.n_rows)
+        self.sv = float(geom.row_spacing)
+        self.step = float(step)
+        self.n_rays = self.m * self.n_det
+        ang = np.asarray(geom.view_angles, np.float64)
+        dev = self.device
+        self.cos_t = torch.from_numpy(np.cos(ang)).to(dev)
+        self.sin_t = torch.from_numpy(np.sin(ang)).to(dev)
+        g = (ptr(self.cos_t), ptr(self.sin_t), self.m, self.n_det,
+             float(geom.detector_spacing), float(geom.source_to_origin),
+             float(geom.origin_to_detector), self.w, self.h, self.step)
+        sb = size_query("splatct_cone_setup_scratch_bytes", self.m, self.n_det, self.w, self.h)
+        scratch = torch.empty(sb, dtype=torch.uint8, device=dev)
+        self.rptr = torch.empty(self.n_rays + 1, dtype=torch.int64, device=dev)
+        self.inv_len = torch.empty(self.n_rays, dtype=torch.float32, device=dev)
+        ns = ctypes.c_int64(0)
+        call("splatct_cone_count", *g, ptr(self.rptr), ptr(self.inv_len), ptr(scratch), sb,
+             ctypes.byref(ns), stream_handle())
+        self.n_samples = int(ns.value)
+        self.samples = torch.empty((max(self.n_samples, 1), 4), dtype=torch.float32, device=dev)
+        call("splatct_cone_fill", *g, ptr(self.rptr), ptr(self.samples), stream_handle())
+        self.eptr = torch.empty(self.w * self.h + 1, dtype=torch.int64, device=dev)
+        ne = ctypes.c_int64(0)
+        call("splatct_cone_entry_count", ptr(self.samples), ptr(self.rptr), self.n_rays, self.w,
+             self.h, ptr(self.eptr), ptr(scratch), sb, ctypes.byref(ne), stream_handle())
+        self.n_entries = int(ne.value)
+        self.entries = torch.empty((max(self.n_entries, 1), 4), dtype=torch.float32, device=dev)
+        eb = size_query("splatct_cone_entry_scratch_bytes", self.n_entries, self.w, self.h)
+        escr = torch.empty(eb, dtype=torch.uint8, device=dev)
+        call("splatct_cone_entry_fill", ptr(self.samples), ptr(self.rptr), self.n_rays, self.w,
+             self.h, ptr(self.eptr), self.n_entries, ptr(self.entries), ptr(escr), eb,
+             stream_handle())
+        del scratch, escr
+        self.gscaled = torch.empty(self.n_rays * self.nv, dtype=torch.float32, device=dev)
+        self.tvop = tv_operator(self.w, self.h, dev)
+
+    @property
+    def matrix_bytes(self) -> int:
+        return 16 * (self.n_samples + self.n_entries) + 8 * (self.n_rays + self.w * self.h + 2)
+
+    def _zc(self, z0: int) -> float:
+        return 0.5 * (self.c_global - 1) - float(z0)
+
+    def forward(self, vol: torch.Tensor, out: torch.Tensor | None = None, halt=None, z0: int = 0,
+                blocked=None):
+        """vol slab (h, w, c_local) -> partial cone projections (m, nu, nv)."""
+        cl = int(vol.shape[2])
+        if out is None:
+            out = torch.empty((self.m, self.n_det, self.nv), dtype=torch.float32,
+                              device=vol.device)
+        call("splatct_cone_forward", ptr(self.samples), ptr(self.rptr), ptr(self.inv_len),
+             self.n_rays, self.nv, self.sv, self.step, self.w, self.h, cl, self._zc(z0),
+             ptr(vol), ptr(out), ptr(halt), stream_handle())
+        return out
+
+    def adjoint(self, gsino: torch.Tensor, out: torch.Tensor | None = None, vol=None,
+                halo_lo=None, halo_hi=None, lambda_tv: float = 0.0, tv_count: float = 1.0,
+                tv_partial=None, halt=None, z0: int = 0, c_local: int | None = None,
+                blocked=None):
+        """(m, nu, nv) -> volume slab (h, w, c_local) [+ lambda_tv * TV subgradient of vol]."""
+        cl = int(c_local if c_local is not None else
+                 (out.shape[2] if out is not None else
+                  (vol.shape[2] if vol is not None else self.c_global)))
+        if out is None:
+            out = torch.empty((self.h, self.w, cl), dtype=torch.float32, device=gsino.device)
+        acc = 0
+        if vol is not None and lambda_tv > 0:
+            # TV first (the empty-operator adjoint writes out = l3 dTV and the
+            # TV value partials), then the cone adjoint accumulates into it
+            self.tvop.adjoint(gsino, out, vol=vol, halo_lo=halo_lo, halo_hi=halo_hi,
+                              lambda_tv=lambda_tv, tv_count=tv_count, tv_partial=tv_partial,
+                              halt=halt, blocked=False, c_local=cl)
+            acc = 1
+        call("splatct_cone_adjoint", ptr(self.entries), ptr(self.eptr), ptr(self.inv_len),
+             self.n_rays, self.nv, self.sv, self.step, self.w, self.h, cl, self._zc(z0),
+             ptr(gsino), ptr(self.gscaled), ptr(out), acc, ptr(halt), stream_handle())
+        return out
+
+
+_CONE_CACHE: "OrderedDict[tuple, ConeOperator]" = OrderedDict()
+
+
+def cone_projector_for(geom: ScanGeometry, w: int, h: int, c_global: int, step: float = 0.5,
+                       device=None) -> ConeOperator:
+    dev = require_cuda(device)
+    key = (geom.key(), int(w), int(h), int(c_global), float(step), str(dev))
+    op = _CONE_CACHE.get(key)
+    if op is None:
+        op = ConeOperator(geom, w, h, c_global, step, dev)
+        _CONE_CACHE[key] = op
+        while len(_CONE_CACHE) > 2:
+            _CONE_CACHE.popitem(last=False)
+    else:
+        _CONE_CACHE.move_to_end(key)
+    return op
+
+
+def operator_for(geom: ScanGeometry, w: int, h: int, c_global: int, step: float = 0.5,
+                 device=None):
+    """The projector of a geometry: per-slice (ProjectorOperator) or cone."""
+    if geom.variant == "cone":
+        return cone_projector_for(geom, w, h, c_global, step, device)
+    return projector_for(geom, w, h, step, device)
 
 
 def tv_partial_len(w: int, h: int, c: int) -> int:

@@ -11,6 +11,12 @@ and SSIM are slab-local.  Exchanges per iteration:
   * all-reduce(sum) of the float64 [5, N] partial gradient block (a Gaussian
     whose box straddles a slab boundary gets contributions from two ranks).
 
+Cone beam ("partial projections summed"): rays cross slabs,
+so each rank projects its slab into partial line integrals of the FULL
+(m, nu, nv) sinogram and an all-reduce(sum) of the prediction completes them;
+every rank then evaluates the (replicated) projection loss -- counted once in
+the loss sums -- and back-projects dL/dpred onto its own slab.
+
 Adam then runs identically on every rank (replicated cloud).  The
 communicator is written against torch.distributed and works for NCCL on
 device tensors and for gloo on CPU tensors (tests/test_distributed.py).
@@ -136,7 +142,10 @@ def run_reconstruction_sharded(measured, geom, settings, init_cloud, comm=None,
     dims = tuple(int(v) for v in settings.dims)
     s = slab_bounds(dims[2], comm.world, comm.rank)
     dev = D.require_cuda()
-    local = np.ascontiguousarray(measured.views[:, :, s.z0:s.z0 + s.c_local])
+    # per-slice geometries: the rank's sinogram slab; cone beam: the full
+    # sinogram on every rank (partial projections are summed in the Trainer)
+    local = (np.ascontiguousarray(measured.views[:, :, s.z0:s.z0 + s.c_local])
+             if geom.per_slice else np.ascontiguousarray(measured.views))
     tr = Trainer(D.sino_to_device(local, dev), geom, dims, settings.box, settings.weights,
                  D.cloud_to_params(init_cloud, dev), lr0=settings.lr_initial,
                  lrf=settings.lr_final, max_iters=settings.max_iters, slab=s, comm=comm)

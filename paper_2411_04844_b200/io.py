@@ -130,6 +130,9 @@ def geometry_to_dict(geom: ScanGeometry) -> dict:
     if geom.source_to_origin is not None:
         d["source_to_origin"] = float(geom.source_to_origin)
         d["origin_to_detector"] = float(geom.origin_to_detector)
+    if geom.n_rows is not None:
+        d["n_rows"] = int(geom.n_rows)
+        d["row_spacing"] = float(geom.row_spacing)
     return d
 
 
@@ -142,7 +145,7 @@ def geometry_from_dict(d: dict) -> ScanGeometry:
     if "view_angles" in d:
         ang = np.asarray(d["view_angles"], np.float64)
         return ScanGeometry(variant, m, n, spacing, ang, d.get("source_to_origin"),
-                            d.get("origin_to_detector"))
+                            d.get("origin_to_detector"), d.get("n_rows"), d.get("row_spacing"))
     start = float(d.get("angle_start", 0.0))
     extent = float(d.get("angle_extent", np.pi))
     if variant == "parallel":
@@ -150,4 +153,8 @@ def geometry_from_dict(d: dict) -> ScanGeometry:
     if variant == "fan":
         return ScanGeometry.fan(m, n, spacing, float(d["source_to_origin"]),
                                 float(d["origin_to_detector"]), start, extent)
+    if variant == "cone":
+        return ScanGeometry.cone(m, n, int(d["n_rows"]), spacing, float(d["source_to_origin"]),
+                                 float(d["origin_to_detector"]), d.get("row_spacing"), start,
+                                 float(d.get("angle_extent", 2 * np.pi)))
     raise ValidationError(f"unknown geometry variant {variant!r}")

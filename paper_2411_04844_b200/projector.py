@@ -21,7 +21,8 @@ from . import device as D
 from ._lib import call
 from .core import ScanGeometry, Sinogram, ValidationError, VolumeGrid
 
-__all__ = ["RaySamplingConfig", "add_noise", "back_project", "fbp", "forward_project"]
+__all__ = ["RaySamplingConfig", "add_noise", "back_project", "cone_init_volume", "fbp",
+           "forward_project"]
 
 
 @dataclass(frozen=True)
@@ -41,7 +42,7 @@ def forward_project(volume: VolumeGrid, geom: ScanGeometry,
     geom.check_volume(volume.dims)
     w, h, c = volume.dims
     dev = D.require_cuda()
-    op = D.projector_for(geom, w, h, sampling.step_length, dev)
+    op = D.operator_for(geom, w, h, c, sampling.step_length, dev)
     vol = D.zyx_to_yxz(volume.zyx, dev)
     sino = op.forward(vol)
     return Sinogram.from_views(sino.cpu().numpy())
@@ -59,14 +60,30 @@ def back_project(sino: Sinogram, geom: ScanGeometry, dims,
     if (m, n) != (geom.n_views, geom.n_detectors):
         raise ValidationError(f"sinogram dims {sino.dims} do not match geometry "
                               f"({geom.n_views} views x {geom.n_detectors} detectors)")
-    if p != c:
-        raise ValidationError(f"sinogram has {p} slices, volume has {c}")
+    if p != geom.sino_depth(c):
+        raise ValidationError(f"sinogram depth {p} does not match {geom.sino_depth(c)} "
+                              f"({geom.variant} geometry, volume has {c} slices)")
     geom.check_volume(dims)
     dev = D.require_cuda()
-    op = D.projector_for(geom, w, h, sampling.step_length, dev)
+    op = D.operator_for(geom, w, h, c, sampling.step_length, dev)
     g = D.sino_to_device(sino.views, dev)
-    out = op.adjoint(g)
+    out = op.adjoint(g, c_local=c)
     return VolumeGrid.from_zyx(D.yxz_to_zyx(out))
+
+
+def cone_init_volume(sino: Sinogram, geom: ScanGeometry, dims,
+                     sampling: RaySamplingConfig = RaySamplingConfig()) -> VolumeGrid:
+    """Initialiser volume for cone beam (the reference's FBP is per-slice only):
+    the normalised back projection A^T y / A^T A 1, clipped at 0."""
+    w, h, c = (int(v) for v in dims)
+    dev = D.require_cuda()
+    op = D.cone_projector_for(geom, w, h, c, sampling.step_length, dev)
+    bp = op.adjoint(D.sino_to_device(sino.views, dev), c_local=c)
+    norm = op.adjoint(op.forward(torch.ones((h, w, c), dtype=torch.float32, device=dev)),
+                      c_local=c)
+    vol = torch.where(norm > 1e-6 * norm.max(), bp / norm.clamp_min(1e-30),
+                      torch.zeros_like(bp)).clamp_min(0)
+    return VolumeGrid.from_zyx(D.yxz_to_zyx(vol))
 
 
 def _ramp_response(n_pad: int, spacing: float, window: str) -> np.ndarray:
@@ -143,6 +160,9 @@ def fbp(sino: Sinogram, geom: ScanGeometry, dims, filter_name: str = "ramp") -> 
     if m < 2:
         raise ValidationError("FBP needs at least 2 views")
     w, h, c = (int(v) for v in dims)
+    if not geom.per_slice:
+        raise ValidationError("FBP is per-slice (parallel / fan); cone beam initialises with "
+                              "cone_init_volume")
     if p != c:
         raise ValidationError(f"sinogram has {p} slices, volume has {c}")
     geom.check_volume(dims)

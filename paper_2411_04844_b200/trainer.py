@@ -72,15 +72,24 @@ class Trainer:
         self.comm = comm or NullComm()
         self.lr0, self.lrf, self.max_iters = float(lr0), float(lrf), int(max_iters)
         self.sigma_ceiling = 3.0 * box.extent
-        m, n, cl = (int(v) for v in measured.shape)
-        if cl != self.slab.c_local:
-            raise ValueError(f"measured slab has {cl} slices, slab owns {self.slab.c_local}")
+        m, n, p = (int(v) for v in measured.shape)
+        # per-slice geometries: the rank's sinogram slab mirrors its volume
+        # slab; cone beam: every rank holds the full (m, nu, nv) sinogram and
+        # its slab's projections are partial line integrals summed across
+        # ranks (the north star's partial-projection reduction)
+        self.per_slice = geom.per_slice
+        cl = self.slab.c_local
+        if self.per_slice and p != cl:
+            raise ValueError(f"measured slab has {p} slices, slab owns {cl}")
+        if not self.per_slice and p != geom.n_rows:
+            raise ValueError(f"cone sinogram has {p} rows, geometry has {geom.n_rows}")
+        self.p_global = self.slab.c_global if self.per_slice else p
         self.m, self.n = m, n
         self.meas = measured
         dev = self.device
-        self.op = D.projector_for(geom, self.w, self.h, step_length, dev)
-        self.loss = D.LossPlan(m, n, cl, dev)
-        self.pred = torch.empty((m, n, cl), dtype=torch.float32, device=dev)
+        self.op = D.operator_for(geom, self.w, self.h, self.slab.c_global, step_length, dev)
+        self.loss = D.LossPlan(m, n, p, dev)
+        self.pred = torch.empty((m, n, p), dtype=torch.float32, device=dev)
         self.gpred = torch.empty_like(self.pred)
         self.vol = torch.empty((self.h, self.w, cl), dtype=torch.float32, device=dev)
         self.dl = torch.empty_like(self.vol)
@@ -98,8 +107,8 @@ class Trainer:
         self.comm.allreduce_max_(lm)
         self.lmax = float(lm.item())
         cg = self.slab.c_global
-        self.l1_count = float(m * n * cg)
-        self.ssim_count = float(self.loss.valid * cg)
+        self.l1_count = float(m * n * self.p_global)
+        self.ssim_count = float(self.loss.valid * self.p_global)
         self.tv_count = float(self.w * self.h * cg)
         self.graph = None
         self._set_params(params, m1, m2, accum)
@@ -163,21 +172,28 @@ class Trainer:
     def iteration(self):
         lw = self.weights
         halt = self.halt
-        self.op.forward(self.vol, self.pred, halt)
+        z0 = self.slab.z0
+        self.op.forward(self.vol, self.pred, halt, z0=z0)
+        replicated = not self.per_slice and self.comm.world > 1
+        if replicated:
+            self.comm.allreduce_sum_(self.pred)   # partial cone projections -> full
         if lw.lambda1 > 0 or lw.lambda2 > 0:
             self.loss.fused(self.pred, self.meas, self.lmax, lw.lambda1, lw.lambda2,
-                            self.l1_count, float(self.slab.c_global), self.gpred, self.sums,
+                            self.l1_count, float(self.p_global), self.gpred, self.sums,
                             halt)
+            if replicated and self.comm.rank != 0:
+                self.sums[0:2].zero_()   # every rank holds the full loss: count it once
         else:
             self.gpred.zero_()
         if lw.lambda3 > 0:
             lo, hi = self.comm.halo(self.vol)
             self.op.adjoint(self.gpred, self.dl, vol=self.vol, halo_lo=lo, halo_hi=hi,
                             lambda_tv=lw.lambda3, tv_count=self.tv_count,
-                            tv_partial=self.tv_part, halt=halt)
+                            tv_partial=self.tv_part, halt=halt, z0=z0)
             D.reduce_sum(self.tv_part, self.sums[2:3])
         else:
-            self.op.adjoint(self.gpred, self.dl, halt=halt)
+            self.op.adjoint(self.gpred, self.dl, halt=halt, z0=z0,
+                            c_local=self.slab.c_local)
         self.comm.allreduce_sum_(self.sums)
         D.call("splatct_iter_finalize", D.ptr(self.sums), float(lw.lambda1), float(lw.lambda2),
                float(lw.lambda3), self.l1_count, self.ssim_count, self.tv_count, self.lr0,
