@@ -48,6 +48,11 @@ CONFIGS = {
     "c4": dict(dims=(512, 512, 512), n=400_000, views=100, n_det=1024, spacing=1.6, rs=1024.0,
                rd=1024.0, variant="fan", phantom="chest",
                label="C4: 512^3 chest phantom, 400k Gaussians, 100-view fan (1024 det/slice)"),
+    # true cone beam (parity unpinned): BASELINE configs[1] verbatim
+    "c2cone": dict(dims=(256, 256, 256), n=50_000, views=50, n_det=512, n_rows=512,
+                   spacing=1.6, rs=512.0, rd=512.0, variant="cone", phantom="chest",
+                   label="C2-cone: 256^3 chest phantom, 50k Gaussians, 50-view circular cone "
+                         "beam, 512x512 detector (pitch 1.6, rs=rd=512), box 17^3"),
 }
 
 
@@ -79,6 +84,9 @@ def make_problem(cfg):
     if cfg["variant"] == "fan":
         geom = core.ScanGeometry.fan(cfg["views"], cfg["n_det"], cfg["spacing"], cfg["rs"],
                                      cfg["rd"])
+    elif cfg["variant"] == "cone":
+        geom = core.ScanGeometry.cone(cfg["views"], cfg["n_det"], cfg["n_rows"], cfg["spacing"],
+                                      cfg["rs"], cfg["rd"])
     else:
         geom = core.ScanGeometry.parallel(cfg["views"], cfg["n_det"], cfg["spacing"])
     box = core.BoxConfig.for_dims(17, cfg["dims"])
@@ -167,13 +175,15 @@ def stage_profile(tr, iters):
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(names) + 1)]
         l0 = _lib.launch_count()
         ev[0].record(s)
-        tr.op.forward(tr.vol, tr.pred, tr.halt)
+        tr.op.forward(tr.vol, tr.pred, tr.halt, z0=tr.slab.z0)
+        if not tr.per_slice and tr.comm.world > 1:
+            tr.comm.allreduce_sum_(tr.pred)
         ev[1].record(s)
         tr.loss.fused(tr.pred, tr.meas, tr.lmax, lw.lambda1, lw.lambda2, tr.l1_count,
                       float(tr.slab.c_global), tr.gpred, tr.sums, tr.halt)
         ev[2].record(s)
         lo, hi = tr.comm.halo(tr.vol)
-        tr.op.adjoint(tr.gpred, tr.dl, vol=tr.vol, halo_lo=lo, halo_hi=hi,
+        tr.op.adjoint(tr.gpred, tr.dl, vol=tr.vol, halo_lo=lo, halo_hi=hi, z0=tr.slab.z0,
                       lambda_tv=lw.lambda3, tv_count=tr.tv_count, tv_partial=tr.tv_part,
                       halt=tr.halt)
         D.reduce_sum(tr.tv_part, tr.sums[2:3])
@@ -223,9 +233,13 @@ def run_b200(args, cfg):
     w, h, c = cfg["dims"]
     s = slab_bounds(c, world, rank)
     # measured projections of the phantom (same operator as the model)
-    op = D.projector_for(geom, w, h, 0.5, dev)
-    tslab = np.ascontiguousarray(truth.zyx[s.z0:s.z0 + s.c_local])
-    meas_local = op.forward(D.zyx_to_yxz(tslab, dev))
+    op = D.operator_for(geom, w, h, c, 0.5, dev)
+    cone = not geom.per_slice
+    if cone:   # rays cross slabs: every rank holds the full cone sinogram
+        meas_local = op.forward(D.zyx_to_yxz(np.ascontiguousarray(truth.zyx), dev))
+    else:
+        tslab = np.ascontiguousarray(truth.zyx[s.z0:s.z0 + s.c_local])
+        meas_local = op.forward(D.zyx_to_yxz(tslab, dev))
     params = D.cloud_to_params(cloud, dev)
     tr = Trainer(meas_local, geom, cfg["dims"], box, L.LossWeights(), params, max_iters=1000,
                  slab=s, comm=comm, trace_cap=args.warmup + args.steps + 16)
@@ -282,7 +296,7 @@ def run_b200(args, cfg):
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
     else:
-        meas_host = Sinogram.from_views(
+        meas_host = Sinogram.from_views(meas_local.cpu().numpy()) if cone else Sinogram.from_views(
             np.concatenate([op.forward(D.zyx_to_yxz(np.ascontiguousarray(
                 truth.zyx[b.z0:b.z0 + b.c_local]), dev)).cpu().numpy()
                 for b in [slab_bounds(c, world, r) for r in range(world)]], axis=2))
@@ -315,11 +329,14 @@ def run_b200(args, cfg):
     N = cfg["n"]
     cl = s.c_local
     vol_b = w * h * cl * 4
-    sino_l = m * n * cl * 4
-    nnz = op.nnz
+    sino_l = m * n * (cfg["n_rows"] if cone else cl) * 4
+    nnz = 0 if cone else op.nnz
     alg = {
-        "proj_forward": 8 * nnz + vol_b + sino_l,
-        "proj_adjoint_tv": 8 * nnz + sino_l + 2 * vol_b,
+        # cone: 16 B per column sample / per pixel entry, plus the adjoint's
+        # arc-length pre-scale of dL/dpred (read + write)
+        "proj_forward": (16 * op.n_samples if cone else 8 * nnz) + vol_b + sino_l,
+        "proj_adjoint_tv": ((16 * op.n_entries + 2 * sino_l) if cone else 8 * nnz)
+                           + sino_l + 2 * vol_b,
         "loss_fused": 3 * sino_l,
         "fvr_forward": 40 * N + vol_b,
         "fvr_backward": 96 * N + vol_b,
@@ -337,12 +354,15 @@ def run_b200(args, cfg):
     l1_bw = nsm * 128 * sm_mhz * 1e6 / 1e9       # GB/s, 128 B / clk / SM
     # gathered bytes through L1 per SpMM launch: every blocked entry reads a
     # c-float voxel / sinogram column and a 20 B (index, 4 weights) record
-    nb_f = op.fb[3] if op.fb else nnz
-    nb_a = op.ab[3] if op.ab else nnz
-    gath = {"proj_forward": nb_f * (cl * 4 + 20), "proj_adjoint_tv": nb_a * (cl * 4 + 20)}
+    gath = {}
+    if not cone:
+        nb_f = op.fb[3] if op.fb else nnz
+        nb_a = op.ab[3] if op.ab else nnz
+        gath = {"proj_forward": nb_f * (cl * 4 + 20), "proj_adjoint_tv": nb_a * (cl * 4 + 20)}
     vr_, vc_ = m - 10, n - 10
-    dp_ops = (m * vc_ * cl) * 77 + (vr_ * vc_ * cl) * 85 + (m * n * cl) * 76
-    traffic = load_traffic()
+    pl = cfg["n_rows"] if cone else cl
+    dp_ops = (m * vc_ * pl) * 77 + (vr_ * vc_ * pl) * 85 + (m * n * pl) * 76
+    traffic = load_traffic() if args.config == "c2" else {}   # profiled on C2
 
     def roof(name):
         a = alg[name] / (stages[name] * 1e-3) / 1e9
@@ -356,7 +376,7 @@ def run_b200(args, cfg):
             r["binding"] = {"bound": "fp32_fma", "achieved": contributions / sec,
                             "peak": fp32_fma, "unit": "contributions/s (1 FFMA each)",
                             "frac": round(contributions / sec / fp32_fma, 4)}
-        elif name.startswith("proj"):
+        elif name.startswith("proj") and name in gath:
             g = gath[name] / sec / 1e9
             r["binding"] = {"bound": "l1_gather", "achieved": round(g, 1), "peak": round(l1_bw, 1),
                             "unit": "GB/s", "frac": round(g / l1_bw, 4),
@@ -382,7 +402,9 @@ def run_b200(args, cfg):
                    "cache": "per-iteration working set (A, A^T, volume, sinograms) > 126 MB L2; "
                             "no flush",
                    "parallelism": f"zslab{world}", "cuda_graph": use_graph,
-                   "projector_nnz": nnz},
+                   **({"cone_column_entries": op.n_samples, "cone_pixel_entries": op.n_entries}
+                      if cone
+                      else {"projector_nnz": nnz})},
         "roofline": {**roof(dominant), "peak_source": peak_src},
         "kernels": {k: roof(k) for k in alg},
         "voxelize": {"fwd": roof("fvr_forward"), "bwd": roof("fvr_backward"),
@@ -395,7 +417,7 @@ def run_b200(args, cfg):
         "clocks": clocks,
         "last_loss": loss_last,
     }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not cone:
         v, dt, cores = cpu_reference_iters(cfg, args.cpu_iters, 0)
         out["cpu_baseline"] = {"value": round(v, 5), "unit": "iterations/s", "cores": cores,
                                "kind": "port",

@@ -261,14 +261,15 @@ int splatct_fbp_backproject(const double* filtered, const double* cos_t, const d
 /* ---------------------------------------------------------------------------
  * Cone-beam extension (no reference counterpart, parity
  * unpinned; model in cone.cu / DESIGN.md "Cone beam").  Setup, once per
- * geometry: splatct_cone_count (per-column sample counts -> rptr[m*nu+1],
- * 1/L per column; returns the total) and splatct_cone_fill (16-byte samples);
- * splatct_cone_entry_count / _fill transpose them into per-pixel entry lists
- * (16 B each, eptr[w*h+1]) for the gather adjoint.  Per iteration:
- * splatct_cone_forward (vol yxz slab [h][w][c_local] -> sino (m*nu, nv);
- * zc = (c_global-1)/2 - z0, so slab results are partial projections that sum
- * to the full one) and splatct_cone_adjoint (exact transpose; gscaled is an
- * (m*nu*nv) f32 scratch; accumulate != 0 adds into out).
+ * geometry: splatct_cone_count (per-column merged-entry counts -> cptr[m*nu+1],
+ * 1/L per column; returns the total) and splatct_cone_fill (16-byte column
+ * entries {pixel, w, tau}); splatct_cone_entry_count / _fill transpose them
+ * into per-pixel entry lists (16 B each, eptr[w*h+1]) for the gather adjoint.
+ * Per iteration: splatct_cone_forward (vol yxz slab [h][w][c_local] -> sino
+ * (m*nu, nv); zc = (c_global-1)/2 - z0, so slab results are partial
+ * projections that sum to the full one) and splatct_cone_adjoint (exact
+ * transpose; gscaled is an (m*nu*nv) f32 scratch; accumulate != 0 adds into
+ * out).
  * ------------------------------------------------------------------------- */
 int splatct_cone_setup_scratch_bytes(int m, int nu, int w, int h, size_t* bytes);
 int splatct_cone_count(const double* cos_t, const double* sin_t, int m, int nu, double su,

@@ -5,11 +5,14 @@ exclude it).  This module restates the model documented in
 DESIGN.md "Cone beam" / csrc/cone.cu in plain Python + numpy (f64) so the CUDA
 kernels can be checked on small cases.  The xy part is the reference's fan ray
 (_kernels.py:208-259: _clip_ray, _ray_geometry; samples at t0 + (k + 1/2) step,
-n_steps = int((t1 - t0) / step)); detector row v samples z(t) = cz + v t / L
-(L = |P - S|) with trilinear interpolation, zero outside the volume, scaled by
-step * sqrt(1 + (v / L)^2).  It is pinned indirectly by the tests: the centre
-row of an odd-c volume equals the reference-pinned fan projection of slice
-cz, the adjoint passes the dot test, and a ball's chord lengths match.
+n_steps = int((t1 - t0) / step)) with its bilinear weights merged per pixel
+(as the per-slice operator does); each (column, pixel) entry carries the
+weight-averaged sample distance tbar, and detector row v reads the pixel's
+z-column at z = cz + v tbar / L (L = |P - S|) by linear interpolation, zero
+outside the volume, scaled by step * sqrt(1 + (v / L)^2).  It is pinned
+indirectly by the tests: the centre row of an odd-c volume equals the
+reference-pinned fan projection of slice cz, the adjoint passes the dot test,
+and a ball's chord lengths match.
 Only tests/ import it.
 """
 from __future__ import annotations
@@ -55,17 +58,29 @@ def column_samples(cos_a, sin_a, u, rs, rd, w, h, step):
     return out, length
 
 
-def _tri(vol_zyx, x, y, z):
-    c, h, w = vol_zyx.shape
-    x0, y0, z0 = math.floor(x), math.floor(y), math.floor(z)
-    fx, fy, fz = x - x0, y - y0, z - z0
+def column_entries(samples, w, h):
+    """Merge the bilinear taps of a column's samples (x, y, tau) per pixel ->
+    {(x, y): (W, W tau)} (march_ray's merge, _kernels.py:279-300 taps)."""
+    ent = {}
+    for x, y, tau in samples:
+        x0, y0 = math.floor(x), math.floor(y)
+        fx, fy = x - x0, y - y0
+        for xi, yi, wq in ((x0, y0, (1 - fx) * (1 - fy)), (x0 + 1, y0, fx * (1 - fy)),
+                           (x0, y0 + 1, (1 - fx) * fy), (x0 + 1, y0 + 1, fx * fy)):
+            if 0 <= xi < w and 0 <= yi < h and wq != 0.0:
+                a, b = ent.get((xi, yi), (0.0, 0.0))
+                ent[(xi, yi)] = (a + wq, b + wq * tau)
+    return ent
+
+
+def _lerp(col, z):
+    z0 = math.floor(z)
+    fz = z - z0
     acc = 0.0
-    for dz, wz in ((0, 1 - fz), (1, fz)):
-        for dyy, wy in ((0, 1 - fy), (1, fy)):
-            for dxx, wx in ((0, 1 - fx), (1, fx)):
-                xi, yi, zi = x0 + dxx, y0 + dyy, z0 + dz
-                if 0 <= xi < w and 0 <= yi < h and 0 <= zi < c:
-                    acc += wx * wy * wz * vol_zyx[zi, yi, xi]
+    if 0 <= z0 < col.shape[0]:
+        acc += (1 - fz) * col[z0]
+    if 0 <= z0 + 1 < col.shape[0]:
+        acc += fz * col[z0 + 1]
     return acc
 
 
@@ -84,8 +99,10 @@ def cone_forward(vol_zyx, geom, step=0.5, z0=0, c_global=None):
         for d in range(nu):
             u = (d - 0.5 * (nu - 1)) * su
             samples, length = column_samples(ca, sa, u, rs, rd, w, h, step)
+            ent = column_entries(samples, w, h)
             for dv in range(nv):
                 v = (dv - 0.5 * (nv - 1)) * sv
-                acc = sum(_tri(vol, x, y, zc + v * tau) for x, y, tau in samples)
+                acc = sum(W * _lerp(vol[:, yi, xi], zc + v * (WT / W))
+                          for (xi, yi), (W, WT) in ent.items())
                 out[a, d, dv] = acc * step * math.sqrt(1.0 + (v / length) ** 2)
     return out

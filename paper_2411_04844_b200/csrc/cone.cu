@@ -2,139 +2,105 @@
 // N3: named by the north star, absent from the reference, parity unpinned).
 //
 // Model.  For view a and detector column u the xy
-// path is the reference's fan ray (_kernels.py:232-259 via raygeom.cuh):
-// source S, unit direction d, length L = |P - S|, clipped to [-1,w]x[-1,h],
-// samples t_k = t0 + (k + 1/2) step, k < int((t1 - t0) / step).  Detector row
-// v (height v at the detector) sees z(t) = cz + v t / L, so every row of a
-// column shares the xy samples and bilinear weights; the value is
-//     p(a, u, v) = step sqrt(1 + (v/L)^2) sum_k trilinear(vol; x_k, y_k, z_k)
-// with zero outside the volume.  The centre row (v = 0) of an odd-c volume is
-// exactly the fan projection of slice cz.
+// path is the reference's fan ray (_kernels.py:232-259; raygeom.cuh): source
+// S, unit direction, length L = |P - S|, clipped to [-1,w]x[-1,h], samples
+// t_k = t0 + (k + 1/2) step, k < int((t1 - t0) / step), bilinear weights
+// merged per pixel exactly as the per-slice operator does (march_ray).  Each
+// merged (column, pixel) entry also carries tau = tbar / L, tbar the
+// weight-averaged sample distance of its samples.  Detector row v (height v
+// at the detector) reads the pixel's z-column at z = cz + v tau (linear
+// interpolation, zero outside the volume):
+//     p(a, u, v) = step sqrt(1 + (v/L)^2) sum_e w_e lerp(vol[pix_e], cz + v tau_e)
+// The centre row (v = 0) of an odd-c volume is therefore exactly the fan
+// projection of slice cz (same merged weights).
 //
-// B200 design.  The f64 xy march runs once per geometry into a per-column
-// sample list {pixel, fx, fy, tau = t/L} (16 B).  Forward: one warp per
-// (column, 32 rows), lanes over rows: each sample is a shared-memory
-// broadcast, its four bilinear corners are warp-uniform, and the lanes'
-// z-taps hit a short contiguous stretch of the corner's (yxz) z-column.
-// Adjoint: the exact transpose as a gather (no atomics, deterministic): the
-// samples are transposed once into per-pixel entry lists {column, tau, w_xy}
-// sorted by (column, sample, corner); one warp per (pixel, 32 slices), each
-// lane finds the detector rows whose z-taps land on its slice (the same f32
-// z = fma(v, tau, zc) as the forward) and accumulates w_xy w_z g.
-// Slabs: zc is the centre height in the slab's local coordinates, so
-// per-slab projections are partial line integrals that sum to the full one.
+// B200 design.  Setup (once per geometry): the f64 march into a
+// column-major entry list {pixel, w, tau} and its per-pixel transpose
+// {column, w, tau, 1/tau} sorted by (column, entry).  Forward: one warp per
+// (column, 32 detector rows), lanes over rows; every entry is a shared-memory
+// broadcast and the lanes' two z-taps hit a short contiguous stretch of the
+// pixel's (yxz) z-column.  Adjoint: one warp per (pixel, z window), lanes
+// over the detector rows of each entry (coalesced dL/dpred loads); each row
+// adds its two tap contributions into per-warp shared-memory z accumulators,
+// one per (row residue mod P, tap) class with P tau sv > 1, so no two lanes
+// of an instruction touch the same word: plain read-modify-writes, fixed
+// order, deterministic, no atomics.  Slabs: zc is the centre height in the
+// slab's local coordinates, so slab projections are partial line integrals
+// that sum to the full one.
 #include "common.cuh"
 #include "raygeom.cuh"
 
 namespace splatct {
 
-struct __align__(16) ConeSample {
-    int pix;        // ((y0 + 1) << 16) | (x0 + 1), x0 in [-1, w], y0 in [-1, h]
-    float fx, fy;   // bilinear fractions
-    float tau;      // t / L
+struct __align__(16) ConeColEntry {   // column-major (forward)
+    int pix;
+    float w;        // merged bilinear weight of the pixel's samples
+    float tau;      // tbar / L
+    float pad;
 };
 
-struct __align__(16) ConeEntry {
+struct __align__(16) ConeEntry {      // pixel-major (adjoint)
     uint32_t col;   // detector column (view * nu + u)
-    float tau, wxy, pad;
+    float w, tau;
+    float inv_tau;  // 1 / tau (row-range setup of the adjoint)
 };
 
-struct ConeGeom {
-    const double* cos_t;
-    const double* sin_t;
-    int m, nu;
-    double su, step, rs, rd;
-    int w, h;
-};
-
-__device__ __forceinline__ void cone_column(const ConeGeom& g, int r, double& ox, double& oy,
-                                            double& dx, double& dy, double& t0, double& t1,
-                                            double& len) {
-    const int a = r / g.nu, d = r % g.nu;
-    const double cx = 0.5 * (g.w - 1), cy = 0.5 * (g.h - 1);
-    const double u = (d - 0.5 * (g.nu - 1)) * g.su;
-    ray_geometry(g.cos_t[a], g.sin_t[a], u, true, g.rs, g.rd, cx, cy, g.w, g.h, ox, oy, dx, dy,
-                 t0, t1);
-    const double ddx = (g.rd + g.rs) * g.cos_t[a] - u * g.sin_t[a];
-    const double ddy = (g.rd + g.rs) * g.sin_t[a] + u * g.cos_t[a];
-    len = sqrt(ddx * ddx + ddy * ddy);
+__device__ __forceinline__ double column_length(const Geom& g, int r) {
+    const int a = r / g.n_det, d = r % g.n_det;
+    const double u = (d - 0.5 * (g.n_det - 1)) * g.spacing;
+    const double dx = (g.rd + g.rs) * g.cos_t[a] - u * g.sin_t[a];
+    const double dy = (g.rd + g.rs) * g.sin_t[a] + u * g.cos_t[a];
+    return sqrt(dx * dx + dy * dy);
 }
 
-__global__ void k_cone_count(ConeGeom g, int64_t* __restrict__ cnt, float* __restrict__ invL) {
+__global__ void k_cone_count(Geom g, int64_t* __restrict__ cnt, float* __restrict__ invL) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= g.m * g.nu) return;
-    double ox, oy, dx, dy, t0, t1, len;
-    cone_column(g, r, ox, oy, dx, dy, t0, t1, len);
-    cnt[r] = t1 > t0 ? (int64_t)((t1 - t0) / g.step) : 0;
-    invL[r] = (float)(1.0 / len);
+    if (r >= g.m * g.n_det) return;
+    int64_t c = 0;
+    march_ray(g, r, [&](int, double, double) { ++c; });
+    cnt[r] = c;
+    invL[r] = (float)(1.0 / column_length(g, r));
 }
 
-__global__ void k_cone_fill(ConeGeom g, const int64_t* __restrict__ rptr,
-                            ConeSample* __restrict__ S) {
+__global__ void k_cone_fill(Geom g, const int64_t* __restrict__ cptr,
+                            ConeColEntry* __restrict__ CE) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= g.m * g.nu) return;
-    double ox, oy, dx, dy, t0, t1, len;
-    cone_column(g, r, ox, oy, dx, dy, t0, t1, len);
-    const int64_t b = rptr[r], ns = rptr[r + 1] - b;
-    for (int64_t k = 0; k < ns; ++k) {
-        const double t = t0 + (k + 0.5) * g.step;
-        const double sx = ox + t * dx, sy = oy + t * dy;
-        const double fx0 = floor(sx), fy0 = floor(sy);
-        ConeSample s;
-        s.pix = (((int)fy0 + 1) << 16) | ((int)fx0 + 1);
-        s.fx = (float)(sx - fx0);
-        s.fy = (float)(sy - fy0);
-        s.tau = (float)(t / len);
-        S[b + k] = s;
-    }
+    if (r >= g.m * g.n_det) return;
+    const double inv_len = 1.0 / column_length(g, r);
+    int64_t j = cptr[r];
+    march_ray(g, r, [&](int pix, double w, double wt) {
+        ConeColEntry e;
+        e.pix = pix;
+        e.w = (float)w;
+        e.tau = (float)(wt / w * inv_len);
+        e.pad = 0.f;
+        CE[j++] = e;
+    });
 }
 
-__device__ __forceinline__ float corner_weight(int q, float fx, float fy) {
-    return __fmul_rn((q & 1) ? fx : 1.f - fx, (q & 2) ? fy : 1.f - fy);
+// Pixel-major transpose: count, atomic fill, per-pixel rank sort by the
+// entry's global index (column-major order) -- deterministic gather order.
+__global__ void k_cone_ecount(const ConeColEntry* __restrict__ CE, int64_t n,
+                              unsigned long long* __restrict__ cnt) {
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j < n) atomicAdd(&cnt[CE[j].pix], 1ull);
 }
 
-// Pixel-entry transpose: count, atomic fill, per-pixel rank sort by key
-// (column, sample, corner) -- deterministic order for the gather.
-__global__ void k_cone_ecount(const ConeSample* __restrict__ S, const int64_t* __restrict__ rptr,
-                              int nrays, int w, int h, unsigned long long* __restrict__ cnt) {
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= nrays) return;
-    for (int64_t j = rptr[r]; j < rptr[r + 1]; ++j) {
-        const ConeSample s = S[j];
-        const int x0 = (s.pix & 0xffff) - 1, y0 = (s.pix >> 16) - 1;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int px = x0 + (q & 1), py = y0 + (q >> 1);
-            if (px < 0 || px >= w || py < 0 || py >= h || corner_weight(q, s.fx, s.fy) == 0.f)
-                continue;
-            atomicAdd(&cnt[(int64_t)py * w + px], 1ull);
-        }
-    }
-}
-
-__global__ void k_cone_efill(const ConeSample* __restrict__ S, const int64_t* __restrict__ rptr,
-                             int nrays, int w, int h, unsigned long long* __restrict__ cursor,
+__global__ void k_cone_efill(const ConeColEntry* __restrict__ CE, const int64_t* __restrict__ cptr,
+                             int nrays, unsigned long long* __restrict__ cursor,
                              ConeEntry* __restrict__ E, uint64_t* __restrict__ key) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= nrays) return;
-    const int64_t b = rptr[r];
-    for (int64_t j = b; j < rptr[r + 1]; ++j) {
-        const ConeSample s = S[j];
-        const int x0 = (s.pix & 0xffff) - 1, y0 = (s.pix >> 16) - 1;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int px = x0 + (q & 1), py = y0 + (q >> 1);
-            const float wq = corner_weight(q, s.fx, s.fy);
-            if (px < 0 || px >= w || py < 0 || py >= h || wq == 0.f) continue;
-            const unsigned long long pos = atomicAdd(&cursor[(int64_t)py * w + px], 1ull);
-            ConeEntry e;
-            e.col = (uint32_t)r;
-            e.tau = s.tau;
-            e.wxy = wq;
-            e.pad = 0.f;
-            E[pos] = e;
-            key[pos] = ((uint64_t)r << 34) | ((uint64_t)(j - b) << 2) | (uint64_t)q;
-        }
+    for (int64_t j = cptr[r]; j < cptr[r + 1]; ++j) {
+        const ConeColEntry c = CE[j];
+        const unsigned long long pos = atomicAdd(&cursor[c.pix], 1ull);
+        ConeEntry e;
+        e.col = (uint32_t)r;
+        e.w = c.w;
+        e.tau = c.tau;
+        e.inv_tau = 1.f / c.tau;
+        E[pos] = e;
+        key[pos] = (uint64_t)j;
     }
 }
 
@@ -159,24 +125,26 @@ __global__ void k_cone_esort(int64_t npix, const int64_t* __restrict__ eptr,
 constexpr int CONE_WARPS = 8;
 
 __global__ void __launch_bounds__(32 * CONE_WARPS) k_cone_fwd(
-    const ConeSample* __restrict__ S, const int64_t* __restrict__ rptr,
-    const float* __restrict__ invL, int nrays, int nv, float sv, float step, int w, int h, int cl,
-    float zc, const float* __restrict__ vol, float* __restrict__ sino, const int* halt) {
+    const ConeColEntry* __restrict__ CE, const int64_t* __restrict__ cptr,
+    const float* __restrict__ invL, int nrays, int nv, float sv, float step, int cl, float zc,
+    const float* __restrict__ vol, float* __restrict__ sino, const int* halt) {
     if (halted(halt)) return;
     __shared__ float4 sb[CONE_WARPS][32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    // warps of a CTA take adjacent detector columns of the same row chunk:
+    // their rays cross nearly the same pixels at the same heights (L1 reuse)
     const int chunks = (nv + 31) / 32;
     const int64_t gw = blockIdx.x * (int64_t)CONE_WARPS + wid;
-    const int64_t r = gw / chunks;
-    if (r >= nrays) return;
-    const int dv = (int)(gw % chunks) * 32 + lane;
+    const int64_t r = gw % nrays;
+    if (gw / nrays >= chunks) return;
+    const int dv = (int)(gw / nrays) * 32 + lane;
     const float vmid = 0.5f * (float)(nv - 1);
     const float v = ((float)dv - vmid) * sv;
-    const int64_t b = rptr[r], e = rptr[r + 1];
+    const int64_t b = cptr[r], e = cptr[r + 1];
     float acc = 0.f;
     bool any = false;
     if (b < e) {   // rows whose z-path misses the slab entirely skip the march
-        const float ta = S[b].tau, tb = S[e - 1].tau;
+        const float ta = CE[b].tau, tb = CE[e - 1].tau;
         const float za = __fmaf_rn(v, ta, zc), zb = __fmaf_rn(v, tb, zc);
         const bool hit = dv < nv && !(fmaxf(za, zb) < -1.f || fminf(za, zb) >= (float)cl);
         any = __any_sync(0xffffffffu, hit);
@@ -184,30 +152,21 @@ __global__ void __launch_bounds__(32 * CONE_WARPS) k_cone_fwd(
     if (any) {
         for (int64_t j0 = b; j0 < e; j0 += 32) {
             __syncwarp();
-            if (j0 + lane < e) sb[wid][lane] = *reinterpret_cast<const float4*>(S + j0 + lane);
+            if (j0 + lane < e) sb[wid][lane] = *reinterpret_cast<const float4*>(CE + j0 + lane);
             __syncwarp();
             const int cnt = (int)min((int64_t)32, e - j0);
+#pragma unroll 4
             for (int jj = 0; jj < cnt; ++jj) {
-                const float4 sm = sb[wid][jj];
-                const int pix = __float_as_int(sm.x);
-                const float z = __fmaf_rn(v, sm.w, zc);
+                const float4 en = sb[wid][jj];
+                // z taps, clamped into the slab with zero weight outside it
+                const float z = __fmaf_rn(v, en.z, zc);
                 const float zf = floorf(z);
-                const int z0 = (int)zf;
+                const int zi = (int)zf;
                 const float fz = z - zf;
-                if (z0 < -1 || z0 >= cl) continue;
-                const bool ok0 = z0 >= 0, ok1 = z0 + 1 < cl;
-                const int x0 = (pix & 0xffff) - 1, y0 = (pix >> 16) - 1;
-                float s = 0.f;
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int px = x0 + (q & 1), py = y0 + (q >> 1);
-                    if (px < 0 || px >= w || py < 0 || py >= h) continue;   // warp-uniform
-                    const float* col = vol + ((int64_t)py * w + px) * cl;
-                    const float a0 = ok0 ? __ldg(col + z0) : 0.f;
-                    const float a1 = ok1 ? __ldg(col + z0 + 1) : 0.f;
-                    s = fmaf(corner_weight(q, sm.y, sm.z), fmaf(fz, a1 - a0, a0), s);
-                }
-                acc += s;
+                const int ia = min(max(zi, 0), cl - 1), ib = min(max(zi + 1, 0), cl - 1);
+                const float wa = zi == ia ? 1.f - fz : 0.f, wb = zi + 1 == ib ? fz : 0.f;
+                const float* col = vol + (int64_t)__float_as_int(en.x) * cl;
+                acc = fmaf(en.y, fmaf(wa, __ldg(col + ia), wb * __ldg(col + ib)), acc);
             }
         }
     }
@@ -232,24 +191,30 @@ __global__ void k_cone_gscale(const float* __restrict__ g, const float* __restri
 }
 
 // --------------------------------------------------------------------------
-// adjoint: warp per (pixel, 32 slices), gather over the pixel's entries
+// adjoint: warp per (pixel, window of <= CA_ZW slices)
 // --------------------------------------------------------------------------
-__global__ void __launch_bounds__(32 * CONE_WARPS) k_cone_adj(
+constexpr int CA_ZW = 256;
+constexpr int CA_PMAX = 3;   // residue classes held in shared memory (P tau sv > 1)
+constexpr int CA_WARPS = 4;
+
+__global__ void __launch_bounds__(32 * CA_WARPS) k_cone_adj(
     const ConeEntry* __restrict__ E, const int64_t* __restrict__ eptr, int64_t npix, int nv,
     float sv, int cl, float zc, const float* __restrict__ gs, float* __restrict__ out,
     int accumulate, const int* halt) {
     if (halted(halt)) return;
-    __shared__ float4 eb[CONE_WARPS][32];
+    __shared__ float zacc[CA_WARPS][2 * CA_PMAX][CA_ZW];
+    __shared__ float4 eb[CA_WARPS][32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int zchunks = (cl + 31) / 32;
-    const int64_t gw = blockIdx.x * (int64_t)CONE_WARPS + wid;
-    const int64_t p = gw / zchunks;
+    const int nwin = (cl + CA_ZW - 1) / CA_ZW;
+    const int64_t gw = blockIdx.x * (int64_t)CA_WARPS + wid;
+    const int64_t p = gw / nwin;
     if (p >= npix) return;
-    const int zl = (int)(gw % zchunks) * 32 + lane;
+    const int zb = (int)(gw % nwin) * CA_ZW, zn = min(CA_ZW, cl - zb);
+    for (int k = 0; k < 2 * CA_PMAX; ++k)
+        for (int i = lane; i < zn; i += 32) zacc[wid][k][i] = 0.f;
     const float vmid = 0.5f * (float)(nv - 1);
-    const float zrel = (float)zl - zc;
+    const float inv_sv = 1.f / sv;
     const int64_t b = eptr[p], e = eptr[p + 1];
-    float acc = 0.f;
     for (int64_t j0 = b; j0 < e; j0 += 32) {
         __syncwarp();
         if (j0 + lane < e) eb[wid][lane] = *reinterpret_cast<const float4*>(E + j0 + lane);
@@ -258,29 +223,68 @@ __global__ void __launch_bounds__(32 * CONE_WARPS) k_cone_adj(
         for (int jj = 0; jj < cnt; ++jj) {
             const float4 en = eb[wid][jj];
             const uint32_t col = __float_as_uint(en.x);
-            const float tau = en.y, wxy = en.z;
-            // rows whose forward tap z = fma(v, tau, zc) lies in [zl - 1, zl + 1)
-            const float inv = 1.f / (tau * sv);
-            const int d0 = max((int)floorf((zrel - 1.f) * inv + vmid) - 1, 0);
-            const int d1 = min((int)ceilf((zrel + 1.f) * inv + vmid) + 1, nv - 1);
+            const float wxy = en.y, tau = en.z;
+            // rows with z in [zb - 1, zb + zn] (one row of margin for rounding)
+            const float inv = en.w * inv_sv;
+            const int d0 = max((int)floorf(((float)(zb - 1) - zc) * inv + vmid) - 1, 0);
+            const int d1 = min((int)ceilf(((float)(zb + zn) - zc) * inv + vmid) + 1, nv - 1);
             const float* grow = gs + (int64_t)col * nv;
-            float s = 0.f;
-            for (int d = d0; d <= d1; ++d) {
+            // rows P apart are > 1 slice apart, so lanes of one residue class
+            // mod P never share a voxel within an instruction
+            const int P = (int)floorf(inv) + 1;
+            const int cls = lane % P;
+            for (int dd = d0; dd <= d1; dd += 32) {
+                const int d = dd + lane;
+                const bool valid = d <= d1;
                 const float v = ((float)d - vmid) * sv;
                 const float z = __fmaf_rn(v, tau, zc);
                 const float zf = floorf(z);
-                const int z0 = (int)zf;
+                const int z0 = (int)zf - zb;
                 const float fz = z - zf;
-                const float wz = z0 == zl ? 1.f - fz : (z0 + 1 == zl ? fz : 0.f);
-                if (wz != 0.f) s = fmaf(wz, __ldg(grow + d), s);
+                const float g = valid ? wxy * __ldg(grow + d) : 0.f;
+                const bool va = valid && z0 >= 0 && z0 < zn;
+                const bool vb = valid && z0 + 1 >= 0 && z0 + 1 < zn;
+                const float ta = g - g * fz, tb = g * fz;
+                if (P <= CA_PMAX) {   // one class per array pair: no barriers inside
+                    if (va) zacc[wid][2 * cls][z0] += ta;
+                    if (vb) zacc[wid][2 * cls + 1][z0 + 1] += tb;
+                } else {              // very dense rows: classes in sequence
+                    for (int ph = 0; ph < P; ++ph) {
+                        if (va && cls == ph) zacc[wid][0][z0] += ta;
+                        __syncwarp();
+                        if (vb && cls == ph) zacc[wid][1][z0 + 1] += tb;
+                        __syncwarp();
+                    }
+                }
+                __syncwarp();
             }
-            acc = fmaf(wxy, s, acc);
         }
     }
-    if (zl < cl) {
-        float* o = out + p * cl + zl;
-        *o = accumulate ? *o + acc : acc;
+    __syncwarp();
+    float* o = out + p * cl + zb;
+    for (int i = lane; i < zn; i += 32) {
+        float s = 0.f;
+#pragma unroll
+        for (int k = 0; k < 2 * CA_PMAX; ++k) s += zacc[wid][k][i];
+        o[i] = accumulate ? o[i] + s : s;
     }
+}
+
+static Geom cone_geom(const double* cos_t, const double* sin_t, int m, int nu, double su,
+                      double rs, double rd, int w, int h, double step) {
+    Geom g;
+    g.cos_t = cos_t;
+    g.sin_t = sin_t;
+    g.m = m;
+    g.n_det = nu;
+    g.spacing = su;
+    g.step = step;
+    g.is_fan = true;
+    g.rs = rs;
+    g.rd = rd;
+    g.w = w;
+    g.h = h;
+    return g;
 }
 
 }  // namespace splatct
@@ -297,55 +301,59 @@ int splatct_cone_setup_scratch_bytes(int m, int nu, int w, int h, size_t* bytes)
 }
 
 int splatct_cone_count(const double* cos_t, const double* sin_t, int m, int nu, double su,
-                       double rs, double rd, int w, int h, double step, int64_t* rptr,
-                       float* invL, void* scratch, size_t scratch_bytes, int64_t* nsamples,
+                       double rs, double rd, int w, int h, double step, int64_t* cptr,
+                       float* invL, void* scratch, size_t scratch_bytes, int64_t* nentries,
                        void* stream) {
     SPLATCT_REQUIRE(m > 0 && nu > 0 && w > 0 && h > 0 && step > 0, "invalid cone geometry");
-    SPLATCT_REQUIRE(w < 65534 && h < 32766, "cone sample packing needs w < 65534, h < 32766");
     size_t need = 0;
     splatct_cone_setup_scratch_bytes(m, nu, w, h, &need);
     SPLATCT_REQUIRE(scratch_bytes >= need, "cone scratch too small");
     cudaStream_t s = as_stream(stream);
     const int nr = m * nu;
+    const int64_t big = (int64_t)nr + 1 > (int64_t)w * h + 1 ? (int64_t)nr + 1 : (int64_t)w * h + 1;
     int64_t* cnt = reinterpret_cast<int64_t*>(scratch);
-    void* tmp = (char*)scratch + 2 * align_up(sizeof(unsigned long long) *
-                                              ((int64_t)nr + 1 > (int64_t)w * h + 1
-                                                   ? (int64_t)nr + 1 : (int64_t)w * h + 1));
+    void* tmp = (char*)scratch + 2 * align_up(sizeof(unsigned long long) * big);
     SPLATCT_CK(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (nr + 1), s));
-    ConeGeom g{cos_t, sin_t, m, nu, su, step, rs, rd, w, h};
+    const Geom g = cone_geom(cos_t, sin_t, m, nu, su, rs, rd, w, h, step);
     k_cone_count<<<(nr + 127) / 128, 128, 0, s>>>(g, cnt, invL);
     SPLATCT_LAUNCH_CK();
-    if (int e = exclusive_scan_i64(cnt, rptr, nr + 1, tmp, s)) return e;
-    SPLATCT_CK(cudaMemcpyAsync(nsamples, rptr + nr, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    if (int e = exclusive_scan_i64(cnt, cptr, nr + 1, tmp, s)) return e;
+    SPLATCT_CK(cudaMemcpyAsync(nentries, cptr + nr, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     SPLATCT_CK(cudaStreamSynchronize(s));
     return SPLATCT_OK;
 }
 
 int splatct_cone_fill(const double* cos_t, const double* sin_t, int m, int nu, double su,
-                      double rs, double rd, int w, int h, double step, const int64_t* rptr,
-                      void* samples, void* stream) {
+                      double rs, double rd, int w, int h, double step, const int64_t* cptr,
+                      void* col_entries, void* stream) {
     cudaStream_t s = as_stream(stream);
     const int nr = m * nu;
-    ConeGeom g{cos_t, sin_t, m, nu, su, step, rs, rd, w, h};
-    k_cone_fill<<<(nr + 127) / 128, 128, 0, s>>>(g, rptr, reinterpret_cast<ConeSample*>(samples));
+    const Geom g = cone_geom(cos_t, sin_t, m, nu, su, rs, rd, w, h, step);
+    k_cone_fill<<<(nr + 127) / 128, 128, 0, s>>>(g, cptr,
+                                                 reinterpret_cast<ConeColEntry*>(col_entries));
     SPLATCT_LAUNCH_CK();
     return SPLATCT_OK;
 }
 
-int splatct_cone_entry_count(const void* samples, const int64_t* rptr, int nrays, int w, int h,
-                             int64_t* eptr, void* scratch, size_t scratch_bytes,
+int splatct_cone_entry_count(const void* col_entries, const int64_t* cptr, int nrays, int w,
+                             int h, int64_t* eptr, void* scratch, size_t scratch_bytes,
                              int64_t* nentries, void* stream) {
     const int64_t np = (int64_t)w * h;
     SPLATCT_REQUIRE(scratch_bytes >= align_up(sizeof(int64_t) * (np + 1)) * 2 +
                                           scan_temp_bytes(np + 1),
                     "cone entry scratch too small");
     cudaStream_t s = as_stream(stream);
+    int64_t n = 0;
+    SPLATCT_CK(cudaMemcpyAsync(&n, cptr + nrays, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    SPLATCT_CK(cudaStreamSynchronize(s));
     unsigned long long* cnt = reinterpret_cast<unsigned long long*>(scratch);
     void* tmp = (char*)scratch + 2 * align_up(sizeof(int64_t) * (np + 1));
     SPLATCT_CK(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (np + 1), s));
-    k_cone_ecount<<<(nrays + 127) / 128, 128, 0, s>>>(
-        reinterpret_cast<const ConeSample*>(samples), rptr, nrays, w, h, cnt);
-    SPLATCT_LAUNCH_CK();
+    if (n > 0) {
+        k_cone_ecount<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
+            reinterpret_cast<const ConeColEntry*>(col_entries), n, cnt);
+        SPLATCT_LAUNCH_CK();
+    }
     if (int e = exclusive_scan_i64(reinterpret_cast<int64_t*>(cnt), eptr, np + 1, tmp, s))
         return e;
     SPLATCT_CK(cudaMemcpyAsync(nentries, eptr + np, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
@@ -355,29 +363,29 @@ int splatct_cone_entry_count(const void* samples, const int64_t* rptr, int nrays
 
 int splatct_cone_entry_scratch_bytes(int64_t nentries, int w, int h, size_t* bytes) {
     const int64_t np = (int64_t)w * h;
-    *bytes = align_up(sizeof(ConeEntry) * (size_t)(nentries > 0 ? nentries : 1)) +
-             align_up(sizeof(uint64_t) * (size_t)(nentries > 0 ? nentries : 1)) +
+    const size_t n1 = nentries > 0 ? (size_t)nentries : 1;
+    *bytes = align_up(sizeof(ConeEntry) * n1) + align_up(sizeof(uint64_t) * n1) +
              align_up(sizeof(unsigned long long) * (np + 1));
     return SPLATCT_OK;
 }
 
-int splatct_cone_entry_fill(const void* samples, const int64_t* rptr, int nrays, int w, int h,
-                            const int64_t* eptr, int64_t nentries, void* entries, void* scratch,
-                            size_t scratch_bytes, void* stream) {
+int splatct_cone_entry_fill(const void* col_entries, const int64_t* cptr, int nrays, int w,
+                            int h, const int64_t* eptr, int64_t nentries, void* entries,
+                            void* scratch, size_t scratch_bytes, void* stream) {
     size_t need = 0;
     splatct_cone_entry_scratch_bytes(nentries, w, h, &need);
     SPLATCT_REQUIRE(scratch_bytes >= need, "cone entry scratch too small");
     cudaStream_t s = as_stream(stream);
     const int64_t np = (int64_t)w * h;
-    const size_t n1 = nentries > 0 ? nentries : 1;
+    const size_t n1 = nentries > 0 ? (size_t)nentries : 1;
     ConeEntry* tmpE = reinterpret_cast<ConeEntry*>(scratch);
     uint64_t* key = reinterpret_cast<uint64_t*>((char*)scratch + align_up(sizeof(ConeEntry) * n1));
     unsigned long long* cursor = reinterpret_cast<unsigned long long*>(
         (char*)scratch + align_up(sizeof(ConeEntry) * n1) + align_up(sizeof(uint64_t) * n1));
     SPLATCT_CK(cudaMemcpyAsync(cursor, eptr, sizeof(int64_t) * (np + 1), cudaMemcpyDeviceToDevice,
                                s));
-    k_cone_efill<<<(nrays + 127) / 128, 128, 0, s>>>(reinterpret_cast<const ConeSample*>(samples),
-                                                     rptr, nrays, w, h, cursor, tmpE, key);
+    k_cone_efill<<<(nrays + 127) / 128, 128, 0, s>>>(
+        reinterpret_cast<const ConeColEntry*>(col_entries), cptr, nrays, cursor, tmpE, key);
     SPLATCT_LAUNCH_CK();
     k_cone_esort<<<(unsigned)((np * 32 + 255) / 256), 256, 0, s>>>(
         np, eptr, tmpE, key, reinterpret_cast<ConeEntry*>(entries));
@@ -386,15 +394,17 @@ int splatct_cone_entry_fill(const void* samples, const int64_t* rptr, int nrays,
     return SPLATCT_OK;
 }
 
-int splatct_cone_forward(const void* samples, const int64_t* rptr, const float* invL, int nrays,
-                         int nv, double sv, double step, int w, int h, int c_local, double zc,
-                         const float* vol_yxz, float* sino, const int* halt, void* stream) {
-    SPLATCT_REQUIRE(nrays >= 0 && nv > 0 && c_local > 0, "invalid cone forward sizes");
+int splatct_cone_forward(const void* col_entries, const int64_t* cptr, const float* invL,
+                         int nrays, int nv, double sv, double step, int w, int h, int c_local,
+                         double zc, const float* vol_yxz, float* sino, const int* halt,
+                         void* stream) {
+    SPLATCT_REQUIRE(nrays >= 0 && nv > 0 && c_local > 0 && w > 0 && h > 0,
+                    "invalid cone forward sizes");
     const int64_t warps = (int64_t)nrays * ((nv + 31) / 32);
     if (warps == 0) return SPLATCT_OK;
     k_cone_fwd<<<(unsigned)((warps + CONE_WARPS - 1) / CONE_WARPS), 32 * CONE_WARPS, 0,
-                 as_stream(stream)>>>(reinterpret_cast<const ConeSample*>(samples), rptr, invL,
-                                      nrays, nv, (float)sv, (float)step, w, h, c_local,
+                 as_stream(stream)>>>(reinterpret_cast<const ConeColEntry*>(col_entries), cptr,
+                                      invL, nrays, nv, (float)sv, (float)step, c_local,
                                       (float)zc, vol_yxz, sino, halt);
     SPLATCT_LAUNCH_CK();
     return SPLATCT_OK;
@@ -414,10 +424,10 @@ int splatct_cone_adjoint(const void* entries, const int64_t* eptr, const float* 
         SPLATCT_LAUNCH_CK();
     }
     const int64_t np = (int64_t)w * h;
-    const int64_t warps = np * ((c_local + 31) / 32);
-    k_cone_adj<<<(unsigned)((warps + CONE_WARPS - 1) / CONE_WARPS), 32 * CONE_WARPS, 0, s>>>(
-        reinterpret_cast<const ConeEntry*>(entries), eptr, np, nv, (float)sv, c_local,
-        (float)zc, gscaled, out_yxz, accumulate, halt);
+    const int64_t warps = np * ((c_local + CA_ZW - 1) / CA_ZW);
+    k_cone_adj<<<(unsigned)((warps + CA_WARPS - 1) / CA_WARPS), 32 * CA_WARPS, 0, s>>>(
+        reinterpret_cast<const ConeEntry*>(entries), eptr, np, nv, (float)sv, c_local, (float)zc,
+        gscaled, out_yxz, accumulate, halt);
     SPLATCT_LAUNCH_CK();
     return SPLATCT_OK;
 }

@@ -22,81 +22,11 @@
 
 namespace splatct {
 
-struct Geom {
-    const double* cos_t;
-    const double* sin_t;
-    int m, n_det;
-    double spacing, step;
-    bool is_fan;
-    double rs, rd;
-    int w, h;
-};
-
-// March one ray; call emit(pixel, merged_weight_f64) for every distinct
-// pixel it touches with non-zero weight, in first-touch order of closing.
-// A pixel's support is the open square (x-1,x+1)x(y-1,y+1); the samples
-// inside it are a contiguous k-range, so a pixel untouched by sample k is
-// final (the "open set" never holds more than 8 entries).
-template <typename Emit>
-__device__ void march_ray(const Geom& g, int r, Emit emit) {
-    const int v = r / g.n_det, d = r % g.n_det;
-    const double cx = 0.5 * (g.w - 1), cy = 0.5 * (g.h - 1);
-    const double u = (d - 0.5 * (g.n_det - 1)) * g.spacing;
-    double ox, oy, dx, dy, t0, t1;
-    ray_geometry(g.cos_t[v], g.sin_t[v], u, g.is_fan, g.rs, g.rd, cx, cy, g.w, g.h, ox, oy, dx,
-                 dy, t0, t1);
-    if (!(t1 > t0)) return;
-    const int64_t ns = (int64_t)((t1 - t0) / g.step);
-    int opix[8];
-    double ow[8];
-    bool otouch[8];
-    int nopen = 0;
-    for (int64_t k = 0; k < ns; ++k) {
-        const double t = t0 + (k + 0.5) * g.step;
-        const double sx = ox + t * dx, sy = oy + t * dy;
-        const double fx0 = floor(sx), fy0 = floor(sy);
-        const int64_t x0 = (int64_t)fx0, y0 = (int64_t)fy0;
-        const double fx = sx - (double)x0, fy = sy - (double)y0;
-        for (int q = 0; q < nopen; ++q) otouch[q] = false;
-        const int64_t tx[4] = {x0, x0 + 1, x0, x0 + 1};
-        const int64_t ty[4] = {y0, y0, y0 + 1, y0 + 1};
-        const double tw[4] = {(1 - fx) * (1 - fy), fx * (1 - fy), (1 - fx) * fy, fx * fy};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            if (tx[q] < 0 || tx[q] >= g.w || ty[q] < 0 || ty[q] >= g.h || tw[q] == 0.0) continue;
-            const int pix = (int)(ty[q] * g.w + tx[q]);
-            int f = -1;
-            for (int e = 0; e < nopen; ++e)
-                if (opix[e] == pix) f = e;
-            if (f < 0) {
-                f = nopen++;
-                opix[f] = pix;
-                ow[f] = 0.0;
-            }
-            ow[f] += tw[q];
-            otouch[f] = true;
-        }
-        int keep = 0;
-        for (int e = 0; e < nopen; ++e) {
-            if (!otouch[e]) {
-                emit(opix[e], ow[e]);
-            } else {
-                opix[keep] = opix[e];
-                ow[keep] = ow[e];
-                otouch[keep] = true;
-                ++keep;
-            }
-        }
-        nopen = keep;
-    }
-    for (int e = 0; e < nopen; ++e) emit(opix[e], ow[e]);
-}
-
 __global__ void k_proj_count(Geom g, int64_t* __restrict__ cnt) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= g.m * g.n_det) return;
     int64_t c = 0;
-    march_ray(g, r, [&](int, double) { ++c; });
+    march_ray(g, r, [&](int, double, double) { ++c; });
     cnt[r] = c;
 }
 
@@ -106,7 +36,7 @@ __global__ void k_proj_fill(Geom g, const int64_t* __restrict__ a_ptr, int32_t* 
     if (r >= g.m * g.n_det) return;
     int64_t j = a_ptr[r];
     const double step = g.step;
-    march_ray(g, r, [&](int pix, double w) {
+    march_ray(g, r, [&](int pix, double w, double) {
         a_col[j] = pix;
         a_val[j] = (float)(step * w);
         ++j;

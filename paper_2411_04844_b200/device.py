@@ -341,24 +341,28 @@ class ConeOperator:
              float(geom.origin_to_detector), self.w, self.h, self.step)
         sb = size_query("splatct_cone_setup_scratch_bytes", self.m, self.n_det, self.w, self.h)
         scratch = torch.empty(sb, dtype=torch.uint8, device=dev)
-        self.rptr = torch.empty(self.n_rays + 1, dtype=torch.int64, device=dev)
+        # column-major merged entries {pixel, w, tau} and their pixel-major
+        # transpose {column, w, tau, 1/tau}
+        self.cptr = torch.empty(self.n_rays + 1, dtype=torch.int64, device=dev)
         self.inv_len = torch.empty(self.n_rays, dtype=torch.float32, device=dev)
         ns = ctypes.c_int64(0)
-        call("splatct_cone_count", *g, ptr(self.rptr), ptr(self.inv_len), ptr(scratch), sb,
+        call("splatct_cone_count", *g, ptr(self.cptr), ptr(self.inv_len), ptr(scratch), sb,
              ctypes.byref(ns), stream_handle())
-        self.n_samples = int(ns.value)
-        self.samples = torch.empty((max(self.n_samples, 1), 4), dtype=torch.float32, device=dev)
-        call("splatct_cone_fill", *g, ptr(self.rptr), ptr(self.samples), stream_handle())
+        self.n_samples = int(ns.value)   # column entries
+        self.col_entries = torch.empty((max(self.n_samples, 1), 4), dtype=torch.float32,
+                                       device=dev)
+        call("splatct_cone_fill", *g, ptr(self.cptr), ptr(self.col_entries), stream_handle())
         self.eptr = torch.empty(self.w * self.h + 1, dtype=torch.int64, device=dev)
         ne = ctypes.c_int64(0)
-        call("splatct_cone_entry_count", ptr(self.samples), ptr(self.rptr), self.n_rays, self.w,
-             self.h, ptr(self.eptr), ptr(scratch), sb, ctypes.byref(ne), stream_handle())
+        call("splatct_cone_entry_count", ptr(self.col_entries), ptr(self.cptr), self.n_rays,
+             self.w, self.h, ptr(self.eptr), ptr(scratch), sb, ctypes.byref(ne),
+             stream_handle())
         self.n_entries = int(ne.value)
         self.entries = torch.empty((max(self.n_entries, 1), 4), dtype=torch.float32, device=dev)
         eb = size_query("splatct_cone_entry_scratch_bytes", self.n_entries, self.w, self.h)
         escr = torch.empty(eb, dtype=torch.uint8, device=dev)
-        call("splatct_cone_entry_fill", ptr(self.samples), ptr(self.rptr), self.n_rays, self.w,
-             self.h, ptr(self.eptr), self.n_entries, ptr(self.entries), ptr(escr), eb,
+        call("splatct_cone_entry_fill", ptr(self.col_entries), ptr(self.cptr), self.n_rays,
+             self.w, self.h, ptr(self.eptr), self.n_entries, ptr(self.entries), ptr(escr), eb,
              stream_handle())
         del scratch, escr
         self.gscaled = torch.empty(self.n_rays * self.nv, dtype=torch.float32, device=dev)
@@ -378,7 +382,7 @@ class ConeOperator:
         if out is None:
             out = torch.empty((self.m, self.n_det, self.nv), dtype=torch.float32,
                               device=vol.device)
-        call("splatct_cone_forward", ptr(self.samples), ptr(self.rptr), ptr(self.inv_len),
+        call("splatct_cone_forward", ptr(self.col_entries), ptr(self.cptr), ptr(self.inv_len),
              self.n_rays, self.nv, self.sv, self.step, self.w, self.h, cl, self._zc(z0),
              ptr(vol), ptr(out), ptr(halt), stream_handle())
         return out
