@@ -76,21 +76,63 @@ def zyx_to_yxz(arr, device) -> torch.Tensor:
     return _host_f32(arr).to(device).permute(1, 2, 0).contiguous()
 
 
-def to_host(t: torch.Tensor) -> np.ndarray:
-    """Device -> fresh numpy array via a pinned staging buffer (DMA-speed D2H)."""
+_PINNED: dict = {}
+
+
+def _pinned(numel: int, dtype) -> torch.Tensor:
+    """A cached page-locked staging buffer of at least numel elements (reused:
+    cudaHostAlloc of tens of MB costs more than the copy it serves)."""
+    buf = _PINNED.get(dtype)
+    if buf is None or buf.numel() < numel:
+        buf = torch.empty(max(numel, 1), dtype=dtype, pin_memory=True)
+        _PINNED[dtype] = buf
+    return buf[:numel]
+
+
+class HostArray:
+    """A host array allocated and page-faulted on a background thread, so a
+    later device->host copy into it runs at memcpy speed (fresh pages would
+    otherwise be faulted in during the copy)."""
+
+    def __init__(self, shape, dtype=np.float32):
+        import threading
+        self._out = None
+        self._th = threading.Thread(target=self._alloc, args=(tuple(shape), dtype), daemon=True)
+        self._th.start()
+
+    def _alloc(self, shape, dtype):
+        a = np.empty(shape, dtype)
+        a.fill(0)
+        self._out = a
+
+    def get(self) -> np.ndarray:
+        self._th.join()
+        return self._out
+
+
+def to_host(t: torch.Tensor, out: np.ndarray | None = None) -> np.ndarray:
+    """Device -> numpy via a cached pinned staging buffer (DMA-speed D2H)."""
     if t.device.type != "cuda":
         return t.numpy().copy()
-    pinned = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
-    pinned.copy_(t)
-    return pinned.numpy().copy()
+    t = t.contiguous()
+    st = _pinned(t.numel(), t.dtype).view(t.shape)
+    st.copy_(t)
+    if out is None:
+        return st.numpy().copy()
+    np.copyto(out.reshape(t.shape), st.numpy())
+    return out
 
 
-def yxz_to_zyx(t: torch.Tensor) -> np.ndarray:
-    return to_host(t.permute(2, 0, 1).contiguous())
+def yxz_to_zyx(t: torch.Tensor, out: np.ndarray | None = None) -> np.ndarray:
+    return to_host(t.permute(2, 0, 1).contiguous(), out)
 
 
 def sino_to_device(views, device) -> torch.Tensor:
-    return _host_f32(views).to(device)
+    """(m, n, p) host array -> device f32 through the pinned staging buffer."""
+    a = np.asarray(views)
+    st = _pinned(a.size, torch.float32)
+    np.copyto(st.numpy().reshape(a.shape), a, casting="same_kind")
+    return st.view(a.shape).to(device, non_blocking=False)
 
 
 # ---------------------------------------------------------------------------
