@@ -484,6 +484,103 @@ __global__ void k_tile_starts(const uint32_t* __restrict__ skeys, int64_t np, in
 constexpr int BG_WARPS = 8;
 constexpr int BG_XC = 17;   // box columns per register row (default box 17^3)
 
+// Fast path for boxes up to 17 columns x 17 slices (the default 17^3 box):
+// the 32 lanes take two columns at a time (lane = column parity x 16 slices),
+// so a row costs 9 column-pair loads instead of 17 half-empty ones; the 17th
+// slice of the box is one lanes-over-columns load per row.  Lane-private x
+// tables (9 pairs x {e, e r, e r^2}) stay in registers, the two halves are
+// combined once per Gaussian.  Same moments as the general path below.
+__device__ __forceinline__ void bwd_moments17(const GRec& r, int xlo, int nx, int ylo, int ny,
+                                              int zlo, int nz, int w, int c, int zoff,
+                                              const float* __restrict__ up, float& S0, float& Sx,
+                                              float& Sy, float& Sz, float& S2) {
+    const int lane = threadIdx.x & 31, hf = lane >> 4, zl = lane & 15;
+    // slice of this lane (first 16 of the box) and the optional 17th slice
+    const bool zok = zl < nz;
+    const float rz = (float)(zlo + zl + zoff - r.fz) - r.dz;
+    const float ez = zok ? exp2f(-r.inv2 * rz * rz) : 0.f;
+    const bool has16 = nz > 16;
+    const float rz16 = (float)(zlo + 16 + zoff - r.fz) - r.dz;
+    const float ez16 = has16 ? exp2f(-r.inv2 * rz16 * rz16) : 0.f;
+    // x weights: column pair k -> column 2k + hf (main), column lane (17th slice)
+    float wx0[9], wx1[9], wx2[9];
+    uint32_t coff[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+        const int col = 2 * k + hf;
+        const float rx = (float)(xlo + col - r.fx) - r.dx;
+        const float ex = col < nx ? exp2f(-r.inv2 * rx * rx) : 0.f;
+        wx0[k] = ex;
+        wx1[k] = ex * rx;
+        wx2[k] = ex * rx * rx;
+        coff[k] = (uint32_t)min(col, nx - 1) * (uint32_t)c;
+    }
+    const float rxp = (float)(xlo + lane - r.fx) - r.dx;
+    const float exp_ = (has16 && lane < nx) ? exp2f(-r.inv2 * rxp * rxp) : 0.f;
+    const float wp0 = exp_, wp1 = exp_ * rxp, wp2 = exp_ * rxp * rxp;
+    const uint32_t poff = (uint32_t)min(lane, nx - 1) * (uint32_t)c + 16u;
+    const int64_t rstride = (int64_t)w * c;
+    const float* row = up + ((int64_t)ylo * w + xlo) * c + zlo + (zok ? zl : 0);
+    const float* prow = up + ((int64_t)ylo * w + xlo) * c + zlo;
+    float A0 = 0.f, Ax = 0.f, Ay = 0.f, Ar = 0.f;   // main slices, per lane
+    float Q0 = 0.f, Qx = 0.f, Qy = 0.f, Qr = 0.f;   // 17th slice, per column lane
+    float u[9], un[9], pu = 0.f, pn = 0.f;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) u[k] = zok ? __ldg(row + coff[k]) : 0.f;
+    if (has16) pu = __ldg(prow + poff);
+    for (int yi = 0; yi < ny; ++yi) {
+        const bool more = yi + 1 < ny;
+        if (more) {   // prefetch the next row
+            row += rstride;
+            prow += rstride;
+#pragma unroll
+            for (int k = 0; k < 9; ++k) un[k] = zok ? __ldg(row + coff[k]) : 0.f;
+            if (has16) pn = __ldg(prow + poff);
+        }
+        const float ry = (float)(ylo + yi - r.fy) - r.dy;
+        const float ey = exp2f(-r.inv2 * ry * ry);
+        float C0 = 0.f, C1 = 0.f, C2 = 0.f;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) {
+            C0 = fmaf(wx0[k], u[k], C0);
+            C1 = fmaf(wx1[k], u[k], C1);
+            C2 = fmaf(wx2[k], u[k], C2);
+        }
+        const float eyry = ey * ry, eyry2 = eyry * ry;
+        A0 = fmaf(ey, C0, A0);
+        Ax = fmaf(ey, C1, Ax);
+        Ay = fmaf(eyry, C0, Ay);
+        Ar = fmaf(ey, C2, fmaf(eyry2, C0, Ar));
+        Q0 = fmaf(ey * wp0, pu, Q0);
+        Qx = fmaf(ey * wp1, pu, Qx);
+        Qy = fmaf(eyry * wp0, pu, Qy);
+        Qr = fmaf(fmaf(ey, wp2, eyry2 * wp0), pu, Qr);
+        if (more) {
+#pragma unroll
+            for (int k = 0; k < 9; ++k) u[k] = un[k];
+            pu = pn;
+        }
+    }
+    // the two column-parity halves hold the same slices: fold them, then apply
+    // the lane-private z factors (lanes 16..31 duplicate lanes 0..15: weight 0)
+    A0 += __shfl_xor_sync(0xffffffffu, A0, 16);
+    Ax += __shfl_xor_sync(0xffffffffu, Ax, 16);
+    Ay += __shfl_xor_sync(0xffffffffu, Ay, 16);
+    Ar += __shfl_xor_sync(0xffffffffu, Ar, 16);
+    const float eh = hf ? 0.f : ez;
+    S0 = eh * A0;
+    Sx = eh * Ax;
+    Sy = eh * Ay;
+    Sz = eh * rz * A0;
+    S2 = eh * fmaf(rz * rz, A0, Ar);
+    // 17th slice: per-column-lane partials, all with the same z factor
+    S0 = fmaf(ez16, Q0, S0);
+    Sx = fmaf(ez16, Qx, Sx);
+    Sy = fmaf(ez16, Qy, Sy);
+    Sz = fmaf(ez16 * rz16, Q0, Sz);
+    S2 = fmaf(ez16, fmaf(rz16 * rz16, Q0, Qr), S2);
+}
+
 __global__ void __launch_bounds__(32 * BG_WARPS, 2) k_fvr_bwd(const double* __restrict__ P, int64_t n,
                                                           const int32_t* __restrict__ fp,
                                                           const GRec* __restrict__ rec, int w,
@@ -501,7 +598,11 @@ __global__ void __launch_bounds__(32 * BG_WARPS, 2) k_fvr_bwd(const double* __re
     const int xlo = fp[6 * i], xhi = fp[6 * i + 1], ylo = fp[6 * i + 2], yhi = fp[6 * i + 3];
     const int zlo = fp[6 * i + 4], zhi = fp[6 * i + 5];
     float S0 = 0.f, Sx = 0.f, Sy = 0.f, Sz = 0.f, S2 = 0.f;
-    if (xlo <= xhi && ylo <= yhi && zlo <= zhi) {
+    if (xlo <= xhi && ylo <= yhi && zlo <= zhi && xhi - xlo < 17 && zhi - zlo < 17) {
+        const GRec r = rec[i];
+        bwd_moments17(r, xlo, xhi - xlo + 1, ylo, yhi - ylo + 1, zlo, zhi - zlo + 1, w, c, zoff,
+                      up, S0, Sx, Sy, Sz, S2);
+    } else if (xlo <= xhi && ylo <= yhi && zlo <= zhi) {
         const GRec r = rec[i];
         for (int zc = zlo; zc <= zhi; zc += 32) {
             const int z = zc + lane;
