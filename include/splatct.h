@@ -215,6 +215,17 @@ int splatct_loss_fused(const float* pred, const float* ref, int m, int n, int p,
                        float* grad_pred, void* ws, size_t ws_bytes, double* sums,
                        const int* halt, void* stream);
 
+/* The measured sinogram is constant over a run: splatct_loss_prepare_ref
+ * stores its per-window SSIM moments (mean_y, E[y^2]) in ws once, and
+ * splatct_loss_fused_prepared (same arguments as splatct_loss_fused, same ref
+ * and ws) then carries only the three pred-dependent moments per iteration. */
+int splatct_loss_prepare_ref(const float* ref, int m, int n, int p, void* ws, size_t ws_bytes,
+                             void* stream);
+int splatct_loss_fused_prepared(const float* pred, const float* ref, int m, int n, int p,
+                                double lmax, double lambda1, double lambda2, double l1_count,
+                                double ssim_slices, float* grad_pred, void* ws, size_t ws_bytes,
+                                double* sums, const int* halt, void* stream);
+
 /* out[0] = sum (x-y)^2 over count elements (f64, fixed order); ws holds
  * SPLATCT_SQDIFF_BLOCKS doubles.  Used for PSNR (metrics.psnr, metrics.py:24-38). */
 #define SPLATCT_SQDIFF_BLOCKS 592

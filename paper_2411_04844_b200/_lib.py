@@ -59,6 +59,9 @@ SIGNATURES: dict[str, list] = {
     "splatct_sino_max": [c_vp, c_i64, c_vp, c_vp],
     "splatct_loss_fused": [c_vp, c_vp, c_i32, c_i32, c_i32, c_f64, c_f64, c_f64, c_f64, c_f64,
                            c_vp, c_vp, c_sz, c_vp, c_vp, c_vp],
+    "splatct_loss_prepare_ref": [c_vp, c_i32, c_i32, c_i32, c_vp, c_sz, c_vp],
+    "splatct_loss_fused_prepared": [c_vp, c_vp, c_i32, c_i32, c_i32, c_f64, c_f64, c_f64, c_f64,
+                                    c_f64, c_vp, c_vp, c_sz, c_vp, c_vp, c_vp],
     "splatct_sum_sq_diff": [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp],
     "splatct_reduce_sum": [c_vp, c_i64, c_vp, c_vp],
     "splatct_iter_finalize": [c_vp, c_f64, c_f64, c_f64, c_f64, c_f64, c_f64, c_f64, c_f64, c_i64,

@@ -57,7 +57,7 @@ struct LossLayout {
     int64_t nb_v, nb_g;    // blocks per chunk of the SSIM-map and gradient passes
     int64_t nb_s11, nb_g11;   // blocks of the 11x11 row-walking kernels
     bool k11;
-    size_t o_H, o_D, o_T, o_ps, o_pl, o_D11, total;
+    size_t o_H, o_D, o_T, o_ps, o_pl, o_D11, o_RS, total;
 };
 
 constexpr int ZC = 64;    // slices per chunk (one block = 4 columns x ZC slices)
@@ -81,6 +81,7 @@ static LossLayout loss_layout(int m, int n, int p) {
         L.o_H = L.o_T = 0;
         L.o_D11 = take(sizeof(double) * 3 * (size_t)L.vr * L.vc * p);
         L.o_D = L.o_D11;
+        L.o_RS = take(sizeof(double) * 2 * (size_t)L.vr * L.vc * p);   // ref window stats
         L.o_ps = take(sizeof(double) * L.nb_s11);
         L.o_pl = take(sizeof(double) * L.nb_g11);
     } else {
@@ -341,13 +342,21 @@ __device__ __forceinline__ void cp_wait_group() { asm volatile("cp.async.wait_gr
 constexpr int S_CHUNKS = 2 * R_SPAN * 8;                  // x, y: 18 columns x 8 chunks
 constexpr int S_SLOTS = (S_CHUNKS + R_NT - 1) / R_NT;      // chunks per thread
 
-__global__ void __launch_bounds__(R_NT, 1) k_ssim_stats11(const float* __restrict__ X,
+// MODE 0: all five window moments from X and Y (loss.py:112-141).
+// MODE 1: the reference-only moments (mean_y, E[y^2]) are read from RS, the
+//         per-window statistics of the measured sinogram computed once per
+//         run (MODE 2), so the per-iteration pass carries three fields.
+// MODE 2: writes RS = {mean_y, E[y^2]} per valid window (X unused).
+template <int MODE>
+__global__ void __launch_bounds__(R_NT, MODE == 1 ? 2 : 1) k_ssim_stats11(const float* __restrict__ X,
                                                           const float* __restrict__ Y, int m, int n,
                                                           int p, Win W, double c1, double c2,
                                                           int vr, int vc, double* __restrict__ D,
                                                           double* __restrict__ part,
+                                                          double* __restrict__ RS,
                                                           const int* halt) {
     if (halted(halt)) return;
+    constexpr int NF = MODE == 0 ? 5 : (MODE == 1 ? 3 : 2);   // ring fields
     __shared__ __align__(16) float sf[R_BUF][2][R_SPAN][32];    // cp.async landing (f32)
     __shared__ __align__(16) double sd[2][2][R_SPAN][32];       // converted rows (f64)
     __shared__ double red[R_NT / 32];
@@ -371,6 +380,7 @@ __global__ void __launch_bounds__(R_NT, 1) k_ssim_stats11(const float* __restric
         goff[k] = gok[k] ? (int64_t)(j0 + col) * p + zb + 4 * q : 0;
         soff[k] = (arr * R_SPAN + col) * 32 + 4 * q;     // within one [2][R_SPAN][32] row
         if (arr) goff[k] = -goff[k] - 1;                  // sign selects Y
+        if (MODE == 2 && !arr) mine[k] = false;           // ref-only: no X rows
     }
     auto issue = [&](int v) {
         if (v < m) {
@@ -400,7 +410,7 @@ __global__ void __launch_bounds__(R_NT, 1) k_ssim_stats11(const float* __restric
     };
     issue(0);
     issue(1);
-    double ring[11][5];
+    double ring[11][NF];
     double ssum = 0.0;
     for (int v0 = 0; v0 < m; v0 += 11) {
 #pragma unroll
@@ -413,55 +423,77 @@ __global__ void __launch_bounds__(R_NT, 1) k_ssim_stats11(const float* __restric
             __syncthreads();      // row v (f64) complete; everyone is past row v-2's reads
             const double* xr = &sd[v & 1][0][cl][lane];
             const double* yr = &sd[v & 1][1][cl][lane];
-            double h[2][5] = {{0, 0, 0, 0, 0}, {0, 0, 0, 0, 0}};
+            double h[2][NF];
+#pragma unroll
+            for (int f = 0; f < NF; ++f) h[0][f] = h[1][f] = 0.0;
 #pragma unroll
             for (int b = 0; b < 11; ++b) {
-                const double xv = xr[32 * b], yv = yr[32 * b];
-                const double gx = W.gc[b] * xv, gy = W.gc[b] * yv;
                 double* hb = h[b & 1];
-                hb[0] += gx;
-                hb[1] += gy;
-                hb[2] = fma(gx, xv, hb[2]);
-                hb[3] = fma(gy, yv, hb[3]);
-                hb[4] = fma(gx, yv, hb[4]);
+                const double yv = yr[32 * b];
+                if (MODE == 2) {          // {y, y^2}
+                    const double gy = W.gc[b] * yv;
+                    hb[0] += gy;
+                    hb[1] = fma(gy, yv, hb[1]);
+                } else {
+                    const double xv = xr[32 * b];
+                    const double gx = W.gc[b] * xv;
+                    hb[0] += gx;                       // x
+                    hb[1] = fma(gx, xv, hb[1]);        // x^2
+                    hb[2] = fma(gx, yv, hb[2]);        // xy
+                    if (MODE == 0) {
+                        const double gy = W.gc[b] * yv;
+                        hb[3] += gy;                   // y
+                        hb[4] = fma(gy, yv, hb[4]);    // y^2
+                    }
+                }
             }
 #pragma unroll
-            for (int f = 0; f < 5; ++f) ring[ph][f] = h[0][f] + h[1][f];
+            for (int f = 0; f < NF; ++f) ring[ph][f] = h[0][f] + h[1][f];
             if (v >= 10 && act) {
-                double a[2][5] = {{0, 0, 0, 0, 0}, {0, 0, 0, 0, 0}};
+                double a[2][NF];
+#pragma unroll
+                for (int f = 0; f < NF; ++f) a[0][f] = a[1][f] = 0.0;
 #pragma unroll
                 for (int t = 0; t < 11; ++t) {   // row v-10+t lives in slot (ph+1+t) % 11
                     const double g = W.gr[t];
                     double* at = a[t & 1];
 #pragma unroll
-                    for (int f = 0; f < 5; ++f) at[f] = fma(g, ring[(ph + 1 + t) % 11][f], at[f]);
+                    for (int f = 0; f < NF; ++f) at[f] = fma(g, ring[(ph + 1 + t) % 11][f], at[f]);
                 }
-                const double mx = a[0][0] + a[1][0], my = a[0][1] + a[1][1],
-                             x2w = a[0][2] + a[1][2], y2w = a[0][3] + a[1][3],
-                             xyw = a[0][4] + a[1][4];
-                const double sx2 = x2w - mx * mx, sy2 = y2w - my * my, sxy = xyw - mx * my;
-                const double a1 = 2.0 * mx * my + c1, a2 = 2.0 * sxy + c2;
-                const double b1 = mx * mx + my * my + c1, b2 = sx2 + sy2 + c2;
-                const double inv = 1.0 / (b1 * b2);   // 1/b1 = b2*inv, 1/b2 = b1*inv
-                const double s = (a1 * a2) * inv;
-                ssum += s;
                 const int64_t o = ((int64_t)(v - 10) * vc + j) * p + z;
-                D[o] = (2.0 * my * (a2 - a1)) * inv - 2.0 * mx * s * ((b2 - b1) * inv);
-                D[plane + o] = -s * (b1 * inv);
-                D[2 * plane + o] = 2.0 * a1 * inv;
+                if (MODE == 2) {
+                    RS[o] = a[0][0] + a[1][0];
+                    RS[plane + o] = a[0][1] + a[1][1];
+                } else {
+                    const double mx = a[0][0] + a[1][0], x2w = a[0][1] + a[1][1],
+                                 xyw = a[0][2] + a[1][2];
+                    const double my = MODE == 0 ? a[0][3] + a[1][3] : RS[o];
+                    const double y2w = MODE == 0 ? a[0][4] + a[1][4] : RS[plane + o];
+                    const double sx2 = x2w - mx * mx, sy2 = y2w - my * my, sxy = xyw - mx * my;
+                    const double a1 = 2.0 * mx * my + c1, a2 = 2.0 * sxy + c2;
+                    const double b1 = mx * mx + my * my + c1, b2 = sx2 + sy2 + c2;
+                    const double inv = 1.0 / (b1 * b2);   // 1/b1 = b2*inv, 1/b2 = b1*inv
+                    const double s = (a1 * a2) * inv;
+                    ssum += s;
+                    D[o] = (2.0 * my * (a2 - a1)) * inv - 2.0 * mx * s * ((b2 - b1) * inv);
+                    D[plane + o] = -s * (b1 * inv);
+                    D[2 * plane + o] = 2.0 * a1 * inv;
+                }
             }
         }
     }
     cp_wait_group<0>();
-    const double r = block_sum<R_NT>(ssum, red);
-    if (threadIdx.x == 0) part[blockIdx.y * gridDim.x + blockIdx.x] = r;
+    if (MODE != 2) {
+        const double r = block_sum<R_NT>(ssum, red);
+        if (threadIdx.x == 0) part[blockIdx.y * gridDim.x + blockIdx.x] = r;
+    }
 }
 
 constexpr int G_DCHUNKS = 3 * R_SPAN * 16;                   // D: 3 fields x 18 cols x 16
 constexpr int G_DSLOTS = (G_DCHUNKS + R_NT - 1) / R_NT;
 constexpr int G_XCHUNKS = 2 * R_COLS * 8;                    // x, y: 8 cols x 8 chunks
 
-__global__ void __launch_bounds__(R_NT, 1) k_loss_grad11(const float* __restrict__ X,
+__global__ void __launch_bounds__(R_NT, 2) k_loss_grad11(const float* __restrict__ X,
                                                          const float* __restrict__ Y, int m, int n,
                                                          int p, Win W, int vr, int vc,
                                                          const double* __restrict__ D, double l1w,
@@ -704,10 +736,12 @@ int splatct_sino_max(const float* x, int64_t count, double* out, void* stream) {
     return SPLATCT_OK;
 }
 
-int splatct_loss_fused(const float* pred, const float* ref, int m, int n, int p, double lmax,
-                       double lambda1, double lambda2, double l1_count, double ssim_slices,
-                       float* grad_pred, void* ws, size_t ws_bytes, double* sums,
-                       const int* halt, void* stream) {
+}  // extern "C"
+
+static int loss_fused_impl(const float* pred, const float* ref, int m, int n, int p, double lmax,
+                           double lambda1, double lambda2, double l1_count, double ssim_slices,
+                           float* grad_pred, void* ws, size_t ws_bytes, double* sums,
+                           const int* halt, void* stream, bool prepared) {
     SPLATCT_REQUIRE(m > 0 && n > 0 && p > 0, "invalid sinogram dims");
     LossLayout L = loss_layout(m, n, p);
     SPLATCT_REQUIRE(ws_bytes >= L.total, "loss workspace too small");
@@ -726,8 +760,13 @@ int splatct_loss_fused(const float* pred, const float* ref, int m, int n, int p,
         double* D11 = reinterpret_cast<double*>(base + L.o_D11);
         const dim3 gs((p + 31) / 32, (L.vc + 7) / 8), gg((p + 31) / 32, (n + 7) / 8);
         if (lambda2 > 0.0) {
-            k_ssim_stats11<<<gs, R_NT, 0, s>>>(pred, ref, m, n, p, W, c1, c2, L.vr, L.vc, D11, ps,
-                                               halt);
+            double* RS = reinterpret_cast<double*>(base + L.o_RS);
+            if (prepared)
+                k_ssim_stats11<1><<<gs, R_NT, 0, s>>>(pred, ref, m, n, p, W, c1, c2, L.vr, L.vc,
+                                                      D11, ps, RS, halt);
+            else
+                k_ssim_stats11<0><<<gs, R_NT, 0, s>>>(pred, ref, m, n, p, W, c1, c2, L.vr, L.vc,
+                                                      D11, ps, RS, halt);
             SPLATCT_LAUNCH_CK();
             if (int e = reduce_sum_f64(ps, L.nb_s11, sums + 1, s)) return e;
         } else {
@@ -777,6 +816,40 @@ int splatct_loss_fused(const float* pred, const float* ref, int m, int n, int p,
     }
     if (int e = reduce_sum_f64(pl, L.nb_g * L.nchunks, sums, s)) return e;
     return SPLATCT_OK;
+}
+
+extern "C" {
+
+int splatct_loss_fused(const float* pred, const float* ref, int m, int n, int p, double lmax,
+                       double lambda1, double lambda2, double l1_count, double ssim_slices,
+                       float* grad_pred, void* ws, size_t ws_bytes, double* sums,
+                       const int* halt, void* stream) {
+    return loss_fused_impl(pred, ref, m, n, p, lmax, lambda1, lambda2, l1_count, ssim_slices,
+                           grad_pred, ws, ws_bytes, sums, halt, stream, false);
+}
+
+int splatct_loss_prepare_ref(const float* ref, int m, int n, int p, void* ws, size_t ws_bytes,
+                             void* stream) {
+    SPLATCT_REQUIRE(m > 0 && n > 0 && p > 0, "invalid sinogram dims");
+    LossLayout L = loss_layout(m, n, p);
+    SPLATCT_REQUIRE(ws_bytes >= L.total, "loss workspace too small");
+    if (!L.k11) return SPLATCT_OK;   // the generic path recomputes everything
+    Win W = make_win(m, n);
+    char* base = reinterpret_cast<char*>(ws);
+    const dim3 gs((p + 31) / 32, (L.vc + 7) / 8);
+    k_ssim_stats11<2><<<gs, R_NT, 0, as_stream(stream)>>>(
+        nullptr, ref, m, n, p, W, 0.0, 0.0, L.vr, L.vc, nullptr, nullptr,
+        reinterpret_cast<double*>(base + L.o_RS), nullptr);
+    SPLATCT_LAUNCH_CK();
+    return SPLATCT_OK;
+}
+
+int splatct_loss_fused_prepared(const float* pred, const float* ref, int m, int n, int p,
+                                double lmax, double lambda1, double lambda2, double l1_count,
+                                double ssim_slices, float* grad_pred, void* ws, size_t ws_bytes,
+                                double* sums, const int* halt, void* stream) {
+    return loss_fused_impl(pred, ref, m, n, p, lmax, lambda1, lambda2, l1_count, ssim_slices,
+                           grad_pred, ws, ws_bytes, sums, halt, stream, true);
 }
 
 int splatct_sum_sq_diff(const float* x, const float* y, int64_t count, double* ws, double* out,

@@ -515,9 +515,20 @@ class LossPlan:
         kc -= 1 - kc % 2
         self.valid = (self.m - kr + 1) * (self.n - kc + 1)
 
+        self.prepared_ref = None   # data_ptr of the ref whose window stats are in ws
+
+    def prepare(self, ref: torch.Tensor) -> None:
+        """Cache the constant reference sinogram's SSIM window moments (call
+        again whenever ref's contents change)."""
+        call("splatct_loss_prepare_ref", ptr(ref), self.m, self.n, self.p, ptr(self.ws),
+             self.ws_bytes, stream_handle())
+        self.prepared_ref = ref.data_ptr()
+
     def fused(self, pred, ref, lmax: float, lambda1: float, lambda2: float, l1_count: float,
               ssim_slices: float, grad_out, sums, halt=None):
-        call("splatct_loss_fused", ptr(pred), ptr(ref), self.m, self.n, self.p, float(lmax),
+        fn = ("splatct_loss_fused_prepared" if self.prepared_ref == ref.data_ptr()
+              else "splatct_loss_fused")
+        call(fn, ptr(pred), ptr(ref), self.m, self.n, self.p, float(lmax),
              float(lambda1), float(lambda2), float(l1_count), float(ssim_slices), ptr(grad_out),
              ptr(self.ws), self.ws_bytes, ptr(sums), ptr(halt), stream_handle())
 

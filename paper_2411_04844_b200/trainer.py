@@ -89,6 +89,7 @@ class Trainer:
         dev = self.device
         self.op = D.operator_for(geom, self.w, self.h, self.slab.c_global, step_length, dev)
         self.loss = D.LossPlan(m, n, p, dev)
+        self.loss.prepare(measured)   # the measured sinogram is constant over a run
         self.pred = torch.empty((m, n, p), dtype=torch.float32, device=dev)
         self.gpred = torch.empty_like(self.pred)
         self.vol = torch.empty((self.h, self.w, cl), dtype=torch.float32, device=dev)
@@ -140,6 +141,7 @@ class Trainer:
                 tuple(params.shape) != tuple(self.params.shape):
             raise ValueError("reload needs the same sinogram and cloud shapes")
         self.meas.copy_(measured)
+        self.loss.prepare(self.meas)
         self.params.copy_(params)
         if m1 is None:
             self.m1.zero_()
