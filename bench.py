@@ -346,6 +346,23 @@ def run_b200(args, cfg):
     dimv = np.array(cfg["dims"])
     span = np.minimum(fl + hv, dimv - 1) - np.maximum(fl - hv, 0) + 1
     contributions = int(np.prod(np.clip(span, 0, None), axis=1).sum())
+    # executed tensor-core work of the forward splat: every (tile, 8-Gaussian
+    # k-step) issues M16 x N256 x K8 MACs three times (3xTF32) -- per-tile
+    # Gaussian counts from the host footprints of the bench cloud
+    lo = np.maximum(fl - hv, 0).astype(np.int64)
+    hi = np.minimum(fl + hv, dimv - 1).astype(np.int64)
+    ok = np.all(hi >= lo, axis=1)
+    tdim = (dimv + 15) // 16
+    t_lo, t_hi = lo[ok] // 16, hi[ok] // 16
+    counts = np.zeros(int(np.prod(tdim)), np.int64)
+    for dz in range(int((t_hi[:, 2] - t_lo[:, 2]).max(initial=0)) + 1):
+        for dy in range(int((t_hi[:, 1] - t_lo[:, 1]).max(initial=0)) + 1):
+            for dx in range(int((t_hi[:, 0] - t_lo[:, 0]).max(initial=0)) + 1):
+                tz, ty, tx = t_lo[:, 2] + dz, t_lo[:, 1] + dy, t_lo[:, 0] + dx
+                m_ = (tz <= t_hi[:, 2]) & (ty <= t_hi[:, 1]) & (tx <= t_hi[:, 0])
+                np.add.at(counts, ((tz * tdim[1] + ty) * tdim[0] + tx)[m_], 1)
+    kslots = int((-(-counts // 8) * 8).sum())
+    tc_flops = 2.0 * 16 * 256 * kslots * 3
     sm_mhz = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["sm_max_mhz"]) \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 1965.0
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
@@ -372,7 +389,15 @@ def run_b200(args, cfg):
              "traffic": int(t["dram_bytes_per_launch"]) if t else None,
              "ms": round(stages[name], 4), "algorithmic_bytes": int(alg[name])}
         sec = stages[name] * 1e-3
-        if name.startswith("fvr"):
+        if name == "fvr_forward":
+            tf = tc_flops / sec / 1e12
+            r["binding"] = {"bound": "tensor", "achieved": round(tf, 2), "peak": 1100.0,
+                            "unit": "TFLOP/s (TF32 mma.sync, 3xTF32 executed)",
+                            "frac": round(tf / 1100.0, 4),
+                            "contributions_per_s": contributions / sec,
+                            "note": "operand preparation (outer products, TF32 splits) and "
+                                    "issue bound the kernel, not the tensor pipe"}
+        elif name.startswith("fvr"):
             r["binding"] = {"bound": "fp32_fma", "achieved": contributions / sec,
                             "peak": fp32_fma, "unit": "contributions/s (1 FFMA each)",
                             "frac": round(contributions / sec / fp32_fma, 4)}
