@@ -16,7 +16,8 @@ if _ROOT not in sys.path:
     sys.path.insert(0, _ROOT)
 
 _impl = importlib.import_module("paper_2411_04844_b200")
-for _name in ("core", "fvr", "projector", "loss", "optim", "densify", "metrics", "phantom"):
+for _name in ("core", "fvr", "projector", "loss", "optim", "densify", "metrics", "phantom", "io",
+              "cli", "distributed"):
     _mod = importlib.import_module(f"paper_2411_04844_b200.{_name}")
     sys.modules[f"{__name__}.{_name}"] = _mod
     globals()[_name] = _mod
