@@ -454,19 +454,18 @@ __global__ void __launch_bounds__(256, 4) k_fvr_fwd(const GRec* __restrict__ rec
     }   // fetch
 }
 
-// tstart[t] = lower_bound(sorted keys, t) for t in [0, nt]; keys >= nt are
-// the empty-slot sentinels, so tstart[nt] = number of real pairs.
+// tstart[t] = lower_bound(sorted keys, t) for t in [0, nt] from the key
+// boundaries: sorted position j starts every tile in (key[j-1], key[j]] (keys
+// >= nt are the empty-slot sentinels, so tstart[nt] = number of real pairs).
+// One coalesced pass; each tile start is written exactly once.
 __global__ void k_tile_starts(const uint32_t* __restrict__ skeys, int64_t np, int64_t nt,
                               uint32_t* __restrict__ tstart, const int* halt) {
     if (halted(halt)) return;
-    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (t > nt) return;
-    int64_t lo = 0, hi = np;
-    while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (skeys[mid] < (uint32_t)t) lo = mid + 1; else hi = mid;
-    }
-    tstart[t] = (uint32_t)lo;
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j > np) return;
+    const int64_t prev = j == 0 ? -1 : (int64_t)min(skeys[j - 1], (uint32_t)nt);
+    const int64_t cur = j == np ? nt : (int64_t)min(skeys[j], (uint32_t)nt);
+    for (int64_t t = prev + 1; t <= cur; ++t) tstart[t] = (uint32_t)j;
 }
 
 // --------------------------------------------------------------------------
@@ -766,7 +765,8 @@ int splatct_fvr_bin(const double* params, int64_t n, int w, int h, int c, int z0
     }
     {   // tile offsets from the sorted keys (sentinels sort last): no atomics
         const size_t ko = L.final_buf ? L.o_k1 : L.o_k0;
-        k_tile_starts<<<(unsigned)((L.nt + 1 + 255) / 256), 256, 0, s>>>(
+        const int64_t npk = n > 0 ? L.np : 0;
+        k_tile_starts<<<(unsigned)((npk + 1 + 255) / 256), 256, 0, s>>>(
             n > 0 ? at<uint32_t>(ws, ko) : nullptr, n > 0 ? L.np : 0, L.nt,
             at<uint32_t>(ws, L.o_tstart), halt);
         SPLATCT_LAUNCH_CK();

@@ -54,65 +54,64 @@ __device__ __forceinline__ T block_excl_scan(T v, T* sh, T* total) {
     return wprefix + inc - v;
 }
 
-template <typename T>
-__global__ void __launch_bounds__(SCAN_NT) k_chunk_sums(const T* __restrict__ in, int64_t n,
-                                                        T* __restrict__ sums) {
-    __shared__ T sh[SCAN_NT / 32];
-    const int64_t base = blockIdx.x * SCAN_CHUNK;
-    T acc = 0;
-    for (int i = threadIdx.x; i < SCAN_CHUNK; i += SCAN_NT) {
-        int64_t g = base + i;
-        if (g < n) acc += in[g];
-    }
-    T tot;
-    block_excl_scan<T, SCAN_NT>(acc, sh, &tot);
-    if (threadIdx.x == 0) sums[blockIdx.x] = tot;
+size_t scan_temp_bytes(int64_t n) {
+    int64_t nb = (n + SCAN_CHUNK - 1) / SCAN_CHUNK;
+    return align_up((size_t)(nb > 0 ? nb : 1) * sizeof(int64_t)) + 256;   // + tile counter
 }
 
-// One CTA scans the chunk sums (exclusive) in place.
-template <typename T>
-__global__ void __launch_bounds__(1024) k_scan_single(T* __restrict__ a, int64_t n) {
-    __shared__ T sh[32];
-    const int64_t per = (n + 1023) / 1024;
-    const int64_t beg = threadIdx.x * per;
-    const int64_t end = beg + per < n ? beg + per : n;
-    T acc = 0;
-    for (int64_t i = beg; i < end; ++i) acc += a[i];
-    T tot;
-    T off = block_excl_scan<T, 1024>(acc, sh, &tot);
-    for (int64_t i = beg; i < end; ++i) {
-        T v = a[i];
-        a[i] = off;
-        off += v;
-    }
-}
+// Single-pass scan with decoupled look-back: each CTA takes the next tile id
+// from a counter (so predecessors are always already running), publishes its
+// aggregate, then walks back over predecessors' aggregates until one
+// publishes an inclusive prefix.  Status words: 2-bit flag | 62-bit value
+// (the scanned arrays are non-negative counts).
+constexpr unsigned long long ST_A = 1ull << 62, ST_P = 2ull << 62, ST_V = ST_A - 1;
 
 template <typename T>
-__global__ void __launch_bounds__(SCAN_NT) k_chunk_scan(const T* __restrict__ in, T* __restrict__ out,
-                                                        int64_t n, const T* __restrict__ offs) {
+__global__ void __launch_bounds__(SCAN_NT) k_scan_lookback(const T* __restrict__ in,
+                                                           T* __restrict__ out, int64_t n,
+                                                           unsigned long long* status,
+                                                           unsigned int* counter) {
     __shared__ T sh[SCAN_NT / 32];
-    const int64_t base = blockIdx.x * SCAN_CHUNK + (int64_t)threadIdx.x * SCAN_PER_THREAD;
+    __shared__ unsigned int s_tile;
+    __shared__ T s_excl;
+    if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
+    __syncthreads();
+    const int64_t tile = s_tile;
+    const int64_t base = tile * SCAN_CHUNK + (int64_t)threadIdx.x * SCAN_PER_THREAD;
     T v[SCAN_PER_THREAD];
     T acc = 0;
 #pragma unroll
     for (int k = 0; k < SCAN_PER_THREAD; ++k) {
-        int64_t g = base + k;
-        v[k] = g < n ? in[g] : T(0);
+        v[k] = base + k < n ? in[base + k] : T(0);
         acc += v[k];
     }
     T tot;
-    T off = block_excl_scan<T, SCAN_NT>(acc, sh, &tot) + offs[blockIdx.x];
+    T off = block_excl_scan<T, SCAN_NT>(acc, sh, &tot);
+    if (threadIdx.x == 0) {
+        T excl = 0;
+        if (tile == 0) {
+            atomicExch(&status[0], ST_P | (unsigned long long)tot);
+        } else {
+            atomicExch(&status[tile], ST_A | (unsigned long long)tot);
+            for (int64_t pred = tile - 1;; --pred) {
+                unsigned long long st;
+                do {
+                    st = atomicAdd(&status[pred], 0ull);
+                } while ((st >> 62) == 0);
+                excl += (T)(st & ST_V);
+                if ((st >> 62) == 2) break;
+            }
+            atomicExch(&status[tile], ST_P | (unsigned long long)(excl + tot));
+        }
+        s_excl = excl;
+    }
+    __syncthreads();
+    off += s_excl;
 #pragma unroll
     for (int k = 0; k < SCAN_PER_THREAD; ++k) {
-        int64_t g = base + k;
-        if (g < n) out[g] = off;
+        if (base + k < n) out[base + k] = off;
         off += v[k];
     }
-}
-
-size_t scan_temp_bytes(int64_t n) {
-    int64_t nb = (n + SCAN_CHUNK - 1) / SCAN_CHUNK;
-    return align_up((size_t)(nb > 0 ? nb : 1) * sizeof(int64_t));
 }
 
 // Whole array in one CTA (n <= SMALL_SCAN): one launch instead of three.
@@ -144,13 +143,12 @@ static int exclusive_scan(const T* in, T* out, int64_t n, void* temp, cudaStream
         SPLATCT_LAUNCH_CK();
         return SPLATCT_OK;
     }
-    int64_t nb = (n + SCAN_CHUNK - 1) / SCAN_CHUNK;
-    T* sums = reinterpret_cast<T*>(temp);
-    k_chunk_sums<T><<<(unsigned)nb, SCAN_NT, 0, s>>>(in, n, sums);
-    SPLATCT_LAUNCH_CK();
-    k_scan_single<T><<<1, 1024, 0, s>>>(sums, nb);
-    SPLATCT_LAUNCH_CK();
-    k_chunk_scan<T><<<(unsigned)nb, SCAN_NT, 0, s>>>(in, out, n, sums);
+    const int64_t nb = (n + SCAN_CHUNK - 1) / SCAN_CHUNK;
+    unsigned long long* status = reinterpret_cast<unsigned long long*>(temp);
+    unsigned int* counter = reinterpret_cast<unsigned int*>(
+        reinterpret_cast<char*>(temp) + align_up((size_t)nb * sizeof(int64_t)));
+    SPLATCT_CK(cudaMemsetAsync(temp, 0, align_up((size_t)nb * sizeof(int64_t)) + 256, s));
+    k_scan_lookback<T><<<(unsigned)nb, SCAN_NT, 0, s>>>(in, out, n, status, counter);
     SPLATCT_LAUNCH_CK();
     return SPLATCT_OK;
 }
