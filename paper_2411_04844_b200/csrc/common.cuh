@@ -76,6 +76,19 @@ __device__ __forceinline__ double block_sum(double v, double* sh /* >= NT/32 */)
     return r;
 }
 
+// Packed FP32 FMA (sm_100 FFMA2): d = a * b + c on both halves; with b a
+// broadcast scalar the compiler uses the .F32 operand form, so one issue slot
+// does two FMAs.
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;"
+        : "=l"(d)
+        : "l"(*reinterpret_cast<const unsigned long long*>(&a)),
+          "l"(*reinterpret_cast<const unsigned long long*>(&b)),
+          "l"(*reinterpret_cast<const unsigned long long*>(&c)));
+    return *reinterpret_cast<float2*>(&d);
+}
+
 // Device-wide exclusive scan helpers (scan.cu).
 size_t scan_temp_bytes(int64_t n);
 int exclusive_scan_i64(const int64_t* in, int64_t* out, int64_t n, void* temp, cudaStream_t s);

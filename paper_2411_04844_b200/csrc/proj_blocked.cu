@@ -195,6 +195,48 @@ __device__ __forceinline__ int sgnf(float d) { return (d > 0.f) - (d < 0.f); }
 constexpr int BS_WARPS = 8;
 constexpr int UNR = 8;    // z-vector gathers in flight per warp (16 measured no faster)
 
+// Per-lane accumulators of the four group rows over the lane's V slices,
+// held as packed pairs so every (row, slice pair) update is one FFMA2.
+template <int V>
+struct Acc4 {
+    static constexpr int P = (V + 1) / 2;
+    float2 a[4][P];
+    __device__ __forceinline__ void zero() {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int q = 0; q < P; ++q) a[k][q] = make_float2(0.f, 0.f);
+    }
+    __device__ __forceinline__ void add(const float4& w, const float (&x)[V]) {
+        if constexpr (V == 1) {
+            a[0][0].x = fmaf(w.x, x[0], a[0][0].x);
+            a[1][0].x = fmaf(w.y, x[0], a[1][0].x);
+            a[2][0].x = fmaf(w.z, x[0], a[2][0].x);
+            a[3][0].x = fmaf(w.w, x[0], a[3][0].x);
+        } else {
+#pragma unroll
+            for (int q = 0; q < P; ++q) {
+                const float2 xv = make_float2(x[2 * q], x[2 * q + 1]);
+                a[0][q] = ffma2(make_float2(w.x, w.x), xv, a[0][q]);
+                a[1][q] = ffma2(make_float2(w.y, w.y), xv, a[1][q]);
+                a[2][q] = ffma2(make_float2(w.z, w.z), xv, a[2][q]);
+                a[3][q] = ffma2(make_float2(w.w, w.w), xv, a[3][q]);
+            }
+        }
+    }
+    __device__ __forceinline__ void row(int k, float (&o)[V]) const {
+        if constexpr (V == 1) {
+            o[0] = a[k][0].x;
+        } else {
+#pragma unroll
+            for (int q = 0; q < P; ++q) {
+                o[2 * q] = a[k][q].x;
+                o[2 * q + 1] = a[k][q].y;
+            }
+        }
+    }
+};
+
 // TV epilogue for one pixel row and the lane's V consecutive slices
 // [zb, zb+V): forward-difference subgradient of loss.tv_loss (loss.py:195-206)
 // with the x/y neighbours loaded as V-vectors and the z neighbours taken from
@@ -296,11 +338,8 @@ __global__ void __launch_bounds__(32 * BS_WARPS, 3) k_bspmm(GroupMap gm, const i
     const int zb = (int)(gw % zsplit) * 32 * V + lane * V;
     const bool zok = zb < c;
     const int zl = zok ? zb : 0;   // keep loads in bounds for idle lanes
-    float acc[4][V];
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-#pragma unroll
-        for (int t = 0; t < V; ++t) acc[k][t] = 0.f;
+    Acc4<V> acc;
+    acc.zero();
     const int64_t b = gptr[g], e = gptr[g + 1];
     // entries of the next batch are prefetched into registers while the
     // current batch is consumed from shared memory
@@ -326,61 +365,37 @@ __global__ void __launch_bounds__(32 * BS_WARPS, 3) k_bspmm(GroupMap gm, const i
 #pragma unroll
             for (int u = 0; u < UNR; ++u) ldvb<V>(X + (int64_t)s_col[wid][jj + u] * c + zl, xv[u]);
 #pragma unroll
-            for (int u = 0; u < UNR; ++u) {
-                const float4 w4 = s_w[wid][jj + u];
-#pragma unroll
-                for (int t = 0; t < V; ++t) {
-                    acc[0][t] = fmaf(w4.x, xv[u][t], acc[0][t]);
-                    acc[1][t] = fmaf(w4.y, xv[u][t], acc[1][t]);
-                    acc[2][t] = fmaf(w4.z, xv[u][t], acc[2][t]);
-                    acc[3][t] = fmaf(w4.w, xv[u][t], acc[3][t]);
-                }
-            }
+            for (int u = 0; u < UNR; ++u) acc.add(s_w[wid][jj + u], xv[u]);
         }
         for (; jj + 4 <= cnt; jj += 4) {
             float xv[4][V];
 #pragma unroll
             for (int u = 0; u < 4; ++u) ldvb<V>(X + (int64_t)s_col[wid][jj + u] * c + zl, xv[u]);
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const float4 w4 = s_w[wid][jj + u];
-#pragma unroll
-                for (int t = 0; t < V; ++t) {
-                    acc[0][t] = fmaf(w4.x, xv[u][t], acc[0][t]);
-                    acc[1][t] = fmaf(w4.y, xv[u][t], acc[1][t]);
-                    acc[2][t] = fmaf(w4.z, xv[u][t], acc[2][t]);
-                    acc[3][t] = fmaf(w4.w, xv[u][t], acc[3][t]);
-                }
-            }
+            for (int u = 0; u < 4; ++u) acc.add(s_w[wid][jj + u], xv[u]);
         }
         for (; jj < cnt; ++jj) {
             float xv[V];
             ldvb<V>(X + (int64_t)s_col[wid][jj] * c + zl, xv);
-            const float4 w4 = s_w[wid][jj];
-#pragma unroll
-            for (int t = 0; t < V; ++t) {
-                acc[0][t] = fmaf(w4.x, xv[t], acc[0][t]);
-                acc[1][t] = fmaf(w4.y, xv[t], acc[1][t]);
-                acc[2][t] = fmaf(w4.z, xv[t], acc[2][t]);
-                acc[3][t] = fmaf(w4.w, xv[t], acc[3][t]);
-            }
+            acc.add(s_w[wid][jj], xv);
         }
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const int64_t row = gm.row(g, k);
         if (row < 0) continue;   // uniform across the warp
-        float o[V];
+        float o[V], ak[V];
+        acc.row(k, ak);
         if constexpr (TV) {
             double tvsum = 0.0;
-            tv_epilogue<V>(tv, row, zb, c, zok, acc[k], o, tvsum);
+            tv_epilogue<V>(tv, row, zb, c, zok, ak, o, tvsum);
             if (zok) stvb<V>(Y + row * c + zb, o);
             if (tv.partial) {   // slot (z-chunk, row): written once, reduced in fixed order
                 tvsum = warp_sum(tvsum);
                 if (lane == 0) tv.partial[(gw % zsplit) * (int64_t)gm.nrows + row] = tvsum;
             }
         } else {
-            if (zok) stvb<V>(Y + row * c + zb, acc[k]);
+            if (zok) stvb<V>(Y + row * c + zb, ak);
         }
     }
 }
