@@ -502,15 +502,15 @@ __device__ __forceinline__ void bwd_moments17(const GRec& r, int xlo, int nx, in
     const float rz16 = (float)(zlo + 16 + zoff - r.fz) - r.dz;
     const float ez16 = has16 ? exp2f(-r.inv2 * rz16 * rz16) : 0.f;
     // x weights: column pair k -> column 2k + hf (main), column lane (17th slice)
-    float wx0[9], wx1[9], wx2[9];
+    float2 wx01[9];   // {e, e r}: one FFMA2 per column
+    float wx2[9];
     uint32_t coff[9];
 #pragma unroll
     for (int k = 0; k < 9; ++k) {
         const int col = 2 * k + hf;
         const float rx = (float)(xlo + col - r.fx) - r.dx;
         const float ex = col < nx ? exp2f(-r.inv2 * rx * rx) : 0.f;
-        wx0[k] = ex;
-        wx1[k] = ex * rx;
+        wx01[k] = make_float2(ex, ex * rx);
         wx2[k] = ex * rx * rx;
         coff[k] = (uint32_t)min(col, nx - 1) * (uint32_t)c;
     }
@@ -538,13 +538,14 @@ __device__ __forceinline__ void bwd_moments17(const GRec& r, int xlo, int nx, in
         }
         const float ry = (float)(ylo + yi - r.fy) - r.dy;
         const float ey = exp2f(-r.inv2 * ry * ry);
-        float C0 = 0.f, C1 = 0.f, C2 = 0.f;
+        float2 C01 = make_float2(0.f, 0.f);
+        float C2 = 0.f;
 #pragma unroll
         for (int k = 0; k < 9; ++k) {
-            C0 = fmaf(wx0[k], u[k], C0);
-            C1 = fmaf(wx1[k], u[k], C1);
+            C01 = ffma2(make_float2(u[k], u[k]), wx01[k], C01);
             C2 = fmaf(wx2[k], u[k], C2);
         }
+        const float C0 = C01.x, C1 = C01.y;
         const float eyry = ey * ry, eyry2 = eyry * ry;
         A0 = fmaf(ey, C0, A0);
         Ax = fmaf(ey, C1, Ax);
