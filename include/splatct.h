@@ -152,14 +152,15 @@ int splatct_proj_adjoint(const int64_t* at_ptr, const int32_t* at_ray, const flo
                          double tv_count, float* out_yxz, double* tv_partial, const int* halt,
                          void* stream);
 
-/* 4-row blocked form of a CSR operator (proj_blocked.cu).  kind 0 groups
- * rows 4g..4g+3 (consecutive rays of A); kind 1 groups the 2x2 pixel quad
- * (2qx+dx, 2qy+dy), k = 2*dy + dx, of A^T on a w x h slice.  A group entry
- * is (column, w[4]) with the member rows' weights (0 where absent), columns
- * ascending -- or, with order_dir (device float[ngroups][2], the group's ray
- * direction; kind 0 only), in march order along that direction so concurrent
- * warps sweep the slice together.  count (synchronous) -> gptr[ngroups+1]
- * and *nb; fill -> gidx, gval (float[nb][4], 16-byte aligned). */
+/* Row-blocked form of a CSR operator (proj_blocked.cu).  kind 0 groups rows
+ * 4g..4g+3 and kind 2 rows 8g..8g+7 (consecutive rays of A); kind 1 groups
+ * the 2x2 pixel quad (2qx+dx, 2qy+dy), k = 2*dy + dx, of A^T on a w x h
+ * slice.  A group entry is (column, w[R]) with the R member rows' weights (0
+ * where absent), columns ascending -- or, with order_dir (device
+ * float[ngroups][2], the group's ray direction; ray groups only), in march
+ * order along that direction so concurrent warps sweep the slice together.
+ * count (synchronous) -> gptr[ngroups+1] and *nb; fill -> gidx, gval
+ * (float[nb][R], 16-byte aligned). */
 int splatct_proj_block_scratch_bytes(int nrows, int kind, int w, int h, size_t* bytes);
 int splatct_proj_block_count(const int64_t* ptr, const int32_t* idx, int nrows, int kind, int w,
                              int h, const float* order_dir, int64_t* gptr, void* scratch,
@@ -176,9 +177,9 @@ int splatct_proj_tv_partial_len(int w, int h, int c, int64_t* len);
 
 /* Blocked applications: same results as splatct_proj_forward /
  * splatct_proj_adjoint (up to f32 summation order), one z-column load per
- * group entry feeding four rows. */
+ * group entry feeding the group's rows (forward: kind 0 or 2 groups). */
 int splatct_proj_forward_blocked(const int64_t* gptr, const int32_t* gidx, const float* gval,
-                                 int n_rays, const float* vol_yxz, float* sino, int c,
+                                 int n_rays, int kind, const float* vol_yxz, float* sino, int c,
                                  const int* halt, void* stream);
 int splatct_proj_adjoint_blocked(const int64_t* gptr, const int32_t* gidx, const float* gval,
                                  int w, int h, int c, const float* gsino, const float* vol_yxz,

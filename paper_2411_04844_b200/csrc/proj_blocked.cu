@@ -23,15 +23,17 @@ constexpr int BLK_NT = 256;
 constexpr int BLK_CAP = 8192;   // max gathered entries per group (4 rows)
 
 struct GroupMap {
-    int kind, nrows, w, h;
+    int kind, nrows, w, h;   // kind 0: 4 rays, kind 2: 8 rays, kind 1: 2x2 pixel quads
+    __host__ __device__ int rows() const { return kind == 2 ? 8 : 4; }
     __host__ __device__ int64_t ngroups() const {
         if (kind == 0) return (nrows + 3) / 4;
+        if (kind == 2) return (nrows + 7) / 8;
         return (int64_t)((w + 1) / 2) * ((h + 1) / 2);
     }
-    // member row k (0..3) of group g, or -1
+    // member row k (0..rows()-1) of group g, or -1
     __host__ __device__ int64_t row(int64_t g, int k) const {
-        if (kind == 0) {
-            const int64_t r = 4 * g + k;
+        if (kind == 0 || kind == 2) {
+            const int64_t r = (int64_t)rows() * g + k;
             return r < nrows ? r : -1;
         }
         const int qw = (w + 1) / 2;
@@ -58,17 +60,19 @@ __global__ void __launch_bounds__(BLK_NT) k_block_build(GroupMap gm, const int64
     uint32_t* key = reinterpret_cast<uint32_t*>(smem);            // [cap]
     uint32_t* pay = key + BLK_CAP;                                // [cap] (k << 29 | src)
     float* wv = reinterpret_cast<float*>(pay + BLK_CAP);          // [cap]
-    __shared__ int64_t beg[4], len[4];
+    __shared__ int64_t beg[8], len[8];
     __shared__ int total, nuniq;
     const int64_t g = blockIdx.x;
-    if (threadIdx.x < 4) {
-        const int64_t r = gm.row(g, threadIdx.x);
+    const int NR = gm.rows();
+    if (threadIdx.x < 8) {
+        const int64_t r = (int)threadIdx.x < NR ? gm.row(g, threadIdx.x) : -1;
         beg[threadIdx.x] = r >= 0 ? ptr[r] : 0;
         len[threadIdx.x] = r >= 0 ? ptr[r + 1] - ptr[r] : 0;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        int64_t t = len[0] + len[1] + len[2] + len[3];
+        int64_t t = 0;
+        for (int k = 0; k < NR; ++k) t += len[k];
         if (t > BLK_CAP) {
             atomicExch(overflow, 1);
             t = 0;
@@ -102,7 +106,7 @@ __global__ void __launch_bounds__(BLK_NT) k_block_build(GroupMap gm, const int64
             } else {
                 key[i] = pix;
             }
-            pay[i] = ((uint32_t)k << 29) | (uint32_t)i;
+            pay[i] = ((uint32_t)k << 28) | (uint32_t)i;
             wv[i] = mode == 1 ? val[j] : 0.f;
         } else {
             key[i] = 0xffffffffu;
@@ -138,14 +142,15 @@ __global__ void __launch_bounds__(BLK_NT) k_block_build(GroupMap gm, const int64
             const unsigned m = __ballot_sync(0xffffffffu, head);
             const int pos = base + __popc(m & ((1u << threadIdx.x) - 1u));
             if (head && mode == 1) {
-                float w4[4] = {0.f, 0.f, 0.f, 0.f};
+                float wr[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
                 for (int e = i; e < L && key[e] == key[i]; ++e) {
                     const uint32_t pl = pay[e];
-                    w4[pl >> 29] = wv[pl & 0x1fffffffu];
+                    wr[pl >> 28] = wv[pl & 0x0fffffffu];
                 }
                 const int64_t o = gptr[g] + pos;
                 gidx[o] = (int32_t)(march ? (key[i] & 0x7ffffu) : key[i]);
-                gval[o] = make_float4(w4[0], w4[1], w4[2], w4[3]);
+                gval[o * (NR / 4)] = make_float4(wr[0], wr[1], wr[2], wr[3]);
+                if (NR == 8) gval[o * 2 + 1] = make_float4(wr[4], wr[5], wr[6], wr[7]);
             }
             base += __popc(m);
         }
@@ -195,32 +200,35 @@ __device__ __forceinline__ int sgnf(float d) { return (d > 0.f) - (d < 0.f); }
 constexpr int BS_WARPS = 8;
 constexpr int UNR = 8;    // z-vector gathers in flight per warp (16 measured no faster)
 
-// Per-lane accumulators of the four group rows over the lane's V slices,
-// held as packed pairs so every (row, slice pair) update is one FFMA2.
-template <int V>
-struct Acc4 {
+// Per-lane accumulators of the R group rows over the lane's V slices, held
+// as packed pairs so every (row, slice pair) update is one FFMA2.
+template <int R, int V>
+struct AccR {
     static constexpr int P = (V + 1) / 2;
-    float2 a[4][P];
+    float2 a[R][P];
     __device__ __forceinline__ void zero() {
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
+        for (int k = 0; k < R; ++k)
 #pragma unroll
             for (int q = 0; q < P; ++q) a[k][q] = make_float2(0.f, 0.f);
     }
-    __device__ __forceinline__ void add(const float4& w, const float (&x)[V]) {
-        if constexpr (V == 1) {
-            a[0][0].x = fmaf(w.x, x[0], a[0][0].x);
-            a[1][0].x = fmaf(w.y, x[0], a[1][0].x);
-            a[2][0].x = fmaf(w.z, x[0], a[2][0].x);
-            a[3][0].x = fmaf(w.w, x[0], a[3][0].x);
-        } else {
+    // w: the entry's R row weights as R/4 float4
+    __device__ __forceinline__ void add(const float4* w, const float (&x)[V]) {
 #pragma unroll
-            for (int q = 0; q < P; ++q) {
-                const float2 xv = make_float2(x[2 * q], x[2 * q + 1]);
-                a[0][q] = ffma2(make_float2(w.x, w.x), xv, a[0][q]);
-                a[1][q] = ffma2(make_float2(w.y, w.y), xv, a[1][q]);
-                a[2][q] = ffma2(make_float2(w.z, w.z), xv, a[2][q]);
-                a[3][q] = ffma2(make_float2(w.w, w.w), xv, a[3][q]);
+        for (int k4 = 0; k4 < R / 4; ++k4) {
+            const float4 w4 = w[k4];
+            const float wk[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int k = 4 * k4 + j;
+                if constexpr (V == 1) {
+                    a[k][0].x = fmaf(wk[j], x[0], a[k][0].x);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < P; ++q)
+                        a[k][q] = ffma2(make_float2(wk[j], wk[j]),
+                                        make_float2(x[2 * q], x[2 * q + 1]), a[k][q]);
+                }
             }
         }
     }
@@ -318,19 +326,20 @@ __device__ __forceinline__ void tv_epilogue(const TvB& a, int64_t row, int zb, i
     }
 }
 
-// Warp per (group, z-chunk of 32*V slices); groups of 4 rows share every
+// Warp per (group, z-chunk of 32*V slices); the R rows of a group share every
 // column load.  Entries are staged per warp in shared memory and consumed
-// four at a time (four independent vector loads in flight).
-template <int V, bool TV>
-__global__ void __launch_bounds__(32 * BS_WARPS, 3) k_bspmm(GroupMap gm, const int64_t* __restrict__ gptr,
+// UNR at a time (UNR independent vector loads in flight).
+template <int V, bool TV, int R>
+__global__ void __launch_bounds__(32 * BS_WARPS, R == 8 ? 2 : 3) k_bspmm(GroupMap gm, const int64_t* __restrict__ gptr,
                                                         const int32_t* __restrict__ gidx,
                                                         const float4* __restrict__ gval,
                                                         const float* __restrict__ X,
                                                         float* __restrict__ Y, int c, int zsplit,
                                                         TvB tv, const int* halt) {
     if (halted(halt)) return;
+    constexpr int RW = R / 4;   // float4 weight words per entry
     __shared__ int s_col[BS_WARPS][32];
-    __shared__ float4 s_w[BS_WARPS][32];
+    __shared__ float4 s_w[BS_WARPS][32 * RW];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t gw = blockIdx.x * (int64_t)BS_WARPS + wid;
     const int64_t g = gw / zsplit;
@@ -338,25 +347,30 @@ __global__ void __launch_bounds__(32 * BS_WARPS, 3) k_bspmm(GroupMap gm, const i
     const int zb = (int)(gw % zsplit) * 32 * V + lane * V;
     const bool zok = zb < c;
     const int zl = zok ? zb : 0;   // keep loads in bounds for idle lanes
-    Acc4<V> acc;
+    AccR<R, V> acc;
     acc.zero();
     const int64_t b = gptr[g], e = gptr[g + 1];
     // entries of the next batch are prefetched into registers while the
     // current batch is consumed from shared memory
     int nc = 0;
-    float4 nw = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 nw[RW];
+#pragma unroll
+    for (int q = 0; q < RW; ++q) nw[q] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (b + lane < e) {
         nc = __ldcs(gidx + b + lane);
-        nw = __ldcs(gval + b + lane);
+#pragma unroll
+        for (int q = 0; q < RW; ++q) nw[q] = __ldcs(gval + (b + lane) * RW + q);
     }
     for (int64_t j0 = b; j0 < e; j0 += 32) {
         __syncwarp();
         s_col[wid][lane] = nc;
-        s_w[wid][lane] = nw;
+#pragma unroll
+        for (int q = 0; q < RW; ++q) s_w[wid][lane * RW + q] = nw[q];
         __syncwarp();
         if (j0 + 32 + lane < e) {
             nc = __ldcs(gidx + j0 + 32 + lane);
-            nw = __ldcs(gval + j0 + 32 + lane);
+#pragma unroll
+            for (int q = 0; q < RW; ++q) nw[q] = __ldcs(gval + (j0 + 32 + lane) * RW + q);
         }
         const int cnt = (int)min((int64_t)32, e - j0);
         int jj = 0;
@@ -365,23 +379,23 @@ __global__ void __launch_bounds__(32 * BS_WARPS, 3) k_bspmm(GroupMap gm, const i
 #pragma unroll
             for (int u = 0; u < UNR; ++u) ldvb<V>(X + (int64_t)s_col[wid][jj + u] * c + zl, xv[u]);
 #pragma unroll
-            for (int u = 0; u < UNR; ++u) acc.add(s_w[wid][jj + u], xv[u]);
+            for (int u = 0; u < UNR; ++u) acc.add(&s_w[wid][(jj + u) * RW], xv[u]);
         }
         for (; jj + 4 <= cnt; jj += 4) {
             float xv[4][V];
 #pragma unroll
             for (int u = 0; u < 4; ++u) ldvb<V>(X + (int64_t)s_col[wid][jj + u] * c + zl, xv[u]);
 #pragma unroll
-            for (int u = 0; u < 4; ++u) acc.add(s_w[wid][jj + u], xv[u]);
+            for (int u = 0; u < 4; ++u) acc.add(&s_w[wid][(jj + u) * RW], xv[u]);
         }
         for (; jj < cnt; ++jj) {
             float xv[V];
             ldvb<V>(X + (int64_t)s_col[wid][jj] * c + zl, xv);
-            acc.add(s_w[wid][jj], xv);
+            acc.add(&s_w[wid][jj * RW], xv);
         }
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < R; ++k) {
         const int64_t row = gm.row(g, k);
         if (row < 0) continue;   // uniform across the warp
         float o[V], ak[V];
@@ -407,9 +421,14 @@ static int launch_bspmm_v(const GroupMap& gm, const int64_t* gptr, const int32_t
     const int zsplit = (c + 32 * V - 1) / (32 * V);
     const int64_t warps = gm.ngroups() * zsplit;
     const unsigned grid = (unsigned)((warps + BS_WARPS - 1) / BS_WARPS);
-    k_bspmm<V, TV><<<grid, 32 * BS_WARPS, 0, s>>>(gm, gptr, gidx,
-                                                  reinterpret_cast<const float4*>(gval), X, Y, c,
-                                                  zsplit, tv, halt);
+    if (gm.rows() == 8)
+        k_bspmm<V, TV, 8><<<grid, 32 * BS_WARPS, 0, s>>>(gm, gptr, gidx,
+                                                         reinterpret_cast<const float4*>(gval), X,
+                                                         Y, c, zsplit, tv, halt);
+    else
+        k_bspmm<V, TV, 4><<<grid, 32 * BS_WARPS, 0, s>>>(gm, gptr, gidx,
+                                                         reinterpret_cast<const float4*>(gval), X,
+                                                         Y, c, zsplit, tv, halt);
     SPLATCT_LAUNCH_CK();
     return SPLATCT_OK;
 }
@@ -457,7 +476,8 @@ int splatct_proj_block_scratch_bytes(int nrows, int kind, int w, int h, size_t* 
 int splatct_proj_block_count(const int64_t* ptr, const int32_t* idx, int nrows, int kind, int w,
                              int h, const float* order_dir, int64_t* gptr, void* scratch,
                              size_t scratch_bytes, int64_t* nb, void* stream) {
-    SPLATCT_REQUIRE(kind == 0 || kind == 1, "kind must be 0 (row groups) or 1 (pixel quads)");
+    SPLATCT_REQUIRE(kind == 0 || kind == 1 || kind == 2,
+                    "kind must be 0 (4-ray groups), 1 (pixel quads) or 2 (8-ray groups)");
     GroupMap gm{kind, nrows, w, h};
     const int64_t ng = gm.ngroups();
     size_t need = 0;
@@ -484,7 +504,7 @@ int splatct_proj_block_count(const int64_t* ptr, const int32_t* idx, int nrows, 
     SPLATCT_CK(cudaMemcpyAsync(nb, gptr + ng, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     SPLATCT_CK(cudaMemcpyAsync(&ovf, overflow, sizeof(int), cudaMemcpyDeviceToHost, s));
     SPLATCT_CK(cudaStreamSynchronize(s));
-    SPLATCT_REQUIRE(!ovf, "a 4-row group has more than %d entries", BLK_CAP);
+    SPLATCT_REQUIRE(!ovf, "a row group has more than %d entries", BLK_CAP);
     return SPLATCT_OK;
 }
 
@@ -511,10 +531,11 @@ int splatct_proj_block_fill(const int64_t* ptr, const int32_t* idx, const float*
 }
 
 int splatct_proj_forward_blocked(const int64_t* gptr, const int32_t* gidx, const float* gval,
-                                 int n_rays, const float* vol_yxz, float* sino, int c,
+                                 int n_rays, int kind, const float* vol_yxz, float* sino, int c,
                                  const int* halt, void* stream) {
     SPLATCT_REQUIRE(n_rays >= 0 && c > 0, "invalid sizes");
-    GroupMap gm{0, n_rays, 0, 0};
+    SPLATCT_REQUIRE(kind == 0 || kind == 2, "forward groups are kind 0 or 2");
+    GroupMap gm{kind, n_rays, 0, 0};
     TvB tv{};
     return launch_bspmm<false>(gm, gptr, gidx, gval, vol_yxz, sino, c, tv, halt,
                                as_stream(stream));
