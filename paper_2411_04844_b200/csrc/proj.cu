@@ -120,7 +120,7 @@ struct TvArgs {
     const float* vol;      // yxz, local slab
     const float* halo_lo;  // plane z = -1 ([h*w]) or null
     const float* halo_hi;  // plane z = c ([h*w]) or null
-    double lambda, count;
+    double coef;           // lambda_tv / tv_count
     double* partial;       // per-row sum |forward diffs| (or null)
     int w, h;
 };
@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(256) k_csr_spmm(const int64_t* __restrict__ pt
             if constexpr (TV) {
                 const float v0 = __ldg(tv.vol + row * c + zb[q] + t);
                 const float gt = tv_at(tv, row, zb[q] + t, c, v0, tvsum);
-                o[t] = (float)((double)acc[q][t] + tv.lambda * ((double)gt / tv.count));
+                o[t] = (float)fma((double)gt, tv.coef, (double)acc[q][t]);
             } else {
                 o[t] = acc[q][t];
             }
@@ -445,7 +445,8 @@ int splatct_proj_adjoint(const int64_t* at_ptr, const int32_t* at_ray, const flo
     SPLATCT_REQUIRE(w > 0 && h > 0 && c > 0, "invalid sizes");
     TvArgs tv{};
     tv.vol = vol_yxz; tv.halo_lo = halo_lo; tv.halo_hi = halo_hi;
-    tv.lambda = lambda_tv; tv.count = tv_count; tv.partial = tv_partial; tv.w = w; tv.h = h;
+    tv.coef = tv_count > 0.0 ? lambda_tv / tv_count : 0.0;
+    tv.partial = tv_partial; tv.w = w; tv.h = h;
     const int64_t pix = (int64_t)w * h;
     cudaStream_t s = as_stream(stream);
     if (vol_yxz != nullptr && lambda_tv > 0.0) {

@@ -190,7 +190,7 @@ struct TvB {
     const float* vol;
     const float* halo_lo;
     const float* halo_hi;
-    double lambda, count;
+    double coef;   // lambda_tv / tv_count (one DFMA per voxel instead of a DDIV)
     double* partial;
     int w, h;
 };
@@ -245,84 +245,120 @@ struct AccR {
     }
 };
 
-// TV epilogue for one pixel row and the lane's V consecutive slices
-// [zb, zb+V): forward-difference subgradient of loss.tv_loss (loss.py:195-206)
-// with the x/y neighbours loaded as V-vectors and the z neighbours taken from
-// the adjacent lanes (shuffles) or, at warp/slab edges, from memory / halos.
+// TV epilogue for a whole 2x2 pixel quad (the adjoint's group): the four
+// own z-vectors are loaded once and serve as each other's x / y neighbours,
+// so a lane loads 4 own + at most 8 outside neighbour vectors instead of 20;
+// the quad's TV value is one warp reduction.  Same arithmetic per voxel as
+// the per-row forward-difference subgradient of loss.tv_loss (loss.py:195-206),
+// z neighbours from adjacent lanes (shuffles) or, at warp / slab edges, from
+// memory / halos.
 template <int V>
-__device__ __forceinline__ void tv_epilogue(const TvB& a, int64_t row, int zb, int c, bool zok,
-                                            const float (&acc)[V], float (&o)[V],
-                                            double& tvsum) {
+__device__ __forceinline__ void tv_epilogue_quad(const TvB& a, const GroupMap& gm, int64_t g,
+                                                 int zb, int c, bool zok,
+                                                 const AccR<4, V>& acc, float* __restrict__ Y,
+                                                 double& tvsum) {
     const int lane = threadIdx.x & 31;
-    const int y = (int)(row / a.w), x = (int)(row % a.w);
-    const float* col = a.vol + row * c;
-    float v[V];
-    if (zok) ldvb<V>(col + zb, v);
-    else
+    const int qw = (gm.w + 1) / 2;
+    const int x0 = 2 * (int)(g % qw), y0 = 2 * (int)(g / qw);
+    bool has[4];
+    const float* col[4];
+    float v[4][V];
+    float up_prev[4], dn_next[4];
 #pragma unroll
-        for (int t = 0; t < V; ++t) v[t] = 0.f;
-    // z neighbours across lanes (all lanes execute the shuffles)
-    const float up_prev = __shfl_up_sync(0xffffffffu, v[V - 1], 1);
-    const float dn_next = __shfl_down_sync(0xffffffffu, v[0], 1);
+    for (int k = 0; k < 4; ++k) {
+        const int x = x0 + (k & 1), y = y0 + (k >> 1);
+        has[k] = x < gm.w && y < gm.h;
+        col[k] = a.vol + ((int64_t)y * gm.w + x) * c;
+        if (has[k] && zok) ldvb<V>(col[k] + zb, v[k]);
+        else
+#pragma unroll
+            for (int t = 0; t < V; ++t) v[k][t] = 0.f;
+        up_prev[k] = __shfl_up_sync(0xffffffffu, v[k][V - 1], 1);
+        dn_next[k] = __shfl_down_sync(0xffffffffu, v[k][0], 1);
+    }
     if (!zok) return;
-    int g[V];
-    float s1[V];
 #pragma unroll
-    for (int t = 0; t < V; ++t) { g[t] = 0; s1[t] = 0.f; }
-    auto along = [&](const float* nb_col, bool has_next, bool has_prev, const float* pb_col) {
-        if (has_next) {
-            float n[V];
-            ldvb<V>(nb_col + zb, n);
+    for (int k = 0; k < 4; ++k) {
+        if (!has[k]) continue;   // warp-uniform
+        const int dx = k & 1, dy = k >> 1;
+        const int x = x0 + dx, y = y0 + dy;
+        int gs[V];
+        float s1[V];
 #pragma unroll
-            for (int t = 0; t < V; ++t) {
-                const float d = n[t] - v[t];
-                s1[t] += fabsf(d);
-                g[t] -= sgnf(d);
+        for (int t = 0; t < V; ++t) { gs[t] = 0; s1[t] = 0.f; }
+        // one axis: forward difference to the next neighbour, subgradient from
+        // the previous one; in-quad neighbours come from registers
+        auto axis = [&](bool has_next, int kn, const float* ncol, bool has_prev, int kp,
+                        const float* pcol) {
+            if (has_next) {
+                float n[V];
+                if (kn >= 0) {
+#pragma unroll
+                    for (int t = 0; t < V; ++t) n[t] = v[kn][t];
+                } else {
+                    ldvb<V>(ncol + zb, n);
+                }
+#pragma unroll
+                for (int t = 0; t < V; ++t) {
+                    const float d = n[t] - v[k][t];
+                    s1[t] += fabsf(d);
+                    gs[t] -= sgnf(d);
+                }
             }
-        }
-        if (has_prev) {
-            float p[V];
-            ldvb<V>(pb_col + zb, p);
+            if (has_prev) {
+                float pv[V];
+                if (kp >= 0) {
 #pragma unroll
-            for (int t = 0; t < V; ++t) g[t] += sgnf(v[t] - p[t]);
-        }
-    };
-    along(col + c, x + 1 < a.w, x > 0, col - c);
-    along(col + (int64_t)a.w * c, y + 1 < a.h, y > 0, col - (int64_t)a.w * c);
-    // z direction
+                    for (int t = 0; t < V; ++t) pv[t] = v[kp][t];
+                } else {
+                    ldvb<V>(pcol + zb, pv);
+                }
 #pragma unroll
-    for (int t = 0; t < V; ++t) {
-        const int z = zb + t;
-        float zn = 0.f;
-        bool hn = true;
-        if (t + 1 < V) {
-            zn = v[t + 1];
-        } else if (z + 1 < c) {
-            zn = lane < 31 ? dn_next : __ldg(col + z + 1);
-        } else if (a.halo_hi) {
-            zn = __ldg(a.halo_hi + row);
-        } else {
-            hn = false;
+                for (int t = 0; t < V; ++t) gs[t] += sgnf(v[k][t] - pv[t]);
+            }
+        };
+        axis(x + 1 < gm.w, dx == 0 ? k + 1 : -1, col[k] + c, x > 0, dx == 1 ? k - 1 : -1,
+             col[k] - c);
+        axis(y + 1 < gm.h, dy == 0 ? k + 2 : -1, col[k] + (int64_t)gm.w * c, y > 0,
+             dy == 1 ? k - 2 : -1, col[k] - (int64_t)gm.w * c);
+        const int64_t row = (int64_t)y * gm.w + x;
+        float ak[V], o[V];
+        acc.row(k, ak);
+#pragma unroll
+        for (int t = 0; t < V; ++t) {
+            const int z = zb + t;
+            float zn = 0.f;
+            bool hn = true;
+            if (t + 1 < V) {
+                zn = v[k][t + 1];
+            } else if (z + 1 < c) {
+                zn = lane < 31 ? dn_next[k] : __ldg(col[k] + z + 1);
+            } else if (a.halo_hi) {
+                zn = __ldg(a.halo_hi + row);
+            } else {
+                hn = false;
+            }
+            if (hn) {
+                const float d = zn - v[k][t];
+                s1[t] += fabsf(d);
+                gs[t] -= sgnf(d);
+            }
+            float zp = 0.f;
+            bool hp = true;
+            if (t > 0) {
+                zp = v[k][t - 1];
+            } else if (z > 0) {
+                zp = lane > 0 ? up_prev[k] : __ldg(col[k] + z - 1);
+            } else if (a.halo_lo) {
+                zp = __ldg(a.halo_lo + row);
+            } else {
+                hp = false;
+            }
+            if (hp) gs[t] += sgnf(v[k][t] - zp);
+            o[t] = (float)fma((double)gs[t], a.coef, (double)ak[t]);
+            tvsum += (double)s1[t];
         }
-        if (hn) {
-            const float d = zn - v[t];
-            s1[t] += fabsf(d);
-            g[t] -= sgnf(d);
-        }
-        float zp = 0.f;
-        bool hp = true;
-        if (t > 0) {
-            zp = v[t - 1];
-        } else if (z > 0) {
-            zp = lane > 0 ? up_prev : __ldg(col + z - 1);
-        } else if (a.halo_lo) {
-            zp = __ldg(a.halo_lo + row);
-        } else {
-            hp = false;
-        }
-        if (hp) g[t] += sgnf(v[t] - zp);
-        o[t] = (float)((double)acc[t] + a.lambda * ((double)g[t] / a.count));
-        tvsum += (double)s1[t];
+        stvb<V>(Y + row * c + zb, o);
     }
 }
 
@@ -394,21 +430,20 @@ __global__ void __launch_bounds__(32 * BS_WARPS, R == 8 ? 2 : 3) k_bspmm(GroupMa
             acc.add(&s_w[wid][jj * RW], xv);
         }
     }
+    if constexpr (TV) {   // TV groups are the adjoint's 2x2 pixel quads (R == 4)
+        double tvsum = 0.0;
+        tv_epilogue_quad<V>(tv, gm, g, zb, c, zok, acc, Y, tvsum);
+        if (tv.partial) {   // slot (z-chunk, quad): written once, reduced in fixed order
+            tvsum = warp_sum(tvsum);
+            if (lane == 0) tv.partial[(gw % zsplit) * (int64_t)gm.nrows + g] = tvsum;
+        }
+    } else {
 #pragma unroll
-    for (int k = 0; k < R; ++k) {
-        const int64_t row = gm.row(g, k);
-        if (row < 0) continue;   // uniform across the warp
-        float o[V], ak[V];
-        acc.row(k, ak);
-        if constexpr (TV) {
-            double tvsum = 0.0;
-            tv_epilogue<V>(tv, row, zb, c, zok, ak, o, tvsum);
-            if (zok) stvb<V>(Y + row * c + zb, o);
-            if (tv.partial) {   // slot (z-chunk, row): written once, reduced in fixed order
-                tvsum = warp_sum(tvsum);
-                if (lane == 0) tv.partial[(gw % zsplit) * (int64_t)gm.nrows + row] = tvsum;
-            }
-        } else {
+        for (int k = 0; k < R; ++k) {
+            const int64_t row = gm.row(g, k);
+            if (row < 0) continue;   // uniform across the warp
+            float ak[V];
+            acc.row(k, ak);
             if (zok) stvb<V>(Y + row * c + zb, ak);
         }
     }
@@ -421,8 +456,8 @@ static int launch_bspmm_v(const GroupMap& gm, const int64_t* gptr, const int32_t
     const int zsplit = (c + 32 * V - 1) / (32 * V);
     const int64_t warps = gm.ngroups() * zsplit;
     const unsigned grid = (unsigned)((warps + BS_WARPS - 1) / BS_WARPS);
-    if (gm.rows() == 8)
-        k_bspmm<V, TV, 8><<<grid, 32 * BS_WARPS, 0, s>>>(gm, gptr, gidx,
+    if (!TV && gm.rows() == 8)
+        k_bspmm<V, false, 8><<<grid, 32 * BS_WARPS, 0, s>>>(gm, gptr, gidx,
                                                          reinterpret_cast<const float4*>(gval), X,
                                                          Y, c, zsplit, tv, halt);
     else
@@ -548,7 +583,8 @@ int splatct_proj_adjoint_blocked(const int64_t* gptr, const int32_t* gidx, const
                                  const int* halt, void* stream) {
     SPLATCT_REQUIRE(w > 0 && h > 0 && c > 0, "invalid sizes");
     GroupMap gm{1, w * h, w, h};
-    TvB tv{vol_yxz, halo_lo, halo_hi, lambda_tv, tv_count, tv_partial, w, h};
+    TvB tv{vol_yxz, halo_lo, halo_hi, tv_count > 0.0 ? lambda_tv / tv_count : 0.0, tv_partial,
+           w, h};
     cudaStream_t s = as_stream(stream);
     if (vol_yxz != nullptr && lambda_tv > 0.0) {
         SPLATCT_REQUIRE(tv_count > 0.0, "tv_count must be positive");
