@@ -489,6 +489,7 @@ constexpr int BG_XC = 17;   // box columns per register row (default box 17^3)
 // slice of the box is one lanes-over-columns load per row.  Lane-private x
 // tables (9 pairs x {e, e r, e r^2}) stay in registers, the two halves are
 // combined once per Gaussian.  Same moments as the general path below.
+template <bool PF>   // PF: prefetch the next row (register-hungry; more ILP)
 __device__ __forceinline__ void bwd_moments17(const GRec& r, int xlo, int nx, int ylo, int ny,
                                               int zlo, int nz, int w, int c, int zoff,
                                               const float* __restrict__ up, float& S0, float& Sx,
@@ -529,7 +530,14 @@ __device__ __forceinline__ void bwd_moments17(const GRec& r, int xlo, int nx, in
     if (has16) pu = __ldg(prow + poff);
     for (int yi = 0; yi < ny; ++yi) {
         const bool more = yi + 1 < ny;
-        if (more) {   // prefetch the next row
+        if (!PF && yi > 0) {   // load this row now
+            row += rstride;
+            prow += rstride;
+#pragma unroll
+            for (int k = 0; k < 9; ++k) u[k] = zok ? __ldg(row + coff[k]) : 0.f;
+            if (has16) pu = __ldg(prow + poff);
+        }
+        if (PF && more) {   // prefetch the next row
             row += rstride;
             prow += rstride;
 #pragma unroll
@@ -555,7 +563,7 @@ __device__ __forceinline__ void bwd_moments17(const GRec& r, int xlo, int nx, in
         Qx = fmaf(ey * wp1, pu, Qx);
         Qy = fmaf(eyry * wp0, pu, Qy);
         Qr = fmaf(fmaf(ey, wp2, eyry2 * wp0), pu, Qr);
-        if (more) {
+        if (PF && more) {
 #pragma unroll
             for (int k = 0; k < 9; ++k) u[k] = un[k];
             pu = pn;
@@ -581,7 +589,10 @@ __device__ __forceinline__ void bwd_moments17(const GRec& r, int xlo, int nx, in
     S2 = fmaf(ez16, fmaf(rz16 * rz16, Q0, Qr), S2);
 }
 
-__global__ void __launch_bounds__(32 * BG_WARPS, 2) k_fvr_bwd(const double* __restrict__ P, int64_t n,
+// FAST: every box is at most 17 columns x 17 slices (box halves hx, hz <= 8),
+// so only the column-pair path is compiled (its own register budget).
+template <bool FAST>
+__global__ void __launch_bounds__(32 * BG_WARPS, FAST ? 3 : 2) k_fvr_bwd(const double* __restrict__ P, int64_t n,
                                                           const int32_t* __restrict__ fp,
                                                           const GRec* __restrict__ rec, int w,
                                                           int h, int c, int zoff,
@@ -598,10 +609,12 @@ __global__ void __launch_bounds__(32 * BG_WARPS, 2) k_fvr_bwd(const double* __re
     const int xlo = fp[6 * i], xhi = fp[6 * i + 1], ylo = fp[6 * i + 2], yhi = fp[6 * i + 3];
     const int zlo = fp[6 * i + 4], zhi = fp[6 * i + 5];
     float S0 = 0.f, Sx = 0.f, Sy = 0.f, Sz = 0.f, S2 = 0.f;
-    if (xlo <= xhi && ylo <= yhi && zlo <= zhi && xhi - xlo < 17 && zhi - zlo < 17) {
-        const GRec r = rec[i];
-        bwd_moments17(r, xlo, xhi - xlo + 1, ylo, yhi - ylo + 1, zlo, zhi - zlo + 1, w, c, zoff,
-                      up, S0, Sx, Sy, Sz, S2);
+    if (FAST || (xlo <= xhi && ylo <= yhi && zlo <= zhi && xhi - xlo < 17 && zhi - zlo < 17)) {
+        if (xlo <= xhi && ylo <= yhi && zlo <= zhi) {
+            const GRec r = rec[i];
+            bwd_moments17<!FAST>(r, xlo, xhi - xlo + 1, ylo, yhi - ylo + 1, zlo, zhi - zlo + 1, w,
+                                 c, zoff, up, S0, Sx, Sy, Sz, S2);
+        }
     } else if (xlo <= xhi && ylo <= yhi && zlo <= zhi) {
         const GRec r = rec[i];
         for (int zc = zlo; zc <= zhi; zc += 32) {
@@ -800,9 +813,15 @@ int splatct_fvr_backward(const double* params, int64_t n, int w, int h, int c, i
     if (int e = check_args(n, w, h, c, hx, hy, hz, ws_bytes, L)) return e;
     if (n == 0) return SPLATCT_OK;
     cudaStream_t s = as_stream(stream);
-    k_fvr_bwd<<<(unsigned)((n + BG_WARPS - 1) / BG_WARPS), 32 * BG_WARPS, 0, s>>>(
-        params, n, at<int32_t>(ws, L.o_fp), at<GRec>(ws, L.o_rec), w, h, c, z0, up_yxz, grads,
-        accum, halt);
+    const unsigned grid = (unsigned)((n + BG_WARPS - 1) / BG_WARPS);
+    if (2 * hx + 1 <= 17 && 2 * hz + 1 <= 17)
+        k_fvr_bwd<true><<<grid, 32 * BG_WARPS, 0, s>>>(params, n, at<int32_t>(ws, L.o_fp),
+                                                       at<GRec>(ws, L.o_rec), w, h, c, z0, up_yxz,
+                                                       grads, accum, halt);
+    else
+        k_fvr_bwd<false><<<grid, 32 * BG_WARPS, 0, s>>>(params, n, at<int32_t>(ws, L.o_fp),
+                                                        at<GRec>(ws, L.o_rec), w, h, c, z0,
+                                                        up_yxz, grads, accum, halt);
     SPLATCT_LAUNCH_CK();
     return SPLATCT_OK;
 }
