@@ -421,6 +421,14 @@ __global__ void __launch_bounds__(R_NT, MODE == 1 ? 2 : 1) k_ssim_stats11(const 
             convert(v);
             issue(v + 2);         // my landing slot of row v-1 is free (converted last step)
             __syncthreads();      // row v (f64) complete; everyone is past row v-2's reads
+            // MODE 1: the reference window moments of output row v-10, loaded
+            // before the row's arithmetic so their latency overlaps it
+            double rs_my = 0.0, rs_y2 = 0.0;
+            if (MODE == 1 && v >= 10 && act) {
+                const int64_t o = ((int64_t)(v - 10) * vc + j) * p + z;
+                rs_my = RS[o];
+                rs_y2 = RS[plane + o];
+            }
             const double* xr = &sd[v & 1][0][cl][lane];
             const double* yr = &sd[v & 1][1][cl][lane];
             double h[2][NF];
@@ -467,8 +475,8 @@ __global__ void __launch_bounds__(R_NT, MODE == 1 ? 2 : 1) k_ssim_stats11(const 
                 } else {
                     const double mx = a[0][0] + a[1][0], x2w = a[0][1] + a[1][1],
                                  xyw = a[0][2] + a[1][2];
-                    const double my = MODE == 0 ? a[0][3] + a[1][3] : RS[o];
-                    const double y2w = MODE == 0 ? a[0][4] + a[1][4] : RS[plane + o];
+                    const double my = MODE == 0 ? a[0][3] + a[1][3] : rs_my;
+                    const double y2w = MODE == 0 ? a[0][4] + a[1][4] : rs_y2;
                     const double sx2 = x2w - mx * mx, sy2 = y2w - my * my, sxy = xyw - mx * my;
                     const double a1 = 2.0 * mx * my + c1, a2 = 2.0 * sxy + c2;
                     const double b1 = mx * mx + my * my + c1, b2 = sx2 + sy2 + c2;
