@@ -325,7 +325,10 @@ __global__ void __launch_bounds__(PT) k_loss_gv(const float* __restrict__ X, con
 constexpr int R_COLS = 8;                 // output columns per block
 constexpr int R_SPAN = R_COLS + 10;       // staged input columns
 constexpr int R_NT = 32 * R_COLS;
-constexpr int R_BUF = 3;                  // staged rows in flight
+constexpr int R_AHEAD = 2;                // rows staged ahead of the compute (3 measured no faster)
+constexpr int R_BUF = R_AHEAD + 1;        // staging ring depth
+constexpr int G_AHEAD = 2;                // gradient kernel (48 KB static smem bound)
+constexpr int G_BUF = G_AHEAD + 1;
 
 __device__ __forceinline__ void cp16_zfill(void* smem, const void* gmem, bool valid) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -408,8 +411,8 @@ __global__ void __launch_bounds__(R_NT, MODE == 1 ? 2 : 1) k_ssim_stats11(const 
             d2[1] = make_double2((double)f.z, (double)f.w);
         }
     };
-    issue(0);
-    issue(1);
+#pragma unroll
+    for (int q = 0; q < R_AHEAD; ++q) issue(q);
     double ring[11][NF];
     double ssum = 0.0;
     for (int v0 = 0; v0 < m; v0 += 11) {
@@ -417,9 +420,9 @@ __global__ void __launch_bounds__(R_NT, MODE == 1 ? 2 : 1) k_ssim_stats11(const 
         for (int ph = 0; ph < 11; ++ph) {
             const int v = v0 + ph;
             if (v >= m) break;
-            cp_wait_group<1>();   // my chunks of row v landed (row v+1 may be in flight)
+            cp_wait_group<R_AHEAD - 1>();   // my chunks of row v landed (later rows in flight)
             convert(v);
-            issue(v + 2);         // my landing slot of row v-1 is free (converted last step)
+            issue(v + R_AHEAD);   // my landing slot of row v-1 is free (converted last step)
             __syncthreads();      // row v (f64) complete; everyone is past row v-2's reads
             // MODE 1: the reference window moments of output row v-10, loaded
             // before the row's arithmetic so their latency overlaps it
@@ -511,8 +514,8 @@ __global__ void __launch_bounds__(R_NT, 2) k_loss_grad11(const float* __restrict
                                                          const int* halt) {
     if (halted(halt)) return;
     // per staged row: D columns s0-10 .. s0+7 (3 fields) and x, y columns s0 .. s0+7
-    __shared__ __align__(16) double sd[R_BUF][3][R_SPAN][32];
-    __shared__ __align__(16) float sxy[R_BUF][2][R_COLS][32];
+    __shared__ __align__(16) double sd[G_BUF][3][R_SPAN][32];
+    __shared__ __align__(16) float sxy[G_BUF][2][R_COLS][32];
     __shared__ double red[R_NT / 32];
     const int lane = threadIdx.x & 31, cl = threadIdx.x >> 5;
     const int zb = blockIdx.x * 32, s0 = blockIdx.y * R_COLS;
@@ -546,7 +549,7 @@ __global__ void __launch_bounds__(R_NT, 2) k_loss_grad11(const float* __restrict
     const int64_t drow = (int64_t)vc * p, xrowstride = (int64_t)n * p;
     auto issue = [&](int r) {
         if (r < m) {
-            const int buf = r % R_BUF;
+            const int buf = r % G_BUF;
             if (ss && r < vr) {
                 double* db = &sd[buf][0][0][0];
 #pragma unroll
@@ -558,8 +561,8 @@ __global__ void __launch_bounds__(R_NT, 2) k_loss_grad11(const float* __restrict
         }
         cp_commit_group();
     };
-    issue(0);
-    issue(1);
+#pragma unroll
+    for (int q = 0; q < G_AHEAD; ++q) issue(q);
     double ring[11][3];
 #pragma unroll
     for (int q = 0; q < 11; ++q) ring[q][0] = ring[q][1] = ring[q][2] = 0.0;
@@ -569,10 +572,10 @@ __global__ void __launch_bounds__(R_NT, 2) k_loss_grad11(const float* __restrict
         for (int ph = 0; ph < 11; ++ph) {
             const int r = r0 + ph;
             if (r >= m) break;
-            cp_wait_group<1>();
+            cp_wait_group<G_AHEAD - 1>();
             __syncthreads();
-            issue(r + 2);
-            const int buf = r % R_BUF;
+            issue(r + G_AHEAD);
+            const int buf = r % G_BUF;
             if (ss && r < vr) {
                 double t[2][3] = {{0, 0, 0}, {0, 0, 0}};
 #pragma unroll
