@@ -16,10 +16,10 @@
 //
 // B200 design.  Setup (once per geometry): the f64 march into a
 // column-major entry list {pixel, w, tau} and its per-pixel transpose
-// {column, w, tau, 1/tau} sorted by (column, entry).  Forward: one warp per
-// (column, 32 detector rows), lanes over rows; every entry is a shared-memory
-// broadcast and the lanes' two z-taps hit a short contiguous stretch of the
-// pixel's (yxz) z-column.  Adjoint: one warp per (pixel, z window), lanes
+// {column, w, tau, 1/tau} sorted by (column, entry).  Forward: one CTA per
+// detector column (16 warps x 32 rows), the column's entries staged once in
+// shared memory and broadcast to every row; the lanes' two z-taps hit a short
+// contiguous stretch of the pixel's (yxz) z-column.  Adjoint: one warp per (pixel, z window), lanes
 // over the detector rows of each entry (coalesced dL/dpred loads); each row
 // adds its two tap contributions into per-warp shared-memory z accumulators,
 // one per (row residue mod P, tap) class with P tau sv > 1, so no two lanes
@@ -119,55 +119,65 @@ __global__ void k_cone_esort(int64_t npix, const int64_t* __restrict__ eptr,
     }
 }
 
+// Integer cell and fraction of a z coordinate without the conversion pipe:
+// (z - 1/2) rounded to nearest by the 1.5*2^23 trick.  The cell is floor(z)
+// except at exact integers, where it may be z - 1 with fraction 1 -- the same
+// interpolated value (the adjoint's floor cell gives the same nonzero taps).
+// |z| < 2^22.
+__device__ __forceinline__ int zcell(float z, float& fz) {
+    const float t = __fadd_rn(__fadd_rn(z, -0.5f), 12582912.0f);
+    fz = __fadd_rn(z, -__fadd_rn(t, -12582912.0f));
+    return __float_as_int(t) - 0x4B400000;
+}
+
 // --------------------------------------------------------------------------
-// forward: warp per (column, 32 detector rows)
+// forward: one CTA per (column, up to CONE_WARPS x 32 detector rows); the
+// column's entries are staged in shared memory once per CTA (every row of the
+// column reads the same entries) and each warp walks them for its 32 rows
 // --------------------------------------------------------------------------
-constexpr int CONE_WARPS = 8;
+constexpr int CONE_WARPS = 16;
+constexpr int CONE_BATCH = 128;   // entries staged per round
 
 __global__ void __launch_bounds__(32 * CONE_WARPS) k_cone_fwd(
     const ConeColEntry* __restrict__ CE, const int64_t* __restrict__ cptr,
     const float* __restrict__ invL, int nrays, int nv, float sv, float step, int cl, float zc,
     const float* __restrict__ vol, float* __restrict__ sino, const int* halt) {
     if (halted(halt)) return;
-    __shared__ float4 sb[CONE_WARPS][32];
+    __shared__ float4 sb[CONE_BATCH];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    // warps of a CTA take adjacent detector columns of the same row chunk:
-    // their rays cross nearly the same pixels at the same heights (L1 reuse)
     const int chunks = (nv + 31) / 32;
-    const int64_t gw = blockIdx.x * (int64_t)CONE_WARPS + wid;
-    const int64_t r = gw % nrays;
-    if (gw / nrays >= chunks) return;
-    const int dv = (int)(gw / nrays) * 32 + lane;
+    const int cgroups = (chunks + CONE_WARPS - 1) / CONE_WARPS;
+    const int64_t r = blockIdx.x / cgroups;
+    const int chunk = (int)(blockIdx.x % cgroups) * CONE_WARPS + wid;
+    const int dv = chunk * 32 + lane;
     const float vmid = 0.5f * (float)(nv - 1);
     const float v = ((float)dv - vmid) * sv;
     const int64_t b = cptr[r], e = cptr[r + 1];
     float acc = 0.f;
     bool any = false;
-    if (b < e) {   // rows whose z-path misses the slab entirely skip the march
+    if (b < e) {   // rows whose z-path misses the slab entirely skip the arithmetic
         const float ta = CE[b].tau, tb = CE[e - 1].tau;
         const float za = __fmaf_rn(v, ta, zc), zb = __fmaf_rn(v, tb, zc);
         const bool hit = dv < nv && !(fmaxf(za, zb) < -1.f || fminf(za, zb) >= (float)cl);
         any = __any_sync(0xffffffffu, hit);
     }
-    if (any) {
-        for (int64_t j0 = b; j0 < e; j0 += 32) {
-            __syncwarp();
-            if (j0 + lane < e) sb[wid][lane] = *reinterpret_cast<const float4*>(CE + j0 + lane);
-            __syncwarp();
-            const int cnt = (int)min((int64_t)32, e - j0);
+    for (int64_t j0 = b; j0 < e; j0 += CONE_BATCH) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < CONE_BATCH && j0 + i < e; i += 32 * CONE_WARPS)
+            sb[i] = *reinterpret_cast<const float4*>(CE + j0 + i);
+        __syncthreads();
+        if (!any) continue;
+        const int cnt = (int)min((int64_t)CONE_BATCH, e - j0);
 #pragma unroll 4
-            for (int jj = 0; jj < cnt; ++jj) {
-                const float4 en = sb[wid][jj];
-                // z taps, clamped into the slab with zero weight outside it
-                const float z = __fmaf_rn(v, en.z, zc);
-                const float zf = floorf(z);
-                const int zi = (int)zf;
-                const float fz = z - zf;
-                const int ia = min(max(zi, 0), cl - 1), ib = min(max(zi + 1, 0), cl - 1);
-                const float wa = zi == ia ? 1.f - fz : 0.f, wb = zi + 1 == ib ? fz : 0.f;
-                const float* col = vol + (int64_t)__float_as_int(en.x) * cl;
-                acc = fmaf(en.y, fmaf(wa, __ldg(col + ia), wb * __ldg(col + ib)), acc);
-            }
+        for (int jj = 0; jj < cnt; ++jj) {
+            const float4 en = sb[jj];
+            // z taps, clamped into the slab with zero weight outside it
+            float fz;
+            const int zi = zcell(__fmaf_rn(v, en.z, zc), fz);
+            const float* col = vol + (int64_t)__float_as_int(en.x) * cl + zi;
+            const float a0 = (unsigned)zi < (unsigned)cl ? __ldg(col) : 0.f;
+            const float a1 = (unsigned)(zi + 1) < (unsigned)cl ? __ldg(col + 1) : 0.f;
+            acc = fmaf(en.y, fmaf(fz, a1 - a0, a0), acc);
         }
     }
     if (dv < nv) {
@@ -237,6 +247,8 @@ __global__ void __launch_bounds__(32 * CA_WARPS) k_cone_adj(
                 const int d = dd + lane;
                 const bool valid = d <= d1;
                 const float v = ((float)d - vmid) * sv;
+                // floor cell: at exact integers this picks the forward's other
+                // (zero-weight) neighbour, so the taps -- and the transpose -- agree
                 const float z = __fmaf_rn(v, tau, zc);
                 const float zf = floorf(z);
                 const int z0 = (int)zf - zb;
@@ -400,10 +412,10 @@ int splatct_cone_forward(const void* col_entries, const int64_t* cptr, const flo
                          void* stream) {
     SPLATCT_REQUIRE(nrays >= 0 && nv > 0 && c_local > 0 && w > 0 && h > 0,
                     "invalid cone forward sizes");
-    const int64_t warps = (int64_t)nrays * ((nv + 31) / 32);
-    if (warps == 0) return SPLATCT_OK;
-    k_cone_fwd<<<(unsigned)((warps + CONE_WARPS - 1) / CONE_WARPS), 32 * CONE_WARPS, 0,
-                 as_stream(stream)>>>(reinterpret_cast<const ConeColEntry*>(col_entries), cptr,
+    const int chunks = (nv + 31) / 32;
+    const int64_t blocks = (int64_t)nrays * ((chunks + CONE_WARPS - 1) / CONE_WARPS);
+    if (blocks == 0) return SPLATCT_OK;
+    k_cone_fwd<<<(unsigned)blocks, 32 * CONE_WARPS, 0, as_stream(stream)>>>(reinterpret_cast<const ConeColEntry*>(col_entries), cptr,
                                       invL, nrays, nv, (float)sv, (float)step, c_local,
                                       (float)zc, vol_yxz, sino, halt);
     SPLATCT_LAUNCH_CK();
