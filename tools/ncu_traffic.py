@@ -12,8 +12,8 @@ import json
 import sys
 
 STAGES = {
-    "proj_forward": ["k_bspmm<4, 0>"],
-    "proj_adjoint_tv": ["k_bspmm<4, 1>"],
+    "proj_forward": ["k_bspmm<4, 0,"],
+    "proj_adjoint_tv": ["k_bspmm<4, 1,"],
     "loss_fused": ["k_ssim_stats11<1>", "k_loss_grad11"],
     "fvr_forward": ["k_fvr_fwd"],
     "fvr_backward": ["k_fvr_bwd"],
