@@ -224,8 +224,12 @@ def run_b200(args, cfg):
                                                    run_reconstruction_sharded, slab_bounds)
     from paper_2411_04844_b200.trainer import NullComm, Trainer
 
-    rank, world = init_from_env("nccl")
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # NCCL over NVLink in production; SPLATCT_DIST_BACKEND=gloo runs the same
+    # multi-rank flow with host-staged collectives (ranks may share a GPU: a
+    # smoke test of the N > 1 path on a one-GPU box, not a measurement)
+    backend = os.environ.get("SPLATCT_DIST_BACKEND", "nccl")
+    rank, world = init_from_env(backend)
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     comm = SlabComm() if world > 1 else NullComm()
@@ -244,10 +248,7 @@ def run_b200(args, cfg):
     tr = Trainer(meas_local, geom, cfg["dims"], box, L.LossWeights(), params, max_iters=1000,
                  slab=s, comm=comm, trace_cap=args.warmup + args.steps + 16)
     tr.initial_volume()
-    use_graph = world == 1
-    done = 0
-    if use_graph:
-        done = tr.capture()
+    done = tr.capture() if world == 1 else tr.capture_segments()
     for _ in range(max(args.warmup - done, 0)):
         tr.step()
     torch.cuda.synchronize()
@@ -426,7 +427,9 @@ def run_b200(args, cfg):
                    "precision": "f32 voxelizer/projector, f64 params/Adam/SSIM statistics",
                    "cache": "per-iteration working set (A, A^T, volume, sinograms) > 126 MB L2; "
                             "no flush",
-                   "parallelism": f"zslab{world}", "cuda_graph": use_graph,
+                   "parallelism": f"zslab{world}",
+                   "cuda_graph": "whole iteration" if world == 1 else
+                                 "GPU segments between eager NCCL collectives",
                    **({"cone_column_entries": op.n_samples, "cone_pixel_entries": op.n_entries}
                       if cone
                       else {"projector_nnz": nnz})},

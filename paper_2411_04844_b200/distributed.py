@@ -121,7 +121,7 @@ def init_from_env(backend: str = "nccl"):
 
 
 def run_reconstruction_sharded(measured, geom, settings, init_cloud, comm=None,
-                               use_graph: bool = False):
+                               use_graph: bool = True):
     """run_reconstruction (optim.py:286-427) over a z-slab-sharded volume.
 
     Every rank calls this with the same host inputs; rank r keeps slices
@@ -151,8 +151,10 @@ def run_reconstruction_sharded(measured, geom, settings, init_cloud, comm=None,
                  lrf=settings.lr_final, max_iters=settings.max_iters, slab=s, comm=comm)
     tr.initial_volume()
     done = 0
-    if use_graph and settings.max_iters > 0 and comm.world == 1:
-        done = tr.capture()
+    if use_graph and settings.max_iters > 0:
+        # one graph per iteration on a single rank; with ranks, graphs for the
+        # GPU segments between the (eager) slab collectives
+        done = tr.capture() if comm.world == 1 else tr.capture_segments()
     for _ in range(done, settings.max_iters):
         tr.step()
     torch.cuda.synchronize()

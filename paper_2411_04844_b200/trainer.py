@@ -130,6 +130,7 @@ class Trainer:
         s = self.slab
         self.fvr = D.FvrPlan(nG, (self.w, self.h, s.c_local), self.box.half, s.z0, dev)
         self.graph = None
+        self.segments = None
 
     def reload(self, measured, params, m1=None, m2=None, step: int = 0, accum=None):
         """Re-initialise the state in place (same shapes and lmax).
@@ -171,47 +172,78 @@ class Trainer:
         self.fvr.bin(self.params, self.halt)
         self.fvr.forward(self.params, self.vol, self.halt)
 
-    def iteration(self):
+    def _stages(self):
+        """The iteration as an ordered list of ("gpu" | "comm", fn) stages.
+
+        GPU stages are stream-ordered kernel launches (graph-capturable); comm
+        stages are the slab collectives, which run eagerly between captured
+        segments when the job is sharded (capture_segments)."""
         lw = self.weights
         halt = self.halt
         z0 = self.slab.z0
-        self.op.forward(self.vol, self.pred, halt, z0=z0)
-        replicated = not self.per_slice and self.comm.world > 1
-        if replicated:
-            self.comm.allreduce_sum_(self.pred)   # partial cone projections -> full
-        if lw.lambda1 > 0 or lw.lambda2 > 0:
-            self.loss.fused(self.pred, self.meas, self.lmax, lw.lambda1, lw.lambda2,
-                            self.l1_count, float(self.p_global), self.gpred, self.sums,
-                            halt)
-            if replicated and self.comm.rank != 0:
-                self.sums[0:2].zero_()   # every rank holds the full loss: count it once
-        else:
-            self.gpred.zero_()
-        if lw.lambda3 > 0:
-            lo, hi = self.comm.halo(self.vol)
-            self.op.adjoint(self.gpred, self.dl, vol=self.vol, halo_lo=lo, halo_hi=hi,
-                            lambda_tv=lw.lambda3, tv_count=self.tv_count,
-                            tv_partial=self.tv_part, halt=halt, z0=z0)
-            D.reduce_sum(self.tv_part, self.sums[2:3])
-        else:
-            self.op.adjoint(self.gpred, self.dl, halt=halt, z0=z0,
-                            c_local=self.slab.c_local)
-        self.comm.allreduce_sum_(self.sums)
-        D.call("splatct_iter_finalize", D.ptr(self.sums), float(lw.lambda1), float(lw.lambda2),
-               float(lw.lambda3), self.l1_count, self.ssim_count, self.tv_count, self.lr0,
-               self.lrf, self.max_iters, D.ptr(self.step_t), D.ptr(self.iter_t),
-               D.ptr(self.trace), self.trace_cap, D.ptr(self.adam_s), D.ptr(halt),
-               D.stream_handle())
         sharded = self.comm.world > 1
-        self.fvr.backward(self.params, self.dl, self.grads, None if sharded else self.accum,
-                          halt)
+        replicated = not self.per_slice and sharded
+        st = []
+
+        def project():
+            self.op.forward(self.vol, self.pred, halt, z0=z0)
+        st.append(("gpu", project))
+        if replicated:   # partial cone projections -> full
+            st.append(("comm", lambda: self.comm.allreduce_sum_(self.pred)))
+
+        def data_loss():
+            if lw.lambda1 > 0 or lw.lambda2 > 0:
+                self.loss.fused(self.pred, self.meas, self.lmax, lw.lambda1, lw.lambda2,
+                                self.l1_count, float(self.p_global), self.gpred, self.sums,
+                                halt)
+                if replicated and self.comm.rank != 0:
+                    self.sums[0:2].zero_()   # every rank holds the full loss: count it once
+            else:
+                self.gpred.zero_()
+        st.append(("gpu", data_loss))
+        if lw.lambda3 > 0:
+            def halo():
+                self._halo = self.comm.halo(self.vol)
+            st.append(("comm", halo))
+
+            def adjoint_tv():
+                lo, hi = self._halo
+                self.op.adjoint(self.gpred, self.dl, vol=self.vol, halo_lo=lo, halo_hi=hi,
+                                lambda_tv=lw.lambda3, tv_count=self.tv_count,
+                                tv_partial=self.tv_part, halt=halt, z0=z0)
+                D.reduce_sum(self.tv_part, self.sums[2:3])
+            st.append(("gpu", adjoint_tv))
+        else:
+            st.append(("gpu", lambda: self.op.adjoint(self.gpred, self.dl, halt=halt, z0=z0,
+                                                      c_local=self.slab.c_local)))
         if sharded:
-            self.comm.allreduce_sum_(self.grads)
-            D.grad_norm_accum(self.grads, self.accum, halt)
-        D.adam(self.params, self.grads, self.m1, self.m2, self.adam_s, SIGMA_FLOOR,
-               self.sigma_ceiling, halt)
-        self.fvr.bin(self.params, halt)
-        self.fvr.forward(self.params, self.vol, halt)
+            st.append(("comm", lambda: self.comm.allreduce_sum_(self.sums)))
+
+        def finalize_backward():
+            D.call("splatct_iter_finalize", D.ptr(self.sums), float(lw.lambda1),
+                   float(lw.lambda2), float(lw.lambda3), self.l1_count, self.ssim_count,
+                   self.tv_count, self.lr0, self.lrf, self.max_iters, D.ptr(self.step_t),
+                   D.ptr(self.iter_t), D.ptr(self.trace), self.trace_cap, D.ptr(self.adam_s),
+                   D.ptr(halt), D.stream_handle())
+            self.fvr.backward(self.params, self.dl, self.grads,
+                              None if sharded else self.accum, halt)
+        st.append(("gpu", finalize_backward))
+        if sharded:
+            st.append(("comm", lambda: self.comm.allreduce_sum_(self.grads)))
+
+        def update_resplat():
+            if sharded:
+                D.grad_norm_accum(self.grads, self.accum, halt)
+            D.adam(self.params, self.grads, self.m1, self.m2, self.adam_s, SIGMA_FLOOR,
+                   self.sigma_ceiling, halt)
+            self.fvr.bin(self.params, halt)
+            self.fvr.forward(self.params, self.vol, halt)
+        st.append(("gpu", update_resplat))
+        return st
+
+    def iteration(self):
+        for _, fn in self._stages():
+            fn()
 
     def capture(self):
         """Capture one iteration as a CUDA graph (runs one real iteration first)."""
@@ -226,9 +258,47 @@ class Trainer:
         self.graph = g
         return 1   # iterations executed
 
+    def capture_segments(self):
+        """Sharded jobs: capture the runs of GPU stages between collectives as
+        CUDA graphs and keep the collectives eager (runs one real iteration
+        first).  A step is then a few graph launches interleaved with the
+        slab collectives instead of ~30 kernel launches."""
+        stages = self._stages()
+        self.iteration()
+        torch.cuda.synchronize(self.device)
+        plan, run = [], []
+
+        def flush():
+            if run:
+                g = torch.cuda.CUDAGraph()
+                side = torch.cuda.Stream(device=self.device)
+                side.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(side):
+                    with torch.cuda.graph(g):
+                        for fn in run:
+                            fn()
+                torch.cuda.current_stream().wait_stream(side)
+                plan.append(("graph", g))
+                run.clear()
+        for kind, fn in stages:
+            if kind == "gpu":
+                run.append(fn)
+            else:
+                flush()
+                plan.append(("comm", fn))
+        flush()
+        self.segments = plan
+        return 1
+
     def step(self):
         if self.graph is not None:
             self.graph.replay()
+        elif getattr(self, "segments", None):
+            for kind, x in self.segments:
+                if kind == "graph":
+                    x.replay()
+                else:
+                    x()
         else:
             self.iteration()
 

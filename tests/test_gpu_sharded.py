@@ -77,3 +77,23 @@ def test_two_slab_ranks_match_single_device(variant):
     v = res[0][1]
     assert np.linalg.norm(v - vol1.zyx) / np.linalg.norm(vol1.zyx) < (1e-6 if variant == "fan"
                                                                       else 1e-5)
+
+
+def test_bench_two_ranks_smoke():
+    """bench.py's N > 1 flow (torchrun, slab sharding, segmented graphs, max-over-ranks
+    timing, sharded e2e) end to end with host-staged gloo collectives on one GPU."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SPLATCT_DIST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+           os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "2", "--warmup", "3",
+           "--no-cpu-baseline", "--config", "c1"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1   # rank 0 only
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
