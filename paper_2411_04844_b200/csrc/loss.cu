@@ -23,6 +23,9 @@
 namespace splatct {
 
 constexpr int KMAX = 11;
+// 11x11 fast path: output columns per block.  7 (224 threads) makes the C2
+// grids 576 / 592 blocks = ~2 full waves of 2 CTAs x 148 SMs (8 gave 1.7).
+constexpr int R_COLS = 7;
 constexpr int LZ = 32;     // slices per CTA (lanes)
 constexpr int LCOL = 4;    // columns per CTA
 constexpr int LNT = LZ * LCOL;
@@ -75,8 +78,8 @@ static LossLayout loss_layout(int m, int n, int p) {
     size_t off = 0;
     auto take = [&](size_t b) { size_t o = off; off += align_up(b > 0 ? b : 1); return o; };
     L.k11 = W.kr == 11 && W.kc == 11 && p % 4 == 0;
-    L.nb_s11 = (int64_t)((p + 31) / 32) * ((L.vc + 7) / 8);
-    L.nb_g11 = (int64_t)((p + 31) / 32) * ((n + 7) / 8);
+    L.nb_s11 = (int64_t)((p + 31) / 32) * ((L.vc + R_COLS - 1) / R_COLS);
+    L.nb_g11 = (int64_t)((p + 31) / 32) * ((n + R_COLS - 1) / R_COLS);
     if (L.k11) {   // row-walking kernels: full-p D, no H/T
         L.o_H = L.o_T = 0;
         L.o_D11 = take(sizeof(double) * 3 * (size_t)L.vr * L.vc * p);
@@ -315,14 +318,13 @@ __global__ void __launch_bounds__(PT) k_loss_gv(const float* __restrict__ X, con
 
 // ---------------------------------------------------------------------------
 // 11 x 11 window fast path (the default: every image with >= 11 views and
-// detectors, p % 4 == 0).  A block owns 32 slices x 8 output columns and walks
-// the view axis.  Input rows (18 columns x 32 slices) are gathered with
+// detectors, p % 4 == 0).  A block owns 32 slices x R_COLS output columns and
+// walks the view axis.  Input rows (R_COLS + 10 columns x 32 slices) are gathered with
 // cp.async into a 3-deep shared-memory ring two rows ahead of the compute, and
 // the last 11 rows of horizontal window sums live in REGISTERS: the row loop
 // is unrolled by 11 so every ring slot is a compile-time index.  f64
 // throughout like loss.py:112-141.
 // ---------------------------------------------------------------------------
-constexpr int R_COLS = 8;                 // output columns per block
 constexpr int R_SPAN = R_COLS + 10;       // staged input columns
 constexpr int R_NT = 32 * R_COLS;
 constexpr int R_AHEAD = 2;                // rows staged ahead of the compute (3 measured no faster)
@@ -342,7 +344,7 @@ __device__ __forceinline__ void cp_wait_group() { asm volatile("cp.async.wait_gr
 // Each thread issues (and later converts) the same 16-byte chunks of every
 // staged row, so the f32 landing buffer is private per chunk: only the
 // converted f64 row (read by 11 neighbouring columns) needs a barrier.
-constexpr int S_CHUNKS = 2 * R_SPAN * 8;                  // x, y: 18 columns x 8 chunks
+constexpr int S_CHUNKS = 2 * R_SPAN * 8;                  // x, y: R_SPAN columns x 8 chunks
 constexpr int S_SLOTS = (S_CHUNKS + R_NT - 1) / R_NT;      // chunks per thread
 
 // MODE 0: all five window moments from X and Y (loss.py:112-141).
@@ -502,7 +504,7 @@ __global__ void __launch_bounds__(R_NT, MODE == 1 ? 2 : 1) k_ssim_stats11(const 
 
 constexpr int G_DCHUNKS = 3 * R_SPAN * 16;                   // D: 3 fields x 18 cols x 16
 constexpr int G_DSLOTS = (G_DCHUNKS + R_NT - 1) / R_NT;
-constexpr int G_XCHUNKS = 2 * R_COLS * 8;                    // x, y: 8 cols x 8 chunks
+constexpr int G_XCHUNKS = 2 * R_COLS * 8;                    // x, y: R_COLS cols x 8 chunks
 
 __global__ void __launch_bounds__(R_NT, 2) k_loss_grad11(const float* __restrict__ X,
                                                          const float* __restrict__ Y, int m, int n,
@@ -769,7 +771,8 @@ static int loss_fused_impl(const float* pred, const float* ref, int m, int n, in
     const bool k11 = L.k11;
     if (k11) {
         double* D11 = reinterpret_cast<double*>(base + L.o_D11);
-        const dim3 gs((p + 31) / 32, (L.vc + 7) / 8), gg((p + 31) / 32, (n + 7) / 8);
+        const dim3 gs((p + 31) / 32, (L.vc + R_COLS - 1) / R_COLS),
+            gg((p + 31) / 32, (n + R_COLS - 1) / R_COLS);
         if (lambda2 > 0.0) {
             double* RS = reinterpret_cast<double*>(base + L.o_RS);
             if (prepared)
@@ -847,7 +850,7 @@ int splatct_loss_prepare_ref(const float* ref, int m, int n, int p, void* ws, si
     if (!L.k11) return SPLATCT_OK;   // the generic path recomputes everything
     Win W = make_win(m, n);
     char* base = reinterpret_cast<char*>(ws);
-    const dim3 gs((p + 31) / 32, (L.vc + 7) / 8);
+    const dim3 gs((p + 31) / 32, (L.vc + R_COLS - 1) / R_COLS);
     k_ssim_stats11<2><<<gs, R_NT, 0, as_stream(stream)>>>(
         nullptr, ref, m, n, p, W, 0.0, 0.0, L.vr, L.vc, nullptr, nullptr,
         reinterpret_cast<double*>(base + L.o_RS), nullptr);
