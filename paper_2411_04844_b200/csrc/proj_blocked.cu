@@ -197,7 +197,7 @@ struct TvB {
 
 __device__ __forceinline__ int sgnf(float d) { return (d > 0.f) - (d < 0.f); }
 
-constexpr int BS_WARPS = 8;
+constexpr int BS_WARPS = 4;
 constexpr int UNR = 8;    // z-vector gathers in flight per warp (16 measured no faster)
 
 // Per-lane accumulators of the R group rows over the lane's V slices, held
@@ -366,7 +366,7 @@ __device__ __forceinline__ void tv_epilogue_quad(const TvB& a, const GroupMap& g
 // column load.  Entries are staged per warp in shared memory and consumed
 // UNR at a time (UNR independent vector loads in flight).
 template <int V, bool TV, int R>
-__global__ void __launch_bounds__(32 * BS_WARPS, R == 8 ? 2 : 3) k_bspmm(GroupMap gm, const int64_t* __restrict__ gptr,
+__global__ void __launch_bounds__(32 * BS_WARPS, R == 8 ? 4 : 6) k_bspmm(GroupMap gm, const int64_t* __restrict__ gptr,
                                                         const int32_t* __restrict__ gidx,
                                                         const float4* __restrict__ gval,
                                                         const float* __restrict__ X,
