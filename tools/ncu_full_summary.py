@@ -21,6 +21,10 @@ KEYS = [
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue_%"),
     ("l1tex__t_sector_hit_rate.pct", "l1_hit_%"),
     ("lts__t_sector_hit_rate.pct", "l2_hit_%"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", "smem_%"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem_bank_conflicts"),
+    ("l1tex__t_set_accesses_pipe_lsu_mem_global_op_atom.sum", "global_atomics"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum", "smem_atomic_wavefronts"),
 ]
 
 
