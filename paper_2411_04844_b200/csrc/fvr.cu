@@ -22,6 +22,9 @@
 //     straight from L2, separable moment contraction (x inner, y outer, z
 //     per lane), warp-shuffle reduction, f64 chain rule; no atomics, no
 //     partial buffers, deterministic.
+#include <cstdlib>
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace splatct {
@@ -52,7 +55,7 @@ struct FvrLayout {
     int passes;
     int64_t sort_blocks;
     size_t o_fp, o_gcount, o_k0, o_v0, o_k1, o_v1, o_tcount, o_tstart, o_hist, o_scan, o_rec,
-        total;
+        o_flag, o_pos, o_order, o_scan2, total;
     int final_buf;    // which (k,v) buffer holds the sorted result
 };
 
@@ -97,6 +100,12 @@ static FvrLayout make_layout(int64_t n, int w, int h, int c, int hx, int hy, int
     size_t sc2 = scan_temp_bytes(L.nt + 1);
     L.o_scan = take(sc1 > sc2 ? sc1 : sc2);
     L.o_rec = take(sizeof(GRec) * (size_t)n);
+    // backward visiting order for volumes that exceed L2 (Gaussians sorted by
+    // their first tile): first-slot flags, their exclusive scan, the list
+    L.o_flag = take(sizeof(uint32_t) * (size_t)(L.np + 1));
+    L.o_pos = take(sizeof(uint32_t) * (size_t)(L.np + 1));
+    L.o_order = take(sizeof(uint32_t) * (size_t)(n + 1));
+    L.o_scan2 = take(scan_temp_bytes(L.np + 1));
     L.total = off;
     L.final_buf = L.passes % 2;   // pass p reads buf p%2, writes (p+1)%2
     return L;
@@ -589,10 +598,31 @@ __device__ __forceinline__ void bwd_moments17(const GRec& r, int xlo, int nx, in
     S2 = fmaf(ez16, fmaf(rz16 * rz16, Q0, Qr), S2);
 }
 
+// flags[j] = 1 for the sorted pair that is its Gaussian's first tile (slot 0)
+__global__ void k_first_flags(const uint32_t* __restrict__ svals, const uint32_t* __restrict__ tstart,
+                              int64_t nt, int64_t np, int S, uint32_t* __restrict__ flags) {
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j > np) return;
+    const uint32_t npairs = tstart[nt];
+    flags[j] = (j < (int64_t)npairs && (svals[j] & ((1u << S) - 1u)) == 0u) ? 1u : 0u;
+}
+
+__global__ void k_order_scatter(const uint32_t* __restrict__ svals,
+                                const uint32_t* __restrict__ flags,
+                                const uint32_t* __restrict__ pos, int64_t np, int S,
+                                uint32_t* __restrict__ order) {
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j > np) return;
+    if (j == np) order[0] = pos[np];                      // count of listed Gaussians
+    else if (flags[j]) order[1 + pos[j]] = svals[j] >> S;
+}
+
 // FAST: every box is at most 17 columns x 17 slices (box halves hx, hz <= 8),
 // so only the column-pair path is compiled (its own register budget).
-template <bool FAST>
+// ORD: visit Gaussians in first-tile order (order[0] = count, order[1..])
+template <bool FAST, bool ORD>
 __global__ void __launch_bounds__(32 * BG_WARPS, FAST ? 3 : 2) k_fvr_bwd(const double* __restrict__ P, int64_t n,
+                                                          const uint32_t* __restrict__ order,
                                                           const int32_t* __restrict__ fp,
                                                           const GRec* __restrict__ rec, int w,
                                                           int h, int c, int zoff,
@@ -604,8 +634,9 @@ __global__ void __launch_bounds__(32 * BG_WARPS, FAST ? 3 : 2) k_fvr_bwd(const d
     __shared__ float xt[3][BG_WARPS][32];   // ex, ex rx, ex rx^2
     __shared__ float2 yt[BG_WARPS][32];   // {ey, ry}
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int64_t i = blockIdx.x * (int64_t)BG_WARPS + wid;
-    if (i >= n) return;   // warp-uniform: only warp-level syncs below
+    const int64_t gw = blockIdx.x * (int64_t)BG_WARPS + wid;
+    if (gw >= (ORD ? (int64_t)order[0] : n)) return;   // warp-uniform: warp-level syncs only
+    const int64_t i = ORD ? (int64_t)order[1 + gw] : gw;
     const int xlo = fp[6 * i], xhi = fp[6 * i + 1], ylo = fp[6 * i + 2], yhi = fp[6 * i + 3];
     const int zlo = fp[6 * i + 4], zhi = fp[6 * i + 5];
     float S0 = 0.f, Sx = 0.f, Sy = 0.f, Sz = 0.f, S2 = 0.f;
@@ -814,14 +845,38 @@ int splatct_fvr_backward(const double* params, int64_t n, int w, int h, int c, i
     if (n == 0) return SPLATCT_OK;
     cudaStream_t s = as_stream(stream);
     const unsigned grid = (unsigned)((n + BG_WARPS - 1) / BG_WARPS);
-    if (2 * hx + 1 <= 17 && 2 * hz + 1 <= 17)
-        k_fvr_bwd<true><<<grid, 32 * BG_WARPS, 0, s>>>(params, n, at<int32_t>(ws, L.o_fp),
-                                                       at<GRec>(ws, L.o_rec), w, h, c, z0, up_yxz,
-                                                       grads, accum, halt);
-    else
-        k_fvr_bwd<false><<<grid, 32 * BG_WARPS, 0, s>>>(params, n, at<int32_t>(ws, L.o_fp),
-                                                        at<GRec>(ws, L.o_rec), w, h, c, z0,
-                                                        up_yxz, grads, accum, halt);
+    // an upstream larger than ~half of L2 is read from HBM: visit the
+    // Gaussians in tile order so neighbouring warps share DRAM pages / lines
+    // (index order spreads concurrent warps out, best while L2-resident)
+    bool ord = (int64_t)w * h * c * 4 > ((int64_t)64 << 20);
+    if (const char* e = getenv("SPLATCT_BWD_ORDER")) ord = atoi(e) != 0;
+    uint32_t* order = at<uint32_t>(ws, L.o_order);
+    if (ord) {
+        const size_t vs = L.final_buf ? L.o_v1 : L.o_v0;    // sorted values
+        uint32_t* flags = at<uint32_t>(ws, L.o_flag);
+        uint32_t* pos = at<uint32_t>(ws, L.o_pos);
+        const unsigned gb = (unsigned)((L.np + 1 + 255) / 256);
+        k_first_flags<<<gb, 256, 0, s>>>(at<uint32_t>(ws, vs), at<uint32_t>(ws, L.o_tstart), L.nt,
+                                         L.np, L.Sl, flags);
+        SPLATCT_LAUNCH_CK();
+        if (int e = exclusive_scan_u32(flags, pos, L.np + 1, at<void>(ws, L.o_scan2), s)) return e;
+        k_order_scatter<<<gb, 256, 0, s>>>(at<uint32_t>(ws, vs), flags, pos, L.np, L.Sl, order);
+        SPLATCT_LAUNCH_CK();
+        SPLATCT_CK(cudaMemsetAsync(grads, 0, sizeof(double) * 5 * (size_t)n, s));   // unlisted
+    }
+    const bool fast = 2 * hx + 1 <= 17 && 2 * hz + 1 <= 17;
+    auto launch = [&](auto fast_c, auto ord_c) {
+        k_fvr_bwd<decltype(fast_c)::value, decltype(ord_c)::value>
+            <<<grid, 32 * BG_WARPS, 0, s>>>(params, n, order, at<int32_t>(ws, L.o_fp),
+                                            at<GRec>(ws, L.o_rec), w, h, c, z0, up_yxz, grads,
+                                            accum, halt);
+    };
+    using T = std::true_type;
+    using F = std::false_type;
+    if (fast && ord) launch(T{}, T{});
+    else if (fast) launch(T{}, F{});
+    else if (ord) launch(F{}, T{});
+    else launch(F{}, F{});
     SPLATCT_LAUNCH_CK();
     return SPLATCT_OK;
 }

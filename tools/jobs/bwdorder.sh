@@ -1,0 +1,21 @@
+# Ordered-backward experiment: parity with the order forced on, then sweeps
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+SPLATCT_BWD_ORDER=1 timeout 900 python -m pytest tests -m gpu -q --timeout 600 -p no:cacheprovider -k "fvr or spec or edges or parity" > gpurun_out/pytest_ord.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_ord.log
+tail -3 gpurun_out/pytest_ord.log
+for o in 0 1; do
+  SPLATCT_BWD_ORDER=$o timeout 600 python tools/voxel_sweep.py --grids 256,512,1024 --ns 400000,2000000 > gpurun_out/sweep_ord$o.jsonl 2>&1
+  SPLATCT_BWD_ORDER=$o timeout 600 python bench.py --steps 30 --warmup 5 --no-cpu-baseline > gpurun_out/bench_ord$o.log 2>&1
+done
+python - <<'PY'
+import json
+for o in (0,1):
+    print("ORDER",o)
+    for l in open(f"gpurun_out/sweep_ord{o}.jsonl"):
+        try: d=json.loads(l)
+        except Exception: continue
+        print({k:d[k] for k in d if k in ("grid","n","fwd_ms","bwd_ms")})
+    for l in open(f"gpurun_out/bench_ord{o}.log"):
+        try: d=json.loads(l); print("bench", d["value"], d["stages_ms"])
+        except Exception: pass
+PY
