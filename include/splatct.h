@@ -307,6 +307,31 @@ int splatct_cone_adjoint(const void* entries, const int64_t* eptr, const float* 
                          double zc, const float* gsino, float* gscaled, float* out_yxz,
                          int accumulate, const int* halt, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Densification on the device: densify.densify_and_prune,
+ * reference densify.py:86-147, plus the Adam-moment remap optim.py:92-106.
+ * params / m1 / m2 are [5, n] f64 (x, y, z, sigma, intensity rows).
+ *  - classify: cls[n] = 0 keep | 1 prune | 2 clone candidate | 3 split
+ *    candidate (densify.py:97-110, avg = accum / iters; sigma_prune = 3 x box
+ *    size); keys[n] = bit pattern of avg; counts[3] = (prune, clone cand.,
+ *    split cand.) -- the host reads them to size the budgets.
+ *  - select: mark (cls += 2) the k highest-avg members of class `which`
+ *    (_limit, densify.py:73-83; ties at the cut: lower index first).
+ *  - apply: new cloud [kept | clones | split children] of n_new rows; noise
+ *    is the reference's rng.standard_normal((2 * n_split, 3)) (optim.py:394),
+ *    row-major f64 on the device; cbrt2 = numpy.cbrt(2.0).
+ * ------------------------------------------------------------------------- */
+int splatct_densify_workspace_bytes(int64_t n, size_t* bytes);
+int splatct_densify_classify(const double* params, const double* accum, int64_t n, double iters,
+                             double tau, double theta, double sigma_prune, int grad_prune,
+                             uint8_t* cls, uint64_t* keys, uint64_t* counts, void* stream);
+int splatct_densify_select(uint8_t* cls, const uint64_t* keys, int64_t n, int which, int64_t k,
+                           int64_t count, void* ws, size_t ws_bytes, void* stream);
+int splatct_densify_apply(const double* params, const double* m1, const double* m2,
+                          const uint8_t* cls, const double* noise, int64_t n, int64_t n_new,
+                          double cbrt2, double* new_params, double* new_m1, double* new_m2,
+                          void* ws, size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -85,6 +85,12 @@ SIGNATURES: dict[str, list] = {
                              c_f64, c_vp, c_vp, c_vp, c_vp],
     "splatct_cone_adjoint": [c_vp, c_vp, c_vp, c_i32, c_i32, c_f64, c_f64, c_i32, c_i32, c_i32,
                              c_f64, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp],
+    "splatct_densify_workspace_bytes": [c_i64, c_szp],
+    "splatct_densify_classify": [c_vp, c_vp, c_i64, c_f64, c_f64, c_f64, c_f64, c_i32, c_vp, c_vp,
+                                 c_vp, c_vp],
+    "splatct_densify_select": [c_vp, c_vp, c_i64, c_i32, c_i64, c_i64, c_vp, c_sz, c_vp],
+    "splatct_densify_apply": [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_f64, c_vp, c_vp, c_vp,
+                              c_vp, c_sz, c_vp],
 }
 
 SQDIFF_BLOCKS = 592   # SPLATCT_SQDIFF_BLOCKS

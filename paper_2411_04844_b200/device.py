@@ -570,3 +570,47 @@ def adam(params, grads, m1, m2, scalars, sigma_floor, sigma_ceiling, halt=None):
 def grad_norm_accum(grads, accum, halt=None):
     call("splatct_grad_norm_accum", ptr(grads), int(grads.shape[1]), ptr(accum), ptr(halt),
          stream_handle())
+
+
+def densify(params: torch.Tensor, m1: torch.Tensor, m2: torch.Tensor, accum: torch.Tensor,
+            iters: int, dparams, rng: np.random.Generator):
+    """One clone / split / prune event on the device (csrc/densify.cu).
+
+    Same result as ``densify.densify_and_prune`` + ``OptimizerState.remap``
+    (reference densify.py:86-147, optim.py:92-106) without moving the cloud
+    through host memory: the host reads three counts, sizes the budgets
+    exactly as the reference does, and draws the split children's normals
+    from ``rng`` (the reference's ``default_rng([seed, it+1])``, optim.py:394).
+    Returns (params', m1', m2', DensifyReport) with ``report.kept`` None.
+    """
+    from .densify import CBRT2, DensifyReport
+
+    dev = params.device
+    n = int(params.shape[1])
+    if iters <= 0:
+        from .core import ValidationError
+        raise ValidationError("no backward passes accumulated since last event")
+    cls = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
+    keys = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    counts = torch.empty(3, dtype=torch.int64, device=dev)
+    ws_bytes = size_query("splatct_densify_workspace_bytes", n)
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+    s = stream_handle()
+    call("splatct_densify_classify", ptr(params), ptr(accum), n, float(iters), float(dparams.tau),
+         float(dparams.theta), 3.0 * float(dparams.box_size), int(dparams.grad_prune_enabled),
+         ptr(cls), ptr(keys), ptr(counts), s)
+    n_prune, c_clone, c_split = (int(v) for v in counts.cpu().tolist())
+    k_clone = min(dparams.n_max - n, c_clone)                      # densify.py:104-106
+    n_clone = max(k_clone, 0) if c_clone > 0 else 0
+    call("splatct_densify_select", ptr(cls), ptr(keys), n, 2, k_clone, c_clone, ptr(ws), ws_bytes, s)
+    k_split = min(dparams.n_max - n - n_clone, c_split)            # densify.py:107-110
+    n_split = max(k_split, 0) if c_split > 0 else 0
+    call("splatct_densify_select", ptr(cls), ptr(keys), n, 3, k_split, c_split, ptr(ws), ws_bytes, s)
+    n_new = n - n_prune - n_split + n_clone + 2 * n_split
+    noise = None
+    if n_split:
+        noise = torch.from_numpy(rng.standard_normal((2 * n_split, 3))).to(dev)
+    out = [torch.empty((5, n_new), dtype=torch.float64, device=dev) for _ in range(3)]
+    call("splatct_densify_apply", ptr(params), ptr(m1), ptr(m2), ptr(cls), ptr(noise), n, n_new,
+         float(CBRT2), ptr(out[0]), ptr(out[1]), ptr(out[2]), ptr(ws), ws_bytes, s)
+    return out[0], out[1], out[2], DensifyReport(n_clone, n_split, n_prune, n_new, None)

@@ -22,6 +22,8 @@ Reference call sites exercised (file:line in /root/reference/pkg/src/splatct):
   loss.l1_loss / ssim_loss / tv_loss / total_loss_detailed  loss.py:64-239
   optim.adam_step            optim.py:109
   optim.run_reconstruction   optim.py:286
+  densify.densify_and_prune  densify.py:86  + OptimizerState.remap optim.py:92
+                             (-> densify.npz; ``--only densify`` writes just that)
 """
 
 from __future__ import annotations
@@ -40,7 +42,7 @@ os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_ref")
 sys.path.insert(0, REF_SRC)
 
 import splatct  # noqa: E402  (the reference)
-from splatct import core, fvr, loss, optim, phantom, projector, metrics  # noqa: E402
+from splatct import core, densify, fvr, loss, optim, phantom, projector, metrics  # noqa: E402
 
 assert os.path.dirname(splatct.__file__).startswith(REF_SRC), splatct.__file__
 
@@ -189,6 +191,61 @@ def gen_adam(out):
         out[f"adam_out_{k}"] = v
 
 
+# (n, n_max offset or None, grad_prune, tau, theta, box) per case; budgets:
+# unlimited, clone-limited, split-limited, negative budget, sigma pruning
+DENSIFY_CASES = [
+    (400, None, True, 2e-4, 1.0, 17),
+    (400, 10, True, 2e-4, 1.0, 17),
+    (400, "split", True, 2e-4, 1.0, 17),
+    (300, -5, False, 2e-4, 1.2, 5),
+    (500, None, False, 1e-3, 0.8, 3),
+]
+
+
+def gen_densify(out):
+    for ci, (n, nmax, gp, tau, theta, box) in enumerate(DENSIFY_CASES):
+        rng = np.random.default_rng(100 + ci)
+        mu = rng.uniform(-5, 70, (n, 3))
+        sigma = rng.uniform(0.3, 4.0 * box if ci >= 3 else 3.0, n)
+        inten = rng.uniform(0.0, 1.0, n)
+        iters = int(rng.integers(1, 120))
+        # avg spans tau: about a third below, the rest above (distinct values)
+        accum = np.exp(rng.uniform(np.log(tau) - 2.0, np.log(tau) + 3.0, n)) * iters
+        cl = core.GaussianCloud(mu, sigma, inten)
+        g = core.ParamGradients(np.zeros((n, 3)), np.zeros(n), np.zeros(n), accum, iters)
+        hot = (accum / iters >= tau)
+        if nmax == "split":
+            n_clone = int((hot & (sigma <= theta)).sum())
+            n_max = n + n_clone + 7
+        elif nmax is None:
+            n_max = 10 * n
+        else:
+            n_max = n + nmax
+        prm = densify.DensifyParams(n_max=n_max, tau=tau, theta=theta, box_size=box,
+                                    grad_prune_enabled=gp)
+        seed, it = 7 + ci, 100 * (ci + 1)
+        new, rep = densify.densify_and_prune(cl, g, prm, np.random.default_rng([seed, it]))
+        st = optim.OptimizerState(rng.standard_normal((n, 3)), rng.uniform(0, 1, (n, 3)),
+                                  rng.standard_normal(n), rng.uniform(0, 1, n),
+                                  rng.standard_normal(n), rng.uniform(0, 1, n), 5, 3e-4, 3e-5, 100)
+        st2 = st.remap(rep)
+        pre = f"d{ci}_"
+        for k, v in dict(mu=mu, sigma=sigma, intensity=inten, accum=accum, iters=iters,
+                         n_max=n_max, grad_prune=int(gp), tau=tau, theta=theta, box=box,
+                         seed=seed, it=it).items():
+            out[pre + k] = np.asarray(v)
+        for k, v in cloud_arrays(new).items():
+            out[pre + "out_" + k] = v
+        out[pre + "report"] = np.array([rep.clones, rep.splits, rep.prunes, rep.n_after])
+        out[pre + "kept"] = np.asarray(rep.kept)
+        for k in ("m_mu", "v_mu", "m_sigma", "v_sigma", "m_intensity", "v_intensity"):
+            out[pre + "in_" + k] = np.array(getattr(st, k))
+            out[pre + "out_" + k] = np.array(getattr(st2, k))
+        print(f"densify case {ci}: n {n} -> {rep.n_after} (clones {rep.clones}, "
+              f"splits {rep.splits}, prunes {rep.prunes})")
+    out["d_ncases"] = np.array(len(DENSIFY_CASES))
+
+
 def c1_problem():
     dims = (64, 64, 64)
     truth = phantom.shepp_logan_3d(*dims)
@@ -233,7 +290,14 @@ def gen_traj(out, iters=500):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--traj", action="store_true")
+    ap.add_argument("--only", choices=["densify"], default=None)
     args = ap.parse_args()
+    d = {}
+    gen_densify(d)
+    np.savez_compressed(os.path.join(HERE, "densify.npz"), **d)
+    print("wrote densify.npz with", len(d), "arrays")
+    if args.only == "densify":
+        return
     out = {}
     gen_fvr(out)
     gen_proj(out)

@@ -122,3 +122,23 @@ def test_misc_helpers():
     s = core.Sinogram.from_views(np.zeros((20, 8, 1)))
     (gt, st), (gv, sv) = _holdout_split(g, s, 0.1)
     assert gt.n_views + gv.n_views == 20 and gv.n_views == 2
+
+
+def test_densify_matches_reference_golden():
+    """Host restatement == the reference's densify_and_prune + remap, bitwise."""
+    from densify_golden import cases
+    from paper_2411_04844_b200 import optim
+    for ci, cloud, grads, prm, (seed, it), g in cases():
+        new, rep = densify.densify_and_prune(cloud, grads, prm, np.random.default_rng([seed, it]))
+        assert [rep.clones, rep.splits, rep.prunes, rep.n_after] == g["report"].tolist(), ci
+        np.testing.assert_array_equal(rep.kept, g["kept"])
+        np.testing.assert_array_equal(new.mu, g["out_mu"])
+        np.testing.assert_array_equal(new.sigma, g["out_sigma"])
+        np.testing.assert_array_equal(new.intensity, g["out_intensity"])
+        n = cloud.n
+        st = optim.OptimizerState(g["in_m_mu"], g["in_v_mu"], g["in_m_sigma"], g["in_v_sigma"],
+                                  g["in_m_intensity"], g["in_v_intensity"], 5, 3e-4, 3e-5, 100)
+        assert st.n == n
+        st2 = st.remap(rep)
+        for k in ("m_mu", "v_mu", "m_sigma", "v_sigma", "m_intensity", "v_intensity"):
+            np.testing.assert_array_equal(getattr(st2, k), g["out_" + k])
