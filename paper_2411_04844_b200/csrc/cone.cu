@@ -206,22 +206,24 @@ __global__ void k_cone_gscale(const float* __restrict__ g, const float* __restri
 constexpr int CA_ZW = 256;
 constexpr int CA_PMAX = 3;   // residue classes held in shared memory (P tau sv > 1)
 constexpr int CA_WARPS = 4;
+constexpr int CA_LEN = CA_ZW + 4;   // slot 0 = slice zb - 1, slots zn + 1.. = spill-over
 
 __global__ void __launch_bounds__(32 * CA_WARPS) k_cone_adj(
     const ConeEntry* __restrict__ E, const int64_t* __restrict__ eptr, int64_t npix, int nv,
     float sv, int cl, float zc, const float* __restrict__ gs, float* __restrict__ out,
     int accumulate, const int* halt) {
     if (halted(halt)) return;
-    __shared__ float zacc[CA_WARPS][2 * CA_PMAX][CA_ZW];
+    __shared__ float zacc[CA_WARPS][2 * CA_PMAX][CA_LEN];
     __shared__ float4 eb[CA_WARPS][32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int lm2 = lane & 1, lm3 = lane % 3;
     const int nwin = (cl + CA_ZW - 1) / CA_ZW;
     const int64_t gw = blockIdx.x * (int64_t)CA_WARPS + wid;
     const int64_t p = gw / nwin;
     if (p >= npix) return;
     const int zb = (int)(gw % nwin) * CA_ZW, zn = min(CA_ZW, cl - zb);
     for (int k = 0; k < 2 * CA_PMAX; ++k)
-        for (int i = lane; i < zn; i += 32) zacc[wid][k][i] = 0.f;
+        for (int i = lane; i < zn + 3; i += 32) zacc[wid][k][i] = 0.f;
     const float vmid = 0.5f * (float)(nv - 1);
     const float inv_sv = 1.f / sv;
     const int64_t b = eptr[p], e = eptr[p + 1];
@@ -242,33 +244,53 @@ __global__ void __launch_bounds__(32 * CA_WARPS) k_cone_adj(
             // rows P apart are > 1 slice apart, so lanes of one residue class
             // mod P never share a voxel within an instruction
             const int P = (int)floorf(inv) + 1;
-            const int cls = lane % P;
-            for (int dd = d0; dd <= d1; dd += 32) {
-                const int d = dd + lane;
-                const bool valid = d <= d1;
-                const float v = ((float)d - vmid) * sv;
-                // floor cell: at exact integers this picks the forward's other
-                // (zero-weight) neighbour, so the taps -- and the transpose -- agree
-                const float z = __fmaf_rn(v, tau, zc);
-                const float zf = floorf(z);
-                const int z0 = (int)zf - zb;
-                const float fz = z - zf;
-                const float g = valid ? wxy * __ldg(grow + d) : 0.f;
-                const bool va = valid && z0 >= 0 && z0 < zn;
-                const bool vb = valid && z0 + 1 >= 0 && z0 + 1 < zn;
-                const float ta = g - g * fz, tb = g * fz;
-                if (P <= CA_PMAX) {   // one class per array pair: no barriers inside
-                    if (va) zacc[wid][2 * cls][z0] += ta;
-                    if (vb) zacc[wid][2 * cls + 1][z0 + 1] += tb;
-                } else {              // very dense rows: classes in sequence
+            if (P <= CA_PMAX) {   // one array pair per class: no barriers inside
+                const int cls = P == 1 ? 0 : (P == 2 ? lm2 : lm3);
+                float* ra = &zacc[wid][2 * cls][1];        // slot of slice z0 (local)
+                float* rb = &zacc[wid][2 * cls + 1][2];    // slot of slice z0 + 1
+                // the upstream rows come from L2: keep two chunks of loads in
+                // flight ahead of the shared-memory read-modify-writes
+                float g1 = d0 + lane <= d1 ? __ldg(grow + d0 + lane) : 0.f;
+                float g2 = d0 + 32 + lane <= d1 ? __ldg(grow + d0 + 32 + lane) : 0.f;
+                for (int dd = d0; dd <= d1; dd += 32) {
+                    const int d = dd + lane;
+                    const float gc = g1;
+                    g1 = g2;
+                    g2 = d + 64 <= d1 ? __ldg(grow + d + 64) : 0.f;
+                    const float v = ((float)d - vmid) * sv;
+                    // floor cell: at exact integers this picks the forward's other
+                    // (zero-weight) neighbour, so the taps -- and the transpose -- agree
+                    const float z = __fmaf_rn(v, tau, zc);
+                    const float zf = floorf(z);
+                    const int z0 = (int)zf - zb;
+                    // taps of slices -1 .. zn land in padded slots, dropped at the end
+                    const bool ok = d <= d1 && (unsigned)(z0 + 1) <= (unsigned)zn;
+                    const float g = ok ? wxy * gc : 0.f;
+                    const float tb = g * (z - zf);
+                    if (ok) {
+                        ra[z0] += g - tb;
+                        rb[z0] += tb;
+                    }
+                    __syncwarp();
+                }
+            } else {              // very dense rows: classes in sequence
+                const int cls = lane % P;
+                for (int dd = d0; dd <= d1; dd += 32) {
+                    const int d = dd + lane;
+                    const float v = ((float)d - vmid) * sv;
+                    const float z = __fmaf_rn(v, tau, zc);
+                    const float zf = floorf(z);
+                    const int z0 = (int)zf - zb;
+                    const bool ok = d <= d1 && (unsigned)(z0 + 1) <= (unsigned)zn;
+                    const float g = ok ? wxy * __ldg(grow + d) : 0.f;
+                    const float tb = g * (z - zf);
                     for (int ph = 0; ph < P; ++ph) {
-                        if (va && cls == ph) zacc[wid][0][z0] += ta;
+                        if (ok && cls == ph) zacc[wid][0][z0 + 1] += g - tb;
                         __syncwarp();
-                        if (vb && cls == ph) zacc[wid][1][z0 + 1] += tb;
+                        if (ok && cls == ph) zacc[wid][1][z0 + 2] += tb;
                         __syncwarp();
                     }
                 }
-                __syncwarp();
             }
         }
     }
@@ -277,7 +299,7 @@ __global__ void __launch_bounds__(32 * CA_WARPS) k_cone_adj(
     for (int i = lane; i < zn; i += 32) {
         float s = 0.f;
 #pragma unroll
-        for (int k = 0; k < 2 * CA_PMAX; ++k) s += zacc[wid][k][i];
+        for (int k = 0; k < 2 * CA_PMAX; ++k) s += zacc[wid][k][i + 1];
         o[i] = accumulate ? o[i] + s : s;
     }
 }
