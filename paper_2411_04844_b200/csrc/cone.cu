@@ -136,7 +136,7 @@ __device__ __forceinline__ int zcell(float z, float& fz) {
 // column reads the same entries) and each warp walks them for its 32 rows
 // --------------------------------------------------------------------------
 constexpr int CONE_WARPS = 16;
-constexpr int CONE_BATCH = 128;   // entries staged per round
+constexpr int CONE_BATCH = 512;   // entries staged per round
 
 __global__ void __launch_bounds__(32 * CONE_WARPS) k_cone_fwd(
     const ConeColEntry* __restrict__ CE, const int64_t* __restrict__ cptr,

@@ -4,11 +4,17 @@
 
 For each (grid, N): init_cloud_random (sigma 1.5, box 17^3, unclipped), then
 device times (CUDA events, median of 10 after 3 warm-ups) of
-  fwd = bins + tile splat     (fvr.reconstruct)
-  bwd = tile partial moments + combine (fvr.backward, standard-normal upstream)
-reported as voxel contributions/s, algorithmic HBM GB/s (fwd 40 N + 4 W H C,
-bwd 96 N + 4 W H C bytes) and their fractions of the measured HBM peak and of
-the FP32 FMA peak (148 SMs x 128 lanes x sm clock).  One JSON line per point.
+  bin   = footprints + radix sort + tile starts        (FvrPlan.bin)
+  splat = the tile splat alone, on the binned cloud    (FvrPlan.forward)
+  fwd   = bin + splat                                  (fvr.reconstruct)
+  bwd   = the backward (gradients + norm accumulation; FvrPlan.backward,
+          standard-normal upstream)
+reported as voxel contributions/s and algorithmic HBM GB/s with their
+fractions of the measured HBM peak and of the FP32 FMA peak (148 SMs x 128
+lanes x sm clock).  Algorithmic bytes: splat 40 N + 4 W H C (params read,
+volume written once); bwd 96 N + 4 min(C, W H C) -- the backward reads only
+the upstream voxels inside footprints, each at most once, so a sparse cloud
+in a large grid does not owe the whole upstream.  One JSON line per point.
 """
 import argparse
 import json
@@ -67,6 +73,7 @@ def main():
 
             fwd()
             t_bin = med_ms(lambda: plan.bin(params))
+            t_s = med_ms(lambda: plan.forward(params, vol))
             t_f = med_ms(fwd)
             t_b = med_ms(lambda: plan.backward(params, up, grads, accum))
             fl = np.floor(cl.mu)
@@ -75,11 +82,15 @@ def main():
             contrib = int(np.prod(np.clip(span, 0, None), axis=1).sum())
             vb = 4.0 * g ** 3
             row = {"grid": g, "n": n, "contributions": contrib,
-                   "bin_ms": round(t_bin, 4), "fwd_ms": round(t_f, 4), "bwd_ms": round(t_b, 4),
+                   "bin_ms": round(t_bin, 4), "splat_ms": round(t_s, 4), "fwd_ms": round(t_f, 4),
+                   "bwd_ms": round(t_b, 4),
                    "fwd_contrib_per_s": contrib / (t_f * 1e-3),
+                   "splat_contrib_per_s": contrib / (t_s * 1e-3),
                    "bwd_contrib_per_s": contrib / (t_b * 1e-3),
                    "fwd_gbs": (40 * n + vb) / (t_f * 1e-3) / 1e9,
-                   "bwd_gbs": (96 * n + vb) / (t_b * 1e-3) / 1e9}
+                   "splat_gbs": (40 * n + vb) / (t_s * 1e-3) / 1e9,
+                   "bwd_gbs": (96 * n + 4.0 * min(contrib, g ** 3)) / (t_b * 1e-3) / 1e9}
+            row["splat_hbm_frac"] = row["splat_gbs"] / hbm
             row["fwd_hbm_frac"] = row["fwd_gbs"] / hbm
             row["bwd_hbm_frac"] = row["bwd_gbs"] / hbm
             row["fwd_fma_frac"] = row["fwd_contrib_per_s"] / fma
