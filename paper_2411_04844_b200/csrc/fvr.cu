@@ -12,9 +12,10 @@
 // B200 design:
 //   * volume stored yxz (slice fastest) so a tile's (y,x) column is a
 //     contiguous 64 B segment;
-//   * (tile, Gaussian) pairs emitted per Gaussian in slot order and stably
-//     LSD-radix-sorted by tile id -> per-tile lists in ascending Gaussian id
-//     (bit-exact against the CPU restatement, deterministic sums);
+//   * per-Gaussian tile counts, an exclusive scan, then (tile, Gaussian) pairs
+//     emitted densely in Gaussian / slot order and stably LSD-radix-sorted by
+//     tile id (pair count read on the device) -> per-tile lists in ascending
+//     Gaussian id (bit-exact against the CPU restatement, deterministic sums);
 //   * forward: one CTA per 16^3 tile, each thread owns a (y,x) column of 16
 //     voxels in registers; per-Gaussian separable tables staged in shared
 //     memory; every voxel stored exactly once (no memset, no atomics);
@@ -31,9 +32,11 @@ namespace splatct {
 
 constexpr int TT = SPLATCT_TILE;   // tile edge (16)
 constexpr int SORT_NT = 256;
-constexpr int SORT_IPT = 8;
+constexpr int SORT_IPT = 16;
 constexpr int SORT_CHUNK = SORT_NT * SORT_IPT;
 constexpr int RADIX = 256;
+constexpr int MAX_PASSES = 4;     // 8-bit digits of a 32-bit tile id
+constexpr int BIN_NT = 1024;      // Gaussians per block in the emit pass
 
 // Per-Gaussian record written by the footprint pass: integer floor (global
 // voxel coordinates), fractional offsets, 0.5/sigma^2 and intensity in f32,
@@ -51,11 +54,12 @@ struct FvrLayout {
     int64_t nt;
     int S;            // slots per Gaussian (power of two >= max tiles per Gaussian)
     int Sl;           // log2(S)
-    int64_t np;       // n * S
+    int64_t np;       // worst-case number of (tile, Gaussian) pairs
     int passes;
     int64_t sort_blocks;
-    size_t o_fp, o_gcount, o_k0, o_v0, o_k1, o_v1, o_tcount, o_tstart, o_hist, o_scan, o_rec,
-        o_flag, o_pos, o_order, o_scan2, total;
+    int64_t emit_blocks;
+    size_t o_fp, o_k0, o_v0, o_k1, o_v1, o_tcount, o_tstart, o_ctl, o_tickets, o_ghist, o_stat_e,
+        o_stat_s, ctl_bytes, o_rec, o_flag, o_pos, o_order, o_scan2, total;
     int final_buf;    // which (k,v) buffer holds the sorted result
 };
 
@@ -73,32 +77,39 @@ static FvrLayout make_layout(int64_t n, int w, int h, int c, int hx, int hy, int
     L.nty = (h + TT - 1) / TT;
     L.ntz = (c + TT - 1) / TT;
     L.nt = (int64_t)L.ntx * L.nty * L.ntz;
-    {   // slots per Gaussian, rounded up to a power of two (slot -> Gaussian is a shift)
+    {   // slot field of a pair's value: a power of two >= the maximum tiles per
+        // Gaussian (value = Gaussian << Sl | slot); worst-case pair count
         const int s_raw = axis_span(hx, w) * axis_span(hy, h) * axis_span(hz, c);
         L.Sl = 0;
         while ((1 << L.Sl) < s_raw) ++L.Sl;
         L.S = 1 << L.Sl;
+        L.np = n * s_raw;
     }
-    L.np = n * L.S;
     int bits = 0;
-    while (((int64_t)1 << bits) <= L.nt) ++bits;   // keys in [0, nt] (nt = sentinel)
+    while (((int64_t)1 << bits) < L.nt) ++bits;   // keys in [0, nt)
     L.passes = (bits + 7) / 8;
     if (L.passes < 1) L.passes = 1;
     L.sort_blocks = (L.np + SORT_CHUNK - 1) / SORT_CHUNK;
+    L.emit_blocks = (n + BIN_NT - 1) / BIN_NT;
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off += align_up(bytes > 0 ? bytes : 1); return o; };
     L.o_fp = take(sizeof(int32_t) * 6 * (size_t)n);
-    L.o_gcount = take(sizeof(int32_t) * (size_t)n);
     L.o_k0 = take(sizeof(uint32_t) * (size_t)L.np);
     L.o_v0 = take(sizeof(uint32_t) * (size_t)L.np);
     L.o_k1 = take(sizeof(uint32_t) * (size_t)L.np);
     L.o_v1 = take(sizeof(uint32_t) * (size_t)L.np);
     L.o_tcount = take(sizeof(uint32_t) * 4);   // forward's dynamic tile counter
     L.o_tstart = take(sizeof(uint32_t) * (size_t)(L.nt + 1));
-    L.o_hist = take(sizeof(uint32_t) * RADIX * (size_t)(L.sort_blocks > 0 ? L.sort_blocks : 1));
-    size_t sc1 = scan_temp_bytes(RADIX * (L.sort_blocks > 0 ? L.sort_blocks : 1));
-    size_t sc2 = scan_temp_bytes(L.nt + 1);
-    L.o_scan = take(sc1 > sc2 ? sc1 : sc2);
+    // per-call control block, zeroed by one memset: block tickets, the pair
+    // count, per-pass global digit counts, the emit pass's look-back words,
+    // then every sort pass's per-(block, digit) look-back words
+    L.o_ctl = off;
+    L.o_tickets = take(sizeof(uint32_t) * 8);
+    L.o_ghist = take(sizeof(uint32_t) * RADIX * MAX_PASSES);
+    L.o_stat_e = take(sizeof(unsigned long long) * (size_t)(L.emit_blocks > 0 ? L.emit_blocks : 1));
+    L.o_stat_s = take(sizeof(unsigned long long) * RADIX * (size_t)L.passes *
+                      (size_t)(L.sort_blocks > 0 ? L.sort_blocks : 1));
+    L.ctl_bytes = off - L.o_ctl;
     L.o_rec = take(sizeof(GRec) * (size_t)n);
     // backward visiting order for volumes that exceed L2 (Gaussians sorted by
     // their first tile): first-slot flags, their exclusive scan, the list
@@ -123,131 +134,273 @@ static inline const T* at(const void* base, size_t off) {
 // --------------------------------------------------------------------------
 // footprints + pair emission
 // --------------------------------------------------------------------------
-__global__ void k_footprint(const double* __restrict__ P, int64_t n, int w, int h, int c, int zoff,
-                            int hx, int hy, int hz, int ntx, int nty, int S, uint32_t sentinel,
-                            int32_t* __restrict__ fp, int32_t* __restrict__ gcount,
-                            uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
-                            GRec* __restrict__ rec,
-                            const int* halt) {
-    if (halted(halt)) return;
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const int half[3] = {hx, hy, hz};
-    const int dim[3] = {w, h, c};
-    const int org[3] = {0, 0, zoff};
-    int lo[3], hi[3];
-    bool empty = false;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        // local coordinates: global footprint minus the slab origin
-        double f = floor(P[a * n + i]) - org[a];
-        double l = f - half[a], u = f + half[a];
-        if (l < 0.0) l = 0.0;
-        if (u > dim[a] - 1) u = dim[a] - 1;
-        if (!(l <= u)) {   // also catches NaN
-            empty = true;
-            lo[a] = 1; hi[a] = 0;
-        } else {
-            lo[a] = (int)l; hi[a] = (int)u;
+// Look-back status words: 2-bit flag (1 = aggregate, 2 = inclusive prefix) |
+// 62-bit value; the words are zeroed once per bin call.
+constexpr unsigned long long LB_A = 1ull << 62, LB_P = 2ull << 62, LB_V = LB_A - 1;
+
+// Walk back from block b over predecessors' status words (stride apart)
+// until an inclusive prefix is found; returns the exclusive prefix of b.
+__device__ __forceinline__ unsigned long long lookback(unsigned long long* st, int64_t b,
+                                                       int64_t stride) {
+    unsigned long long excl = 0;
+    for (int64_t pred = b - 1; pred >= 0; --pred) {
+        unsigned long long w;
+        do {
+            w = *reinterpret_cast<volatile unsigned long long*>(&st[pred * stride]);
+        } while ((w >> 62) == 0);
+        excl += w & LB_V;
+        if ((w >> 62) == 2) break;
+    }
+    return excl;
+}
+
+// The same walk for a whole warp, 32 predecessors per step (blocks that start
+// together all publish aggregates first, so a serial walk would be long):
+// the nearest inclusive word ends the sum.  Returns the exclusive prefix.
+__device__ __forceinline__ unsigned long long lookback_warp(unsigned long long* st, int64_t b) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long excl = 0;
+    for (int64_t top = b - 1; top >= 0; top -= 32) {
+        const int64_t pred = top - lane;
+        unsigned long long w = 0;
+        if (pred >= 0) {
+            do {
+                w = *reinterpret_cast<volatile unsigned long long*>(&st[pred]);
+            } while ((w >> 62) == 0);
         }
-        fp[6 * i + 2 * a] = lo[a];
-        fp[6 * i + 2 * a + 1] = hi[a];
+        const unsigned incl = __ballot_sync(0xffffffffu, pred >= 0 && (w >> 62) == 2);
+        // lanes up to (and including) the nearest inclusive word contribute
+        const int stop = incl ? __ffs(incl) - 1 : 31;
+        unsigned long long v = (pred >= 0 && lane <= stop) ? (w & LB_V) : 0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        excl += v;
+        if (incl) break;
     }
-    int cnt = 0;
-    const uint32_t base = (uint32_t)(i * S);
-    if (!empty) {   // binned Gaussians have |floor(mu)| <= dim + half: int32 is exact
-        GRec r;
-        const double mx = P[i], my = P[n + i], mz = P[2 * n + i], sg = P[3 * n + i];
-        const double fx = floor(mx), fy = floor(my), fz = floor(mz);
-        r.fx = (int)fx; r.fy = (int)fy; r.fz = (int)fz;
-        r.dx = (float)(mx - fx); r.dy = (float)(my - fy); r.dz = (float)(mz - fz);
-        r.inv2 = (float)(0.5 / (sg * sg) * 1.4426950408889634);   // exp(-a) = exp2(-a log2 e)
-        r.I = (float)P[4 * n + i];
-        rec[i] = r;
-        for (int tz = lo[2] / TT; tz <= hi[2] / TT; ++tz)
-            for (int ty = lo[1] / TT; ty <= hi[1] / TT; ++ty)
-                for (int tx = lo[0] / TT; tx <= hi[0] / TT; ++tx) {
-                    uint32_t tid = (uint32_t)((tz * nty + ty) * ntx + tx);
-                    keys[base + cnt] = tid;
-                    vals[base + cnt] = base + cnt;
-                    ++cnt;
-                }
+    return excl;
+}
+
+// Footprints + dense (tile, Gaussian) pairs in one pass.  Each block takes
+// BIN_NT Gaussians in index order (block ids from a ticket, so look-back
+// predecessors are always resident): footprint, GRec and tile count per
+// Gaussian, a block scan of the counts, a decoupled look-back for the block's
+// offset, then the block's pairs are written cooperatively (coalesced) in
+// Gaussian order and (tz, ty, tx) slot order -- the value encodes
+// Gaussian << Sl | slot.  The kernel also counts every sort pass's digits
+// (global histograms), so each sort pass is a single kernel.
+__global__ void __launch_bounds__(BIN_NT) k_bin_emit(
+    const double* __restrict__ P, int64_t n, int w, int h, int c, int zoff, int hx, int hy,
+    int hz, int ntx, int nty, int Sl, int passes, int32_t* __restrict__ fp,
+    GRec* __restrict__ rec, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
+    uint32_t* __restrict__ ghist, unsigned long long* __restrict__ status,
+    uint32_t* __restrict__ tickets, const int* halt) {
+    if (halted(halt)) return;
+    __shared__ unsigned s_blk;
+    __shared__ uint32_t s_off[BIN_NT + 1];
+    __shared__ int4 s_tile[BIN_NT];        // tx0, ty0, tz0, nx | ny << 16
+    __shared__ uint32_t s_warp[BIN_NT / 32];
+    __shared__ uint32_t s_hist[MAX_PASSES][RADIX];
+    __shared__ unsigned long long s_base;
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    if (t == 0) s_blk = atomicAdd(&tickets[0], 1u);
+    if (t < RADIX)
+        for (int p = 0; p < MAX_PASSES; ++p) s_hist[p][t] = 0u;
+    __syncthreads();
+    const int64_t blk = s_blk;
+    const int64_t i = blk * BIN_NT + t;
+    uint32_t cnt = 0;
+    int4 ti = make_int4(0, 0, 0, 1 | (1 << 16));
+    if (i < n) {
+        const int half[3] = {hx, hy, hz};
+        const int dim[3] = {w, h, c};
+        const int org[3] = {0, 0, zoff};
+        int lo[3], hi[3];
+        bool empty = false;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            // local coordinates: global footprint minus the slab origin
+            double f = floor(P[a * n + i]) - org[a];
+            double l = f - half[a], u = f + half[a];
+            if (l < 0.0) l = 0.0;
+            if (u > dim[a] - 1) u = dim[a] - 1;
+            if (!(l <= u)) {   // also catches NaN
+                empty = true;
+                lo[a] = 1; hi[a] = 0;
+            } else {
+                lo[a] = (int)l; hi[a] = (int)u;
+            }
+            fp[6 * i + 2 * a] = lo[a];
+            fp[6 * i + 2 * a + 1] = hi[a];
+        }
+        if (!empty) {   // binned Gaussians have |floor(mu)| <= dim + half: int32 is exact
+            GRec r;
+            const double mx = P[i], my = P[n + i], mz = P[2 * n + i], sg = P[3 * n + i];
+            const double fx = floor(mx), fy = floor(my), fz = floor(mz);
+            r.fx = (int)fx; r.fy = (int)fy; r.fz = (int)fz;
+            r.dx = (float)(mx - fx); r.dy = (float)(my - fy); r.dz = (float)(mz - fz);
+            r.inv2 = (float)(0.5 / (sg * sg) * 1.4426950408889634);   // exp(-a) = exp2(-a log2 e)
+            r.I = (float)P[4 * n + i];
+            rec[i] = r;
+            const int nx = hi[0] / TT - lo[0] / TT + 1, ny = hi[1] / TT - lo[1] / TT + 1;
+            const int nz = hi[2] / TT - lo[2] / TT + 1;
+            cnt = (uint32_t)(nx * ny * nz);
+            ti = make_int4(lo[0] / TT, lo[1] / TT, lo[2] / TT, nx | (ny << 16));
+        }
     }
-    for (int s = cnt; s < S; ++s) {
-        keys[base + s] = sentinel;
-        vals[base + s] = base + s;
+    s_tile[t] = ti;
+    // block exclusive scan of the counts
+    uint32_t inc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += u;
     }
-    gcount[i] = cnt;
+    if (lane == 31) s_warp[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        uint32_t v = lane < BIN_NT / 32 ? s_warp[lane] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += u;
+        }
+        if (lane < BIN_NT / 32) s_warp[lane] = v;
+    }
+    __syncthreads();
+    const uint32_t excl = (wid > 0 ? s_warp[wid - 1] : 0u) + inc - cnt;
+    const uint32_t total = s_warp[BIN_NT / 32 - 1];
+    s_off[t] = excl;
+    if (t == BIN_NT - 1) s_off[BIN_NT] = excl + cnt;
+    if (wid == 0) {   // decoupled look-back over the preceding blocks' totals, 32 at a time
+        unsigned long long base = 0;
+        if (blk == 0) {
+            if (lane == 0) atomicExch(&status[0], LB_P | (unsigned long long)total);
+        } else {
+            if (lane == 0) atomicExch(&status[blk], LB_A | (unsigned long long)total);
+            base = lookback_warp(status, blk);
+            if (lane == 0) atomicExch(&status[blk], LB_P | (base + total));
+        }
+        if (lane == 0) {
+            s_base = base;
+            if (blk == (int64_t)gridDim.x - 1) tickets[1] = (uint32_t)(base + total);   // pairs
+        }
+    }
+    __syncthreads();
+    const uint64_t base = s_base;
+    for (uint32_t q = t; q < total; q += BIN_NT) {
+        // owner: the last Gaussian whose offset is <= q (empty Gaussians share offsets)
+        int lo = 0, hi = BIN_NT;
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (s_off[mid] <= q) lo = mid; else hi = mid;
+        }
+        const uint32_t slot = q - s_off[lo];
+        const int4 g = s_tile[lo];
+        const int nx = g.w & 0xffff, ny = g.w >> 16;
+        // small exact quotients through f32 (slot < S, a few thousand at most:
+        // the half-unit margin dwarfs the approximate division's error)
+        const int sy = (int)__fdividef((float)slot + 0.5f, (float)nx);
+        const int sz = (int)__fdividef((float)sy + 0.5f, (float)ny);
+        const int tx = g.x + (int)slot - sy * nx, ty = g.y + sy - sz * ny, tz = g.z + sz;
+        const uint32_t key = (uint32_t)((tz * nty + ty) * ntx + tx);
+        keys[base + q] = key;
+        vals[base + q] = ((uint32_t)(blk * BIN_NT + lo) << Sl) | slot;
+        for (int p = 0; p < passes; ++p) atomicAdd(&s_hist[p][(key >> (8 * p)) & 255u], 1u);
+    }
+    __syncthreads();
+    if (t < RADIX)
+        for (int p = 0; p < passes; ++p)
+            if (s_hist[p][t]) atomicAdd(&ghist[p * RADIX + t], s_hist[p][t]);
 }
 
 // --------------------------------------------------------------------------
 // stable LSD radix sort, 8-bit digits
 // --------------------------------------------------------------------------
-__global__ void __launch_bounds__(SORT_NT) k_radix_hist(const uint32_t* __restrict__ keys,
-                                                        int64_t np, int shift, int64_t nblk,
-                                                        uint32_t* __restrict__ hist,
-                                                        const int* halt) {
-    if (halted(halt)) return;
-    __shared__ uint32_t sh[RADIX];
-    sh[threadIdx.x] = 0;
-    __syncthreads();
-    const int64_t base = blockIdx.x * (int64_t)SORT_CHUNK;
-#pragma unroll
-    for (int r = 0; r < SORT_IPT; ++r) {
-        int64_t g = base + r * SORT_NT + threadIdx.x;
-        if (g < np) atomicAdd(&sh[(keys[g] >> shift) & 255u], 1u);
-    }
-    __syncthreads();
-    hist[(int64_t)threadIdx.x * nblk + blockIdx.x] = sh[threadIdx.x];   // digit-major
-}
-
-__global__ void __launch_bounds__(SORT_NT) k_radix_scatter(
+// One stable LSD pass ("onesweep"): a block takes SORT_CHUNK keys, each warp
+// a contiguous run of 32 * SORT_IPT kept in registers.  Warps rank their own
+// keys (match_any per 32-key round, per-warp digit counters in shared
+// memory, warp-synchronous); the block's per-digit totals are published and
+// each digit's offset among preceding blocks comes from a decoupled
+// look-back (one thread per digit); the global digit offsets come from the
+// histograms counted by k_bin_emit.  Three block barriers per pass, one
+// kernel per pass, no separate histogram or scan.
+__global__ void __launch_bounds__(SORT_NT) k_onesweep(
     const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
-    uint32_t* __restrict__ kout, uint32_t* __restrict__ vout, int64_t np, int shift,
-    int64_t nblk, const uint32_t* __restrict__ hist_scanned, const int* halt) {
+    uint32_t* __restrict__ kout, uint32_t* __restrict__ vout, const uint32_t* __restrict__ npairs,
+    int shift, const uint32_t* __restrict__ ghist, unsigned long long* __restrict__ status,
+    uint32_t* __restrict__ ticket, const int* halt) {
     if (halted(halt)) return;
     constexpr int NW = SORT_NT / 32;
-    __shared__ uint32_t run[RADIX];
-    __shared__ uint32_t wcnt[NW][RADIX];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    run[threadIdx.x] = hist_scanned[(int64_t)threadIdx.x * nblk + blockIdx.x];
-    const int64_t base = blockIdx.x * (int64_t)SORT_CHUNK;
+    __shared__ unsigned s_blk;
+    __shared__ uint32_t wh[NW][RADIX];    // per-warp digit counts, then warp offsets
+    __shared__ uint32_t s_warp[NW];
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    if (t == 0) s_blk = atomicAdd(ticket, 1u);
+#pragma unroll
+    for (int q = 0; q < NW; ++q) wh[q][t] = 0u;
+    __syncthreads();
+    const int64_t b = s_blk;
+    const int64_t np = *npairs;
+    const int64_t base = b * (int64_t)SORT_CHUNK;
+    if (base >= np) return;   // block-uniform: later tickets are past the end too
+    const int64_t wbase = base + (int64_t)wid * 32 * SORT_IPT + lane;
     const uint32_t lt_mask = (1u << lane) - 1u;
+    uint32_t k[SORT_IPT], v[SORT_IPT], rk[SORT_IPT];
+#pragma unroll
     for (int r = 0; r < SORT_IPT; ++r) {
-#pragma unroll
-        for (int q = 0; q < NW; ++q) wcnt[q][threadIdx.x] = 0;
-        __syncthreads();
-        const int64_t g = base + r * SORT_NT + threadIdx.x;
+        const int64_t g = wbase + r * 32;
         const bool valid = g < np;
-        uint32_t k = 0, v = 0;
-        uint32_t d = RADIX;   // invalid lanes form their own group
-        if (valid) {
-            k = kin[g];
-            v = vin[g];
-            d = (k >> shift) & 255u;
-        }
+        k[r] = valid ? kin[g] : 0u;
+        v[r] = valid ? vin[g] : 0u;
+        const uint32_t d = valid ? (k[r] >> shift) & 255u : (uint32_t)RADIX;   // invalid: own group
         const uint32_t peers = __match_any_sync(0xffffffffu, d);
-        const uint32_t rank = __popc(peers & lt_mask);
-        const int leader = __ffs(peers) - 1;
-        if (valid && lane == leader) wcnt[wid][d] = __popc(peers);
-        __syncthreads();
-        {   // per-digit exclusive prefix over warps, in warp order
-            uint32_t acc = run[threadIdx.x];
+        const uint32_t before = valid ? wh[wid][d] : 0u;
+        rk[r] = before + __popc(peers & lt_mask);
+        __syncwarp();
+        if (valid && lane == __ffs(peers) - 1) wh[wid][d] = before + __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    {   // digit t: block total, offset among preceding blocks, global digit offset
+        uint32_t mine = 0;
 #pragma unroll
-            for (int q = 0; q < NW; ++q) {
-                uint32_t t = wcnt[q][threadIdx.x];
-                wcnt[q][threadIdx.x] = acc;
-                acc += t;
-            }
-            run[threadIdx.x] = acc;
+        for (int q = 0; q < NW; ++q) mine += wh[q][t];
+        unsigned long long* st = status + t;   // word (block, digit) at block * RADIX + digit
+        unsigned long long prev = 0;
+        if (b == 0) {
+            atomicExch(&st[0], LB_P | (unsigned long long)mine);
+        } else {
+            atomicExch(&st[b * RADIX], LB_A | (unsigned long long)mine);
+            prev = lookback(st, b, RADIX);
+            atomicExch(&st[b * RADIX], LB_P | (prev + mine));
         }
-        __syncthreads();
-        if (valid) {
-            uint32_t pos = wcnt[wid][d] + rank;
-            kout[pos] = k;
-            vout[pos] = v;
+        const uint32_t gd = ghist[t];
+        uint32_t inc = gd;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += u;
         }
+        if (lane == 31) s_warp[wid] = inc;
         __syncthreads();
+        uint32_t acc = (uint32_t)prev + inc - gd;
+        for (int q = 0; q < wid; ++q) acc += s_warp[q];
+#pragma unroll
+        for (int q = 0; q < NW; ++q) {   // warp offsets for digit t, in warp order
+            const uint32_t c2 = wh[q][t];
+            wh[q][t] = acc;
+            acc += c2;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < SORT_IPT; ++r) {
+        const int64_t g = wbase + r * 32;
+        if (g < np) {
+            const uint32_t pos = wh[wid][(k[r] >> shift) & 255u] + rk[r];
+            kout[pos] = k[r];
+            vout[pos] = v[r];
+        }
     }
 }
 
@@ -464,16 +617,18 @@ __global__ void __launch_bounds__(256, 4) k_fvr_fwd(const GRec* __restrict__ rec
 }
 
 // tstart[t] = lower_bound(sorted keys, t) for t in [0, nt] from the key
-// boundaries: sorted position j starts every tile in (key[j-1], key[j]] (keys
-// >= nt are the empty-slot sentinels, so tstart[nt] = number of real pairs).
+// boundaries: sorted position j starts every tile in (key[j-1], key[j]], and
+// tstart[nt] = number of pairs (read on the device: the bins are dense).
 // One coalesced pass; each tile start is written exactly once.
-__global__ void k_tile_starts(const uint32_t* __restrict__ skeys, int64_t np, int64_t nt,
+__global__ void k_tile_starts(const uint32_t* __restrict__ skeys,
+                              const uint32_t* __restrict__ npairs, int64_t nt,
                               uint32_t* __restrict__ tstart, const int* halt) {
     if (halted(halt)) return;
+    const int64_t np = npairs ? (int64_t)*npairs : 0;
     const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (j > np) return;
-    const int64_t prev = j == 0 ? -1 : (int64_t)min(skeys[j - 1], (uint32_t)nt);
-    const int64_t cur = j == np ? nt : (int64_t)min(skeys[j], (uint32_t)nt);
+    const int64_t prev = j == 0 ? -1 : (int64_t)skeys[j - 1];
+    const int64_t cur = j == np ? nt : (int64_t)skeys[j];
     for (int64_t t = prev + 1; t <= cur; ++t) tstart[t] = (uint32_t)j;
 }
 
@@ -761,8 +916,8 @@ static int check_args(int64_t n, int w, int h, int c, int hx, int hy, int hz, si
     SPLATCT_REQUIRE(n >= 0 && w > 0 && h > 0 && c > 0, "invalid sizes n=%lld dims=(%d,%d,%d)",
                     (long long)n, w, h, c);
     SPLATCT_REQUIRE(hx >= 0 && hy >= 0 && hz >= 0, "negative box half");
-    SPLATCT_REQUIRE(L.np < ((int64_t)1 << 32) - 1, "too many (tile, Gaussian) slots: %lld",
-                    (long long)L.np);
+    SPLATCT_REQUIRE(L.np < ((int64_t)1 << 32) - 1 && (n << L.Sl) < ((int64_t)1 << 32),
+                    "too many (tile, Gaussian) pairs: %lld", (long long)L.np);
     SPLATCT_REQUIRE(L.nt < ((int64_t)1 << 31), "too many tiles");
     SPLATCT_REQUIRE(ws_bytes >= L.total, "workspace too small: %zu < %zu", ws_bytes, L.total);
     return SPLATCT_OK;
@@ -786,33 +941,32 @@ int splatct_fvr_bin(const double* params, int64_t n, int w, int h, int c, int z0
     FvrLayout L = make_layout(n, w, h, c, hx, hy, hz);
     if (int e = check_args(n, w, h, c, hx, hy, hz, ws_bytes, L)) return e;
     cudaStream_t s = as_stream(stream);
+    uint32_t* tickets = at<uint32_t>(ws, L.o_tickets);   // [0] emit, [1] pair count, [2..] passes
+    const uint32_t* npairs = tickets + 1;
     if (n > 0) {
-        k_footprint<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
-            params, n, w, h, c, z0, hx, hy, hz, L.ntx, L.nty, L.S, (uint32_t)L.nt,
-            at<int32_t>(ws, L.o_fp), at<int32_t>(ws, L.o_gcount), at<uint32_t>(ws, L.o_k0),
-            at<uint32_t>(ws, L.o_v0), at<GRec>(ws, L.o_rec), halt);
+        SPLATCT_CK(cudaMemsetAsync(at<char>(ws, L.o_ctl), 0, L.ctl_bytes, s));
+        k_bin_emit<<<(unsigned)L.emit_blocks, BIN_NT, 0, s>>>(
+            params, n, w, h, c, z0, hx, hy, hz, L.ntx, L.nty, L.Sl, L.passes,
+            at<int32_t>(ws, L.o_fp), at<GRec>(ws, L.o_rec), at<uint32_t>(ws, L.o_k0),
+            at<uint32_t>(ws, L.o_v0), at<uint32_t>(ws, L.o_ghist),
+            at<unsigned long long>(ws, L.o_stat_e), tickets, halt);
         SPLATCT_LAUNCH_CK();
-        uint32_t* hist = at<uint32_t>(ws, L.o_hist);
         for (int p = 0; p < L.passes; ++p) {
             const size_t ki = p % 2 ? L.o_k1 : L.o_k0, vi = p % 2 ? L.o_v1 : L.o_v0;
             const size_t ko = p % 2 ? L.o_k0 : L.o_k1, vo = p % 2 ? L.o_v0 : L.o_v1;
-            k_radix_hist<<<(unsigned)L.sort_blocks, SORT_NT, 0, s>>>(
-                at<uint32_t>(ws, ki), L.np, 8 * p, L.sort_blocks, hist, halt);
-            SPLATCT_LAUNCH_CK();
-            if (int e = exclusive_scan_u32(hist, hist, RADIX * L.sort_blocks,
-                                           at<void>(ws, L.o_scan), s))
-                return e;
-            k_radix_scatter<<<(unsigned)L.sort_blocks, SORT_NT, 0, s>>>(
+            k_onesweep<<<(unsigned)L.sort_blocks, SORT_NT, 0, s>>>(
                 at<uint32_t>(ws, ki), at<uint32_t>(ws, vi), at<uint32_t>(ws, ko),
-                at<uint32_t>(ws, vo), L.np, 8 * p, L.sort_blocks, hist, halt);
+                at<uint32_t>(ws, vo), npairs, 8 * p, at<uint32_t>(ws, L.o_ghist) + p * RADIX,
+                at<unsigned long long>(ws, L.o_stat_s) + (size_t)p * RADIX * L.sort_blocks,
+                tickets + 2 + p, halt);
             SPLATCT_LAUNCH_CK();
         }
     }
-    {   // tile offsets from the sorted keys (sentinels sort last): no atomics
+    {   // tile offsets from the sorted keys: no atomics
         const size_t ko = L.final_buf ? L.o_k1 : L.o_k0;
         const int64_t npk = n > 0 ? L.np : 0;
         k_tile_starts<<<(unsigned)((npk + 1 + 255) / 256), 256, 0, s>>>(
-            n > 0 ? at<uint32_t>(ws, ko) : nullptr, n > 0 ? L.np : 0, L.nt,
+            n > 0 ? at<uint32_t>(ws, ko) : nullptr, n > 0 ? npairs : nullptr, L.nt,
             at<uint32_t>(ws, L.o_tstart), halt);
         SPLATCT_LAUNCH_CK();
     }
