@@ -17,6 +17,7 @@ STAGES = {
     "loss_fused": ["k_ssim_stats11<1>", "k_loss_grad11"],
     "fvr_forward": ["k_fvr_fwd"],
     "fvr_backward": ["k_fvr_bwd"],
+    "fvr_bin": ["k_bin_emit", "k_onesweep", "k_tile_starts"],
 }
 
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
