@@ -364,6 +364,10 @@ __global__ void __launch_bounds__(R_NT, MODE == 1 ? 2 : 1) k_ssim_stats11(const 
     constexpr int NF = MODE == 0 ? 5 : (MODE == 1 ? 3 : 2);   // ring fields
     __shared__ __align__(16) float sf[R_BUF][2][R_SPAN][32];    // cp.async landing (f32)
     __shared__ __align__(16) double sd[2][2][R_SPAN][32];       // converted rows (f64)
+    // MODE 1: the reference window moments of an output row, staged by cp.async
+    // with the input rows (4 slots: a slot is rewritten two barriers after its read)
+    constexpr int RS_BUF = R_AHEAD + 2;
+    __shared__ __align__(16) double srs[MODE == 1 ? RS_BUF : 1][2][MODE == 1 ? R_COLS : 1][32];
     __shared__ double red[R_NT / 32];
     const int lane = threadIdx.x & 31, cl = threadIdx.x >> 5;
     const int zb = blockIdx.x * 32, j0 = blockIdx.y * R_COLS;
@@ -387,7 +391,21 @@ __global__ void __launch_bounds__(R_NT, MODE == 1 ? 2 : 1) k_ssim_stats11(const 
         if (arr) goff[k] = -goff[k] - 1;                  // sign selects Y
         if (MODE == 2 && !arr) mine[k] = false;           // ref-only: no X rows
     }
+    // MODE 1 staging of RS: thread t copies 16 bytes (two slices) of one
+    // (field, column) row segment: 2 fields x R_COLS columns x 16 chunks
+    const int rs_f = threadIdx.x / (R_COLS * 16), rs_c = (threadIdx.x / 16) % R_COLS,
+              rs_q = threadIdx.x % 16;
+    const bool rs_ok = MODE == 1 && rs_f < 2 && j0 + rs_c < vc && zb + 2 * rs_q < p;
     auto issue = [&](int v) {
+        if (MODE == 1) {   // reference moments of output row v - 10 (needed at iteration v)
+            const int u = v - 10;
+            if (u >= 0 && u < vr && rs_f < 2) {
+                const double* src =
+                    rs_ok ? RS + rs_f * plane + ((int64_t)u * vc + j0 + rs_c) * p + zb + 2 * rs_q
+                          : RS;
+                cp16_zfill(&srs[v % RS_BUF][rs_f][rs_c][2 * rs_q], src, rs_ok);
+            }
+        }
         if (v < m) {
             float* buf = &sf[v % R_BUF][0][0][0];
 #pragma unroll
@@ -429,10 +447,9 @@ __global__ void __launch_bounds__(R_NT, MODE == 1 ? 2 : 1) k_ssim_stats11(const 
             // MODE 1: the reference window moments of output row v-10, loaded
             // before the row's arithmetic so their latency overlaps it
             double rs_my = 0.0, rs_y2 = 0.0;
-            if (MODE == 1 && v >= 10 && act) {
-                const int64_t o = ((int64_t)(v - 10) * vc + j) * p + z;
-                rs_my = RS[o];
-                rs_y2 = RS[plane + o];
+            if (MODE == 1 && v >= 10 && act) {   // staged with row v (cp.async, barrier above)
+                rs_my = srs[v % RS_BUF][0][cl][lane];
+                rs_y2 = srs[v % RS_BUF][1][cl][lane];
             }
             const double* xr = &sd[v & 1][0][cl][lane];
             const double* yr = &sd[v & 1][1][cl][lane];
