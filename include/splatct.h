@@ -92,6 +92,12 @@ int splatct_fvr_backward(const double* params, int64_t n, int w, int h, int c, i
 /* accum[i] += |(grads[0][i], grads[1][i], grads[2][i])| -- the densification
  * statistic of fvr.py:266-273, applied after the cross-slab gradient
  * all-reduce when the volume is sharded. */
+/* Byte offset, inside the splatct_fvr_bin workspace, of the tile-column
+ * occupancy words (uint64 per (ty, tx) tile column, bit tz = the tile has
+ * Gaussians), written by splatct_fvr_forward; SIZE_MAX when the volume has
+ * more than 64 z tiles (no mask). */
+int splatct_fvr_occupancy_offset(int64_t n, int w, int h, int c, int hx, int hy, int hz,
+                                 size_t* offset);
 int splatct_grad_norm_accum(const double* grads, int64_t n, double* accum, const int* halt,
                             void* stream);
 
@@ -178,9 +184,14 @@ int splatct_proj_tv_partial_len(int w, int h, int c, int64_t* len);
 /* Blocked applications: same results as splatct_proj_forward /
  * splatct_proj_adjoint (up to f32 summation order), one z-column load per
  * group entry feeding the group's rows (forward: kind 0 or 2 groups). */
+/* col_occ (optional, NULL = off): the voxelizer's tile-column occupancy of
+ * vol_yxz (splatct_fvr_occupancy_offset into the bins workspace, valid after
+ * splatct_fvr_forward); entries whose pixel column has no occupied z tile in
+ * a warp's z range are skipped -- they would add exact zeros.  w: volume
+ * width (pixel = y * w + x). */
 int splatct_proj_forward_blocked(const int64_t* gptr, const int32_t* gidx, const float* gval,
                                  int n_rays, int kind, const float* vol_yxz, float* sino, int c,
-                                 const int* halt, void* stream);
+                                 const uint64_t* col_occ, int w, const int* halt, void* stream);
 int splatct_proj_adjoint_blocked(const int64_t* gptr, const int32_t* gidx, const float* gval,
                                  int w, int h, int c, const float* gsino, const float* vol_yxz,
                                  const float* halo_lo, const float* halo_hi, double lambda_tv,

@@ -59,7 +59,7 @@ struct FvrLayout {
     int64_t sort_blocks;
     int64_t emit_blocks;
     size_t o_fp, o_k0, o_v0, o_k1, o_v1, o_tcount, o_tstart, o_ctl, o_tickets, o_ghist, o_stat_e,
-        o_stat_s, ctl_bytes, o_rec, o_flag, o_pos, o_order, o_scan2, total;
+        o_stat_s, o_occ, ctl_bytes, o_rec, o_flag, o_pos, o_order, o_scan2, total;
     int final_buf;    // which (k,v) buffer holds the sorted result
 };
 
@@ -109,6 +109,9 @@ static FvrLayout make_layout(int64_t n, int w, int h, int c, int hx, int hy, int
     L.o_stat_e = take(sizeof(unsigned long long) * (size_t)(L.emit_blocks > 0 ? L.emit_blocks : 1));
     L.o_stat_s = take(sizeof(unsigned long long) * RADIX * (size_t)L.passes *
                       (size_t)(L.sort_blocks > 0 ? L.sort_blocks : 1));
+    // per (ty, tx) tile column: bit tz set when that tile has Gaussians
+    // (written by the forward; read by the projector to skip all-zero z-runs)
+    L.o_occ = take(sizeof(unsigned long long) * (size_t)L.ntx * L.nty);
     L.ctl_bytes = off - L.o_ctl;
     L.o_rec = take(sizeof(GRec) * (size_t)n);
     // backward visiting order for volumes that exceed L2 (Gaussians sorted by
@@ -457,6 +460,7 @@ __global__ void __launch_bounds__(256, 4) k_fvr_fwd(const GRec* __restrict__ rec
                                                  const uint32_t* __restrict__ svals,
                                                  float* __restrict__ vol,
                                                  unsigned int* __restrict__ counter, int fetch,
+                                                 unsigned long long* __restrict__ occ,
                                                  const int* halt) {
     if (halted(halt)) return;
     __shared__ __align__(16) float tab[FWD_BATCH * TAB_STRIDE];
@@ -486,6 +490,7 @@ __global__ void __launch_bounds__(256, 4) k_fvr_fwd(const GRec* __restrict__ rec
     const int x0 = txi * TT, y0 = tyi * TT, z0 = tzi * TT;
     const uint32_t beg = tstart[t], end = tstart[t + 1];
     const bool empty = beg == end;
+    if (!empty && threadIdx.x == 0 && ntz <= 64) atomicOr(&occ[rest], 1ull << tzi);
     float acc[4][4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
@@ -986,7 +991,8 @@ int splatct_fvr_forward(const double* params, int64_t n, int w, int h, int c, in
     SPLATCT_CK(cudaMemsetAsync(counter, 0, sizeof(unsigned int), as_stream(stream)));
     k_fvr_fwd<<<(unsigned)grid, 256, 0, as_stream(stream)>>>(
         at<GRec>(ws, L.o_rec), w, h, c, z0, hx, hy, hz, L.ntx, L.nty, L.nt, L.Sl,
-        at<uint32_t>(ws, L.o_tstart), at<uint32_t>(ws, vo), vol_yxz, counter, (int)fetch, halt);
+        at<uint32_t>(ws, L.o_tstart), at<uint32_t>(ws, vo), vol_yxz, counter, (int)fetch,
+        at<unsigned long long>(ws, L.o_occ), halt);
     SPLATCT_LAUNCH_CK();
     return SPLATCT_OK;
 }
@@ -1032,6 +1038,15 @@ int splatct_fvr_backward(const double* params, int64_t n, int w, int h, int c, i
     else if (ord) launch(F{}, T{});
     else launch(F{}, F{});
     SPLATCT_LAUNCH_CK();
+    return SPLATCT_OK;
+}
+
+int splatct_fvr_occupancy_offset(int64_t n, int w, int h, int c, int hx, int hy, int hz,
+                                 size_t* offset) {
+    FvrLayout L = make_layout(n, w, h, c, hx, hy, hz);
+    SPLATCT_REQUIRE(offset != nullptr, "null offset");
+    // the mask needs one bit per z tile
+    *offset = L.ntz <= 64 ? L.o_occ : (size_t)-1;
     return SPLATCT_OK;
 }
 

@@ -197,6 +197,14 @@ struct TvB {
 
 __device__ __forceinline__ int sgnf(float d) { return (d > 0.f) - (d < 0.f); }
 
+// Empty-space skipping for the forward (null occ: off): bit tz of
+// occ[(y / 16) * ntx + x / 16] says tile (x/16, y/16, tz) of the volume holds
+// Gaussians; other tiles are exactly zero (the voxelizer stores them as zeros)
+struct Occ {
+    const unsigned long long* occ;
+    int w, ntx;
+};
+
 constexpr int BS_WARPS = 4;
 constexpr int UNR = 8;    // z-vector gathers in flight per warp (16 measured no faster)
 
@@ -371,7 +379,7 @@ __global__ void __launch_bounds__(32 * BS_WARPS, R == 8 ? 4 : 6) k_bspmm(GroupMa
                                                         const float4* __restrict__ gval,
                                                         const float* __restrict__ X,
                                                         float* __restrict__ Y, int c, int zsplit,
-                                                        TvB tv, const int* halt) {
+                                                        TvB tv, Occ oc, const int* halt) {
     if (halted(halt)) return;
     constexpr int RW = R / 4;   // float4 weight words per entry
     __shared__ int s_col[BS_WARPS][32];
@@ -382,6 +390,14 @@ __global__ void __launch_bounds__(32 * BS_WARPS, R == 8 ? 4 : 6) k_bspmm(GroupMa
     if (g >= gm.ngroups()) return;
     const int zb = (int)(gw % zsplit) * 32 * V + lane * V;
     const bool zok = zb < c;
+    // empty-space skipping (forward only): the z tiles this warp's chunk covers;
+    // an entry whose pixel column has no Gaussian in them reads only zeros
+    unsigned long long zmask = ~0ull;
+    if (!TV && oc.occ) {
+        const int zlo = (int)(gw % zsplit) * 32 * V, zhi = min(zlo + 32 * V, c) - 1;
+        const int tlo = zlo / 16, thi = zhi / 16;
+        zmask = (thi >= 63 ? ~0ull : ((1ull << (thi + 1)) - 1ull)) & ~((1ull << tlo) - 1ull);
+    }
     const int zl = zok ? zb : 0;   // keep loads in bounds for idle lanes
     AccR<R, V> acc;
     acc.zero();
@@ -399,16 +415,32 @@ __global__ void __launch_bounds__(32 * BS_WARPS, R == 8 ? 4 : 6) k_bspmm(GroupMa
     }
     for (int64_t j0 = b; j0 < e; j0 += 32) {
         __syncwarp();
-        s_col[wid][lane] = nc;
+        int cnt = (int)min((int64_t)32, e - j0);
+        if (!TV && oc.occ) {   // keep the entries whose column is occupied, in order
+            bool keep = lane < cnt;
+            if (keep) {
+                const int py = nc / oc.w, px = nc - py * oc.w;
+                keep = (oc.occ[(py >> 4) * oc.ntx + (px >> 4)] & zmask) != 0ull;
+            }
+            const unsigned km = __ballot_sync(0xffffffffu, keep);
+            if (keep) {
+                const int slot = __popc(km & ((1u << lane) - 1u));
+                s_col[wid][slot] = nc;
 #pragma unroll
-        for (int q = 0; q < RW; ++q) s_w[wid][lane * RW + q] = nw[q];
+                for (int q = 0; q < RW; ++q) s_w[wid][slot * RW + q] = nw[q];
+            }
+            cnt = __popc(km);
+        } else {
+            s_col[wid][lane] = nc;
+#pragma unroll
+            for (int q = 0; q < RW; ++q) s_w[wid][lane * RW + q] = nw[q];
+        }
         __syncwarp();
         if (j0 + 32 + lane < e) {
             nc = __ldcs(gidx + j0 + 32 + lane);
 #pragma unroll
             for (int q = 0; q < RW; ++q) nw[q] = __ldcs(gval + (j0 + 32 + lane) * RW + q);
         }
-        const int cnt = (int)min((int64_t)32, e - j0);
         int jj = 0;
         for (; jj + UNR <= cnt; jj += UNR) {   // UNR z-vector gathers in flight
             float xv[UNR][V];
@@ -452,18 +484,18 @@ __global__ void __launch_bounds__(32 * BS_WARPS, R == 8 ? 4 : 6) k_bspmm(GroupMa
 template <int V, bool TV>
 static int launch_bspmm_v(const GroupMap& gm, const int64_t* gptr, const int32_t* gidx,
                           const float* gval, const float* X, float* Y, int c, const TvB& tv,
-                          const int* halt, cudaStream_t s) {
+                          const Occ& oc, const int* halt, cudaStream_t s) {
     const int zsplit = (c + 32 * V - 1) / (32 * V);
     const int64_t warps = gm.ngroups() * zsplit;
     const unsigned grid = (unsigned)((warps + BS_WARPS - 1) / BS_WARPS);
     if (!TV && gm.rows() == 8)
         k_bspmm<V, false, 8><<<grid, 32 * BS_WARPS, 0, s>>>(gm, gptr, gidx,
                                                          reinterpret_cast<const float4*>(gval), X,
-                                                         Y, c, zsplit, tv, halt);
+                                                         Y, c, zsplit, tv, oc, halt);
     else
         k_bspmm<V, TV, 4><<<grid, 32 * BS_WARPS, 0, s>>>(gm, gptr, gidx,
                                                          reinterpret_cast<const float4*>(gval), X,
-                                                         Y, c, zsplit, tv, halt);
+                                                         Y, c, zsplit, tv, oc, halt);
     SPLATCT_LAUNCH_CK();
     return SPLATCT_OK;
 }
@@ -477,14 +509,14 @@ static int vec_width(int c) {
 template <bool TV>
 static int launch_bspmm(const GroupMap& gm, const int64_t* gptr, const int32_t* gidx,
                         const float* gval, const float* X, float* Y, int c, const TvB& tv,
-                        const int* halt, cudaStream_t s) {
+                        const int* halt, cudaStream_t s, const Occ& oc = Occ{nullptr, 0, 0}) {
     const int V = vec_width(c);
     SPLATCT_REQUIRE((uintptr_t)X % (4 * V) == 0 && (uintptr_t)Y % (4 * V) == 0 &&
                         (!TV || (uintptr_t)tv.vol % (4 * V) == 0),
                     "projector operands must be %d-byte aligned", 4 * V);
-    if (V == 4) return launch_bspmm_v<4, TV>(gm, gptr, gidx, gval, X, Y, c, tv, halt, s);
-    if (V == 2) return launch_bspmm_v<2, TV>(gm, gptr, gidx, gval, X, Y, c, tv, halt, s);
-    return launch_bspmm_v<1, TV>(gm, gptr, gidx, gval, X, Y, c, tv, halt, s);
+    if (V == 4) return launch_bspmm_v<4, TV>(gm, gptr, gidx, gval, X, Y, c, tv, oc, halt, s);
+    if (V == 2) return launch_bspmm_v<2, TV>(gm, gptr, gidx, gval, X, Y, c, tv, oc, halt, s);
+    return launch_bspmm_v<1, TV>(gm, gptr, gidx, gval, X, Y, c, tv, oc, halt, s);
 }
 
 static size_t block_smem() { return (size_t)BLK_CAP * 12; }
@@ -567,13 +599,16 @@ int splatct_proj_block_fill(const int64_t* ptr, const int32_t* idx, const float*
 
 int splatct_proj_forward_blocked(const int64_t* gptr, const int32_t* gidx, const float* gval,
                                  int n_rays, int kind, const float* vol_yxz, float* sino, int c,
-                                 const int* halt, void* stream) {
+                                 const uint64_t* col_occ, int w, const int* halt, void* stream) {
     SPLATCT_REQUIRE(n_rays >= 0 && c > 0, "invalid sizes");
     SPLATCT_REQUIRE(kind == 0 || kind == 2, "forward groups are kind 0 or 2");
+    SPLATCT_REQUIRE(col_occ == nullptr || (w > 0 && c <= 64 * 16),
+                    "occupancy skipping needs the volume width and <= 64 z tiles");
     GroupMap gm{kind, n_rays, 0, 0};
     TvB tv{};
+    const Occ oc{reinterpret_cast<const unsigned long long*>(col_occ), w, (w + 15) / 16};
     return launch_bspmm<false>(gm, gptr, gidx, gval, vol_yxz, sino, c, tv, halt,
-                               as_stream(stream));
+                               as_stream(stream), oc);
 }
 
 int splatct_proj_adjoint_blocked(const int64_t* gptr, const int32_t* gidx, const float* gval,

@@ -178,6 +178,19 @@ class FvrPlan:
         self.ws_bytes = size_query("splatct_fvr_workspace_bytes", self.n, self.w, self.h, self.c,
                                    self.hx, self.hy, self.hz)
         self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
+        off = size_query("splatct_fvr_occupancy_offset", self.n, self.w, self.h, self.c,
+                         self.hx, self.hy, self.hz)
+        # tile-column occupancy of the last forward (projector empty-space skipping)
+        self.occupancy = (None if off == ctypes.c_size_t(-1).value
+                          else VP(self.ws.data_ptr() + off))
+        self._occ_off = None if self.occupancy is None else off
+
+    def occupancy_words(self) -> torch.Tensor | None:
+        """The occupancy words as an int64 tensor [nty * ntx] (a view of the workspace)."""
+        if self._occ_off is None:
+            return None
+        nw = ((self.w + 15) // 16) * ((self.h + 15) // 16)
+        return self.ws[self._occ_off:self._occ_off + 8 * nw].view(torch.int64)
 
     def _geo(self):
         return (self.n, self.w, self.h, self.c, self.z0, self.hx, self.hy, self.hz)
@@ -330,15 +343,19 @@ class ProjectorOperator:
         return b
 
     def forward(self, vol: torch.Tensor, out: torch.Tensor | None = None, halt=None,
-                blocked: bool | None = None, z0: int = 0):
-        """vol (h, w, c) -> sinogram (m, n, c); per-slice, so a slab's z0 is irrelevant."""
+                blocked: bool | None = None, z0: int = 0, occ=None):
+        """vol (h, w, c) -> sinogram (m, n, c); per-slice, so a slab's z0 is irrelevant.
+
+        occ: the voxelizer's tile-column occupancy of `vol` (FvrPlan.occupancy
+        after its forward) -- entries in all-zero z runs are skipped."""
         c = int(vol.shape[2])
         if out is None:
             out = torch.empty((self.m, self.n_det, c), dtype=torch.float32, device=vol.device)
         if self.blocked if blocked is None else blocked:
             g = self.fb
             call("splatct_proj_forward_blocked", ptr(g[0]), ptr(g[1]), ptr(g[2]), self.n_rays,
-                 self.fkind, ptr(vol), ptr(out), c, ptr(halt), stream_handle())
+                 self.fkind, ptr(vol), ptr(out), c, occ if occ is not None else VP(0), self.w,
+                 ptr(halt), stream_handle())
         else:
             call("splatct_proj_forward", ptr(self.a_ptr), ptr(self.a_col), ptr(self.a_val),
                  self.n_rays, ptr(vol), ptr(out), c, ptr(halt), stream_handle())
@@ -453,7 +470,7 @@ class ConeOperator:
         return 0.5 * (self.c_global - 1) - float(z0)
 
     def forward(self, vol: torch.Tensor, out: torch.Tensor | None = None, halt=None, z0: int = 0,
-                blocked=None):
+                blocked=None, occ=None):
         """vol slab (h, w, c_local) -> partial cone projections (m, nu, nv)."""
         cl = int(vol.shape[2])
         if out is None:

@@ -185,8 +185,8 @@ class Trainer:
         replicated = not self.per_slice and sharded
         st = []
 
-        def project():
-            self.op.forward(self.vol, self.pred, halt, z0=z0)
+        def project():   # empty-space skipping from the voxelizer's tile occupancy
+            self.op.forward(self.vol, self.pred, halt, z0=z0, occ=self.fvr.occupancy)
         st.append(("gpu", project))
         if replicated:   # partial cone projections -> full
             st.append(("comm", lambda: self.comm.allreduce_sum_(self.pred)))

@@ -392,3 +392,29 @@ def test_blocked_operator_matches_csr(variant, dims, m, n):
     b = op.adjoint(y, vol=x, lambda_tv=0.3, tv_count=float(w * h * c), tv_partial=pb, blocked=False)
     assert rel_l2(a.cpu().numpy(), b.cpu().numpy()) < 1e-6
     assert abs(float(pa.sum()) - float(pb.sum())) <= 1e-8 * abs(float(pb.sum()))
+
+
+@pytest.mark.parametrize("dims,c_note", [((96, 80, 256), "c=256: two 128-z chunks"),
+                                         ((64, 48, 40), "c=40: 32-z chunks, partial tile")])
+def test_projector_occupancy_skip_is_exact(dims, c_note):
+    """Empty-space skipping (voxelizer tile occupancy) changes nothing: a cloud
+    confined to part of the volume, projected with and without the mask."""
+    dev = D.require_cuda()
+    w, h, c = dims
+    rng = np.random.default_rng(12)
+    n = 3000
+    mu = np.stack([rng.uniform(10, w * 0.45, n), rng.uniform(5, h - 5, n),
+                   rng.uniform(c * 0.2, c * 0.5, n)], 1)
+    cloud = core.GaussianCloud(mu, rng.uniform(0.6, 2.0, n), rng.uniform(0, 1, n))
+    box = core.BoxConfig.for_dims(17, dims)
+    plan = D.FvrPlan(n, dims, box.half, 0, dev)
+    params = D.cloud_to_params(cloud, dev)
+    plan.bin(params)
+    vol = plan.forward(params, plan.new_volume())
+    occ = plan.occupancy_words().cpu().numpy().view(np.uint64)
+    assert 0 < int(sum(bin(int(v)).count("1") for v in occ)) < occ.size * ((c + 15) // 16)
+    geom = core.ScanGeometry.fan(20, 90, 1.3, 120.0, 90.0)
+    op = D.ProjectorOperator(geom, w, h, 0.5, dev)
+    dense = op.forward(vol)
+    skip = op.forward(vol, occ=plan.occupancy)
+    np.testing.assert_array_equal(skip.cpu().numpy(), dense.cpu().numpy())
