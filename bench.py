@@ -219,7 +219,7 @@ def stage_profile(tr, iters):
         lo, hi = tr.comm.halo(tr.vol)
         tr.op.adjoint(tr.gpred, tr.dl, vol=tr.vol, halo_lo=lo, halo_hi=hi, z0=tr.slab.z0,
                       lambda_tv=lw.lambda3, tv_count=tr.tv_count, tv_partial=tr.tv_part,
-                      halt=tr.halt)
+                      halt=tr.halt, occ=tr.fvr.occupancy)
         D.reduce_sum(tr.tv_part, tr.sums[2:3])
         ev[3].record(s)
         tr.comm.allreduce_sum_(tr.sums)

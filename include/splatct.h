@@ -192,11 +192,17 @@ int splatct_proj_tv_partial_len(int w, int h, int c, int64_t* len);
 int splatct_proj_forward_blocked(const int64_t* gptr, const int32_t* gidx, const float* gval,
                                  int n_rays, int kind, const float* vol_yxz, float* sino, int c,
                                  const uint64_t* col_occ, int w, const int* halt, void* stream);
+/* col_occ (optional, NULL = dense): the voxelizer's tile-column occupancy of
+ * vol_yxz.  A 2x2-pixel quad x z-chunk whose one-voxel neighbourhood lies in
+ * empty tiles is skipped: its TV terms are zero and its out_yxz values are
+ * LEFT UNWRITTEN -- only for callers that read the result inside occupied
+ * tiles (the training step's voxelizer backward reads it inside Gaussian
+ * footprints).  Its tv_partial slots are written as 0. */
 int splatct_proj_adjoint_blocked(const int64_t* gptr, const int32_t* gidx, const float* gval,
                                  int w, int h, int c, const float* gsino, const float* vol_yxz,
                                  const float* halo_lo, const float* halo_hi, double lambda_tv,
                                  double tv_count, float* out_yxz, double* tv_partial,
-                                 const int* halt, void* stream);
+                                 const uint64_t* col_occ, const int* halt, void* stream);
 
 /* Direct ray-marching forward projection (no matrix), same f64 ray setup and
  * sample enumeration as _kernels.py:262-303; used as a cross-check and for

@@ -54,7 +54,7 @@ SIGNATURES: dict[str, list] = {
                                      c_i32, c_vp, c_vp],
     "splatct_fvr_occupancy_offset": [c_i64, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_szp],
     "splatct_proj_adjoint_blocked": [c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp,
-                                     c_f64, c_f64, c_vp, c_vp, c_vp, c_vp],
+                                     c_f64, c_f64, c_vp, c_vp, c_vp, c_vp, c_vp],
     "splatct_proj_march_forward": [c_vp, c_vp, c_i32, c_i32, c_f64, c_f64, c_i32, c_f64, c_f64,
                                    c_i32, c_i32, c_i32, c_vp, c_vp, c_vp],
     "splatct_loss_workspace_bytes": [c_i32, c_i32, c_i32, c_szp],

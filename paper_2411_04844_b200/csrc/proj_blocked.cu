@@ -200,9 +200,14 @@ __device__ __forceinline__ int sgnf(float d) { return (d > 0.f) - (d < 0.f); }
 // Empty-space skipping for the forward (null occ: off): bit tz of
 // occ[(y / 16) * ntx + x / 16] says tile (x/16, y/16, tz) of the volume holds
 // Gaussians; other tiles are exactly zero (the voxelizer stores them as zeros)
+// Adjoint (mode 2): a 2x2-pixel quad x z-chunk whose one-voxel neighbourhood
+// is all empty tiles is skipped entirely: its TV value and subgradient are
+// zero and its output is left unwritten -- the caller (the training step's
+// voxelizer backward) reads the adjoint only inside Gaussian footprints,
+// i.e. inside occupied tiles.
 struct Occ {
     const unsigned long long* occ;
-    int w, ntx;
+    int w, ntx, mode;   // mode 1: forward entry skipping, 2: adjoint quad skipping
 };
 
 constexpr int BS_WARPS = 4;
@@ -393,12 +398,30 @@ __global__ void __launch_bounds__(32 * BS_WARPS, R == 8 ? 4 : 6) k_bspmm(GroupMa
     // empty-space skipping (forward only): the z tiles this warp's chunk covers;
     // an entry whose pixel column has no Gaussian in them reads only zeros
     unsigned long long zmask = ~0ull;
-    if (!TV && oc.occ) {
+    if (oc.mode == 1) {
         const int zlo = (int)(gw % zsplit) * 32 * V, zhi = min(zlo + 32 * V, c) - 1;
         const int tlo = zlo / 16, thi = zhi / 16;
         zmask = (thi >= 63 ? ~0ull : ((1ull << (thi + 1)) - 1ull)) & ~((1ull << tlo) - 1ull);
     }
     const int zl = zok ? zb : 0;   // keep loads in bounds for idle lanes
+    if (oc.mode == 2) {   // adjoint quads (kind 1): skip all-empty neighbourhoods
+        const int qw = (gm.w + 1) / 2;
+        const int x0 = 2 * (int)(g % qw), y0 = 2 * (int)(g / qw);
+        const int zlo = (int)(gw % zsplit) * 32 * V, zhi = min(zlo + 32 * V, c) - 1;
+        const bool halo = (zlo == 0 && tv.halo_lo) || (zhi == c - 1 && tv.halo_hi);
+        const int tlo = max(zlo - 1, 0) / 16, thi = min(zhi + 1, c - 1) / 16;
+        const unsigned long long zm =
+            (thi >= 63 ? ~0ull : ((1ull << (thi + 1)) - 1ull)) & ~((1ull << tlo) - 1ull);
+        const int txa = max(x0 - 1, 0) >> 4, txb = min(x0 + 2, gm.w - 1) >> 4;
+        const int tya = max(y0 - 1, 0) >> 4, tyb = min(y0 + 2, gm.h - 1) >> 4;
+        unsigned long long any = 0ull;
+        for (int ty = tya; ty <= tyb; ++ty)
+            for (int tx = txa; tx <= txb; ++tx) any |= oc.occ[ty * oc.ntx + tx];
+        if (!halo && (any & zm) == 0ull) {   // warp-uniform
+            if (TV && tv.partial && lane == 0) tv.partial[(gw % zsplit) * (int64_t)gm.nrows + g] = 0.0;
+            return;
+        }
+    }
     AccR<R, V> acc;
     acc.zero();
     const int64_t b = gptr[g], e = gptr[g + 1];
@@ -416,7 +439,7 @@ __global__ void __launch_bounds__(32 * BS_WARPS, R == 8 ? 4 : 6) k_bspmm(GroupMa
     for (int64_t j0 = b; j0 < e; j0 += 32) {
         __syncwarp();
         int cnt = (int)min((int64_t)32, e - j0);
-        if (!TV && oc.occ) {   // keep the entries whose column is occupied, in order
+        if (oc.mode == 1) {   // keep the entries whose column is occupied, in order
             bool keep = lane < cnt;
             if (keep) {
                 const int py = nc / oc.w, px = nc - py * oc.w;
@@ -509,7 +532,7 @@ static int vec_width(int c) {
 template <bool TV>
 static int launch_bspmm(const GroupMap& gm, const int64_t* gptr, const int32_t* gidx,
                         const float* gval, const float* X, float* Y, int c, const TvB& tv,
-                        const int* halt, cudaStream_t s, const Occ& oc = Occ{nullptr, 0, 0}) {
+                        const int* halt, cudaStream_t s, const Occ& oc = Occ{nullptr, 0, 0, 0}) {
     const int V = vec_width(c);
     SPLATCT_REQUIRE((uintptr_t)X % (4 * V) == 0 && (uintptr_t)Y % (4 * V) == 0 &&
                         (!TV || (uintptr_t)tv.vol % (4 * V) == 0),
@@ -606,7 +629,8 @@ int splatct_proj_forward_blocked(const int64_t* gptr, const int32_t* gidx, const
                     "occupancy skipping needs the volume width and <= 64 z tiles");
     GroupMap gm{kind, n_rays, 0, 0};
     TvB tv{};
-    const Occ oc{reinterpret_cast<const unsigned long long*>(col_occ), w, (w + 15) / 16};
+    const Occ oc{reinterpret_cast<const unsigned long long*>(col_occ), w, (w + 15) / 16,
+                 col_occ ? 1 : 0};
     return launch_bspmm<false>(gm, gptr, gidx, gval, vol_yxz, sino, c, tv, halt,
                                as_stream(stream), oc);
 }
@@ -615,17 +639,20 @@ int splatct_proj_adjoint_blocked(const int64_t* gptr, const int32_t* gidx, const
                                  int w, int h, int c, const float* gsino, const float* vol_yxz,
                                  const float* halo_lo, const float* halo_hi, double lambda_tv,
                                  double tv_count, float* out_yxz, double* tv_partial,
-                                 const int* halt, void* stream) {
+                                 const uint64_t* col_occ, const int* halt, void* stream) {
     SPLATCT_REQUIRE(w > 0 && h > 0 && c > 0, "invalid sizes");
+    SPLATCT_REQUIRE(col_occ == nullptr || c <= 64 * 16, "occupancy needs <= 64 z tiles");
     GroupMap gm{1, w * h, w, h};
     TvB tv{vol_yxz, halo_lo, halo_hi, tv_count > 0.0 ? lambda_tv / tv_count : 0.0, tv_partial,
            w, h};
+    const Occ oc{reinterpret_cast<const unsigned long long*>(col_occ), w, (w + 15) / 16,
+                 col_occ ? 2 : 0};
     cudaStream_t s = as_stream(stream);
     if (vol_yxz != nullptr && lambda_tv > 0.0) {
         SPLATCT_REQUIRE(tv_count > 0.0, "tv_count must be positive");
-        return launch_bspmm<true>(gm, gptr, gidx, gval, gsino, out_yxz, c, tv, halt, s);
+        return launch_bspmm<true>(gm, gptr, gidx, gval, gsino, out_yxz, c, tv, halt, s, oc);
     }
-    return launch_bspmm<false>(gm, gptr, gidx, gval, gsino, out_yxz, c, tv, halt, s);
+    return launch_bspmm<false>(gm, gptr, gidx, gval, gsino, out_yxz, c, tv, halt, s, oc);
 }
 
 }  // extern "C"

@@ -364,8 +364,12 @@ class ProjectorOperator:
     def adjoint(self, gsino: torch.Tensor, out: torch.Tensor | None = None, vol=None,
                 halo_lo=None, halo_hi=None, lambda_tv: float = 0.0, tv_count: float = 1.0,
                 tv_partial=None, halt=None, blocked: bool | None = None, z0: int = 0,
-                c_local: int | None = None):
-        """sinogram (m, n, c) -> volume (h, w, c) [+ lambda_tv * TV subgradient of vol]."""
+                c_local: int | None = None, occ=None):
+        """sinogram (m, n, c) -> volume (h, w, c) [+ lambda_tv * TV subgradient of vol].
+
+        occ (training step only): the voxelizer's tile-column occupancy of vol;
+        the result is then written only around occupied tiles (the voxelizer
+        backward reads it only inside Gaussian footprints)."""
         c = int(c_local if c_local is not None else gsino.shape[2])
         if out is None:
             out = torch.empty((self.h, self.w, c), dtype=torch.float32, device=gsino.device)
@@ -374,7 +378,7 @@ class ProjectorOperator:
         if getattr(self, "blocked", False) if blocked is None else blocked:
             g = self.ab
             call("splatct_proj_adjoint_blocked", ptr(g[0]), ptr(g[1]), ptr(g[2]), self.w, self.h,
-                 c, *args)
+                 c, *args[:8], occ if occ is not None else VP(0), *args[8:])
         else:
             call("splatct_proj_adjoint", ptr(self.at_ptr), ptr(self.at_ray), ptr(self.at_val),
                  self.w, self.h, c, *args)
@@ -484,7 +488,7 @@ class ConeOperator:
     def adjoint(self, gsino: torch.Tensor, out: torch.Tensor | None = None, vol=None,
                 halo_lo=None, halo_hi=None, lambda_tv: float = 0.0, tv_count: float = 1.0,
                 tv_partial=None, halt=None, z0: int = 0, c_local: int | None = None,
-                blocked=None):
+                blocked=None, occ=None):
         """(m, nu, nv) -> volume slab (h, w, c_local) [+ lambda_tv * TV subgradient of vol]."""
         cl = int(c_local if c_local is not None else
                  (out.shape[2] if out is not None else

@@ -208,14 +208,17 @@ class Trainer:
 
             def adjoint_tv():
                 lo, hi = self._halo
+                # dl is read only inside footprints: skip empty neighbourhoods
                 self.op.adjoint(self.gpred, self.dl, vol=self.vol, halo_lo=lo, halo_hi=hi,
                                 lambda_tv=lw.lambda3, tv_count=self.tv_count,
-                                tv_partial=self.tv_part, halt=halt, z0=z0)
+                                tv_partial=self.tv_part, halt=halt, z0=z0,
+                                occ=self.fvr.occupancy)
                 D.reduce_sum(self.tv_part, self.sums[2:3])
             st.append(("gpu", adjoint_tv))
         else:
             st.append(("gpu", lambda: self.op.adjoint(self.gpred, self.dl, halt=halt, z0=z0,
-                                                      c_local=self.slab.c_local)))
+                                                      c_local=self.slab.c_local,
+                                                      occ=self.fvr.occupancy)))
         if sharded:
             st.append(("comm", lambda: self.comm.allreduce_sum_(self.sums)))
 
