@@ -298,7 +298,11 @@ int splatct_fbp_backproject(const double* filtered, const double* cos_t, const d
  * (m*nu, nv); zc = (c_global-1)/2 - z0, so slab results are partial
  * projections that sum to the full one) and splatct_cone_adjoint (exact
  * transpose; gscaled is an (m*nu*nv) f32 scratch; accumulate != 0 adds into
- * out).
+ * out).  col_occ (optional, NULL = dense) is the voxelizer's tile-column
+ * occupancy of the slab (splatct_fvr_occupancy_offset): the forward skips
+ * entries whose pixel column has no occupied tile (exact zeros); the adjoint
+ * then leaves pixels x z-windows without occupied tiles UNWRITTEN (training
+ * step only: its consumer reads inside Gaussian footprints).
  * ------------------------------------------------------------------------- */
 int splatct_cone_setup_scratch_bytes(int m, int nu, int w, int h, size_t* bytes);
 int splatct_cone_count(const double* cos_t, const double* sin_t, int m, int nu, double su,
@@ -317,12 +321,12 @@ int splatct_cone_entry_fill(const void* samples, const int64_t* rptr, int nrays,
                             size_t scratch_bytes, void* stream);
 int splatct_cone_forward(const void* samples, const int64_t* rptr, const float* inv_len,
                          int nrays, int nv, double sv, double step, int w, int h, int c_local,
-                         double zc, const float* vol_yxz, float* sino, const int* halt,
-                         void* stream);
+                         double zc, const float* vol_yxz, const uint64_t* col_occ, float* sino,
+                         const int* halt, void* stream);
 int splatct_cone_adjoint(const void* entries, const int64_t* eptr, const float* inv_len,
                          int nrays, int nv, double sv, double step, int w, int h, int c_local,
                          double zc, const float* gsino, float* gscaled, float* out_yxz,
-                         int accumulate, const int* halt, void* stream);
+                         int accumulate, const uint64_t* col_occ, const int* halt, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Densification on the device: densify.densify_and_prune,

@@ -83,9 +83,9 @@ SIGNATURES: dict[str, list] = {
     "splatct_cone_entry_fill": [c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_i64, c_vp, c_vp, c_sz,
                                 c_vp],
     "splatct_cone_forward": [c_vp, c_vp, c_vp, c_i32, c_i32, c_f64, c_f64, c_i32, c_i32, c_i32,
-                             c_f64, c_vp, c_vp, c_vp, c_vp],
+                             c_f64, c_vp, c_vp, c_vp, c_vp, c_vp],
     "splatct_cone_adjoint": [c_vp, c_vp, c_vp, c_i32, c_i32, c_f64, c_f64, c_i32, c_i32, c_i32,
-                             c_f64, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp],
+                             c_f64, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp],
     "splatct_densify_workspace_bytes": [c_i64, c_szp],
     "splatct_densify_classify": [c_vp, c_vp, c_i64, c_f64, c_f64, c_f64, c_f64, c_i32, c_vp, c_vp,
                                  c_vp, c_vp],

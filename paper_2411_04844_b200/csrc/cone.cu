@@ -36,7 +36,7 @@ struct __align__(16) ConeColEntry {   // column-major (forward)
     int pix;
     float w;        // merged bilinear weight of the pixel's samples
     float tau;      // tbar / L
-    float pad;
+    int tcol;       // 16 x 16 tile column of the pixel (empty-space skipping)
 };
 
 struct __align__(16) ConeEntry {      // pixel-major (adjoint)
@@ -73,7 +73,7 @@ __global__ void k_cone_fill(Geom g, const int64_t* __restrict__ cptr,
         e.pix = pix;
         e.w = (float)w;
         e.tau = (float)(wt / w * inv_len);
-        e.pad = 0.f;
+        e.tcol = (pix / g.w >> 4) * ((g.w + 15) >> 4) + ((pix % g.w) >> 4);
         CE[j++] = e;
     });
 }
@@ -141,7 +141,8 @@ constexpr int CONE_BATCH = 512;   // entries staged per round
 __global__ void __launch_bounds__(32 * CONE_WARPS) k_cone_fwd(
     const ConeColEntry* __restrict__ CE, const int64_t* __restrict__ cptr,
     const float* __restrict__ invL, int nrays, int nv, float sv, float step, int cl, float zc,
-    const float* __restrict__ vol, float* __restrict__ sino, const int* halt) {
+    const float* __restrict__ vol, const unsigned long long* __restrict__ occ,
+    float* __restrict__ sino, const int* halt) {
     if (halted(halt)) return;
     __shared__ float4 sb[CONE_BATCH];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -161,13 +162,32 @@ __global__ void __launch_bounds__(32 * CONE_WARPS) k_cone_fwd(
         const bool hit = dv < nv && !(fmaxf(za, zb) < -1.f || fminf(za, zb) >= (float)cl);
         any = __any_sync(0xffffffffu, hit);
     }
+    static_assert(CONE_BATCH == 32 * CONE_WARPS, "one staged entry per thread");
+    __shared__ int s_wcnt[CONE_WARPS];
     for (int64_t j0 = b; j0 < e; j0 += CONE_BATCH) {
         __syncthreads();
-        for (int i = threadIdx.x; i < CONE_BATCH && j0 + i < e; i += 32 * CONE_WARPS)
-            sb[i] = *reinterpret_cast<const float4*>(CE + j0 + i);
+        // stage this batch, compacted to the entries whose pixel column has an
+        // occupied tile (the others read only zeros); order is kept
+        const int t = threadIdx.x;
+        float4 en_t = make_float4(0.f, 0.f, 0.f, 0.f);
+        bool keep = j0 + t < e;
+        if (keep) {
+            en_t = *reinterpret_cast<const float4*>(CE + j0 + t);
+            if (occ) keep = occ[__float_as_int(en_t.w)] != 0ull;
+        }
+        const unsigned km = __ballot_sync(0xffffffffu, keep);
+        if (lane == 0) s_wcnt[wid] = __popc(km);
+        __syncthreads();
+        int base = 0, cnt = 0;
+#pragma unroll
+        for (int q = 0; q < CONE_WARPS; ++q) {
+            const int v = s_wcnt[q];
+            base += q < wid ? v : 0;
+            cnt += v;
+        }
+        if (keep) sb[base + __popc(km & ((1u << lane) - 1u))] = en_t;
         __syncthreads();
         if (!any) continue;
-        const int cnt = (int)min((int64_t)CONE_BATCH, e - j0);
 #pragma unroll 4
         for (int jj = 0; jj < cnt; ++jj) {
             const float4 en = sb[jj];
@@ -211,7 +231,7 @@ constexpr int CA_LEN = CA_ZW + 4;   // slot 0 = slice zb - 1, slots zn + 1.. = s
 __global__ void __launch_bounds__(32 * CA_WARPS) k_cone_adj(
     const ConeEntry* __restrict__ E, const int64_t* __restrict__ eptr, int64_t npix, int nv,
     float sv, int cl, float zc, const float* __restrict__ gs, float* __restrict__ out,
-    int accumulate, const int* halt) {
+    int accumulate, const unsigned long long* __restrict__ occ, int w, const int* halt) {
     if (halted(halt)) return;
     __shared__ float zacc[CA_WARPS][2 * CA_PMAX][CA_LEN];
     __shared__ float4 eb[CA_WARPS][32];
@@ -222,6 +242,13 @@ __global__ void __launch_bounds__(32 * CA_WARPS) k_cone_adj(
     const int64_t p = gw / nwin;
     if (p >= npix) return;
     const int zb = (int)(gw % nwin) * CA_ZW, zn = min(CA_ZW, cl - zb);
+    if (occ) {   // training step: output read only inside occupied tiles
+        const int tlo = zb >> 4, thi = (zb + zn - 1) >> 4;
+        const unsigned long long zm =
+            (thi >= 63 ? ~0ull : ((1ull << (thi + 1)) - 1ull)) & ~((1ull << tlo) - 1ull);
+        const int py = (int)(p / w), px = (int)(p - (int64_t)py * w);
+        if ((occ[(py >> 4) * ((w + 15) >> 4) + (px >> 4)] & zm) == 0ull) return;   // warp-uniform
+    }
     for (int k = 0; k < 2 * CA_PMAX; ++k)
         for (int i = lane; i < zn + 3; i += 32) zacc[wid][k][i] = 0.f;
     const float vmid = 0.5f * (float)(nv - 1);
@@ -430,16 +457,19 @@ int splatct_cone_entry_fill(const void* col_entries, const int64_t* cptr, int nr
 
 int splatct_cone_forward(const void* col_entries, const int64_t* cptr, const float* invL,
                          int nrays, int nv, double sv, double step, int w, int h, int c_local,
-                         double zc, const float* vol_yxz, float* sino, const int* halt,
-                         void* stream) {
+                         double zc, const float* vol_yxz, const uint64_t* col_occ, float* sino,
+                         const int* halt, void* stream) {
     SPLATCT_REQUIRE(nrays >= 0 && nv > 0 && c_local > 0 && w > 0 && h > 0,
                     "invalid cone forward sizes");
+    SPLATCT_REQUIRE(col_occ == nullptr || c_local <= 64 * 16, "occupancy needs <= 64 z tiles");
     const int chunks = (nv + 31) / 32;
     const int64_t blocks = (int64_t)nrays * ((chunks + CONE_WARPS - 1) / CONE_WARPS);
     if (blocks == 0) return SPLATCT_OK;
     k_cone_fwd<<<(unsigned)blocks, 32 * CONE_WARPS, 0, as_stream(stream)>>>(reinterpret_cast<const ConeColEntry*>(col_entries), cptr,
                                       invL, nrays, nv, (float)sv, (float)step, c_local,
-                                      (float)zc, vol_yxz, sino, halt);
+                                      (float)zc, vol_yxz,
+                                      reinterpret_cast<const unsigned long long*>(col_occ), sino,
+                                      halt);
     SPLATCT_LAUNCH_CK();
     return SPLATCT_OK;
 }
@@ -447,8 +477,9 @@ int splatct_cone_forward(const void* col_entries, const int64_t* cptr, const flo
 int splatct_cone_adjoint(const void* entries, const int64_t* eptr, const float* invL, int nrays,
                          int nv, double sv, double step, int w, int h, int c_local, double zc,
                          const float* gsino, float* gscaled, float* out_yxz, int accumulate,
-                         const int* halt, void* stream) {
+                         const uint64_t* col_occ, const int* halt, void* stream) {
     SPLATCT_REQUIRE(nv > 0 && c_local > 0 && w > 0 && h > 0, "invalid cone adjoint sizes");
+    SPLATCT_REQUIRE(col_occ == nullptr || c_local <= 64 * 16, "occupancy needs <= 64 z tiles");
     cudaStream_t s = as_stream(stream);
     const int64_t ng = (int64_t)nrays * nv;
     if (ng > 0) {
@@ -461,7 +492,8 @@ int splatct_cone_adjoint(const void* entries, const int64_t* eptr, const float* 
     const int64_t warps = np * ((c_local + CA_ZW - 1) / CA_ZW);
     k_cone_adj<<<(unsigned)((warps + CA_WARPS - 1) / CA_WARPS), 32 * CA_WARPS, 0, s>>>(
         reinterpret_cast<const ConeEntry*>(entries), eptr, np, nv, (float)sv, c_local, (float)zc,
-        gscaled, out_yxz, accumulate, halt);
+        gscaled, out_yxz, accumulate, reinterpret_cast<const unsigned long long*>(col_occ), w,
+        halt);
     SPLATCT_LAUNCH_CK();
     return SPLATCT_OK;
 }

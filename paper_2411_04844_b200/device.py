@@ -482,7 +482,7 @@ class ConeOperator:
                               device=vol.device)
         call("splatct_cone_forward", ptr(self.col_entries), ptr(self.cptr), ptr(self.inv_len),
              self.n_rays, self.nv, self.sv, self.step, self.w, self.h, cl, self._zc(z0),
-             ptr(vol), ptr(out), ptr(halt), stream_handle())
+             ptr(vol), occ if occ is not None else VP(0), ptr(out), ptr(halt), stream_handle())
         return out
 
     def adjoint(self, gsino: torch.Tensor, out: torch.Tensor | None = None, vol=None,
@@ -505,7 +505,8 @@ class ConeOperator:
             acc = 1
         call("splatct_cone_adjoint", ptr(self.entries), ptr(self.eptr), ptr(self.inv_len),
              self.n_rays, self.nv, self.sv, self.step, self.w, self.h, cl, self._zc(z0),
-             ptr(gsino), ptr(self.gscaled), ptr(out), acc, ptr(halt), stream_handle())
+             ptr(gsino), ptr(self.gscaled), ptr(out), acc, occ if occ is not None else VP(0),
+             ptr(halt), stream_handle())
         return out
 
 
