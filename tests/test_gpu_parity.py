@@ -426,11 +426,19 @@ def test_trainer_occupancy_skipping_is_exact():
     after ten iterations on a phantom with empty space around the body."""
     dev = D.require_cuda()
     dims = (96, 96, 64)
-    truth = phantom.shepp_logan_3d(*dims)
+    # a ball in a larger field of view: empty space around it
+    zz, yy, xx = np.mgrid[0:64, 0:96, 0:96]
+    ball = ((xx - 40.0) ** 2 + (yy - 52.0) ** 2 + (zz - 30.0) ** 2 <= 18.0 ** 2)
+    truth = core.VolumeGrid.from_zyx(ball.astype(np.float32))
     geom = core.ScanGeometry.fan(30, 160, 1.0, 150.0, 110.0)
     meas = projector.forward_project(truth, geom)
     box = core.BoxConfig.for_dims(17, dims)
-    cl = optim.init_cloud_fbp(projector.fbp(meas, geom, dims), 4000, 0, box=box)
+    rng = np.random.default_rng(13)
+    n = 3000
+    d = rng.normal(size=(n, 3))
+    d *= (rng.uniform(0, 1, n) ** (1 / 3) * 15.0 / np.linalg.norm(d, axis=1))[:, None]
+    cl = core.GaussianCloud(d + np.array([40.0, 52.0, 30.0]), np.full(n, 1.5),
+                            np.full(n, 0.05))
     outs = []
     for skip in (True, False):
         tr = Trainer(D.sino_to_device(meas.views, dev), geom, dims, box, loss.LossWeights(),
