@@ -15,3 +15,8 @@ timeout 1800 ncu --set full --clock-control none --import-source on -k regex:"k_
 echo "full rc=$?"
 timeout 1200 python tools/voxel_sweep.py > gpurun_out/${R}_voxel_sweep.jsonl 2> gpurun_out/voxel_sweep.err; echo "sweep rc=$?"
 tail -2 gpurun_out/${R}_pytest_gpu.log; tail -1 gpurun_out/${R}_smoke.log; tail -c 600 gpurun_out/${R}_bench.log; tail -c 400 gpurun_out/${R}_bench_ref.log
+# secondary configs (one line each)
+for cfg in c3 c4 c2cone; do
+  timeout 900 python bench.py --config $cfg --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/${R}_bench_$cfg.log 2>&1
+  tail -1 gpurun_out/${R}_bench_$cfg.log | python -c "import sys,json; d=json.loads(sys.stdin.read()); print('$cfg', d['value'], d['ms_per_step'], d['stages_ms'])" 2>/dev/null || tail -3 gpurun_out/${R}_bench_$cfg.log
+done
