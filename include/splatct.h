@@ -187,11 +187,12 @@ int splatct_proj_tv_partial_len(int w, int h, int c, int64_t* len);
 /* col_occ (optional, NULL = off): the voxelizer's tile-column occupancy of
  * vol_yxz (splatct_fvr_occupancy_offset into the bins workspace, valid after
  * splatct_fvr_forward); entries whose pixel column has no occupied z tile in
- * a warp's z range are skipped -- they would add exact zeros.  w: volume
- * width (pixel = y * w + x). */
+ * a warp's z range are skipped -- they would add exact zeros.  w, h: volume
+ * width and height (pixel = y * w + x). */
 int splatct_proj_forward_blocked(const int64_t* gptr, const int32_t* gidx, const float* gval,
                                  int n_rays, int kind, const float* vol_yxz, float* sino, int c,
-                                 const uint64_t* col_occ, int w, const int* halt, void* stream);
+                                 const uint64_t* col_occ, int w, int h, const int* halt,
+                                 void* stream);
 /* col_occ (optional, NULL = dense): the voxelizer's tile-column occupancy of
  * vol_yxz.  A 2x2-pixel quad x z-chunk whose one-voxel neighbourhood lies in
  * empty tiles is skipped: its TV terms are zero and its out_yxz values are

@@ -51,7 +51,7 @@ SIGNATURES: dict[str, list] = {
     "splatct_proj_block_fill": [c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp,
                                 c_vp, c_sz, c_vp],
     "splatct_proj_forward_blocked": [c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_i32, c_vp,
-                                     c_i32, c_vp, c_vp],
+                                     c_i32, c_i32, c_vp, c_vp],
     "splatct_fvr_occupancy_offset": [c_i64, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_szp],
     "splatct_proj_adjoint_blocked": [c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp,
                                      c_f64, c_f64, c_vp, c_vp, c_vp, c_vp, c_vp],

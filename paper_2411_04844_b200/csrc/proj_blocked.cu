@@ -384,22 +384,29 @@ __global__ void __launch_bounds__(32 * BS_WARPS, R == 8 ? 4 : 6) k_bspmm(GroupMa
                                                         const float4* __restrict__ gval,
                                                         const float* __restrict__ X,
                                                         float* __restrict__ Y, int c, int zsplit,
-                                                        TvB tv, Occ oc, const int* halt) {
+                                                        int zmajor, TvB tv, Occ oc,
+                                                        const int* halt) {
     if (halted(halt)) return;
     constexpr int RW = R / 4;   // float4 weight words per entry
     __shared__ int s_col[BS_WARPS][32];
     __shared__ float4 s_w[BS_WARPS][32 * RW];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t gw = blockIdx.x * (int64_t)BS_WARPS + wid;
-    const int64_t g = gw / zsplit;
-    if (g >= gm.ngroups()) return;
-    const int zb = (int)(gw % zsplit) * 32 * V + lane * V;
+    // zmajor (gathered operand larger than L2): z-chunk-major order, so the
+    // warps in flight share one z-chunk and the L2 working set is 1/zsplit of
+    // the operand (C4: 512 MB volume); otherwise a group's chunks run together
+    // and share its entry list
+    const int64_t ngr = gm.ngroups();
+    const int64_t g = zmajor ? gw % ngr : gw / zsplit;
+    const int zch = zmajor ? (int)(gw / ngr) : (int)(gw % zsplit);
+    if (g >= ngr || zch >= zsplit) return;
+    const int zb = zch * 32 * V + lane * V;
     const bool zok = zb < c;
     // empty-space skipping (forward only): the z tiles this warp's chunk covers;
     // an entry whose pixel column has no Gaussian in them reads only zeros
     unsigned long long zmask = ~0ull;
     if (oc.mode == 1) {
-        const int zlo = (int)(gw % zsplit) * 32 * V, zhi = min(zlo + 32 * V, c) - 1;
+        const int zlo = zch * 32 * V, zhi = min(zlo + 32 * V, c) - 1;
         const int tlo = zlo / 16, thi = zhi / 16;
         zmask = (thi >= 63 ? ~0ull : ((1ull << (thi + 1)) - 1ull)) & ~((1ull << tlo) - 1ull);
     }
@@ -407,7 +414,7 @@ __global__ void __launch_bounds__(32 * BS_WARPS, R == 8 ? 4 : 6) k_bspmm(GroupMa
     if (oc.mode == 2) {   // adjoint quads (kind 1): skip all-empty neighbourhoods
         const int qw = (gm.w + 1) / 2;
         const int x0 = 2 * (int)(g % qw), y0 = 2 * (int)(g / qw);
-        const int zlo = (int)(gw % zsplit) * 32 * V, zhi = min(zlo + 32 * V, c) - 1;
+        const int zlo = zch * 32 * V, zhi = min(zlo + 32 * V, c) - 1;
         const bool halo = (zlo == 0 && tv.halo_lo) || (zhi == c - 1 && tv.halo_hi);
         const int tlo = max(zlo - 1, 0) / 16, thi = min(zhi + 1, c - 1) / 16;
         const unsigned long long zm =
@@ -418,7 +425,7 @@ __global__ void __launch_bounds__(32 * BS_WARPS, R == 8 ? 4 : 6) k_bspmm(GroupMa
         for (int ty = tya; ty <= tyb; ++ty)
             for (int tx = txa; tx <= txb; ++tx) any |= oc.occ[ty * oc.ntx + tx];
         if (!halo && (any & zm) == 0ull) {   // warp-uniform
-            if (TV && tv.partial && lane == 0) tv.partial[(gw % zsplit) * (int64_t)gm.nrows + g] = 0.0;
+            if (TV && tv.partial && lane == 0) tv.partial[zch * (int64_t)gm.nrows + g] = 0.0;
             return;
         }
     }
@@ -490,7 +497,7 @@ __global__ void __launch_bounds__(32 * BS_WARPS, R == 8 ? 4 : 6) k_bspmm(GroupMa
         tv_epilogue_quad<V>(tv, gm, g, zb, c, zok, acc, Y, tvsum);
         if (tv.partial) {   // slot (z-chunk, quad): written once, reduced in fixed order
             tvsum = warp_sum(tvsum);
-            if (lane == 0) tv.partial[(gw % zsplit) * (int64_t)gm.nrows + g] = tvsum;
+            if (lane == 0) tv.partial[zch * (int64_t)gm.nrows + g] = tvsum;
         }
     } else {
 #pragma unroll
@@ -507,18 +514,21 @@ __global__ void __launch_bounds__(32 * BS_WARPS, R == 8 ? 4 : 6) k_bspmm(GroupMa
 template <int V, bool TV>
 static int launch_bspmm_v(const GroupMap& gm, const int64_t* gptr, const int32_t* gidx,
                           const float* gval, const float* X, float* Y, int c, const TvB& tv,
-                          const Occ& oc, const int* halt, cudaStream_t s) {
+                          const Occ& oc, int64_t vol_bytes, const int* halt, cudaStream_t s) {
     const int zsplit = (c + 32 * V - 1) / (32 * V);
     const int64_t warps = gm.ngroups() * zsplit;
+    // z-chunk-major order once the volume (the forward's gathered operand; a
+    // proxy for the adjoint's sinogram) outgrows ~3/4 of L2
+    const int zmajor = zsplit > 1 && vol_bytes > ((int64_t)96 << 20);
     const unsigned grid = (unsigned)((warps + BS_WARPS - 1) / BS_WARPS);
     if (!TV && gm.rows() == 8)
         k_bspmm<V, false, 8><<<grid, 32 * BS_WARPS, 0, s>>>(gm, gptr, gidx,
                                                          reinterpret_cast<const float4*>(gval), X,
-                                                         Y, c, zsplit, tv, oc, halt);
+                                                         Y, c, zsplit, zmajor, tv, oc, halt);
     else
         k_bspmm<V, TV, 4><<<grid, 32 * BS_WARPS, 0, s>>>(gm, gptr, gidx,
                                                          reinterpret_cast<const float4*>(gval), X,
-                                                         Y, c, zsplit, tv, oc, halt);
+                                                         Y, c, zsplit, zmajor, tv, oc, halt);
     SPLATCT_LAUNCH_CK();
     return SPLATCT_OK;
 }
@@ -532,14 +542,17 @@ static int vec_width(int c) {
 template <bool TV>
 static int launch_bspmm(const GroupMap& gm, const int64_t* gptr, const int32_t* gidx,
                         const float* gval, const float* X, float* Y, int c, const TvB& tv,
-                        const int* halt, cudaStream_t s, const Occ& oc = Occ{nullptr, 0, 0, 0}) {
+                        const int* halt, cudaStream_t s, const Occ& oc = Occ{nullptr, 0, 0, 0},
+                        int64_t vol_bytes = 0) {
     const int V = vec_width(c);
     SPLATCT_REQUIRE((uintptr_t)X % (4 * V) == 0 && (uintptr_t)Y % (4 * V) == 0 &&
                         (!TV || (uintptr_t)tv.vol % (4 * V) == 0),
                     "projector operands must be %d-byte aligned", 4 * V);
-    if (V == 4) return launch_bspmm_v<4, TV>(gm, gptr, gidx, gval, X, Y, c, tv, oc, halt, s);
-    if (V == 2) return launch_bspmm_v<2, TV>(gm, gptr, gidx, gval, X, Y, c, tv, oc, halt, s);
-    return launch_bspmm_v<1, TV>(gm, gptr, gidx, gval, X, Y, c, tv, oc, halt, s);
+    if (V == 4)
+        return launch_bspmm_v<4, TV>(gm, gptr, gidx, gval, X, Y, c, tv, oc, vol_bytes, halt, s);
+    if (V == 2)
+        return launch_bspmm_v<2, TV>(gm, gptr, gidx, gval, X, Y, c, tv, oc, vol_bytes, halt, s);
+    return launch_bspmm_v<1, TV>(gm, gptr, gidx, gval, X, Y, c, tv, oc, vol_bytes, halt, s);
 }
 
 static size_t block_smem() { return (size_t)BLK_CAP * 12; }
@@ -622,17 +635,17 @@ int splatct_proj_block_fill(const int64_t* ptr, const int32_t* idx, const float*
 
 int splatct_proj_forward_blocked(const int64_t* gptr, const int32_t* gidx, const float* gval,
                                  int n_rays, int kind, const float* vol_yxz, float* sino, int c,
-                                 const uint64_t* col_occ, int w, const int* halt, void* stream) {
-    SPLATCT_REQUIRE(n_rays >= 0 && c > 0, "invalid sizes");
+                                 const uint64_t* col_occ, int w, int h, const int* halt,
+                                 void* stream) {
+    SPLATCT_REQUIRE(n_rays >= 0 && c > 0 && w > 0 && h > 0, "invalid sizes");
     SPLATCT_REQUIRE(kind == 0 || kind == 2, "forward groups are kind 0 or 2");
-    SPLATCT_REQUIRE(col_occ == nullptr || (w > 0 && c <= 64 * 16),
-                    "occupancy skipping needs the volume width and <= 64 z tiles");
+    SPLATCT_REQUIRE(col_occ == nullptr || c <= 64 * 16, "occupancy needs <= 64 z tiles");
     GroupMap gm{kind, n_rays, 0, 0};
     TvB tv{};
     const Occ oc{reinterpret_cast<const unsigned long long*>(col_occ), w, (w + 15) / 16,
                  col_occ ? 1 : 0};
     return launch_bspmm<false>(gm, gptr, gidx, gval, vol_yxz, sino, c, tv, halt,
-                               as_stream(stream), oc);
+                               as_stream(stream), oc, (int64_t)w * h * c * 4);
 }
 
 int splatct_proj_adjoint_blocked(const int64_t* gptr, const int32_t* gidx, const float* gval,
@@ -650,9 +663,11 @@ int splatct_proj_adjoint_blocked(const int64_t* gptr, const int32_t* gidx, const
     cudaStream_t s = as_stream(stream);
     if (vol_yxz != nullptr && lambda_tv > 0.0) {
         SPLATCT_REQUIRE(tv_count > 0.0, "tv_count must be positive");
-        return launch_bspmm<true>(gm, gptr, gidx, gval, gsino, out_yxz, c, tv, halt, s, oc);
+        return launch_bspmm<true>(gm, gptr, gidx, gval, gsino, out_yxz, c, tv, halt, s, oc,
+                                  (int64_t)w * h * c * 4);
     }
-    return launch_bspmm<false>(gm, gptr, gidx, gval, gsino, out_yxz, c, tv, halt, s, oc);
+    return launch_bspmm<false>(gm, gptr, gidx, gval, gsino, out_yxz, c, tv, halt, s, oc,
+                               (int64_t)w * h * c * 4);
 }
 
 }  // extern "C"

@@ -355,7 +355,7 @@ class ProjectorOperator:
             g = self.fb
             call("splatct_proj_forward_blocked", ptr(g[0]), ptr(g[1]), ptr(g[2]), self.n_rays,
                  self.fkind, ptr(vol), ptr(out), c, occ if occ is not None else VP(0), self.w,
-                 ptr(halt), stream_handle())
+                 self.h, ptr(halt), stream_handle())
         else:
             call("splatct_proj_forward", ptr(self.a_ptr), ptr(self.a_col), ptr(self.a_val),
                  self.n_rays, ptr(vol), ptr(out), c, ptr(halt), stream_handle())
