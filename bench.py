@@ -496,6 +496,8 @@ def run_b200(args, cfg):
                    "parallelism": f"zslab{world}",
                    "cuda_graph": "whole iteration" if world == 1 else
                                  "GPU segments between eager NCCL collectives",
+                   "empty_space_skipping": "projector forward/adjoint skip tiles the voxelizer "
+                                           "left empty (bitwise-identical step)",
                    **({"cone_column_entries": op.n_samples, "cone_pixel_entries": op.n_entries}
                       if cone
                       else {"projector_nnz": nnz})},
