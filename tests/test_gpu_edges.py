@@ -102,3 +102,28 @@ def test_projector_ragged_depths(c):
     bp = projector.back_project(core.Sinogram.from_views(g), geom, (w, h, c))
     obp = O.project_adjoint(g, O.Geometry.fan(9, 40, 1.1, 60.0, 40.0), (w, h, c), 0.5)
     assert rel_l2(bp.zyx, obp) < VOL_TOL
+
+
+def test_deep_volume_has_no_occupancy_mask():
+    """More than 64 z tiles: no occupancy words (the step stays dense) and the
+    training step still runs through the same stages."""
+    import torch
+    from paper_2411_04844_b200 import device as D, loss
+    from paper_2411_04844_b200.trainer import Trainer
+    dev = D.require_cuda()
+    dims = (24, 20, 1040)
+    box = core.BoxConfig.cube(9)
+    plan = D.FvrPlan(10, dims, box.half, 0, dev)
+    assert plan.occupancy is None and plan.occupancy_words() is None
+    rng = np.random.default_rng(7)
+    n = 200
+    mu = np.stack([rng.uniform(2, d - 2, n) for d in dims], 1)
+    cloud = core.GaussianCloud(mu, rng.uniform(0.6, 1.5, n), rng.uniform(0, 1, n))
+    geom = core.ScanGeometry.parallel(6, 30)
+    meas = torch.rand((6, 30, dims[2]), device=dev)
+    tr = Trainer(meas, geom, dims, box, loss.LossWeights(), D.cloud_to_params(cloud, dev),
+                 max_iters=10, trace_cap=2)
+    tr.initial_volume()
+    tr.step()
+    tr.step()
+    assert np.all(np.isfinite(tr.trace_rows()[:, 0]))
