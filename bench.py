@@ -209,7 +209,7 @@ def stage_profile(tr, iters):
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(names) + 1)]
         l0 = _lib.launch_count()
         ev[0].record(s)
-        tr.op.forward(tr.vol, tr.pred, tr.halt, z0=tr.slab.z0, occ=tr.fvr.occupancy)
+        tr.op.forward(tr.vol, tr.pred, tr.halt, z0=tr.slab.z0, occ=tr.fvr)
         if not tr.per_slice and tr.comm.world > 1:
             tr.comm.allreduce_sum_(tr.pred)
         ev[1].record(s)
@@ -219,7 +219,7 @@ def stage_profile(tr, iters):
         lo, hi = tr.comm.halo(tr.vol)
         tr.op.adjoint(tr.gpred, tr.dl, vol=tr.vol, halo_lo=lo, halo_hi=hi, z0=tr.slab.z0,
                       lambda_tv=lw.lambda3, tv_count=tr.tv_count, tv_partial=tr.tv_part,
-                      halt=tr.halt, occ=tr.fvr.occupancy)
+                      halt=tr.halt, occ=tr.fvr)
         D.reduce_sum(tr.tv_part, tr.sums[2:3])
         ev[3].record(s)
         tr.comm.allreduce_sum_(tr.sums)
@@ -421,13 +421,11 @@ def run_b200(args, cfg):
         nb_f = op.fb[3] if op.fb else nnz
         nb_a = op.ab[3] if op.ab else nnz
         gath = {"proj_forward": nb_f * (cl * 4 + 20), "proj_adjoint_tv": nb_a * (cl * 4 + 20)}
-        occ_w = tr.fvr.occupancy_words()
+        occ_w = tr.fvr.pixel_occupancy_words()
         if op.fb and occ_w is not None:
             # empty-space skipping: (entry, z-chunk) gathers the forward actually makes
             zc = 128 if cl % 4 == 0 and cl >= 128 else (64 if cl % 2 == 0 and cl >= 64 else 32)
-            gidx = op.fb[1].long()
-            ct = (gidx // w // 16) * ((w + 15) // 16) + (gidx % w) // 16
-            words = occ_w[ct]
+            words = occ_w[op.fb[1].long()]
             n_kept = 0
             for z0_ in range(0, cl, zc):
                 lo_, hi_ = z0_ // 16, (min(z0_ + zc, cl) - 1) // 16

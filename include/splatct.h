@@ -98,6 +98,10 @@ int splatct_fvr_backward(const double* params, int64_t n, int w, int h, int c, i
  * more than 64 z tiles (no mask). */
 int splatct_fvr_occupancy_offset(int64_t n, int w, int h, int c, int hx, int hy, int hz,
                                  size_t* offset);
+/* The same per pixel column (w * h words, bit tz = the column's 16-slice
+ * segment in z tile tz has a non-zero voxel), recorded as the volume is stored. */
+int splatct_fvr_pixel_occupancy_offset(int64_t n, int w, int h, int c, int hx, int hy, int hz,
+                                       size_t* offset);
 int splatct_grad_norm_accum(const double* grads, int64_t n, double* accum, const int* halt,
                             void* stream);
 
@@ -184,11 +188,11 @@ int splatct_proj_tv_partial_len(int w, int h, int c, int64_t* len);
 /* Blocked applications: same results as splatct_proj_forward /
  * splatct_proj_adjoint (up to f32 summation order), one z-column load per
  * group entry feeding the group's rows (forward: kind 0 or 2 groups). */
-/* col_occ (optional, NULL = off): the voxelizer's tile-column occupancy of
- * vol_yxz (splatct_fvr_occupancy_offset into the bins workspace, valid after
- * splatct_fvr_forward); entries whose pixel column has no occupied z tile in
- * a warp's z range are skipped -- they would add exact zeros.  w, h: volume
- * width and height (pixel = y * w + x). */
+/* col_occ (optional, NULL = off): the voxelizer's PIXEL-column occupancy of
+ * vol_yxz (splatct_fvr_pixel_occupancy_offset into the bins workspace, valid
+ * after splatct_fvr_forward); entries whose pixel column is zero in a warp's
+ * z range are skipped -- they would add exact zeros.  w, h: volume width and
+ * height (pixel = y * w + x). */
 int splatct_proj_forward_blocked(const int64_t* gptr, const int32_t* gidx, const float* gval,
                                  int n_rays, int kind, const float* vol_yxz, float* sino, int c,
                                  const uint64_t* col_occ, int w, int h, const int* halt,
@@ -299,11 +303,12 @@ int splatct_fbp_backproject(const double* filtered, const double* cos_t, const d
  * (m*nu, nv); zc = (c_global-1)/2 - z0, so slab results are partial
  * projections that sum to the full one) and splatct_cone_adjoint (exact
  * transpose; gscaled is an (m*nu*nv) f32 scratch; accumulate != 0 adds into
- * out).  col_occ (optional, NULL = dense) is the voxelizer's tile-column
- * occupancy of the slab (splatct_fvr_occupancy_offset): the forward skips
- * entries whose pixel column has no occupied tile (exact zeros); the adjoint
- * then leaves pixels x z-windows without occupied tiles UNWRITTEN (training
- * step only: its consumer reads inside Gaussian footprints).
+ * out).  Optional occupancy (NULL = dense): the forward's col_occ is the
+ * voxelizer's PIXEL-column occupancy (splatct_fvr_pixel_occupancy_offset;
+ * entries whose column is all zero are skipped, exact); the adjoint's is the
+ * TILE-column occupancy (splatct_fvr_occupancy_offset): pixel x z-windows
+ * without an occupied tile are left UNWRITTEN (training step only: its
+ * consumer reads inside Gaussian footprints, i.e. occupied tiles).
  * ------------------------------------------------------------------------- */
 int splatct_cone_setup_scratch_bytes(int m, int nu, int w, int h, size_t* bytes);
 int splatct_cone_count(const double* cos_t, const double* sin_t, int m, int nu, double su,

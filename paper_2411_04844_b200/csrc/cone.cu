@@ -36,7 +36,7 @@ struct __align__(16) ConeColEntry {   // column-major (forward)
     int pix;
     float w;        // merged bilinear weight of the pixel's samples
     float tau;      // tbar / L
-    int tcol;       // 16 x 16 tile column of the pixel (empty-space skipping)
+    float pad;
 };
 
 struct __align__(16) ConeEntry {      // pixel-major (adjoint)
@@ -73,7 +73,7 @@ __global__ void k_cone_fill(Geom g, const int64_t* __restrict__ cptr,
         e.pix = pix;
         e.w = (float)w;
         e.tau = (float)(wt / w * inv_len);
-        e.tcol = (pix / g.w >> 4) * ((g.w + 15) >> 4) + ((pix % g.w) >> 4);
+        e.pad = 0.f;
         CE[j++] = e;
     });
 }
@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(32 * CONE_WARPS) k_cone_fwd(
         bool keep = j0 + t < e;
         if (keep) {
             en_t = *reinterpret_cast<const float4*>(CE + j0 + t);
-            if (occ) keep = occ[__float_as_int(en_t.w)] != 0ull;
+            if (occ) keep = occ[__float_as_int(en_t.x)] != 0ull;   // pixel column occupancy
         }
         const unsigned km = __ballot_sync(0xffffffffu, keep);
         if (lane == 0) s_wcnt[wid] = __popc(km);
@@ -246,6 +246,8 @@ __global__ void __launch_bounds__(32 * CA_WARPS) k_cone_adj(
         const int tlo = zb >> 4, thi = (zb + zn - 1) >> 4;
         const unsigned long long zm =
             (thi >= 63 ? ~0ull : ((1ull << (thi + 1)) - 1ull)) & ~((1ull << tlo) - 1ull);
+        // tile (footprint) occupancy: the backward reads every footprint voxel,
+        // including exact zeros, so value-based pixel occupancy would not do
         const int py = (int)(p / w), px = (int)(p - (int64_t)py * w);
         if ((occ[(py >> 4) * ((w + 15) >> 4) + (px >> 4)] & zm) == 0ull) return;   // warp-uniform
     }

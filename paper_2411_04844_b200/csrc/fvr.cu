@@ -59,7 +59,7 @@ struct FvrLayout {
     int64_t sort_blocks;
     int64_t emit_blocks;
     size_t o_fp, o_k0, o_v0, o_k1, o_v1, o_tcount, o_tstart, o_ctl, o_tickets, o_ghist, o_stat_e,
-        o_stat_s, o_occ, ctl_bytes, o_rec, o_flag, o_pos, o_order, o_scan2, total;
+        o_stat_s, o_occ, o_pocc, ctl_bytes, o_rec, o_flag, o_pos, o_order, o_scan2, total;
     int final_buf;    // which (k,v) buffer holds the sorted result
 };
 
@@ -112,6 +112,9 @@ static FvrLayout make_layout(int64_t n, int w, int h, int c, int hx, int hy, int
     // per (ty, tx) tile column: bit tz set when that tile has Gaussians
     // (written by the forward; read by the projector to skip all-zero z-runs)
     L.o_occ = take(sizeof(unsigned long long) * (size_t)L.ntx * L.nty);
+    // per pixel column (y * w + x): bit tz set when its 16-slice segment in z
+    // tile tz holds a non-zero voxel (the projector forward's skip test)
+    L.o_pocc = take(sizeof(unsigned long long) * (size_t)w * h);
     L.ctl_bytes = off - L.o_ctl;
     L.o_rec = take(sizeof(GRec) * (size_t)n);
     // backward visiting order for volumes that exceed L2 (Gaussians sorted by
@@ -461,6 +464,7 @@ __global__ void __launch_bounds__(256, 4) k_fvr_fwd(const GRec* __restrict__ rec
                                                  float* __restrict__ vol,
                                                  unsigned int* __restrict__ counter, int fetch,
                                                  unsigned long long* __restrict__ occ,
+                                                 unsigned long long* __restrict__ pocc,
                                                  const int* halt) {
     if (halted(halt)) return;
     __shared__ __align__(16) float tab[FWD_BATCH * TAB_STRIDE];
@@ -600,21 +604,29 @@ __global__ void __launch_bounds__(256, 4) k_fvr_fwd(const GRec* __restrict__ rec
                                    : sacc[cid][ch ^ ((cid >> 1) & 3)];
             if (x < w && y < h)
                 *reinterpret_cast<float4*>(vol + ((int64_t)y * w + x) * c + z0 + 4 * ch) = v;
+            if (!empty && ntz <= 64) {   // column segment occupancy (4 lanes per column)
+                const bool nz = v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f;
+                const unsigned b = __ballot_sync(0xffffffffu, nz);
+                if (ch == 0 && ((b >> (lane & ~3)) & 0xfu) && x < w && y < h)
+                    atomicOr(&pocc[(int64_t)y * w + x], 1ull << tzi);
+            }
         }
     } else {   // ragged z tile: one column per thread, scalar stores
         const int cid = threadIdx.x;
         const int x = x0 + (cid & (TT - 1)), y = y0 + cid / TT;
         if (x < w && y < h) {
             float* col = vol + ((int64_t)y * w + x) * c;
+            bool nz = false;
 #pragma unroll
             for (int q = 0; q < TT / 4; ++q) {
                 const float4 v = empty ? make_float4(0.f, 0.f, 0.f, 0.f)
                                        : sacc[cid][q ^ ((cid >> 1) & 3)];
-                if (z0 + 4 * q + 0 < c) col[z0 + 4 * q + 0] = v.x;
-                if (z0 + 4 * q + 1 < c) col[z0 + 4 * q + 1] = v.y;
-                if (z0 + 4 * q + 2 < c) col[z0 + 4 * q + 2] = v.z;
-                if (z0 + 4 * q + 3 < c) col[z0 + 4 * q + 3] = v.w;
+                if (z0 + 4 * q + 0 < c) { col[z0 + 4 * q + 0] = v.x; nz |= v.x != 0.f; }
+                if (z0 + 4 * q + 1 < c) { col[z0 + 4 * q + 1] = v.y; nz |= v.y != 0.f; }
+                if (z0 + 4 * q + 2 < c) { col[z0 + 4 * q + 2] = v.z; nz |= v.z != 0.f; }
+                if (z0 + 4 * q + 3 < c) { col[z0 + 4 * q + 3] = v.w; nz |= v.w != 0.f; }
             }
+            if (nz && ntz <= 64) atomicOr(&pocc[(int64_t)y * w + x], 1ull << tzi);
         }
     }
     }   // tile
@@ -992,7 +1004,7 @@ int splatct_fvr_forward(const double* params, int64_t n, int w, int h, int c, in
     k_fvr_fwd<<<(unsigned)grid, 256, 0, as_stream(stream)>>>(
         at<GRec>(ws, L.o_rec), w, h, c, z0, hx, hy, hz, L.ntx, L.nty, L.nt, L.Sl,
         at<uint32_t>(ws, L.o_tstart), at<uint32_t>(ws, vo), vol_yxz, counter, (int)fetch,
-        at<unsigned long long>(ws, L.o_occ), halt);
+        at<unsigned long long>(ws, L.o_occ), at<unsigned long long>(ws, L.o_pocc), halt);
     SPLATCT_LAUNCH_CK();
     return SPLATCT_OK;
 }
@@ -1047,6 +1059,14 @@ int splatct_fvr_occupancy_offset(int64_t n, int w, int h, int c, int hx, int hy,
     SPLATCT_REQUIRE(offset != nullptr, "null offset");
     // the mask needs one bit per z tile
     *offset = L.ntz <= 64 ? L.o_occ : (size_t)-1;
+    return SPLATCT_OK;
+}
+
+int splatct_fvr_pixel_occupancy_offset(int64_t n, int w, int h, int c, int hx, int hy, int hz,
+                                       size_t* offset) {
+    FvrLayout L = make_layout(n, w, h, c, hx, hy, hz);
+    SPLATCT_REQUIRE(offset != nullptr, "null offset");
+    *offset = L.ntz <= 64 ? L.o_pocc : (size_t)-1;
     return SPLATCT_OK;
 }
 

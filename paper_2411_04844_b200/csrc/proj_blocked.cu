@@ -197,9 +197,11 @@ struct TvB {
 
 __device__ __forceinline__ int sgnf(float d) { return (d > 0.f) - (d < 0.f); }
 
-// Empty-space skipping for the forward (null occ: off): bit tz of
-// occ[(y / 16) * ntx + x / 16] says tile (x/16, y/16, tz) of the volume holds
-// Gaussians; other tiles are exactly zero (the voxelizer stores them as zeros)
+// Empty-space skipping (null occ: off).  Forward (mode 1): occ is per pixel
+// column, bit tz = its 16-slice segment in z tile tz has a non-zero voxel
+// (recorded by the voxelizer as it stores the volume); other segments are
+// exactly zero.  Adjoint (mode 2): occ is per 16 x 16 tile column, bit tz =
+// the tile holds Gaussians.
 // Adjoint (mode 2): a 2x2-pixel quad x z-chunk whose one-voxel neighbourhood
 // is all empty tiles is skipped entirely: its TV value and subgradient are
 // zero and its output is left unwritten -- the caller (the training step's
@@ -448,10 +450,7 @@ __global__ void __launch_bounds__(32 * BS_WARPS, R == 8 ? 4 : 6) k_bspmm(GroupMa
         int cnt = (int)min((int64_t)32, e - j0);
         if (oc.mode == 1) {   // keep the entries whose column is occupied, in order
             bool keep = lane < cnt;
-            if (keep) {
-                const int py = nc / oc.w, px = nc - py * oc.w;
-                keep = (oc.occ[(py >> 4) * oc.ntx + (px >> 4)] & zmask) != 0ull;
-            }
+            if (keep) keep = (oc.occ[nc] & zmask) != 0ull;   // the pixel column's segments
             const unsigned km = __ballot_sync(0xffffffffu, keep);
             if (keep) {
                 const int slot = __popc(km & ((1u << lane) - 1u));

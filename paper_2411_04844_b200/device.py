@@ -184,6 +184,18 @@ class FvrPlan:
         self.occupancy = (None if off == ctypes.c_size_t(-1).value
                           else VP(self.ws.data_ptr() + off))
         self._occ_off = None if self.occupancy is None else off
+        poff = size_query("splatct_fvr_pixel_occupancy_offset", self.n, self.w, self.h, self.c,
+                          self.hx, self.hy, self.hz)
+        # per pixel column: which 16-slice segments hold non-zero voxels
+        self.pixel_occupancy = (None if poff == ctypes.c_size_t(-1).value
+                                else VP(self.ws.data_ptr() + poff))
+        self._pocc_off = None if self.pixel_occupancy is None else poff
+
+    def pixel_occupancy_words(self) -> torch.Tensor | None:
+        """The pixel-column occupancy words as an int64 tensor [h * w] (a workspace view)."""
+        if self._pocc_off is None:
+            return None
+        return self.ws[self._pocc_off:self._pocc_off + 8 * self.w * self.h].view(torch.int64)
 
     def occupancy_words(self) -> torch.Tensor | None:
         """The occupancy words as an int64 tensor [nty * ntx] (a view of the workspace)."""
@@ -239,6 +251,14 @@ class FvrPlan:
 # resident warps and the zero-weight FMAs double -- so it stays available in
 # the ABI but unused.
 FWD_GROUP_KIND = 0
+
+
+def _occ(occ, kind: str):
+    """The occupancy pointer an operator needs from `occ`: an FvrPlan (its
+    pixel mask for forwards, its tile mask for adjoints), a raw pointer, or None."""
+    if occ is None or isinstance(occ, VP):
+        return occ
+    return occ.pixel_occupancy if kind == "pixel" else occ.occupancy
 
 
 class ProjectorOperator:
@@ -351,6 +371,7 @@ class ProjectorOperator:
         c = int(vol.shape[2])
         if out is None:
             out = torch.empty((self.m, self.n_det, c), dtype=torch.float32, device=vol.device)
+        occ = _occ(occ, "pixel")
         if self.blocked if blocked is None else blocked:
             g = self.fb
             call("splatct_proj_forward_blocked", ptr(g[0]), ptr(g[1]), ptr(g[2]), self.n_rays,
@@ -375,6 +396,7 @@ class ProjectorOperator:
             out = torch.empty((self.h, self.w, c), dtype=torch.float32, device=gsino.device)
         args = (ptr(gsino), ptr(vol), ptr(halo_lo), ptr(halo_hi), float(lambda_tv),
                 float(tv_count), ptr(out), ptr(tv_partial), ptr(halt), stream_handle())
+        occ = _occ(occ, "tile")
         if getattr(self, "blocked", False) if blocked is None else blocked:
             g = self.ab
             call("splatct_proj_adjoint_blocked", ptr(g[0]), ptr(g[1]), ptr(g[2]), self.w, self.h,
@@ -480,6 +502,7 @@ class ConeOperator:
         if out is None:
             out = torch.empty((self.m, self.n_det, self.nv), dtype=torch.float32,
                               device=vol.device)
+        occ = _occ(occ, "pixel")
         call("splatct_cone_forward", ptr(self.col_entries), ptr(self.cptr), ptr(self.inv_len),
              self.n_rays, self.nv, self.sv, self.step, self.w, self.h, cl, self._zc(z0),
              ptr(vol), occ if occ is not None else VP(0), ptr(out), ptr(halt), stream_handle())
@@ -503,6 +526,7 @@ class ConeOperator:
                               lambda_tv=lambda_tv, tv_count=tv_count, tv_partial=tv_partial,
                               halt=halt, blocked=False, c_local=cl)
             acc = 1
+        occ = _occ(occ, "tile")
         call("splatct_cone_adjoint", ptr(self.entries), ptr(self.eptr), ptr(self.inv_len),
              self.n_rays, self.nv, self.sv, self.step, self.w, self.h, cl, self._zc(z0),
              ptr(gsino), ptr(self.gscaled), ptr(out), acc, occ if occ is not None else VP(0),

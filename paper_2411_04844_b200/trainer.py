@@ -186,7 +186,7 @@ class Trainer:
         st = []
 
         def project():   # empty-space skipping from the voxelizer's tile occupancy
-            self.op.forward(self.vol, self.pred, halt, z0=z0, occ=self.fvr.occupancy)
+            self.op.forward(self.vol, self.pred, halt, z0=z0, occ=self.fvr)
         st.append(("gpu", project))
         if replicated:   # partial cone projections -> full
             st.append(("comm", lambda: self.comm.allreduce_sum_(self.pred)))
@@ -211,14 +211,13 @@ class Trainer:
                 # dl is read only inside footprints: skip empty neighbourhoods
                 self.op.adjoint(self.gpred, self.dl, vol=self.vol, halo_lo=lo, halo_hi=hi,
                                 lambda_tv=lw.lambda3, tv_count=self.tv_count,
-                                tv_partial=self.tv_part, halt=halt, z0=z0,
-                                occ=self.fvr.occupancy)
+                                tv_partial=self.tv_part, halt=halt, z0=z0, occ=self.fvr)
                 D.reduce_sum(self.tv_part, self.sums[2:3])
             st.append(("gpu", adjoint_tv))
         else:
             st.append(("gpu", lambda: self.op.adjoint(self.gpred, self.dl, halt=halt, z0=z0,
                                                       c_local=self.slab.c_local,
-                                                      occ=self.fvr.occupancy)))
+                                                      occ=self.fvr)))
         if sharded:
             st.append(("comm", lambda: self.comm.allreduce_sum_(self.sums)))
 

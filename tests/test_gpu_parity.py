@@ -416,7 +416,7 @@ def test_projector_occupancy_skip_is_exact(dims, c_note):
     geom = core.ScanGeometry.fan(20, 90, 1.3, 120.0, 90.0)
     op = D.ProjectorOperator(geom, w, h, 0.5, dev)
     dense = op.forward(vol)
-    skip = op.forward(vol, occ=plan.occupancy)
+    skip = op.forward(vol, occ=plan)
     np.testing.assert_array_equal(skip.cpu().numpy(), dense.cpu().numpy())
 
 
@@ -444,7 +444,7 @@ def test_trainer_occupancy_skipping_is_exact():
         tr = Trainer(D.sino_to_device(meas.views, dev), geom, dims, box, loss.LossWeights(),
                      D.cloud_to_params(cl, dev), max_iters=100, trace_cap=10)
         if not skip:
-            tr.fvr.occupancy = None
+            tr.fvr.occupancy = tr.fvr.pixel_occupancy = None
         tr.initial_volume()
         for _ in range(10):
             tr.step()
