@@ -92,16 +92,17 @@ int splatct_fvr_backward(const double* params, int64_t n, int w, int h, int c, i
 /* accum[i] += |(grads[0][i], grads[1][i], grads[2][i])| -- the densification
  * statistic of fvr.py:266-273, applied after the cross-slab gradient
  * all-reduce when the volume is sharded. */
-/* Byte offset, inside the splatct_fvr_bin workspace, of the tile-column
- * occupancy words (uint64 per (ty, tx) tile column, bit tz = the tile has
- * Gaussians), written by splatct_fvr_forward; SIZE_MAX when the volume has
- * more than 64 z tiles (no mask). */
-int splatct_fvr_occupancy_offset(int64_t n, int w, int h, int c, int hx, int hy, int hz,
-                                 size_t* offset);
-/* The same per pixel column (w * h words, bit tz = the column's 16-slice
- * segment in z tile tz has a non-zero voxel), recorded as the volume is stored. */
+/* Empty-space masks inside the splatct_fvr_bin workspace, written by
+ * splatct_fvr_forward (one uint64 per pixel column, w * h words; SIZE_MAX
+ * offset when the volume has more than 64 z tiles):
+ *  - pixel occupancy: bit tz = the column's 16-slice segment in z tile tz holds
+ *    a non-zero voxel (value-based; the projector forwards' skip test);
+ *  - footprint coverage: bit tz = a Gaussian footprint covers the column in z
+ *    tile tz (what splatct_fvr_backward reads; the adjoints' skip test). */
 int splatct_fvr_pixel_occupancy_offset(int64_t n, int w, int h, int c, int hx, int hy, int hz,
                                        size_t* offset);
+int splatct_fvr_footprint_coverage_offset(int64_t n, int w, int h, int c, int hx, int hy, int hz,
+                                          size_t* offset);
 int splatct_grad_norm_accum(const double* grads, int64_t n, double* accum, const int* halt,
                             void* stream);
 
@@ -197,12 +198,12 @@ int splatct_proj_forward_blocked(const int64_t* gptr, const int32_t* gidx, const
                                  int n_rays, int kind, const float* vol_yxz, float* sino, int c,
                                  const uint64_t* col_occ, int w, int h, const int* halt,
                                  void* stream);
-/* col_occ (optional, NULL = dense): the voxelizer's tile-column occupancy of
- * vol_yxz.  A 2x2-pixel quad x z-chunk whose one-voxel neighbourhood lies in
- * empty tiles is skipped: its TV terms are zero and its out_yxz values are
- * LEFT UNWRITTEN -- only for callers that read the result inside occupied
- * tiles (the training step's voxelizer backward reads it inside Gaussian
- * footprints).  Its tv_partial slots are written as 0. */
+/* col_occ (optional, NULL = dense): the voxelizer's footprint coverage of
+ * vol_yxz (splatct_fvr_footprint_coverage_offset).  A 2x2-pixel quad x
+ * z-chunk whose one-voxel neighbourhood no footprint covers is skipped: its
+ * TV terms are zero (the volume is zero there) and its out_yxz values are
+ * LEFT UNWRITTEN -- only for callers that read the result inside footprints
+ * (the training step's voxelizer backward).  Its tv_partial slots are 0. */
 int splatct_proj_adjoint_blocked(const int64_t* gptr, const int32_t* gidx, const float* gval,
                                  int w, int h, int c, const float* gsino, const float* vol_yxz,
                                  const float* halo_lo, const float* halo_hi, double lambda_tv,
@@ -306,9 +307,9 @@ int splatct_fbp_backproject(const double* filtered, const double* cos_t, const d
  * out).  Optional occupancy (NULL = dense): the forward's col_occ is the
  * voxelizer's PIXEL-column occupancy (splatct_fvr_pixel_occupancy_offset;
  * entries whose column is all zero are skipped, exact); the adjoint's is the
- * TILE-column occupancy (splatct_fvr_occupancy_offset): pixel x z-windows
- * without an occupied tile are left UNWRITTEN (training step only: its
- * consumer reads inside Gaussian footprints, i.e. occupied tiles).
+ * FOOTPRINT coverage (splatct_fvr_footprint_coverage_offset): pixel x
+ * z-windows no footprint covers are left UNWRITTEN (training step only: its
+ * consumer, splatct_fvr_backward, reads inside Gaussian footprints).
  * ------------------------------------------------------------------------- */
 int splatct_cone_setup_scratch_bytes(int m, int nu, int w, int h, size_t* bytes);
 int splatct_cone_count(const double* cos_t, const double* sin_t, int m, int nu, double su,

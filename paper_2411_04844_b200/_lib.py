@@ -52,7 +52,8 @@ SIGNATURES: dict[str, list] = {
                                 c_vp, c_sz, c_vp],
     "splatct_proj_forward_blocked": [c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_i32, c_vp,
                                      c_i32, c_i32, c_vp, c_vp],
-    "splatct_fvr_occupancy_offset": [c_i64, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_szp],
+    "splatct_fvr_footprint_coverage_offset": [c_i64, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32,
+                                              c_szp],
     "splatct_fvr_pixel_occupancy_offset": [c_i64, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32,
                                            c_szp],
     "splatct_proj_adjoint_blocked": [c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp,

@@ -246,10 +246,9 @@ __global__ void __launch_bounds__(32 * CA_WARPS) k_cone_adj(
         const int tlo = zb >> 4, thi = (zb + zn - 1) >> 4;
         const unsigned long long zm =
             (thi >= 63 ? ~0ull : ((1ull << (thi + 1)) - 1ull)) & ~((1ull << tlo) - 1ull);
-        // tile (footprint) occupancy: the backward reads every footprint voxel,
-        // including exact zeros, so value-based pixel occupancy would not do
-        const int py = (int)(p / w), px = (int)(p - (int64_t)py * w);
-        if ((occ[(py >> 4) * ((w + 15) >> 4) + (px >> 4)] & zm) == 0ull) return;   // warp-uniform
+        // footprint coverage (the backward reads every footprint voxel, including
+        // exact zeros, so the value-based pixel occupancy would not do)
+        if ((occ[p] & zm) == 0ull) return;   // warp-uniform
     }
     for (int k = 0; k < 2 * CA_PMAX; ++k)
         for (int i = lane; i < zn + 3; i += 32) zacc[wid][k][i] = 0.f;

@@ -59,7 +59,8 @@ struct FvrLayout {
     int64_t sort_blocks;
     int64_t emit_blocks;
     size_t o_fp, o_k0, o_v0, o_k1, o_v1, o_tcount, o_tstart, o_ctl, o_tickets, o_ghist, o_stat_e,
-        o_stat_s, o_occ, o_pocc, ctl_bytes, o_rec, o_flag, o_pos, o_order, o_scan2, total;
+        o_stat_s, o_pocc, o_fcov, ctl_bytes, o_rec, o_flag, o_pos, o_order, o_scan2,
+        total;
     int final_buf;    // which (k,v) buffer holds the sorted result
 };
 
@@ -109,12 +110,12 @@ static FvrLayout make_layout(int64_t n, int w, int h, int c, int hx, int hy, int
     L.o_stat_e = take(sizeof(unsigned long long) * (size_t)(L.emit_blocks > 0 ? L.emit_blocks : 1));
     L.o_stat_s = take(sizeof(unsigned long long) * RADIX * (size_t)L.passes *
                       (size_t)(L.sort_blocks > 0 ? L.sort_blocks : 1));
-    // per (ty, tx) tile column: bit tz set when that tile has Gaussians
-    // (written by the forward; read by the projector to skip all-zero z-runs)
-    L.o_occ = take(sizeof(unsigned long long) * (size_t)L.ntx * L.nty);
     // per pixel column (y * w + x): bit tz set when its 16-slice segment in z
     // tile tz holds a non-zero voxel (the projector forward's skip test)
     L.o_pocc = take(sizeof(unsigned long long) * (size_t)w * h);
+    // per pixel column: bit tz set when a Gaussian footprint covers the column
+    // inside z tile tz (what the backward reads; the adjoints' skip test)
+    L.o_fcov = take(sizeof(unsigned long long) * (size_t)w * h);
     L.ctl_bytes = off - L.o_ctl;
     L.o_rec = take(sizeof(GRec) * (size_t)n);
     // backward visiting order for volumes that exceed L2 (Gaussians sorted by
@@ -463,13 +464,14 @@ __global__ void __launch_bounds__(256, 4) k_fvr_fwd(const GRec* __restrict__ rec
                                                  const uint32_t* __restrict__ svals,
                                                  float* __restrict__ vol,
                                                  unsigned int* __restrict__ counter, int fetch,
-                                                 unsigned long long* __restrict__ occ,
                                                  unsigned long long* __restrict__ pocc,
+                                                 unsigned long long* __restrict__ fcov,
                                                  const int* halt) {
     if (halted(halt)) return;
     __shared__ __align__(16) float tab[FWD_BATCH * TAB_STRIDE];
     __shared__ __align__(16) float4 sacc[TT * TT][TT / 4];   // [y*16+x][z/4], swizzled
     __shared__ int64_t s_next;
+    __shared__ unsigned s_rows[TT];   // footprint coverage: x bits per tile row
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int g = lane >> 2, t4 = lane & 3;        // mma fragment coordinates
     const int r0 = 2 * wid;                        // this warp's two tile rows (y)
@@ -494,7 +496,8 @@ __global__ void __launch_bounds__(256, 4) k_fvr_fwd(const GRec* __restrict__ rec
     const int x0 = txi * TT, y0 = tyi * TT, z0 = tzi * TT;
     const uint32_t beg = tstart[t], end = tstart[t + 1];
     const bool empty = beg == end;
-    if (!empty && threadIdx.x == 0 && ntz <= 64) atomicOr(&occ[rest], 1ull << tzi);
+    // (the previous tile's readers passed the barrier after their read)
+    if (threadIdx.x < TT) s_rows[threadIdx.x] = 0u;
     float acc[4][4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
@@ -513,6 +516,18 @@ __global__ void __launch_bounds__(256, 4) k_fvr_fwd(const GRec* __restrict__ rec
             float* row = tab + tg * TAB_STRIDE;
             uint32_t* urow = reinterpret_cast<uint32_t*>(row);
             if (tg < nb) {
+                {   // footprint coverage of this tile's columns: rows tj, tj + 8
+                    const int bx0 = max(r.fx - hx, x0), bx1 = min(min(r.fx + hx, w - 1), x0 + TT - 1);
+                    const int by0 = max(r.fy - hy, y0), by1 = min(min(r.fy + hy, h - 1), y0 + TT - 1);
+                    if (bx0 <= bx1) {
+                        const unsigned xb = ((2u << (bx1 - x0)) - 1u) & ~((1u << (bx0 - x0)) - 1u);
+#pragma unroll
+                        for (int rr = 0; rr < 2; ++rr) {
+                            const int yy = y0 + tj + 8 * rr;
+                            if (yy >= by0 && yy <= by1) atomicOr(&s_rows[tj + 8 * rr], xb);
+                        }
+                    }
+                }
 #pragma unroll
                 for (int q = 0; q < 3 * TT / 8; ++q) {
                     const int e = tj + 8 * q, a = e / TT, l = e % TT;   // compile-time a per q
@@ -590,6 +605,12 @@ __global__ void __launch_bounds__(256, 4) k_fvr_fwd(const GRec* __restrict__ rec
             }
         }
         __syncthreads();
+    }
+    if (!empty && ntz <= 64) {   // after the last batch's barrier: coverage rows complete
+        const int x = x0 + (threadIdx.x & (TT - 1)), y = y0 + (threadIdx.x >> 4);
+        if (x < w && y < h && ((s_rows[threadIdx.x >> 4] >> (threadIdx.x & (TT - 1))) & 1u))
+            atomicOr(&fcov[(int64_t)y * w + x], 1ull << tzi);
+        __syncthreads();   // before the next tile zeroes the rows
     }
     // store: the tile's 256 columns x 64 B are written 8 columns per warp
     // instruction (4 lanes x 16 B per column) instead of 32 scattered
@@ -1004,7 +1025,8 @@ int splatct_fvr_forward(const double* params, int64_t n, int w, int h, int c, in
     k_fvr_fwd<<<(unsigned)grid, 256, 0, as_stream(stream)>>>(
         at<GRec>(ws, L.o_rec), w, h, c, z0, hx, hy, hz, L.ntx, L.nty, L.nt, L.Sl,
         at<uint32_t>(ws, L.o_tstart), at<uint32_t>(ws, vo), vol_yxz, counter, (int)fetch,
-        at<unsigned long long>(ws, L.o_occ), at<unsigned long long>(ws, L.o_pocc), halt);
+        at<unsigned long long>(ws, L.o_pocc),
+        at<unsigned long long>(ws, L.o_fcov), halt);
     SPLATCT_LAUNCH_CK();
     return SPLATCT_OK;
 }
@@ -1053,20 +1075,19 @@ int splatct_fvr_backward(const double* params, int64_t n, int w, int h, int c, i
     return SPLATCT_OK;
 }
 
-int splatct_fvr_occupancy_offset(int64_t n, int w, int h, int c, int hx, int hy, int hz,
-                                 size_t* offset) {
-    FvrLayout L = make_layout(n, w, h, c, hx, hy, hz);
-    SPLATCT_REQUIRE(offset != nullptr, "null offset");
-    // the mask needs one bit per z tile
-    *offset = L.ntz <= 64 ? L.o_occ : (size_t)-1;
-    return SPLATCT_OK;
-}
-
 int splatct_fvr_pixel_occupancy_offset(int64_t n, int w, int h, int c, int hx, int hy, int hz,
                                        size_t* offset) {
     FvrLayout L = make_layout(n, w, h, c, hx, hy, hz);
     SPLATCT_REQUIRE(offset != nullptr, "null offset");
     *offset = L.ntz <= 64 ? L.o_pocc : (size_t)-1;
+    return SPLATCT_OK;
+}
+
+int splatct_fvr_footprint_coverage_offset(int64_t n, int w, int h, int c, int hx, int hy, int hz,
+                                          size_t* offset) {
+    FvrLayout L = make_layout(n, w, h, c, hx, hy, hz);
+    SPLATCT_REQUIRE(offset != nullptr, "null offset");
+    *offset = L.ntz <= 64 ? L.o_fcov : (size_t)-1;
     return SPLATCT_OK;
 }
 

@@ -197,16 +197,16 @@ struct TvB {
 
 __device__ __forceinline__ int sgnf(float d) { return (d > 0.f) - (d < 0.f); }
 
-// Empty-space skipping (null occ: off).  Forward (mode 1): occ is per pixel
-// column, bit tz = its 16-slice segment in z tile tz has a non-zero voxel
-// (recorded by the voxelizer as it stores the volume); other segments are
-// exactly zero.  Adjoint (mode 2): occ is per 16 x 16 tile column, bit tz =
-// the tile holds Gaussians.
+// Empty-space skipping (null occ: off); one uint64 per pixel column.
+// Forward (mode 1): bit tz = the column's 16-slice segment in z tile tz has a
+// non-zero voxel (recorded by the voxelizer as it stores the volume); other
+// segments are exactly zero.  Adjoint (mode 2): bit tz = a Gaussian footprint
+// covers the column in z tile tz (what the voxelizer backward reads).
 // Adjoint (mode 2): a 2x2-pixel quad x z-chunk whose one-voxel neighbourhood
-// is all empty tiles is skipped entirely: its TV value and subgradient are
-// zero and its output is left unwritten -- the caller (the training step's
-// voxelizer backward) reads the adjoint only inside Gaussian footprints,
-// i.e. inside occupied tiles.
+// no footprint covers is skipped entirely: the volume is zero there, so its
+// TV value and subgradient are zero, and its output is left unwritten -- the
+// caller (the training step's voxelizer backward) reads the adjoint only
+// inside Gaussian footprints.
 struct Occ {
     const unsigned long long* occ;
     int w, ntx, mode;   // mode 1: forward entry skipping, 2: adjoint quad skipping
@@ -421,11 +421,12 @@ __global__ void __launch_bounds__(32 * BS_WARPS, R == 8 ? 4 : 6) k_bspmm(GroupMa
         const int tlo = max(zlo - 1, 0) / 16, thi = min(zhi + 1, c - 1) / 16;
         const unsigned long long zm =
             (thi >= 63 ? ~0ull : ((1ull << (thi + 1)) - 1ull)) & ~((1ull << tlo) - 1ull);
-        const int txa = max(x0 - 1, 0) >> 4, txb = min(x0 + 2, gm.w - 1) >> 4;
-        const int tya = max(y0 - 1, 0) >> 4, tyb = min(y0 + 2, gm.h - 1) >> 4;
+        // footprint coverage of the quad's pixels and their one-pixel ring
+        const int xa = max(x0 - 1, 0), xb = min(x0 + 2, gm.w - 1);
+        const int ya = max(y0 - 1, 0), yb = min(y0 + 2, gm.h - 1);
         unsigned long long any = 0ull;
-        for (int ty = tya; ty <= tyb; ++ty)
-            for (int tx = txa; tx <= txb; ++tx) any |= oc.occ[ty * oc.ntx + tx];
+        for (int yy = ya; yy <= yb; ++yy)
+            for (int xx = xa; xx <= xb; ++xx) any |= oc.occ[(int64_t)yy * gm.w + xx];
         if (!halo && (any & zm) == 0ull) {   // warp-uniform
             if (TV && tv.partial && lane == 0) tv.partial[zch * (int64_t)gm.nrows + g] = 0.0;
             return;

@@ -178,31 +178,31 @@ class FvrPlan:
         self.ws_bytes = size_query("splatct_fvr_workspace_bytes", self.n, self.w, self.h, self.c,
                                    self.hx, self.hy, self.hz)
         self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
-        off = size_query("splatct_fvr_occupancy_offset", self.n, self.w, self.h, self.c,
-                         self.hx, self.hy, self.hz)
-        # tile-column occupancy of the last forward (projector empty-space skipping)
-        self.occupancy = (None if off == ctypes.c_size_t(-1).value
-                          else VP(self.ws.data_ptr() + off))
-        self._occ_off = None if self.occupancy is None else off
+        # empty-space masks of the last forward (one word per pixel column):
+        # value-based occupancy for the projector forwards, footprint coverage
+        # for the adjoints (the backward reads every footprint voxel)
+        none = ctypes.c_size_t(-1).value
         poff = size_query("splatct_fvr_pixel_occupancy_offset", self.n, self.w, self.h, self.c,
                           self.hx, self.hy, self.hz)
-        # per pixel column: which 16-slice segments hold non-zero voxels
-        self.pixel_occupancy = (None if poff == ctypes.c_size_t(-1).value
-                                else VP(self.ws.data_ptr() + poff))
-        self._pocc_off = None if self.pixel_occupancy is None else poff
+        foff = size_query("splatct_fvr_footprint_coverage_offset", self.n, self.w, self.h,
+                          self.c, self.hx, self.hy, self.hz)
+        self._pocc_off = None if poff == none else poff
+        self._fcov_off = None if foff == none else foff
+        self.pixel_occupancy = None if poff == none else VP(self.ws.data_ptr() + poff)
+        self.footprint_coverage = None if foff == none else VP(self.ws.data_ptr() + foff)
+
+    def _words(self, off):
+        if off is None:
+            return None
+        return self.ws[off:off + 8 * self.w * self.h].view(torch.int64)
 
     def pixel_occupancy_words(self) -> torch.Tensor | None:
-        """The pixel-column occupancy words as an int64 tensor [h * w] (a workspace view)."""
-        if self._pocc_off is None:
-            return None
-        return self.ws[self._pocc_off:self._pocc_off + 8 * self.w * self.h].view(torch.int64)
+        """Pixel-column occupancy words, int64 [h * w] (a workspace view)."""
+        return self._words(self._pocc_off)
 
-    def occupancy_words(self) -> torch.Tensor | None:
-        """The occupancy words as an int64 tensor [nty * ntx] (a view of the workspace)."""
-        if self._occ_off is None:
-            return None
-        nw = ((self.w + 15) // 16) * ((self.h + 15) // 16)
-        return self.ws[self._occ_off:self._occ_off + 8 * nw].view(torch.int64)
+    def footprint_coverage_words(self) -> torch.Tensor | None:
+        """Pixel-column footprint coverage words, int64 [h * w] (a workspace view)."""
+        return self._words(self._fcov_off)
 
     def _geo(self):
         return (self.n, self.w, self.h, self.c, self.z0, self.hx, self.hy, self.hz)
@@ -254,11 +254,12 @@ FWD_GROUP_KIND = 0
 
 
 def _occ(occ, kind: str):
-    """The occupancy pointer an operator needs from `occ`: an FvrPlan (its
-    pixel mask for forwards, its tile mask for adjoints), a raw pointer, or None."""
+    """The mask an operator needs from `occ`: an FvrPlan (its value-based pixel
+    occupancy for forwards, its footprint coverage for adjoints), a raw
+    pointer, or None."""
     if occ is None or isinstance(occ, VP):
         return occ
-    return occ.pixel_occupancy if kind == "pixel" else occ.occupancy
+    return occ.pixel_occupancy if kind == "pixel" else occ.footprint_coverage
 
 
 class ProjectorOperator:
@@ -366,8 +367,8 @@ class ProjectorOperator:
                 blocked: bool | None = None, z0: int = 0, occ=None):
         """vol (h, w, c) -> sinogram (m, n, c); per-slice, so a slab's z0 is irrelevant.
 
-        occ: the voxelizer's tile-column occupancy of `vol` (FvrPlan.occupancy
-        after its forward) -- entries in all-zero z runs are skipped."""
+        occ: the FvrPlan whose forward produced `vol` (or its pixel_occupancy
+        pointer) -- entries in all-zero column segments are skipped (exact)."""
         c = int(vol.shape[2])
         if out is None:
             out = torch.empty((self.m, self.n_det, c), dtype=torch.float32, device=vol.device)
@@ -388,9 +389,9 @@ class ProjectorOperator:
                 c_local: int | None = None, occ=None):
         """sinogram (m, n, c) -> volume (h, w, c) [+ lambda_tv * TV subgradient of vol].
 
-        occ (training step only): the voxelizer's tile-column occupancy of vol;
-        the result is then written only around occupied tiles (the voxelizer
-        backward reads it only inside Gaussian footprints)."""
+        occ (training step only): the FvrPlan of vol (or its footprint_coverage
+        pointer); the result is then written only around Gaussian footprints,
+        which is where the voxelizer backward reads it."""
         c = int(c_local if c_local is not None else gsino.shape[2])
         if out is None:
             out = torch.empty((self.h, self.w, c), dtype=torch.float32, device=gsino.device)

@@ -114,7 +114,8 @@ def test_deep_volume_has_no_occupancy_mask():
     dims = (24, 20, 1040)
     box = core.BoxConfig.cube(9)
     plan = D.FvrPlan(10, dims, box.half, 0, dev)
-    assert plan.occupancy is None and plan.occupancy_words() is None
+    assert plan.pixel_occupancy is None and plan.footprint_coverage is None
+    assert plan.pixel_occupancy_words() is None
     rng = np.random.default_rng(7)
     n = 200
     mu = np.stack([rng.uniform(2, d - 2, n) for d in dims], 1)

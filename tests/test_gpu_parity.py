@@ -411,7 +411,7 @@ def test_projector_occupancy_skip_is_exact(dims, c_note):
     params = D.cloud_to_params(cloud, dev)
     plan.bin(params)
     vol = plan.forward(params, plan.new_volume())
-    occ = plan.occupancy_words().cpu().numpy().view(np.uint64)
+    occ = plan.pixel_occupancy_words().cpu().numpy().view(np.uint64)
     assert 0 < int(sum(bin(int(v)).count("1") for v in occ)) < occ.size * ((c + 15) // 16)
     geom = core.ScanGeometry.fan(20, 90, 1.3, 120.0, 90.0)
     op = D.ProjectorOperator(geom, w, h, 0.5, dev)
@@ -444,12 +444,12 @@ def test_trainer_occupancy_skipping_is_exact():
         tr = Trainer(D.sino_to_device(meas.views, dev), geom, dims, box, loss.LossWeights(),
                      D.cloud_to_params(cl, dev), max_iters=100, trace_cap=10)
         if not skip:
-            tr.fvr.occupancy = tr.fvr.pixel_occupancy = None
+            tr.fvr.footprint_coverage = tr.fvr.pixel_occupancy = None
         tr.initial_volume()
         for _ in range(10):
             tr.step()
         if skip:   # the phantom leaves empty tiles, so the skipping paths run
-            words = tr.fvr.occupancy_words().cpu().numpy().view(np.uint64)
+            words = tr.fvr.footprint_coverage_words().cpu().numpy().view(np.uint64)
             assert sum(bin(int(v)).count("1") for v in words) < words.size * 4
         outs.append((tr.trace_rows().copy(), tr.params.cpu().numpy()))
     np.testing.assert_array_equal(outs[0][0], outs[1][0])
