@@ -682,7 +682,7 @@ __global__ void k_tile_starts(const uint32_t* __restrict__ skeys,
 // warp sums a Gaussian's moments in a fixed order: deterministic, with no
 // partial buffer and no combine pass.  Gradient formulas: _kernels.py:132-205.
 // --------------------------------------------------------------------------
-constexpr int BG_WARPS = 8;
+constexpr int BG_WARPS = 4;
 constexpr int BG_XC = 17;   // box columns per register row (default box 17^3)
 
 // Fast path for boxes up to 17 columns x 17 slices (the default 17^3 box):
@@ -814,7 +814,7 @@ __global__ void k_order_scatter(const uint32_t* __restrict__ svals,
 // so only the column-pair path is compiled (its own register budget).
 // ORD: visit Gaussians in first-tile order (order[0] = count, order[1..])
 template <bool FAST, bool ORD>
-__global__ void __launch_bounds__(32 * BG_WARPS, FAST ? 3 : 2) k_fvr_bwd(const double* __restrict__ P, int64_t n,
+__global__ void __launch_bounds__(32 * BG_WARPS, FAST ? 6 : 4) k_fvr_bwd(const double* __restrict__ P, int64_t n,
                                                           const uint32_t* __restrict__ order,
                                                           const int32_t* __restrict__ fp,
                                                           const GRec* __restrict__ rec, int w,
