@@ -201,6 +201,7 @@ __global__ void __launch_bounds__(BIN_NT) k_bin_emit(
     GRec* __restrict__ rec, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
     uint32_t* __restrict__ ghist, unsigned long long* __restrict__ status,
     uint32_t* __restrict__ tickets, const int* halt) {
+    griddep_wait();
     if (halted(halt)) return;
     __shared__ unsigned s_blk;
     __shared__ uint32_t s_off[BIN_NT + 1];
@@ -336,6 +337,7 @@ __global__ void __launch_bounds__(SORT_NT) k_onesweep(
     uint32_t* __restrict__ kout, uint32_t* __restrict__ vout, const uint32_t* __restrict__ npairs,
     int shift, const uint32_t* __restrict__ ghist, unsigned long long* __restrict__ status,
     uint32_t* __restrict__ ticket, const int* halt) {
+    griddep_wait();
     if (halted(halt)) return;
     constexpr int NW = SORT_NT / 32;
     __shared__ unsigned s_blk;
@@ -467,6 +469,7 @@ __global__ void __launch_bounds__(256, 4) k_fvr_fwd(const GRec* __restrict__ rec
                                                  unsigned long long* __restrict__ pocc,
                                                  unsigned long long* __restrict__ fcov,
                                                  const int* halt) {
+    griddep_wait();
     if (halted(halt)) return;
     __shared__ __align__(16) float tab[FWD_BATCH * TAB_STRIDE];
     __shared__ __align__(16) float4 sacc[TT * TT][TT / 4];   // [y*16+x][z/4], swizzled
@@ -661,6 +664,7 @@ __global__ void __launch_bounds__(256, 4) k_fvr_fwd(const GRec* __restrict__ rec
 __global__ void k_tile_starts(const uint32_t* __restrict__ skeys,
                               const uint32_t* __restrict__ npairs, int64_t nt,
                               uint32_t* __restrict__ tstart, const int* halt) {
+    griddep_wait();
     if (halted(halt)) return;
     const int64_t np = npairs ? (int64_t)*npairs : 0;
     const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -823,6 +827,7 @@ __global__ void __launch_bounds__(32 * BG_WARPS, FAST ? 6 : 4) k_fvr_bwd(const d
                                                           double* __restrict__ G,
                                                           double* __restrict__ accum,
                                                           const int* halt) {
+    griddep_wait();
     if (halted(halt)) return;
     __shared__ float xt[3][BG_WARPS][32];   // ex, ex rx, ex rx^2
     __shared__ float2 yt[BG_WARPS][32];   // {ey, ry}
@@ -983,29 +988,32 @@ int splatct_fvr_bin(const double* params, int64_t n, int w, int h, int c, int z0
     const uint32_t* npairs = tickets + 1;
     if (n > 0) {
         SPLATCT_CK(cudaMemsetAsync(at<char>(ws, L.o_ctl), 0, L.ctl_bytes, s));
-        k_bin_emit<<<(unsigned)L.emit_blocks, BIN_NT, 0, s>>>(
-            params, n, w, h, c, z0, hx, hy, hz, L.ntx, L.nty, L.Sl, L.passes,
-            at<int32_t>(ws, L.o_fp), at<GRec>(ws, L.o_rec), at<uint32_t>(ws, L.o_k0),
-            at<uint32_t>(ws, L.o_v0), at<uint32_t>(ws, L.o_ghist),
-            at<unsigned long long>(ws, L.o_stat_e), tickets, halt);
+        SPLATCT_CK(launch_pdl(k_bin_emit, dim3((unsigned)L.emit_blocks), dim3(BIN_NT), 0, s,
+                              params, n, w, h, c, z0, hx, hy, hz, L.ntx, L.nty, L.Sl, L.passes,
+                              at<int32_t>(ws, L.o_fp), at<GRec>(ws, L.o_rec),
+                              at<uint32_t>(ws, L.o_k0), at<uint32_t>(ws, L.o_v0),
+                              at<uint32_t>(ws, L.o_ghist),
+                              at<unsigned long long>(ws, L.o_stat_e), tickets, halt));
         SPLATCT_LAUNCH_CK();
         for (int p = 0; p < L.passes; ++p) {
             const size_t ki = p % 2 ? L.o_k1 : L.o_k0, vi = p % 2 ? L.o_v1 : L.o_v0;
             const size_t ko = p % 2 ? L.o_k0 : L.o_k1, vo = p % 2 ? L.o_v0 : L.o_v1;
-            k_onesweep<<<(unsigned)L.sort_blocks, SORT_NT, 0, s>>>(
+            SPLATCT_CK(launch_pdl(
+                k_onesweep, dim3((unsigned)L.sort_blocks), dim3(SORT_NT), 0, s,
                 at<uint32_t>(ws, ki), at<uint32_t>(ws, vi), at<uint32_t>(ws, ko),
                 at<uint32_t>(ws, vo), npairs, 8 * p, at<uint32_t>(ws, L.o_ghist) + p * RADIX,
                 at<unsigned long long>(ws, L.o_stat_s) + (size_t)p * RADIX * L.sort_blocks,
-                tickets + 2 + p, halt);
+                tickets + 2 + p, halt));
             SPLATCT_LAUNCH_CK();
         }
     }
     {   // tile offsets from the sorted keys: no atomics
         const size_t ko = L.final_buf ? L.o_k1 : L.o_k0;
         const int64_t npk = n > 0 ? L.np : 0;
-        k_tile_starts<<<(unsigned)((npk + 1 + 255) / 256), 256, 0, s>>>(
-            n > 0 ? at<uint32_t>(ws, ko) : nullptr, n > 0 ? npairs : nullptr, L.nt,
-            at<uint32_t>(ws, L.o_tstart), halt);
+        SPLATCT_CK(launch_pdl(k_tile_starts, dim3((unsigned)((npk + 1 + 255) / 256)), dim3(256),
+                              0, s, n > 0 ? at<uint32_t>(ws, ko) : nullptr,
+                              n > 0 ? npairs : nullptr, L.nt, at<uint32_t>(ws, L.o_tstart),
+                              halt));
         SPLATCT_LAUNCH_CK();
     }
     return SPLATCT_OK;
@@ -1022,11 +1030,11 @@ int splatct_fvr_forward(const double* params, int64_t n, int w, int h, int c, in
     fetch = fetch < 1 ? 1 : (fetch > 32 ? 32 : fetch);
     unsigned int* counter = at<uint32_t>(ws, L.o_tcount);
     SPLATCT_CK(cudaMemsetAsync(counter, 0, sizeof(unsigned int), as_stream(stream)));
-    k_fvr_fwd<<<(unsigned)grid, 256, 0, as_stream(stream)>>>(
-        at<GRec>(ws, L.o_rec), w, h, c, z0, hx, hy, hz, L.ntx, L.nty, L.nt, L.Sl,
+    SPLATCT_CK(launch_pdl(k_fvr_fwd, dim3((unsigned)grid), dim3(256), 0, as_stream(stream),
+                          at<GRec>(ws, L.o_rec), w, h, c, z0, hx, hy, hz, L.ntx, L.nty, L.nt, L.Sl,
         at<uint32_t>(ws, L.o_tstart), at<uint32_t>(ws, vo), vol_yxz, counter, (int)fetch,
         at<unsigned long long>(ws, L.o_pocc),
-        at<unsigned long long>(ws, L.o_fcov), halt);
+        at<unsigned long long>(ws, L.o_fcov), halt));
     SPLATCT_LAUNCH_CK();
     return SPLATCT_OK;
 }
@@ -1060,17 +1068,18 @@ int splatct_fvr_backward(const double* params, int64_t n, int w, int h, int c, i
     }
     const bool fast = 2 * hx + 1 <= 17 && 2 * hz + 1 <= 17;
     auto launch = [&](auto fast_c, auto ord_c) {
-        k_fvr_bwd<decltype(fast_c)::value, decltype(ord_c)::value>
-            <<<grid, 32 * BG_WARPS, 0, s>>>(params, n, order, at<int32_t>(ws, L.o_fp),
-                                            at<GRec>(ws, L.o_rec), w, h, c, z0, up_yxz, grads,
-                                            accum, halt);
+        return launch_pdl(k_fvr_bwd<decltype(fast_c)::value, decltype(ord_c)::value>,
+                          dim3(grid), dim3(32 * BG_WARPS), 0, s, params, n,
+                          (const uint32_t*)order, (const int32_t*)at<int32_t>(ws, L.o_fp),
+                          (const GRec*)at<GRec>(ws, L.o_rec), w, h, c, z0, up_yxz, grads, accum,
+                          halt);
     };
     using T = std::true_type;
     using F = std::false_type;
-    if (fast && ord) launch(T{}, T{});
-    else if (fast) launch(T{}, F{});
-    else if (ord) launch(F{}, T{});
-    else launch(F{}, F{});
+    if (fast && ord) SPLATCT_CK(launch(T{}, T{}));
+    else if (fast) SPLATCT_CK(launch(T{}, F{}));
+    else if (ord) SPLATCT_CK(launch(F{}, T{}));
+    else SPLATCT_CK(launch(F{}, F{}));
     SPLATCT_LAUNCH_CK();
     return SPLATCT_OK;
 }

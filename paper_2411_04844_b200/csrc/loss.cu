@@ -360,6 +360,7 @@ __global__ void __launch_bounds__(R_NT, MODE == 1 ? 2 : 1) k_ssim_stats11(const 
                                                           double* __restrict__ part,
                                                           double* __restrict__ RS,
                                                           const int* halt) {
+    griddep_wait();
     if (halted(halt)) return;
     constexpr int NF = MODE == 0 ? 5 : (MODE == 1 ? 3 : 2);   // ring fields
     __shared__ __align__(16) float sf[R_BUF][2][R_SPAN][32];    // cp.async landing (f32)
@@ -531,6 +532,7 @@ __global__ void __launch_bounds__(R_NT, 2) k_loss_grad11(const float* __restrict
                                                          double ssim_slices, float* __restrict__ G,
                                                          double* __restrict__ part,
                                                          const int* halt) {
+    griddep_wait();
     if (halted(halt)) return;
     // per staged row: D columns s0-10 .. s0+7 (3 fields) and x, y columns s0 .. s0+7
     __shared__ __align__(16) double sd[G_BUF][3][R_SPAN][32];
@@ -693,6 +695,7 @@ __global__ void k_iter_finalize(const double* __restrict__ sums, double l1w, dou
                                 double lr0, double lrf, int64_t max_iters, int64_t* step,
                                 int64_t* iter, double* trace, int64_t trace_cap, double* adam,
                                 int* halt) {
+    griddep_wait();
     if (*halt) return;
     const double nan = __longlong_as_double(0x7ff8000000000000LL);
     const double l1 = l1w > 0 ? sums[0] / l1_count : nan;
@@ -727,6 +730,7 @@ __global__ void k_adam(double* __restrict__ P, const double* __restrict__ G,
                        double* __restrict__ M1, double* __restrict__ M2, int64_t n,
                        const double* __restrict__ adam, double sfloor, double sceil,
                        const int* halt) {
+    griddep_wait();
     if (halted(halt)) return;
     const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (idx >= 5 * n) return;
@@ -793,8 +797,8 @@ static int loss_fused_impl(const float* pred, const float* ref, int m, int n, in
         if (lambda2 > 0.0) {
             double* RS = reinterpret_cast<double*>(base + L.o_RS);
             if (prepared)
-                k_ssim_stats11<1><<<gs, R_NT, 0, s>>>(pred, ref, m, n, p, W, c1, c2, L.vr, L.vc,
-                                                      D11, ps, RS, halt);
+                SPLATCT_CK(launch_pdl(k_ssim_stats11<1>, gs, dim3(R_NT), 0, s, pred, ref, m, n, p,
+                                      W, c1, c2, L.vr, L.vc, D11, ps, RS, halt));
             else
                 k_ssim_stats11<0><<<gs, R_NT, 0, s>>>(pred, ref, m, n, p, W, c1, c2, L.vr, L.vc,
                                                       D11, ps, RS, halt);
@@ -803,8 +807,9 @@ static int loss_fused_impl(const float* pred, const float* ref, int m, int n, in
         } else {
             SPLATCT_CK(cudaMemsetAsync(sums + 1, 0, sizeof(double), s));
         }
-        k_loss_grad11<<<gg, R_NT, 0, s>>>(pred, ref, m, n, p, W, L.vr, L.vc, D11, lambda1,
-                                          l1_count, lambda2, ssim_slices, grad_pred, pl, halt);
+        SPLATCT_CK(launch_pdl(k_loss_grad11, gg, dim3(R_NT), 0, s, pred, ref, m, n, p, W, L.vr,
+                              L.vc, D11, lambda1, l1_count, lambda2, ssim_slices, grad_pred, pl,
+                              halt));
         SPLATCT_LAUNCH_CK();
         return reduce_sum_f64(pl, L.nb_g11, sums, s);
     }
@@ -896,9 +901,9 @@ int splatct_iter_finalize(const double* sums, double lambda1, double lambda2, do
                           double lrf, int64_t max_iters, int64_t* step, int64_t* iter,
                           double* trace, int64_t trace_cap, double* adam, int* halt,
                           void* stream) {
-    k_iter_finalize<<<1, 1, 0, as_stream(stream)>>>(sums, lambda1, lambda2, lambda3, l1_count,
-                                                    ssim_count, tv_count, lr0, lrf, max_iters,
-                                                    step, iter, trace, trace_cap, adam, halt);
+    SPLATCT_CK(launch_pdl(k_iter_finalize, dim3(1), dim3(1), 0, as_stream(stream), sums, lambda1,
+                          lambda2, lambda3, l1_count, ssim_count, tv_count, lr0, lrf, max_iters,
+                          step, iter, trace, trace_cap, adam, halt));
     SPLATCT_LAUNCH_CK();
     return SPLATCT_OK;
 }
@@ -908,8 +913,9 @@ int splatct_adam(double* params, const double* grads, double* m1, double* m2, in
                  void* stream) {
     if (n <= 0) return SPLATCT_OK;
     const int64_t tot = 5 * n;
-    k_adam<<<(unsigned)((tot + 255) / 256), 256, 0, as_stream(stream)>>>(
-        params, grads, m1, m2, n, adam, sigma_floor, sigma_ceiling, halt);
+    SPLATCT_CK(launch_pdl(k_adam, dim3((unsigned)((tot + 255) / 256)), dim3(256), 0,
+                          as_stream(stream), params, grads, m1, m2, n, adam, sigma_floor,
+                          sigma_ceiling, halt));
     SPLATCT_LAUNCH_CK();
     return SPLATCT_OK;
 }

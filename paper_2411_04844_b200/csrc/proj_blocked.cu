@@ -388,6 +388,7 @@ __global__ void __launch_bounds__(32 * BS_WARPS, R == 8 ? 4 : 6) k_bspmm(GroupMa
                                                         float* __restrict__ Y, int c, int zsplit,
                                                         int zmajor, TvB tv, Occ oc,
                                                         const int* halt) {
+    griddep_wait();
     if (halted(halt)) return;
     constexpr int RW = R / 4;   // float4 weight words per entry
     __shared__ int s_col[BS_WARPS][32];
@@ -521,14 +522,13 @@ static int launch_bspmm_v(const GroupMap& gm, const int64_t* gptr, const int32_t
     // proxy for the adjoint's sinogram) outgrows ~3/4 of L2
     const int zmajor = zsplit > 1 && vol_bytes > ((int64_t)96 << 20);
     const unsigned grid = (unsigned)((warps + BS_WARPS - 1) / BS_WARPS);
+    const float4* gv = reinterpret_cast<const float4*>(gval);
     if (!TV && gm.rows() == 8)
-        k_bspmm<V, false, 8><<<grid, 32 * BS_WARPS, 0, s>>>(gm, gptr, gidx,
-                                                         reinterpret_cast<const float4*>(gval), X,
-                                                         Y, c, zsplit, zmajor, tv, oc, halt);
+        SPLATCT_CK(launch_pdl(k_bspmm<V, false, 8>, dim3(grid), dim3(32 * BS_WARPS), 0, s, gm,
+                              gptr, gidx, gv, X, Y, c, zsplit, zmajor, tv, oc, halt));
     else
-        k_bspmm<V, TV, 4><<<grid, 32 * BS_WARPS, 0, s>>>(gm, gptr, gidx,
-                                                         reinterpret_cast<const float4*>(gval), X,
-                                                         Y, c, zsplit, zmajor, tv, oc, halt);
+        SPLATCT_CK(launch_pdl(k_bspmm<V, TV, 4>, dim3(grid), dim3(32 * BS_WARPS), 0, s, gm, gptr,
+                              gidx, gv, X, Y, c, zsplit, zmajor, tv, oc, halt));
     SPLATCT_LAUNCH_CK();
     return SPLATCT_OK;
 }

@@ -163,6 +163,7 @@ int exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, void* temp,
 
 __global__ void __launch_bounds__(1024) k_reduce_sum(const double* __restrict__ in, int64_t n,
                                                      double* __restrict__ out) {
+    griddep_wait();
     __shared__ double sh[32];
     double acc = 0.0;
     for (int64_t i = threadIdx.x; i < n; i += 1024) acc += in[i];
@@ -171,7 +172,7 @@ __global__ void __launch_bounds__(1024) k_reduce_sum(const double* __restrict__ 
 }
 
 int reduce_sum_f64(const double* in, int64_t n, double* out, cudaStream_t s) {
-    k_reduce_sum<<<1, 1024, 0, s>>>(in, n, out);
+    SPLATCT_CK(launch_pdl(k_reduce_sum, dim3(1), dim3(1024), 0, s, in, n, out));
     SPLATCT_LAUNCH_CK();
     return SPLATCT_OK;
 }
