@@ -53,18 +53,21 @@ def _worker(rank, world, port, q, variant):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("variant", ["fan", "cone"])
-def test_two_slab_ranks_match_single_device(variant):
+@pytest.mark.parametrize("variant,world", [("fan", 2), ("cone", 2), ("fan", 4)])
+def test_two_slab_ranks_match_single_device(variant, world):
+    """world 4: 9-10-slice slabs under a 17-slice box, so Gaussians straddle
+    three slabs (gradient all-reduce, TV halos on both sides)."""
     from paper_2411_04844_b200 import optim
     meas, geom, settings, cloud = _problem(variant)
     vol1, cl1, tr1 = optim.run_reconstruction(meas, geom, settings, init_cloud=cloud)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, variant)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, variant))
+             for r in range(world)]
     for p in procs:
         p.start()
-    res = sorted([q.get(timeout=300) for _ in range(2)], key=lambda t: t[0])
+    res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda t: t[0])
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -73,7 +76,8 @@ def test_two_slab_ranks_match_single_device(variant):
     rtol = 1e-6 if variant == "fan" else 1e-5
     for rank, vol, mu, trace in res:
         np.testing.assert_allclose(trace[:, 0], loss1, rtol=rtol)
-        np.testing.assert_allclose(mu, cl1.mu, rtol=0, atol=1e-6)   # all-reduce order
+        # all-reduce order (4 ranks: a few centres differ at 2e-7 relative)
+        np.testing.assert_allclose(mu, cl1.mu, rtol=1e-6, atol=1e-6)
     v = res[0][1]
     assert np.linalg.norm(v - vol1.zyx) / np.linalg.norm(vol1.zyx) < (1e-6 if variant == "fan"
                                                                       else 1e-5)
