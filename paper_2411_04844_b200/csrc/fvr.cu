@@ -341,8 +341,10 @@ __global__ void __launch_bounds__(SORT_NT) k_onesweep(
     if (halted(halt)) return;
     constexpr int NW = SORT_NT / 32;
     __shared__ unsigned s_blk;
-    __shared__ uint32_t wh[NW][RADIX];    // per-warp digit counts, then warp offsets
-    __shared__ uint32_t s_warp[NW];
+    __shared__ uint32_t wh[NW][RADIX];    // per-warp digit counts, then local warp offsets
+    __shared__ uint32_t s_warp[NW], s_lwarp[NW];
+    __shared__ uint32_t s_lstart[RADIX], s_gstart[RADIX];   // digit starts: block-local, global
+    __shared__ uint32_t sk[SORT_CHUNK], sv[SORT_CHUNK];      // the block's keys, locally sorted
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
     if (t == 0) s_blk = atomicAdd(ticket, 1u);
 #pragma unroll
@@ -383,33 +385,59 @@ __global__ void __launch_bounds__(SORT_NT) k_onesweep(
             prev = lookback(st, b, RADIX);
             atomicExch(&st[b * RADIX], LB_P | (prev + mine));
         }
+        // exclusive scans over digits: global digit counts and this block's totals
         const uint32_t gd = ghist[t];
-        uint32_t inc = gd;
+        uint32_t inc = gd, linc = mine;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += u;
+            const uint32_t lu = __shfl_up_sync(0xffffffffu, linc, o);
+            if (lane >= o) {
+                inc += u;
+                linc += lu;
+            }
         }
-        if (lane == 31) s_warp[wid] = inc;
+        if (lane == 31) {
+            s_warp[wid] = inc;
+            s_lwarp[wid] = linc;
+        }
         __syncthreads();
-        uint32_t acc = (uint32_t)prev + inc - gd;
-        for (int q = 0; q < wid; ++q) acc += s_warp[q];
+        uint32_t gpre = inc - gd, lpre = linc - mine;
+        for (int q = 0; q < wid; ++q) {
+            gpre += s_warp[q];
+            lpre += s_lwarp[q];
+        }
+        s_gstart[t] = (uint32_t)prev + gpre;   // global position of the block's first key t
+        s_lstart[t] = lpre;                    // its position in the block's sorted order
+        uint32_t acc = lpre;
 #pragma unroll
-        for (int q = 0; q < NW; ++q) {   // warp offsets for digit t, in warp order
+        for (int q = 0; q < NW; ++q) {   // local warp offsets for digit t, in warp order
             const uint32_t c2 = wh[q][t];
             wh[q][t] = acc;
             acc += c2;
         }
     }
     __syncthreads();
+    // sort the block's keys in shared memory, then write each digit's run with
+    // consecutive threads at consecutive global positions (coalesced)
+    int nvalid = 0;
 #pragma unroll
     for (int r = 0; r < SORT_IPT; ++r) {
         const int64_t g = wbase + r * 32;
         if (g < np) {
-            const uint32_t pos = wh[wid][(k[r] >> shift) & 255u] + rk[r];
-            kout[pos] = k[r];
-            vout[pos] = v[r];
+            const uint32_t lp = wh[wid][(k[r] >> shift) & 255u] + rk[r];
+            sk[lp] = k[r];
+            sv[lp] = v[r];
         }
+    }
+    nvalid = (int)min((int64_t)SORT_CHUNK, np - base);
+    __syncthreads();
+    for (int i = t; i < nvalid; i += SORT_NT) {
+        const uint32_t kk = sk[i];
+        const uint32_t d = (kk >> shift) & 255u;
+        const uint32_t pos = s_gstart[d] + ((uint32_t)i - s_lstart[d]);
+        kout[pos] = kk;
+        vout[pos] = sv[i];
     }
 }
 
