@@ -238,7 +238,7 @@ def stage_profile(tr, iters):
         ev[6].record(s)
         tr.fvr.bin(tr.params, tr.halt)
         ev[7].record(s)
-        tr.fvr.forward(tr.params, tr.vol, tr.halt)
+        tr.fvr.forward(tr.params, tr.vol, tr.halt, masks=True)
         ev[8].record(s)
         torch.cuda.synchronize()
         launches = _lib.launch_count() - l0

@@ -77,6 +77,12 @@ int splatct_fvr_bin(const double* params, int64_t n, int w, int h, int c, int z0
 int splatct_fvr_forward(const double* params, int64_t n, int w, int h, int c, int z0, int hx,
                         int hy, int hz, void* ws, size_t ws_bytes, float* vol_yxz,
                         const int* halt, void* stream);
+/* The same, also recording the two empty-space masks of the volume (pixel
+ * occupancy, footprint coverage; see splatct_fvr_pixel_occupancy_offset) --
+ * the training step's variant (the masks cost ~5-10 % of the splat). */
+int splatct_fvr_forward_masked(const double* params, int64_t n, int w, int h, int c, int z0,
+                               int hx, int hy, int hz, void* ws, size_t ws_bytes, float* vol_yxz,
+                               const int* halt, void* stream);
 
 /* Per-Gaussian gradients from dL/dV (yxz), fvr.py:227-273: per-tile partial
  * moments, combined per Gaussian in fixed slot order (deterministic).
@@ -93,7 +99,7 @@ int splatct_fvr_backward(const double* params, int64_t n, int w, int h, int c, i
  * statistic of fvr.py:266-273, applied after the cross-slab gradient
  * all-reduce when the volume is sharded. */
 /* Empty-space masks inside the splatct_fvr_bin workspace, written by
- * splatct_fvr_forward (one uint64 per pixel column, w * h words; SIZE_MAX
+ * splatct_fvr_forward_masked (one uint64 per pixel column, w * h words; SIZE_MAX
  * offset when the volume has more than 64 z tiles):
  *  - pixel occupancy: bit tz = the column's 16-slice segment in z tile tz holds
  *    a non-zero voxel (value-based; the projector forwards' skip test);

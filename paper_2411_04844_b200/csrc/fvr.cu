@@ -110,13 +110,14 @@ static FvrLayout make_layout(int64_t n, int w, int h, int c, int hx, int hy, int
     L.o_stat_e = take(sizeof(unsigned long long) * (size_t)(L.emit_blocks > 0 ? L.emit_blocks : 1));
     L.o_stat_s = take(sizeof(unsigned long long) * RADIX * (size_t)L.passes *
                       (size_t)(L.sort_blocks > 0 ? L.sort_blocks : 1));
+    L.ctl_bytes = off - L.o_ctl;
+    // empty-space masks (zeroed and written by the masked forward)
     // per pixel column (y * w + x): bit tz set when its 16-slice segment in z
     // tile tz holds a non-zero voxel (the projector forward's skip test)
     L.o_pocc = take(sizeof(unsigned long long) * (size_t)w * h);
     // per pixel column: bit tz set when a Gaussian footprint covers the column
     // inside z tile tz (what the backward reads; the adjoints' skip test)
     L.o_fcov = take(sizeof(unsigned long long) * (size_t)w * h);
-    L.ctl_bytes = off - L.o_ctl;
     L.o_rec = take(sizeof(GRec) * (size_t)n);
     // backward visiting order for volumes that exceed L2 (Gaussians sorted by
     // their first tile): first-slot flags, their exclusive scan, the list
@@ -547,7 +548,7 @@ __global__ void __launch_bounds__(256, 4) k_fvr_fwd(const GRec* __restrict__ rec
             float* row = tab + tg * TAB_STRIDE;
             uint32_t* urow = reinterpret_cast<uint32_t*>(row);
             if (tg < nb) {
-                {   // footprint coverage of this tile's columns: rows tj, tj + 8
+                if (fcov) {   // footprint coverage of this tile's columns: rows tj, tj + 8
                     const int bx0 = max(r.fx - hx, x0), bx1 = min(min(r.fx + hx, w - 1), x0 + TT - 1);
                     const int by0 = max(r.fy - hy, y0), by1 = min(min(r.fy + hy, h - 1), y0 + TT - 1);
                     if (bx0 <= bx1) {
@@ -637,7 +638,7 @@ __global__ void __launch_bounds__(256, 4) k_fvr_fwd(const GRec* __restrict__ rec
         }
         __syncthreads();
     }
-    if (!empty && ntz <= 64) {   // after the last batch's barrier: coverage rows complete
+    if (fcov && !empty && ntz <= 64) {   // after the last batch's barrier: rows complete
         const int x = x0 + (threadIdx.x & (TT - 1)), y = y0 + (threadIdx.x >> 4);
         if (x < w && y < h && ((s_rows[threadIdx.x >> 4] >> (threadIdx.x & (TT - 1))) & 1u))
             atomicOr(&fcov[(int64_t)y * w + x], 1ull << tzi);
@@ -656,7 +657,7 @@ __global__ void __launch_bounds__(256, 4) k_fvr_fwd(const GRec* __restrict__ rec
                                    : sacc[cid][ch ^ ((cid >> 1) & 3)];
             if (x < w && y < h)
                 *reinterpret_cast<float4*>(vol + ((int64_t)y * w + x) * c + z0 + 4 * ch) = v;
-            if (!empty && ntz <= 64) {   // column segment occupancy (4 lanes per column)
+            if (pocc && !empty && ntz <= 64) {   // column segment occupancy (4 lanes per column)
                 const bool nz = v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f;
                 const unsigned b = __ballot_sync(0xffffffffu, nz);
                 if (ch == 0 && ((b >> (lane & ~3)) & 0xfu) && x < w && y < h)
@@ -678,7 +679,7 @@ __global__ void __launch_bounds__(256, 4) k_fvr_fwd(const GRec* __restrict__ rec
                 if (z0 + 4 * q + 2 < c) { col[z0 + 4 * q + 2] = v.z; nz |= v.z != 0.f; }
                 if (z0 + 4 * q + 3 < c) { col[z0 + 4 * q + 3] = v.w; nz |= v.w != 0.f; }
             }
-            if (nz && ntz <= 64) atomicOr(&pocc[(int64_t)y * w + x], 1ull << tzi);
+            if (pocc && nz && ntz <= 64) atomicOr(&pocc[(int64_t)y * w + x], 1ull << tzi);
         }
     }
     }   // tile
@@ -1047,9 +1048,9 @@ int splatct_fvr_bin(const double* params, int64_t n, int w, int h, int c, int z0
     return SPLATCT_OK;
 }
 
-int splatct_fvr_forward(const double* params, int64_t n, int w, int h, int c, int z0, int hx,
-                        int hy, int hz, void* ws, size_t ws_bytes, float* vol_yxz,
-                        const int* halt, void* stream) {
+static int fvr_forward_impl(const double* params, int64_t n, int w, int h, int c, int z0, int hx,
+                            int hy, int hz, void* ws, size_t ws_bytes, float* vol_yxz,
+                            const int* halt, void* stream, bool masks) {
     FvrLayout L = make_layout(n, w, h, c, hx, hy, hz);
     if (int e = check_args(n, w, h, c, hx, hy, hz, ws_bytes, L)) return e;
     const size_t vo = L.final_buf ? L.o_v1 : L.o_v0;
@@ -1058,13 +1059,31 @@ int splatct_fvr_forward(const double* params, int64_t n, int w, int h, int c, in
     fetch = fetch < 1 ? 1 : (fetch > 32 ? 32 : fetch);
     unsigned int* counter = at<uint32_t>(ws, L.o_tcount);
     SPLATCT_CK(cudaMemsetAsync(counter, 0, sizeof(unsigned int), as_stream(stream)));
+    if (masks && L.ntz <= 64)
+        SPLATCT_CK(cudaMemsetAsync(at<char>(ws, L.o_pocc), 0,
+                                   L.o_fcov + sizeof(unsigned long long) * (size_t)w * h - L.o_pocc,
+                                   as_stream(stream)));
     SPLATCT_CK(launch_pdl(k_fvr_fwd, dim3((unsigned)grid), dim3(256), 0, as_stream(stream),
                           at<GRec>(ws, L.o_rec), w, h, c, z0, hx, hy, hz, L.ntx, L.nty, L.nt, L.Sl,
         at<uint32_t>(ws, L.o_tstart), at<uint32_t>(ws, vo), vol_yxz, counter, (int)fetch,
-        at<unsigned long long>(ws, L.o_pocc),
-        at<unsigned long long>(ws, L.o_fcov), halt));
+        masks ? at<unsigned long long>(ws, L.o_pocc) : nullptr,
+        masks ? at<unsigned long long>(ws, L.o_fcov) : nullptr, halt));
     SPLATCT_LAUNCH_CK();
     return SPLATCT_OK;
+}
+
+int splatct_fvr_forward(const double* params, int64_t n, int w, int h, int c, int z0, int hx,
+                        int hy, int hz, void* ws, size_t ws_bytes, float* vol_yxz,
+                        const int* halt, void* stream) {
+    return fvr_forward_impl(params, n, w, h, c, z0, hx, hy, hz, ws, ws_bytes, vol_yxz, halt,
+                            stream, false);
+}
+
+int splatct_fvr_forward_masked(const double* params, int64_t n, int w, int h, int c, int z0,
+                               int hx, int hy, int hz, void* ws, size_t ws_bytes, float* vol_yxz,
+                               const int* halt, void* stream) {
+    return fvr_forward_impl(params, n, w, h, c, z0, hx, hy, hz, ws, ws_bytes, vol_yxz, halt,
+                            stream, true);
 }
 
 int splatct_fvr_backward(const double* params, int64_t n, int w, int h, int c, int z0, int hx,

@@ -207,13 +207,19 @@ class FvrPlan:
     def _geo(self):
         return (self.n, self.w, self.h, self.c, self.z0, self.hx, self.hy, self.hz)
 
+    masks_valid = False
+
     def bin(self, params: torch.Tensor, halt=None) -> None:
         call("splatct_fvr_bin", ptr(params), *self._geo(), ptr(self.ws), self.ws_bytes,
              ptr(halt), stream_handle())
 
-    def forward(self, params: torch.Tensor, out: torch.Tensor, halt=None) -> torch.Tensor:
-        call("splatct_fvr_forward", ptr(params), *self._geo(), ptr(self.ws), self.ws_bytes,
-             ptr(out), ptr(halt), stream_handle())
+    def forward(self, params: torch.Tensor, out: torch.Tensor, halt=None,
+                masks: bool = False) -> torch.Tensor:
+        """masks: also record the empty-space masks (pixel_occupancy,
+        footprint_coverage) the training step's projector pair uses."""
+        call("splatct_fvr_forward_masked" if masks else "splatct_fvr_forward", ptr(params),
+             *self._geo(), ptr(self.ws), self.ws_bytes, ptr(out), ptr(halt), stream_handle())
+        self.masks_valid = masks   # the masks describe the volume of the last forward
         return out
 
     def backward(self, params, upstream, grads, accum=None, halt=None) -> torch.Tensor:
@@ -259,6 +265,8 @@ def _occ(occ, kind: str):
     pointer, or None."""
     if occ is None or isinstance(occ, VP):
         return occ
+    if not occ.masks_valid:   # the plan's last forward did not record masks: stay dense
+        return None
     return occ.pixel_occupancy if kind == "pixel" else occ.footprint_coverage
 
 

@@ -170,7 +170,7 @@ class Trainer:
     # -- iteration ----------------------------------------------------------
     def initial_volume(self):
         self.fvr.bin(self.params, self.halt)
-        self.fvr.forward(self.params, self.vol, self.halt)
+        self.fvr.forward(self.params, self.vol, self.halt, masks=True)
 
     def _stages(self):
         """The iteration as an ordered list of ("gpu" | "comm", fn) stages.
@@ -239,7 +239,7 @@ class Trainer:
             D.adam(self.params, self.grads, self.m1, self.m2, self.adam_s, SIGMA_FLOOR,
                    self.sigma_ceiling, halt)
             self.fvr.bin(self.params, halt)
-            self.fvr.forward(self.params, self.vol, halt)
+            self.fvr.forward(self.params, self.vol, halt, masks=True)   # + empty-space masks
         st.append(("gpu", update_resplat))
         return st
 

@@ -410,7 +410,7 @@ def test_projector_occupancy_skip_is_exact(dims, c_note):
     plan = D.FvrPlan(n, dims, box.half, 0, dev)
     params = D.cloud_to_params(cloud, dev)
     plan.bin(params)
-    vol = plan.forward(params, plan.new_volume())
+    vol = plan.forward(params, plan.new_volume(), masks=True)
     occ = plan.pixel_occupancy_words().cpu().numpy().view(np.uint64)
     assert 0 < int(sum(bin(int(v)).count("1") for v in occ)) < occ.size * ((c + 15) // 16)
     geom = core.ScanGeometry.fan(20, 90, 1.3, 120.0, 90.0)
