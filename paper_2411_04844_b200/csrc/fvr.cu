@@ -36,7 +36,7 @@ constexpr int SORT_IPT = 16;
 constexpr int SORT_CHUNK = SORT_NT * SORT_IPT;
 constexpr int RADIX = 256;
 constexpr int MAX_PASSES = 4;     // 8-bit digits of a 32-bit tile id
-constexpr int BIN_NT = 1024;      // Gaussians per block in the emit pass
+constexpr int BIN_NT = 256;       // Gaussians per block in the emit pass
 
 // Per-Gaussian record written by the footprint pass: integer floor (global
 // voxel coordinates), fractional offsets, 0.5/sigma^2 and intensity in f32,
