@@ -23,7 +23,11 @@
 //     straight from L2, separable moment contraction (x inner, y outer, z
 //     per lane), warp-shuffle reduction, f64 chain rule; no atomics, no
 //     partial buffers, deterministic.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstdlib>
+#include <cstring>
 #include <type_traits>
 
 #include "common.cuh"
@@ -497,11 +501,14 @@ __global__ void __launch_bounds__(256, 4) k_fvr_fwd(const GRec* __restrict__ rec
                                                  unsigned int* __restrict__ counter, int fetch,
                                                  unsigned long long* __restrict__ pocc,
                                                  unsigned long long* __restrict__ fcov,
-                                                 const int* halt) {
+                                                 const __grid_constant__ CUtensorMap tmap,
+                                                 int use_tma, const int* halt) {
     griddep_wait();
     if (halted(halt)) return;
     __shared__ __align__(16) float tab[FWD_BATCH * TAB_STRIDE];
-    __shared__ __align__(16) float4 sacc[TT * TT][TT / 4];   // [y*16+x][z/4], swizzled
+    // [y*16+x][z/4] with the 16-byte chunk XOR-swizzled by (row >> 1) & 3: exactly
+    // TMA's 64-byte swizzle, so the tile leaves through one bulk tensor store
+    __shared__ __align__(1024) float4 sacc[TT * TT][TT / 4];
     __shared__ int64_t s_next;
     __shared__ unsigned s_rows[TT];   // footprint coverage: x bits per tile row
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -528,6 +535,8 @@ __global__ void __launch_bounds__(256, 4) k_fvr_fwd(const GRec* __restrict__ rec
     const int x0 = txi * TT, y0 = tyi * TT, z0 = tzi * TT;
     const uint32_t beg = tstart[t], end = tstart[t + 1];
     const bool empty = beg == end;
+    if (use_tma && threadIdx.x == 0)   // sacc is rewritten after this tile's barriers
+        asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
     // (the previous tile's readers passed the barrier after their read)
     if (threadIdx.x < TT) s_rows[threadIdx.x] = 0u;
     float acc[4][4];
@@ -636,6 +645,7 @@ __global__ void __launch_bounds__(256, 4) k_fvr_fwd(const GRec* __restrict__ rec
                 *dst = make_float2(acc[j][2 * hx8], acc[j][2 * hx8 + 1]);
             }
         }
+        if (use_tma) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         __syncthreads();
     }
     if (fcov && !empty && ntz <= 64) {   // after the last batch's barrier: rows complete
@@ -644,10 +654,29 @@ __global__ void __launch_bounds__(256, 4) k_fvr_fwd(const GRec* __restrict__ rec
             atomicOr(&fcov[(int64_t)y * w + x], 1ull << tzi);
         __syncthreads();   // before the next tile zeroes the rows
     }
-    // store: the tile's 256 columns x 64 B are written 8 columns per warp
-    // instruction (4 lanes x 16 B per column) instead of 32 scattered
-    // half-sectors; empty tiles store zeros directly
-    if ((c & 3) == 0 && z0 + TT <= c) {
+    // store: non-empty tiles leave through one TMA bulk tensor store (the
+    // tensor map clips tiles at the volume edges); otherwise the tile's 256
+    // columns x 64 B are written 8 columns per warp instruction (4 lanes x
+    // 16 B per column); empty tiles store zeros directly
+    if (use_tma && !empty) {
+        if (threadIdx.x == 0) {
+            const unsigned sa = (unsigned)__cvta_generic_to_shared(&sacc[0][0]);
+            asm volatile(
+                "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n"
+                "cp.async.bulk.commit_group;\n" ::"l"(&tmap), "r"(z0), "r"(x0), "r"(y0), "r"(sa)
+                : "memory");
+        }
+        if (pocc && ntz <= 64) {   // column segment occupancy from the staged tile
+            const int x = x0 + (threadIdx.x & (TT - 1)), y = y0 + (threadIdx.x >> 4);
+            bool nz = false;
+#pragma unroll
+            for (int q = 0; q < TT / 4; ++q) {
+                const float4 v = sacc[threadIdx.x][q];
+                nz |= v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f;
+            }
+            if (nz && x < w && y < h) atomicOr(&pocc[(int64_t)y * w + x], 1ull << tzi);
+        }
+    } else if ((c & 3) == 0 && z0 + TT <= c) {
         const int ch = lane & 3;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -684,6 +713,7 @@ __global__ void __launch_bounds__(256, 4) k_fvr_fwd(const GRec* __restrict__ rec
     }
     }   // tile
     }   // fetch
+    if (use_tma && threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
 
 // tstart[t] = lower_bound(sorted keys, t) for t in [0, nt] from the key
@@ -1048,6 +1078,34 @@ int splatct_fvr_bin(const double* params, int64_t n, int w, int h, int c, int z0
     return SPLATCT_OK;
 }
 
+// TMA descriptor of the (h, w, c) volume for 16^3 boxes with the 64-byte
+// swizzle (false: no driver entry point or unsupported strides -- the kernel
+// then stores with plain vector stores)
+static bool volume_tensor_map(CUtensorMap* m, float* vol, int w, int h, int c) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    memset(m, 0, sizeof(*m));
+    if (!encode || (c & 3) != 0 || ((uintptr_t)vol & 15) != 0 || getenv("SPLATCT_NO_TMA"))
+        return false;
+    const cuuint64_t dim[3] = {(cuuint64_t)c, (cuuint64_t)w, (cuuint64_t)h};
+    const cuuint64_t stride[2] = {(cuuint64_t)c * 4, (cuuint64_t)c * w * 4};
+    const cuuint32_t box[3] = {TT, TT, TT};
+    const cuuint32_t estride[3] = {1, 1, 1};
+    return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, vol, dim, stride, box, estride,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                  CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+           CUDA_SUCCESS;
+}
+
 static int fvr_forward_impl(const double* params, int64_t n, int w, int h, int c, int z0, int hx,
                             int hy, int hz, void* ws, size_t ws_bytes, float* vol_yxz,
                             const int* halt, void* stream, bool masks) {
@@ -1063,11 +1121,13 @@ static int fvr_forward_impl(const double* params, int64_t n, int w, int h, int c
         SPLATCT_CK(cudaMemsetAsync(at<char>(ws, L.o_pocc), 0,
                                    L.o_fcov + sizeof(unsigned long long) * (size_t)w * h - L.o_pocc,
                                    as_stream(stream)));
+    CUtensorMap tmap;
+    const int use_tma = volume_tensor_map(&tmap, vol_yxz, w, h, c) ? 1 : 0;
     SPLATCT_CK(launch_pdl(k_fvr_fwd, dim3((unsigned)grid), dim3(256), 0, as_stream(stream),
                           at<GRec>(ws, L.o_rec), w, h, c, z0, hx, hy, hz, L.ntx, L.nty, L.nt, L.Sl,
         at<uint32_t>(ws, L.o_tstart), at<uint32_t>(ws, vo), vol_yxz, counter, (int)fetch,
         masks ? at<unsigned long long>(ws, L.o_pocc) : nullptr,
-        masks ? at<unsigned long long>(ws, L.o_fcov) : nullptr, halt));
+        masks ? at<unsigned long long>(ws, L.o_fcov) : nullptr, tmap, use_tma, halt));
     SPLATCT_LAUNCH_CK();
     return SPLATCT_OK;
 }
