@@ -854,6 +854,116 @@ __device__ __forceinline__ void bwd_moments17(const GRec& r, int xlo, int nx, in
     S2 = fmaf(ez16, fmaf(rz16 * rz16, Q0, Qr), S2);
 }
 
+// FAST-path moments with the upstream rows brought in by TMA: one lane
+// issues a {20 z, 17 x, 1 y} box load per row into a 4-slot per-warp ring
+// (completion on per-slot mbarriers, out-of-volume taps zero-filled), so three
+// rows are in flight ahead of the arithmetic at the cost of one instruction
+// per row.  Lanes then read their column-pair words from shared memory.
+constexpr int BT_RING = 4;
+constexpr int BT_ZB = 20;   // box z extent: 17 taps from a 16 B-aligned start (z0 & ~3)
+constexpr int BT_SLOT = 1408;                      // 17 x 20 x 4 B = 1360, rounded to 128 B
+constexpr unsigned BT_BYTES = 17u * BT_ZB * 4u;
+
+__device__ __forceinline__ void bwd_moments17_tma(const GRec& r, int xlo, int nx, int ylo, int ny,
+                                                  int zlo, int nz, int zoff,
+                                                  const CUtensorMap* tmap, float* ring,
+                                                  unsigned long long* bars, float& S0, float& Sx,
+                                                  float& Sy, float& Sz, float& S2) {
+    const int lane = threadIdx.x & 31, hf = lane >> 4, zl = lane & 15;
+    const bool zok = zl < nz;
+    const float rz = (float)(zlo + zl + zoff - r.fz) - r.dz;
+    const float ez = zok ? exp2f(-r.inv2 * rz * rz) : 0.f;
+    const bool has16 = nz > 16;
+    const float rz16 = (float)(zlo + 16 + zoff - r.fz) - r.dz;
+    const float ez16 = has16 ? exp2f(-r.inv2 * rz16 * rz16) : 0.f;
+    float2 wx01[9];
+    float wx2[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+        const int col = 2 * k + hf;
+        const float rx = (float)(xlo + col - r.fx) - r.dx;
+        const float ex = col < nx ? exp2f(-r.inv2 * rx * rx) : 0.f;
+        wx01[k] = make_float2(ex, ex * rx);
+        wx2[k] = ex * rx * rx;
+    }
+    const float rxp = (float)(xlo + lane - r.fx) - r.dx;
+    const float exp_ = (has16 && lane < nx) ? exp2f(-r.inv2 * rxp * rxp) : 0.f;
+    const float wp0 = exp_, wp1 = exp_ * rxp, wp2 = exp_ * rxp * rxp;
+    const unsigned ring_s = (unsigned)__cvta_generic_to_shared(ring);
+    const unsigned bar_s = (unsigned)__cvta_generic_to_shared(bars);
+    auto issue = [&](int yi) {   // lane 0
+        const int q = yi % BT_RING;
+        const unsigned b = bar_s + 8 * q, dst = ring_s + BT_SLOT * q;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(b),
+                     "r"(BT_BYTES)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
+            "[%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(dst),
+            "l"(tmap), "r"(zlo & ~3), "r"(xlo), "r"(ylo + yi), "r"(b)
+            : "memory");
+    };
+    if (lane == 0)
+        for (int q = 0; q < BT_RING - 1 && q < ny; ++q) issue(q);
+    float A0 = 0.f, Ax = 0.f, Ay = 0.f, Ar = 0.f;
+    float Q0 = 0.f, Qx = 0.f, Qy = 0.f, Qr = 0.f;
+    for (int yi = 0; yi < ny; ++yi) {
+        __syncwarp();   // every lane is done with the slot refilled next (row yi - 1)
+        if (lane == 0 && yi + BT_RING - 1 < ny) issue(yi + BT_RING - 1);
+        const int q = yi % BT_RING;
+        const unsigned parity = (unsigned)(yi / BT_RING) & 1u;
+        {   // wait for row yi
+            unsigned done = 0;
+            do {
+                asm volatile(
+                    "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                    " selp.u32 %0, 1, 0, p;\n}\n"
+                    : "=r"(done)
+                    : "r"(bar_s + 8 * q), "r"(parity)
+                    : "memory");
+            } while (!done);
+        }
+        const float* src = ring + (BT_SLOT / 4) * q + (zlo & 3);
+        const float ry = (float)(ylo + yi - r.fy) - r.dy;
+        const float ey = exp2f(-r.inv2 * ry * ry);
+        float2 C01 = make_float2(0.f, 0.f);
+        float C2 = 0.f;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) {
+            // column 17 (k = 8, upper half-warp) lies past the box: never read it
+            const float u = (zok && (k < 8 || !hf)) ? src[(2 * k + hf) * BT_ZB + zl] : 0.f;
+            C01 = ffma2(make_float2(u, u), wx01[k], C01);
+            C2 = fmaf(wx2[k], u, C2);
+        }
+        const float pu = (has16 && lane < 17) ? src[lane * BT_ZB + 16] : 0.f;
+        const float C0 = C01.x, C1 = C01.y;
+        const float eyry = ey * ry, eyry2 = eyry * ry;
+        A0 = fmaf(ey, C0, A0);
+        Ax = fmaf(ey, C1, Ax);
+        Ay = fmaf(eyry, C0, Ay);
+        Ar = fmaf(ey, C2, fmaf(eyry2, C0, Ar));
+        Q0 = fmaf(ey * wp0, pu, Q0);
+        Qx = fmaf(ey * wp1, pu, Qx);
+        Qy = fmaf(eyry * wp0, pu, Qy);
+        Qr = fmaf(fmaf(ey, wp2, eyry2 * wp0), pu, Qr);
+    }
+    A0 += __shfl_xor_sync(0xffffffffu, A0, 16);
+    Ax += __shfl_xor_sync(0xffffffffu, Ax, 16);
+    Ay += __shfl_xor_sync(0xffffffffu, Ay, 16);
+    Ar += __shfl_xor_sync(0xffffffffu, Ar, 16);
+    const float eh = hf ? 0.f : ez;
+    S0 = eh * A0;
+    Sx = eh * Ax;
+    Sy = eh * Ay;
+    Sz = eh * rz * A0;
+    S2 = eh * fmaf(rz * rz, A0, Ar);
+    S0 = fmaf(ez16, Q0, S0);
+    Sx = fmaf(ez16, Qx, Sx);
+    Sy = fmaf(ez16, Qy, Sy);
+    Sz = fmaf(ez16 * rz16, Q0, Sz);
+    S2 = fmaf(ez16, fmaf(rz16 * rz16, Q0, Qr), S2);
+}
+
 // flags[j] = 1 for the sorted pair that is its Gaussian's first tile (slot 0)
 __global__ void k_first_flags(const uint32_t* __restrict__ svals, const uint32_t* __restrict__ tstart,
                               int64_t nt, int64_t np, int S, uint32_t* __restrict__ flags) {
@@ -885,12 +995,23 @@ __global__ void __launch_bounds__(32 * BG_WARPS, FAST ? 6 : 4) k_fvr_bwd(const d
                                                           const float* __restrict__ up,
                                                           double* __restrict__ G,
                                                           double* __restrict__ accum,
-                                                          const int* halt) {
+                                                          const __grid_constant__ CUtensorMap utmap,
+                                                          int use_tma, const int* halt) {
     griddep_wait();
     if (halted(halt)) return;
+    __shared__ __align__(128) float bring[FAST ? BG_WARPS : 1][FAST ? BT_RING * BT_SLOT / 4 : 1];
+    __shared__ __align__(8) unsigned long long bbar[BG_WARPS][BT_RING];
     __shared__ float xt[3][BG_WARPS][32];   // ex, ex rx, ex rx^2
     __shared__ float2 yt[BG_WARPS][32];   // {ey, ry}
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (FAST && use_tma) {   // every ring barrier initialised once, before any copy in the CTA
+        if (threadIdx.x < BG_WARPS * BT_RING) {
+            const unsigned b = (unsigned)__cvta_generic_to_shared(&bbar[0][0]) + 8 * threadIdx.x;
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(b));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        __syncthreads();
+    }
     const int64_t gw = blockIdx.x * (int64_t)BG_WARPS + wid;
     if (gw >= (ORD ? (int64_t)order[0] : n)) return;   // warp-uniform: warp-level syncs only
     const int64_t i = ORD ? (int64_t)order[1 + gw] : gw;
@@ -900,8 +1021,13 @@ __global__ void __launch_bounds__(32 * BG_WARPS, FAST ? 6 : 4) k_fvr_bwd(const d
     if (FAST || (xlo <= xhi && ylo <= yhi && zlo <= zhi && xhi - xlo < 17 && zhi - zlo < 17)) {
         if (xlo <= xhi && ylo <= yhi && zlo <= zhi) {
             const GRec r = rec[i];
-            bwd_moments17<!FAST>(r, xlo, xhi - xlo + 1, ylo, yhi - ylo + 1, zlo, zhi - zlo + 1, w,
-                                 c, zoff, up, S0, Sx, Sy, Sz, S2);
+            if (FAST && use_tma)
+                bwd_moments17_tma(r, xlo, xhi - xlo + 1, ylo, yhi - ylo + 1, zlo, zhi - zlo + 1,
+                                  zoff, &utmap, bring[FAST ? wid : 0], bbar[wid], S0, Sx, Sy, Sz,
+                                  S2);
+            else
+                bwd_moments17<!FAST>(r, xlo, xhi - xlo + 1, ylo, yhi - ylo + 1, zlo,
+                                     zhi - zlo + 1, w, c, zoff, up, S0, Sx, Sy, Sz, S2);
         }
     } else if (xlo <= xhi && ylo <= yhi && zlo <= zhi) {
         const GRec r = rec[i];
@@ -1081,7 +1207,8 @@ int splatct_fvr_bin(const double* params, int64_t n, int w, int h, int c, int z0
 // TMA descriptor of the (h, w, c) volume for 16^3 boxes with the 64-byte
 // swizzle (false: no driver entry point or unsupported strides -- the kernel
 // then stores with plain vector stores)
-static bool volume_tensor_map(CUtensorMap* m, float* vol, int w, int h, int c) {
+static bool volume_tensor_map(CUtensorMap* m, const float* vol, int w, int h, int c,
+                              int bz = 16, int bx = 16, int by = 16, bool swizzle = true) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     static bool tried = false;
     if (!tried) {
@@ -1098,10 +1225,11 @@ static bool volume_tensor_map(CUtensorMap* m, float* vol, int w, int h, int c) {
         return false;
     const cuuint64_t dim[3] = {(cuuint64_t)c, (cuuint64_t)w, (cuuint64_t)h};
     const cuuint64_t stride[2] = {(cuuint64_t)c * 4, (cuuint64_t)c * w * 4};
-    const cuuint32_t box[3] = {TT, TT, TT};
+    const cuuint32_t box[3] = {(cuuint32_t)bz, (cuuint32_t)bx, (cuuint32_t)by};
     const cuuint32_t estride[3] = {1, 1, 1};
-    return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, vol, dim, stride, box, estride,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+    return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(vol), dim, stride,
+                  box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  swizzle ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE,
                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
            CUDA_SUCCESS;
 }
@@ -1174,12 +1302,18 @@ int splatct_fvr_backward(const double* params, int64_t n, int w, int h, int c, i
         SPLATCT_CK(cudaMemsetAsync(grads, 0, sizeof(double) * 5 * (size_t)n, s));   // unlisted
     }
     const bool fast = 2 * hx + 1 <= 17 && 2 * hz + 1 <= 17;
+    CUtensorMap utmap;
+    int use_tma = 0;
+    if (fast && !getenv("SPLATCT_BWD_NO_TMA"))
+        use_tma = volume_tensor_map(&utmap, up_yxz, w, h, c, BT_ZB, 17, 1, false) ? 1 : 0;
+    else
+        memset(&utmap, 0, sizeof(utmap));
     auto launch = [&](auto fast_c, auto ord_c) {
         return launch_pdl(k_fvr_bwd<decltype(fast_c)::value, decltype(ord_c)::value>,
                           dim3(grid), dim3(32 * BG_WARPS), 0, s, params, n,
                           (const uint32_t*)order, (const int32_t*)at<int32_t>(ws, L.o_fp),
                           (const GRec*)at<GRec>(ws, L.o_rec), w, h, c, z0, up_yxz, grads, accum,
-                          halt);
+                          utmap, use_tma, halt);
     };
     using T = std::true_type;
     using F = std::false_type;

@@ -1,0 +1,22 @@
+# TMA-fed backward experiment: parity with TMA on (default), then sweeps on/off
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -q --timeout 600 -p no:cacheprovider -k "fvr or spec or edges or parity or fullsize or trainer" > gpurun_out/pytest_tma.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_tma.log
+tail -3 gpurun_out/pytest_tma.log
+for o in 0 1; do
+  if [ $o = 1 ]; then export SPLATCT_BWD_NO_TMA=1; fi
+  timeout 600 python tools/voxel_sweep.py --grids 256,512,1024 --ns 400000,2000000 > gpurun_out/sweep_tma$o.jsonl 2>&1
+  timeout 600 python bench.py --steps 30 --warmup 5 --no-cpu-baseline > gpurun_out/bench_tma$o.log 2>&1
+done
+python - <<'PY'
+import json
+for o in (0,1):
+    print("NO_TMA",o)
+    for l in open(f"gpurun_out/sweep_tma{o}.jsonl"):
+        try: d=json.loads(l)
+        except Exception: continue
+        print({k:d[k] for k in d if k in ("grid","n","fwd_ms","bwd_ms")})
+    for l in open(f"gpurun_out/bench_tma{o}.log"):
+        try: d=json.loads(l); print("bench", d["value"], d["stages_ms"])
+        except Exception: pass
+PY
