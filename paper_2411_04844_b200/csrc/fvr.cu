@@ -864,6 +864,12 @@ constexpr int BT_ZB = 20;   // box z extent: 17 taps from a 16 B-aligned start (
 constexpr int BT_SLOT = 1408;                      // 17 x 20 x 4 B = 1360, rounded to 128 B
 constexpr unsigned BT_BYTES = 17u * BT_ZB * 4u;
 
+// Column of step k for half-warp hf: {0-3, 8-11, 16} and {4-7, 12-15}.  The
+// half-warps then sit 4 columns = 80 words apart (= 16 banks), so a step's 32
+// shared-memory reads hit 32 distinct banks (adjacent columns, 20 words apart,
+// would overlap by 4 banks).
+__device__ __forceinline__ int tcol(int k, int hf) { return 8 * (k >> 2) + (k & 3) + 4 * hf; }
+
 __device__ __forceinline__ void bwd_moments17_tma(const GRec& r, int xlo, int nx, int ylo, int ny,
                                                   int zlo, int nz, int zoff,
                                                   const CUtensorMap* tmap, float* ring,
@@ -880,7 +886,7 @@ __device__ __forceinline__ void bwd_moments17_tma(const GRec& r, int xlo, int nx
     float wx2[9];
 #pragma unroll
     for (int k = 0; k < 9; ++k) {
-        const int col = 2 * k + hf;
+        const int col = tcol(k, hf);
         const float rx = (float)(xlo + col - r.fx) - r.dx;
         const float ex = col < nx ? exp2f(-r.inv2 * rx * rx) : 0.f;
         wx01[k] = make_float2(ex, ex * rx);
@@ -930,8 +936,8 @@ __device__ __forceinline__ void bwd_moments17_tma(const GRec& r, int xlo, int nx
         float C2 = 0.f;
 #pragma unroll
         for (int k = 0; k < 9; ++k) {
-            // column 17 (k = 8, upper half-warp) lies past the box: never read it
-            const float u = (zok && (k < 8 || !hf)) ? src[(2 * k + hf) * BT_ZB + zl] : 0.f;
+            // column 20 (k = 8, upper half-warp) lies past the box: never read it
+            const float u = (zok && (k < 8 || !hf)) ? src[tcol(k, hf) * BT_ZB + zl] : 0.f;
             C01 = ffma2(make_float2(u, u), wx01[k], C01);
             C2 = fmaf(wx2[k], u, C2);
         }
