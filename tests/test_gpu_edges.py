@@ -53,7 +53,8 @@ def test_centres_outside_and_clipped_boxes():
     _check(mu, rng.uniform(0.5, 3.0, n), rng.uniform(0, 1, n), box, dims)
 
 
-@pytest.mark.parametrize("dims", [(20, 9, 5), (37, 23, 19), (16, 16, 1), (3, 50, 7)])
+@pytest.mark.parametrize("dims", [(20, 9, 5), (37, 23, 19), (16, 16, 1), (3, 50, 7),
+                                  (6, 5, 8), (9, 20, 4)])
 def test_flat_and_ragged_dims(dims):
     """Per-axis box clamping (BoxConfig.for_dims) and non-tile-multiple dims."""
     rng = np.random.default_rng(2)
@@ -128,3 +129,22 @@ def test_deep_volume_has_no_occupancy_mask():
     tr.step()
     tr.step()
     assert np.all(np.isfinite(tr.trace_rows()[:, 0]))
+
+
+@pytest.mark.parametrize("dims", [(40, 36, 32), (6, 5, 8)])
+def test_backward_tma_rows_match_direct_loads(dims, monkeypatch):
+    """The TMA-fed backward (c % 4 == 0; boxes larger than tiny volumes are
+    zero-filled by the tensor map) against the direct-load path, which sums the
+    same terms in another column order."""
+    rng = np.random.default_rng(9)
+    box = core.BoxConfig.for_dims(17, dims)
+    n = 1500
+    mu = np.stack([rng.uniform(-3, d + 3, n) for d in dims], 1)
+    cloud = core.GaussianCloud(mu, rng.uniform(0.5, 2.5, n), rng.uniform(0, 1, n))
+    up = core.VolumeGrid.from_zyx(rng.standard_normal(dims[::-1]).astype(np.float32))
+    a = fvr.backward(cloud, box, dims, up)
+    monkeypatch.setenv("SPLATCT_BWD_NO_TMA", "1")
+    b = fvr.backward(cloud, box, dims, up)
+    for x, y in ((a.d_mu, b.d_mu), (a.d_sigma, b.d_sigma), (a.d_intensity, b.d_intensity),
+                 (a.accum_pos_grad_norm, b.accum_pos_grad_norm)):
+        assert rel_l2(x, y) < 1e-6
