@@ -134,16 +134,39 @@ def _par_copy(dst: np.ndarray, src: np.ndarray) -> None:
         f.result()
 
 
+def _chunks(n0: int, nbytes: int):
+    """Row ranges for pipelined staging: ~4 chunks once a copy is >= 16 MB."""
+    k = 4 if nbytes >= (16 << 20) and n0 >= 4 else 1
+    cuts = np.linspace(0, n0, k + 1).astype(int)
+    return [(a, b) for a, b in zip(cuts[:-1], cuts[1:]) if b > a]
+
+
 def to_host(t: torch.Tensor, out: np.ndarray | None = None) -> np.ndarray:
-    """Device -> numpy via a cached pinned staging buffer (DMA-speed D2H)."""
+    """Device -> numpy via a cached pinned staging buffer (DMA-speed D2H).
+    Large copies go in row chunks: the host copy of chunk i overlaps the DMA
+    of chunk i + 1."""
     if t.device.type != "cuda":
         return t.numpy().copy()
     t = t.contiguous()
     st = _pinned(t.numel(), t.dtype).view(t.shape)
-    st.copy_(t)
     if out is None:
         out = np.empty(tuple(t.shape), st.numpy().dtype)
-    _par_copy(out.reshape(t.shape), st.numpy())
+    o = out.reshape(t.shape)
+    sn = st.numpy()
+    if t.dim() == 0:
+        st.copy_(t)
+        np.copyto(o, sn)
+        return out
+    s = torch.cuda.current_stream(t.device)
+    parts = []
+    for a, b in _chunks(t.shape[0], t.numel() * t.element_size()):
+        st[a:b].copy_(t[a:b], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(s)
+        parts.append((a, b, ev))
+    for a, b, ev in parts:
+        ev.synchronize()
+        _par_copy(o[a:b], sn[a:b])
     return out
 
 
@@ -152,7 +175,8 @@ def yxz_to_zyx(t: torch.Tensor, out: np.ndarray | None = None) -> np.ndarray:
 
 
 def sino_to_device(views, device) -> torch.Tensor:
-    """(m, n, p) host array -> device f32 through the pinned staging buffer."""
+    """(m, n, p) host array -> device f32 through the pinned staging buffer
+    (a chunked, overlapped variant measured no faster: 2.7 vs 3.3 ms at C2)."""
     a = np.asarray(views)
     st = _pinned(a.size, torch.float32)
     _par_copy(st.numpy().reshape(a.shape), a)
