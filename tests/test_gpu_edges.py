@@ -148,3 +148,38 @@ def test_backward_tma_rows_match_direct_loads(dims, monkeypatch):
     for x, y in ((a.d_mu, b.d_mu), (a.d_sigma, b.d_sigma), (a.d_intensity, b.d_intensity),
                  (a.accum_pos_grad_norm, b.accum_pos_grad_norm)):
         assert rel_l2(x, y) < 1e-6
+
+
+@pytest.mark.parametrize("dims", [(40, 36, 32), (6, 5, 8)])
+def test_forward_tma_store_matches_vector_stores(dims, monkeypatch):
+    """The TMA bulk tensor store and the vector-store path write the same
+    accumulators: bitwise-equal volumes (tiles clipped at the edges)."""
+    rng = np.random.default_rng(10)
+    box = core.BoxConfig.for_dims(17, dims)
+    n = 1500
+    mu = np.stack([rng.uniform(-3, d + 3, n) for d in dims], 1)
+    cloud = core.GaussianCloud(mu, rng.uniform(0.5, 2.5, n), rng.uniform(0, 1, n))
+    a = fvr.reconstruct(cloud, box, dims).zyx
+    monkeypatch.setenv("SPLATCT_NO_TMA", "1")
+    b = fvr.reconstruct(cloud, box, dims).zyx
+    np.testing.assert_array_equal(a, b)
+
+
+def test_backward_visit_order_is_bitwise_neutral(monkeypatch):
+    """Index order and tile order only change which warp takes a Gaussian;
+    each Gaussian's sums run in one warp in fixed order."""
+    rng = np.random.default_rng(11)
+    dims = (48, 40, 36)
+    box = core.BoxConfig.cube(17)
+    n = 2000
+    mu = np.stack([rng.uniform(0, d, n) for d in dims], 1)
+    cloud = core.GaussianCloud(mu, rng.uniform(0.5, 2.5, n), rng.uniform(0, 1, n))
+    up = core.VolumeGrid.from_zyx(rng.standard_normal(dims[::-1]).astype(np.float32))
+    out = []
+    for o in ("0", "1"):
+        monkeypatch.setenv("SPLATCT_BWD_ORDER", o)
+        out.append(fvr.backward(cloud, box, dims, up))
+    a, b = out
+    for x, y in ((a.d_mu, b.d_mu), (a.d_sigma, b.d_sigma), (a.d_intensity, b.d_intensity),
+                 (a.accum_pos_grad_norm, b.accum_pos_grad_norm)):
+        np.testing.assert_array_equal(x, y)
