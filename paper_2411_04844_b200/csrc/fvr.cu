@@ -716,6 +716,183 @@ __global__ void __launch_bounds__(256, 4) k_fvr_fwd(const GRec* __restrict__ rec
     if (use_tma && threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
 
+// --------------------------------------------------------------------------
+// forward on the FP32 pipe: register-blocked FFMA2 with the work cut to the
+// footprints at warp granularity.
+//
+// One 64-thread CTA per 16^3 tile (persistent, tiles claimed from a counter).
+// A thread owns two adjacent columns (x, x+1) of two adjacent rows (y, y+1),
+// 16 slices each: 32 float2 accumulators {V[y][x][z], V[y][x+1][z]}.  A warp
+// owns 8 rows x 16 columns x 16 slices.  Per 32-Gaussian batch of the tile
+// list (ascending id: deterministic sums) the table builders write, per
+// Gaussian, ex (column pairs), I ey, ez (zero outside box, tile and volume)
+// and the integer footprint inside the tile (rows, columns, z halves); each
+// warp then ballots the Gaussians whose rows meet its 8 rows and walks only
+// those.  The z overlap of a box with a 16-slice tile is a prefix, a suffix or
+// both halves, so only covered half-tiles are summed (uniform branch).  Per
+// Gaussian and lane: w = (I ey[y], I ey[y+1]) x {ex[x], ex[x+1]} (two FMUL2),
+// then acc[r][z] += w[r] * ez[z] (one FFMA2 per row and slice).  Columns leave
+// as 64-byte float4 runs straight from registers.
+// --------------------------------------------------------------------------
+constexpr int FF_THREADS = 64;
+constexpr int FF_BATCH = 32;
+
+struct __align__(16) FTab {
+    float ez[16];     // z weights (zero outside box, tile, volume)
+    float2 ex[8];     // x weights, column pairs
+    float2 ey[8];     // I * y weights, row pairs
+    int ym;           // rows covered (bits 0..15) | z halves (bit 16: low, bit 17: high)
+    int xm;           // columns covered by the footprint (coverage mask)
+    int pad[2];
+};
+
+template <bool MASKS>
+__global__ void __launch_bounds__(FF_THREADS, 8)
+    k_fvr_fwd_ff(const GRec* __restrict__ rec, int w, int h, int c, int zoff, int hx, int hy,
+                 int hz, int ntx, int nty, int64_t nt, int S,
+                 const uint32_t* __restrict__ tstart, const uint32_t* __restrict__ svals,
+                 float* __restrict__ vol, unsigned int* __restrict__ counter, int fetch,
+                 unsigned long long* __restrict__ pocc, unsigned long long* __restrict__ fcov,
+                 const int* halt) {
+    griddep_wait();
+    if (halted(halt)) return;
+    __shared__ FTab tab[FF_BATCH];
+    __shared__ int64_t s_next;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int xp = lane & 7;                   // column pair
+    const int rp = wid * 4 + (lane >> 3);      // row pair: rows 2 rp, 2 rp + 1
+    const int ntz = (int)(nt / ((int64_t)ntx * nty));
+    const int tg = threadIdx.x >> 1, th = threadIdx.x & 1;   // table builder: Gaussian, half
+    for (;;) {
+        __syncthreads();
+        if (threadIdx.x == 0) s_next = (int64_t)atomicAdd(counter, (unsigned)fetch);
+        __syncthreads();
+        const int64_t kc = s_next;
+        if (kc >= nt) break;
+        const int kend = (int)min(kc + fetch, nt);
+        for (int k32 = (int)kc; k32 < kend; ++k32) {
+            const int tzi = k32 % ntz;
+            const int rest = k32 / ntz;
+            const int txi = rest % ntx, tyi = rest / ntx;
+            const int64_t t = ((int64_t)tzi * nty + tyi) * ntx + txi;
+            const int x0 = txi * TT, y0 = tyi * TT, z0 = tzi * TT;
+            const uint32_t beg = tstart[t], end = tstart[t + 1];
+            float2 acc0[16], acc1[16];
+#pragma unroll
+            for (int z = 0; z < 16; ++z) acc0[z] = acc1[z] = make_float2(0.f, 0.f);
+            unsigned cov0 = 0u, cov1 = 0u;
+            GRec rn;
+            if (beg + tg < end) rn = rec[svals[beg + tg] >> S];
+            for (uint32_t b0 = beg; b0 < end; b0 += FF_BATCH) {
+                const int nb = (int)min((uint32_t)FF_BATCH, end - b0);
+                const GRec r = rn;
+                if (b0 + FF_BATCH + tg < end) rn = rec[svals[b0 + FF_BATCH + tg] >> S];
+                __syncthreads();   // the previous batch's table reads are done
+                if (tg < nb) {     // half th: entries 8 th .. 8 th + 7 of ex, ey, ez
+                    FTab& T = tab[tg];
+                    float vx[8], vy[8], vz[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const int l = 8 * th + q;
+                        vx[q] = tab_weight(x0 + l, 0, w, r.fx, hx, r.dx, r.inv2);
+                        vy[q] = tab_weight(y0 + l, 0, h, r.fy, hy, r.dy, r.inv2) * r.I;
+                        vz[q] = tab_weight(z0 + l, zoff, c, r.fz, hz, r.dz, r.inv2);
+                    }
+                    float4* ex4 = reinterpret_cast<float4*>(T.ex) + 2 * th;
+                    float4* ey4 = reinterpret_cast<float4*>(T.ey) + 2 * th;
+                    float4* ez4 = reinterpret_cast<float4*>(T.ez) + 2 * th;
+                    ex4[0] = make_float4(vx[0], vx[1], vx[2], vx[3]);
+                    ex4[1] = make_float4(vx[4], vx[5], vx[6], vx[7]);
+                    ey4[0] = make_float4(vy[0], vy[1], vy[2], vy[3]);
+                    ey4[1] = make_float4(vy[4], vy[5], vy[6], vy[7]);
+                    ez4[0] = make_float4(vz[0], vz[1], vz[2], vz[3]);
+                    ez4[1] = make_float4(vz[4], vz[5], vz[6], vz[7]);
+                    if (th == 0) {   // integer footprint inside the tile (a3): rows, columns, z halves
+                        const int by0 = max(r.fy - hy, y0), by1 = min(min(r.fy + hy, h - 1), y0 + TT - 1);
+                        const int bx0 = max(r.fx - hx, x0), bx1 = min(min(r.fx + hx, w - 1), x0 + TT - 1);
+                        const int bz0 = max(r.fz - zoff - hz, z0);
+                        const int bz1 = min(min(r.fz - zoff + hz, c - 1), z0 + TT - 1);
+                        int ym = 0, xm = 0;
+                        if (by0 <= by1 && bx0 <= bx1 && bz0 <= bz1) {
+                            ym = (int)(((2u << (by1 - y0)) - 1u) & ~((1u << (by0 - y0)) - 1u));
+                            xm = (int)(((2u << (bx1 - x0)) - 1u) & ~((1u << (bx0 - x0)) - 1u));
+                            if (bz0 - z0 < 8) ym |= 1 << 16;
+                            if (bz1 - z0 >= 8) ym |= 1 << 17;
+                        }
+                        T.ym = ym;
+                        T.xm = xm;
+                    }
+                }
+                __syncthreads();
+                // the Gaussians whose rows meet this warp's 8 rows
+                unsigned todo = __ballot_sync(
+                    0xffffffffu, lane < nb && ((tab[lane].ym >> (8 * wid)) & 0xFF) != 0);
+                while (todo) {
+                    const int kb = __ffs(todo) - 1;
+                    todo &= todo - 1u;
+                    const FTab& T = tab[kb];
+                    const int2 m = *reinterpret_cast<const int2*>(&T.ym);
+                    const float2 e = T.ex[xp];
+                    const float2 wy = T.ey[rp];
+                    const float4* ez4 = reinterpret_cast<const float4*>(T.ez);
+                    const float4 za = ez4[0], zb = ez4[1], zc = ez4[2], zd = ez4[3];
+                    const float2 wa = make_float2(e.x * wy.x, e.y * wy.x);
+                    const float2 wb = make_float2(e.x * wy.y, e.y * wy.y);
+                    if (MASKS) {
+                        if ((m.x >> (2 * rp)) & 1) cov0 |= (unsigned)m.y;
+                        if ((m.x >> (2 * rp + 1)) & 1) cov1 |= (unsigned)m.y;
+                    }
+#define FF_Q(Z, V, K)                                                        \
+    acc0[K] = ffma2(make_float2(V, V), wa, acc0[K]);                         \
+    acc1[K] = ffma2(make_float2(V, V), wb, acc1[K]);
+                    if (m.x & (1 << 16)) {
+                        FF_Q(0, za.x, 0) FF_Q(0, za.y, 1) FF_Q(0, za.z, 2) FF_Q(0, za.w, 3)
+                        FF_Q(0, zb.x, 4) FF_Q(0, zb.y, 5) FF_Q(0, zb.z, 6) FF_Q(0, zb.w, 7)
+                    }
+                    if (m.x & (1 << 17)) {
+                        FF_Q(0, zc.x, 8) FF_Q(0, zc.y, 9) FF_Q(0, zc.z, 10) FF_Q(0, zc.w, 11)
+                        FF_Q(0, zd.x, 12) FF_Q(0, zd.y, 13) FF_Q(0, zd.z, 14) FF_Q(0, zd.w, 15)
+                    }
+#undef FF_Q
+                }
+            }
+            // store: each column's 16 slices are one 64-byte run
+#pragma unroll
+            for (int rr = 0; rr < 2; ++rr) {
+                const int y = y0 + 2 * rp + rr;
+#pragma unroll
+                for (int hc = 0; hc < 2; ++hc) {
+                    const int x = x0 + 2 * xp + hc;
+                    if (x >= w || y >= h) continue;
+                    float v[16];
+#pragma unroll
+                    for (int z = 0; z < 16; ++z)
+                        v[z] = rr ? (hc ? acc1[z].y : acc1[z].x) : (hc ? acc0[z].y : acc0[z].x);
+                    float* col = vol + ((int64_t)y * w + x) * c + z0;
+                    if ((c & 3) == 0 && z0 + TT <= c) {
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            reinterpret_cast<float4*>(col)[q] =
+                                make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                    } else {
+#pragma unroll
+                        for (int z = 0; z < 16; ++z)
+                            if (z0 + z < c) col[z] = v[z];
+                    }
+                    if (MASKS && ntz <= 64) {
+                        bool nz = false;
+#pragma unroll
+                        for (int z = 0; z < 16; ++z) nz |= v[z] != 0.f;
+                        if (nz) atomicOr(&pocc[(int64_t)y * w + x], 1ull << tzi);
+                        if ((((rr ? cov1 : cov0) >> (2 * xp + hc)) & 1u))
+                            atomicOr(&fcov[(int64_t)y * w + x], 1ull << tzi);
+                    }
+                }
+            }
+        }
+    }
+}
+
 // tstart[t] = lower_bound(sorted keys, t) for t in [0, nt] from the key
 // boundaries: sorted position j starts every tile in (key[j-1], key[j]], and
 // tstart[nt] = number of pairs (read on the device: the bins are dense).
@@ -937,11 +1114,14 @@ __device__ __forceinline__ void bwd_moments17_tma(const GRec& r, int xlo, int nx
 #pragma unroll
         for (int k = 0; k < 9; ++k) {
             // column 20 (k = 8, upper half-warp) lies past the box: never read it
-            const float u = (zok && (k < 8 || !hf)) ? src[tcol(k, hf) * BT_ZB + zl] : 0.f;
+            // columns past the footprint (nx < 17) are never read either: the masked
+            // adjoint leaves upstream outside every footprint unwritten (0 x NaN = NaN)
+            const float u = (zok && (k < 8 || !hf) && tcol(k, hf) < nx)
+                                ? src[tcol(k, hf) * BT_ZB + zl] : 0.f;
             C01 = ffma2(make_float2(u, u), wx01[k], C01);
             C2 = fmaf(wx2[k], u, C2);
         }
-        const float pu = (has16 && lane < 17) ? src[lane * BT_ZB + 16] : 0.f;
+        const float pu = (has16 && lane < nx) ? src[lane * BT_ZB + 16] : 0.f;
         const float C0 = C01.x, C1 = C01.y;
         const float eyry = ey * ry, eyry2 = eyry * ry;
         A0 = fmaf(ey, C0, A0);
@@ -1130,6 +1310,171 @@ __global__ void __launch_bounds__(32 * BG_WARPS, FAST ? 6 : 4) k_fvr_bwd(const d
     }
 }
 
+// --------------------------------------------------------------------------
+// backward, spatially ordered (the default for boxes <= 17^3): persistent
+// CTAs walk the tile-sorted (tile, Gaussian) pairs and take each Gaussian at
+// its first tile (slot 0), so every CTA sweeps one contiguous run of tiles and
+// the Gaussians resident on an SM at any moment are neighbours -- their boxes
+// overlap, and the upstream rows they read are L1 hits instead of one private
+// L2 stream per Gaussian (the TMA row ring read 1.2 GB from L2 per C2 launch).
+// A full 17^3 box (every interior Gaussian) runs a branch-free row loop with
+// compile-time column offsets: 9 column-pair loads + 1 seventeenth-slice load,
+// 9 FFMA2 + 9 FFMA and 7 row FMAs per row, the row weights {ey, ey ry, ey ry^2}
+// from a per-warp table.  Footprints clipped by the volume take the clamped
+// general path (bwd_moments17).  Moments, reduction and f64 chain rule as in
+// k_fvr_bwd; each Gaussian is summed by one warp in a fixed order
+// (deterministic, independent of which warp takes it).
+// --------------------------------------------------------------------------
+constexpr int BS_WARPS = 16;
+
+template <int C>   // compile-time volume depth (0: runtime c)
+__device__ __forceinline__ void bwd_moments17_full(const GRec& r, int xlo, int ylo, int zlo,
+                                                   int w, int c_rt, int zoff,
+                                                   const float* __restrict__ up,
+                                                   const float4* ytab, float& S0, float& Sx,
+                                                   float& Sy, float& Sz, float& S2) {
+    const int cc = C ? C : c_rt;
+    const int lane = threadIdx.x & 31, hf = lane >> 4, zl = lane & 15;
+    const float rz = (float)(zlo + zl + zoff - r.fz) - r.dz;
+    const float ez = exp2f(-r.inv2 * rz * rz);
+    const float rz16 = (float)(zlo + 16 + zoff - r.fz) - r.dz;
+    const float ez16 = exp2f(-r.inv2 * rz16 * rz16);
+    float2 wx01[9];
+    float wx2[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {   // column 2k + hf; column 17 (k = 8, hf = 1) is not in the box
+        const float rx = (float)(xlo + 2 * k + hf - r.fx) - r.dx;
+        const float ex = (k < 8 || !hf) ? exp2f(-r.inv2 * rx * rx) : 0.f;
+        wx01[k] = make_float2(ex, ex * rx);
+        wx2[k] = ex * rx * rx;
+    }
+    const int pl = lane < 17 ? lane : 16;   // 17th slice: lanes over columns
+    const float rxp = (float)(xlo + lane - r.fx) - r.dx;
+    const float exp_ = lane < 17 ? exp2f(-r.inv2 * rxp * rxp) : 0.f;
+    const int64_t rstride = (int64_t)w * cc;
+    const float* pb = up + ((int64_t)ylo * w + xlo + hf) * cc + zlo + zl;
+    const float* pp = up + ((int64_t)ylo * w + xlo + pl) * cc + zlo + 16;
+    float A0 = 0.f, Ax = 0.f, Ay = 0.f, Ar = 0.f, P0 = 0.f, P1 = 0.f, P2 = 0.f;
+    float ua[9], ub[9], pa, pbv;
+#define BS_LOAD(U, PU)                                                              \
+    {                                                                               \
+        _Pragma("unroll") for (int k = 0; k < 8; ++k) U[k] = __ldg(pb + 2 * k * cc); \
+        U[8] = hf ? 0.f : __ldg(pb + 16 * cc);                                      \
+        PU = __ldg(pp);                                                             \
+        pb += rstride;                                                              \
+        pp += rstride;                                                              \
+    }
+#define BS_ROW(U, PU, YI)                                                           \
+    {                                                                               \
+        float2 C01 = make_float2(0.f, 0.f);                                         \
+        float C2 = 0.f;                                                             \
+        _Pragma("unroll") for (int k = 0; k < 9; ++k) {                             \
+            C01 = ffma2(make_float2(U[k], U[k]), wx01[k], C01);                     \
+            C2 = fmaf(wx2[k], U[k], C2);                                            \
+        }                                                                           \
+        const float4 t = ytab[YI];                                                  \
+        A0 = fmaf(t.x, C01.x, A0);                                                  \
+        Ax = fmaf(t.x, C01.y, Ax);                                                  \
+        Ay = fmaf(t.y, C01.x, Ay);                                                  \
+        Ar = fmaf(t.x, C2, fmaf(t.z, C01.x, Ar));                                   \
+        P0 = fmaf(t.x, PU, P0);                                                     \
+        P1 = fmaf(t.y, PU, P1);                                                     \
+        P2 = fmaf(t.z, PU, P2);                                                     \
+    }
+    BS_LOAD(ua, pa);
+#pragma unroll
+    for (int yi = 0; yi < 16; yi += 2) {   // rows 0..15 in pairs, next row in flight
+        BS_LOAD(ub, pbv);
+        BS_ROW(ua, pa, yi);
+        if (yi + 2 < 17) BS_LOAD(ua, pa);
+        BS_ROW(ub, pbv, yi + 1);
+    }
+    BS_ROW(ua, pa, 16);
+#undef BS_LOAD
+#undef BS_ROW
+    A0 += __shfl_xor_sync(0xffffffffu, A0, 16);
+    Ax += __shfl_xor_sync(0xffffffffu, Ax, 16);
+    Ay += __shfl_xor_sync(0xffffffffu, Ay, 16);
+    Ar += __shfl_xor_sync(0xffffffffu, Ar, 16);
+    const float eh = hf ? 0.f : ez;
+    S0 = eh * A0;
+    Sx = eh * Ax;
+    Sy = eh * Ay;
+    Sz = eh * rz * A0;
+    S2 = eh * fmaf(rz * rz, A0, Ar);
+    // 17th slice: per-column sums over rows, column weights applied once
+    const float Q0 = exp_ * P0, Qx = exp_ * rxp * P0, Qy = exp_ * P1;
+    const float Qr = fmaf(exp_ * rxp * rxp, P0, exp_ * P2);
+    S0 = fmaf(ez16, Q0, S0);
+    Sx = fmaf(ez16, Qx, Sx);
+    Sy = fmaf(ez16, Qy, Sy);
+    Sz = fmaf(ez16 * rz16, Q0, Sz);
+    S2 = fmaf(ez16, fmaf(rz16 * rz16, Q0, Qr), S2);
+}
+
+template <int C>
+__global__ void __launch_bounds__(32 * BS_WARPS, 1)
+    k_fvr_bwd_sp(const double* __restrict__ P, int64_t n, const uint32_t* __restrict__ svals,
+                 const uint32_t* __restrict__ tstart, int64_t nt, int Sl,
+                 const int32_t* __restrict__ fp, const GRec* __restrict__ rec, int w, int h,
+                 int c, int zoff, const float* __restrict__ up, double* __restrict__ G,
+                 double* __restrict__ accum, const int* halt) {
+    griddep_wait();
+    if (halted(halt)) return;
+    __shared__ float4 ytab[BS_WARPS][17];   // per warp: {ey, ey ry, ey ry^2} per box row
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint32_t np = tstart[nt];
+    // contiguous pair range of this CTA (tile order): one run of neighbouring tiles
+    const uint32_t per = (np + gridDim.x - 1) / gridDim.x;
+    const uint32_t j0 = min(np, blockIdx.x * per), j1 = min(np, j0 + per);
+    const uint32_t smask = (1u << Sl) - 1u;
+    for (uint32_t jb = j0 + 32u * wid; jb < j1; jb += 32u * BS_WARPS) {
+        const uint32_t j = jb + lane;
+        const uint32_t v = j < j1 ? svals[j] : 1u;
+        unsigned first = __ballot_sync(0xffffffffu, j < j1 && (v & smask) == 0u);
+        while (first) {
+            const int src = __ffs(first) - 1;
+            first &= first - 1u;
+            const int64_t i = (int64_t)(__shfl_sync(0xffffffffu, v, src) >> Sl);
+            const int xlo = fp[6 * i], xhi = fp[6 * i + 1], ylo = fp[6 * i + 2];
+            const int yhi = fp[6 * i + 3], zlo = fp[6 * i + 4], zhi = fp[6 * i + 5];
+            const GRec r = rec[i];
+            float S0, Sx, Sy, Sz, S2;
+            if (xhi - xlo == 16 && yhi - ylo == 16 && zhi - zlo == 16) {
+                __syncwarp();   // the previous Gaussian's table reads are done
+                if (lane < 17) {
+                    const float ry = (float)(ylo + lane - r.fy) - r.dy;
+                    const float ey = exp2f(-r.inv2 * ry * ry);
+                    ytab[wid][lane] = make_float4(ey, ey * ry, ey * ry * ry, 0.f);
+                }
+                __syncwarp();
+                bwd_moments17_full<C>(r, xlo, ylo, zlo, w, c, zoff, up, ytab[wid], S0, Sx, Sy,
+                                      Sz, S2);
+            } else {
+                bwd_moments17<false>(r, xlo, xhi - xlo + 1, ylo, yhi - ylo + 1, zlo,
+                                     zhi - zlo + 1, w, c, zoff, up, S0, Sx, Sy, Sz, S2);
+            }
+            S0 = warp_sum(S0);
+            Sx = warp_sum(Sx);
+            Sy = warp_sum(Sy);
+            Sz = warp_sum(Sz);
+            S2 = warp_sum(S2);
+            if (lane == 0) {   // chain rule in f64 (fvr.py:227-273)
+                const double amp = P[4 * n + i], sg = P[3 * n + i];
+                const double inv_s2 = 1.0 / (sg * sg), inv_s3 = inv_s2 / sg;
+                const double k2 = amp * inv_s2;
+                const double gx = k2 * Sx, gy = k2 * Sy, gz = k2 * Sz;
+                G[i] = gx;
+                G[n + i] = gy;
+                G[2 * n + i] = gz;
+                G[3 * n + i] = amp * inv_s3 * S2;
+                G[4 * n + i] = S0;
+                if (accum) accum[i] += sqrt(gx * gx + gy * gy + gz * gz);
+            }
+        }
+    }
+}
+
 __global__ void k_grad_norm_accum(const double* __restrict__ G, int64_t n,
                                   double* __restrict__ accum, const int* halt) {
     if (halted(halt)) return;
@@ -1255,6 +1600,27 @@ static int fvr_forward_impl(const double* params, int64_t n, int w, int h, int c
         SPLATCT_CK(cudaMemsetAsync(at<char>(ws, L.o_pocc), 0,
                                    L.o_fcov + sizeof(unsigned long long) * (size_t)w * h - L.o_pocc,
                                    as_stream(stream)));
+    const char* kern = getenv("SPLATCT_FWD_KERNEL");   // "ff": the FP32 register-blocked kernel
+    if (kern && !strcmp(kern, "ff")) {
+        int dev = 0, nsm = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        const int64_t g2 = L.nt < (int64_t)nsm * 8 ? L.nt : (int64_t)nsm * 8;
+        int64_t f2 = L.nt / (8 * g2);
+        f2 = f2 < 1 ? 1 : (f2 > 32 ? 32 : f2);
+        auto go = [&](auto mk) {
+            return launch_pdl(k_fvr_fwd_ff<decltype(mk)::value>, dim3((unsigned)g2),
+                              dim3(FF_THREADS), 0, as_stream(stream), at<GRec>(ws, L.o_rec), w, h,
+                              c, z0, hx, hy, hz, L.ntx, L.nty, L.nt, L.Sl,
+                              at<uint32_t>(ws, L.o_tstart), at<uint32_t>(ws, vo), vol_yxz,
+                              counter, (int)f2, at<unsigned long long>(ws, L.o_pocc),
+                              at<unsigned long long>(ws, L.o_fcov), halt);
+        };
+        if (masks) SPLATCT_CK(go(std::true_type{}));
+        else SPLATCT_CK(go(std::false_type{}));
+        SPLATCT_LAUNCH_CK();
+        return SPLATCT_OK;
+    }
     CUtensorMap tmap;
     const int use_tma = volume_tensor_map(&tmap, vol_yxz, w, h, c) ? 1 : 0;
     SPLATCT_CK(launch_pdl(k_fvr_fwd, dim3((unsigned)grid), dim3(256), 0, as_stream(stream),
@@ -1288,6 +1654,33 @@ int splatct_fvr_backward(const double* params, int64_t n, int w, int h, int c, i
     if (n == 0) return SPLATCT_OK;
     cudaStream_t s = as_stream(stream);
     const unsigned grid = (unsigned)((n + BG_WARPS - 1) / BG_WARPS);
+    const bool fast = 2 * hx + 1 <= 17 && 2 * hz + 1 <= 17;
+    const char* kern = getenv("SPLATCT_BWD_KERNEL");   // "sp": the spatially ordered kernel
+    if (fast && kern && !strcmp(kern, "sp")) {
+        // spatially ordered persistent kernel; Gaussians with no pair (footprint
+        // outside the volume) are never visited: their gradients are zero
+        SPLATCT_CK(cudaMemsetAsync(grads, 0, sizeof(double) * 5 * (size_t)n, s));
+        int dev = 0, nsm = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        const size_t vs = L.final_buf ? L.o_v1 : L.o_v0;    // sorted values
+        auto go = [&](auto kc) {
+            return launch_pdl(k_fvr_bwd_sp<decltype(kc)::value>, dim3(nsm), dim3(32 * BS_WARPS), 0,
+                              s, params, n, (const uint32_t*)at<uint32_t>(ws, vs),
+                              (const uint32_t*)at<uint32_t>(ws, L.o_tstart), L.nt, L.Sl,
+                              (const int32_t*)at<int32_t>(ws, L.o_fp),
+                              (const GRec*)at<GRec>(ws, L.o_rec), w, h, c, z0, up_yxz, grads,
+                              accum, halt);
+        };
+        if (c == 256) SPLATCT_CK(go(std::integral_constant<int, 256>{}));
+        else if (c == 512) SPLATCT_CK(go(std::integral_constant<int, 512>{}));
+        else if (c == 1024) SPLATCT_CK(go(std::integral_constant<int, 1024>{}));
+        else if (c == 128) SPLATCT_CK(go(std::integral_constant<int, 128>{}));
+        else SPLATCT_CK(go(std::integral_constant<int, 0>{}));
+        SPLATCT_LAUNCH_CK();
+        return SPLATCT_OK;
+    }
+    // per-Gaussian-warp kernel (boxes > 17, or SPLATCT_BWD_KERNEL=warp):
     // an upstream larger than ~half of L2 is read from HBM: visit the
     // Gaussians in tile order so neighbouring warps share DRAM pages / lines
     // (index order spreads concurrent warps out, best while L2-resident)
@@ -1307,7 +1700,6 @@ int splatct_fvr_backward(const double* params, int64_t n, int w, int h, int c, i
         SPLATCT_LAUNCH_CK();
         SPLATCT_CK(cudaMemsetAsync(grads, 0, sizeof(double) * 5 * (size_t)n, s));   // unlisted
     }
-    const bool fast = 2 * hx + 1 <= 17 && 2 * hz + 1 <= 17;
     CUtensorMap utmap;
     int use_tma = 0;
     if (fast && !getenv("SPLATCT_BWD_NO_TMA"))

@@ -149,10 +149,16 @@ def to_host(t: torch.Tensor, out: np.ndarray | None = None) -> np.ndarray:
         return t.numpy().copy()
     t = t.contiguous()
     st = _pinned(t.numel(), t.dtype).view(t.shape)
-    if out is None:
-        out = np.empty(tuple(t.shape), st.numpy().dtype)
-    o = out.reshape(t.shape)
     sn = st.numpy()
+    if out is None:
+        out = np.empty(tuple(t.shape), sn.dtype)
+    elif (out.shape != tuple(t.shape) or out.dtype != sn.dtype
+          or not out.flags.c_contiguous or not out.flags.writeable):
+        # a reshape of anything else would be a copy: the chunks would land in
+        # a temporary and the caller's array would come back untouched
+        raise ValueError(f"to_host: out must be a writeable C-contiguous {sn.dtype} array of "
+                         f"shape {tuple(t.shape)}, got {out.dtype} {out.shape}")
+    o = out
     if t.dim() == 0:
         st.copy_(t)
         np.copyto(o, sn)
@@ -583,6 +589,13 @@ def cone_projector_for(geom: ScanGeometry, w: int, h: int, c_global: int, step: 
     else:
         _CONE_CACHE.move_to_end(key)
     return op
+
+
+def clear_operator_caches() -> None:
+    """Drop every cached projector operator (the next call rebuilds it: a
+    cold API call, as bench.py's e2e "cold" leg measures)."""
+    _PROJ_CACHE.clear()
+    _CONE_CACHE.clear()
 
 
 def operator_for(geom: ScanGeometry, w: int, h: int, c_global: int, step: float = 0.5,

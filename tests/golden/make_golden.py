@@ -24,6 +24,10 @@ Reference call sites exercised (file:line in /root/reference/pkg/src/splatct):
   optim.run_reconstruction   optim.py:286
   densify.densify_and_prune  densify.py:86  + OptimizerState.remap optim.py:92
                              (-> densify.npz; ``--only densify`` writes just that)
+  headline pins (``--only c2pins`` -> c2pins.npz): SURVEY section 8(c)'s short
+  C2/C3 runs -- 256^3 Shepp-Logan, fan(50|25, 512, 1.6, 512, 512), FBP init
+  (projector.fbp :154 + optim.init_cloud_fbp :158, seed 0, 50k), 4 iterations
+  of optim.run_reconstruction :286 with deterministic=True, densify off.
 """
 
 from __future__ import annotations
@@ -287,11 +291,135 @@ def gen_traj(out, iters=500):
           f"psnr {rep['psnr_volume']:.4f}, ssim {rep['ssim_volume']:.4f}")
 
 
+def gen_c2pins(out, iters=4, n=50_000, n_samples=8192):
+    """SURVEY 8(c) C2/C3 short pins, run by the reference itself.
+
+    The 64 MB volumes and 26 MB sinograms are too big to commit; the fixture
+    keeps the init clouds (the GPU test starts from exactly these), the full
+    loss trace, the per-iteration parameter updates and seeded samples /
+    norms of the measured sinogram, the FBP, and the final volume."""
+    dims = (256, 256, 256)
+    truth = phantom.shepp_logan_3d(*dims)
+    box = core.BoxConfig.for_dims(17, dims)
+    rng = np.random.default_rng(2024)
+    vidx = rng.integers(0, 256 ** 3, n_samples)
+    out["c2p_iters"] = np.array(iters)
+    out["c2p_vol_idx"] = vidx
+    out["c2p_truth_sum"] = np.array(truth.zyx.astype(np.float64).sum())
+    for views in (50, 25):
+        pre = f"c2p{views}_"
+        geom = core.ScanGeometry.fan(views, 512, 1.6, 512.0, 512.0)
+        t0 = time.time()
+        meas = projector.forward_project(truth, geom)
+        base = projector.fbp(meas, geom, dims)
+        init = optim.init_cloud_fbp(base, n, 0, box=box)
+        settings = optim.ReconstructionSettings(
+            dims=dims, box=box, max_iters=iters, n_gaussians=n, seed=0,
+            deterministic=True, densify_interval=0)
+        vol, cloud, trace = optim.run_reconstruction(meas, geom, settings, init_cloud=init)
+        dt = time.time() - t0
+        # the same loop body (optim.py:350-403) spelled out with the reference's
+        # own calls, to also keep the last iteration's parameter gradients
+        c2, grads = init, None
+        state = optim.OptimizerState.fresh(n, settings.lr_initial, settings.lr_final, iters)
+        v2 = fvr.reconstruct(c2, box, dims, True)
+        for it in range(iters):
+            pred = projector.forward_project(v2, geom)
+            value, g_pred, g_tv, _ = loss.total_loss_detailed(pred, meas, v2, settings.weights)
+            assert value == trace[it].loss, (it, value, trace[it].loss)
+            dg = projector.back_project(core.Sinogram.from_views(g_pred), geom, dims,
+                                        deterministic=True).zyx.astype(np.float64)
+            grads = fvr.backward(c2, box, dims, core.VolumeGrid.from_zyx(dg + g_tv), prev=grads)
+            if it == 0:   # the init cloud's gradient: independent of the Adam path
+                out[pre + "first_d_mu"] = np.array(grads.d_mu).astype(np.float32)
+                out[pre + "first_d_sigma"] = np.array(grads.d_sigma).astype(np.float32)
+                out[pre + "first_d_intensity"] = np.array(grads.d_intensity).astype(np.float32)
+            c2, state = optim.adam_step(c2, grads, state, 3.0 * box.extent)
+            v2 = fvr.reconstruct(c2, box, dims, True)
+        assert np.array_equal(np.array(c2.mu), np.array(cloud.mu))
+        out[pre + "last_d_mu"] = np.array(grads.d_mu).astype(np.float32)
+        out[pre + "last_d_sigma"] = np.array(grads.d_sigma).astype(np.float32)
+        out[pre + "last_d_intensity"] = np.array(grads.d_intensity).astype(np.float32)
+        out[pre + "accum"] = np.array(grads.accum_pos_grad_norm).astype(np.float32)
+        mv = meas.views
+        sidx = rng.integers(0, mv.size, n_samples)
+        out[pre + "meas_idx"] = sidx
+        out[pre + "meas_samples"] = mv.reshape(-1)[sidx].copy()
+        out[pre + "meas_norm"] = np.array(np.linalg.norm(mv.astype(np.float64)))
+        out[pre + "fbp_samples"] = base.zyx.reshape(-1)[vidx].copy()
+        out[pre + "fbp_norm"] = np.array(np.linalg.norm(base.zyx.astype(np.float64)))
+        for k, v in cloud_arrays(init).items():
+            out[pre + "init_" + k] = v
+        fin = cloud_arrays(cloud)
+        for k, v in cloud_arrays(init).items():
+            out[pre + "delta_" + k] = fin[k] - v
+        out[pre + "loss"] = np.array([r.loss for r in trace])
+        out[pre + "l1"] = np.array([r.loss_l1 for r in trace])
+        out[pre + "ssim"] = np.array([r.loss_ssim for r in trace])
+        out[pre + "tv"] = np.array([r.loss_tv for r in trace])
+        z = vol.zyx.astype(np.float64)
+        out[pre + "vol_samples"] = vol.zyx.reshape(-1)[vidx].copy()
+        out[pre + "vol_norm"] = np.array(np.linalg.norm(z))
+        out[pre + "vol_sum"] = np.array(z.sum())
+        out[pre + "seconds"] = np.array(dt)
+        print(f"c2pins {views} views: losses {[round(r.loss, 6) for r in trace]} ({dt:.0f} s)")
+
+
+API_NAMES = [
+    ("core", "GaussianCloud"), ("core", "BoxConfig.cube"), ("core", "BoxConfig.for_dims"),
+    ("core", "VolumeGrid.from_zyx"), ("core", "Sinogram.from_views"),
+    ("core", "ScanGeometry.parallel"), ("core", "ScanGeometry.fan"), ("core", "ParamGradients"),
+    ("core", "make_offset_grid"), ("core", "validate_cloud"),
+    ("fvr", "reconstruct"), ("fvr", "reconstruct_nodecomp"), ("fvr", "reconstruct_direct"),
+    ("fvr", "backward"),
+    ("projector", "forward_project"), ("projector", "back_project"), ("projector", "fbp"),
+    ("loss", "l1_loss"), ("loss", "ssim_loss"), ("loss", "tv_loss"), ("loss", "total_loss"),
+    ("loss", "total_loss_detailed"), ("loss", "ssim_value"), ("loss", "LossWeights"),
+    ("optim", "adam_step"), ("optim", "OptimizerState.fresh"), ("optim", "init_cloud_fbp"),
+    ("optim", "init_cloud_random"), ("optim", "run_reconstruction"),
+    ("optim", "ReconstructionSettings"),
+    ("densify", "densify_and_prune"), ("metrics", "psnr"), ("metrics", "volume_metrics"),
+    ("phantom", "shepp_logan_3d"),
+]
+
+
+def gen_api():
+    """Public names and call signatures of the reference package (the drop-in
+    boundary): parameter names, kinds and which have defaults."""
+    import importlib
+    import inspect
+    import json
+    out = {"__all__": list(splatct.__all__), "signatures": {}}
+    for mod, qual in API_NAMES:
+        obj = importlib.import_module(f"splatct.{mod}")
+        for part in qual.split("."):
+            obj = getattr(obj, part)
+        sig = inspect.signature(obj)
+        out["signatures"][f"{mod}.{qual}"] = [
+            [p.name, p.kind.name, p.default is not inspect.Parameter.empty]
+            for p in sig.parameters.values()]
+    with open(os.path.join(HERE, "api_signatures.json"), "w") as f:
+        json.dump(out, f, indent=1)
+    print("wrote api_signatures.json with", len(out["signatures"]), "signatures")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--traj", action="store_true")
-    ap.add_argument("--only", choices=["densify"], default=None)
+    ap.add_argument("--only", choices=["densify", "c2pins", "api"], default=None)
     args = ap.parse_args()
+    if args.only == "api":
+        gen_api()
+        return
+    if args.only == "c2pins":
+        d = {}
+        gen_c2pins(d)
+        d["versions"] = np.array(
+            f"numpy {np.__version__}; scipy {__import__('scipy').__version__}; "
+            f"numba {__import__('numba').__version__}")
+        np.savez_compressed(os.path.join(HERE, "c2pins.npz"), **d)
+        print("wrote c2pins.npz with", len(d), "arrays")
+        return
     d = {}
     gen_densify(d)
     np.savez_compressed(os.path.join(HERE, "densify.npz"), **d)

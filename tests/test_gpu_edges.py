@@ -131,23 +131,41 @@ def test_deep_volume_has_no_occupancy_mask():
     assert np.all(np.isfinite(tr.trace_rows()[:, 0]))
 
 
-@pytest.mark.parametrize("dims", [(40, 36, 32), (6, 5, 8)])
-def test_backward_tma_rows_match_direct_loads(dims, monkeypatch):
-    """The TMA-fed backward (c % 4 == 0; boxes larger than tiny volumes are
-    zero-filled by the tensor map) against the direct-load path, which sums the
-    same terms in another column order."""
+# backward kernel variants: the spatially ordered persistent kernel (default),
+# and the per-Gaussian-warp kernel with TMA-fed rows or direct loads
+BWD_VARIANTS = {"sp": {"SPLATCT_BWD_KERNEL": "sp"}, "warp_tma": {"SPLATCT_BWD_KERNEL": "warp"},
+                "warp_direct": {"SPLATCT_BWD_KERNEL": "warp", "SPLATCT_BWD_NO_TMA": "1"}}
+
+
+@pytest.mark.parametrize("dims", [(40, 36, 32), (6, 5, 8), (64, 48, 256)])
+def test_backward_variants_agree(dims, monkeypatch):
+    """The three backward kernels (TMA boxes zero-filled at tiny volumes; the
+    ordered kernel's branch-free full-box path at c = 256) sum the same terms
+    in different orders: equal to fp32 rounding, and each run-to-run bitwise."""
     rng = np.random.default_rng(9)
     box = core.BoxConfig.for_dims(17, dims)
     n = 1500
     mu = np.stack([rng.uniform(-3, d + 3, n) for d in dims], 1)
     cloud = core.GaussianCloud(mu, rng.uniform(0.5, 2.5, n), rng.uniform(0, 1, n))
     up = core.VolumeGrid.from_zyx(rng.standard_normal(dims[::-1]).astype(np.float32))
-    a = fvr.backward(cloud, box, dims, up)
-    monkeypatch.setenv("SPLATCT_BWD_NO_TMA", "1")
-    b = fvr.backward(cloud, box, dims, up)
-    for x, y in ((a.d_mu, b.d_mu), (a.d_sigma, b.d_sigma), (a.d_intensity, b.d_intensity),
-                 (a.accum_pos_grad_norm, b.accum_pos_grad_norm)):
-        assert rel_l2(x, y) < 1e-6
+    out = {}
+    for name, env in BWD_VARIANTS.items():
+        for k in ("SPLATCT_BWD_KERNEL", "SPLATCT_BWD_NO_TMA"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        out[name] = fvr.backward(cloud, box, dims, up)
+        again = fvr.backward(cloud, box, dims, up)
+        np.testing.assert_array_equal(out[name].d_mu, again.d_mu)
+        np.testing.assert_array_equal(out[name].d_sigma, again.d_sigma)
+    a = out["sp"]
+    dm, ds, di, acc, _ = O.splat_bwd(mu, cloud.sigma, cloud.intensity, box.shape, dims, up.zyx)
+    assert rel_l2(a.d_mu, dm) < GRAD_TOL and rel_l2(a.d_sigma, ds) < GRAD_TOL
+    assert rel_l2(a.d_intensity, di) < GRAD_TOL
+    for b in (out["warp_tma"], out["warp_direct"]):
+        for x, y in ((a.d_mu, b.d_mu), (a.d_sigma, b.d_sigma), (a.d_intensity, b.d_intensity),
+                     (a.accum_pos_grad_norm, b.accum_pos_grad_norm)):
+            assert rel_l2(x, y) < 1e-6
 
 
 @pytest.mark.parametrize("dims", [(40, 36, 32), (6, 5, 8)])
@@ -176,6 +194,7 @@ def test_backward_visit_order_is_bitwise_neutral(monkeypatch):
     cloud = core.GaussianCloud(mu, rng.uniform(0.5, 2.5, n), rng.uniform(0, 1, n))
     up = core.VolumeGrid.from_zyx(rng.standard_normal(dims[::-1]).astype(np.float32))
     out = []
+    monkeypatch.setenv("SPLATCT_BWD_KERNEL", "warp")   # the visit-order switch of that kernel
     for o in ("0", "1"):
         monkeypatch.setenv("SPLATCT_BWD_ORDER", o)
         out.append(fvr.backward(cloud, box, dims, up))
@@ -183,3 +202,81 @@ def test_backward_visit_order_is_bitwise_neutral(monkeypatch):
     for x, y in ((a.d_mu, b.d_mu), (a.d_sigma, b.d_sigma), (a.d_intensity, b.d_intensity),
                  (a.accum_pos_grad_norm, b.accum_pos_grad_norm)):
         np.testing.assert_array_equal(x, y)
+
+
+def _footprint_union(mu, half, dims):
+    """Boolean zyx mask of every voxel inside some Gaussian's clipped footprint
+    (the reference's floor(mu) +- half, _kernels.py:45-47,61-78)."""
+    w, h, c = dims
+    m = np.zeros((c, h, w), bool)
+    f = np.floor(mu).astype(np.int64)
+    hx, hy, hz = half
+    for (x, y, z) in f:
+        x0, x1 = max(x - hx, 0), min(x + hx + 1, w)
+        y0, y1 = max(y - hy, 0), min(y + hy + 1, h)
+        z0, z1 = max(z - hz, 0), min(z + hz + 1, c)
+        if x0 < x1 and y0 < y1 and z0 < z1:
+            m[z0:z1, y0:y1, x0:x1] = True
+    return m
+
+
+@pytest.mark.parametrize("side", [9, 13, 15, 17])
+@pytest.mark.parametrize("variant", sorted(BWD_VARIANTS))
+def test_backward_never_reads_outside_footprints(side, variant, monkeypatch):
+    """Upstream is NaN everywhere outside the union of footprints (what the
+    masked adjoint leaves unwritten): gradients stay finite and match the
+    oracle, on the TMA row path (c % 4 == 0) and the direct-load path, with
+    boxes narrower than the 17-column TMA box and Gaussians clipped at x = 0."""
+    for k, v in BWD_VARIANTS[variant].items():
+        monkeypatch.setenv(k, v)
+    rng = np.random.default_rng(20 + side)
+    dims = (64, 48, 36)
+    box = core.BoxConfig.cube(side)
+    n = 60                                     # 25-80 % of the voxels covered
+    mu = np.stack([rng.uniform(-2, d + 2, n) for d in dims], 1)
+    mu[:10, 0] = rng.uniform(-1.0, 2.0, 10)   # clipped at x = 0
+    sig = rng.uniform(0.5, 2.5, n)
+    inten = rng.uniform(0, 1, n)
+    cloud = core.GaussianCloud(mu, sig, inten)
+    up = rng.standard_normal(dims[::-1]).astype(np.float32)
+    inside = _footprint_union(mu, box.half, dims)
+    assert (~inside).any()
+    poisoned = up.copy()
+    poisoned[~inside] = np.nan
+    gr = fvr.backward(cloud, box, dims, core.VolumeGrid.from_zyx(poisoned))
+    clean = np.where(inside, up, 0).astype(np.float32)
+    dm, ds, di, acc, _ = O.splat_bwd(mu, sig, inten, box.shape, dims, clean)
+    for got, want in ((gr.d_mu, dm), (gr.d_sigma, ds), (gr.d_intensity, di),
+                      (gr.accum_pos_grad_norm, acc)):
+        assert np.all(np.isfinite(got))
+        assert rel_l2(got, want) < GRAD_TOL
+
+
+@pytest.mark.parametrize("side", [9, 13, 17])
+def test_trainer_step_with_poisoned_adjoint_buffer(side):
+    """A training step with the masked adjoint (<= 64 z tiles, c % 4 == 0) whose
+    output buffer starts as NaN: the quads the adjoint skips stay NaN, and the
+    voxelizer backward must never read them."""
+    import torch
+    from paper_2411_04844_b200 import device as D, loss
+    from paper_2411_04844_b200.trainer import Trainer
+    dev = D.require_cuda()
+    dims = (48, 40, 32)
+    box = core.BoxConfig.cube(side)
+    rng = np.random.default_rng(30 + side)
+    n = 150
+    mu = np.stack([rng.uniform(-1, d / 2, n) for d in dims], 1)   # leaves empty space
+    cloud = core.GaussianCloud(mu, rng.uniform(0.6, 1.5, n), rng.uniform(0, 1, n))
+    geom = core.ScanGeometry.parallel(8, 64)
+    meas = torch.rand((8, 64, dims[2]), device=dev)
+    tr = Trainer(meas, geom, dims, box, loss.LossWeights(), D.cloud_to_params(cloud, dev),
+                 max_iters=10, trace_cap=3)
+    assert tr.fvr.footprint_coverage is not None   # the masked adjoint is on
+    tr.dl.fill_(float("nan"))
+    tr.initial_volume()
+    for _ in range(3):
+        tr.step()
+    torch.cuda.synchronize()
+    assert torch.isnan(tr.dl).any()                # skipped quads were left unwritten
+    assert np.all(np.isfinite(tr.trace_rows()[:, 0]))
+    assert torch.isfinite(tr.params).all() and torch.isfinite(tr.grads).all()
