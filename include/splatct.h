@@ -366,6 +366,14 @@ int splatct_densify_apply(const double* params, const double* m1, const double* 
                           double cbrt2, double* new_params, double* new_m1, double* new_m2,
                           void* ws, size_t ws_bytes, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Tensor-core self-test (no reference counterpart; validates the tcgen05
+ * conventions the voxelizer forward builds on): D[128][16] = A[128][8] B[16][8]^T
+ * with A in TMEM, B in shared memory, D in TMEM (kind::tf32, cta_group::1).
+ * mode 0: one TF32 MMA; mode 1: the 3xTF32 split. Device f32 pointers.
+ * ------------------------------------------------------------------------- */
+int splatct_tc_selftest(const float* a, const float* b, float* d, int mode, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -16,7 +16,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "libsplatct.so")
-SOURCES = ["scan.cu", "fvr.cu", "proj.cu", "proj_blocked.cu", "loss.cu", "fbp.cu", "cone.cu", "densify.cu"]
+SOURCES = ["scan.cu", "fvr.cu", "proj.cu", "proj_blocked.cu", "loss.cu", "fbp.cu", "cone.cu", "densify.cu",
+           "tc.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 NVCC_FLAGS = [

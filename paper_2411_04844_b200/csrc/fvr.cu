@@ -31,6 +31,7 @@
 #include <type_traits>
 
 #include "common.cuh"
+#include "tc.cuh"
 
 namespace splatct {
 
@@ -893,6 +894,390 @@ __global__ void __launch_bounds__(FF_THREADS, 8)
     }
 }
 
+// --------------------------------------------------------------------------
+// forward on the 5th-generation tensor cores (tcgen05, the default).
+//
+// Per 16^3 tile the splat is the rank-K GEMM D[(y,x)][z] = sum_k A[(y,x)][k] B[k][z]
+// with A = (I ey) (x) ex (the 256-row outer product of Gaussian k) and B = ez.
+// D is two M = 128 accumulators (rows y 0..7 / 8..15) of N = 16 slices in
+// TMEM; K runs over the tile's Gaussian list (ascending id) in stages of 32.
+// fp32-level accuracy from the 3xTF32 split (hi = x & ~0x1fff, lo = x - hi):
+// D += Alo Bhi + Ahi Blo + Ahi Bhi per k8 chunk (validated bitwise by
+// splatct_tc_selftest).  Warp roles, one persistent 416-thread CTA per SM
+// over a contiguous, cost-balanced range of tiles:
+//   * 8 producer warps: per stage, the separable tables (ex, I ey, ez; zero
+//     outside box, tile and volume) into shared memory, then each thread forms
+//     its row's 32 outer-product values, splits them and writes A straight into
+//     TMEM (tcgen05.st; A never touches shared memory), and B (16 x 32, K-major)
+//     into a shared-memory stage; the footprint coverage rows for the masks;
+//   * 1 MMA warp: one elected thread issues 24 kind::tf32 MMAs per stage
+//     (M 128, N 16, K 8; A from TMEM) and commits to mbarriers;
+//   * 4 epilogue warps: tcgen05.ld of the two accumulators (a thread gets one
+//     pixel column's 16 slices per half), 64-byte column stores, empty-space
+//     masks; empty tiles store zeros without touching the tensor core.
+// Stages (A in TMEM, B in shared memory) and accumulators are double-buffered.
+// --------------------------------------------------------------------------
+constexpr int TC_KS = 32;          // Gaussians per stage
+constexpr int TC_P_WARPS = 16;   // 4 lane quadrants x 2 row halves x 2 k halves
+constexpr int TC_THREADS = 32 * (TC_P_WARPS + 1 + 4);
+constexpr int TC_TS = TC_KS + 4;   // table row stride (floats): conflict-free LDS.128 rows
+constexpr int TC_ALPHA = 4;        // cost of an empty tile, in (tile, Gaussian) pairs
+
+struct TcSmem {
+    float ex[2][16][TC_TS], ey[2][16][TC_TS], ez[2][16][TC_TS];   // [buf][coordinate][k]
+    uint32_t bop[2][2][TC_KS * 16];                               // [slot][hi, lo] B, K-major
+    uint32_t covw[4][TC_P_WARPS][16];                              // per tile: rows' covered columns
+    uint64_t a_full[2], a_empty[2], d_full[2], d_empty[2], cov_full[4];
+    uint32_t tbase;
+    int t_begin, t_end;
+};
+
+// first tile t with cost(t) = tstart[t] + ALPHA t >= target (cost is increasing)
+__device__ __forceinline__ int64_t tc_lower(const uint32_t* tstart, int64_t nt, int64_t target) {
+    int64_t lo = 0, hi = nt;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if ((int64_t)tstart[mid] + TC_ALPHA * mid < target) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ void p_bar() {   // the 256 producer threads
+    asm volatile("bar.sync 1, %0;\n" ::"n"(32 * TC_P_WARPS) : "memory");
+}
+
+constexpr int TC_LIST_CAP = 7680;   // non-empty tiles per CTA (the 120 KB dynamic list)
+
+// Walks the stages (32-Gaussian slices) of the CTA's non-empty tile list.
+struct TcStage {
+    int i;          // list index
+    uint32_t k0;    // first Gaussian of the stage within the tile
+    __device__ __forceinline__ void next(const int4* list) {
+        k0 += TC_KS;
+        if (k0 >= (uint32_t)list[i].z) {
+            k0 = 0;
+            ++i;
+        }
+    }
+};
+
+template <bool MASKS>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    k_fvr_fwd_tc(const GRec* __restrict__ rec, int w, int h, int c, int zoff, int hx, int hy,
+                 int hz, int ntx, int nty, int64_t nt, int S,
+                 const uint32_t* __restrict__ tstart, const uint32_t* __restrict__ svals,
+                 float* __restrict__ vol, unsigned long long* __restrict__ pocc,
+                 unsigned long long* __restrict__ fcov, const int* halt) {
+    griddep_wait();
+    if (halted(halt)) return;
+    __shared__ __align__(128) TcSmem sm;
+    __shared__ int s_wcount[TC_THREADS / 32 + 1];
+    extern __shared__ int4 tlist[];   // {tile, begin, count, 0} of the CTA's non-empty tiles
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int ntz = (int)(nt / ((int64_t)ntx * nty));
+    const int64_t nxy = (int64_t)ntx * nty;
+    if (warp == TC_P_WARPS) tc::tmem_alloc(&sm.tbase, 512);
+    if (tid == 0) {
+        for (int i = 0; i < 2; ++i) {
+            tc::mbar_init(&sm.a_full[i], TC_P_WARPS);
+            tc::mbar_init(&sm.a_empty[i], 1);
+            tc::mbar_init(&sm.d_full[i], 1);
+            tc::mbar_init(&sm.d_empty[i], 4);
+        }
+        for (int i = 0; i < 4; ++i) tc::mbar_init(&sm.cov_full[i], TC_P_WARPS);
+        tc::mbar_init_fence();
+        const int64_t F = (int64_t)tstart[nt] + TC_ALPHA * nt;
+        const int64_t G = gridDim.x;
+        sm.t_begin = (int)tc_lower(tstart, nt, (F * blockIdx.x + G - 1) / G);
+        sm.t_end = blockIdx.x + 1 == gridDim.x
+                       ? (int)nt
+                       : (int)tc_lower(tstart, nt, (F * (blockIdx.x + 1) + G - 1) / G);
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t t0 = sm.tbase;
+    const int tb = sm.t_begin, te = sm.t_end;
+    // the non-empty tiles of [tb, te), in order, into shared memory (block-wide
+    // compaction): the roles then walk stages without global loads on their
+    // critical paths
+    int nlist = 0;
+    for (int base = tb; base < te; base += TC_THREADS) {
+        const int t = base + tid;
+        uint32_t b = 0, e = 0;
+        if (t < te) {
+            b = tstart[t];
+            e = tstart[t + 1];
+        }
+        const bool ne = e > b;
+        const unsigned bal = __ballot_sync(0xffffffffu, ne);
+        if (lane == 0) s_wcount[warp] = __popc(bal);
+        __syncthreads();
+        if (tid == 0) {
+            int acc = 0;
+            for (int k = 0; k < TC_THREADS / 32; ++k) {
+                const int v = s_wcount[k];
+                s_wcount[k] = acc;
+                acc += v;
+            }
+            s_wcount[TC_THREADS / 32] = acc;
+        }
+        __syncthreads();
+        if (ne) {
+            const int pos = nlist + s_wcount[warp] + __popc(bal & ((1u << lane) - 1u));
+            const int tz = (int)(t / nxy), rr = (int)(t % nxy);
+            tlist[pos] = make_int4(t, (int)b, (int)(e - b), (tz << 20) | ((rr / ntx) << 10) | (rr % ntx));
+        }
+        nlist += s_wcount[TC_THREADS / 32];
+        __syncthreads();
+    }
+
+    if (warp < TC_P_WARPS) {
+        // ------------------------------------------------------------ producers
+        // warp w: TMEM lane quadrant q = w % 4, accumulator half hf (rows y 0-7 /
+        // 8-15), stage k half ks (Gaussians 16 ks .. 16 ks + 15)
+        const int q = warp & 3, hf = (warp >> 2) & 1, ks = warp >> 3;
+        const int m = 32 * q + lane;                 // accumulator row (TMEM lane)
+        const int ty = 8 * hf + (m >> 4), tx = m & 15;
+        const uint32_t lane_addr = (uint32_t)(32 * q) << 16;
+        const int gi = tid >> 4, part = tid & 15;    // table builder: Gaussian, coordinate
+        // stage cursor (cur) and the two prefetch cursors: the Gaussian id of
+        // stage +2 and the record of stage +1 are loaded ahead of their use
+        TcStage cur{0, 0u}, n1, n2;
+        n1 = cur;
+        if (nlist > 0) n1.next(tlist);
+        n2 = n1;
+        if (n2.i < nlist) n2.next(tlist);
+        // raw sorted pair value of Gaussian gi of a stage (0xffffffff: none); the
+        // shift to the Gaussian id happens a stage later, off the load's latency
+        auto sval = [&](const TcStage& st) -> uint32_t {
+            if (st.i >= nlist) return 0xffffffffu;
+            const int4 d = tlist[st.i];
+            return st.k0 + gi < (uint32_t)d.z ? svals[d.y + st.k0 + gi] : 0xffffffffu;
+        };
+        GRec rcur, rnext;
+        uint32_t v2 = sval(n2);
+        {
+            const uint32_t v0 = sval(cur), v1 = sval(n1);
+            if (v0 != 0xffffffffu) rcur = rec[v0 >> S];
+            if (v1 != 0xffffffffu) rnext = rec[v1 >> S];
+        }
+        unsigned cov = 0u;   // lanes 0..15 of each warp: row `part`'s covered columns
+        uint32_t gs = 0, dt = 0;
+        // tables of stage gs live in buffer gs & 1; stage gs's are built at the end of stage gs - 1
+        auto build = [&](const TcStage& st, const GRec& r, int buf) {
+            const int4 d = tlist[st.i];
+            const int nb = (int)min((uint32_t)TC_KS, (uint32_t)d.z - st.k0);
+            const int x0 = (d.w & 1023) * TT, y0 = ((d.w >> 10) & 1023) * TT, z0 = (d.w >> 20) * TT;
+            float vx = 0.f, vy = 0.f, vz = 0.f;
+            unsigned rows = 0u;
+            if (gi < nb) {
+                vx = tab_weight(x0 + part, 0, w, r.fx, hx, r.dx, r.inv2);
+                vy = tab_weight(y0 + part, 0, h, r.fy, hy, r.dy, r.inv2) * r.I;
+                vz = tab_weight(z0 + part, zoff, c, r.fz, hz, r.dz, r.inv2);
+                if (MASKS) {   // integer footprint inside the tile (a3): row `part`
+                    const int yy = y0 + part;
+                    const int bx0 = max(r.fx - hx, x0), bx1 = min(min(r.fx + hx, w - 1), x0 + TT - 1);
+                    if (yy >= r.fy - hy && yy <= r.fy + hy && yy < h && bx0 <= bx1)
+                        rows = ((2u << (bx1 - x0)) - 1u) & ~((1u << (bx0 - x0)) - 1u);
+                }
+            }
+            sm.ex[buf][part][gi] = vx;
+            sm.ey[buf][part][gi] = vy;
+            sm.ez[buf][part][gi] = vz;
+            if (MASKS) {   // OR over the warp's two Gaussians (lanes part, part + 16)
+                rows |= __shfl_xor_sync(0xffffffffu, rows, 16);
+                cov |= rows;
+            }
+        };
+        if (cur.i < nlist) build(cur, rcur, 0);
+        p_bar();
+        while (cur.i < nlist) {
+            const uint32_t cnt = (uint32_t)tlist[cur.i].z;
+            const int nb = (int)min((uint32_t)TC_KS, cnt - cur.k0);
+            const int nk8 = (nb + 7) >> 3;
+            const int slot = gs & 1, buf = gs & 1;
+            // prefetch: record of stage +2 (its id was loaded a stage ago), id of stage +3
+            GRec rn2;
+            if (v2 != 0xffffffffu) rn2 = rec[v2 >> S];
+            TcStage n3 = n2;
+            if (n3.i < nlist) n3.next(tlist);
+            const uint32_t v3 = sval(n3);
+            // the MMAs of the stage that last used this slot are complete
+            tc::mbar_wait(&sm.a_empty[slot], ((gs >> 1) & 1) ^ 1);
+            tc::fence_after();
+            // A: this row's outer-product values of k chunks 2 ks, 2 ks + 1, split,
+            // straight into TMEM
+            const float* ey = sm.ey[buf][ty];
+            const float* ex = sm.ex[buf][tx];
+            const uint32_t acol = t0 + lane_addr + 128 + slot * 128 + hf * 64;
+#pragma unroll
+            for (int jj = 0; jj < 2; ++jj) {
+                const int j = 2 * ks + jj;
+                if (j < nk8) {
+                    const float4 ya = *reinterpret_cast<const float4*>(ey + 8 * j);
+                    const float4 yb = *reinterpret_cast<const float4*>(ey + 8 * j + 4);
+                    const float4 xa = *reinterpret_cast<const float4*>(ex + 8 * j);
+                    const float4 xb = *reinterpret_cast<const float4*>(ex + 8 * j + 4);
+                    const float v[8] = {ya.x * xa.x, ya.y * xa.y, ya.z * xa.z, ya.w * xa.w,
+                                        yb.x * xb.x, yb.y * xb.y, yb.z * xb.z, yb.w * xb.w};
+                    uint32_t hi[8], lo[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        hi[e] = __float_as_uint(v[e]) & 0xffffe000u;
+                        lo[e] = __float_as_uint(v[e] - __uint_as_float(hi[e]));
+                    }
+                    tc::st_x8(acol + 8 * j, hi);
+                    tc::st_x8(acol + 32 + 8 * j, lo);
+                }
+            }
+            {   // B: ez (16 slices x 32 Gaussians), canonical K-major, one per thread
+                const int n = tid >> 5, kk = tid & 31;
+                const float v = sm.ez[buf][n][kk];
+                const uint32_t vh = __float_as_uint(v) & 0xffffe000u;
+                const int off = (128 * (kk >> 3) + 64 * ((kk & 7) >> 2) + 32 * (n >> 3) +
+                                 4 * (n & 7) + (kk & 3));
+                sm.bop[slot][0][off] = vh;
+                sm.bop[slot][1][off] = __float_as_uint(v - __uint_as_float(vh));
+            }
+            tc::wait_st();
+            tc::fence_proxy_async();
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&sm.a_full[slot]);
+            const bool last = cur.k0 + TC_KS >= cnt;   // the tile's last stage
+            if (MASKS && last) {   // the tile's footprint coverage rows, for the epilogue
+                const int cb = dt & 3;
+                if (lane < 16) sm.covw[cb][warp][lane] = cov;
+                cov = 0u;
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&sm.cov_full[cb]);
+            }
+            if (last) ++dt;
+            // the next stage's tables (the other buffer), from the prefetched record
+            if (n1.i < nlist) build(n1, rnext, buf ^ 1);
+            p_bar();
+            cur = n1;
+            n1 = n2;
+            n2 = n3;
+            rnext = rn2;
+            v2 = v3;
+            ++gs;
+        }
+    } else if (warp == TC_P_WARPS) {
+        // ---------------------------------------------------------------- MMA
+        if (lane == 0) {
+            const uint32_t id = tc::idesc_tf32(128, 16);
+            uint32_t gs = 0;
+            for (int li = 0; li < nlist; ++li) {
+                const uint32_t cnt = (uint32_t)tlist[li].z;
+                for (uint32_t k0 = 0; k0 < cnt; k0 += TC_KS, ++gs) {
+                    const int nb = (int)min((uint32_t)TC_KS, cnt - k0);
+                    const int nk8 = (nb + 7) >> 3;
+                    const int slot = gs & 1;
+                    tc::mbar_wait(&sm.d_empty[slot], ((gs >> 1) & 1) ^ 1);
+                    tc::mbar_wait(&sm.a_full[slot], (gs >> 1) & 1);
+                    tc::fence_after();
+                    const uint32_t bh = tc::smem_u32(sm.bop[slot][0]);
+                    const uint32_t bl = tc::smem_u32(sm.bop[slot][1]);
+                    // each stage sums into a fresh accumulator (the epilogue adds the
+                    // stages in fp32, round to nearest): the small cross terms first
+                    for (int hf = 0; hf < 2; ++hf) {
+                        const uint32_t d = t0 + slot * 32 + hf * 16;
+                        const uint32_t a = t0 + 128 + slot * 128 + hf * 64;
+                        for (int j = 0; j < nk8; ++j) {
+                            const uint64_t dh = tc::smem_desc(bh + 512 * j, 256, 128);
+                            const uint64_t dl = tc::smem_desc(bl + 512 * j, 256, 128);
+                            tc::mma_tf32_ts(d, a + 32 + 8 * j, dh, id, j ? 1u : 0u);
+                            tc::mma_tf32_ts(d, a + 8 * j, dl, id, 1u);
+                        }
+                        for (int j = 0; j < nk8; ++j) {
+                            const uint64_t dh = tc::smem_desc(bh + 512 * j, 256, 128);
+                            tc::mma_tf32_ts(d, a + 8 * j, dh, id, 1u);
+                        }
+                    }
+                    tc::commit(&sm.a_empty[slot]);   // this slot's A and B are free again
+                    tc::commit(&sm.d_full[slot]);    // the stage's partial sums are final
+                }
+            }
+        }
+        __syncwarp();
+    } else {
+        // ----------------------------------------------------------- epilogue
+        const int q = warp & 3;
+        const int m = 32 * q + lane;
+        const uint32_t lane_addr = (uint32_t)(32 * q) << 16;
+        uint32_t gs = 0, dt = 0;
+        int li = 0;
+        for (int t = tb; t < te; ++t) {
+            uint32_t cnt = 0;
+            if (li < nlist && tlist[li].x == t) cnt = (uint32_t)tlist[li++].z;
+            const int tzi = (int)(t / nxy), rest = (int)(t % nxy);
+            const int x0 = (rest % ntx) * TT, y0 = (rest / ntx) * TT, z0 = tzi * TT;
+            float acc[2][16];
+#pragma unroll
+            for (int z = 0; z < 16; ++z) acc[0][z] = acc[1][z] = 0.f;
+            for (uint32_t k0 = 0; k0 < cnt; k0 += TC_KS, ++gs) {
+                const int slot = gs & 1;
+                tc::mbar_wait(&sm.d_full[slot], (gs >> 1) & 1);
+                tc::fence_after();
+                uint32_t v0[16], v1[16];
+                tc::ld_x16(t0 + lane_addr + slot * 32, v0);
+                tc::ld_x16(t0 + lane_addr + slot * 32 + 16, v1);
+                tc::wait_ld();
+                tc::fence_before();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&sm.d_empty[slot]);
+#pragma unroll
+                for (int z = 0; z < 16; ++z) {
+                    acc[0][z] += __uint_as_float(v0[z]);
+                    acc[1][z] += __uint_as_float(v1[z]);
+                }
+            }
+            unsigned cov[2] = {0u, 0u};
+            if (MASKS && cnt > 0) {
+                const int cb = dt & 3;
+                tc::mbar_wait(&sm.cov_full[cb], (dt >> 2) & 1);
+#pragma unroll
+                for (int wv = 0; wv < TC_P_WARPS; ++wv) {
+                    cov[0] |= sm.covw[cb][wv][m >> 4];
+                    cov[1] |= sm.covw[cb][wv][8 + (m >> 4)];
+                }   // row r's columns: warps hold rows part = lane of Gaussians 2 w, 2 w + 1
+            }
+            if (cnt > 0) ++dt;
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+                const int y = y0 + 8 * hf + (m >> 4), x = x0 + (m & 15);
+                if (x >= w || y >= h) continue;
+                float* col = vol + ((int64_t)y * w + x) * c + z0;
+                if ((c & 3) == 0 && z0 + TT <= c) {
+#pragma unroll
+                    for (int qq = 0; qq < 4; ++qq)
+                        reinterpret_cast<float4*>(col)[qq] =
+                            make_float4(acc[hf][4 * qq], acc[hf][4 * qq + 1], acc[hf][4 * qq + 2],
+                                        acc[hf][4 * qq + 3]);
+                } else {
+#pragma unroll
+                    for (int z = 0; z < 16; ++z)
+                        if (z0 + z < c) col[z] = acc[hf][z];
+                }
+                if (MASKS && ntz <= 64 && cnt > 0) {
+                    bool nz = false;
+#pragma unroll
+                    for (int z = 0; z < 16; ++z) nz |= acc[hf][z] != 0.f;
+                    if (nz) atomicOr(&pocc[(int64_t)y * w + x], 1ull << tzi);
+                    if ((cov[hf] >> (m & 15)) & 1u) atomicOr(&fcov[(int64_t)y * w + x], 1ull << tzi);
+                }
+            }
+        }
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    if (warp == TC_P_WARPS) tc::tmem_free(t0, 512);
+}
+
 // tstart[t] = lower_bound(sorted keys, t) for t in [0, nt] from the key
 // boundaries: sorted position j starts every tile in (key[j-1], key[j]], and
 // tstart[nt] = number of pairs (read on the device: the bins are dense).
@@ -1600,7 +1985,31 @@ static int fvr_forward_impl(const double* params, int64_t n, int w, int h, int c
         SPLATCT_CK(cudaMemsetAsync(at<char>(ws, L.o_pocc), 0,
                                    L.o_fcov + sizeof(unsigned long long) * (size_t)w * h - L.o_pocc,
                                    as_stream(stream)));
-    const char* kern = getenv("SPLATCT_FWD_KERNEL");   // "ff": the FP32 register-blocked kernel
+    const char* kern = getenv("SPLATCT_FWD_KERNEL");   // "mma" / "ff": the other kernels
+    // (the tensor-core kernel keeps each CTA's tile list in shared memory:
+    // volumes beyond 148 x 7680 tiles of 16^3 take the mma.sync kernel)
+    if (kern && !strcmp(kern, "tc") && L.nt <= (int64_t)148 * TC_LIST_CAP) {
+        int dev = 0, nsm = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        const int64_t g3 = L.nt < (int64_t)nsm ? L.nt : (int64_t)nsm;
+        // one CTA per SM (it allocates all 512 TMEM columns): a dynamic
+        // shared-memory reservation above half the SM keeps a second one off
+        constexpr int kPad = TC_LIST_CAP * 16;   // the tile list; > half an SM: 1 CTA / SM
+        auto go = [&](auto mk) {
+            auto kern_fn = k_fvr_fwd_tc<decltype(mk)::value>;
+            cudaFuncSetAttribute(kern_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kPad);
+            return launch_pdl(kern_fn, dim3((unsigned)g3), dim3(TC_THREADS), kPad, as_stream(stream), at<GRec>(ws, L.o_rec), w, h,
+                              c, z0, hx, hy, hz, L.ntx, L.nty, L.nt, L.Sl,
+                              at<uint32_t>(ws, L.o_tstart), at<uint32_t>(ws, vo), vol_yxz,
+                              at<unsigned long long>(ws, L.o_pocc),
+                              at<unsigned long long>(ws, L.o_fcov), halt);
+        };
+        if (masks) SPLATCT_CK(go(std::true_type{}));
+        else SPLATCT_CK(go(std::false_type{}));
+        SPLATCT_LAUNCH_CK();
+        return SPLATCT_OK;
+    }
     if (kern && !strcmp(kern, "ff")) {
         int dev = 0, nsm = 148;
         cudaGetDevice(&dev);
