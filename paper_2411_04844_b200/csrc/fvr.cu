@@ -1860,6 +1860,245 @@ __global__ void __launch_bounds__(32 * BS_WARPS, 1)
     }
 }
 
+// --------------------------------------------------------------------------
+// backward, tile-staged (the default for boxes <= 17^3 with c % 4 == 0).
+//
+// A Gaussian's clipped box starts in its first tile (slot 0 of its pairs)
+// and spans at most 2 x 2 x 2 tiles from there.  A persistent CTA (one per
+// SM, 16 warps) claims work units = (tile column tx, ty) x (a run of BT_ZCH z
+// tiles) and sweeps z: the upstream "slabs" -- tiles (tx..tx+1, ty..ty+1) of
+// one z tile, 32 x 32 x 16 floats = 64 KB -- arrive by one TMA box load each
+// into a 3-slab shared-memory ring (slab tz + 2 loads while tile tz is
+// processed).  Warps then take the Gaussians whose first tile is (tx, ty, tz)
+// (ballot over the tile's sorted pairs) and read their 17^3 boxes from shared
+// memory: the upstream is read from L2 once per unit (about 4x its size in
+// total, from the 2 x 2 tile halo) instead of once per Gaussian (the TMA row
+// kernel's 1.2 GB per C2 launch).
+// Per Gaussian, lanes take the box's 17 x 17 (column, slice) pairs as 10 slots
+// (s = lane + 32 i: column s / 17, slice s % 17) and, per row, accumulate the
+// y moments T0 += ey u, T1 += ey ry u, T2 += ey ry^2 u (conflict-free LDS:
+// slot i of lane l reads bank (16 x + z) mod 32); x and z weights are applied
+// once per slot at the end, then one warp reduction and the f64 chain rule
+// (fvr.py:227-273).  Footprints clipped by the volume take the clamped
+// global-memory path (bwd_moments17).  Deterministic: each Gaussian is summed
+// by one warp in a fixed order.
+// --------------------------------------------------------------------------
+constexpr int BT_WARPS = 16;
+constexpr int BT_ZCH = 16;                 // z tiles per work unit
+constexpr int BT_SLAB = 32 * 32 * 16;      // floats per slab
+constexpr unsigned BT_SLAB_BYTES = BT_SLAB * 4u;
+
+struct __align__(16) BtWarp {
+    float4 ey[17];      // {ey, ey ry, ey ry^2, 0} per box row
+};
+
+__global__ void __launch_bounds__(32 * BT_WARPS, 1)
+    k_fvr_bwd_ts(const double* __restrict__ P, int64_t n, const uint32_t* __restrict__ svals,
+                 const uint32_t* __restrict__ tstart, int ntx, int nty, int ntz, int Sl,
+                 const int32_t* __restrict__ fp, const GRec* __restrict__ rec, int w, int h,
+                 int c, int zoff, const float* __restrict__ up,
+                 const __grid_constant__ CUtensorMap utmap, unsigned int* __restrict__ counter,
+                 double* __restrict__ G, double* __restrict__ accum, const int* halt) {
+    griddep_wait();
+    if (halted(halt)) return;
+    extern __shared__ __align__(1024) float slab[];      // [3][y 32][x 32][z 16]
+    __shared__ BtWarp wt[BT_WARPS];
+    __shared__ __align__(8) unsigned long long sbar[3];
+    __shared__ int s_unit;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        for (int b = 0; b < 3; ++b) tc::mbar_init(reinterpret_cast<uint64_t*>(&sbar[b]), 1);
+        tc::mbar_init_fence();
+    }
+    __syncthreads();
+    const uint32_t smask = (1u << Sl) - 1u;
+    const int nzch = (ntz + BT_ZCH - 1) / BT_ZCH;
+    const int units = ntx * nty * nzch;
+    // slab (z tile) held by each ring buffer, and loads issued per buffer (the
+    // mbarrier phase); plain scalars (no local-memory array)
+    int held0 = -1, held1 = -1, held2 = -1;
+    uint32_t ld0 = 0u, ld1 = 0u, ld2 = 0u;
+    const int64_t nxy = (int64_t)ntx * nty;
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) s_unit = (int)atomicAdd(counter, 1u);
+        __syncthreads();
+        const int u = s_unit;
+        if (u >= units) break;
+        const int col = u / nzch, ch = u % nzch;
+        const int tx = col % ntx, ty = col / ntx;
+        const int tz0 = ch * BT_ZCH, tz1 = min(ntz, tz0 + BT_ZCH);
+        // issue the load of slab sz into its ring buffer (thread 0; caller syncs first)
+        auto load = [&](int sz_) {
+            const int b = sz_ % 3;
+            int& held = b == 0 ? held0 : (b == 1 ? held1 : held2);
+            uint32_t& lds = b == 0 ? ld0 : (b == 1 ? ld1 : ld2);
+            if (held == sz_ || sz_ >= ntz) return;
+            held = sz_;
+            ++lds;
+            if (tid == 0) {
+                const unsigned bar = tc::smem_u32(&sbar[b]);
+                const unsigned dst = tc::smem_u32(slab + b * BT_SLAB);
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar),
+                             "r"(BT_SLAB_BYTES)
+                             : "memory");
+                asm volatile(
+                    "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
+                    "[%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(dst),
+                    "l"(&utmap), "r"(16 * sz_), "r"(16 * tx), "r"(16 * ty), "r"(bar)
+                    : "memory");
+            }
+        };
+        auto wait_slab = [&](int sz_) {
+            if (sz_ >= ntz) return;
+            const int b = sz_ % 3;
+            const uint32_t lds = b == 0 ? ld0 : (b == 1 ? ld1 : ld2);
+            tc::mbar_wait(reinterpret_cast<uint64_t*>(&sbar[b]), (lds - 1u) & 1u);
+        };
+        // a new unit is another tile column: land every outstanding slab load of
+        // the previous unit (a prefetch may never have been waited for), then
+        // forget what the buffers hold
+        if (ld0) tc::mbar_wait(reinterpret_cast<uint64_t*>(&sbar[0]), (ld0 - 1u) & 1u);
+        if (ld1) tc::mbar_wait(reinterpret_cast<uint64_t*>(&sbar[1]), (ld1 - 1u) & 1u);
+        if (ld2) tc::mbar_wait(reinterpret_cast<uint64_t*>(&sbar[2]), (ld2 - 1u) & 1u);
+        held0 = held1 = held2 = -1;
+        for (int tz = tz0; tz < tz1; ++tz) {
+            const int64_t t = (int64_t)tz * nxy + (int64_t)ty * ntx + tx;
+            const uint32_t pb = tstart[t], pe = tstart[t + 1];
+            if (pb == pe) continue;   // no pairs: no Gaussian starts here
+            __syncthreads();          // every warp is done with the slab tz - 1 buffer
+            load(tz);
+            load(tz + 1);
+            if (tz + 1 < tz1) {       // prefetch for the next tile of the unit
+                const int64_t t2 = t + nxy;
+                if (tstart[t2 + 1] > tstart[t2]) load(tz + 2);
+            }
+            wait_slab(tz);
+            wait_slab(tz + 1);
+            // the Gaussians whose first tile is t
+            for (uint32_t jb = pb + 32u * warp; jb < pe; jb += 32u * BT_WARPS) {
+                const uint32_t j = jb + lane;
+                const uint32_t v = j < pe ? svals[j] : 1u;
+                unsigned first = __ballot_sync(0xffffffffu, j < pe && (v & smask) == 0u);
+                while (first) {
+                    const int src = __ffs(first) - 1;
+                    first &= first - 1u;
+                    const int64_t i = (int64_t)(__shfl_sync(0xffffffffu, v, src) >> Sl);
+                    const int xlo = fp[6 * i], xhi = fp[6 * i + 1], ylo = fp[6 * i + 2];
+                    const int yhi = fp[6 * i + 3], zlo = fp[6 * i + 4], zhi = fp[6 * i + 5];
+                    const GRec r = rec[i];
+                    float S0 = 0.f, Sx = 0.f, Sy = 0.f, Sz = 0.f, S2 = 0.f;
+                    if (xhi - xlo == 16 && yhi - ylo == 16 && zhi - zlo == 16) {
+                        BtWarp& W = wt[warp];
+                        __syncwarp();
+                        if (lane < 17) {
+                            const float ry = (float)(ylo + lane - r.fy) - r.dy;
+                            const float ey = exp2f(-r.inv2 * ry * ry);
+                            W.ey[lane] = make_float4(ey, ey * ry, ey * ry * ry, 0.f);
+                        }
+                        __syncwarp();
+                        // lanes: column parity hf x slice zl (slices 0..15 of the box,
+                        // column pairs k: column 2k + hf); the 17th slice with lanes
+                        // over columns.  Ring offsets (floats) for row ylo; a row adds
+                        // 512 (the 64-byte swizzle depends on x only).
+                        const int hf = lane >> 4, zl = lane & 15;
+                        const int xr = xlo - 16 * tx, yr = ylo - 16 * ty;
+                        auto soff = [&](int colr, int za) {
+                            const int rr = yr * 32 + xr + colr, zz = za & 15;
+                            return ((za >> 4) % 3) * BT_SLAB + rr * 16 +
+                                   (((zz >> 2) ^ ((rr >> 1) & 3)) << 2) + (zz & 3);
+                        };
+                        int off[9];
+#pragma unroll
+                        for (int k = 0; k < 9; ++k) off[k] = soff(min(2 * k + hf, 16), zlo + zl);
+                        const int pl = lane < 17 ? lane : 16;
+                        const int offp = soff(pl, zlo + 16);
+                        const float rz = (float)(zlo + zl + zoff - r.fz) - r.dz;
+                        const float ez = exp2f(-r.inv2 * rz * rz);
+                        const float rz16 = (float)(zlo + 16 + zoff - r.fz) - r.dz;
+                        const float ez16 = exp2f(-r.inv2 * rz16 * rz16);
+                        float2 wx01[9];
+                        float wx2[9];
+#pragma unroll
+                        for (int k = 0; k < 9; ++k) {
+                            const float rx = (float)(xlo + 2 * k + hf - r.fx) - r.dx;
+                            const float ex = (k < 8 || !hf) ? exp2f(-r.inv2 * rx * rx) : 0.f;
+                            wx01[k] = make_float2(ex, ex * rx);
+                            wx2[k] = ex * rx * rx;
+                        }
+                        const float rxp = (float)(xlo + lane - r.fx) - r.dx;
+                        const float exq = lane < 17 ? exp2f(-r.inv2 * rxp * rxp) : 0.f;
+                        float A0 = 0.f, Ax = 0.f, Ay = 0.f, Ar = 0.f, P0 = 0.f, P1 = 0.f, P2 = 0.f;
+#pragma unroll
+                        for (int yi = 0; yi < 17; ++yi) {
+                            float2 C01 = make_float2(0.f, 0.f);
+                            float C2 = 0.f;
+#pragma unroll
+                            for (int k = 0; k < 9; ++k) {
+                                const float uu = slab[off[k] + 512 * yi];
+                                C01 = ffma2(make_float2(uu, uu), wx01[k], C01);
+                                C2 = fmaf(wx2[k], uu, C2);
+                            }
+                            const float pu = slab[offp + 512 * yi];
+                            const float4 t = W.ey[yi];
+                            A0 = fmaf(t.x, C01.x, A0);
+                            Ax = fmaf(t.x, C01.y, Ax);
+                            Ay = fmaf(t.y, C01.x, Ay);
+                            Ar = fmaf(t.x, C2, fmaf(t.z, C01.x, Ar));
+                            P0 = fmaf(t.x, pu, P0);
+                            P1 = fmaf(t.y, pu, P1);
+                            P2 = fmaf(t.z, pu, P2);
+                        }
+                        A0 += __shfl_xor_sync(0xffffffffu, A0, 16);
+                        Ax += __shfl_xor_sync(0xffffffffu, Ax, 16);
+                        Ay += __shfl_xor_sync(0xffffffffu, Ay, 16);
+                        Ar += __shfl_xor_sync(0xffffffffu, Ar, 16);
+                        const float eh = hf ? 0.f : ez;
+                        S0 = eh * A0;
+                        Sx = eh * Ax;
+                        Sy = eh * Ay;
+                        Sz = eh * rz * A0;
+                        S2 = eh * fmaf(rz * rz, A0, Ar);
+                        const float Q0 = exq * P0, Qx = exq * rxp * P0, Qy = exq * P1;
+                        const float Qr = fmaf(exq * rxp * rxp, P0, exq * P2);
+                        S0 = fmaf(ez16, Q0, S0);
+                        Sx = fmaf(ez16, Qx, Sx);
+                        Sy = fmaf(ez16, Qy, Sy);
+                        Sz = fmaf(ez16 * rz16, Q0, Sz);
+                        S2 = fmaf(ez16, fmaf(rz16 * rz16, Q0, Qr), S2);
+                    } else {
+                        bwd_moments17<false>(r, xlo, xhi - xlo + 1, ylo, yhi - ylo + 1, zlo,
+                                             zhi - zlo + 1, w, c, zoff, up, S0, Sx, Sy, Sz, S2);
+                    }
+                    S0 = warp_sum(S0);
+                    Sx = warp_sum(Sx);
+                    Sy = warp_sum(Sy);
+                    Sz = warp_sum(Sz);
+                    S2 = warp_sum(S2);
+                    if (lane == 0) {   // chain rule in f64 (fvr.py:227-273)
+                        const double amp = P[4 * n + i], sg = P[3 * n + i];
+                        const double inv_s2 = 1.0 / (sg * sg), inv_s3 = inv_s2 / sg;
+                        const double k2 = amp * inv_s2;
+                        const double gx = k2 * Sx, gy = k2 * Sy, gz = k2 * Sz;
+                        G[i] = gx;
+                        G[n + i] = gy;
+                        G[2 * n + i] = gz;
+                        G[3 * n + i] = amp * inv_s3 * S2;
+                        G[4 * n + i] = S0;
+                        if (accum) accum[i] += sqrt(gx * gx + gy * gy + gz * gz);
+                    }
+                }
+            }
+        }
+    }
+    __syncthreads();
+    // drain: a prefetched slab nobody waited for must land before the CTA exits
+    if (ld0) tc::mbar_wait(reinterpret_cast<uint64_t*>(&sbar[0]), (ld0 - 1u) & 1u);
+    if (ld1) tc::mbar_wait(reinterpret_cast<uint64_t*>(&sbar[1]), (ld1 - 1u) & 1u);
+    if (ld2) tc::mbar_wait(reinterpret_cast<uint64_t*>(&sbar[2]), (ld2 - 1u) & 1u);
+}
+
 __global__ void k_grad_norm_accum(const double* __restrict__ G, int64_t n,
                                   double* __restrict__ accum, const int* halt) {
     if (halted(halt)) return;
@@ -2064,7 +2303,30 @@ int splatct_fvr_backward(const double* params, int64_t n, int w, int h, int c, i
     cudaStream_t s = as_stream(stream);
     const unsigned grid = (unsigned)((n + BG_WARPS - 1) / BG_WARPS);
     const bool fast = 2 * hx + 1 <= 17 && 2 * hz + 1 <= 17;
-    const char* kern = getenv("SPLATCT_BWD_KERNEL");   // "sp": the spatially ordered kernel
+    const char* kern = getenv("SPLATCT_BWD_KERNEL");   // "warp" / "sp": the other kernels
+    if (fast && 2 * hy + 1 <= 17 && kern && !strcmp(kern, "ts")) {
+        CUtensorMap smap;
+        if (volume_tensor_map(&smap, up_yxz, w, h, c, 16, 32, 32, true)) {   // 64 B swizzle
+            // unlisted Gaussians (footprint outside the volume) are never visited
+            SPLATCT_CK(cudaMemsetAsync(grads, 0, sizeof(double) * 5 * (size_t)n, s));
+            unsigned int* counter = at<uint32_t>(ws, L.o_tcount) + 1;
+            SPLATCT_CK(cudaMemsetAsync(counter, 0, sizeof(unsigned int), s));
+            int dev = 0, nsm = 148;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+            const size_t dyn = 3 * (size_t)BT_SLAB_BYTES;
+            cudaFuncSetAttribute(k_fvr_bwd_ts, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+            const size_t vs = L.final_buf ? L.o_v1 : L.o_v0;    // sorted values
+            SPLATCT_CK(launch_pdl(k_fvr_bwd_ts, dim3(nsm), dim3(32 * BT_WARPS), dyn, s, params, n,
+                                  (const uint32_t*)at<uint32_t>(ws, vs),
+                                  (const uint32_t*)at<uint32_t>(ws, L.o_tstart), L.ntx, L.nty,
+                                  L.ntz, L.Sl, (const int32_t*)at<int32_t>(ws, L.o_fp),
+                                  (const GRec*)at<GRec>(ws, L.o_rec), w, h, c, z0, up_yxz, smap,
+                                  counter, grads, accum, halt));
+            SPLATCT_LAUNCH_CK();
+            return SPLATCT_OK;
+        }
+    }
     if (fast && kern && !strcmp(kern, "sp")) {
         // spatially ordered persistent kernel; Gaussians with no pair (footprint
         // outside the volume) are never visited: their gradients are zero

@@ -49,6 +49,14 @@ UPDATE_TOL = 5e-3
 # that update noise (d_mu is the most position-sensitive: 2.2e-4 measured at
 # iteration 4), so only the first iteration's gradients are held to GRAD_TOL.
 LATE_GRAD_TOL = 1e-3
+# The L1 and TV terms are sign subgradients (loss.py:64-74, 183-207): a voxel
+# pair (or detector bin) at a near-tie flips sign under fp32 rounding of the
+# volume.  On the Shepp-Logan pin problem a 2e-7 relative perturbation of the
+# reference's own volume flips 8 of 16.7 M TV entries and moves the TV part of
+# d_mu by 1.2e-4 (tools/grad_diag.py), so d_mu of those
+# terms is held to SIGN_TERM_TOL; the SSIM term is continuous and is held to
+# 1e-5 (test_first_gradient_terms_vs_oracle), d_sigma and d_I to GRAD_TOL.
+SIGN_TERM_TOL = 5e-4
 
 
 @pytest.fixture(scope="module")
@@ -180,9 +188,38 @@ def test_reference_c2_c3_pins(pins, views):
     optim.run_reconstruction(meas, geom, s1, init_cloud=init)
     (tr,) = optim._TRAINER_CACHE.values()
     gd = tr.grads.cpu().numpy()
-    assert rel_l2(gd[0:3].T, g[pre + "first_d_mu"]) < GRAD_TOL
+    assert rel_l2(gd[0:3].T, g[pre + "first_d_mu"]) < SIGN_TERM_TOL
     assert rel_l2(gd[3], g[pre + "first_d_sigma"]) < GRAD_TOL
     assert rel_l2(gd[4], g[pre + "first_d_intensity"]) < GRAD_TOL
+
+
+@pytest.mark.parametrize("lam,tol", [((0.0, 1.0, 0.0), 1e-5), ((1.0, 0.0, 0.0), SIGN_TERM_TOL),
+                                     ((0.0, 0.0, 1.0), SIGN_TERM_TOL)])
+def test_first_gradient_terms_vs_oracle(pins, lam, tol):
+    """Per loss term, the first-iteration gradients of the device step on the
+    reference's C2 pin problem against the oracle (itself equal to the
+    reference's stored gradient to 2.5e-8): the continuous SSIM term to 1e-5,
+    the sign-subgradient terms to SIGN_TERM_TOL."""
+    g = pins
+    dims = (256, 256, 256)
+    truth = phantom.shepp_logan_3d(*dims)
+    og = O.Geometry.fan(50, 512, 1.6, 512.0, 512.0)
+    geom = core.ScanGeometry.fan(50, 512, 1.6, 512.0, 512.0)
+    box = core.BoxConfig.for_dims(17, dims)
+    mu, sg, it = g["c2p50_init_mu"], g["c2p50_init_sigma"], g["c2p50_init_intensity"]
+    meas = O.project_forward(truth.zyx, og)
+    v = O.splat_fwd(mu, sg, it, box.shape, dims)
+    _, gp, gv, _ = O.total_loss_detailed(O.project_forward(v, og), meas, v, lam)
+    dl = O.project_adjoint(gp.astype(np.float32), og, dims).astype(np.float64) + gv
+    dm, ds, di, _, _ = O.splat_bwd(mu, sg, it, box.shape, dims, dl.astype(np.float32))
+    dev = D.require_cuda()
+    tr = Trainer(torch.from_numpy(meas).to(dev), geom, dims, box, loss.LossWeights(*lam),
+                 D.cloud_to_params(core.GaussianCloud(mu, sg, it), dev), max_iters=4, trace_cap=2)
+    tr.initial_volume()
+    tr.iteration()
+    gd = tr.grads.cpu().numpy()
+    assert rel_l2(gd[0:3].T, dm) < tol
+    assert rel_l2(gd[3], ds) < max(tol, 1e-5) and rel_l2(gd[4], di) < max(tol, 1e-5)
     z = vol.zyx.astype(np.float64)
     assert rel_l2(vol.zyx.reshape(-1)[vidx], g[pre + "vol_samples"]) < VOL_TOL
     assert abs(np.linalg.norm(z) - float(g[pre + "vol_norm"])) < VOL_TOL * float(g[pre + "vol_norm"])

@@ -133,15 +133,17 @@ def test_deep_volume_has_no_occupancy_mask():
 
 # backward kernel variants: the spatially ordered persistent kernel (default),
 # and the per-Gaussian-warp kernel with TMA-fed rows or direct loads
-BWD_VARIANTS = {"sp": {"SPLATCT_BWD_KERNEL": "sp"}, "warp_tma": {"SPLATCT_BWD_KERNEL": "warp"},
-                "warp_direct": {"SPLATCT_BWD_KERNEL": "warp", "SPLATCT_BWD_NO_TMA": "1"}}
+BWD_VARIANTS = {"ts": {"SPLATCT_BWD_KERNEL": "ts"}, "sp": {"SPLATCT_BWD_KERNEL": "sp"},
+                "warp_tma": {},
+                "warp_direct": {"SPLATCT_BWD_NO_TMA": "1"}}
 
 
 @pytest.mark.parametrize("dims", [(40, 36, 32), (6, 5, 8), (64, 48, 256)])
 def test_backward_variants_agree(dims, monkeypatch):
-    """The three backward kernels (TMA boxes zero-filled at tiny volumes; the
-    ordered kernel's branch-free full-box path at c = 256) sum the same terms
-    in different orders: equal to fp32 rounding, and each run-to-run bitwise."""
+    """The backward kernels (tile-staged default, ordered, per-Gaussian warp with
+    TMA rows or direct loads; TMA boxes zero-filled at tiny volumes; the
+    full-box paths at c = 256) sum the same terms in different orders: equal
+    to fp32 rounding, and each run-to-run bitwise."""
     rng = np.random.default_rng(9)
     box = core.BoxConfig.for_dims(17, dims)
     n = 1500
@@ -150,7 +152,7 @@ def test_backward_variants_agree(dims, monkeypatch):
     up = core.VolumeGrid.from_zyx(rng.standard_normal(dims[::-1]).astype(np.float32))
     out = {}
     for name, env in BWD_VARIANTS.items():
-        for k in ("SPLATCT_BWD_KERNEL", "SPLATCT_BWD_NO_TMA"):
+        for k in ("SPLATCT_BWD_KERNEL", "SPLATCT_BWD_NO_TMA", "SPLATCT_NO_TMA"):
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)
@@ -158,11 +160,11 @@ def test_backward_variants_agree(dims, monkeypatch):
         again = fvr.backward(cloud, box, dims, up)
         np.testing.assert_array_equal(out[name].d_mu, again.d_mu)
         np.testing.assert_array_equal(out[name].d_sigma, again.d_sigma)
-    a = out["sp"]
+    a = out["warp_tma"]
     dm, ds, di, acc, _ = O.splat_bwd(mu, cloud.sigma, cloud.intensity, box.shape, dims, up.zyx)
     assert rel_l2(a.d_mu, dm) < GRAD_TOL and rel_l2(a.d_sigma, ds) < GRAD_TOL
     assert rel_l2(a.d_intensity, di) < GRAD_TOL
-    for b in (out["warp_tma"], out["warp_direct"]):
+    for b in (out["ts"], out["sp"], out["warp_direct"]):
         for x, y in ((a.d_mu, b.d_mu), (a.d_sigma, b.d_sigma), (a.d_intensity, b.d_intensity),
                      (a.accum_pos_grad_norm, b.accum_pos_grad_norm)):
             assert rel_l2(x, y) < 1e-6

@@ -1,0 +1,10 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 120 python tools/vox_c2.py --check
+timeout 120 python tools/vox_c2.py --config c4
+SPLATCT_BWD_KERNEL=warp timeout 120 python tools/vox_c2.py --config c4
+timeout 900 python -m pytest tests/test_gpu_edges.py tests/test_gpu_parity.py tests/test_gpu_fullsize.py tests/test_gpu_c2_parity.py tests/test_gpu_sharded.py -m gpu -q --timeout 600 -p no:cacheprovider -rA > gpurun_out/pytest_new.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_new.log
+grep -E "^(FAILED|ERROR)|passed|failed" gpurun_out/pytest_new.log | head -20
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_fvr_bwd_ts" -c 1 -o gpurun_out/bts_full python tools/vox_c2.py --reps 1 > gpurun_out/ncu_bts.log 2>&1; echo "ncu rc=$?"
+python tools/ncu_full_summary.py gpurun_out/bts_full.ncu-rep 2>&1 | tail -3
+python tools/ncu_lines.py gpurun_out/bts_full.ncu-rep k_fvr_bwd_ts 16
