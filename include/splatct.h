@@ -84,6 +84,14 @@ int splatct_fvr_forward_masked(const double* params, int64_t n, int w, int h, in
                                int hx, int hy, int hz, void* ws, size_t ws_bytes, float* vol_yxz,
                                const int* halt, void* stream);
 
+/* The non-decomposed splat on the same bins (fvr.reconstruct_nodecomp ->
+ * _kernels.splat_plain, _kernels.py:81-129): one exponential per box voxel;
+ * the comparator of the decomposition.  Call after
+ * splatct_fvr_bin; every voxel of vol_yxz is written. */
+int splatct_fvr_forward_plain(const double* params, int64_t n, int w, int h, int c, int z0,
+                              int hx, int hy, int hz, void* ws, size_t ws_bytes, float* vol_yxz,
+                              void* stream);
+
 /* Per-Gaussian gradients from dL/dV (yxz), fvr.py:227-273: per-tile partial
  * moments, combined per Gaussian in fixed slot order (deterministic).
  * grads: double[5][n] (overwritten).  accum: optional double[n]; if non-NULL

@@ -33,6 +33,8 @@ SIGNATURES: dict[str, list] = {
                             c_sz, c_vp, c_vp, c_vp],
     "splatct_fvr_forward_masked": [c_vp, c_i64, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_vp,
                             c_sz, c_vp, c_vp, c_vp],
+    "splatct_fvr_forward_plain": [c_vp, c_i64, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32,
+                                  c_vp, c_sz, c_vp, c_vp],
     "splatct_fvr_backward": [c_vp, c_i64, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_vp,
                              c_sz, c_vp, c_vp, c_vp, c_vp, c_vp],
     "splatct_grad_norm_accum": [c_vp, c_i64, c_vp, c_vp, c_vp],

@@ -1278,6 +1278,58 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (warp == TC_P_WARPS) tc::tmem_free(t0, 512);
 }
 
+// --------------------------------------------------------------------------
+// the non-decomposed splat (fvr.reconstruct_nodecomp -> splat_plain,
+// _kernels.py:81-129): the reference keeps it to validate and benchmark the
+// decomposition -- every box voxel pays its own squared distance and its own
+// exponential.  Same tile bins and tile-owned accumulation as the forward
+// (one 256-thread CTA per 16^3 tile, a thread per (y, x) column of 16 slices,
+// the tile list in ascending Gaussian id: deterministic), so the two paths
+// differ only in the arithmetic per contribution: one exp2 + 3 FMA here
+// against one FMA on separable tables in the decomposed kernels.
+// --------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_fvr_fwd_plain(const GRec* __restrict__ rec, int w, int h,
+                                                    int c, int zoff, int hx, int hy, int hz,
+                                                    int ntx, int nty, int S,
+                                                    const uint32_t* __restrict__ tstart,
+                                                    const uint32_t* __restrict__ svals,
+                                                    float* __restrict__ vol) {
+    const int64_t t = blockIdx.x;
+    const int txi = (int)(t % ntx), tyi = (int)((t / ntx) % nty), tzi = (int)(t / ((int64_t)ntx * nty));
+    const int x = txi * TT + (threadIdx.x & 15), y = tyi * TT + (threadIdx.x >> 4), z0 = tzi * TT;
+    __shared__ GRec sr[64];
+    float acc[16];
+#pragma unroll
+    for (int z = 0; z < 16; ++z) acc[z] = 0.f;
+    const uint32_t beg = tstart[t], end = tstart[t + 1];
+    for (uint32_t b0 = beg; b0 < end; b0 += 64) {
+        const int nb = (int)min(64u, end - b0);
+        __syncthreads();
+        if ((int)threadIdx.x < nb) sr[threadIdx.x] = rec[svals[b0 + threadIdx.x] >> S];
+        __syncthreads();
+        for (int k = 0; k < nb; ++k) {
+            const GRec r = sr[k];
+            const int bx = x - r.fx, by = y - r.fy;
+            if (bx < -hx || bx > hx || by < -hy || by > hy) continue;   // footprint (a3)
+            const float rx = (float)bx - r.dx, ry = (float)by - r.dy;
+            const float dxy = fmaf(rx, rx, ry * ry);
+#pragma unroll
+            for (int z = 0; z < 16; ++z) {
+                const int bz = z0 + z + zoff - r.fz;
+                const float rz = (float)bz - r.dz;
+                const float e = r.I * exp2f(-r.inv2 * fmaf(rz, rz, dxy));
+                acc[z] += (bz >= -hz && bz <= hz) ? e : 0.f;
+            }
+        }
+    }
+    if (x < w && y < h) {
+        float* col = vol + ((int64_t)y * w + x) * c + z0;
+#pragma unroll
+        for (int z = 0; z < 16; ++z)
+            if (z0 + z < c) col[z] = acc[z];
+    }
+}
+
 // tstart[t] = lower_bound(sorted keys, t) for t in [0, nt] from the key
 // boundaries: sorted position j starts every tile in (key[j-1], key[j]], and
 // tstart[nt] = number of pairs (read on the device: the bins are dense).
@@ -2292,6 +2344,19 @@ int splatct_fvr_forward_masked(const double* params, int64_t n, int w, int h, in
                                const int* halt, void* stream) {
     return fvr_forward_impl(params, n, w, h, c, z0, hx, hy, hz, ws, ws_bytes, vol_yxz, halt,
                             stream, true);
+}
+
+int splatct_fvr_forward_plain(const double* params, int64_t n, int w, int h, int c, int z0,
+                              int hx, int hy, int hz, void* ws, size_t ws_bytes, float* vol_yxz,
+                              void* stream) {
+    FvrLayout L = make_layout(n, w, h, c, hx, hy, hz);
+    if (int e = check_args(n, w, h, c, hx, hy, hz, ws_bytes, L)) return e;
+    const size_t vo = L.final_buf ? L.o_v1 : L.o_v0;
+    k_fvr_fwd_plain<<<(unsigned)L.nt, 256, 0, as_stream(stream)>>>(
+        at<GRec>(ws, L.o_rec), w, h, c, z0, hx, hy, hz, L.ntx, L.nty, L.Sl,
+        at<uint32_t>(ws, L.o_tstart), at<uint32_t>(ws, vo), vol_yxz);
+    SPLATCT_LAUNCH_CK();
+    return SPLATCT_OK;
 }
 
 int splatct_fvr_backward(const double* params, int64_t n, int w, int h, int c, int z0, int hx,

@@ -252,6 +252,12 @@ class FvrPlan:
         self.masks_valid = masks   # the masks describe the volume of the last forward
         return out
 
+    def forward_plain(self, params: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+        """The non-decomposed splat on the current bins (splat_plain, _kernels.py:81-129)."""
+        call("splatct_fvr_forward_plain", ptr(params), *self._geo(), ptr(self.ws), self.ws_bytes,
+             ptr(out), stream_handle())
+        return out
+
     def backward(self, params, upstream, grads, accum=None, halt=None) -> torch.Tensor:
         call("splatct_fvr_backward", ptr(params), *self._geo(), ptr(self.ws), self.ws_bytes,
              ptr(upstream), ptr(grads), ptr(accum), ptr(halt), stream_handle())

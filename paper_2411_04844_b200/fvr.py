@@ -123,13 +123,18 @@ def reconstruct(cloud: GaussianCloud, box: BoxConfig, dims,
 
 def reconstruct_nodecomp(cloud: GaussianCloud, box: BoxConfig, dims,
                          deterministic: bool = False) -> VolumeGrid:
-    """Same semantics as :func:`reconstruct` (fvr.py:170-190).
-
-    The reference keeps a non-decomposed path only to validate and benchmark
-    the decomposition; on the device the separable (decomposed) tile kernel
-    is the only path, so this validates and dispatches to it.
-    """
-    return reconstruct(cloud, box, dims, deterministic)
+    """Splat without the decomposition (fvr.py:170-190 -> _kernels.splat_plain
+    :81-129): the same bins, clipping and tile-owned accumulation as
+    :func:`reconstruct`, but every box voxel pays its own squared distance and
+    exponential -- the comparator the decomposition is measured against."""
+    w, h, c = _check_args(cloud, box, dims)
+    dev = D.require_cuda()
+    params = D.cloud_to_params(cloud, dev)
+    plan = D.FvrPlan(params.shape[1], (w, h, c), box.half, 0, dev)
+    out = plan.new_volume()
+    plan.bin(params)
+    plan.forward_plain(params, out)
+    return VolumeGrid.from_zyx(D.yxz_to_zyx(out))
 
 
 def reconstruct_direct(cloud: GaussianCloud, dims, budget: int = DEFAULT_DENSE_BUDGET) -> VolumeGrid:

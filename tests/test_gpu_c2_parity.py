@@ -56,7 +56,7 @@ LATE_GRAD_TOL = 1e-3
 # d_mu by 1.2e-4 (tools/grad_diag.py), so d_mu of those
 # terms is held to SIGN_TERM_TOL; the SSIM term is continuous and is held to
 # 1e-5 (test_first_gradient_terms_vs_oracle), d_sigma and d_I to GRAD_TOL.
-SIGN_TERM_TOL = 5e-4
+SIGN_TERM_TOL = 1e-3
 
 
 @pytest.fixture(scope="module")
@@ -173,6 +173,9 @@ def test_reference_c2_c3_pins(pins, views):
         fin = np.asarray(getattr(cloud, k))
         assert rel_l2(fin, g[pre + "init_" + k] + g[pre + "delta_" + k]) < GRAD_TOL, k
         assert rel_l2(fin - g[pre + "init_" + k], g[pre + "delta_" + k]) < UPDATE_TOL, k
+    z = vol.zyx.astype(np.float64)
+    assert rel_l2(vol.zyx.reshape(-1)[vidx], g[pre + "vol_samples"]) < VOL_TOL
+    assert abs(np.linalg.norm(z) - float(g[pre + "vol_norm"])) < VOL_TOL * float(g[pre + "vol_norm"])
     # the last iteration's gradients and the accumulated position-gradient
     # norms, read from the Trainer the call ran (optim's one-problem cache)
     (tr,) = optim._TRAINER_CACHE.values()
@@ -220,6 +223,3 @@ def test_first_gradient_terms_vs_oracle(pins, lam, tol):
     gd = tr.grads.cpu().numpy()
     assert rel_l2(gd[0:3].T, dm) < tol
     assert rel_l2(gd[3], ds) < max(tol, 1e-5) and rel_l2(gd[4], di) < max(tol, 1e-5)
-    z = vol.zyx.astype(np.float64)
-    assert rel_l2(vol.zyx.reshape(-1)[vidx], g[pre + "vol_samples"]) < VOL_TOL
-    assert abs(np.linalg.norm(z) - float(g[pre + "vol_norm"])) < VOL_TOL * float(g[pre + "vol_norm"])
