@@ -1587,6 +1587,130 @@ __device__ __forceinline__ void bwd_moments17_tma(const GRec& r, int xlo, int nx
     S2 = fmaf(ez16, fmaf(rz16 * rz16, Q0, Qr), S2);
 }
 
+// The same moments for a full 17 x 17 x 17 box (every interior Gaussian), with
+// the row loop unrolled: two box rows per TMA load ({20 z, 17 x, 2 y}, 3-slot
+// ring: up to 6 rows in flight, half the issues and barrier waits), the row
+// weights {ey, ey ry, ey ry^2} from a per-warp table, and no per-element
+// selects -- the 18th column (k = 8 of the odd half) and the lanes past the
+// 17th column re-read column 16 (inside the footprint, finite) against a zero
+// weight.  Row 17 of the last load is never read.
+constexpr int BT2_RING = 3;
+constexpr int BT2_SLOT = 2816;                      // 2 x 17 x 20 x 4 B = 2720, rounded to 128 B
+constexpr unsigned BT2_BYTES = 2u * 17u * BT_ZB * 4u;
+
+__device__ __forceinline__ void bwd_moments17_tma_full(const GRec& r, int xlo, int ylo, int zlo,
+                                                       int zoff, const CUtensorMap* tmap2,
+                                                       float* ring, unsigned long long* bars,
+                                                       float4* ytab, float& S0, float& Sx,
+                                                       float& Sy, float& Sz, float& S2) {
+    const int lane = threadIdx.x & 31, hf = lane >> 4, zl = lane & 15;
+    const unsigned ring_s = (unsigned)__cvta_generic_to_shared(ring);
+    const unsigned bar_s = (unsigned)__cvta_generic_to_shared(bars);
+    auto issue = [&](int bi) {   // lane 0: rows 2 bi, 2 bi + 1
+        const int q = bi % BT2_RING;
+        const unsigned b = bar_s + 8 * q, dst = ring_s + BT2_SLOT * q;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(b),
+                     "r"(BT2_BYTES)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
+            "[%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(dst),
+            "l"(tmap2), "r"(zlo & ~3), "r"(xlo), "r"(ylo + 2 * bi), "r"(b)
+            : "memory");
+    };
+    if (lane == 0) {
+        issue(0);
+        issue(1);
+        issue(2);
+    }
+    const float rz = (float)(zlo + zl + zoff - r.fz) - r.dz;
+    const float ez = exp2f(-r.inv2 * rz * rz);
+    const float rz16 = (float)(zlo + 16 + zoff - r.fz) - r.dz;
+    const float ez16 = exp2f(-r.inv2 * rz16 * rz16);
+    float2 wx01[9];
+    float wx2[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+        const int col = tcol(k, k < 8 ? hf : 0);
+        const float rx = (float)(xlo + col - r.fx) - r.dx;
+        const float ex = (k < 8 || !hf) ? exp2f(-r.inv2 * rx * rx) : 0.f;
+        wx01[k] = make_float2(ex, ex * rx);
+        wx2[k] = ex * rx * rx;
+    }
+    const int pl = lane < 17 ? lane : 16;
+    const float rxp = (float)(xlo + lane - r.fx) - r.dx;
+    const float exq = lane < 17 ? exp2f(-r.inv2 * rxp * rxp) : 0.f;
+    if (lane < 17) {
+        const float ry = (float)(ylo + lane - r.fy) - r.dy;
+        const float ey = exp2f(-r.inv2 * ry * ry);
+        ytab[lane] = make_float4(ey, ey * ry, ey * ry * ry, 0.f);
+    }
+    int off[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) off[k] = tcol(k, k < 8 ? hf : 0) * BT_ZB + zl + (zlo & 3);
+    const int offp = pl * BT_ZB + 16 + (zlo & 3);
+    float A0 = 0.f, Ax = 0.f, Ay = 0.f, Ar = 0.f, P0 = 0.f, P1 = 0.f, P2 = 0.f;
+#pragma unroll
+    for (int bi = 0; bi < 9; ++bi) {
+        __syncwarp();   // every lane is done with box bi - 1's slot (refilled next); ytab visible
+        if (lane == 0 && bi >= 1 && bi + 2 <= 8) issue(bi + 2);
+        const int q = bi % BT2_RING;
+        {
+            const unsigned parity = (unsigned)(bi / BT2_RING) & 1u;
+            unsigned done = 0;
+            do {
+                asm volatile(
+                    "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                    " selp.u32 %0, 1, 0, p;\n}\n"
+                    : "=r"(done)
+                    : "r"(bar_s + 8 * q), "r"(parity)
+                    : "memory");
+            } while (!done);
+        }
+        const float* src = ring + (BT2_SLOT / 4) * q;
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+            const int yi = 2 * bi + rr;
+            if (yi > 16) break;
+            const float* rs = src + rr * (17 * BT_ZB);
+            float2 C01 = make_float2(0.f, 0.f);
+            float C2 = 0.f;
+#pragma unroll
+            for (int k = 0; k < 9; ++k) {
+                const float u = rs[off[k]];
+                C01 = ffma2(make_float2(u, u), wx01[k], C01);
+                C2 = fmaf(wx2[k], u, C2);
+            }
+            const float pu = rs[offp];
+            const float4 t = ytab[yi];
+            A0 = fmaf(t.x, C01.x, A0);
+            Ax = fmaf(t.x, C01.y, Ax);
+            Ay = fmaf(t.y, C01.x, Ay);
+            Ar = fmaf(t.x, C2, fmaf(t.z, C01.x, Ar));
+            P0 = fmaf(t.x, pu, P0);
+            P1 = fmaf(t.y, pu, P1);
+            P2 = fmaf(t.z, pu, P2);
+        }
+    }
+    A0 += __shfl_xor_sync(0xffffffffu, A0, 16);
+    Ax += __shfl_xor_sync(0xffffffffu, Ax, 16);
+    Ay += __shfl_xor_sync(0xffffffffu, Ay, 16);
+    Ar += __shfl_xor_sync(0xffffffffu, Ar, 16);
+    const float eh = hf ? 0.f : ez;
+    S0 = eh * A0;
+    Sx = eh * Ax;
+    Sy = eh * Ay;
+    Sz = eh * rz * A0;
+    S2 = eh * fmaf(rz * rz, A0, Ar);
+    const float Q0 = exq * P0, Qx = exq * rxp * P0, Qy = exq * P1;
+    const float Qr = fmaf(exq * rxp * rxp, P0, exq * P2);
+    S0 = fmaf(ez16, Q0, S0);
+    Sx = fmaf(ez16, Qx, Sx);
+    Sy = fmaf(ez16, Qy, Sy);
+    Sz = fmaf(ez16 * rz16, Q0, Sz);
+    S2 = fmaf(ez16, fmaf(rz16 * rz16, Q0, Qr), S2);
+}
+
 // flags[j] = 1 for the sorted pair that is its Gaussian's first tile (slot 0)
 __global__ void k_first_flags(const uint32_t* __restrict__ svals, const uint32_t* __restrict__ tstart,
                               int64_t nt, int64_t np, int S, uint32_t* __restrict__ flags) {
@@ -1619,10 +1743,15 @@ __global__ void __launch_bounds__(32 * BG_WARPS, FAST ? 6 : 4) k_fvr_bwd(const d
                                                           double* __restrict__ G,
                                                           double* __restrict__ accum,
                                                           const __grid_constant__ CUtensorMap utmap,
+                                                          const __grid_constant__ CUtensorMap utmap2,
                                                           int use_tma, const int* halt) {
     griddep_wait();
     if (halted(halt)) return;
-    __shared__ __align__(128) float bring[FAST ? BG_WARPS : 1][FAST ? BT_RING * BT_SLOT / 4 : 1];
+    // per warp: the 1-row ring (general boxes) or the 2-row ring (full boxes)
+    constexpr int RING_FL = (BT_RING * BT_SLOT > BT2_RING * BT2_SLOT ? BT_RING * BT_SLOT
+                                                                      : BT2_RING * BT2_SLOT) / 4;
+    __shared__ __align__(128) float bring[FAST ? BG_WARPS : 1][FAST ? RING_FL : 1];
+    __shared__ float4 ytab[FAST ? BG_WARPS : 1][17];
     __shared__ __align__(8) unsigned long long bbar[BG_WARPS][BT_RING];
     __shared__ float xt[3][BG_WARPS][32];   // ex, ex rx, ex rx^2
     __shared__ float2 yt[BG_WARPS][32];   // {ey, ry}
@@ -1644,7 +1773,10 @@ __global__ void __launch_bounds__(32 * BG_WARPS, FAST ? 6 : 4) k_fvr_bwd(const d
     if (FAST || (xlo <= xhi && ylo <= yhi && zlo <= zhi && xhi - xlo < 17 && zhi - zlo < 17)) {
         if (xlo <= xhi && ylo <= yhi && zlo <= zhi) {
             const GRec r = rec[i];
-            if (FAST && use_tma)
+            if (FAST && use_tma && xhi - xlo == 16 && yhi - ylo == 16 && zhi - zlo == 16)
+                bwd_moments17_tma_full(r, xlo, ylo, zlo, zoff, &utmap2, bring[FAST ? wid : 0],
+                                       bbar[wid], ytab[FAST ? wid : 0], S0, Sx, Sy, Sz, S2);
+            else if (FAST && use_tma)
                 bwd_moments17_tma(r, xlo, xhi - xlo + 1, ylo, yhi - ylo + 1, zlo, zhi - zlo + 1,
                                   zoff, &utmap, bring[FAST ? wid : 0], bbar[wid], S0, Sx, Sy, Sz,
                                   S2);
@@ -2436,18 +2568,22 @@ int splatct_fvr_backward(const double* params, int64_t n, int w, int h, int c, i
         SPLATCT_LAUNCH_CK();
         SPLATCT_CK(cudaMemsetAsync(grads, 0, sizeof(double) * 5 * (size_t)n, s));   // unlisted
     }
-    CUtensorMap utmap;
+    CUtensorMap utmap, utmap2;
     int use_tma = 0;
     if (fast && !getenv("SPLATCT_BWD_NO_TMA"))
-        use_tma = volume_tensor_map(&utmap, up_yxz, w, h, c, BT_ZB, 17, 1, false) ? 1 : 0;
-    else
+        use_tma = volume_tensor_map(&utmap, up_yxz, w, h, c, BT_ZB, 17, 1, false) &&
+                          volume_tensor_map(&utmap2, up_yxz, w, h, c, BT_ZB, 17, 2, false)
+                      ? 1 : 0;
+    if (!use_tma) {
         memset(&utmap, 0, sizeof(utmap));
+        memset(&utmap2, 0, sizeof(utmap2));
+    }
     auto launch = [&](auto fast_c, auto ord_c) {
         return launch_pdl(k_fvr_bwd<decltype(fast_c)::value, decltype(ord_c)::value>,
                           dim3(grid), dim3(32 * BG_WARPS), 0, s, params, n,
                           (const uint32_t*)order, (const int32_t*)at<int32_t>(ws, L.o_fp),
                           (const GRec*)at<GRec>(ws, L.o_rec), w, h, c, z0, up_yxz, grads, accum,
-                          utmap, use_tma, halt);
+                          utmap, utmap2, use_tma, halt);
     };
     using T = std::true_type;
     using F = std::false_type;

@@ -82,7 +82,10 @@ static LossLayout loss_layout(int m, int n, int p) {
     L.nb_g11 = (int64_t)((p + 31) / 32) * ((n + R_COLS - 1) / R_COLS);
     if (L.k11) {   // row-walking kernels: full-p D, no H/T
         L.o_H = L.o_T = 0;
-        L.o_D11 = take(sizeof(double) * 3 * (size_t)L.vr * L.vc * p);
+        // the three derivative fields in f32: every statistic and the SSIM value
+        // are f64 (the cancellation is in sigma^2 = E[x^2] - mu^2, done before
+        // the store); the fields only feed the linear adjoint correlation
+        L.o_D11 = take(sizeof(float) * 3 * (size_t)L.vr * L.vc * p);
         L.o_D = L.o_D11;
         L.o_RS = take(sizeof(double) * 2 * (size_t)L.vr * L.vc * p);   // ref window stats
         L.o_ps = take(sizeof(double) * L.nb_s11);
@@ -356,7 +359,7 @@ template <int MODE>
 __global__ void __launch_bounds__(R_NT, MODE == 1 ? 2 : 1) k_ssim_stats11(const float* __restrict__ X,
                                                           const float* __restrict__ Y, int m, int n,
                                                           int p, Win W, double c1, double c2,
-                                                          int vr, int vc, double* __restrict__ D,
+                                                          int vr, int vc, float* __restrict__ D,
                                                           double* __restrict__ part,
                                                           double* __restrict__ RS,
                                                           const int* halt) {
@@ -506,9 +509,9 @@ __global__ void __launch_bounds__(R_NT, MODE == 1 ? 2 : 1) k_ssim_stats11(const 
                     const double inv = 1.0 / (b1 * b2);   // 1/b1 = b2*inv, 1/b2 = b1*inv
                     const double s = (a1 * a2) * inv;
                     ssum += s;
-                    D[o] = (2.0 * my * (a2 - a1)) * inv - 2.0 * mx * s * ((b2 - b1) * inv);
-                    D[plane + o] = -s * (b1 * inv);
-                    D[2 * plane + o] = 2.0 * a1 * inv;
+                    D[o] = (float)((2.0 * my * (a2 - a1)) * inv - 2.0 * mx * s * ((b2 - b1) * inv));
+                    D[plane + o] = (float)(-s * (b1 * inv));
+                    D[2 * plane + o] = (float)(2.0 * a1 * inv);
                 }
             }
         }
@@ -520,14 +523,14 @@ __global__ void __launch_bounds__(R_NT, MODE == 1 ? 2 : 1) k_ssim_stats11(const 
     }
 }
 
-constexpr int G_DCHUNKS = 3 * R_SPAN * 16;                   // D: 3 fields x 18 cols x 16
+constexpr int G_DCHUNKS = 3 * R_SPAN * 8;                    // D (f32): 3 fields x 17 cols x 8
 constexpr int G_DSLOTS = (G_DCHUNKS + R_NT - 1) / R_NT;
 constexpr int G_XCHUNKS = 2 * R_COLS * 8;                    // x, y: R_COLS cols x 8 chunks
 
 __global__ void __launch_bounds__(R_NT, 2) k_loss_grad11(const float* __restrict__ X,
                                                          const float* __restrict__ Y, int m, int n,
                                                          int p, Win W, int vr, int vc,
-                                                         const double* __restrict__ D, double l1w,
+                                                         const float* __restrict__ D, double l1w,
                                                          double l1_count, double ssw,
                                                          double ssim_slices, float* __restrict__ G,
                                                          double* __restrict__ part,
@@ -535,7 +538,7 @@ __global__ void __launch_bounds__(R_NT, 2) k_loss_grad11(const float* __restrict
     griddep_wait();
     if (halted(halt)) return;
     // per staged row: D columns s0-10 .. s0+7 (3 fields) and x, y columns s0 .. s0+7
-    __shared__ __align__(16) double sd[G_BUF][3][R_SPAN][32];
+    __shared__ __align__(16) float sd[G_BUF][3][R_SPAN][32];
     __shared__ __align__(16) float sxy[G_BUF][2][R_COLS][32];
     __shared__ double red[R_NT / 32];
     const int lane = threadIdx.x & 31, cl = threadIdx.x >> 5;
@@ -554,12 +557,12 @@ __global__ void __launch_bounds__(R_NT, 2) k_loss_grad11(const float* __restrict
     for (int k = 0; k < G_DSLOTS; ++k) {
         const int e = threadIdx.x + k * R_NT;
         dmine[k] = e < G_DCHUNKS;
-        const int f = e / (R_SPAN * 16), rem = e % (R_SPAN * 16);
-        const int col = rem >> 4, q = rem & 15;
+        const int f = e / (R_SPAN * 8), rem = e % (R_SPAN * 8);
+        const int col = rem >> 3, q = rem & 7;
         const int jj = s0 - 10 + col;
-        dok[k] = dmine[k] && jj >= 0 && jj < vc && zb + 2 * q < p;
-        dgo[k] = dok[k] ? f * plane + (int64_t)jj * p + zb + 2 * q : 0;
-        dso[k] = (f * R_SPAN + col) * 32 + 2 * q;
+        dok[k] = dmine[k] && jj >= 0 && jj < vc && zb + 4 * q < p;
+        dgo[k] = dok[k] ? f * plane + (int64_t)jj * p + zb + 4 * q : 0;
+        dso[k] = (f * R_SPAN + col) * 32 + 4 * q;
     }
     const bool xmine = threadIdx.x < G_XCHUNKS;
     const int xarr = threadIdx.x / (R_COLS * 8), xrem = threadIdx.x % (R_COLS * 8);
@@ -572,7 +575,7 @@ __global__ void __launch_bounds__(R_NT, 2) k_loss_grad11(const float* __restrict
         if (r < m) {
             const int buf = r % G_BUF;
             if (ss && r < vr) {
-                double* db = &sd[buf][0][0][0];
+                float* db = &sd[buf][0][0][0];
 #pragma unroll
                 for (int k = 0; k < G_DSLOTS; ++k)
                     if (dmine[k]) cp16_zfill(db + dso[k], D + (dok[k] ? r * drow + dgo[k] : 0), dok[k]);
@@ -604,7 +607,8 @@ __global__ void __launch_bounds__(R_NT, 2) k_loss_grad11(const float* __restrict
                     const double g = W.gc[b];
                     double* tb = t[b & 1];
 #pragma unroll
-                    for (int f = 0; f < 3; ++f) tb[f] = fma(g, sd[buf][f][cl + 10 - b][lane], tb[f]);
+                    for (int f = 0; f < 3; ++f)
+                        tb[f] = fma(g, (double)sd[buf][f][cl + 10 - b][lane], tb[f]);
                 }
 #pragma unroll
                 for (int f = 0; f < 3; ++f) ring[ph][f] = t[0][f] + t[1][f];
@@ -791,7 +795,7 @@ static int loss_fused_impl(const float* pred, const float* ref, int m, int n, in
     double* pl = reinterpret_cast<double*>(base + L.o_pl);
     const bool k11 = L.k11;
     if (k11) {
-        double* D11 = reinterpret_cast<double*>(base + L.o_D11);
+        float* D11 = reinterpret_cast<float*>(base + L.o_D11);
         const dim3 gs((p + 31) / 32, (L.vc + R_COLS - 1) / R_COLS),
             gg((p + 31) / 32, (n + R_COLS - 1) / R_COLS);
         if (lambda2 > 0.0) {
