@@ -223,10 +223,12 @@ def stage_profile(tr, iters):
                       float(tr.slab.c_global), tr.gpred, tr.sums, tr.halt)
         ev[2].record(s)
         lo, hi = tr.comm.halo(tr.vol)
-        tr.op.adjoint(tr.gpred, tr.dl, vol=tr.vol, halo_lo=lo, halo_hi=hi, z0=tr.slab.z0,
-                      lambda_tv=lw.lambda3, tv_count=tr.tv_count, tv_partial=tr.tv_part,
-                      halt=tr.halt, occ=tr.fvr)
+        tr.op.adjoint(tr.gpred, tr.dl, vol=tr.vol, z0=tr.slab.z0, lambda_tv=lw.lambda3,
+                      tv_count=tr.tv_count, tv_partial=tr.tv_part, halt=tr.halt, occ=tr.fvr)
         D.reduce_sum(tr.tv_part, tr.sums[2:3])
+        if tr.comm.world > 1:
+            D.tv_halo_fixup(tr.vol, tr.dl, lo, hi, lw.lambda3, tr.tv_count, tr.sums[2:3],
+                            tr.halt)
         ev[3].record(s)
         tr.comm.allreduce_sum_(tr.sums)
         D.call("splatct_iter_finalize", D.ptr(tr.sums), float(lw.lambda1), float(lw.lambda2),
@@ -237,7 +239,7 @@ def stage_profile(tr, iters):
         sharded = tr.comm.world > 1
         tr.fvr.backward(tr.params, tr.dl, tr.grads, None if sharded else tr.accum, tr.halt)
         if sharded:
-            tr.comm.allreduce_sum_(tr.grads)
+            tr.comm.allreduce_grads_(tr.grads)
             D.grad_norm_accum(tr.grads, tr.accum, tr.halt)
         ev[5].record(s)
         D.adam(tr.params, tr.grads, tr.m1, tr.m2, tr.adam_s, 0.3, tr.sigma_ceiling, tr.halt)

@@ -280,6 +280,14 @@ int splatct_reduce_sum(const double* in, int64_t n, double* out, void* stream);
  * the loss is non-finite (optim.py:356), else write the Adam scalars
  * adam[0..2] = {lr, 1-b1^t, 1-b2^t} for the pre-increment *step
  * (optim.py:88-90,123-126) and advance *step and *iter. */
+/* TV terms across a z-slab boundary after an adjoint that ran without halo
+ * planes (the halo exchange then overlaps it), loss.py:183-207: plane c-1 gets
+ * -lambda/count * sign(hi - v) and |hi - v| is added to *tv_sum (this slab
+ * owns that difference); plane 0 gets +lambda/count * sign(v - lo).  NULL
+ * halo = volume edge.  Deterministic (one block, fixed order). */
+int splatct_tv_halo_fixup(const float* vol_yxz, float* dl_yxz, const float* halo_lo,
+                          const float* halo_hi, int w, int h, int c, double lambda_tv,
+                          double tv_count, double* tv_sum, const int* halt, void* stream);
 int splatct_iter_finalize(const double* sums, double lambda1, double lambda2, double lambda3,
                           double l1_count, double ssim_count, double tv_count, double lr0,
                           double lrf, int64_t max_iters, int64_t* step, int64_t* iter,

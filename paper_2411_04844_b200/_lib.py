@@ -39,6 +39,8 @@ SIGNATURES: dict[str, list] = {
                              c_sz, c_vp, c_vp, c_vp, c_vp, c_vp],
     "splatct_grad_norm_accum": [c_vp, c_i64, c_vp, c_vp, c_vp],
     "splatct_tc_selftest": [c_vp, c_vp, c_vp, c_i32, c_vp],
+    "splatct_tv_halo_fixup": [c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_f64, c_f64, c_vp,
+                              c_vp, c_vp],
     "splatct_fvr_export_bins": [c_vp, c_sz, c_i64, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_vp,
                                 c_vp, c_vp, c_i64p, c_i64p, c_vp],
     "splatct_proj_scratch_bytes": [c_i32, c_i32, c_i32, c_i32, c_i64, c_szp],

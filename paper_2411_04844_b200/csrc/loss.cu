@@ -858,6 +858,43 @@ static int loss_fused_impl(const float* pred, const float* ref, int m, int n, in
     return SPLATCT_OK;
 }
 
+// TV terms across a z-slab boundary, added after the fact (the slab's adjoint
+// ran without halo planes, so the halo exchange overlaps it; loss.py:183-207):
+// the forward difference into the upper neighbour's first plane is owned by
+// this slab -- value |hi - v[c-1]| and subgradient -sign(hi - v[c-1]) at
+// plane c-1 -- and the lower neighbour's difference into plane 0 contributes
+// +sign(v[0] - lo) there.  One block, fixed order: deterministic; the value
+// is added to *tv_sum.
+__global__ void __launch_bounds__(1024) k_tv_halo_fixup(const float* __restrict__ vol,
+                                                        float* __restrict__ dl,
+                                                        const float* __restrict__ lo,
+                                                        const float* __restrict__ hi, int64_t npix,
+                                                        int c, double coef,
+                                                        double* __restrict__ tv_sum,
+                                                        const int* halt) {
+    griddep_wait();
+    if (halted(halt)) return;
+    __shared__ double red[32];
+    double acc = 0.0;
+    for (int64_t p = threadIdx.x; p < npix; p += blockDim.x) {
+        const int64_t col = p * c;
+        if (hi) {
+            const float v = vol[col + c - 1];
+            const float d = hi[p] - v;
+            acc += fabs((double)d);
+            const float sg = (float)((d > 0.f) - (d < 0.f));
+            dl[col + c - 1] = (float)fma(-(double)sg, coef, (double)dl[col + c - 1]);
+        }
+        if (lo) {
+            const float d = vol[col] - lo[p];
+            const float sg = (float)((d > 0.f) - (d < 0.f));
+            dl[col] = (float)fma((double)sg, coef, (double)dl[col]);
+        }
+    }
+    const double r = block_sum<1024>(acc, red);
+    if (threadIdx.x == 0 && hi) *tv_sum += r;
+}
+
 extern "C" {
 
 int splatct_loss_fused(const float* pred, const float* ref, int m, int n, int p, double lmax,
@@ -898,6 +935,17 @@ int splatct_sum_sq_diff(const float* x, const float* y, int64_t count, double* w
     k_sq_diff<<<SPLATCT_SQDIFF_BLOCKS, 256, 0, s>>>(x, y, count, ws);
     SPLATCT_LAUNCH_CK();
     return reduce_sum_f64(ws, SPLATCT_SQDIFF_BLOCKS, out, s);
+}
+
+int splatct_tv_halo_fixup(const float* vol_yxz, float* dl_yxz, const float* halo_lo,
+                          const float* halo_hi, int w, int h, int c, double lambda_tv,
+                          double tv_count, double* tv_sum, const int* halt, void* stream) {
+    if (!halo_lo && !halo_hi) return SPLATCT_OK;
+    SPLATCT_CK(launch_pdl(k_tv_halo_fixup, dim3(1), dim3(1024), 0, as_stream(stream), vol_yxz,
+                          dl_yxz, halo_lo, halo_hi, (int64_t)w * h, c,
+                          tv_count > 0.0 ? lambda_tv / tv_count : 0.0, tv_sum, halt));
+    SPLATCT_LAUNCH_CK();
+    return SPLATCT_OK;
 }
 
 int splatct_iter_finalize(const double* sums, double lambda1, double lambda2, double lambda3,

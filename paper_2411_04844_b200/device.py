@@ -672,6 +672,23 @@ def sino_max(x: torch.Tensor) -> float:
     return float(out[0].item())
 
 
+def ssim_valid(m: int, n: int) -> int:
+    """Valid SSIM window positions of an m x n image: the 11 x 11 window shrunk
+    to the largest odd size <= each dimension (loss.py:77-101)."""
+    kr, kc = min(int(m), 11), min(int(n), 11)
+    kr -= 1 - kr % 2
+    kc -= 1 - kc % 2
+    return (int(m) - kr + 1) * (int(n) - kc + 1)
+
+
+def tv_halo_fixup(vol: torch.Tensor, dl: torch.Tensor, halo_lo, halo_hi, lambda_tv: float,
+                  tv_count: float, tv_sum: torch.Tensor, halt=None) -> None:
+    """Cross-slab TV terms after a halo-free adjoint (splatct_tv_halo_fixup)."""
+    h, w, c = (int(v) for v in vol.shape)
+    call("splatct_tv_halo_fixup", ptr(vol), ptr(dl), ptr(halo_lo), ptr(halo_hi), w, h, c,
+         float(lambda_tv), float(tv_count), ptr(tv_sum), ptr(halt), stream_handle())
+
+
 def reduce_sum(x: torch.Tensor, out: torch.Tensor) -> None:
     call("splatct_reduce_sum", ptr(x), int(x.numel()), ptr(out), stream_handle())
 

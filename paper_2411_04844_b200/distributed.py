@@ -8,14 +8,23 @@ and SSIM are slab-local.  Exchanges per iteration:
   * all-reduce(sum) of the 3 loss sums (L1, SSIM, TV) -- bookkeeping only;
   * one xy-plane TV halo with each z-neighbour (the TV subgradient couples
     adjacent slices, loss.py:195-206);
-  * all-reduce(sum) of the float64 [5, N] partial gradient block (a Gaussian
-    whose box straddles a slab boundary gets contributions from two ranks).
+  * all-reduce(sum) of the [5, N] partial gradient block, sent as f32 (a
+    Gaussian whose box straddles a slab boundary gets contributions from two
+    ranks; Adam is replicated, so every rank needs every gradient).
+
+The halo exchange is posted at the start of the iteration (the planes come
+from the previous iteration's splat) and completed after the adjoint, which
+runs without halos; splatct_tv_halo_fixup then adds the two cross-boundary TV
+terms, so the exchange overlaps the projector, the loss and the adjoint.
 
 Cone beam ("partial projections summed"): rays cross slabs,
 so each rank projects its slab into partial line integrals of the FULL
-(m, nu, nv) sinogram and an all-reduce(sum) of the prediction completes them;
-every rank then evaluates the (replicated) projection loss -- counted once in
-the loss sums -- and back-projects dL/dpred onto its own slab.
+(m, nu, nv) sinogram; a reduce-scatter over detector-row bands completes them
+and leaves each rank one band, on which it evaluates the projection loss
+(SSIM windows lie inside a row's (view, column) image); an all-gather of
+dL/dpred then gives every rank the full gradient sinogram to back-project
+onto its own slab.  Same bytes as an all-reduce of the prediction, but the
+loss runs once per band instead of replicated on every rank.
 
 Adam then runs identically on every rank (replicated cloud).  The
 communicator is written against torch.distributed and works for NCCL on
@@ -70,11 +79,18 @@ class SlabComm:
         return self._reduce(t, dist.ReduceOp.MAX)
 
     def halo(self, vol: torch.Tensor):
-        """Exchange boundary z-planes of a (h, w, c_local) slab.
+        """Exchange boundary z-planes of a (h, w, c_local) slab (blocking).
 
         Returns (lo, hi): plane z0-1 from rank-1 and plane z0+c_local from
         rank+1, each a contiguous (h*w,) tensor, or None at the volume edges.
         """
+        self.halo_start(vol)
+        return self.halo_wait()
+
+    def halo_start(self, vol: torch.Tensor):
+        """Post the boundary-plane exchange and return at once (NCCL runs it
+        on its own stream, overlapping the projector, loss and adjoint that
+        follow); halo_wait() completes it."""
         h, w, _ = vol.shape
         buf_dev = torch.device("cpu") if self.host_p2p else vol.device
         if self._lo is None or self._lo.numel() != h * w or self._out_dev != vol.device:
@@ -95,14 +111,84 @@ class SlabComm:
         if r + 1 < n:
             ops.append(dist.P2POp(dist.isend, self._send_hi, r + 1, self.group))
             ops.append(dist.P2POp(dist.irecv, self._hi, r + 1, self.group))
-        if ops:
-            for req in dist.batch_isend_irecv(ops):
-                req.wait()
+        self._reqs = dist.batch_isend_irecv(ops) if ops else []
+        self._halo_cuda = vol.device.type == "cuda"
+
+    def halo_wait(self):
+        for req in self._reqs:
+            req.wait()
+        self._reqs = []
         lo, hi = self._lo, self._hi
-        if self.host_p2p and vol.device.type == "cuda":
+        if self.host_p2p and self._halo_cuda:
             lo = self._lo_dev.copy_(self._lo)
             hi = self._hi_dev.copy_(self._hi)
+        r, n = self.rank, self.world
         return (lo if r > 0 else None), (hi if r + 1 < n else None)
+
+    def reduce_scatter_rows(self, pred: torch.Tensor, bands, out: torch.Tensor) -> torch.Tensor:
+        """Cone beam: sum the ranks' partial projections (m, nu, nv) and leave
+        rank r the rows bands[r] of the sum, out (m, nu, pb_r) -- each rank
+        evaluates the loss on its own band instead of a replicated whole."""
+        m, nu, _ = pred.shape
+        pmax = max(r1 - r0 for r0, r1 in bands)
+        key = (m, nu, pmax, str(pred.device))
+        if getattr(self, "_rs_key", None) != key:
+            self._rs_key = key
+            dev = torch.device("cpu") if self.host_p2p else pred.device
+            self._rs_in = torch.zeros((self.world, m, nu, pmax), dtype=pred.dtype, device=dev)
+            self._rs_out = torch.zeros((m, nu, pmax), dtype=pred.dtype, device=dev)
+            self._ag_in = torch.zeros((m, nu, pmax), dtype=pred.dtype, device=dev)
+            self._ag_out = torch.zeros((self.world, m, nu, pmax), dtype=pred.dtype, device=dev)
+        if self.host_p2p:
+            _pack_rows(pred.cpu(), bands, self._rs_in)
+        else:
+            _pack_rows(pred, bands, self._rs_in)
+        dist.reduce_scatter_tensor(self._rs_out.view(-1), self._rs_in.view(-1), group=self.group)
+        r0, r1 = bands[self.rank]
+        out.copy_(self._rs_out[:, :, : r1 - r0])
+        return out
+
+    def all_gather_rows(self, band: torch.Tensor, bands, out: torch.Tensor) -> torch.Tensor:
+        """The inverse exchange: every rank's band (m, nu, pb_r) -> out (m, nu, nv)."""
+        r0, r1 = bands[self.rank]
+        self._ag_in[:, :, : r1 - r0].copy_(band)
+        dist.all_gather_into_tensor(self._ag_out.view(-1), self._ag_in.view(-1), group=self.group)
+        src = self._ag_out.to(out.device) if self.host_p2p else self._ag_out
+        for g, (a, b) in enumerate(bands):
+            if b > a:
+                out[:, :, a:b].copy_(src[g, :, :, : b - a])
+        return out
+
+    def allreduce_grads_(self, g: torch.Tensor) -> torch.Tensor:
+        """Sum the f64 [5, N] partial gradients over ranks, sent as f32 (half
+        the bytes; the f32 partial sums keep ~1e-7 relative precision against
+        the 1e-4 gradient tolerance)."""
+        g32 = g.to(torch.float32)
+        self._reduce(g32, dist.ReduceOp.SUM)
+        g.copy_(g32)
+        return g
+
+
+def row_bands(nv: int, world: int):
+    """Detector-row bands [r0, r1) of a cone sinogram, one per rank, starts on
+    multiples of 4 where the row count allows (the 11 x 11 SSIM fast path
+    wants a multiple-of-4 slice count); SSIM windows lie inside one row's
+    (view, column) image, so bands are independent for the loss."""
+    q = max(1, -(-int(nv) // int(world)))
+    q = -(-q // 4) * 4 if nv >= 4 * world else q
+    out = []
+    for r in range(world):
+        r0 = min(r * q, nv)
+        out.append((r0, min(r0 + q, nv) if r + 1 < world else nv))
+    return out
+
+
+def _pack_rows(x, bands, buf):
+    """x (m, nu, nv) -> buf (world, m, nu, pmax): band g of the rows, zero-padded."""
+    for g, (r0, r1) in enumerate(bands):
+        if r1 > r0:
+            buf[g, :, :, : r1 - r0].copy_(x[:, :, r0:r1])
+    return buf
 
 
 def init_from_env(backend: str = "nccl"):

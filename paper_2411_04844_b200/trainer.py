@@ -54,6 +54,15 @@ class NullComm:
     def halo(self, vol):
         return None, None
 
+    def halo_start(self, vol):
+        pass
+
+    def halo_wait(self):
+        return None, None
+
+    def allreduce_grads_(self, g):
+        return g
+
 
 class Trainer:
     """The training loop state on one device (one z-slab when sharded)."""
@@ -88,10 +97,24 @@ class Trainer:
         self.meas = measured
         dev = self.device
         self.op = D.operator_for(geom, self.w, self.h, self.slab.c_global, step_length, dev)
-        self.loss = D.LossPlan(m, n, p, dev)
-        self.loss.prepare(measured)   # the measured sinogram is constant over a run
         self.pred = torch.empty((m, n, p), dtype=torch.float32, device=dev)
         self.gpred = torch.empty_like(self.pred)
+        # cone beam across ranks: the loss runs on this rank's detector-row band
+        # (reduce-scatter of the partial projections, all-gather of dL/dpred)
+        self.bands = None
+        if not self.per_slice and self.comm.world > 1:
+            from .distributed import row_bands
+            self.bands = row_bands(p, self.comm.world)
+            r0, r1 = self.bands[self.comm.rank]
+            self.meas_band = measured[:, :, r0:r1].contiguous()
+            self.pred_band = torch.empty_like(self.meas_band)
+            self.gpred_band = torch.empty_like(self.meas_band)
+            self.loss = D.LossPlan(m, n, r1 - r0, dev) if r1 > r0 else None
+            if self.loss is not None:
+                self.loss.prepare(self.meas_band)
+        else:
+            self.loss = D.LossPlan(m, n, p, dev)
+            self.loss.prepare(measured)   # the measured sinogram is constant over a run
         self.vol = torch.empty((self.h, self.w, cl), dtype=torch.float32, device=dev)
         self.dl = torch.empty_like(self.vol)
         self.tv_part = torch.zeros(D.tv_partial_len(self.w, self.h, cl), dtype=torch.float64,
@@ -109,7 +132,7 @@ class Trainer:
         self.lmax = float(lm.item())
         cg = self.slab.c_global
         self.l1_count = float(m * n * self.p_global)
-        self.ssim_count = float(self.loss.valid * self.p_global)
+        self.ssim_count = float(D.ssim_valid(m, n) * self.p_global)
         self.tv_count = float(self.w * self.h * cg)
         self.graph = None
         self._set_params(params, m1, m2, accum)
@@ -142,7 +165,13 @@ class Trainer:
                 tuple(params.shape) != tuple(self.params.shape):
             raise ValueError("reload needs the same sinogram and cloud shapes")
         self.meas.copy_(measured)
-        self.loss.prepare(self.meas)
+        if self.bands is not None:
+            r0, r1 = self.bands[self.comm.rank]
+            self.meas_band.copy_(measured[:, :, r0:r1])
+            if self.loss is not None:
+                self.loss.prepare(self.meas_band)
+        else:
+            self.loss.prepare(self.meas)
         self.params.copy_(params)
         if m1 is None:
             self.m1.zero_()
@@ -184,36 +213,50 @@ class Trainer:
         sharded = self.comm.world > 1
         replicated = not self.per_slice and sharded
         st = []
+        overlap_halo = sharded and lw.lambda3 > 0
+        if overlap_halo:   # planes of the previous splat; completed after the adjoint
+            st.append(("comm", lambda: self.comm.halo_start(self.vol)))
 
         def project():   # empty-space skipping from the voxelizer's tile occupancy
             self.op.forward(self.vol, self.pred, halt, z0=z0, occ=self.fvr)
         st.append(("gpu", project))
-        if replicated:   # partial cone projections -> full
-            st.append(("comm", lambda: self.comm.allreduce_sum_(self.pred)))
+        if replicated:   # partial cone projections -> this rank's row band of their sum
+            st.append(("comm", lambda: self.comm.reduce_scatter_rows(self.pred, self.bands,
+                                                                     self.pred_band)))
 
         def data_loss():
-            if lw.lambda1 > 0 or lw.lambda2 > 0:
-                self.loss.fused(self.pred, self.meas, self.lmax, lw.lambda1, lw.lambda2,
-                                self.l1_count, float(self.p_global), self.gpred, self.sums,
-                                halt)
-                if replicated and self.comm.rank != 0:
-                    self.sums[0:2].zero_()   # every rank holds the full loss: count it once
+            pred, meas, gpred = ((self.pred_band, self.meas_band, self.gpred_band) if replicated
+                                 else (self.pred, self.meas, self.gpred))
+            if (lw.lambda1 > 0 or lw.lambda2 > 0) and self.loss is not None:
+                self.loss.fused(pred, meas, self.lmax, lw.lambda1, lw.lambda2, self.l1_count,
+                                float(self.p_global), gpred, self.sums, halt)
             else:
-                self.gpred.zero_()
+                gpred.zero_()
+                self.sums[0:2].zero_()
         st.append(("gpu", data_loss))
+        if replicated:   # every rank back-projects the full dL/dpred onto its slab
+            st.append(("comm", lambda: self.comm.all_gather_rows(self.gpred_band, self.bands,
+                                                                 self.gpred)))
         if lw.lambda3 > 0:
-            def halo():
-                self._halo = self.comm.halo(self.vol)
-            st.append(("comm", halo))
-
             def adjoint_tv():
-                lo, hi = self._halo
-                # dl is read only inside footprints: skip empty neighbourhoods
-                self.op.adjoint(self.gpred, self.dl, vol=self.vol, halo_lo=lo, halo_hi=hi,
-                                lambda_tv=lw.lambda3, tv_count=self.tv_count,
-                                tv_partial=self.tv_part, halt=halt, z0=z0, occ=self.fvr)
+                # dl is read only inside footprints: skip empty neighbourhoods.
+                # Sharded: no halos here -- the cross-slab TV terms are added by
+                # the fix-up once the (overlapped) exchange completes
+                self.op.adjoint(self.gpred, self.dl, vol=self.vol, lambda_tv=lw.lambda3,
+                                tv_count=self.tv_count, tv_partial=self.tv_part, halt=halt,
+                                z0=z0, occ=self.fvr)
                 D.reduce_sum(self.tv_part, self.sums[2:3])
             st.append(("gpu", adjoint_tv))
+            if overlap_halo:
+                def halo_wait():
+                    self._halo = self.comm.halo_wait()
+                st.append(("comm", halo_wait))
+
+                def tv_fixup():
+                    lo, hi = self._halo
+                    D.tv_halo_fixup(self.vol, self.dl, lo, hi, lw.lambda3, self.tv_count,
+                                    self.sums[2:3], halt)
+                st.append(("gpu", tv_fixup))
         else:
             st.append(("gpu", lambda: self.op.adjoint(self.gpred, self.dl, halt=halt, z0=z0,
                                                       c_local=self.slab.c_local,
@@ -231,7 +274,7 @@ class Trainer:
                               None if sharded else self.accum, halt)
         st.append(("gpu", finalize_backward))
         if sharded:
-            st.append(("comm", lambda: self.comm.allreduce_sum_(self.grads)))
+            st.append(("comm", lambda: self.comm.allreduce_grads_(self.grads)))
 
         def update_resplat():
             if sharded:

@@ -53,7 +53,7 @@ def _worker(rank, world, port, q, variant):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("variant,world", [("fan", 2), ("cone", 2), ("fan", 4)])
+@pytest.mark.parametrize("variant,world", [("fan", 2), ("cone", 2), ("fan", 4), ("cone", 3)])
 def test_two_slab_ranks_match_single_device(variant, world):
     """world 4: 9-10-slice slabs under a 17-slice box, so Gaussians straddle
     three slabs (gradient all-reduce, TV halos on both sides)."""
@@ -101,3 +101,35 @@ def test_bench_two_ranks_smoke():
     assert len(lines) == 1   # rank 0 only
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
+
+
+@pytest.mark.parametrize("edges", [(True, True), (True, False), (False, True)])
+def test_tv_halo_fixup_matches_halo_adjoint(edges):
+    """The overlapped-halo step: adjoint without halos + splatct_tv_halo_fixup
+    equals the adjoint with halo planes (value to 1e-12, dL/dV to f32 rounding)."""
+    import torch
+    from paper_2411_04844_b200 import core, device as D
+    dev = D.require_cuda()
+    w, h, c = 40, 36, 24
+    geom = core.ScanGeometry.fan(16, 60, 1.2, 70.0, 50.0)
+    op = D.ProjectorOperator(geom, w, h, 0.5, dev)
+    g = torch.Generator(device="cpu").manual_seed(3)
+    vol = torch.randint(0, 3, (h, w, c), generator=g).float().to(dev)   # ties: sign 0
+    lo = torch.randint(0, 3, (h * w,), generator=g).float().to(dev) if edges[0] else None
+    hi = torch.randint(0, 3, (h * w,), generator=g).float().to(dev) if edges[1] else None
+    ys = torch.randn((16, 60, c), generator=g).to(dev)
+    cnt = float(w * h * 3 * c)
+    n = D.tv_partial_len(w, h, c)
+    s1 = torch.zeros(3, dtype=torch.float64, device=dev)
+    s2 = torch.zeros(3, dtype=torch.float64, device=dev)
+    tp = torch.zeros(n, dtype=torch.float64, device=dev)
+    a = op.adjoint(ys, vol=vol, halo_lo=lo, halo_hi=hi, lambda_tv=1.0, tv_count=cnt,
+                   tv_partial=tp)
+    D.reduce_sum(tp, s1[2:3])
+    b = op.adjoint(ys, vol=vol, lambda_tv=1.0, tv_count=cnt, tv_partial=tp)
+    D.reduce_sum(tp, s2[2:3])
+    D.tv_halo_fixup(vol, b, lo, hi, 1.0, cnt, s2[2:3])
+    torch.cuda.synchronize()
+    assert abs(float(s1[2]) - float(s2[2])) <= 1e-12 * abs(float(s1[2]))
+    d = (a - b).abs().max().item()
+    assert d <= 2e-7 * a.abs().max().item() + 1e-12
