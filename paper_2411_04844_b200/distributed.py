@@ -34,7 +34,9 @@ device tensors and for gloo on CPU tensors (tests/test_distributed.py).
 from __future__ import annotations
 
 import os
+import time
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -206,46 +208,187 @@ def init_from_env(backend: str = "nccl"):
     return 0, 1
 
 
+class _SlabEvaluator:
+    """Per-iteration truth metrics and held-out view loss of a z-slab sharded
+    run (optim._Evaluator across ranks): per-slab partial sums, all-reduced.
+
+    PSNR: the slab's squared error against the truth slab; mean axial SSIM:
+    the slab's slice images (SSIM is per slice, loss.py:159-180, so slabs are
+    independent); held-out view L1 (optim.py:405-416): per-slice geometries
+    project the slab onto the held-out views' slab slices, cone beam sums the
+    slabs' partial projections first."""
+
+    def __init__(self, tr, comm, truth, geom_val, sino_val, slab):
+        from . import device as D
+        dev = tr.device
+        self.tr, self.comm, self.s = tr, comm, slab
+        self.truth = None
+        if truth is not None:
+            z = np.ascontiguousarray(truth.zyx[slab.z0:slab.z0 + slab.c_local])
+            self.truth = D.zyx_to_yxz(z, dev)
+            self.peak = float(truth.data.max())
+            w, h, c = truth.dims
+            self.n_vox = float(w * h * c)
+            self.c_global = c
+            self.ssim_plan = D.LossPlan(h, w, slab.c_local, dev)
+            self.scratch = torch.empty_like(self.truth)
+            self.sums = torch.zeros(3, dtype=torch.float64, device=dev)
+        self.val = geom_val is not None
+        if self.val:
+            w, h = tr.w, tr.h
+            views = sino_val.views
+            if geom_val.per_slice:
+                self.val_op = D.ProjectorOperator(geom_val, w, h, 0.5, dev)
+                views = views[:, :, slab.z0:slab.z0 + slab.c_local]
+            else:
+                self.val_op = D.ConeOperator(geom_val, w, h, slab.c_global, 0.5, dev)
+            self.per_slice = geom_val.per_slice
+            self.val_ref = D.sino_to_device(np.ascontiguousarray(views), dev)
+            m, n, p = self.val_ref.shape
+            self.val_plan = D.LossPlan(m, n, p, dev)
+            self.val_pred = torch.empty((m, n, p), dtype=torch.float32, device=dev)
+            self.val_g = torch.empty_like(self.val_pred)
+            self.val_sums = torch.zeros(3, dtype=torch.float64, device=dev)
+            self.val_count = float(sino_val.views.size)
+
+    def metrics(self):
+        from . import device as D
+        if self.truth is None:
+            return float("nan"), float("nan")
+        vol = self.tr.vol
+        part = torch.zeros(2, dtype=torch.float64, device=vol.device)
+        part[0] = D.sum_sq_diff(vol, self.truth)
+        p = self.ssim_plan
+        p.fused(vol, self.truth, self.peak, 0.0, 1.0, 1.0, 1.0, self.scratch, self.sums)
+        part[1] = self.sums[1]
+        self.comm.allreduce_sum_(part)
+        mse = float(part[0]) / self.n_vox
+        psnr = 200.0 if mse == 0.0 else min(10.0 * np.log10(self.peak ** 2 / mse), 200.0)
+        return psnr, float(part[1]) / p.valid / self.c_global
+
+    def val_loss(self):
+        self.val_op.forward(self.tr.vol, self.val_pred, z0=self.s.z0)
+        if not self.per_slice:   # partial line integrals of every slab
+            self.comm.allreduce_sum_(self.val_pred)
+        self.val_plan.fused(self.val_pred, self.val_ref, 1.0, 1.0, 0.0, 1.0, 1.0, self.val_g,
+                            self.val_sums)
+        part = self.val_sums[0:1].clone()
+        if self.per_slice:
+            self.comm.allreduce_sum_(part)
+        return float(part.item()) / self.val_count
+
+
 def run_reconstruction_sharded(measured, geom, settings, init_cloud, comm=None,
-                               use_graph: bool = True):
+                               use_graph: bool = True, truth=None):
     """run_reconstruction (optim.py:286-427) over a z-slab-sharded volume.
 
     Every rank calls this with the same host inputs; rank r keeps slices
-    slab_bounds(c, world, r) of the measured sinogram and the volume.  Densify
-    and the per-iteration truth/val hooks of the single-device API are not
-    supported here.  Returns (VolumeGrid on rank 0 else None, GaussianCloud,
-    trace array [iters, 4] = loss, l1, ssim, tv).
+    slab_bounds(c, world, r) of the volume (and of the measured sinogram for
+    the per-slice geometries).  The loop body is the reference's: the sharded
+    iteration (Trainer), densification on its interval (the cloud and the
+    all-reduced gradient statistics are replicated, so every rank runs the
+    identical device event with the same rng), per-iteration truth metrics
+    (PSNR, mean axial SSIM) and the held-out-view stop rule, both from
+    all-reduced slab partial sums.  Returns (VolumeGrid on rank 0 else None,
+    GaussianCloud, list[TraceRow]).
     """
-    import numpy as np
-
     from . import device as D
-    from .core import VolumeGrid
+    from .core import ValidationError, VolumeGrid
+    from .optim import DensifyParams, TraceRow, _holdout_split
     from .trainer import Trainer
 
     if comm is None:
         from .trainer import NullComm
         comm = SlabComm() if dist.is_available() and dist.is_initialized() else NullComm()
     dims = tuple(int(v) for v in settings.dims)
+    box = settings.box
     s = slab_bounds(dims[2], comm.world, comm.rank)
     dev = D.require_cuda()
+    if settings.stop_rule == "val-convergence":
+        (geom_tr, sino_tr), (geom_val, sino_val) = _holdout_split(geom, measured,
+                                                                  settings.holdout_fraction)
+    elif settings.stop_rule == "iters":
+        geom_tr, sino_tr, geom_val, sino_val = geom, measured, None, None
+    else:
+        raise ValidationError(f"unknown stop rule {settings.stop_rule!r}")
     # per-slice geometries: the rank's sinogram slab; cone beam: the full
     # sinogram on every rank (partial projections are summed in the Trainer)
-    local = (np.ascontiguousarray(measured.views[:, :, s.z0:s.z0 + s.c_local])
-             if geom.per_slice else np.ascontiguousarray(measured.views))
-    tr = Trainer(D.sino_to_device(local, dev), geom, dims, settings.box, settings.weights,
+    local = (np.ascontiguousarray(sino_tr.views[:, :, s.z0:s.z0 + s.c_local])
+             if geom.per_slice else np.ascontiguousarray(sino_tr.views))
+    tr = Trainer(D.sino_to_device(local, dev), geom_tr, dims, box, settings.weights,
                  D.cloud_to_params(init_cloud, dev), lr0=settings.lr_initial,
-                 lrf=settings.lr_final, max_iters=settings.max_iters, slab=s, comm=comm)
+                 lrf=settings.lr_final, max_iters=settings.max_iters, slab=s, comm=comm,
+                 trace_cap=max(settings.max_iters, 1))
+    ev = _SlabEvaluator(tr, comm, truth, geom_val, sino_val, s)
+    dparams = settings.densify or DensifyParams.for_volume(dims, box_size=box.extent)
+    per_iter_host = truth is not None or geom_val is not None
     tr.initial_volume()
-    done = 0
-    if use_graph and settings.max_iters > 0:
-        # one graph per iteration on a single rank; with ranks, graphs for the
-        # GPU segments between the (eager) slab collectives
-        done = tr.capture() if comm.world == 1 else tr.capture_segments()
-    for _ in range(done, settings.max_iters):
-        tr.step()
-    torch.cuda.synchronize()
-    if tr.halted():
-        raise RuntimeError(f"non-finite loss at iteration {tr.iterations_done()}")
+    trace = []
+    best_val, best_it = np.inf, 0
+    t_start = time.perf_counter()
+    iters_acc = 0
+    pending = []
+
+    def flush():
+        torch.cuda.current_stream().synchronize()
+        rows = tr.trace.cpu().numpy()
+        halted = tr.halted()
+        out = []
+        for idx, wall in pending:
+            r = rows[idx]
+            if halted and not np.isfinite(r[0]):
+                raise RuntimeError(f"non-finite loss at iteration {idx}")
+            out.append(TraceRow(iteration=idx + 1, loss=float(r[0]), loss_l1=float(r[1]),
+                                loss_ssim=float(r[2]), loss_tv=float(r[3]), psnr=float("nan"),
+                                ssim=float("nan"), n_gaussians=tr.N, wall_seconds=wall))
+        pending.clear()
+        return out
+
+    it = 0
+    captured = False
+    while it < settings.max_iters:
+        densify_due = (settings.densify_interval > 0 and (it + 1) % settings.densify_interval == 0
+                       and it + 1 < settings.max_iters)
+        if use_graph and not captured and not densify_due:
+            # one graph per iteration on a single rank; with ranks, graphs for the
+            # GPU segments between the (eager) slab collectives -- both execute `it`
+            tr.capture() if comm.world == 1 else tr.capture_segments()
+            captured = True
+        else:
+            tr.step()
+        pending.append((it, time.perf_counter() - t_start))
+        iters_acc += 1
+        if densify_due or per_iter_host or it + 1 == settings.max_iters:
+            rows = flush()
+            row = rows[-1]
+            trace.extend(rows[:-1])
+            if densify_due:   # the identical device event on every rank (replicated cloud)
+                rng = np.random.default_rng([settings.seed, it + 1])
+                np_, nm1, nm2, report = D.densify(tr.params, tr.m1, tr.m2, tr.accum, iters_acc,
+                                                  dparams, rng)
+                if report.n_after == 0:
+                    raise ValidationError("cloud is empty (densification pruned every Gaussian)")
+                tr.resize(np_, nm1, nm2, None)
+                captured = False
+                iters_acc = 0
+                row.clones, row.splits, row.prunes = report.clones, report.splits, report.prunes
+                row.n_gaussians = report.n_after
+            if truth is not None:
+                row.psnr, row.ssim = ev.metrics()
+            stop = False
+            if geom_val is not None:
+                val = ev.val_loss()
+                row.val_loss = val
+                if val < best_val - 1e-9:
+                    best_val, best_it = val, it + 1
+                elif it + 1 - best_it >= settings.patience:
+                    stop = True
+            trace.append(row)
+            if stop:
+                break
+        it += 1
+    if pending:
+        trace.extend(flush())
     cmax = -(-dims[2] // comm.world)
     pad = torch.zeros((tr.h, tr.w, cmax), dtype=torch.float32, device=dev)
     pad[:, :, : s.c_local] = tr.vol
@@ -262,4 +405,4 @@ def run_reconstruction_sharded(measured, geom, settings, init_cloud, comm=None,
         cols = [parts[r][:, :, : slab_bounds(dims[2], comm.world, r).c_local]
                 for r in range(comm.world)]
         vol = VolumeGrid.from_zyx(D.yxz_to_zyx(torch.cat(cols, dim=2)))
-    return vol, D.params_to_cloud(tr.params), tr.trace_rows()
+    return vol, D.params_to_cloud(tr.params), trace

@@ -48,7 +48,8 @@ def _worker(rank, world, port, q, variant):
     from paper_2411_04844_b200.distributed import run_reconstruction_sharded
     meas, geom, settings, cloud = _problem(variant)
     vol, cl, trace = run_reconstruction_sharded(meas, geom, settings, cloud)
-    q.put((rank, None if vol is None else vol.zyx.copy(), cl.mu.copy(), trace.copy()))
+    trace = np.array([[r.loss, r.loss_l1, r.loss_ssim, r.loss_tv] for r in trace])
+    q.put((rank, None if vol is None else vol.zyx.copy(), cl.mu.copy(), trace))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -133,3 +134,64 @@ def test_tv_halo_fixup_matches_halo_adjoint(edges):
     assert abs(float(s1[2]) - float(s2[2])) <= 1e-12 * abs(float(s1[2]))
     d = (a - b).abs().max().item()
     assert d <= 2e-7 * a.abs().max().item() + 1e-12
+
+
+def _hooks_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from paper_2411_04844_b200.distributed import run_reconstruction_sharded
+    meas, geom, settings, cloud, truth = _hooks_problem()
+    vol, cl, trace = run_reconstruction_sharded(meas, geom, settings, cloud, truth=truth)
+    q.put((rank, [(r.loss, r.psnr, r.ssim, r.val_loss, r.n_gaussians, r.splits) for r in trace],
+           cl.n))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _hooks_problem():
+    from paper_2411_04844_b200 import core, optim, phantom, projector
+    from paper_2411_04844_b200.densify import DensifyParams
+    dims = (48, 40, 37)
+    truth = phantom.shepp_logan_3d(*dims)
+    geom = core.ScanGeometry.fan(20, 72, 1.2, 80.0, 60.0)
+    meas = projector.forward_project(truth, geom)
+    box = core.BoxConfig.for_dims(17, dims)
+    cloud = optim.init_cloud_random(dims, 2000, seed=3, box=box)
+    dp = DensifyParams(n_max=3000, tau=1e-12, theta=1.0, box_size=17, grad_prune_enabled=False)
+    settings = optim.ReconstructionSettings(dims=dims, box=box, max_iters=14, densify_interval=6,
+                                            densify=dp, stop_rule="val-convergence", patience=50)
+    return meas, geom, settings, cloud, truth
+
+
+def test_sharded_loop_hooks_match_single_device():
+    """The sharded run_reconstruction keeps the reference loop's hooks
+    (optim.py:388-424): a densification event (identical on every rank: the
+    replicated cloud, the all-reduced gradient statistics), per-iteration
+    truth PSNR / SSIM and the held-out-view loss of the stop rule, from
+    all-reduced slab partial sums -- against the single-device run."""
+    from paper_2411_04844_b200 import optim
+    meas, geom, settings, cloud, truth = _hooks_problem()
+    _, cl1, tr1 = optim.run_reconstruction(meas, geom, settings, truth=truth, init_cloud=cloud)
+    want = [(r.loss, r.psnr, r.ssim, r.val_loss, r.n_gaussians, r.splits) for r in tr1]
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_hooks_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert any(w[5] > 0 for w in want)        # the event split Gaussians
+    for rank, rows, n in res:
+        assert n == cl1.n and len(rows) == len(want)
+        got, ref = np.array(rows, np.float64), np.array(want, np.float64)
+        np.testing.assert_array_equal(got[:, 4:], ref[:, 4:])       # N, splits
+        np.testing.assert_allclose(got[:, 0], ref[:, 0], rtol=1e-5)  # loss
+        np.testing.assert_allclose(got[:, 1], ref[:, 1], rtol=1e-6)  # psnr
+        np.testing.assert_allclose(got[:, 2:4], ref[:, 2:4], rtol=1e-5)   # ssim, val loss
