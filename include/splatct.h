@@ -58,8 +58,10 @@ unsigned long long splatct_launch_count(void);
  * ------------------------------------------------------------------------- */
 #define SPLATCT_TILE 16
 
-/* Bytes of the caller-provided voxelizer workspace (bins, sort buffers,
- * backward partials) for n Gaussians on a (w,h,c) grid with box halves. */
+/* Bytes of the caller-provided voxelizer workspace (footprints, GRec records,
+ * sort buffers and tile starts, empty-space masks, tile counters, the
+ * backward's visiting order) for n Gaussians on a (w,h,c) grid with box
+ * halves. */
 int splatct_fvr_workspace_bytes(int64_t n, int w, int h, int c, int hx, int hy, int hz,
                                 size_t* bytes);
 
@@ -92,8 +94,12 @@ int splatct_fvr_forward_plain(const double* params, int64_t n, int w, int h, int
                               int hx, int hy, int hz, void* ws, size_t ws_bytes, float* vol_yxz,
                               void* stream);
 
-/* Per-Gaussian gradients from dL/dV (yxz), fvr.py:227-273: per-tile partial
- * moments, combined per Gaussian in fixed slot order (deterministic).
+/* Per-Gaussian gradients from dL/dV (yxz), fvr.py:227-273: one warp per
+ * Gaussian sums its box's five moments in a fixed order (deterministic, no
+ * partial buffers), the upstream rows arriving by TMA (c % 4 == 0; full 17^3
+ * boxes two rows per load) or direct loads, then the f64 chain rule.  The
+ * general path never reads upstream outside the footprint (the masked
+ * adjoint leaves it unwritten).
  * grads: double[5][n] (overwritten).  accum: optional double[n]; if non-NULL
  * accum[i] += |d_mu_i| (fvr.py:266-273).  Requires the bins of
  * splatct_fvr_bin on the same params.  Replaces _kernels.splat_backward(mu,
