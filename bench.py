@@ -645,7 +645,7 @@ def main():
     ap.add_argument("--cpu-iters", type=int, default=1)
     ap.add_argument("--ref-max-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--extra", default="c2cone",
+    ap.add_argument("--extra", default="c2cone,c4",
                     help="comma-separated secondary configs timed in the same run (N=1, c2 "
                          "only); '' disables")
     args = ap.parse_args()
