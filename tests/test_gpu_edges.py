@@ -282,3 +282,29 @@ def test_trainer_step_with_poisoned_adjoint_buffer(side):
     assert torch.isnan(tr.dl).any()                # skipped quads were left unwritten
     assert np.all(np.isfinite(tr.trace_rows()[:, 0]))
     assert torch.isfinite(tr.params).all() and torch.isfinite(tr.grads).all()
+
+
+def test_pinned_output_pool_results_stay_valid():
+    """run_reconstruction hands its volume out in a reusable page-locked array;
+    results the caller keeps are never overwritten by later calls (the pool
+    falls back to pageable arrays once two results are held)."""
+    import gc
+    from paper_2411_04844_b200 import device as D, optim, phantom, projector
+    dims = (40, 36, 32)
+    truth = phantom.shepp_logan_3d(*dims)
+    geom = core.ScanGeometry.parallel(12, 48)
+    meas = projector.forward_project(truth, geom)
+    box = core.BoxConfig.for_dims(17, dims)
+    st = optim.ReconstructionSettings(dims=dims, box=box, max_iters=3, n_gaussians=500,
+                                      densify_interval=0)
+    cl = optim.init_cloud_random(dims, 500, seed=1, box=box)
+    vols = [optim.run_reconstruction(meas, geom, st, init_cloud=cl)[0] for _ in range(4)]
+    ref = vols[0].zyx.copy()
+    for v in vols:
+        np.testing.assert_array_equal(v.zyx, ref)
+    assert len({v.data.__array_interface__["data"][0] for v in vols}) == 4
+    del vols
+    gc.collect()
+    assert all(not e.busy for e in D._OUT_POOL)
+    v = optim.run_reconstruction(meas, geom, st, init_cloud=cl)[0]
+    np.testing.assert_array_equal(v.zyx, ref)
