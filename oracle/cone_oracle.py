@@ -106,3 +106,43 @@ def cone_forward(vol_zyx, geom, step=0.5, z0=0, c_global=None):
                           for (xi, yi), (W, WT) in ent.items())
                 out[a, d, dv] = acc * step * math.sqrt(1.0 + (v / length) ** 2)
     return out
+
+
+def cone_forward_per_sample(vol_zyx, geom, step=0.5):
+    """The same fan-ray samples, but every sample interpolates z at its OWN
+    distance tau = t / L (trilinear per sample, no per-pixel merge): the
+    finer model the merged one approximates.  Used to bound the merge error
+    at large cone angles (tests/test_gpu_cone.py)."""
+    vol = np.asarray(vol_zyx, np.float64)
+    c, h, w = vol.shape
+    zc = 0.5 * (c - 1)
+    m, nu, nv = geom.n_views, geom.n_detectors, geom.n_rows
+    sv, su = float(geom.row_spacing), float(geom.detector_spacing)
+    rs, rd = float(geom.source_to_origin), float(geom.origin_to_detector)
+    out = np.zeros((m, nu, nv))
+    vs = (np.arange(nv) - 0.5 * (nv - 1)) * sv
+    for a, ang in enumerate(np.asarray(geom.view_angles, np.float64)):
+        ca, sa = math.cos(ang), math.sin(ang)
+        for d in range(nu):
+            u = (d - 0.5 * (nu - 1)) * su
+            smp, length = column_samples(ca, sa, u, rs, rd, w, h, step)
+            if not smp:
+                continue
+            smp = np.array(smp)
+            x, y, tau = smp[:, 0], smp[:, 1], smp[:, 2]
+            x0, y0 = np.floor(x).astype(int), np.floor(y).astype(int)
+            fx, fy = x - x0, y - y0
+            z = zc + tau[:, None] * vs[None, :]
+            z0 = np.floor(z).astype(int)
+            fz = z - z0
+            acc = np.zeros(nv)
+            for xi, yi, wq in ((x0, y0, (1 - fx) * (1 - fy)), (x0 + 1, y0, fx * (1 - fy)),
+                               (x0, y0 + 1, (1 - fx) * fy), (x0 + 1, y0 + 1, fx * fy)):
+                ok = (xi >= 0) & (xi < w) & (yi >= 0) & (yi < h)
+                xc, yc = np.clip(xi, 0, w - 1)[:, None], np.clip(yi, 0, h - 1)[:, None]
+                for zz, wz in ((z0, 1 - fz), (z0 + 1, fz)):
+                    okz = ok[:, None] & (zz >= 0) & (zz < c)
+                    val = np.where(okz, vol[np.clip(zz, 0, c - 1), yc, xc], 0.0)
+                    acc += (wq[:, None] * wz * val).sum(0)
+            out[a, d, :] = acc * step * np.sqrt(1.0 + (vs / length) ** 2)
+    return out
