@@ -537,6 +537,9 @@ __global__ void __launch_bounds__(R_NT, 2) k_loss_grad11(const float* __restrict
                                                          const int* halt) {
     griddep_wait();
     if (halted(halt)) return;
+    float gcf[11];   // the column window in f32 for the horizontal adjoint pass
+#pragma unroll
+    for (int b = 0; b < 11; ++b) gcf[b] = (float)W.gc[b];
     // per staged row: D columns s0-10 .. s0+7 (3 fields) and x, y columns s0 .. s0+7
     __shared__ __align__(16) float sd[G_BUF][3][R_SPAN][32];
     __shared__ __align__(16) float sxy[G_BUF][2][R_COLS][32];
@@ -601,17 +604,20 @@ __global__ void __launch_bounds__(R_NT, 2) k_loss_grad11(const float* __restrict
             issue(r + G_AHEAD);
             const int buf = r % G_BUF;
             if (ss && r < vr) {
-                double t[2][3] = {{0, 0, 0}, {0, 0, 0}};
+                // the derivative fields are f32 already: their 11-tap horizontal
+                // correlation runs on the FP32 pipe (two interleaved partial sums,
+                // ~1e-7 relative), widened once per field for the f64 vertical pass
+                float t[2][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
 #pragma unroll
                 for (int b = 0; b < 11; ++b) {    // column s - b = staged column cl + 10 - b
-                    const double g = W.gc[b];
-                    double* tb = t[b & 1];
+                    const float g = gcf[b];
+                    float* tb = t[b & 1];
 #pragma unroll
                     for (int f = 0; f < 3; ++f)
-                        tb[f] = fma(g, (double)sd[buf][f][cl + 10 - b][lane], tb[f]);
+                        tb[f] = fmaf(g, sd[buf][f][cl + 10 - b][lane], tb[f]);
                 }
 #pragma unroll
-                for (int f = 0; f < 3; ++f) ring[ph][f] = t[0][f] + t[1][f];
+                for (int f = 0; f < 3; ++f) ring[ph][f] = (double)t[0][f] + (double)t[1][f];
             } else {
 #pragma unroll
                 for (int f = 0; f < 3; ++f) ring[ph][f] = 0.0;   // rows >= vr contribute 0
