@@ -1594,9 +1594,17 @@ __device__ __forceinline__ void bwd_moments17_tma(const GRec& r, int xlo, int nx
 // selects -- the 18th column (k = 8 of the odd half) and the lanes past the
 // 17th column re-read column 16 (inside the footprint, finite) against a zero
 // weight.  Row 17 of the last load is never read.
-constexpr int BT2_RING = 3;
-constexpr int BT2_SLOT = 2816;                      // 2 x 17 x 20 x 4 B = 2720, rounded to 128 B
-constexpr unsigned BT2_BYTES = 2u * 17u * BT_ZB * 4u;
+#ifndef SPLATCT_BT2_ROWS
+#define SPLATCT_BT2_ROWS 2
+#endif
+#ifndef SPLATCT_BT2_RING
+#define SPLATCT_BT2_RING 3
+#endif
+constexpr int BT2_ROWS = SPLATCT_BT2_ROWS;          // box rows per TMA load
+constexpr int BT2_RING = SPLATCT_BT2_RING;
+constexpr int BT2_NB = (17 + BT2_ROWS - 1) / BT2_ROWS;   // loads per box
+constexpr int BT2_SLOT = (BT2_ROWS * 17 * BT_ZB * 4 + 127) / 128 * 128;
+constexpr unsigned BT2_BYTES = (unsigned)BT2_ROWS * 17u * BT_ZB * 4u;
 
 __device__ __forceinline__ void bwd_moments17_tma_full(const GRec& r, int xlo, int ylo, int zlo,
                                                        int zoff, const CUtensorMap* tmap2,
@@ -1615,14 +1623,11 @@ __device__ __forceinline__ void bwd_moments17_tma_full(const GRec& r, int xlo, i
         asm volatile(
             "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
             "[%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(dst),
-            "l"(tmap2), "r"(zlo & ~3), "r"(xlo), "r"(ylo + 2 * bi), "r"(b)
+            "l"(tmap2), "r"(zlo & ~3), "r"(xlo), "r"(ylo + BT2_ROWS * bi), "r"(b)
             : "memory");
     };
-    if (lane == 0) {
-        issue(0);
-        issue(1);
-        issue(2);
-    }
+    if (lane == 0)
+        for (int q = 0; q < BT2_RING && q < BT2_NB; ++q) issue(q);
     const float rz = (float)(zlo + zl + zoff - r.fz) - r.dz;
     const float ez = exp2f(-r.inv2 * rz * rz);
     const float rz16 = (float)(zlo + 16 + zoff - r.fz) - r.dz;
@@ -1651,9 +1656,9 @@ __device__ __forceinline__ void bwd_moments17_tma_full(const GRec& r, int xlo, i
     const int offp = pl * BT_ZB + 16 + (zlo & 3);
     float A0 = 0.f, Ax = 0.f, Ay = 0.f, Ar = 0.f, P0 = 0.f, P1 = 0.f, P2 = 0.f;
 #pragma unroll
-    for (int bi = 0; bi < 9; ++bi) {
+    for (int bi = 0; bi < BT2_NB; ++bi) {
         __syncwarp();   // every lane is done with box bi - 1's slot (refilled next); ytab visible
-        if (lane == 0 && bi >= 1 && bi + 2 <= 8) issue(bi + 2);
+        if (lane == 0 && bi >= 1 && bi + BT2_RING - 1 < BT2_NB) issue(bi + BT2_RING - 1);
         const int q = bi % BT2_RING;
         {
             const unsigned parity = (unsigned)(bi / BT2_RING) & 1u;
@@ -1669,8 +1674,8 @@ __device__ __forceinline__ void bwd_moments17_tma_full(const GRec& r, int xlo, i
         }
         const float* src = ring + (BT2_SLOT / 4) * q;
 #pragma unroll
-        for (int rr = 0; rr < 2; ++rr) {
-            const int yi = 2 * bi + rr;
+        for (int rr = 0; rr < BT2_ROWS; ++rr) {
+            const int yi = BT2_ROWS * bi + rr;
             if (yi > 16) break;
             const float* rs = src + rr * (17 * BT_ZB);
             float2 C01 = make_float2(0.f, 0.f);
@@ -2572,7 +2577,7 @@ int splatct_fvr_backward(const double* params, int64_t n, int w, int h, int c, i
     int use_tma = 0;
     if (fast && !getenv("SPLATCT_BWD_NO_TMA"))
         use_tma = volume_tensor_map(&utmap, up_yxz, w, h, c, BT_ZB, 17, 1, false) &&
-                          volume_tensor_map(&utmap2, up_yxz, w, h, c, BT_ZB, 17, 2, false)
+                          volume_tensor_map(&utmap2, up_yxz, w, h, c, BT_ZB, 17, BT2_ROWS, false)
                       ? 1 : 0;
     if (!use_tma) {
         memset(&utmap, 0, sizeof(utmap));
