@@ -2288,6 +2288,272 @@ __global__ void __launch_bounds__(32 * BT_WARPS, 1)
     if (ld2) tc::mbar_wait(reinterpret_cast<uint64_t*>(&sbar[2]), (ld2 - 1u) & 1u);
 }
 
+// --------------------------------------------------------------------------
+// backward, tile-staged and asynchronous (SPLATCT_BWD_KERNEL=ts2).
+//
+// Same staging as k_fvr_bwd_ts (a tile column's upstream slabs, 32 x 32 x 16
+// floats with the 64 B swizzle, one TMA box each, a 3-slab ring), but without
+// any block-wide barrier per tile: a producer warp claims work units (a tile
+// column x BT2Z_CH z tiles), publishes them through a 2-entry unit queue and
+// streams the unit's slabs into the ring, each slab behind a "full" mbarrier
+// and released by an "empty" mbarrier that every consumer warp arrives on
+// once it has moved past the slab's last user tile.  The 16 consumer warps
+// claim 32-pair chunks of the unit's tiles from a shared counter, in tile
+// order, so they spread over at most two neighbouring tiles instead of idling
+// at a per-tile barrier; each chunk's first-tile Gaussians are summed from
+// the staged slabs exactly as in k_fvr_bwd_ts (bit-identical moments).
+// --------------------------------------------------------------------------
+constexpr int BT2Z_CONS = 16;                  // consumer warps
+constexpr int BT2Z_CH = 8;                     // z tiles per unit
+constexpr int BT2Z_THREADS = 32 * (BT2Z_CONS + 1);
+
+struct BtUnit {
+    int tx, ty, tz0, ntiles, nslabs;
+    uint32_t seq0;                 // ring sequence number of the unit's first slab
+    int end;                       // 1: no more units
+    uint32_t beg[BT2Z_CH], nch[BT2Z_CH + 1];   // pair begin per tile, chunk prefix
+    uint32_t pend[BT2Z_CH];        // pair end per tile
+};
+
+__global__ void __launch_bounds__(BT2Z_THREADS, 1)
+    k_fvr_bwd_ts2(const double* __restrict__ P, int64_t n, const uint32_t* __restrict__ svals,
+                  const uint32_t* __restrict__ tstart, int ntx, int nty, int ntz, int Sl,
+                  const int32_t* __restrict__ fp, const GRec* __restrict__ rec, int w, int h,
+                  int c, int zoff, const float* __restrict__ up,
+                  const __grid_constant__ CUtensorMap utmap, unsigned int* __restrict__ counter,
+                  double* __restrict__ G, double* __restrict__ accum, const int* halt) {
+    griddep_wait();
+    if (halted(halt)) return;
+    extern __shared__ __align__(1024) float slab[];      // [3][y 32][x 32][z 16]
+    __shared__ BtWarp wt[BT2Z_CONS];
+    __shared__ BtUnit uq[2];
+    __shared__ unsigned int uchunk[2];
+    __shared__ __align__(8) uint64_t full[3], empty[3], ufull[2], uempty[2];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        for (int b = 0; b < 3; ++b) {
+            tc::mbar_init(&full[b], 1);
+            tc::mbar_init(&empty[b], BT2Z_CONS);
+        }
+        for (int e = 0; e < 2; ++e) {
+            tc::mbar_init(&ufull[e], 1);
+            tc::mbar_init(&uempty[e], BT2Z_CONS);
+        }
+        tc::mbar_init_fence();
+    }
+    __syncthreads();
+    const int64_t nxy = (int64_t)ntx * nty;
+    const int nzch = (ntz + BT2Z_CH - 1) / BT2Z_CH;
+    const int units = ntx * nty * nzch;
+    if (warp == BT2Z_CONS) {
+        // ------------------------------------------------------------ producer
+        if (lane == 0) {
+            uint32_t seq = 0;
+            for (uint32_t k = 0;; ++k) {
+                const int e = k & 1;
+                tc::mbar_wait(&uempty[e], ((k >> 1) & 1) ^ 1);   // the entry is free
+                const int u = (int)atomicAdd(counter, 1u);
+                BtUnit& U = uq[e];
+                if (u >= units) {
+                    U.end = 1;
+                    tc::mbar_arrive(&ufull[e]);
+                    break;
+                }
+                const int col = u / nzch, ch = u % nzch;
+                U.end = 0;
+                U.tx = col % ntx;
+                U.ty = col / ntx;
+                U.tz0 = ch * BT2Z_CH;
+                U.ntiles = min(ntz, U.tz0 + BT2Z_CH) - U.tz0;
+                U.nslabs = min(U.ntiles + 1, ntz - U.tz0);
+                U.seq0 = seq;
+                uint32_t acc = 0;
+                U.nch[0] = 0;
+                for (int i = 0; i < U.ntiles; ++i) {
+                    const int64_t t = (int64_t)(U.tz0 + i) * nxy + (int64_t)U.ty * ntx + U.tx;
+                    const uint32_t b0 = tstart[t], b1 = tstart[t + 1];
+                    U.beg[i] = b0;
+                    U.pend[i] = b1;
+                    acc += (b1 - b0 + 31u) >> 5;
+                    U.nch[i + 1] = acc;
+                }
+                uchunk[e] = 0u;
+                tc::mbar_arrive(&ufull[e]);   // release: the entry is written
+                for (int i = 0; i < U.nslabs; ++i, ++seq) {
+                    const int b = seq % 3;
+                    tc::mbar_wait(&empty[b], ((seq / 3) & 1) ^ 1);   // its last user is done
+                    const unsigned bar = tc::smem_u32(&full[b]);
+                    const unsigned dst = tc::smem_u32(slab + b * BT_SLAB);
+                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar),
+                                 "r"(BT_SLAB_BYTES)
+                                 : "memory");
+                    asm volatile(
+                        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
+                        "[%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(dst),
+                        "l"(&utmap), "r"(16 * (U.tz0 + i)), "r"(16 * U.tx), "r"(16 * U.ty), "r"(bar)
+                        : "memory");
+                }
+            }
+        }
+        return;
+    }
+    // -------------------------------------------------------------- consumers
+    const uint32_t smask = (1u << Sl) - 1u;
+    BtWarp& W = wt[warp];
+    for (uint32_t k = 0;; ++k) {
+        const int e = k & 1;
+        tc::mbar_wait(&ufull[e], (k >> 1) & 1);
+        const BtUnit& U = uq[e];
+        if (U.end) break;
+        const uint32_t total = U.nch[U.ntiles];
+        int rel = 0;   // this warp's released slabs of the unit
+        int cur = -1, waited = -1;
+        // a slab is released only after it landed: the arrival then belongs to
+        // this use of the buffer, and no load is in flight when the CTA exits
+        auto release_below = [&](int lim) {
+            for (; rel < lim; ++rel) {
+                const uint32_t q = U.seq0 + rel;
+                if (rel > waited) {
+                    tc::mbar_wait(&full[q % 3], (q / 3) & 1);
+                    waited = rel;
+                }
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&empty[q % 3]);
+            }
+        };
+        for (;;) {
+            uint32_t cidx = 0;
+            if (lane == 0) cidx = atomicAdd(&uchunk[e], 1u);
+            cidx = __shfl_sync(0xffffffffu, cidx, 0);
+            if (cidx >= total) break;
+            int i = 0;
+            while (U.nch[i + 1] <= cidx) ++i;
+            if (i != cur) {   // moved on: slabs before tile i have no more users here
+                cur = i;
+                release_below(i);
+                for (int sl = max(waited + 1, i); sl <= i + 1 && sl < U.nslabs; ++sl) {
+                    const uint32_t q = U.seq0 + sl;
+                    tc::mbar_wait(&full[q % 3], (q / 3) & 1);
+                    waited = sl;
+                }
+            }
+            const int tz = U.tz0 + i;
+            const int bA = (U.seq0 + i) % 3, bB = (U.seq0 + i + 1) % 3;
+            const uint32_t j = U.beg[i] + ((cidx - U.nch[i]) << 5) + lane;
+            const uint32_t v = j < U.pend[i] ? svals[j] : 1u;
+            unsigned first = __ballot_sync(0xffffffffu, j < U.pend[i] && (v & smask) == 0u);
+            while (first) {
+                const int src = __ffs(first) - 1;
+                first &= first - 1u;
+                const int64_t gi = (int64_t)(__shfl_sync(0xffffffffu, v, src) >> Sl);
+                const int xlo = fp[6 * gi], xhi = fp[6 * gi + 1], ylo = fp[6 * gi + 2];
+                const int yhi = fp[6 * gi + 3], zlo = fp[6 * gi + 4], zhi = fp[6 * gi + 5];
+                const GRec r = rec[gi];
+                float S0 = 0.f, Sx = 0.f, Sy = 0.f, Sz = 0.f, S2 = 0.f;
+                if (xhi - xlo == 16 && yhi - ylo == 16 && zhi - zlo == 16) {
+                    __syncwarp();
+                    if (lane < 17) {
+                        const float ry = (float)(ylo + lane - r.fy) - r.dy;
+                        const float ey = exp2f(-r.inv2 * ry * ry);
+                        W.ey[lane] = make_float4(ey, ey * ry, ey * ry * ry, 0.f);
+                    }
+                    __syncwarp();
+                    const int hf = lane >> 4, zl = lane & 15;
+                    const int xr = xlo - 16 * U.tx, yr = ylo - 16 * U.ty;
+                    auto soff = [&](int colr, int za) {
+                        const int rr = yr * 32 + xr + colr, zz = za & 15;
+                        return ((za >> 4) == tz ? bA : bB) * BT_SLAB + rr * 16 +
+                               (((zz >> 2) ^ ((rr >> 1) & 3)) << 2) + (zz & 3);
+                    };
+                    int off[9];
+#pragma unroll
+                    for (int kk = 0; kk < 9; ++kk) off[kk] = soff(min(2 * kk + hf, 16), zlo + zl);
+                    const int pl = lane < 17 ? lane : 16;
+                    const int offp = soff(pl, zlo + 16);
+                    const float rz = (float)(zlo + zl + zoff - r.fz) - r.dz;
+                    const float ez = exp2f(-r.inv2 * rz * rz);
+                    const float rz16 = (float)(zlo + 16 + zoff - r.fz) - r.dz;
+                    const float ez16 = exp2f(-r.inv2 * rz16 * rz16);
+                    float2 wx01[9];
+                    float wx2[9];
+#pragma unroll
+                    for (int kk = 0; kk < 9; ++kk) {
+                        const float rx = (float)(xlo + 2 * kk + hf - r.fx) - r.dx;
+                        const float ex = (kk < 8 || !hf) ? exp2f(-r.inv2 * rx * rx) : 0.f;
+                        wx01[kk] = make_float2(ex, ex * rx);
+                        wx2[kk] = ex * rx * rx;
+                    }
+                    const float rxp = (float)(xlo + lane - r.fx) - r.dx;
+                    const float exq = lane < 17 ? exp2f(-r.inv2 * rxp * rxp) : 0.f;
+                    float A0 = 0.f, Ax = 0.f, Ay = 0.f, Ar = 0.f, P0 = 0.f, P1 = 0.f, P2 = 0.f;
+#pragma unroll
+                    for (int yi = 0; yi < 17; ++yi) {
+                        float2 C01 = make_float2(0.f, 0.f);
+                        float C2 = 0.f;
+#pragma unroll
+                        for (int kk = 0; kk < 9; ++kk) {
+                            const float uu = slab[off[kk] + 512 * yi];
+                            C01 = ffma2(make_float2(uu, uu), wx01[kk], C01);
+                            C2 = fmaf(wx2[kk], uu, C2);
+                        }
+                        const float pu = slab[offp + 512 * yi];
+                        const float4 t = W.ey[yi];
+                        A0 = fmaf(t.x, C01.x, A0);
+                        Ax = fmaf(t.x, C01.y, Ax);
+                        Ay = fmaf(t.y, C01.x, Ay);
+                        Ar = fmaf(t.x, C2, fmaf(t.z, C01.x, Ar));
+                        P0 = fmaf(t.x, pu, P0);
+                        P1 = fmaf(t.y, pu, P1);
+                        P2 = fmaf(t.z, pu, P2);
+                    }
+                    A0 += __shfl_xor_sync(0xffffffffu, A0, 16);
+                    Ax += __shfl_xor_sync(0xffffffffu, Ax, 16);
+                    Ay += __shfl_xor_sync(0xffffffffu, Ay, 16);
+                    Ar += __shfl_xor_sync(0xffffffffu, Ar, 16);
+                    const float eh = hf ? 0.f : ez;
+                    S0 = eh * A0;
+                    Sx = eh * Ax;
+                    Sy = eh * Ay;
+                    Sz = eh * rz * A0;
+                    S2 = eh * fmaf(rz * rz, A0, Ar);
+                    const float Q0 = exq * P0, Qx = exq * rxp * P0, Qy = exq * P1;
+                    const float Qr = fmaf(exq * rxp * rxp, P0, exq * P2);
+                    S0 = fmaf(ez16, Q0, S0);
+                    Sx = fmaf(ez16, Qx, Sx);
+                    Sy = fmaf(ez16, Qy, Sy);
+                    Sz = fmaf(ez16 * rz16, Q0, Sz);
+                    S2 = fmaf(ez16, fmaf(rz16 * rz16, Q0, Qr), S2);
+                } else {
+                    bwd_moments17<false>(r, xlo, xhi - xlo + 1, ylo, yhi - ylo + 1, zlo,
+                                         zhi - zlo + 1, w, c, zoff, up, S0, Sx, Sy, Sz, S2);
+                }
+                S0 = warp_sum(S0);
+                Sx = warp_sum(Sx);
+                Sy = warp_sum(Sy);
+                Sz = warp_sum(Sz);
+                S2 = warp_sum(S2);
+                if (lane == 0) {   // chain rule in f64 (fvr.py:227-273)
+                    const double amp = P[4 * n + gi], sg = P[3 * n + gi];
+                    const double inv_s2 = 1.0 / (sg * sg), inv_s3 = inv_s2 / sg;
+                    const double k2 = amp * inv_s2;
+                    const double gx = k2 * Sx, gy = k2 * Sy, gz = k2 * Sz;
+                    G[gi] = gx;
+                    G[n + gi] = gy;
+                    G[2 * n + gi] = gz;
+                    G[3 * n + gi] = amp * inv_s3 * S2;
+                    G[4 * n + gi] = S0;
+                    if (accum) accum[gi] += sqrt(gx * gx + gy * gy + gz * gz);
+                }
+            }
+        }
+        // the unit's remaining slabs and its queue entry are released
+        release_below(U.nslabs);
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&uempty[e]);
+    }
+}
+
 __global__ void k_grad_norm_accum(const double* __restrict__ G, int64_t n,
                                   double* __restrict__ accum, const int* halt) {
     if (halted(halt)) return;
@@ -2506,6 +2772,28 @@ int splatct_fvr_backward(const double* params, int64_t n, int w, int h, int c, i
     const unsigned grid = (unsigned)((n + BG_WARPS - 1) / BG_WARPS);
     const bool fast = 2 * hx + 1 <= 17 && 2 * hz + 1 <= 17;
     const char* kern = getenv("SPLATCT_BWD_KERNEL");   // "warp" / "sp": the other kernels
+    if (fast && 2 * hy + 1 <= 17 && kern && !strcmp(kern, "ts2")) {
+        CUtensorMap smap;
+        if (volume_tensor_map(&smap, up_yxz, w, h, c, 16, 32, 32, true)) {
+            SPLATCT_CK(cudaMemsetAsync(grads, 0, sizeof(double) * 5 * (size_t)n, s));
+            unsigned int* counter = at<uint32_t>(ws, L.o_tcount) + 1;
+            SPLATCT_CK(cudaMemsetAsync(counter, 0, sizeof(unsigned int), s));
+            int dev = 0, nsm = 148;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+            const size_t dyn = 3 * (size_t)BT_SLAB_BYTES;
+            cudaFuncSetAttribute(k_fvr_bwd_ts2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+            const size_t vs = L.final_buf ? L.o_v1 : L.o_v0;
+            SPLATCT_CK(launch_pdl(k_fvr_bwd_ts2, dim3(nsm), dim3(BT2Z_THREADS), dyn, s, params, n,
+                                  (const uint32_t*)at<uint32_t>(ws, vs),
+                                  (const uint32_t*)at<uint32_t>(ws, L.o_tstart), L.ntx, L.nty,
+                                  L.ntz, L.Sl, (const int32_t*)at<int32_t>(ws, L.o_fp),
+                                  (const GRec*)at<GRec>(ws, L.o_rec), w, h, c, z0, up_yxz, smap,
+                                  counter, grads, accum, halt));
+            SPLATCT_LAUNCH_CK();
+            return SPLATCT_OK;
+        }
+    }
     if (fast && 2 * hy + 1 <= 17 && kern && !strcmp(kern, "ts")) {
         CUtensorMap smap;
         if (volume_tensor_map(&smap, up_yxz, w, h, c, 16, 32, 32, true)) {   // 64 B swizzle

@@ -133,7 +133,8 @@ def test_deep_volume_has_no_occupancy_mask():
 
 # backward kernel variants: the spatially ordered persistent kernel (default),
 # and the per-Gaussian-warp kernel with TMA-fed rows or direct loads
-BWD_VARIANTS = {"ts": {"SPLATCT_BWD_KERNEL": "ts"}, "sp": {"SPLATCT_BWD_KERNEL": "sp"},
+BWD_VARIANTS = {"ts": {"SPLATCT_BWD_KERNEL": "ts"}, "ts2": {"SPLATCT_BWD_KERNEL": "ts2"},
+                "sp": {"SPLATCT_BWD_KERNEL": "sp"},
                 "warp_tma": {},
                 "warp_direct": {"SPLATCT_BWD_NO_TMA": "1"}}
 
