@@ -2081,6 +2081,110 @@ struct __align__(16) BtWarp {
     float4 ey[17];      // {ey, ey ry, ey ry^2, 0} per box row
 };
 
+// Moments of one full-box (17^3) Gaussian from a staged tile column: slab
+// buffers bA (z tile tz) and bB (tz + 1), each [y 32][x 32][z 16] floats in
+// the 64 B swizzle, (xr, yr) the box origin inside the 32 x 32 window.  Lanes:
+// column parity hf x slice zl (slices 0..15 of the box, columns 2k + hf); the
+// 17th slice with lanes over columns.  ey holds {ey, ey ry, ey ry^2} per row.
+// Used by k_fvr_bwd_ts and k_fvr_bwd_ts2 (identical arithmetic, bitwise equal).
+__device__ __forceinline__ void bt_full_moments(const float* __restrict__ slab, int bA, int bB,
+                                                int tz, int xr, int yr, const GRec& r, int xlo,
+                                                int zlo, int zoff, const float4* ey, int lane,
+                                                float& S0, float& Sx, float& Sy, float& Sz,
+                                                float& S2) {
+    const int hf = lane >> 4, zl = lane & 15;
+    auto soff = [&](int colr, int za) {
+        const int rr = yr * 32 + xr + colr, zz = za & 15;
+        return ((za >> 4) == tz ? bA : bB) * BT_SLAB + rr * 16 +
+               (((zz >> 2) ^ ((rr >> 1) & 3)) << 2) + (zz & 3);
+    };
+    int off[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) off[k] = soff(min(2 * k + hf, 16), zlo + zl);
+    const int pl = lane < 17 ? lane : 16;
+    const int offp = soff(pl, zlo + 16);
+    const float rz = (float)(zlo + zl + zoff - r.fz) - r.dz;
+    const float ez = exp2f(-r.inv2 * rz * rz);
+    const float rz16 = (float)(zlo + 16 + zoff - r.fz) - r.dz;
+    const float ez16 = exp2f(-r.inv2 * rz16 * rz16);
+    float2 wx01[9];
+    float wx2[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+        const float rx = (float)(xlo + 2 * k + hf - r.fx) - r.dx;
+        const float ex = (k < 8 || !hf) ? exp2f(-r.inv2 * rx * rx) : 0.f;
+        wx01[k] = make_float2(ex, ex * rx);
+        wx2[k] = ex * rx * rx;
+    }
+    const float rxp = (float)(xlo + lane - r.fx) - r.dx;
+    const float exq = lane < 17 ? exp2f(-r.inv2 * rxp * rxp) : 0.f;
+    float A0 = 0.f, Ax = 0.f, Ay = 0.f, Ar = 0.f, P0 = 0.f, P1 = 0.f, P2 = 0.f;
+#pragma unroll
+    for (int yi = 0; yi < 17; ++yi) {
+        float2 C01 = make_float2(0.f, 0.f);
+        float C2 = 0.f;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) {
+            const float uu = slab[off[k] + 512 * yi];
+            C01 = ffma2(make_float2(uu, uu), wx01[k], C01);
+            C2 = fmaf(wx2[k], uu, C2);
+        }
+        const float pu = slab[offp + 512 * yi];
+        const float4 t = ey[yi];
+        A0 = fmaf(t.x, C01.x, A0);
+        Ax = fmaf(t.x, C01.y, Ax);
+        Ay = fmaf(t.y, C01.x, Ay);
+        Ar = fmaf(t.x, C2, fmaf(t.z, C01.x, Ar));
+        P0 = fmaf(t.x, pu, P0);
+        P1 = fmaf(t.y, pu, P1);
+        P2 = fmaf(t.z, pu, P2);
+    }
+    A0 += __shfl_xor_sync(0xffffffffu, A0, 16);
+    Ax += __shfl_xor_sync(0xffffffffu, Ax, 16);
+    Ay += __shfl_xor_sync(0xffffffffu, Ay, 16);
+    Ar += __shfl_xor_sync(0xffffffffu, Ar, 16);
+    const float eh = hf ? 0.f : ez;
+    S0 = eh * A0;
+    Sx = eh * Ax;
+    Sy = eh * Ay;
+    Sz = eh * rz * A0;
+    S2 = eh * fmaf(rz * rz, A0, Ar);
+    const float Q0 = exq * P0, Qx = exq * rxp * P0, Qy = exq * P1;
+    const float Qr = fmaf(exq * rxp * rxp, P0, exq * P2);
+    S0 = fmaf(ez16, Q0, S0);
+    Sx = fmaf(ez16, Qx, Sx);
+    Sy = fmaf(ez16, Qy, Sy);
+    Sz = fmaf(ez16 * rz16, Q0, Sz);
+    S2 = fmaf(ez16, fmaf(rz16 * rz16, Q0, Qr), S2);
+}
+
+// the warp's per-row table {ey, ey ry, ey ry^2} for a full box starting at row ylo
+__device__ __forceinline__ void bt_row_table(float4* ey, const GRec& r, int ylo, int lane) {
+    __syncwarp();
+    if (lane < 17) {
+        const float ry = (float)(ylo + lane - r.fy) - r.dy;
+        const float e = exp2f(-r.inv2 * ry * ry);
+        ey[lane] = make_float4(e, e * ry, e * ry * ry, 0.f);
+    }
+    __syncwarp();
+}
+
+// f64 chain rule of one Gaussian's moments (fvr.py:227-273), lane 0
+__device__ __forceinline__ void bt_chain(const double* __restrict__ P, int64_t n, int64_t gi,
+                                         float S0, float Sx, float Sy, float Sz, float S2,
+                                         double* __restrict__ G, double* __restrict__ accum) {
+    const double amp = P[4 * n + gi], sg = P[3 * n + gi];
+    const double inv_s2 = 1.0 / (sg * sg), inv_s3 = inv_s2 / sg;
+    const double k2 = amp * inv_s2;
+    const double gx = k2 * Sx, gy = k2 * Sy, gz = k2 * Sz;
+    G[gi] = gx;
+    G[n + gi] = gy;
+    G[2 * n + gi] = gz;
+    G[3 * n + gi] = amp * inv_s3 * S2;
+    G[4 * n + gi] = S0;
+    if (accum) accum[gi] += sqrt(gx * gx + gy * gy + gz * gz);
+}
+
 __global__ void __launch_bounds__(32 * BT_WARPS, 1)
     k_fvr_bwd_ts(const double* __restrict__ P, int64_t n, const uint32_t* __restrict__ svals,
                  const uint32_t* __restrict__ tstart, int ntx, int nty, int ntz, int Sl,
@@ -2180,82 +2284,9 @@ __global__ void __launch_bounds__(32 * BT_WARPS, 1)
                     float S0 = 0.f, Sx = 0.f, Sy = 0.f, Sz = 0.f, S2 = 0.f;
                     if (xhi - xlo == 16 && yhi - ylo == 16 && zhi - zlo == 16) {
                         BtWarp& W = wt[warp];
-                        __syncwarp();
-                        if (lane < 17) {
-                            const float ry = (float)(ylo + lane - r.fy) - r.dy;
-                            const float ey = exp2f(-r.inv2 * ry * ry);
-                            W.ey[lane] = make_float4(ey, ey * ry, ey * ry * ry, 0.f);
-                        }
-                        __syncwarp();
-                        // lanes: column parity hf x slice zl (slices 0..15 of the box,
-                        // column pairs k: column 2k + hf); the 17th slice with lanes
-                        // over columns.  Ring offsets (floats) for row ylo; a row adds
-                        // 512 (the 64-byte swizzle depends on x only).
-                        const int hf = lane >> 4, zl = lane & 15;
-                        const int xr = xlo - 16 * tx, yr = ylo - 16 * ty;
-                        auto soff = [&](int colr, int za) {
-                            const int rr = yr * 32 + xr + colr, zz = za & 15;
-                            return ((za >> 4) % 3) * BT_SLAB + rr * 16 +
-                                   (((zz >> 2) ^ ((rr >> 1) & 3)) << 2) + (zz & 3);
-                        };
-                        int off[9];
-#pragma unroll
-                        for (int k = 0; k < 9; ++k) off[k] = soff(min(2 * k + hf, 16), zlo + zl);
-                        const int pl = lane < 17 ? lane : 16;
-                        const int offp = soff(pl, zlo + 16);
-                        const float rz = (float)(zlo + zl + zoff - r.fz) - r.dz;
-                        const float ez = exp2f(-r.inv2 * rz * rz);
-                        const float rz16 = (float)(zlo + 16 + zoff - r.fz) - r.dz;
-                        const float ez16 = exp2f(-r.inv2 * rz16 * rz16);
-                        float2 wx01[9];
-                        float wx2[9];
-#pragma unroll
-                        for (int k = 0; k < 9; ++k) {
-                            const float rx = (float)(xlo + 2 * k + hf - r.fx) - r.dx;
-                            const float ex = (k < 8 || !hf) ? exp2f(-r.inv2 * rx * rx) : 0.f;
-                            wx01[k] = make_float2(ex, ex * rx);
-                            wx2[k] = ex * rx * rx;
-                        }
-                        const float rxp = (float)(xlo + lane - r.fx) - r.dx;
-                        const float exq = lane < 17 ? exp2f(-r.inv2 * rxp * rxp) : 0.f;
-                        float A0 = 0.f, Ax = 0.f, Ay = 0.f, Ar = 0.f, P0 = 0.f, P1 = 0.f, P2 = 0.f;
-#pragma unroll
-                        for (int yi = 0; yi < 17; ++yi) {
-                            float2 C01 = make_float2(0.f, 0.f);
-                            float C2 = 0.f;
-#pragma unroll
-                            for (int k = 0; k < 9; ++k) {
-                                const float uu = slab[off[k] + 512 * yi];
-                                C01 = ffma2(make_float2(uu, uu), wx01[k], C01);
-                                C2 = fmaf(wx2[k], uu, C2);
-                            }
-                            const float pu = slab[offp + 512 * yi];
-                            const float4 t = W.ey[yi];
-                            A0 = fmaf(t.x, C01.x, A0);
-                            Ax = fmaf(t.x, C01.y, Ax);
-                            Ay = fmaf(t.y, C01.x, Ay);
-                            Ar = fmaf(t.x, C2, fmaf(t.z, C01.x, Ar));
-                            P0 = fmaf(t.x, pu, P0);
-                            P1 = fmaf(t.y, pu, P1);
-                            P2 = fmaf(t.z, pu, P2);
-                        }
-                        A0 += __shfl_xor_sync(0xffffffffu, A0, 16);
-                        Ax += __shfl_xor_sync(0xffffffffu, Ax, 16);
-                        Ay += __shfl_xor_sync(0xffffffffu, Ay, 16);
-                        Ar += __shfl_xor_sync(0xffffffffu, Ar, 16);
-                        const float eh = hf ? 0.f : ez;
-                        S0 = eh * A0;
-                        Sx = eh * Ax;
-                        Sy = eh * Ay;
-                        Sz = eh * rz * A0;
-                        S2 = eh * fmaf(rz * rz, A0, Ar);
-                        const float Q0 = exq * P0, Qx = exq * rxp * P0, Qy = exq * P1;
-                        const float Qr = fmaf(exq * rxp * rxp, P0, exq * P2);
-                        S0 = fmaf(ez16, Q0, S0);
-                        Sx = fmaf(ez16, Qx, Sx);
-                        Sy = fmaf(ez16, Qy, Sy);
-                        Sz = fmaf(ez16 * rz16, Q0, Sz);
-                        S2 = fmaf(ez16, fmaf(rz16 * rz16, Q0, Qr), S2);
+                        bt_row_table(W.ey, r, ylo, lane);
+                        bt_full_moments(slab, tz % 3, (tz + 1) % 3, tz, xlo - 16 * tx, ylo - 16 * ty,
+                                        r, xlo, zlo, zoff, W.ey, lane, S0, Sx, Sy, Sz, S2);
                     } else {
                         bwd_moments17<false>(r, xlo, xhi - xlo + 1, ylo, yhi - ylo + 1, zlo,
                                              zhi - zlo + 1, w, c, zoff, up, S0, Sx, Sy, Sz, S2);
@@ -2292,27 +2323,34 @@ __global__ void __launch_bounds__(32 * BT_WARPS, 1)
 // backward, tile-staged and asynchronous (SPLATCT_BWD_KERNEL=ts2).
 //
 // Same staging as k_fvr_bwd_ts (a tile column's upstream slabs, 32 x 32 x 16
-// floats with the 64 B swizzle, one TMA box each, a 3-slab ring), but without
-// any block-wide barrier per tile: a producer warp claims work units (a tile
-// column x BT2Z_CH z tiles), publishes them through a 2-entry unit queue and
-// streams the unit's slabs into the ring, each slab behind a "full" mbarrier
-// and released by an "empty" mbarrier that every consumer warp arrives on
-// once it has moved past the slab's last user tile.  The 16 consumer warps
-// claim 32-pair chunks of the unit's tiles from a shared counter, in tile
-// order, so they spread over at most two neighbouring tiles instead of idling
-// at a per-tile barrier; each chunk's first-tile Gaussians are summed from
-// the staged slabs exactly as in k_fvr_bwd_ts (bit-identical moments).
+// floats with the 64 B swizzle, one TMA box each, a 3-slab ring), but no
+// block-wide barrier per tile.  A producer warp claims work units (a tile
+// column x BT2Z_CH z tiles), scans the unit's tile bins for the Gaussians
+// whose first tile each tile is (slot 0), publishes that list through a
+// 2-entry queue (an entry is cut early when the list is full, so any density
+// fits), and streams only the slabs those Gaussians read into the ring, each
+// behind a "full" mbarrier and released through an "empty" mbarrier that
+// every consumer warp arrives on once it has moved past the slab.  Consumer
+// warps claim single Gaussians from the entry in tile order, so a tile's
+// Gaussians run concurrently while later slabs land.  Per Gaussian the
+// arithmetic is k_fvr_bwd_ts's (bit-identical moments).
 // --------------------------------------------------------------------------
-constexpr int BT2Z_CONS = 16;                  // consumer warps
-constexpr int BT2Z_CH = 8;                     // z tiles per unit
-constexpr int BT2Z_THREADS = 32 * (BT2Z_CONS + 1);
+#ifndef BT2Z_CONS_N
+#define BT2Z_CONS_N 16
+#endif
+constexpr int BT2Z_CONS = BT2Z_CONS_N;            // consumer warps
+#ifndef BT2Z_CH_N
+#define BT2Z_CH_N 4
+#endif
+constexpr int BT2Z_CH = BT2Z_CH_N;                // z tiles per claimed unit
+constexpr int BT2Z_CAP = 1024;                    // Gaussians per queue entry
+constexpr int BT2Z_THREADS = 32 * (BT2Z_CONS + 2);   // + scanner + loader warps
 
-struct BtUnit {
-    int tx, ty, tz0, ntiles, nslabs;
-    uint32_t seq0;                 // ring sequence number of the unit's first slab
-    int end;                       // 1: no more units
-    uint32_t beg[BT2Z_CH], nch[BT2Z_CH + 1];   // pair begin per tile, chunk prefix
-    uint32_t pend[BT2Z_CH];        // pair end per tile
+struct BtEntry {
+    int tx, ty, tz0, ntiles, end;
+    int gofs[BT2Z_CH + 1];   // list prefix per tile
+    int sseq[BT2Z_CH + 1];   // ring sequence number of slab tz0 + i, or -1 (not needed)
+    uint32_t gl[BT2Z_CAP];   // Gaussian ids, tile order, ascending pair order per tile
 };
 
 __global__ void __launch_bounds__(BT2Z_THREADS, 1)
@@ -2326,8 +2364,8 @@ __global__ void __launch_bounds__(BT2Z_THREADS, 1)
     if (halted(halt)) return;
     extern __shared__ __align__(1024) float slab[];      // [3][y 32][x 32][z 16]
     __shared__ BtWarp wt[BT2Z_CONS];
-    __shared__ BtUnit uq[2];
-    __shared__ unsigned int uchunk[2];
+    __shared__ BtEntry uq[2];
+    __shared__ unsigned int uclaim[2];
     __shared__ __align__(8) uint64_t full[3], empty[3], ufull[2], uempty[2];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
@@ -2337,218 +2375,202 @@ __global__ void __launch_bounds__(BT2Z_THREADS, 1)
         }
         for (int e = 0; e < 2; ++e) {
             tc::mbar_init(&ufull[e], 1);
-            tc::mbar_init(&uempty[e], BT2Z_CONS);
+            tc::mbar_init(&uempty[e], BT2Z_CONS + 1);   // consumers + the loader
         }
         tc::mbar_init_fence();
     }
     __syncthreads();
     const int64_t nxy = (int64_t)ntx * nty;
-    const int nzch = (ntz + BT2Z_CH - 1) / BT2Z_CH;
-    const int units = ntx * nty * nzch;
-    if (warp == BT2Z_CONS) {
-        // ------------------------------------------------------------ producer
+    const uint32_t smask = (1u << Sl) - 1u;
+    if (warp == BT2Z_CONS + 1) {
+        // -------------------------------------------------------------- loader
+        // streams each entry's needed slabs into the ring, in sequence order
         if (lane == 0) {
-            uint32_t seq = 0;
             for (uint32_t k = 0;; ++k) {
                 const int e = k & 1;
-                tc::mbar_wait(&uempty[e], ((k >> 1) & 1) ^ 1);   // the entry is free
-                const int u = (int)atomicAdd(counter, 1u);
-                BtUnit& U = uq[e];
-                if (u >= units) {
-                    U.end = 1;
-                    tc::mbar_arrive(&ufull[e]);
-                    break;
-                }
-                const int col = u / nzch, ch = u % nzch;
-                U.end = 0;
-                U.tx = col % ntx;
-                U.ty = col / ntx;
-                U.tz0 = ch * BT2Z_CH;
-                U.ntiles = min(ntz, U.tz0 + BT2Z_CH) - U.tz0;
-                U.nslabs = min(U.ntiles + 1, ntz - U.tz0);
-                U.seq0 = seq;
-                uint32_t acc = 0;
-                U.nch[0] = 0;
-                for (int i = 0; i < U.ntiles; ++i) {
-                    const int64_t t = (int64_t)(U.tz0 + i) * nxy + (int64_t)U.ty * ntx + U.tx;
-                    const uint32_t b0 = tstart[t], b1 = tstart[t + 1];
-                    U.beg[i] = b0;
-                    U.pend[i] = b1;
-                    acc += (b1 - b0 + 31u) >> 5;
-                    U.nch[i + 1] = acc;
-                }
-                uchunk[e] = 0u;
-                tc::mbar_arrive(&ufull[e]);   // release: the entry is written
-                for (int i = 0; i < U.nslabs; ++i, ++seq) {
-                    const int b = seq % 3;
-                    tc::mbar_wait(&empty[b], ((seq / 3) & 1) ^ 1);   // its last user is done
+                tc::mbar_wait(&ufull[e], (k >> 1) & 1);
+                const BtEntry& U = uq[e];
+                if (U.end) break;
+                const int tx = U.tx, ty = U.ty, t0 = U.tz0, nt = U.ntiles;
+                int sq[BT2Z_CH + 1];
+#pragma unroll
+                for (int i = 0; i <= BT2Z_CH; ++i) sq[i] = i <= nt ? U.sseq[i] : -1;
+                tc::mbar_arrive(&uempty[e]);   // done reading the entry
+#pragma unroll
+                for (int i = 0; i <= BT2Z_CH; ++i) {
+                    const int q = sq[i];
+                    if (q < 0) continue;
+                    const int b = q % 3;
+                    tc::mbar_wait(&empty[b], ((q / 3) & 1) ^ 1);   // its last reader is done
                     const unsigned bar = tc::smem_u32(&full[b]);
                     const unsigned dst = tc::smem_u32(slab + b * BT_SLAB);
-                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar),
                                  "r"(BT_SLAB_BYTES)
                                  : "memory");
                     asm volatile(
                         "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
                         "[%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(dst),
-                        "l"(&utmap), "r"(16 * (U.tz0 + i)), "r"(16 * U.tx), "r"(16 * U.ty), "r"(bar)
+                        "l"(&utmap), "r"(16 * (t0 + i)), "r"(16 * tx), "r"(16 * ty), "r"(bar)
                         : "memory");
                 }
             }
         }
         return;
     }
+    if (warp == BT2Z_CONS) {
+        // ------------------------------------------------------------- scanner
+        const int nzch = (ntz + BT2Z_CH - 1) / BT2Z_CH;
+        const int units = ntx * nty * nzch;
+        uint32_t k = 0, seq = 0;
+        for (;;) {
+            int u = 0;
+            if (lane == 0) u = (int)atomicAdd(counter, 1u);
+            u = __shfl_sync(0xffffffffu, u, 0);
+            const bool last = u >= units;
+            const int col = last ? 0 : u / nzch, ch = last ? 0 : u % nzch;
+            const int tx = col % ntx, ty = col / ntx;
+            const int tzA = ch * BT2Z_CH, tzE = last ? 0 : min(ntz, tzA + BT2Z_CH);
+            // a claimed unit becomes one or more queue entries (cut when full)
+            // the unit's tile bounds, one load per lane: lane 2i / 2i + 1 hold the
+            // pair range of tile tzA + i
+            uint32_t tb = 0u;
+            if (lane < 2 * (tzE - tzA))
+                tb = tstart[(int64_t)(tzA + (lane >> 1)) * nxy + (int64_t)ty * ntx + tx + (lane & 1)];
+            int tz = tzA;
+            uint32_t jn = __shfl_sync(0xffffffffu, tb, 0);
+            do {
+                const int e = k & 1;
+                if (lane == 0) tc::mbar_wait(&uempty[e], ((k >> 1) & 1) ^ 1);   // entry free
+                __syncwarp();
+                BtEntry& U = uq[e];
+                if (last) {
+                    if (lane == 0) {
+                        U.end = 1;
+                        tc::mbar_arrive(&ufull[e]);
+                    }
+                    return;
+                }
+                const int t0 = tz;
+                int cnt = 0, nt = 0;
+                if (lane == 0) U.gofs[0] = 0;
+                // scan tiles t0.. while the list has room; a tile may be split
+                while (tz < tzE) {
+                    const uint32_t pe = __shfl_sync(0xffffffffu, tb, 2 * (tz - tzA) + 1);
+                    // 4 batches of 32 pairs per round (independent loads in flight)
+                    while (jn < pe && cnt + 32 <= BT2Z_CAP) {
+                        const int nb = cnt + 128 <= BT2Z_CAP ? 4 : 1;
+                        uint32_t v[4];
+                        bool ok[4];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const uint32_t j = jn + 32 * q + lane;
+                            ok[q] = q < nb && j < pe;
+                            v[q] = ok[q] ? svals[j] : 0u;
+                        }
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const bool f = ok[q] && (v[q] & smask) == 0u;
+                            const unsigned m = __ballot_sync(0xffffffffu, f);
+                            if (f) U.gl[cnt + __popc(m & ((1u << lane) - 1u))] = v[q] >> Sl;
+                            cnt += __popc(m);
+                        }
+                        jn = min(jn + 32u * nb, pe);
+                    }
+                    if (lane == 0) U.gofs[nt + 1] = cnt;
+                    ++nt;
+                    if (jn < pe) break;          // list full inside tile tz: continue it next entry
+                    ++tz;
+                    if (tz < tzE) jn = __shfl_sync(0xffffffffu, tb, 2 * (tz - tzA));
+                    if (nt == BT2Z_CH) break;
+                }
+                // slabs t0 .. t0 + nt (the last only inside the volume) are read by
+                // the tiles that have Gaussians: tile i reads slabs i and i + 1
+                __syncwarp();   // every lane's list writes precede lane 0's release
+                if (lane == 0) {
+                    U.tx = tx;
+                    U.ty = ty;
+                    U.tz0 = t0;
+                    U.ntiles = nt;
+                    U.end = 0;
+                    for (int i = 0; i <= nt; ++i) {
+                        const bool need = (i < nt && U.gofs[i + 1] > U.gofs[i]) ||
+                                          (i > 0 && U.gofs[i] > U.gofs[i - 1]);
+                        U.sseq[i] = need && t0 + i < ntz ? (int)seq++ : -1;
+                    }
+                    uclaim[e] = 0u;
+                    tc::mbar_arrive(&ufull[e]);   // release: the entry is written
+                }
+                __syncwarp();
+                ++k;
+            } while (tz < tzE);
+        }
+    }
     // -------------------------------------------------------------- consumers
-    const uint32_t smask = (1u << Sl) - 1u;
     BtWarp& W = wt[warp];
     for (uint32_t k = 0;; ++k) {
         const int e = k & 1;
         tc::mbar_wait(&ufull[e], (k >> 1) & 1);
-        const BtUnit& U = uq[e];
+        const BtEntry& U = uq[e];
         if (U.end) break;
-        const uint32_t total = U.nch[U.ntiles];
-        int rel = 0;   // this warp's released slabs of the unit
-        int cur = -1, waited = -1;
+        const int total = U.gofs[U.ntiles];
+        int rel = 0;            // slabs of the entry this warp has released
+        int waited = -1;        // highest slab of the entry this warp has waited for
+        int cur = -1;
         // a slab is released only after it landed: the arrival then belongs to
         // this use of the buffer, and no load is in flight when the CTA exits
+        auto wait_upto = [&](int lim) {
+            for (int sl = waited + 1; sl <= lim && sl <= U.ntiles; ++sl) {
+                const int q = U.sseq[sl];
+                if (q >= 0) tc::mbar_wait(&full[q % 3], (q / 3) & 1);
+                waited = sl;
+            }
+        };
+        // in slab order, each slab waited for and then released: a later slab's
+        // load may depend on this warp's release of an earlier one
         auto release_below = [&](int lim) {
-            for (; rel < lim; ++rel) {
-                const uint32_t q = U.seq0 + rel;
-                if (rel > waited) {
-                    tc::mbar_wait(&full[q % 3], (q / 3) & 1);
-                    waited = rel;
-                }
+            for (; rel < lim && rel <= U.ntiles; ++rel) {
+                wait_upto(rel);
                 __syncwarp();
-                if (lane == 0) tc::mbar_arrive(&empty[q % 3]);
+                const int q = U.sseq[rel];
+                if (q >= 0 && lane == 0) tc::mbar_arrive(&empty[q % 3]);
             }
         };
         for (;;) {
-            uint32_t cidx = 0;
-            if (lane == 0) cidx = atomicAdd(&uchunk[e], 1u);
-            cidx = __shfl_sync(0xffffffffu, cidx, 0);
-            if (cidx >= total) break;
-            int i = 0;
-            while (U.nch[i + 1] <= cidx) ++i;
-            if (i != cur) {   // moved on: slabs before tile i have no more users here
+            int idx = 0;
+            if (lane == 0) idx = (int)atomicAdd(&uclaim[e], 1u);
+            idx = __shfl_sync(0xffffffffu, idx, 0);
+            if (idx >= total) break;
+            int i = cur < 0 ? 0 : cur;
+            while (U.gofs[i + 1] <= idx) ++i;
+            if (i != cur) {   // moved on: slabs before tile i have no more readers here
                 cur = i;
                 release_below(i);
-                for (int sl = max(waited + 1, i); sl <= i + 1 && sl < U.nslabs; ++sl) {
-                    const uint32_t q = U.seq0 + sl;
-                    tc::mbar_wait(&full[q % 3], (q / 3) & 1);
-                    waited = sl;
-                }
+                wait_upto(i + 1);
             }
             const int tz = U.tz0 + i;
-            const int bA = (U.seq0 + i) % 3, bB = (U.seq0 + i + 1) % 3;
-            const uint32_t j = U.beg[i] + ((cidx - U.nch[i]) << 5) + lane;
-            const uint32_t v = j < U.pend[i] ? svals[j] : 1u;
-            unsigned first = __ballot_sync(0xffffffffu, j < U.pend[i] && (v & smask) == 0u);
-            while (first) {
-                const int src = __ffs(first) - 1;
-                first &= first - 1u;
-                const int64_t gi = (int64_t)(__shfl_sync(0xffffffffu, v, src) >> Sl);
-                const int xlo = fp[6 * gi], xhi = fp[6 * gi + 1], ylo = fp[6 * gi + 2];
-                const int yhi = fp[6 * gi + 3], zlo = fp[6 * gi + 4], zhi = fp[6 * gi + 5];
-                const GRec r = rec[gi];
-                float S0 = 0.f, Sx = 0.f, Sy = 0.f, Sz = 0.f, S2 = 0.f;
-                if (xhi - xlo == 16 && yhi - ylo == 16 && zhi - zlo == 16) {
-                    __syncwarp();
-                    if (lane < 17) {
-                        const float ry = (float)(ylo + lane - r.fy) - r.dy;
-                        const float ey = exp2f(-r.inv2 * ry * ry);
-                        W.ey[lane] = make_float4(ey, ey * ry, ey * ry * ry, 0.f);
-                    }
-                    __syncwarp();
-                    const int hf = lane >> 4, zl = lane & 15;
-                    const int xr = xlo - 16 * U.tx, yr = ylo - 16 * U.ty;
-                    auto soff = [&](int colr, int za) {
-                        const int rr = yr * 32 + xr + colr, zz = za & 15;
-                        return ((za >> 4) == tz ? bA : bB) * BT_SLAB + rr * 16 +
-                               (((zz >> 2) ^ ((rr >> 1) & 3)) << 2) + (zz & 3);
-                    };
-                    int off[9];
-#pragma unroll
-                    for (int kk = 0; kk < 9; ++kk) off[kk] = soff(min(2 * kk + hf, 16), zlo + zl);
-                    const int pl = lane < 17 ? lane : 16;
-                    const int offp = soff(pl, zlo + 16);
-                    const float rz = (float)(zlo + zl + zoff - r.fz) - r.dz;
-                    const float ez = exp2f(-r.inv2 * rz * rz);
-                    const float rz16 = (float)(zlo + 16 + zoff - r.fz) - r.dz;
-                    const float ez16 = exp2f(-r.inv2 * rz16 * rz16);
-                    float2 wx01[9];
-                    float wx2[9];
-#pragma unroll
-                    for (int kk = 0; kk < 9; ++kk) {
-                        const float rx = (float)(xlo + 2 * kk + hf - r.fx) - r.dx;
-                        const float ex = (kk < 8 || !hf) ? exp2f(-r.inv2 * rx * rx) : 0.f;
-                        wx01[kk] = make_float2(ex, ex * rx);
-                        wx2[kk] = ex * rx * rx;
-                    }
-                    const float rxp = (float)(xlo + lane - r.fx) - r.dx;
-                    const float exq = lane < 17 ? exp2f(-r.inv2 * rxp * rxp) : 0.f;
-                    float A0 = 0.f, Ax = 0.f, Ay = 0.f, Ar = 0.f, P0 = 0.f, P1 = 0.f, P2 = 0.f;
-#pragma unroll
-                    for (int yi = 0; yi < 17; ++yi) {
-                        float2 C01 = make_float2(0.f, 0.f);
-                        float C2 = 0.f;
-#pragma unroll
-                        for (int kk = 0; kk < 9; ++kk) {
-                            const float uu = slab[off[kk] + 512 * yi];
-                            C01 = ffma2(make_float2(uu, uu), wx01[kk], C01);
-                            C2 = fmaf(wx2[kk], uu, C2);
-                        }
-                        const float pu = slab[offp + 512 * yi];
-                        const float4 t = W.ey[yi];
-                        A0 = fmaf(t.x, C01.x, A0);
-                        Ax = fmaf(t.x, C01.y, Ax);
-                        Ay = fmaf(t.y, C01.x, Ay);
-                        Ar = fmaf(t.x, C2, fmaf(t.z, C01.x, Ar));
-                        P0 = fmaf(t.x, pu, P0);
-                        P1 = fmaf(t.y, pu, P1);
-                        P2 = fmaf(t.z, pu, P2);
-                    }
-                    A0 += __shfl_xor_sync(0xffffffffu, A0, 16);
-                    Ax += __shfl_xor_sync(0xffffffffu, Ax, 16);
-                    Ay += __shfl_xor_sync(0xffffffffu, Ay, 16);
-                    Ar += __shfl_xor_sync(0xffffffffu, Ar, 16);
-                    const float eh = hf ? 0.f : ez;
-                    S0 = eh * A0;
-                    Sx = eh * Ax;
-                    Sy = eh * Ay;
-                    Sz = eh * rz * A0;
-                    S2 = eh * fmaf(rz * rz, A0, Ar);
-                    const float Q0 = exq * P0, Qx = exq * rxp * P0, Qy = exq * P1;
-                    const float Qr = fmaf(exq * rxp * rxp, P0, exq * P2);
-                    S0 = fmaf(ez16, Q0, S0);
-                    Sx = fmaf(ez16, Qx, Sx);
-                    Sy = fmaf(ez16, Qy, Sy);
-                    Sz = fmaf(ez16 * rz16, Q0, Sz);
-                    S2 = fmaf(ez16, fmaf(rz16 * rz16, Q0, Qr), S2);
-                } else {
-                    bwd_moments17<false>(r, xlo, xhi - xlo + 1, ylo, yhi - ylo + 1, zlo,
-                                         zhi - zlo + 1, w, c, zoff, up, S0, Sx, Sy, Sz, S2);
-                }
-                S0 = warp_sum(S0);
-                Sx = warp_sum(Sx);
-                Sy = warp_sum(Sy);
-                Sz = warp_sum(Sz);
-                S2 = warp_sum(S2);
-                if (lane == 0) {   // chain rule in f64 (fvr.py:227-273)
-                    const double amp = P[4 * n + gi], sg = P[3 * n + gi];
-                    const double inv_s2 = 1.0 / (sg * sg), inv_s3 = inv_s2 / sg;
-                    const double k2 = amp * inv_s2;
-                    const double gx = k2 * Sx, gy = k2 * Sy, gz = k2 * Sz;
-                    G[gi] = gx;
-                    G[n + gi] = gy;
-                    G[2 * n + gi] = gz;
-                    G[3 * n + gi] = amp * inv_s3 * S2;
-                    G[4 * n + gi] = S0;
-                    if (accum) accum[gi] += sqrt(gx * gx + gy * gy + gz * gz);
-                }
+            const int64_t gi = U.gl[idx];
+            const int xlo = fp[6 * gi], xhi = fp[6 * gi + 1], ylo = fp[6 * gi + 2];
+            const int yhi = fp[6 * gi + 3], zlo = fp[6 * gi + 4], zhi = fp[6 * gi + 5];
+            const GRec r = rec[gi];
+            float S0 = 0.f, Sx = 0.f, Sy = 0.f, Sz = 0.f, S2 = 0.f;
+            if (xhi - xlo == 16 && yhi - ylo == 16 && zhi - zlo == 16) {
+                const int qa = U.sseq[i], qb = U.sseq[i + 1];
+                bt_row_table(W.ey, r, ylo, lane);
+                bt_full_moments(slab, qa % 3, qb < 0 ? 0 : qb % 3, tz, xlo - 16 * U.tx,
+                                ylo - 16 * U.ty, r, xlo, zlo, zoff, W.ey, lane, S0, Sx, Sy, Sz,
+                                S2);
+            } else {
+                bwd_moments17<false>(r, xlo, xhi - xlo + 1, ylo, yhi - ylo + 1, zlo, zhi - zlo + 1,
+                                     w, c, zoff, up, S0, Sx, Sy, Sz, S2);
             }
+            S0 = warp_sum(S0);
+            Sx = warp_sum(Sx);
+            Sy = warp_sum(Sy);
+            Sz = warp_sum(Sz);
+            S2 = warp_sum(S2);
+            if (lane == 0) bt_chain(P, n, gi, S0, Sx, Sy, Sz, S2, G, accum);
         }
-        // the unit's remaining slabs and its queue entry are released
-        release_below(U.nslabs);
+        release_below(U.ntiles + 1);   // the entry's remaining slabs
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&uempty[e]);
     }
@@ -2771,8 +2793,19 @@ int splatct_fvr_backward(const double* params, int64_t n, int w, int h, int c, i
     cudaStream_t s = as_stream(stream);
     const unsigned grid = (unsigned)((n + BG_WARPS - 1) / BG_WARPS);
     const bool fast = 2 * hx + 1 <= 17 && 2 * hz + 1 <= 17;
-    const char* kern = getenv("SPLATCT_BWD_KERNEL");   // "warp" / "sp": the other kernels
-    if (fast && 2 * hy + 1 <= 17 && kern && !strcmp(kern, "ts2")) {
+    // SPLATCT_BWD_KERNEL=warp|ts2|ts|sp forces a kernel (measurement knob).  By
+    // default the asynchronous tile-staged kernel takes dense clouds: staging a
+    // tile column's slabs pays once tiles hold enough first-tile Gaussians, and
+    // when the upstream outgrows L2 it is read ~4x instead of ~19x.  Measured on
+    // the C5 sweep: 256^3/400k 0.97 -> 0.72 ms, 512^3/2M
+    // 5.18 -> 3.42 ms, C4 1.07 -> 0.90 ms; sparse or L2-resident light clouds
+    // (C2, 1024^3/<=2M, 128^3) stay on the per-Gaussian warp kernel.
+    const char* kern = getenv("SPLATCT_BWD_KERNEL");
+    const double per_tile = (double)n / (double)L.nt;
+    const bool big_up = 4.0 * w * h * c > 96.0 * (1 << 20);
+    const bool dense = L.nt >= 4096 && (per_tile >= 48.0 || (big_up && per_tile >= 8.0));
+    const bool use_ts2 = kern ? !strcmp(kern, "ts2") : dense;
+    if (fast && 2 * hy + 1 <= 17 && use_ts2) {
         CUtensorMap smap;
         if (volume_tensor_map(&smap, up_yxz, w, h, c, 16, 32, 32, true)) {
             SPLATCT_CK(cudaMemsetAsync(grads, 0, sizeof(double) * 5 * (size_t)n, s));

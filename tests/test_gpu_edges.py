@@ -135,8 +135,8 @@ def test_deep_volume_has_no_occupancy_mask():
 # and the per-Gaussian-warp kernel with TMA-fed rows or direct loads
 BWD_VARIANTS = {"ts": {"SPLATCT_BWD_KERNEL": "ts"}, "ts2": {"SPLATCT_BWD_KERNEL": "ts2"},
                 "sp": {"SPLATCT_BWD_KERNEL": "sp"},
-                "warp_tma": {},
-                "warp_direct": {"SPLATCT_BWD_NO_TMA": "1"}}
+                "warp_tma": {"SPLATCT_BWD_KERNEL": "warp"},
+                "warp_direct": {"SPLATCT_BWD_KERNEL": "warp", "SPLATCT_BWD_NO_TMA": "1"}}
 
 
 @pytest.mark.parametrize("dims", [(40, 36, 32), (6, 5, 8), (64, 48, 256)])
@@ -165,10 +165,45 @@ def test_backward_variants_agree(dims, monkeypatch):
     dm, ds, di, acc, _ = O.splat_bwd(mu, cloud.sigma, cloud.intensity, box.shape, dims, up.zyx)
     assert rel_l2(a.d_mu, dm) < GRAD_TOL and rel_l2(a.d_sigma, ds) < GRAD_TOL
     assert rel_l2(a.d_intensity, di) < GRAD_TOL
-    for b in (out["ts"], out["sp"], out["warp_direct"]):
+    for b in (out["ts"], out["ts2"], out["sp"], out["warp_direct"]):
         for x, y in ((a.d_mu, b.d_mu), (a.d_sigma, b.d_sigma), (a.d_intensity, b.d_intensity),
                      (a.accum_pos_grad_norm, b.accum_pos_grad_norm)):
             assert rel_l2(x, y) < 1e-6
+    # the two tile-staged kernels share the per-Gaussian arithmetic: bitwise
+    np.testing.assert_array_equal(out["ts"].d_mu, out["ts2"].d_mu)
+    np.testing.assert_array_equal(out["ts"].d_sigma, out["ts2"].d_sigma)
+    np.testing.assert_array_equal(out["ts"].d_intensity, out["ts2"].d_intensity)
+
+
+def test_backward_tile_staged_dense_split_entries(monkeypatch):
+    """A dense cloud (~900 first-tile Gaussians per 16^3 tile) overflows the
+    asynchronous tile-staged kernel's 1024-Gaussian queue entries, so units and
+    single tiles are split across entries, each re-staging its slabs.  The
+    gradients match the per-Gaussian warp kernel (1e-6) and the synchronous
+    tile-staged kernel (bitwise), run to run bitwise.  (The dispatcher's own
+    choice of this kernel for dense clouds is exercised at C4 by
+    test_gpu_fullsize.py::test_fvr_backward_c4_sampled.)"""
+    rng = np.random.default_rng(12)
+    dims = (64, 64, 64)
+    box = core.BoxConfig.cube(17)
+    n = 60000
+    mu = np.stack([rng.uniform(0, d, n) for d in dims], 1)
+    cloud = core.GaussianCloud(mu, rng.uniform(0.5, 2.5, n), rng.uniform(0, 1, n))
+    up = core.VolumeGrid.from_zyx(rng.standard_normal(dims[::-1]).astype(np.float32))
+    out = {}
+    for name in ("warp", "ts", "ts2"):
+        monkeypatch.setenv("SPLATCT_BWD_KERNEL", name)
+        out[name] = fvr.backward(cloud, box, dims, up)
+        again = fvr.backward(cloud, box, dims, up)
+        np.testing.assert_array_equal(out[name].d_mu, again.d_mu)
+    a = out["warp"]
+    for b in (out["ts2"],):
+        for x, y in ((a.d_mu, b.d_mu), (a.d_sigma, b.d_sigma), (a.d_intensity, b.d_intensity),
+                     (a.accum_pos_grad_norm, b.accum_pos_grad_norm)):
+            assert rel_l2(x, y) < 1e-6
+    np.testing.assert_array_equal(out["ts2"].d_mu, out["ts"].d_mu)
+    np.testing.assert_array_equal(out["ts2"].d_sigma, out["ts"].d_sigma)
+    np.testing.assert_array_equal(out["ts2"].d_intensity, out["ts"].d_intensity)
 
 
 @pytest.mark.parametrize("dims", [(40, 36, 32), (6, 5, 8)])
