@@ -498,7 +498,7 @@ def run_b200(args, cfg):
         if op.fb and occ_w is not None:
             # empty-space skipping: (entry, z-chunk) gathers the forward actually makes
             zc = 128 if cl % 4 == 0 and cl >= 128 else (64 if cl % 2 == 0 and cl >= 64 else 32)
-            words = occ_w[op.fb[1].long()]
+            words = occ_w[op.forward_entry_pixels().long()]
             n_kept = 0
             for z0_ in range(0, cl, zc):
                 lo_, hi_ = z0_ // 16, (min(z0_ + zc, cl) - 1) // 16

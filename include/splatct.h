@@ -190,8 +190,12 @@ int splatct_proj_adjoint(const int64_t* at_ptr, const int32_t* at_ray, const flo
  * where absent), columns ascending -- or, with order_dir (device
  * float[ngroups][2], the group's ray direction; ray groups only), in march
  * order along that direction so concurrent warps sweep the slice together.
+ * kinds 3 / 4 are bands of 8 / 16 consecutive rays (forward only, w * h <=
+ * 2^27, at most 8192 weights per band): an entry is a sliding 4-ray window,
+ * (k0 << 27 | pixel, w[4]) for band rays k0..k0+3, one per window of a
+ * pixel's run of rays, entries ordered by (k0, pixel); order_dir is ignored.
  * count (synchronous) -> gptr[ngroups+1] and *nb; fill -> gidx, gval
- * (float[nb][R], 16-byte aligned). */
+ * (float[nb][R], R = 8 for kind 2 and 4 otherwise, 16-byte aligned). */
 int splatct_proj_block_scratch_bytes(int nrows, int kind, int w, int h, size_t* bytes);
 int splatct_proj_block_count(const int64_t* ptr, const int32_t* idx, int nrows, int kind, int w,
                              int h, const float* order_dir, int64_t* gptr, void* scratch,
@@ -208,7 +212,8 @@ int splatct_proj_tv_partial_len(int w, int h, int c, int64_t* len);
 
 /* Blocked applications: same results as splatct_proj_forward /
  * splatct_proj_adjoint (up to f32 summation order), one z-column load per
- * group entry feeding the group's rows (forward: kind 0 or 2 groups). */
+ * group entry feeding the group's rows (forward: kind 0, 2, 3 or 4 groups;
+ * bands store each ray once as their 4-ray window slides past it). */
 /* col_occ (optional, NULL = off): the voxelizer's PIXEL-column occupancy of
  * vol_yxz (splatct_fvr_pixel_occupancy_offset into the bins workspace, valid
  * after splatct_fvr_forward); entries whose pixel column is zero in a warp's

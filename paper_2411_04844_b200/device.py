@@ -14,6 +14,7 @@ Layouts (include/splatct.h):
 from __future__ import annotations
 
 import ctypes
+import os
 from collections import OrderedDict
 
 import numpy as np
@@ -336,11 +337,33 @@ class FvrPlan:
 # projector operator
 # ---------------------------------------------------------------------------
 
-# forward row groups: kind 0 (4 rays).  kind 2 (8 rays: 19 % fewer z-column
-# loads) measured 0.54 vs 0.37 ms at C2 -- twice the accumulators halve the
-# resident warps and the zero-weight FMAs double -- so it stays available in
-# the ABI but unused.
-FWD_GROUP_KIND = 0
+# forward row groups: kind 0, aligned 4-ray groups (one z-column gather feeds 4
+# rays).  Measured alternatives, kept in the ABI (SPLATCT_FWD_GROUPS=4|band8|
+# band16 selects one; measurement knob):
+#   kind 2, aligned 8-ray groups with w[8] per entry: 0.54 vs 0.37 ms at C2 --
+#     twice the accumulators halve the resident warps, the zero-weight FMAs double;
+#   kinds 3 / 4, bands of 8 / 16 rays whose entries are sliding 4-ray windows: a
+#     pixel's z-column is gathered once per band (C2: 17 % fewer gathered bytes
+#     for 8-ray bands), but 0.38 vs 0.25 ms -- half the warps with twice the
+#     serial work each, and the L1 sharing between neighbouring groups' warps
+#     (15 % hit rate) is lost.  A band's weights must fit the build kernel's
+#     8192-entry group capacity (C2 rays carry up to ~700: 16-ray bands do not).
+_BLOCK_CAP = 8192
+
+
+def _forward_group_kind(max_row_nnz: int) -> int:
+    force = os.environ.get("SPLATCT_FWD_GROUPS")
+    if force:
+        kind = {"4": 0, "band8": 3, "band16": 4}[force]
+        if _group_rows(kind) * max_row_nnz > _BLOCK_CAP:
+            raise ValueError(f"SPLATCT_FWD_GROUPS={force}: rays of up to {max_row_nnz} "
+                             f"weights overflow a {_BLOCK_CAP}-entry band")
+        return kind
+    return 0
+
+
+def _group_rows(kind: int) -> int:
+    return {0: 4, 1: 4, 2: 8, 3: 8, 4: 16}[kind]
 
 
 def _occ(occ, kind: str):
@@ -403,9 +426,11 @@ class ProjectorOperator:
         self.blocked = blocked
         if blocked:
             # forward: 4-ray groups (one z-column load feeds 4 rays); adjoint: 2x2 quads
-            self.fkind = FWD_GROUP_KIND
+            max_nnz = int((self.a_ptr[1:] - self.a_ptr[:-1]).max().item()) if rays else 0
+            self.fkind = _forward_group_kind(max_nnz)
             self.fb = self._block(self.a_ptr, self.a_col, self.a_val, self.n_rays, self.fkind,
-                                  self._group_dirs(8 if self.fkind == 2 else 4))
+                                  self._group_dirs(_group_rows(self.fkind))
+                                  if self.fkind in (0, 2) else None)
             self.ab = self._block(self.at_ptr, self.at_ray, self.at_val, self.w * self.h, 1)
 
     def _group_dirs(self, rows: int = 4) -> torch.Tensor:
@@ -426,11 +451,12 @@ class ProjectorOperator:
         return torch.from_numpy(np.stack([dx, dy], 1).astype(np.float32)).to(self.device)
 
     def _block(self, ptr_, idx, val, nrows, kind, order_dir=None):
-        """4-row blocked copy (gptr, gidx, gval[nb, 4]) of a CSR operator."""
+        """Blocked copy (gptr, gidx, gval[nb, 4 or 8]) of a CSR operator."""
         sb = size_query("splatct_proj_block_scratch_bytes", nrows, kind, self.w, self.h)
         scratch = torch.empty(sb, dtype=torch.uint8, device=self.device)
-        rows = 8 if kind == 2 else 4
-        ng = ((nrows + rows - 1) // rows if kind in (0, 2)
+        group = _group_rows(kind)
+        rows = 8 if kind == 2 else 4   # weights per entry
+        ng = ((nrows + group - 1) // group if kind != 1
               else ((self.w + 1) // 2) * ((self.h + 1) // 2))
         gptr = torch.empty(ng + 1, dtype=torch.int64, device=self.device)
         nb = ctypes.c_int64(0)
@@ -447,6 +473,12 @@ class ProjectorOperator:
     def _gargs(self):
         return (ptr(self.cos_t), ptr(self.sin_t), self.m, self.n_det, self.spacing, self.step,
                 int(self.is_fan), self.rs, self.rd, self.w, self.h)
+
+    def forward_entry_pixels(self) -> torch.Tensor:
+        """Pixel index of every blocked forward entry (band entries carry their
+        window's first ray in the top bits of the packed index)."""
+        idx = self.fb[1]
+        return (idx & 0x07FFFFFF) if self.fkind in (3, 4) else idx
 
     @property
     def matrix_bytes(self) -> int:

@@ -344,3 +344,43 @@ def test_pinned_output_pool_results_stay_valid():
     assert all(not e.busy for e in D._OUT_POOL)
     v = optim.run_reconstruction(meas, geom, st, init_cloud=cl)[0]
     np.testing.assert_array_equal(v.zyx, ref)
+
+
+@pytest.mark.parametrize("groups", ["band8", "band16"])
+def test_projector_band_groups_match_4ray_groups(groups, monkeypatch):
+    """The opt-in band forms of the forward operator (sliding 4-ray windows
+    over 8 / 16-ray bands, SPLATCT_FWD_GROUPS) give the 4-ray-group forward
+    to f32 summation order, densely and with empty-space skipping, and write
+    every ray (the output starts as NaN; the fan is wider than the slice, so
+    some rays touch no pixel).  Bands that cannot fit the build capacity are
+    refused."""
+    import torch
+    from paper_2411_04844_b200 import device as D
+    dev = D.require_cuda()
+    w, h, c = 64, 48, 256
+    geom = core.ScanGeometry.fan(24, 150, 1.1, 90.0, 70.0)
+    g = torch.Generator(device="cpu").manual_seed(3)
+    x = torch.randn((h, w, c), generator=g)
+    x[:, :, 96:176] = 0.0                         # z tiles 6..10 all zero
+    x[:20, :, :] = 0.0                            # and whole empty columns
+    seg = (x.reshape(h, w, c // 16, 16) != 0).any(-1).numpy()    # (h, w, tiles)
+    bits = (seg.astype(np.uint64) << np.arange(c // 16, dtype=np.uint64)).sum(-1, dtype=np.uint64)
+    occ = torch.from_numpy(bits.reshape(-1).view(np.int64)).to(dev)
+    x = x.to(dev)
+    monkeypatch.setenv("SPLATCT_FWD_GROUPS", "4")
+    ref = D.ProjectorOperator(geom, w, h, 0.5, dev)
+    monkeypatch.setenv("SPLATCT_FWD_GROUPS", groups)
+    op = D.ProjectorOperator(geom, w, h, 0.5, dev)
+    assert op.fkind == (3 if groups == "band8" else 4)
+    a = ref.forward(x)
+    for skip in (None, D.VP(occ.data_ptr())):
+        b = torch.full_like(a, float("nan"))
+        op.forward(x, out=b, occ=skip)
+        assert torch.isfinite(b).all()
+        assert rel_l2(b.cpu().numpy(), a.cpu().numpy()) < 1e-6
+        again = op.forward(x, occ=skip)
+        np.testing.assert_array_equal(again.cpu().numpy(), b.cpu().numpy())
+    big = core.ScanGeometry.fan(8, 700, 1.6, 512.0, 512.0)
+    monkeypatch.setenv("SPLATCT_FWD_GROUPS", "band16")
+    with pytest.raises(ValueError):
+        D.ProjectorOperator(big, 512, 512, 0.5, dev)
