@@ -205,6 +205,7 @@ def stage_profile(tr, iters):
     import torch
     from paper_2411_04844_b200 import device as D
     from paper_2411_04844_b200 import _lib
+    from paper_2411_04844_b200.trainer import ROW_ORDERED_BINS
     s = torch.cuda.current_stream()
     names = ["proj_forward", "loss_fused", "proj_adjoint_tv", "finalize", "fvr_backward", "adam",
              "fvr_bin", "fvr_forward"]
@@ -244,7 +245,7 @@ def stage_profile(tr, iters):
         ev[5].record(s)
         D.adam(tr.params, tr.grads, tr.m1, tr.m2, tr.adam_s, 0.3, tr.sigma_ceiling, tr.halt)
         ev[6].record(s)
-        tr.fvr.bin(tr.params, tr.halt)
+        tr.fvr.bin(tr.params, tr.halt, row_ordered=ROW_ORDERED_BINS)
         ev[7].record(s)
         tr.fvr.forward(tr.params, tr.vol, tr.halt, masks=True)
         ev[8].record(s)

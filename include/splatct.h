@@ -70,6 +70,15 @@ int splatct_fvr_workspace_bytes(int64_t n, int w, int h, int c, int hx, int hy, 
  * counterpart for tiles).  halt: optional device flag; non-zero skips work. */
 int splatct_fvr_bin(const double* params, int64_t n, int w, int h, int c, int z0, int hx,
                     int hy, int hz, void* ws, size_t ws_bytes, const int* halt, void* stream);
+/* Same bins, each tile's list ordered by the Gaussians' first footprint row
+ * relative to the tile (quantised into the radix key's spare bits, no extra
+ * pass), then by Gaussian: the forward then skips whole k8 steps per warp
+ * more often.  The lists hold the same pairs; the forward's per-voxel sums run
+ * in a different (still deterministic) order, so volumes agree with the
+ * canonical bins to f32 rounding.  The training step uses these. */
+int splatct_fvr_bin_row_ordered(const double* params, int64_t n, int w, int h, int c, int z0,
+                                int hx, int hy, int hz, void* ws, size_t ws_bytes,
+                                const int* halt, void* stream);
 
 /* V = sum_i I_i ex_i (x) ey_i (x) ez_i over box intersect volume; one CTA per
  * tile accumulating in registers/shared memory, each voxel written once

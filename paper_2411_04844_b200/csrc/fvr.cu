@@ -203,7 +203,7 @@ __device__ __forceinline__ unsigned long long lookback_warp(unsigned long long* 
 // (global histograms), so each sort pass is a single kernel.
 __global__ void __launch_bounds__(BIN_NT) k_bin_emit(
     const double* __restrict__ P, int64_t n, int w, int h, int c, int zoff, int hx, int hy,
-    int hz, int ntx, int nty, int Sl, int passes, int32_t* __restrict__ fp,
+    int hz, int ntx, int nty, int Sl, int passes, int ybits, int32_t* __restrict__ fp,
     GRec* __restrict__ rec, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
     uint32_t* __restrict__ ghist, unsigned long long* __restrict__ status,
     uint32_t* __restrict__ tickets, const int* halt) {
@@ -212,6 +212,7 @@ __global__ void __launch_bounds__(BIN_NT) k_bin_emit(
     __shared__ unsigned s_blk;
     __shared__ uint32_t s_off[BIN_NT + 1];
     __shared__ int4 s_tile[BIN_NT];        // tx0, ty0, tz0, nx | ny << 16
+    __shared__ int s_ylo[BIN_NT];          // footprint's first row (row-ordered keys)
     __shared__ uint32_t s_warp[BIN_NT / 32];
     __shared__ uint32_t s_hist[MAX_PASSES][RADIX];
     __shared__ unsigned long long s_base;
@@ -224,6 +225,7 @@ __global__ void __launch_bounds__(BIN_NT) k_bin_emit(
     const int64_t i = blk * BIN_NT + t;
     uint32_t cnt = 0;
     int4 ti = make_int4(0, 0, 0, 1 | (1 << 16));
+    int ylo0 = 0;
     if (i < n) {
         const int half[3] = {hx, hy, hz};
         const int dim[3] = {w, h, c};
@@ -259,9 +261,11 @@ __global__ void __launch_bounds__(BIN_NT) k_bin_emit(
             const int nz = hi[2] / TT - lo[2] / TT + 1;
             cnt = (uint32_t)(nx * ny * nz);
             ti = make_int4(lo[0] / TT, lo[1] / TT, lo[2] / TT, nx | (ny << 16));
+            ylo0 = lo[1];
         }
     }
     s_tile[t] = ti;
+    s_ylo[t] = ylo0;
     // block exclusive scan of the counts
     uint32_t inc = cnt;
 #pragma unroll
@@ -316,7 +320,15 @@ __global__ void __launch_bounds__(BIN_NT) k_bin_emit(
         const int sy = (int)__fdividef((float)slot + 0.5f, (float)nx);
         const int sz = (int)__fdividef((float)sy + 0.5f, (float)ny);
         const int tx = g.x + (int)slot - sy * nx, ty = g.y + sy - sz * ny, tz = g.z + sz;
-        const uint32_t key = (uint32_t)((tz * nty + ty) * ntx + tx);
+        // row-ordered bins (ybits > 0): inside a tile, the pairs are ordered by the
+        // footprint's first row relative to the tile (in [-16, 15] for boxes up
+        // to 17 rows; quantised to ybits), then by Gaussian -- so a k8 step of the
+        // forward sees Gaussians covering similar rows and whole warps skip it
+        uint32_t key = (uint32_t)((tz * nty + ty) * ntx + tx);
+        if (ybits) {
+            const int rel = min(max(s_ylo[lo] - TT * ty + 16, 0), 31);
+            key = (key << ybits) | ((uint32_t)rel >> (5 - ybits));
+        }
         keys[base + q] = key;
         vals[base + q] = ((uint32_t)(blk * BIN_NT + lo) << Sl) | slot;
         for (int p = 0; p < passes; ++p) atomicAdd(&s_hist[p][(key >> (8 * p)) & 255u], 1u);
@@ -593,13 +605,18 @@ __global__ void __launch_bounds__(256, 4) k_fvr_fwd(const GRec* __restrict__ rec
         for (int k0 = 0; k0 < nk; k0 += 8) {
             const float* ra = tab + (k0 + t4) * TAB_STRIDE;       // Gaussian k0 + t
             const float* rb = tab + (k0 + t4 + 4) * TAB_STRIDE;   // Gaussian k0 + t + 4
+            const float ya0 = ra[2 * TT + r0], ya1 = ra[2 * TT + r0 + 1];
+            const float yb0 = rb[2 * TT + r0], yb1 = rb[2 * TT + r0 + 1];
+            // none of the step's 8 Gaussians reaches this warp's two rows: its B
+            // operand is all zero and the step would add exact zeros (skipping it
+            // is bitwise neutral); row-ordered bins make this common
+            if (!__any_sync(0xffffffffu, ya0 != 0.f || ya1 != 0.f || yb0 != 0.f || yb1 != 0.f))
+                continue;
             const uint32_t* ua = reinterpret_cast<const uint32_t*>(ra);
             const uint32_t* ub = reinterpret_cast<const uint32_t*>(rb);
             // A[x][k] = ex_k[x], pre-split by the table builder
             const uint32_t ah[4] = {ua[g], ua[g + 8], ub[g], ub[g + 8]};
             const uint32_t al[4] = {ua[TT + g], ua[TT + g + 8], ub[TT + g], ub[TT + g + 8]};
-            const float ya0 = ra[2 * TT + r0], ya1 = ra[2 * TT + r0 + 1];
-            const float yb0 = rb[2 * TT + r0], yb1 = rb[2 * TT + r0 + 1];
             const float za0 = ra[3 * TT + g], za1 = ra[3 * TT + g + 8];
             const float zb0 = rb[3 * TT + g], zb1 = rb[3 * TT + g + 8];
             // n-tile j: row r0 + (j >> 1), z = (j & 1) * 8 + n
@@ -1335,15 +1352,15 @@ __global__ void __launch_bounds__(256) k_fvr_fwd_plain(const GRec* __restrict__ 
 // tstart[nt] = number of pairs (read on the device: the bins are dense).
 // One coalesced pass; each tile start is written exactly once.
 __global__ void k_tile_starts(const uint32_t* __restrict__ skeys,
-                              const uint32_t* __restrict__ npairs, int64_t nt,
+                              const uint32_t* __restrict__ npairs, int64_t nt, int ybits,
                               uint32_t* __restrict__ tstart, const int* halt) {
     griddep_wait();
     if (halted(halt)) return;
     const int64_t np = npairs ? (int64_t)*npairs : 0;
     const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (j > np) return;
-    const int64_t prev = j == 0 ? -1 : (int64_t)skeys[j - 1];
-    const int64_t cur = j == np ? nt : (int64_t)skeys[j];
+    const int64_t prev = j == 0 ? -1 : (int64_t)(skeys[j - 1] >> ybits);
+    const int64_t cur = j == np ? nt : (int64_t)(skeys[j] >> ybits);
     for (int64_t t = prev + 1; t <= cur; ++t) tstart[t] = (uint32_t)j;
 }
 
@@ -2616,10 +2633,16 @@ int splatct_fvr_workspace_bytes(int64_t n, int w, int h, int c, int hx, int hy, 
     return SPLATCT_OK;
 }
 
-int splatct_fvr_bin(const double* params, int64_t n, int w, int h, int c, int z0, int hx,
-                    int hy, int hz, void* ws, size_t ws_bytes, const int* halt, void* stream) {
+static int fvr_bin_impl(const double* params, int64_t n, int w, int h, int c, int z0, int hx,
+                        int hy, int hz, void* ws, size_t ws_bytes, const int* halt, void* stream,
+                        bool row_order) {
     FvrLayout L = make_layout(n, w, h, c, hx, hy, hz);
     if (int e = check_args(n, w, h, c, hx, hy, hz, ws_bytes, L)) return e;
+    // row order uses the key bits the radix passes sort anyway (no extra pass),
+    // at most 4, and only for boxes up to 17 rows (relative first row in [-16, 15])
+    int tile_bits = 0;
+    while (((int64_t)1 << tile_bits) < L.nt) ++tile_bits;
+    const int ybits = row_order && hy <= 8 ? min(4, 8 * L.passes - tile_bits) : 0;
     cudaStream_t s = as_stream(stream);
     uint32_t* tickets = at<uint32_t>(ws, L.o_tickets);   // [0] emit, [1] pair count, [2..] passes
     const uint32_t* npairs = tickets + 1;
@@ -2627,7 +2650,7 @@ int splatct_fvr_bin(const double* params, int64_t n, int w, int h, int c, int z0
         SPLATCT_CK(cudaMemsetAsync(at<char>(ws, L.o_ctl), 0, L.ctl_bytes, s));
         SPLATCT_CK(launch_pdl(k_bin_emit, dim3((unsigned)L.emit_blocks), dim3(BIN_NT), 0, s,
                               params, n, w, h, c, z0, hx, hy, hz, L.ntx, L.nty, L.Sl, L.passes,
-                              at<int32_t>(ws, L.o_fp), at<GRec>(ws, L.o_rec),
+                              ybits, at<int32_t>(ws, L.o_fp), at<GRec>(ws, L.o_rec),
                               at<uint32_t>(ws, L.o_k0), at<uint32_t>(ws, L.o_v0),
                               at<uint32_t>(ws, L.o_ghist),
                               at<unsigned long long>(ws, L.o_stat_e), tickets, halt));
@@ -2649,11 +2672,22 @@ int splatct_fvr_bin(const double* params, int64_t n, int w, int h, int c, int z0
         const int64_t npk = n > 0 ? L.np : 0;
         SPLATCT_CK(launch_pdl(k_tile_starts, dim3((unsigned)((npk + 1 + 255) / 256)), dim3(256),
                               0, s, n > 0 ? at<uint32_t>(ws, ko) : nullptr,
-                              n > 0 ? npairs : nullptr, L.nt, at<uint32_t>(ws, L.o_tstart),
-                              halt));
+                              n > 0 ? npairs : nullptr, L.nt, ybits,
+                              at<uint32_t>(ws, L.o_tstart), halt));
         SPLATCT_LAUNCH_CK();
     }
     return SPLATCT_OK;
+}
+
+int splatct_fvr_bin(const double* params, int64_t n, int w, int h, int c, int z0, int hx,
+                    int hy, int hz, void* ws, size_t ws_bytes, const int* halt, void* stream) {
+    return fvr_bin_impl(params, n, w, h, c, z0, hx, hy, hz, ws, ws_bytes, halt, stream, false);
+}
+
+int splatct_fvr_bin_row_ordered(const double* params, int64_t n, int w, int h, int c, int z0,
+                                int hx, int hy, int hz, void* ws, size_t ws_bytes,
+                                const int* halt, void* stream) {
+    return fvr_bin_impl(params, n, w, h, c, z0, hx, hy, hz, ws, ws_bytes, halt, stream, true);
 }
 
 // TMA descriptor of the (h, w, c) volume for 16^3 boxes with the 64-byte

@@ -288,9 +288,11 @@ class FvrPlan:
 
     masks_valid = False
 
-    def bin(self, params: torch.Tensor, halt=None) -> None:
-        call("splatct_fvr_bin", ptr(params), *self._geo(), ptr(self.ws), self.ws_bytes,
-             ptr(halt), stream_handle())
+    def bin(self, params: torch.Tensor, halt=None, row_ordered: bool = False) -> None:
+        """row_ordered: each tile's list ordered by the Gaussians' first row
+        (same pairs; the forward skips more work, its sums change order)."""
+        call("splatct_fvr_bin_row_ordered" if row_ordered else "splatct_fvr_bin", ptr(params),
+             *self._geo(), ptr(self.ws), self.ws_bytes, ptr(halt), stream_handle())
 
     def forward(self, params: torch.Tensor, out: torch.Tensor, halt=None,
                 masks: bool = False) -> torch.Tensor:

@@ -20,6 +20,7 @@ gradient all-reduce plus a one-plane TV halo.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import torch
@@ -28,6 +29,10 @@ from . import device as D
 from .core import BoxConfig, ScanGeometry
 
 SIGMA_FLOOR = 0.3
+# the step bins with each tile's list ordered by first footprint row, so the
+# forward's warps skip more k8 steps (SPLATCT_ROW_ORDER=0: canonical lists;
+# measurement knob)
+ROW_ORDERED_BINS = os.environ.get("SPLATCT_ROW_ORDER", "1") != "0"
 
 
 @dataclass
@@ -198,7 +203,7 @@ class Trainer:
 
     # -- iteration ----------------------------------------------------------
     def initial_volume(self):
-        self.fvr.bin(self.params, self.halt)
+        self.fvr.bin(self.params, self.halt, row_ordered=ROW_ORDERED_BINS)
         self.fvr.forward(self.params, self.vol, self.halt, masks=True)
 
     def _stages(self):
@@ -281,7 +286,7 @@ class Trainer:
                 D.grad_norm_accum(self.grads, self.accum, halt)
             D.adam(self.params, self.grads, self.m1, self.m2, self.adam_s, SIGMA_FLOOR,
                    self.sigma_ceiling, halt)
-            self.fvr.bin(self.params, halt)
+            self.fvr.bin(self.params, halt, row_ordered=ROW_ORDERED_BINS)
             self.fvr.forward(self.params, self.vol, halt, masks=True)   # + empty-space masks
         st.append(("gpu", update_resplat))
         return st

@@ -384,3 +384,45 @@ def test_projector_band_groups_match_4ray_groups(groups, monkeypatch):
     monkeypatch.setenv("SPLATCT_FWD_GROUPS", "band16")
     with pytest.raises(ValueError):
         D.ProjectorOperator(big, 512, 512, 0.5, dev)
+
+
+@pytest.mark.parametrize("dims,n", [((64, 48, 40), 3000), ((256, 256, 64), 20000)])
+def test_row_ordered_bins_same_pairs(dims, n):
+    """splatct_fvr_bin_row_ordered (the training step's bins): every tile holds
+    the same (tile, Gaussian) pairs as the canonical bins, ordered by the
+    footprint's first row relative to the tile (quantised), then by Gaussian;
+    the forward over them matches the canonical forward to f32 rounding and is
+    run-to-run bitwise (its k8-step skipping only drops exact zeros)."""
+    import torch
+    from paper_2411_04844_b200 import device as D, optim
+    dev = D.require_cuda()
+    box = core.BoxConfig.for_dims(17, dims)
+    cloud = optim.init_cloud_random(dims, n, seed=5, box=box)
+    params = D.cloud_to_params(cloud, dev)
+    plan = D.FvrPlan(n, dims, box.half, 0, dev)
+    plan.bin(params)
+    fp, ts, items = plan.export_bins()
+    vol_a = plan.forward(params, plan.new_volume()).cpu().numpy()
+    plan.bin(params, row_ordered=True)
+    fp2, ts2, items2 = plan.export_bins()
+    vol_b = plan.forward(params, plan.new_volume()).cpu().numpy()
+    vol_c = plan.forward(params, plan.new_volume()).cpu().numpy()
+    np.testing.assert_array_equal(fp, fp2)
+    np.testing.assert_array_equal(ts, ts2)
+    nt = len(ts) - 1
+    ty = (np.arange(nt) // ((dims[0] + 15) // 16)) % ((dims[1] + 15) // 16)
+    tile_bits = int(np.ceil(np.log2(nt)))
+    ybits = min(4, 8 * max(1, -(-tile_bits // 8)) - tile_bits)   # the radix key's spare bits
+    reordered = 0
+    for t in range(nt):
+        a, b = items[ts[t]:ts[t + 1]], items2[ts[t]:ts[t + 1]]
+        np.testing.assert_array_equal(np.sort(a), np.sort(b))
+        np.testing.assert_array_equal(a, np.sort(a))          # canonical: ascending Gaussian
+        # first footprint row relative to the tile, quantised; then ascending Gaussian
+        q = np.clip(fp[b, 2] - 16 * ty[t] + 16, 0, 31) >> (5 - ybits)
+        order = np.lexsort((b, q))
+        np.testing.assert_array_equal(order, np.arange(len(b)))
+        reordered += int(not np.array_equal(a, b))
+    assert reordered > 0
+    assert rel_l2(vol_b, vol_a) < 1e-6
+    np.testing.assert_array_equal(vol_b, vol_c)
