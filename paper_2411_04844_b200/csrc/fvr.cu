@@ -557,14 +557,18 @@ __global__ void __launch_bounds__(256, 4) k_fvr_fwd(const GRec* __restrict__ rec
     for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
     const int tg = threadIdx.x >> 3, tj = threadIdx.x & 7;   // table builder: Gaussian, part
 
-    // the next batch's Gaussian records are loaded while this batch's MMAs run
+    // the next batch's Gaussian records are loaded while this batch's MMAs run,
+    // from pair values loaded one batch earlier still (the value -> record
+    // chain would otherwise stall the warp in order at the record load)
     GRec rn;
     if (beg + tg < end) rn = rec[svals[beg + tg] >> S];   // S = log2(slots per Gaussian)
+    uint32_t vn = beg + FWD_BATCH + tg < end ? svals[beg + FWD_BATCH + tg] : 0u;
     for (uint32_t b0 = beg; b0 < end; b0 += FWD_BATCH) {
         const int nb = (int)min((uint32_t)FWD_BATCH, end - b0);
         const int nk = (nb + 7) & ~7;
         const GRec r = rn;
-        if (b0 + FWD_BATCH + tg < end) rn = rec[svals[b0 + FWD_BATCH + tg] >> S];
+        if (b0 + FWD_BATCH + tg < end) rn = rec[vn >> S];
+        if (b0 + 2 * FWD_BATCH + tg < end) vn = svals[b0 + 2 * FWD_BATCH + tg];
         __syncthreads();
         if (tg < nk) {
             float* row = tab + tg * TAB_STRIDE;

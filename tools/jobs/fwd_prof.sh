@@ -1,0 +1,5 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+KREGEX="k_fvr_fwd" COUNT=1 TAG=fwd_full bash tools/jobs/ncu_full.sh
+python tools/ncu_full_summary.py gpurun_out/fwd_full.ncu-rep 2>&1 | tail -3
+python tools/ncu_lines.py gpurun_out/fwd_full.ncu-rep k_fvr_fwd 40
