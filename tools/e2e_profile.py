@@ -10,7 +10,7 @@ dev = torch.device("cuda", 0)
 w, h, c = cfg["dims"]
 op = D.projector_for(geom, w, h, 0.5, dev)
 meas = Sinogram.from_views(op.forward(D.zyx_to_yxz(truth.zyx, dev)).cpu().numpy())
-st = optim.ReconstructionSettings(dims=cfg["dims"], box=box, max_iters=50, densify_interval=0)
+st = optim.ReconstructionSettings(dims=cfg["dims"], box=box, max_iters=int(os.environ.get("STEPS", "20")), densify_interval=0)
 for _ in range(2): optim.run_reconstruction(meas, geom, st, init_cloud=cloud)
 import cProfile, pstats
 torch.cuda.synchronize()
