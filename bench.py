@@ -361,8 +361,18 @@ def run_b200(args, cfg):
         raise RuntimeError("non-finite loss during the benchmark")
     loss_last = float(tr.trace_rows()[-1, 0])
 
-    # per-stage device times (eager, instrumented) + launch count
-    stages, launches = stage_profile(tr, 5)
+    # per-stage device times (eager, instrumented)
+    stages, _ = stage_profile(tr, 5)
+    # launches per iteration: one eager pass of exactly the stages the captured
+    # graph replays
+    from paper_2411_04844_b200 import _lib
+    if world == 1:
+        l0 = _lib.launch_count()
+        tr.iteration()
+        torch.cuda.synchronize()
+        launches = _lib.launch_count() - l0
+    else:
+        _, launches = stage_profile(tr, 1)
     st = torch.tensor([stages[k] for k in sorted(stages)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(st, op=dist.ReduceOp.MAX)

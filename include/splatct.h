@@ -215,8 +215,9 @@ int splatct_proj_block_fill(const int64_t* ptr, const int32_t* idx, const float*
                             void* stream);
 
 /* Length (doubles) of the tv_partial buffer splatct_proj_adjoint_blocked
- * writes for a w x h x c slab: one slot per (pixel column, 32*V-slice chunk),
- * each written exactly once (reduce the whole buffer in a fixed order). */
+ * writes for a w x h x c slab: one slot per (2 x 2 pixel quad, 32*V-slice
+ * chunk), each written exactly once (reduce the whole buffer in a fixed
+ * order). */
 int splatct_proj_tv_partial_len(int w, int h, int c, int64_t* len);
 
 /* Blocked applications: same results as splatct_proj_forward /
@@ -283,6 +284,18 @@ int splatct_loss_fused_prepared(const float* pred, const float* ref, int m, int 
                                 double lmax, double lambda1, double lambda2, double l1_count,
                                 double ssim_slices, float* grad_pred, void* ws, size_t ws_bytes,
                                 double* sums, const int* halt, void* stream);
+/* The same, leaving the l1 and SSIM sums as block partials in ws (sums[0] and
+ * sums[1] are not written, except sums[1] = 0 when lambda2 = 0):
+ * splatct_iter_finalize_partials reduces them.  splatct_loss_partials gives
+ * their addresses and counts (n_ssim = 0 when lambda2 = 0). */
+int splatct_loss_fused_prepared_deferred(const float* pred, const float* ref, int m, int n, int p,
+                                         double lmax, double lambda1, double lambda2,
+                                         double l1_count, double ssim_slices, float* grad_pred,
+                                         void* ws, size_t ws_bytes, double* sums,
+                                         const int* halt, void* stream);
+int splatct_loss_partials(int m, int n, int p, double lambda2, void* ws, size_t ws_bytes,
+                          const double** l1_part, int64_t* n_l1, const double** ssim_part,
+                          int64_t* n_ssim);
 
 /* out[0] = sum (x-y)^2 over count elements (f64, fixed order); ws holds
  * SPLATCT_SQDIFF_BLOCKS doubles.  Used for PSNR (metrics.psnr, metrics.py:24-38). */
@@ -293,13 +306,6 @@ int splatct_sum_sq_diff(const float* x, const float* y, int64_t count, double* w
 /* Sum n doubles in a fixed order into out[0] (deterministic reductions). */
 int splatct_reduce_sum(const double* in, int64_t n, double* out, void* stream);
 
-/* Iteration bookkeeping (optim.py:350-386): from the global sums
- * {l1_sum, ssim_sum, tv_sum} compute the loss parts
- * (zero-weight terms -> NaN, loss.py:216-239), write
- * trace[4*it .. 4*it+3] = {loss, l1, ssim, tv} with it = *iter, set *halt if
- * the loss is non-finite (optim.py:356), else write the Adam scalars
- * adam[0..2] = {lr, 1-b1^t, 1-b2^t} for the pre-increment *step
- * (optim.py:88-90,123-126) and advance *step and *iter. */
 /* TV terms across a z-slab boundary after an adjoint that ran without halo
  * planes (the halo exchange then overlaps it), loss.py:183-207: plane c-1 gets
  * -lambda/count * sign(hi - v) and |hi - v| is added to *tv_sum (this slab
@@ -308,11 +314,30 @@ int splatct_reduce_sum(const double* in, int64_t n, double* out, void* stream);
 int splatct_tv_halo_fixup(const float* vol_yxz, float* dl_yxz, const float* halo_lo,
                           const float* halo_hi, int w, int h, int c, double lambda_tv,
                           double tv_count, double* tv_sum, const int* halt, void* stream);
+/* Iteration bookkeeping (optim.py:350-386): from the global sums
+ * {l1_sum, ssim_sum, tv_sum} compute the loss parts
+ * (zero-weight terms -> NaN, loss.py:216-239), write
+ * trace[4*it .. 4*it+3] = {loss, l1, ssim, tv} with it = *iter, set *halt if
+ * the loss is non-finite (optim.py:356), else write the Adam scalars
+ * adam[0..2] = {lr, 1-b1^t, 1-b2^t} for the pre-increment *step
+ * (optim.py:88-90,123-126) and advance *step and *iter. */
 int splatct_iter_finalize(const double* sums, double lambda1, double lambda2, double lambda3,
                           double l1_count, double ssim_count, double tv_count, double lr0,
                           double lrf, int64_t max_iters, int64_t* step, int64_t* iter,
                           double* trace, int64_t trace_cap, double* adam, int* halt,
                           void* stream);
+/* The same, first reducing sums[0..2] = {l1, ssim, tv} from block partials
+ * (one 1024-thread block, the fixed order of splatct_reduce_sum, so bitwise
+ * its results); a part with n = 0 keeps sums[f] as given.  Replaces the three
+ * separate reductions of the single-device training step. */
+int splatct_iter_finalize_partials(double* sums, const double* l1_part, int64_t n_l1,
+                                   const double* ssim_part, int64_t n_ssim,
+                                   const double* tv_part, int64_t n_tv, double lambda1,
+                                   double lambda2, double lambda3, double l1_count,
+                                   double ssim_count, double tv_count, double lr0, double lrf,
+                                   int64_t max_iters, int64_t* step, int64_t* iter,
+                                   double* trace, int64_t trace_cap, double* adam, int* halt,
+                                   void* stream);
 
 /* ---------------------------------------------------------------------------
  * Adam: optim.adam_step (optim.py:109-144): bias-corrected Adam on the

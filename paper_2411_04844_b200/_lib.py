@@ -20,6 +20,7 @@ c_sz = ctypes.c_size_t
 c_vp = ctypes.c_void_p
 c_szp = ctypes.POINTER(ctypes.c_size_t)
 c_i64p = ctypes.POINTER(ctypes.c_int64)
+c_vpp = ctypes.POINTER(ctypes.c_void_p)
 
 # name -> argtypes (all return int status except where noted)
 SIGNATURES: dict[str, list] = {
@@ -80,6 +81,14 @@ SIGNATURES: dict[str, list] = {
     "splatct_reduce_sum": [c_vp, c_i64, c_vp, c_vp],
     "splatct_iter_finalize": [c_vp, c_f64, c_f64, c_f64, c_f64, c_f64, c_f64, c_f64, c_f64, c_i64,
                               c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp],
+    "splatct_iter_finalize_partials": [c_vp, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_f64, c_f64,
+                                       c_f64, c_f64, c_f64, c_f64, c_f64, c_f64, c_i64, c_vp,
+                                       c_vp, c_vp, c_i64, c_vp, c_vp, c_vp],
+    "splatct_loss_partials": [c_i32, c_i32, c_i32, c_f64, c_vp, c_sz, c_vpp, c_i64p, c_vpp,
+                              c_i64p],
+    "splatct_loss_fused_prepared_deferred": [c_vp, c_vp, c_i32, c_i32, c_i32, c_f64, c_f64,
+                                             c_f64, c_f64, c_f64, c_vp, c_vp, c_sz, c_vp, c_vp,
+                                             c_vp],
     "splatct_adam": [c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_f64, c_f64, c_vp, c_vp],
     "splatct_fbp_filter": [c_vp, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp],
     "splatct_fbp_backproject": [c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_i32, c_f64,

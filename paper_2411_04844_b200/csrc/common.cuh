@@ -99,6 +99,21 @@ __device__ __forceinline__ double block_sum(double v, double* sh /* >= NT/32 */)
     return r;
 }
 
+// Sum of in[0, n) by one 1024-thread block, fixed order (8 independent
+// accumulators per thread, then block_sum): bitwise the same wherever it runs.
+__device__ __forceinline__ double block_reduce_f64(const double* __restrict__ in, int64_t n,
+                                                   double* sh) {
+    double a[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    int64_t i = threadIdx.x;
+    for (; i + 7 * 1024 < n; i += 8 * 1024) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) a[k] += in[i + k * 1024];
+    }
+    for (int k = 0; i < n; i += 1024, ++k) a[k & 7] += in[i];
+    const double acc = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+    return block_sum<1024>(acc, sh);
+}
+
 // Packed FP32 FMA (sm_100 FFMA2): d = a * b + c on both halves; with b a
 // broadcast scalar the compiler uses the .F32 operand form, so one issue slot
 // does two FMAs.

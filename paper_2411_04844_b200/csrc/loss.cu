@@ -700,13 +700,29 @@ __global__ void __launch_bounds__(256) k_sq_diff(const float* __restrict__ x,
     if (threadIdx.x == 0) part[blockIdx.x] = r;
 }
 
-__global__ void k_iter_finalize(const double* __restrict__ sums, double l1w, double ssw,
-                                double tvw, double l1_count, double ssim_count, double tv_count,
-                                double lr0, double lrf, int64_t max_iters, int64_t* step,
-                                int64_t* iter, double* trace, int64_t trace_cap, double* adam,
-                                int* halt) {
+// Optional first stage (one 1024-thread block, Part.n[f] > 0): sums[f] is
+// reduced here from the block partials the loss and the adjoint left, in the
+// fixed order of k_reduce_sum (bitwise its result), saving three launches.
+struct FinParts {
+    const double* p[3];   // l1, ssim, tv partials (or null: sums[f] is final)
+    int64_t n[3];
+};
+
+__global__ void k_iter_finalize(double* __restrict__ sums, FinParts parts, double l1w,
+                                double ssw, double tvw, double l1_count, double ssim_count,
+                                double tv_count, double lr0, double lrf, int64_t max_iters,
+                                int64_t* step, int64_t* iter, double* trace, int64_t trace_cap,
+                                double* adam, int* halt) {
     griddep_wait();
     if (*halt) return;
+    __shared__ double sh[32];
+#pragma unroll
+    for (int f = 0; f < 3; ++f) {
+        if (parts.p[f] == nullptr) continue;   // uniform
+        const double r = block_reduce_f64(parts.p[f], parts.n[f], sh);
+        if (threadIdx.x == 0) sums[f] = r;
+    }
+    if (threadIdx.x != 0) return;
     const double nan = __longlong_as_double(0x7ff8000000000000LL);
     const double l1 = l1w > 0 ? sums[0] / l1_count : nan;
     const double ss = ssw > 0 ? 1.0 - sums[1] / ssim_count : nan;
@@ -785,7 +801,9 @@ int splatct_sino_max(const float* x, int64_t count, double* out, void* stream) {
 static int loss_fused_impl(const float* pred, const float* ref, int m, int n, int p, double lmax,
                            double lambda1, double lambda2, double l1_count, double ssim_slices,
                            float* grad_pred, void* ws, size_t ws_bytes, double* sums,
-                           const int* halt, void* stream, bool prepared) {
+                           const int* halt, void* stream, bool prepared, bool defer = false) {
+    // defer: leave the block partials in ws (splatct_loss_partials) for
+    // splatct_iter_finalize_partials to reduce, instead of two reduce launches
     SPLATCT_REQUIRE(m > 0 && n > 0 && p > 0, "invalid sinogram dims");
     LossLayout L = loss_layout(m, n, p);
     SPLATCT_REQUIRE(ws_bytes >= L.total, "loss workspace too small");
@@ -813,7 +831,8 @@ static int loss_fused_impl(const float* pred, const float* ref, int m, int n, in
                 k_ssim_stats11<0><<<gs, R_NT, 0, s>>>(pred, ref, m, n, p, W, c1, c2, L.vr, L.vc,
                                                       D11, ps, RS, halt);
             SPLATCT_LAUNCH_CK();
-            if (int e = reduce_sum_f64(ps, L.nb_s11, sums + 1, s)) return e;
+            if (!defer)
+                if (int e = reduce_sum_f64(ps, L.nb_s11, sums + 1, s)) return e;
         } else {
             SPLATCT_CK(cudaMemsetAsync(sums + 1, 0, sizeof(double), s));
         }
@@ -821,7 +840,7 @@ static int loss_fused_impl(const float* pred, const float* ref, int m, int n, in
                               L.vc, D11, lambda1, l1_count, lambda2, ssim_slices, grad_pred, pl,
                               halt));
         SPLATCT_LAUNCH_CK();
-        return reduce_sum_f64(pl, L.nb_g11, sums, s);
+        return defer ? SPLATCT_OK : reduce_sum_f64(pl, L.nb_g11, sums, s);
     }
     for (int ci = 0; ci < L.nchunks; ++ci) {
         const int z0 = ci * ZC, zc = min(ZC, p - z0);
@@ -856,11 +875,13 @@ static int loss_fused_impl(const float* pred, const float* ref, int m, int n, in
         SPLATCT_LAUNCH_CK();
     }
     if (lambda2 > 0.0) {
-        if (int e = reduce_sum_f64(ps, L.nb_v * L.nchunks, sums + 1, s)) return e;
+        if (!defer)
+            if (int e = reduce_sum_f64(ps, L.nb_v * L.nchunks, sums + 1, s)) return e;
     } else {
         SPLATCT_CK(cudaMemsetAsync(sums + 1, 0, sizeof(double), s));
     }
-    if (int e = reduce_sum_f64(pl, L.nb_g * L.nchunks, sums, s)) return e;
+    if (!defer)
+        if (int e = reduce_sum_f64(pl, L.nb_g * L.nchunks, sums, s)) return e;
     return SPLATCT_OK;
 }
 
@@ -959,11 +980,54 @@ int splatct_iter_finalize(const double* sums, double lambda1, double lambda2, do
                           double lrf, int64_t max_iters, int64_t* step, int64_t* iter,
                           double* trace, int64_t trace_cap, double* adam, int* halt,
                           void* stream) {
-    SPLATCT_CK(launch_pdl(k_iter_finalize, dim3(1), dim3(1), 0, as_stream(stream), sums, lambda1,
-                          lambda2, lambda3, l1_count, ssim_count, tv_count, lr0, lrf, max_iters,
-                          step, iter, trace, trace_cap, adam, halt));
+    const FinParts none{{nullptr, nullptr, nullptr}, {0, 0, 0}};
+    SPLATCT_CK(launch_pdl(k_iter_finalize, dim3(1), dim3(1), 0, as_stream(stream),
+                          const_cast<double*>(sums), none, lambda1, lambda2, lambda3, l1_count,
+                          ssim_count, tv_count, lr0, lrf, max_iters, step, iter, trace, trace_cap,
+                          adam, halt));
     SPLATCT_LAUNCH_CK();
     return SPLATCT_OK;
+}
+
+int splatct_iter_finalize_partials(double* sums, const double* l1_part, int64_t n_l1,
+                                   const double* ssim_part, int64_t n_ssim,
+                                   const double* tv_part, int64_t n_tv, double lambda1,
+                                   double lambda2, double lambda3, double l1_count,
+                                   double ssim_count, double tv_count, double lr0, double lrf,
+                                   int64_t max_iters, int64_t* step, int64_t* iter,
+                                   double* trace, int64_t trace_cap, double* adam, int* halt,
+                                   void* stream) {
+    const FinParts parts{{n_l1 > 0 ? l1_part : nullptr, n_ssim > 0 ? ssim_part : nullptr,
+                          n_tv > 0 ? tv_part : nullptr},
+                         {n_l1, n_ssim, n_tv}};
+    SPLATCT_CK(launch_pdl(k_iter_finalize, dim3(1), dim3(1024), 0, as_stream(stream), sums,
+                          parts, lambda1, lambda2, lambda3, l1_count, ssim_count, tv_count, lr0,
+                          lrf, max_iters, step, iter, trace, trace_cap, adam, halt));
+    SPLATCT_LAUNCH_CK();
+    return SPLATCT_OK;
+}
+
+int splatct_loss_partials(int m, int n, int p, double lambda2, void* ws, size_t ws_bytes,
+                          const double** l1_part, int64_t* n_l1, const double** ssim_part,
+                          int64_t* n_ssim) {
+    SPLATCT_REQUIRE(m > 0 && n > 0 && p > 0, "invalid sinogram dims");
+    LossLayout L = loss_layout(m, n, p);
+    SPLATCT_REQUIRE(ws_bytes >= L.total, "loss workspace too small");
+    char* base = reinterpret_cast<char*>(ws);
+    *l1_part = reinterpret_cast<const double*>(base + L.o_pl);
+    *n_l1 = L.k11 ? L.nb_g11 : L.nb_g * L.nchunks;
+    *ssim_part = reinterpret_cast<const double*>(base + L.o_ps);
+    *n_ssim = lambda2 > 0.0 ? (L.k11 ? L.nb_s11 : L.nb_v * L.nchunks) : 0;
+    return SPLATCT_OK;
+}
+
+int splatct_loss_fused_prepared_deferred(const float* pred, const float* ref, int m, int n, int p,
+                                         double lmax, double lambda1, double lambda2,
+                                         double l1_count, double ssim_slices, float* grad_pred,
+                                         void* ws, size_t ws_bytes, double* sums,
+                                         const int* halt, void* stream) {
+    return loss_fused_impl(pred, ref, m, n, p, lmax, lambda1, lambda2, l1_count, ssim_slices,
+                           grad_pred, ws, ws_bytes, sums, halt, stream, true, true);
 }
 
 int splatct_adam(double* params, const double* grads, double* m1, double* m2, int64_t n,

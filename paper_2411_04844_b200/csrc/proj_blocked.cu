@@ -508,7 +508,7 @@ __global__ void __launch_bounds__(32 * BS_WARPS, R == 8 ? 4 : 6) k_bspmm(GroupMa
         for (int yy = ya; yy <= yb; ++yy)
             for (int xx = xa; xx <= xb; ++xx) any |= oc.occ[(int64_t)yy * gm.w + xx];
         if (!halo && (any & zm) == 0ull) {   // warp-uniform
-            if (TV && tv.partial && lane == 0) tv.partial[zch * (int64_t)gm.nrows + g] = 0.0;
+            if (TV && tv.partial && lane == 0) tv.partial[zch * ngr + g] = 0.0;
             return;
         }
     }
@@ -577,7 +577,7 @@ __global__ void __launch_bounds__(32 * BS_WARPS, R == 8 ? 4 : 6) k_bspmm(GroupMa
         tv_epilogue_quad<V>(tv, gm, g, zb, c, zok, acc, Y, tvsum);
         if (tv.partial) {   // slot (z-chunk, quad): written once, reduced in fixed order
             tvsum = warp_sum(tvsum);
-            if (lane == 0) tv.partial[zch * (int64_t)gm.nrows + g] = tvsum;
+            if (lane == 0) tv.partial[zch * ngr + g] = tvsum;
         }
     } else {
 #pragma unroll
@@ -755,8 +755,8 @@ using namespace splatct;
 extern "C" {
 
 int splatct_proj_tv_partial_len(int w, int h, int c, int64_t* len) {
-    const int V = vec_width(c);
-    *len = (int64_t)w * h * ((c + 32 * V - 1) / (32 * V));
+    const int V = vec_width(c);   // one slot per (z-chunk, 2 x 2 quad)
+    *len = (int64_t)((w + 1) / 2) * ((h + 1) / 2) * ((c + 32 * V - 1) / (32 * V));
     return SPLATCT_OK;
 }
 

@@ -167,15 +167,7 @@ __global__ void __launch_bounds__(1024) k_reduce_sum(const double* __restrict__ 
     __shared__ double sh[32];
     // 8 independent loads in flight per thread (a fixed order: deterministic);
     // the strided single loop was latency-bound (~17 us for the C2 TV partials)
-    double a[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    int64_t i = threadIdx.x;
-    for (; i + 7 * 1024 < n; i += 8 * 1024) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) a[k] += in[i + k * 1024];
-    }
-    for (int k = 0; i < n; i += 1024, ++k) a[k & 7] += in[i];
-    const double acc = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
-    double r = block_sum<1024>(acc, sh);
+    const double r = block_reduce_f64(in, n, sh);
     if (threadIdx.x == 0) out[0] = r;
 }
 

@@ -713,11 +713,12 @@ def operator_for(geom: ScanGeometry, w: int, h: int, c_global: int, step: float 
     return projector_for(geom, w, h, step, device)
 
 
-def tv_partial_len(w: int, h: int, c: int) -> int:
-    """Doubles in the tv_partial buffer of the blocked adjoint (+ CSR: w*h)."""
+def tv_partial_len(w: int, h: int, c: int, blocked: bool = False) -> int:
+    """Doubles in a tv_partial buffer: what the blocked adjoint writes
+    (blocked=True), else room for either adjoint (the CSR one writes w*h)."""
     n = ctypes.c_int64(0)
     call("splatct_proj_tv_partial_len", int(w), int(h), int(c), ctypes.byref(n))
-    return max(int(n.value), int(w) * int(h))
+    return int(n.value) if blocked else max(int(n.value), int(w) * int(h))
 
 
 def tv_operator(w: int, h: int, device=None) -> ProjectorOperator:
@@ -759,12 +760,25 @@ class LossPlan:
         self.prepared_ref = ref.data_ptr()
 
     def fused(self, pred, ref, lmax: float, lambda1: float, lambda2: float, l1_count: float,
-              ssim_slices: float, grad_out, sums, halt=None):
-        fn = ("splatct_loss_fused_prepared" if self.prepared_ref == ref.data_ptr()
-              else "splatct_loss_fused")
+              ssim_slices: float, grad_out, sums, halt=None, defer: bool = False):
+        """defer (prepared ref only): leave sums[0:2] as block partials for
+        iter_finalize_partials (partials() gives them)."""
+        prepared = self.prepared_ref == ref.data_ptr()
+        if defer and not prepared:
+            raise ValueError("a deferred loss needs the prepared reference")
+        fn = ("splatct_loss_fused_prepared_deferred" if defer
+              else "splatct_loss_fused_prepared" if prepared else "splatct_loss_fused")
         call(fn, ptr(pred), ptr(ref), self.m, self.n, self.p, float(lmax),
              float(lambda1), float(lambda2), float(l1_count), float(ssim_slices), ptr(grad_out),
              ptr(self.ws), self.ws_bytes, ptr(sums), ptr(halt), stream_handle())
+
+    def partials(self, lambda2: float):
+        """(l1 pointer, count, SSIM pointer, count) of a deferred loss's block partials."""
+        a, b = ctypes.c_void_p(0), ctypes.c_void_p(0)
+        na, nb = ctypes.c_int64(0), ctypes.c_int64(0)
+        call("splatct_loss_partials", self.m, self.n, self.p, float(lambda2), ptr(self.ws),
+             self.ws_bytes, ctypes.byref(a), ctypes.byref(na), ctypes.byref(b), ctypes.byref(nb))
+        return a, int(na.value), b, int(nb.value)
 
 
 def sino_max(x: torch.Tensor) -> float:

@@ -229,12 +229,19 @@ class Trainer:
             st.append(("comm", lambda: self.comm.reduce_scatter_rows(self.pred, self.bands,
                                                                      self.pred_band)))
 
+        # single device: the loss and TV sums stay block partials that the
+        # iteration's finalize reduces (three reduction launches saved)
+        fused_loss = (lw.lambda1 > 0 or lw.lambda2 > 0) and self.loss is not None
+        defer = not sharded and fused_loss and self.loss.prepared_ref == self.meas.data_ptr()
+        tv_blocked = getattr(self.op, "blocked", False)
+        defer_tv = not sharded and lw.lambda3 > 0 and tv_blocked
+
         def data_loss():
             pred, meas, gpred = ((self.pred_band, self.meas_band, self.gpred_band) if replicated
                                  else (self.pred, self.meas, self.gpred))
-            if (lw.lambda1 > 0 or lw.lambda2 > 0) and self.loss is not None:
+            if fused_loss:
                 self.loss.fused(pred, meas, self.lmax, lw.lambda1, lw.lambda2, self.l1_count,
-                                float(self.p_global), gpred, self.sums, halt)
+                                float(self.p_global), gpred, self.sums, halt, defer=defer)
             else:
                 gpred.zero_()
                 self.sums[0:2].zero_()
@@ -250,7 +257,8 @@ class Trainer:
                 self.op.adjoint(self.gpred, self.dl, vol=self.vol, lambda_tv=lw.lambda3,
                                 tv_count=self.tv_count, tv_partial=self.tv_part, halt=halt,
                                 z0=z0, occ=self.fvr)
-                D.reduce_sum(self.tv_part, self.sums[2:3])
+                if not defer_tv:
+                    D.reduce_sum(self.tv_part, self.sums[2:3])
             st.append(("gpu", adjoint_tv))
             if overlap_halo:
                 def halo_wait():
@@ -269,12 +277,23 @@ class Trainer:
         if sharded:
             st.append(("comm", lambda: self.comm.allreduce_sum_(self.sums)))
 
+        parts = None
+        if defer or defer_tv:
+            l1p, nl1, ssp, nss = (self.loss.partials(lw.lambda2) if defer
+                                  else (D.VP(0), 0, D.VP(0), 0))
+            tvn = D.tv_partial_len(self.w, self.h, self.slab.c_local, blocked=True)
+            parts = (l1p, nl1, ssp, nss, D.ptr(self.tv_part) if defer_tv else D.VP(0),
+                     tvn if defer_tv else 0)
+
         def finalize_backward():
-            D.call("splatct_iter_finalize", D.ptr(self.sums), float(lw.lambda1),
-                   float(lw.lambda2), float(lw.lambda3), self.l1_count, self.ssim_count,
-                   self.tv_count, self.lr0, self.lrf, self.max_iters, D.ptr(self.step_t),
-                   D.ptr(self.iter_t), D.ptr(self.trace), self.trace_cap, D.ptr(self.adam_s),
-                   D.ptr(halt), D.stream_handle())
+            scal = (float(lw.lambda1), float(lw.lambda2), float(lw.lambda3), self.l1_count,
+                    self.ssim_count, self.tv_count, self.lr0, self.lrf, self.max_iters,
+                    D.ptr(self.step_t), D.ptr(self.iter_t), D.ptr(self.trace), self.trace_cap,
+                    D.ptr(self.adam_s), D.ptr(halt), D.stream_handle())
+            if parts is not None:
+                D.call("splatct_iter_finalize_partials", D.ptr(self.sums), *parts, *scal)
+            else:
+                D.call("splatct_iter_finalize", D.ptr(self.sums), *scal)
             self.fvr.backward(self.params, self.dl, self.grads,
                               None if sharded else self.accum, halt)
         st.append(("gpu", finalize_backward))
