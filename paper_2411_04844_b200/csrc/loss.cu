@@ -366,8 +366,11 @@ __global__ void __launch_bounds__(R_NT, MODE == 1 ? 2 : 1) k_ssim_stats11(const 
     griddep_wait();
     if (halted(halt)) return;
     constexpr int NF = MODE == 0 ? 5 : (MODE == 1 ? 3 : 2);   // ring fields
-    __shared__ __align__(16) float sf[R_BUF][2][R_SPAN][32];    // cp.async landing (f32)
-    __shared__ __align__(16) double sd[2][2][R_SPAN][32];       // converted rows (f64)
+    // cp.async landing ring (f32), read in place: one slot more than the
+    // staging depth, so a row is rewritten only after every warp has passed
+    // the barrier that follows its last read
+    constexpr int S_BUF = R_BUF + 1;
+    __shared__ __align__(16) float sf[S_BUF][2][R_SPAN][32];
     // MODE 1: the reference window moments of an output row, staged by cp.async
     // with the input rows (4 slots: a slot is rewritten two barriers after its read)
     constexpr int RS_BUF = R_AHEAD + 2;
@@ -411,7 +414,7 @@ __global__ void __launch_bounds__(R_NT, MODE == 1 ? 2 : 1) k_ssim_stats11(const 
             }
         }
         if (v < m) {
-            float* buf = &sf[v % R_BUF][0][0][0];
+            float* buf = &sf[v % S_BUF][0][0][0];
 #pragma unroll
             for (int k = 0; k < S_SLOTS; ++k) {
                 if (!mine[k]) continue;
@@ -423,18 +426,6 @@ __global__ void __launch_bounds__(R_NT, MODE == 1 ? 2 : 1) k_ssim_stats11(const 
         }
         cp_commit_group();
     };
-    auto convert = [&](int v) {   // own chunks of row v: f32 landing -> f64 row buffer
-        const float* fb = &sf[v % R_BUF][0][0][0];
-        double* db = &sd[v & 1][0][0][0];
-#pragma unroll
-        for (int k = 0; k < S_SLOTS; ++k) {
-            if (!mine[k]) continue;
-            const float4 f = *reinterpret_cast<const float4*>(fb + soff[k]);
-            double2* d2 = reinterpret_cast<double2*>(db + soff[k]);
-            d2[0] = make_double2((double)f.x, (double)f.y);
-            d2[1] = make_double2((double)f.z, (double)f.w);
-        }
-    };
 #pragma unroll
     for (int q = 0; q < R_AHEAD; ++q) issue(q);
     double ring[11][NF];
@@ -445,9 +436,8 @@ __global__ void __launch_bounds__(R_NT, MODE == 1 ? 2 : 1) k_ssim_stats11(const 
             const int v = v0 + ph;
             if (v >= m) break;
             cp_wait_group<R_AHEAD - 1>();   // my chunks of row v landed (later rows in flight)
-            convert(v);
-            issue(v + R_AHEAD);   // my landing slot of row v-1 is free (converted last step)
-            __syncthreads();      // row v (f64) complete; everyone is past row v-2's reads
+            issue(v + R_AHEAD);   // slot (v+2) % 4: last read at row v-2, before the previous barrier
+            __syncthreads();      // row v complete in shared memory
             // MODE 1: the reference window moments of output row v-10, loaded
             // before the row's arithmetic so their latency overlaps it
             double rs_my = 0.0, rs_y2 = 0.0;
@@ -455,21 +445,21 @@ __global__ void __launch_bounds__(R_NT, MODE == 1 ? 2 : 1) k_ssim_stats11(const 
                 rs_my = srs[v % RS_BUF][0][cl][lane];
                 rs_y2 = srs[v % RS_BUF][1][cl][lane];
             }
-            const double* xr = &sd[v & 1][0][cl][lane];
-            const double* yr = &sd[v & 1][1][cl][lane];
+            const float* xr = &sf[v % S_BUF][0][cl][lane];
+            const float* yr = &sf[v % S_BUF][1][cl][lane];
             double h[2][NF];
 #pragma unroll
             for (int f = 0; f < NF; ++f) h[0][f] = h[1][f] = 0.0;
 #pragma unroll
             for (int b = 0; b < 11; ++b) {
                 double* hb = h[b & 1];
-                const double yv = yr[32 * b];
+                const double yv = (double)yr[32 * b];
                 if (MODE == 2) {          // {y, y^2}
                     const double gy = W.gc[b] * yv;
                     hb[0] += gy;
                     hb[1] = fma(gy, yv, hb[1]);
                 } else {
-                    const double xv = xr[32 * b];
+                    const double xv = (double)xr[32 * b];
                     const double gx = W.gc[b] * xv;
                     hb[0] += gx;                       // x
                     hb[1] = fma(gx, xv, hb[1]);        // x^2
