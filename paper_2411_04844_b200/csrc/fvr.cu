@@ -25,6 +25,7 @@
 //     partial buffers, deterministic.
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include "tmap.cuh"
 
 #include <cstdlib>
 #include <cstring>
@@ -2699,29 +2700,15 @@ int splatct_fvr_bin_row_ordered(const double* params, int64_t n, int w, int h, i
 // then stores with plain vector stores)
 static bool volume_tensor_map(CUtensorMap* m, const float* vol, int w, int h, int c,
                               int bz = 16, int bx = 16, int by = 16, bool swizzle = true) {
-    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-    static bool tried = false;
-    if (!tried) {
-        tried = true;
-        cudaDriverEntryPointQueryResult q;
-        void* fn = nullptr;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
-                cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-    }
-    memset(m, 0, sizeof(*m));
-    if (!encode || (c & 3) != 0 || ((uintptr_t)vol & 15) != 0 || getenv("SPLATCT_NO_TMA"))
+    if ((c & 3) != 0) {
+        memset(m, 0, sizeof(*m));
         return false;
+    }
     const cuuint64_t dim[3] = {(cuuint64_t)c, (cuuint64_t)w, (cuuint64_t)h};
     const cuuint64_t stride[2] = {(cuuint64_t)c * 4, (cuuint64_t)c * w * 4};
     const cuuint32_t box[3] = {(cuuint32_t)bz, (cuuint32_t)bx, (cuuint32_t)by};
-    const cuuint32_t estride[3] = {1, 1, 1};
-    return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(vol), dim, stride,
-                  box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  swizzle ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE,
-                  CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
-           CUDA_SUCCESS;
+    return encode_tiled(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, vol, dim, stride, box,
+                        swizzle ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE);
 }
 
 static int fvr_forward_impl(const double* params, int64_t n, int w, int h, int c, int z0, int hx,

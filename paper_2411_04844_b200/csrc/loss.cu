@@ -19,6 +19,8 @@
 // cancels).  Pass 1 writes the three SSIM derivative fields, pass 2 applies
 // the transposed correlation and fuses the L1 term and the f32 store.
 #include "common.cuh"
+#include "tc.cuh"
+#include "tmap.cuh"
 
 namespace splatct {
 
@@ -517,6 +519,17 @@ constexpr int G_DCHUNKS = 3 * R_SPAN * 8;                    // D (f32): 3 field
 constexpr int G_DSLOTS = (G_DCHUNKS + R_NT - 1) / R_NT;
 constexpr int G_XCHUNKS = 2 * R_COLS * 8;                    // x, y: R_COLS cols x 8 chunks
 
+// The staged rows of the gradient kernel (bytes): D fields 3 x R_SPAN x 32 f32,
+// x and y R_COLS x 32 f32 each -- also the TMA boxes' sizes.
+constexpr unsigned G_DBYTES = 3 * R_SPAN * 32 * 4;
+constexpr unsigned G_XBYTES = R_COLS * 32 * 4;
+
+// Tensor maps of the gradient kernel's row loads (use = 0: cp.async path).
+struct GradMaps {
+    CUtensorMap d, x, y;   // D [3][vr][vc][p] box {32, R_SPAN, 1, 3}; X, Y [m][n][p] box {32, R_COLS, 1}
+    int use;
+};
+
 __global__ void __launch_bounds__(R_NT, 2) k_loss_grad11(const float* __restrict__ X,
                                                          const float* __restrict__ Y, int m, int n,
                                                          int p, Win W, int vr, int vc,
@@ -524,6 +537,7 @@ __global__ void __launch_bounds__(R_NT, 2) k_loss_grad11(const float* __restrict
                                                          double l1_count, double ssw,
                                                          double ssim_slices, float* __restrict__ G,
                                                          double* __restrict__ part,
+                                                         const __grid_constant__ GradMaps tm,
                                                          const int* halt) {
     griddep_wait();
     if (halted(halt)) return;
@@ -531,9 +545,20 @@ __global__ void __launch_bounds__(R_NT, 2) k_loss_grad11(const float* __restrict
 #pragma unroll
     for (int b = 0; b < 11; ++b) gcf[b] = (float)W.gc[b];
     // per staged row: D columns s0-10 .. s0+7 (3 fields) and x, y columns s0 .. s0+7
-    __shared__ __align__(16) float sd[G_BUF][3][R_SPAN][32];
-    __shared__ __align__(16) float sxy[G_BUF][2][R_COLS][32];
+    __shared__ __align__(128) float sd[G_BUF][3][R_SPAN][32];
+    __shared__ __align__(128) float sxy[G_BUF][2][R_COLS][32];
     __shared__ double red[R_NT / 32];
+    // TMA path: one thread loads a row's three boxes (D fields, x, y) behind a
+    // per-buffer mbarrier instead of 224 threads issuing 16-byte cp.async chunks;
+    // the tensor maps zero-fill columns and slices outside the sinogram
+    __shared__ __align__(8) uint64_t gbar[G_BUF];
+    if (tm.use) {
+        if (threadIdx.x == 0) {
+            for (int b = 0; b < G_BUF; ++b) tc::mbar_init(&gbar[b], 1);
+            tc::mbar_init_fence();
+        }
+        __syncthreads();
+    }
     const int lane = threadIdx.x & 31, cl = threadIdx.x >> 5;
     const int zb = blockIdx.x * 32, s0 = blockIdx.y * R_COLS;
     const int z = zb + lane, s = s0 + cl;
@@ -564,7 +589,36 @@ __global__ void __launch_bounds__(R_NT, 2) k_loss_grad11(const float* __restrict
     const int64_t xgo = xok ? (int64_t)(s0 + xcol) * p + zb + 4 * xq : 0;
     const float* xsrc = xarr ? Y : X;
     const int64_t drow = (int64_t)vc * p, xrowstride = (int64_t)n * p;
+    auto issue_tma = [&](int r) {   // thread 0
+        if (r >= m) return;
+        const int buf = r % G_BUF;
+        const bool dr = ss && r < vr;
+        const unsigned bar = tc::smem_u32(&gbar[buf]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar),
+                     "r"((dr ? G_DBYTES : 0u) + 2u * G_XBYTES)
+                     : "memory");
+        if (dr)
+            asm volatile(
+                "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes "
+                "[%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(tc::smem_u32(&sd[buf][0][0][0])),
+                "l"(&tm.d), "r"(zb), "r"(s0 - 10), "r"(r), "r"(0), "r"(bar)
+                : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
+            "[%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(tc::smem_u32(&sxy[buf][0][0][0])),
+            "l"(&tm.x), "r"(zb), "r"(s0), "r"(r), "r"(bar)
+            : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
+            "[%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(tc::smem_u32(&sxy[buf][1][0][0])),
+            "l"(&tm.y), "r"(zb), "r"(s0), "r"(r), "r"(bar)
+            : "memory");
+    };
     auto issue = [&](int r) {
+        if (tm.use) {
+            if (threadIdx.x == 0) issue_tma(r);
+            return;
+        }
         if (r < m) {
             const int buf = r % G_BUF;
             if (ss && r < vr) {
@@ -589,8 +643,11 @@ __global__ void __launch_bounds__(R_NT, 2) k_loss_grad11(const float* __restrict
         for (int ph = 0; ph < 11; ++ph) {
             const int r = r0 + ph;
             if (r >= m) break;
-            cp_wait_group<G_AHEAD - 1>();
-            __syncthreads();
+            if (tm.use)
+                tc::mbar_wait(&gbar[r % G_BUF], (uint32_t)(r / G_BUF) & 1u);   // row r landed
+            else
+                cp_wait_group<G_AHEAD - 1>();
+            __syncthreads();   // and every warp is past row r - 1: its buffer is free
             issue(r + G_AHEAD);
             const int buf = r % G_BUF;
             if (ss && r < vr) {
@@ -637,9 +694,30 @@ __global__ void __launch_bounds__(R_NT, 2) k_loss_grad11(const float* __restrict
             }
         }
     }
-    cp_wait_group<0>();
+    if (!tm.use) cp_wait_group<0>();   // TMA: rows >= m are never issued, all issued were waited
     const double rr = block_sum<R_NT>(l1sum, red);
     if (threadIdx.x == 0) part[blockIdx.y * gridDim.x + blockIdx.x] = rr;
+}
+
+// Tensor maps for k_loss_grad11 (p % 4 == 0 and 16-byte aligned bases: the
+// k11 path's requirements); use = 0 when TMA is unavailable.
+static GradMaps grad_maps(const float* X, const float* Y, const float* D, int m, int n, int p,
+                          int vr, int vc) {
+    GradMaps g;
+    const cuuint64_t fp = (cuuint64_t)p * 4;
+    const cuuint64_t ddim[4] = {(cuuint64_t)p, (cuuint64_t)vc, (cuuint64_t)vr, 3};
+    const cuuint64_t dstr[3] = {fp, fp * vc, fp * vc * vr};
+    const cuuint32_t dbox[4] = {32, R_SPAN, 1, 3};
+    const cuuint64_t xdim[3] = {(cuuint64_t)p, (cuuint64_t)n, (cuuint64_t)m};
+    const cuuint64_t xstr[2] = {fp, fp * n};
+    const cuuint32_t xbox[3] = {32, R_COLS, 1};
+    g.use = encode_tiled(&g.d, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, D, ddim, dstr, dbox,
+                         CU_TENSOR_MAP_SWIZZLE_NONE) &&
+            encode_tiled(&g.x, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, X, xdim, xstr, xbox,
+                         CU_TENSOR_MAP_SWIZZLE_NONE) &&
+            encode_tiled(&g.y, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, Y, xdim, xstr, xbox,
+                         CU_TENSOR_MAP_SWIZZLE_NONE);
+    return g;
 }
 
 // max(x) over count floats: per-block maxima (grid-stride, 16 B loads), then
@@ -826,9 +904,10 @@ static int loss_fused_impl(const float* pred, const float* ref, int m, int n, in
         } else {
             SPLATCT_CK(cudaMemsetAsync(sums + 1, 0, sizeof(double), s));
         }
+        const GradMaps gm = grad_maps(pred, ref, D11, m, n, p, L.vr, L.vc);
         SPLATCT_CK(launch_pdl(k_loss_grad11, gg, dim3(R_NT), 0, s, pred, ref, m, n, p, W, L.vr,
                               L.vc, D11, lambda1, l1_count, lambda2, ssim_slices, grad_pred, pl,
-                              halt));
+                              gm, halt));
         SPLATCT_LAUNCH_CK();
         return defer ? SPLATCT_OK : reduce_sum_f64(pl, L.nb_g11, sums, s);
     }
