@@ -357,6 +357,14 @@ constexpr int S_SLOTS = (S_CHUNKS + R_NT - 1) / R_NT;      // chunks per thread
 //         per-window statistics of the measured sinogram computed once per
 //         run (MODE 2), so the per-iteration pass carries three fields.
 // MODE 2: writes RS = {mean_y, E[y^2]} per valid window (X unused).
+// Tensor maps of the stats kernel's row loads (use = 0: cp.async path).
+struct StatMaps {
+    CUtensorMap x, y, rs;   // X, Y [m][n][p] box {32, R_SPAN, 1}; RS [2][vr][vc][p] f64 box {32, R_COLS, 1, 2}
+    int use;
+};
+constexpr unsigned S_ROWBYTES = R_SPAN * 32 * 4;       // one x or y box
+constexpr unsigned S_RSBYTES = 2 * R_COLS * 32 * 8;    // one RS box
+
 template <int MODE>
 __global__ void __launch_bounds__(R_NT, MODE == 1 ? 2 : 1) k_ssim_stats11(const float* __restrict__ X,
                                                           const float* __restrict__ Y, int m, int n,
@@ -364,20 +372,33 @@ __global__ void __launch_bounds__(R_NT, MODE == 1 ? 2 : 1) k_ssim_stats11(const 
                                                           int vr, int vc, float* __restrict__ D,
                                                           double* __restrict__ part,
                                                           double* __restrict__ RS,
+                                                          const __grid_constant__ StatMaps tm,
                                                           const int* halt) {
     griddep_wait();
     if (halted(halt)) return;
     constexpr int NF = MODE == 0 ? 5 : (MODE == 1 ? 3 : 2);   // ring fields
-    // cp.async landing ring (f32), read in place: one slot more than the
-    // staging depth, so a row is rewritten only after every warp has passed
-    // the barrier that follows its last read
+    // landing ring (f32), read in place: one slot more than the staging depth,
+    // so a row is rewritten only after every warp has passed the barrier that
+    // follows its last read
     constexpr int S_BUF = R_BUF + 1;
-    __shared__ __align__(16) float sf[S_BUF][2][R_SPAN][32];
-    // MODE 1: the reference window moments of an output row, staged by cp.async
-    // with the input rows (4 slots: a slot is rewritten two barriers after its read)
+    __shared__ __align__(128) float sf[S_BUF][2][R_SPAN][32];
+    // MODE 1: the reference window moments of an output row, staged with the
+    // input rows (4 slots: a slot is rewritten two barriers after its read)
     constexpr int RS_BUF = R_AHEAD + 2;
-    __shared__ __align__(16) double srs[MODE == 1 ? RS_BUF : 1][2][MODE == 1 ? R_COLS : 1][32];
+    static_assert(RS_BUF == S_BUF, "one mbarrier per slot covers both rings");
+    __shared__ __align__(128) double srs[MODE == 1 ? RS_BUF : 1][2][MODE == 1 ? R_COLS : 1][32];
     __shared__ double red[R_NT / 32];
+    // TMA path: thread 0 loads a row's boxes (x, y, and in MODE 1 the reference
+    // moments of output row v - 10) behind the slot's mbarrier; the tensor
+    // maps zero-fill columns and slices outside the sinogram
+    __shared__ __align__(8) uint64_t sbar[S_BUF];
+    if (tm.use) {
+        if (threadIdx.x == 0) {
+            for (int b = 0; b < S_BUF; ++b) tc::mbar_init(&sbar[b], 1);
+            tc::mbar_init_fence();
+        }
+        __syncthreads();
+    }
     const int lane = threadIdx.x & 31, cl = threadIdx.x >> 5;
     const int zb = blockIdx.x * 32, j0 = blockIdx.y * R_COLS;
     const int z = zb + lane, j = j0 + cl;
@@ -405,7 +426,37 @@ __global__ void __launch_bounds__(R_NT, MODE == 1 ? 2 : 1) k_ssim_stats11(const 
     const int rs_f = threadIdx.x / (R_COLS * 16), rs_c = (threadIdx.x / 16) % R_COLS,
               rs_q = threadIdx.x % 16;
     const bool rs_ok = MODE == 1 && rs_f < 2 && j0 + rs_c < vc && zb + 2 * rs_q < p;
+    auto issue_tma = [&](int v) {   // thread 0
+        if (v >= m) return;
+        const int slot = v % S_BUF, u = v - 10;
+        const bool rs = MODE == 1 && u >= 0 && u < vr;
+        const unsigned bar = tc::smem_u32(&sbar[slot]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar),
+                     "r"((MODE == 2 ? 1u : 2u) * S_ROWBYTES + (rs ? S_RSBYTES : 0u))
+                     : "memory");
+        if (MODE != 2)
+            asm volatile(
+                "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
+                "[%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(tc::smem_u32(&sf[slot][0][0][0])),
+                "l"(&tm.x), "r"(zb), "r"(j0), "r"(v), "r"(bar)
+                : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
+            "[%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(tc::smem_u32(&sf[slot][1][0][0])),
+            "l"(&tm.y), "r"(zb), "r"(j0), "r"(v), "r"(bar)
+            : "memory");
+        if (rs)
+            asm volatile(
+                "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes "
+                "[%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(tc::smem_u32(&srs[slot][0][0][0])),
+                "l"(&tm.rs), "r"(zb), "r"(j0), "r"(u), "r"(0), "r"(bar)
+                : "memory");
+    };
     auto issue = [&](int v) {
+        if (tm.use) {
+            if (threadIdx.x == 0) issue_tma(v);
+            return;
+        }
         if (MODE == 1) {   // reference moments of output row v - 10 (needed at iteration v)
             const int u = v - 10;
             if (u >= 0 && u < vr && rs_f < 2) {
@@ -437,7 +488,10 @@ __global__ void __launch_bounds__(R_NT, MODE == 1 ? 2 : 1) k_ssim_stats11(const 
         for (int ph = 0; ph < 11; ++ph) {
             const int v = v0 + ph;
             if (v >= m) break;
-            cp_wait_group<R_AHEAD - 1>();   // my chunks of row v landed (later rows in flight)
+            if (tm.use)
+                tc::mbar_wait(&sbar[v % S_BUF], (uint32_t)(v / S_BUF) & 1u);   // row v landed
+            else
+                cp_wait_group<R_AHEAD - 1>();   // my chunks of row v landed (later rows in flight)
             issue(v + R_AHEAD);   // slot (v+2) % 4: last read at row v-2, before the previous barrier
             __syncthreads();      // row v complete in shared memory
             // MODE 1: the reference window moments of output row v-10, loaded
@@ -508,7 +562,7 @@ __global__ void __launch_bounds__(R_NT, MODE == 1 ? 2 : 1) k_ssim_stats11(const 
             }
         }
     }
-    cp_wait_group<0>();
+    if (!tm.use) cp_wait_group<0>();
     if (MODE != 2) {
         const double r = block_sum<R_NT>(ssum, red);
         if (threadIdx.x == 0) part[blockIdx.y * gridDim.x + blockIdx.x] = r;
@@ -697,6 +751,30 @@ __global__ void __launch_bounds__(R_NT, 2) k_loss_grad11(const float* __restrict
     if (!tm.use) cp_wait_group<0>();   // TMA: rows >= m are never issued, all issued were waited
     const double rr = block_sum<R_NT>(l1sum, red);
     if (threadIdx.x == 0) part[blockIdx.y * gridDim.x + blockIdx.x] = rr;
+}
+
+// Tensor maps for k_ssim_stats11 (X may be null in MODE 2; RS only in MODE 1).
+static StatMaps stat_maps(const float* X, const float* Y, const double* RS, int m, int n, int p,
+                          int vr, int vc) {
+    StatMaps g;
+    memset(&g, 0, sizeof(g));
+    const cuuint64_t fp = (cuuint64_t)p * 4;
+    const cuuint64_t xdim[3] = {(cuuint64_t)p, (cuuint64_t)n, (cuuint64_t)m};
+    const cuuint64_t xstr[2] = {fp, fp * n};
+    const cuuint32_t xbox[3] = {32, R_SPAN, 1};
+    const cuuint64_t rdim[4] = {(cuuint64_t)p, (cuuint64_t)vc, (cuuint64_t)vr, 2};
+    const cuuint64_t rstr[3] = {2 * fp, 2 * fp * vc, 2 * fp * vc * vr};
+    const cuuint32_t rbox[4] = {32, R_COLS, 1, 2};
+    bool ok = encode_tiled(&g.y, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, Y, xdim, xstr, xbox,
+                           CU_TENSOR_MAP_SWIZZLE_NONE);
+    if (ok && X)
+        ok = encode_tiled(&g.x, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, X, xdim, xstr, xbox,
+                          CU_TENSOR_MAP_SWIZZLE_NONE);
+    if (ok && RS)
+        ok = encode_tiled(&g.rs, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, RS, rdim, rstr, rbox,
+                          CU_TENSOR_MAP_SWIZZLE_NONE);
+    g.use = ok;
+    return g;
 }
 
 // Tensor maps for k_loss_grad11 (p % 4 == 0 and 16-byte aligned bases: the
@@ -894,10 +972,14 @@ static int loss_fused_impl(const float* pred, const float* ref, int m, int n, in
             double* RS = reinterpret_cast<double*>(base + L.o_RS);
             if (prepared)
                 SPLATCT_CK(launch_pdl(k_ssim_stats11<1>, gs, dim3(R_NT), 0, s, pred, ref, m, n, p,
-                                      W, c1, c2, L.vr, L.vc, D11, ps, RS, halt));
+                                      W, c1, c2, L.vr, L.vc, D11, ps, RS,
+                                      stat_maps(pred, ref, RS, m, n, p, L.vr, L.vc), halt));
             else
                 k_ssim_stats11<0><<<gs, R_NT, 0, s>>>(pred, ref, m, n, p, W, c1, c2, L.vr, L.vc,
-                                                      D11, ps, RS, halt);
+                                                      D11, ps, RS,
+                                                      stat_maps(pred, ref, nullptr, m, n, p,
+                                                                L.vr, L.vc),
+                                                      halt);
             SPLATCT_LAUNCH_CK();
             if (!defer)
                 if (int e = reduce_sum_f64(ps, L.nb_s11, sums + 1, s)) return e;
@@ -1012,7 +1094,8 @@ int splatct_loss_prepare_ref(const float* ref, int m, int n, int p, void* ws, si
     const dim3 gs((p + 31) / 32, (L.vc + R_COLS - 1) / R_COLS);
     k_ssim_stats11<2><<<gs, R_NT, 0, as_stream(stream)>>>(
         nullptr, ref, m, n, p, W, 0.0, 0.0, L.vr, L.vc, nullptr, nullptr,
-        reinterpret_cast<double*>(base + L.o_RS), nullptr);
+        reinterpret_cast<double*>(base + L.o_RS),
+        stat_maps(nullptr, ref, nullptr, m, n, p, L.vr, L.vc), nullptr);
     SPLATCT_LAUNCH_CK();
     return SPLATCT_OK;
 }
