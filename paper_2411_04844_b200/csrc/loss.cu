@@ -391,10 +391,16 @@ __global__ void __launch_bounds__(R_NT, MODE == 1 ? 2 : 1) k_ssim_stats11(const 
     // TMA path: thread 0 loads a row's boxes (x, y, and in MODE 1 the reference
     // moments of output row v - 10) behind the slot's mbarrier; the tensor
     // maps zero-fill columns and slices outside the sinogram
-    __shared__ __align__(8) uint64_t sbar[S_BUF];
+    // ("full", count 1 + bytes) and released by every warp ("empty", count
+    // R_COLS) once it has read the slot, so warps never meet at a block
+    // barrier: thread 0 re-issues a slot only after all warps released it
+    __shared__ __align__(8) uint64_t sbar[S_BUF], ebar[S_BUF];
     if (tm.use) {
         if (threadIdx.x == 0) {
-            for (int b = 0; b < S_BUF; ++b) tc::mbar_init(&sbar[b], 1);
+            for (int b = 0; b < S_BUF; ++b) {
+                tc::mbar_init(&sbar[b], 1);
+                tc::mbar_init(&ebar[b], R_COLS);
+            }
             tc::mbar_init_fence();
         }
         __syncthreads();
@@ -488,12 +494,19 @@ __global__ void __launch_bounds__(R_NT, MODE == 1 ? 2 : 1) k_ssim_stats11(const 
         for (int ph = 0; ph < 11; ++ph) {
             const int v = v0 + ph;
             if (v >= m) break;
-            if (tm.use)
+            if (tm.use) {
                 tc::mbar_wait(&sbar[v % S_BUF], (uint32_t)(v / S_BUF) & 1u);   // row v landed
-            else
+                const int w = v + R_AHEAD;   // next row to stage: its slot held row w - 4
+                if (threadIdx.x == 0 && w < m) {
+                    if (w >= S_BUF)
+                        tc::mbar_wait(&ebar[w % S_BUF], (uint32_t)(w / S_BUF - 1) & 1u);
+                    issue_tma(w);
+                }
+            } else {
                 cp_wait_group<R_AHEAD - 1>();   // my chunks of row v landed (later rows in flight)
-            issue(v + R_AHEAD);   // slot (v+2) % 4: last read at row v-2, before the previous barrier
-            __syncthreads();      // row v complete in shared memory
+                issue(v + R_AHEAD);   // slot (v+2) % 4: last read at row v-2, before the previous barrier
+                __syncthreads();      // row v complete in shared memory
+            }
             // MODE 1: the reference window moments of output row v-10, loaded
             // before the row's arithmetic so their latency overlaps it
             double rs_my = 0.0, rs_y2 = 0.0;
@@ -529,6 +542,10 @@ __global__ void __launch_bounds__(R_NT, MODE == 1 ? 2 : 1) k_ssim_stats11(const 
             }
 #pragma unroll
             for (int f = 0; f < NF; ++f) ring[ph][f] = h[0][f] + h[1][f];
+            if (tm.use) {   // this warp is done with slot v % 4 (rows and moments)
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&ebar[v % S_BUF]);
+            }
             if (v >= 10 && act) {
                 double a[2][NF];
 #pragma unroll
