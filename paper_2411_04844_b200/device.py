@@ -53,16 +53,29 @@ def require_cuda(device=None) -> torch.device:
 # ---------------------------------------------------------------------------
 
 def cloud_to_params(cloud: GaussianCloud, device) -> torch.Tensor:
-    p = np.empty((5, cloud.n), np.float64)
-    p[0:3] = cloud.mu.T
-    p[3] = cloud.sigma
-    p[4] = cloud.intensity
-    return torch.from_numpy(p).to(device)
+    """Host cloud -> the device's f64 [5, N] block.  The (N, 3) -> (3, N)
+    transpose runs on the device: on the host it is a strided copy (~0.4 ms
+    at 50 k Gaussians), the packed upload is three contiguous copies."""
+    n = cloud.n
+    st = _pinned(5 * n, torch.float64)   # packed in page-locked memory: one DMA
+    h = st.numpy()
+    h[: 3 * n] = cloud.mu.reshape(-1)
+    h[3 * n: 4 * n] = cloud.sigma
+    h[4 * n:] = cloud.intensity
+    d = st.to(device, non_blocking=False)
+    p = torch.empty((5, n), dtype=torch.float64, device=d.device)
+    p[0:3].copy_(d[: 3 * n].view(n, 3).t())
+    p[3:5].copy_(d[3 * n:].view(2, n))
+    return p
 
 
 def params_to_cloud(params: torch.Tensor) -> GaussianCloud:
-    p = to_host(params.detach())
-    return GaussianCloud(np.ascontiguousarray(p[0:3].T), p[3].copy(), p[4].copy())
+    """The inverse: transposed on the device, one download, host views."""
+    p = params.detach()
+    n = int(p.shape[1])
+    packed = torch.cat([p[0:3].t().reshape(-1), p[3], p[4]])
+    h = to_host(packed)
+    return GaussianCloud(h[: 3 * n].reshape(n, 3), h[3 * n: 4 * n], h[4 * n:])
 
 
 def _host_f32(arr) -> torch.Tensor:
