@@ -50,9 +50,13 @@ def main():
         optim.run_reconstruction(meas, geom, st, init_cloud=cloud)
         torch.cuda.synchronize()
         print(f"plain run {rep}: {1e3 * (time.perf_counter() - t0):.1f} ms")
-    for name in ("sino_to_device", "cloud_to_params", "yxz_to_zyx", "params_to_cloud"):
+    for name in ("cloud_to_params", "params_to_cloud", "to_pinned_host", "pinned_output"):
         wrap(D, name)
     wrap(optim, "_trainer_for")
+    from paper_2411_04844_b200.trainer import Trainer
+    wrap(D.StagedHost, "to")
+    for name in ("initial_volume", "step", "trace_rows"):
+        wrap(Trainer, name)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     optim.run_reconstruction(meas, geom, st, init_cloud=cloud)
