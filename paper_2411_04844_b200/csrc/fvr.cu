@@ -737,6 +737,12 @@ __global__ void __launch_bounds__(256, 4) k_fvr_fwd(const GRec* __restrict__ rec
     }   // tile
     }   // fetch
     if (use_tma && threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+    // every CTA has made its last claim once it gets here: the last one to
+    // exit resets the claim counter (and the exit ticket) for the next forward
+    if (threadIdx.x == 0 && atomicAdd(&counter[2], 1u) == gridDim.x - 1) {
+        counter[0] = 0u;
+        counter[2] = 0u;
+    }
 }
 
 // --------------------------------------------------------------------------
@@ -1356,13 +1362,24 @@ __global__ void __launch_bounds__(256) k_fvr_fwd_plain(const GRec* __restrict__ 
 // boundaries: sorted position j starts every tile in (key[j-1], key[j]], and
 // tstart[nt] = number of pairs (read on the device: the bins are dense).
 // One coalesced pass; each tile start is written exactly once.
+// It also readies the forward that follows the bins: the tile-claim counter
+// and its exit ticket (fcounter[0], [2]) are zeroed, and so are the two
+// empty-space masks (mask_words u64; the masked forward ORs into them), which
+// would otherwise each take a memset node between the bins and the forward.
 __global__ void k_tile_starts(const uint32_t* __restrict__ skeys,
                               const uint32_t* __restrict__ npairs, int64_t nt, int ybits,
-                              uint32_t* __restrict__ tstart, const int* halt) {
+                              uint32_t* __restrict__ tstart, unsigned int* __restrict__ fcounter,
+                              unsigned long long* __restrict__ masks, int64_t mask_words,
+                              const int* halt) {
     griddep_wait();
     if (halted(halt)) return;
     const int64_t np = npairs ? (int64_t)*npairs : 0;
     const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j == 0) {
+        fcounter[0] = 0u;
+        fcounter[2] = 0u;
+    }
+    for (int64_t k = j; k < mask_words; k += (int64_t)gridDim.x * blockDim.x) masks[k] = 0ull;
     if (j > np) return;
     const int64_t prev = j == 0 ? -1 : (int64_t)(skeys[j - 1] >> ybits);
     const int64_t cur = j == np ? nt : (int64_t)(skeys[j] >> ybits);
@@ -2675,10 +2692,14 @@ static int fvr_bin_impl(const double* params, int64_t n, int w, int h, int c, in
     {   // tile offsets from the sorted keys: no atomics
         const size_t ko = L.final_buf ? L.o_k1 : L.o_k0;
         const int64_t npk = n > 0 ? L.np : 0;
+        // both masks: pocc .. the end of fcov (each w*h u64)
+        const int64_t mwords =
+            L.ntz <= 64 ? (int64_t)((L.o_fcov - L.o_pocc) / 8) + (int64_t)w * h : 0;
         SPLATCT_CK(launch_pdl(k_tile_starts, dim3((unsigned)((npk + 1 + 255) / 256)), dim3(256),
                               0, s, n > 0 ? at<uint32_t>(ws, ko) : nullptr,
                               n > 0 ? npairs : nullptr, L.nt, ybits,
-                              at<uint32_t>(ws, L.o_tstart), halt));
+                              at<uint32_t>(ws, L.o_tstart), at<uint32_t>(ws, L.o_tcount),
+                              at<unsigned long long>(ws, L.o_pocc), mwords, halt));
         SPLATCT_LAUNCH_CK();
     }
     return SPLATCT_OK;
@@ -2720,16 +2741,19 @@ static int fvr_forward_impl(const double* params, int64_t n, int w, int h, int c
     const int64_t grid = L.nt < 148 * 4 ? L.nt : 148 * 4;   // persistent: 4 CTAs/SM resident
     int64_t fetch = L.nt / (8 * grid);                       // >= 8 claims per CTA
     fetch = fetch < 1 ? 1 : (fetch > 32 ? 32 : fetch);
+    // the bins zeroed the tile counter and the masks; the default kernel
+    // leaves its counter at zero again, so repeated forwards need no memset
     unsigned int* counter = at<uint32_t>(ws, L.o_tcount);
-    SPLATCT_CK(cudaMemsetAsync(counter, 0, sizeof(unsigned int), as_stream(stream)));
-    if (masks && L.ntz <= 64)
+    const char* kern = getenv("SPLATCT_FWD_KERNEL");   // "mma" / "ff": the other kernels
+    const bool tc_path = kern && !strcmp(kern, "tc") && L.nt <= (int64_t)148 * TC_LIST_CAP;
+    const bool ff_path = kern && !strcmp(kern, "ff");
+    if ((tc_path || ff_path) && masks && L.ntz <= 64)   // they may follow another forward
         SPLATCT_CK(cudaMemsetAsync(at<char>(ws, L.o_pocc), 0,
                                    L.o_fcov + sizeof(unsigned long long) * (size_t)w * h - L.o_pocc,
                                    as_stream(stream)));
-    const char* kern = getenv("SPLATCT_FWD_KERNEL");   // "mma" / "ff": the other kernels
     // (the tensor-core kernel keeps each CTA's tile list in shared memory:
     // volumes beyond 148 x 7680 tiles of 16^3 take the mma.sync kernel)
-    if (kern && !strcmp(kern, "tc") && L.nt <= (int64_t)148 * TC_LIST_CAP) {
+    if (tc_path) {
         int dev = 0, nsm = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -2751,7 +2775,7 @@ static int fvr_forward_impl(const double* params, int64_t n, int w, int h, int c
         SPLATCT_LAUNCH_CK();
         return SPLATCT_OK;
     }
-    if (kern && !strcmp(kern, "ff")) {
+    if (ff_path) {
         int dev = 0, nsm = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -2766,9 +2790,11 @@ static int fvr_forward_impl(const double* params, int64_t n, int w, int h, int c
                               counter, (int)f2, at<unsigned long long>(ws, L.o_pocc),
                               at<unsigned long long>(ws, L.o_fcov), halt);
         };
+        SPLATCT_CK(cudaMemsetAsync(counter, 0, sizeof(unsigned int), as_stream(stream)));
         if (masks) SPLATCT_CK(go(std::true_type{}));
         else SPLATCT_CK(go(std::false_type{}));
         SPLATCT_LAUNCH_CK();
+        SPLATCT_CK(cudaMemsetAsync(counter, 0, sizeof(unsigned int), as_stream(stream)));
         return SPLATCT_OK;
     }
     CUtensorMap tmap;

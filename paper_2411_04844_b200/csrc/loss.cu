@@ -869,7 +869,9 @@ __global__ void __launch_bounds__(256) k_sq_diff(const float* __restrict__ x,
 struct FinParts {
     const double* p[3];   // l1, ssim, tv partials (or null: sums[f] is final)
     int64_t n[3];
+    double* scratch;      // FIN_BLOCKS x 3 block sums, then a ticket word (zero between calls)
 };
+constexpr int FIN_BLOCKS = 32, FIN_NT = 256;
 
 __global__ void k_iter_finalize(double* __restrict__ sums, FinParts parts, double l1w,
                                 double ssw, double tvw, double l1_count, double ssim_count,
@@ -878,14 +880,50 @@ __global__ void k_iter_finalize(double* __restrict__ sums, FinParts parts, doubl
                                 double* adam, int* halt) {
     griddep_wait();
     if (*halt) return;
-    __shared__ double sh[32];
+    if (parts.scratch != nullptr) {
+        // FIN_BLOCKS blocks each sum a fixed slice of every partial array, the
+        // last block to finish combines the block sums in block order
+        // (deterministic whichever block is last) and does the bookkeeping
+        __shared__ double sh[FIN_NT / 32];
+        __shared__ bool last;
 #pragma unroll
-    for (int f = 0; f < 3; ++f) {
-        if (parts.p[f] == nullptr) continue;   // uniform
-        const double r = block_reduce_f64(parts.p[f], parts.n[f], sh);
-        if (threadIdx.x == 0) sums[f] = r;
+        for (int f = 0; f < 3; ++f) {
+            if (parts.p[f] == nullptr) continue;   // uniform
+            const int64_t per = (parts.n[f] + FIN_BLOCKS - 1) / FIN_BLOCKS;
+            const int64_t lo = blockIdx.x * per, hi = min(parts.n[f], lo + per);
+            double a0 = 0.0, a1 = 0.0;
+            int64_t i = lo + threadIdx.x;
+            for (; i + FIN_NT < hi; i += 2 * FIN_NT) {
+                a0 += parts.p[f][i];
+                a1 += parts.p[f][i + FIN_NT];
+            }
+            if (i < hi) a0 += parts.p[f][i];
+            const double r = block_sum<FIN_NT>(a0 + a1, sh);
+            if (threadIdx.x == 0) parts.scratch[f * FIN_BLOCKS + blockIdx.x] = r;
+        }
+        if (threadIdx.x == 0) {
+            __threadfence();
+            unsigned* ticket = reinterpret_cast<unsigned*>(parts.scratch + 3 * FIN_BLOCKS);
+            last = atomicAdd(ticket, 1u) == FIN_BLOCKS - 1;
+        }
+        __syncthreads();
+        if (!last) return;
+        __threadfence();
+        __shared__ double bs[3 * FIN_BLOCKS];   // the block sums, loaded in parallel
+        if (threadIdx.x < 3 * FIN_BLOCKS)
+            bs[threadIdx.x] = reinterpret_cast<volatile double*>(parts.scratch)[threadIdx.x];
+        __syncthreads();
+        if (threadIdx.x != 0) return;
+        for (int f = 0; f < 3; ++f) {
+            if (parts.p[f] == nullptr) continue;
+            double t = 0.0;
+            for (int b = 0; b < FIN_BLOCKS; ++b) t += bs[f * FIN_BLOCKS + b];
+            sums[f] = t;
+        }
+        *reinterpret_cast<unsigned*>(parts.scratch + 3 * FIN_BLOCKS) = 0u;   // next call
+    } else if (threadIdx.x != 0) {
+        return;
     }
-    if (threadIdx.x != 0) return;
     const double nan = __longlong_as_double(0x7ff8000000000000LL);
     const double l1 = l1w > 0 ? sums[0] / l1_count : nan;
     const double ss = ssw > 0 ? 1.0 - sums[1] / ssim_count : nan;
@@ -1149,7 +1187,7 @@ int splatct_iter_finalize(const double* sums, double lambda1, double lambda2, do
                           double lrf, int64_t max_iters, int64_t* step, int64_t* iter,
                           double* trace, int64_t trace_cap, double* adam, int* halt,
                           void* stream) {
-    const FinParts none{{nullptr, nullptr, nullptr}, {0, 0, 0}};
+    const FinParts none{{nullptr, nullptr, nullptr}, {0, 0, 0}, nullptr};
     SPLATCT_CK(launch_pdl(k_iter_finalize, dim3(1), dim3(1), 0, as_stream(stream),
                           const_cast<double*>(sums), none, lambda1, lambda2, lambda3, l1_count,
                           ssim_count, tv_count, lr0, lrf, max_iters, step, iter, trace, trace_cap,
@@ -1160,16 +1198,18 @@ int splatct_iter_finalize(const double* sums, double lambda1, double lambda2, do
 
 int splatct_iter_finalize_partials(double* sums, const double* l1_part, int64_t n_l1,
                                    const double* ssim_part, int64_t n_ssim,
-                                   const double* tv_part, int64_t n_tv, double lambda1,
-                                   double lambda2, double lambda3, double l1_count,
-                                   double ssim_count, double tv_count, double lr0, double lrf,
-                                   int64_t max_iters, int64_t* step, int64_t* iter,
-                                   double* trace, int64_t trace_cap, double* adam, int* halt,
-                                   void* stream) {
+                                   const double* tv_part, int64_t n_tv, double* scratch,
+                                   double lambda1, double lambda2, double lambda3,
+                                   double l1_count, double ssim_count, double tv_count,
+                                   double lr0, double lrf, int64_t max_iters, int64_t* step,
+                                   int64_t* iter, double* trace, int64_t trace_cap, double* adam,
+                                   int* halt, void* stream) {
+    SPLATCT_REQUIRE(scratch != nullptr, "finalize scratch required");
     const FinParts parts{{n_l1 > 0 ? l1_part : nullptr, n_ssim > 0 ? ssim_part : nullptr,
                           n_tv > 0 ? tv_part : nullptr},
-                         {n_l1, n_ssim, n_tv}};
-    SPLATCT_CK(launch_pdl(k_iter_finalize, dim3(1), dim3(1024), 0, as_stream(stream), sums,
+                         {n_l1, n_ssim, n_tv},
+                         scratch};
+    SPLATCT_CK(launch_pdl(k_iter_finalize, dim3(FIN_BLOCKS), dim3(FIN_NT), 0, as_stream(stream), sums,
                           parts, lambda1, lambda2, lambda3, l1_count, ssim_count, tv_count, lr0,
                           lrf, max_iters, step, iter, trace, trace_cap, adam, halt));
     SPLATCT_LAUNCH_CK();

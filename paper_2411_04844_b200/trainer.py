@@ -125,6 +125,7 @@ class Trainer:
         self.tv_part = torch.zeros(D.tv_partial_len(self.w, self.h, cl), dtype=torch.float64,
                                    device=dev)
         self.sums = torch.zeros(3, dtype=torch.float64, device=dev)
+        self.fin_scratch = torch.zeros(97, dtype=torch.float64, device=dev)   # SPLATCT_FIN_SCRATCH_DOUBLES
         self.adam_s = torch.zeros(3, dtype=torch.float64, device=dev)
         self.step_t = torch.tensor([int(step)], dtype=torch.int64, device=dev)
         self.iter_t = torch.zeros(1, dtype=torch.int64, device=dev)
@@ -283,7 +284,7 @@ class Trainer:
                                   else (D.VP(0), 0, D.VP(0), 0))
             tvn = D.tv_partial_len(self.w, self.h, self.slab.c_local, blocked=True)
             parts = (l1p, nl1, ssp, nss, D.ptr(self.tv_part) if defer_tv else D.VP(0),
-                     tvn if defer_tv else 0)
+                     tvn if defer_tv else 0, D.ptr(self.fin_scratch))
 
         def finalize_backward():
             scal = (float(lw.lambda1), float(lw.lambda2), float(lw.lambda3), self.l1_count,
