@@ -79,6 +79,14 @@ int splatct_fvr_bin(const double* params, int64_t n, int w, int h, int c, int z0
 int splatct_fvr_bin_row_ordered(const double* params, int64_t n, int w, int h, int c, int z0,
                                 int hx, int hy, int hz, void* ws, size_t ws_bytes,
                                 const int* halt, void* stream);
+/* splatct_adam (params, m1, m2 updated in place with the scalars adam =
+ * {lr, 1-b1^t, 1-b2^t}, sigma clamped, intensity >= 0) followed by the bins of
+ * the updated params (row-ordered when row_ordered != 0), in one pass: each
+ * thread updates its own Gaussian and bins it.  The training step's form. */
+int splatct_fvr_adam_bin(double* params, const double* grads, double* m1, double* m2,
+                         const double* adam, double sigma_floor, double sigma_ceiling, int64_t n,
+                         int w, int h, int c, int z0, int hx, int hy, int hz, void* ws,
+                         size_t ws_bytes, int row_ordered, const int* halt, void* stream);
 
 /* V = sum_i I_i ex_i (x) ey_i (x) ez_i over box intersect volume; one CTA per
  * tile accumulating in registers/shared memory, each voxel written once

@@ -32,6 +32,8 @@ SIGNATURES: dict[str, list] = {
                         c_vp, c_vp],
     "splatct_fvr_bin_row_ordered": [c_vp, c_i64, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32,
                                     c_vp, c_sz, c_vp, c_vp],
+    "splatct_fvr_adam_bin": [c_vp, c_vp, c_vp, c_vp, c_vp, c_f64, c_f64, c_i64, c_i32, c_i32,
+                             c_i32, c_i32, c_i32, c_i32, c_i32, c_vp, c_sz, c_i32, c_vp, c_vp],
     "splatct_fvr_forward": [c_vp, c_i64, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_vp,
                             c_sz, c_vp, c_vp, c_vp],
     "splatct_fvr_forward_masked": [c_vp, c_i64, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_vp,

@@ -83,6 +83,24 @@ __device__ __forceinline__ float warp_sum(float v) {
     return v;
 }
 
+// One Adam step of parameter element idx (row = idx / n: 3 = sigma, clamped to
+// [sfloor, sceil]; 4 = intensity, >= 0), optim.py:109-144; shared by k_adam and
+// the Adam-fused binning pass so both compute it identically.
+__device__ __forceinline__ void adam_elem(double* __restrict__ P, const double* __restrict__ G,
+                                          double* __restrict__ M1, double* __restrict__ M2,
+                                          int64_t idx, int row, double lr, double bc1, double bc2,
+                                          double sfloor, double sceil) {
+    const double g = G[idx];
+    const double m = 0.9 * M1[idx] + (1.0 - 0.9) * g;
+    const double v = 0.999 * M2[idx] + (1.0 - 0.999) * g * g;
+    double p = P[idx] - lr * (m / bc1) / (sqrt(v / bc2) + 1e-8);
+    if (row == 3) p = fmin(fmax(p, sfloor), sceil);
+    if (row == 4) p = fmax(p, 0.0);
+    M1[idx] = m;
+    M2[idx] = v;
+    P[idx] = p;
+}
+
 // Block-wide sum of a double into lane 0 of warp 0 (deterministic order).
 template <int NT>
 __device__ __forceinline__ double block_sum(double v, double* sh /* >= NT/32 */) {

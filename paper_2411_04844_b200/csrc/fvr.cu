@@ -202,12 +202,23 @@ __device__ __forceinline__ unsigned long long lookback_warp(unsigned long long* 
 // Gaussian order and (tz, ty, tx) slot order -- the value encodes
 // Gaussian << Sl | slot.  The kernel also counts every sort pass's digits
 // (global histograms), so each sort pass is a single kernel.
+// Optional Adam step fused ahead of the binning (G null: none): each thread
+// first updates its own Gaussian's five parameters and moments (adam_elem,
+// bitwise k_adam's), then bins the updated Gaussian -- one pass and one
+// launch fewer per training step.
+struct AdamFuse {
+    const double* G;
+    double *M1, *M2;
+    const double* s;   // {lr, 1 - b1^t, 1 - b2^t} from the iteration finalize
+    double sfloor, sceil;
+};
+
 __global__ void __launch_bounds__(BIN_NT) k_bin_emit(
     const double* __restrict__ P, int64_t n, int w, int h, int c, int zoff, int hx, int hy,
     int hz, int ntx, int nty, int Sl, int passes, int ybits, int32_t* __restrict__ fp,
     GRec* __restrict__ rec, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
     uint32_t* __restrict__ ghist, unsigned long long* __restrict__ status,
-    uint32_t* __restrict__ tickets, const int* halt) {
+    uint32_t* __restrict__ tickets, AdamFuse af, const int* halt) {
     griddep_wait();
     if (halted(halt)) return;
     __shared__ unsigned s_blk;
@@ -224,6 +235,13 @@ __global__ void __launch_bounds__(BIN_NT) k_bin_emit(
     __syncthreads();
     const int64_t blk = s_blk;
     const int64_t i = blk * BIN_NT + t;
+    if (af.G != nullptr && i < n) {   // P is read back below by this thread only
+        const double lr = af.s[0], bc1 = af.s[1], bc2 = af.s[2];
+#pragma unroll
+        for (int f = 0; f < 5; ++f)
+            adam_elem(const_cast<double*>(P), af.G, af.M1, af.M2, f * n + i, f, lr, bc1, bc2,
+                      af.sfloor, af.sceil);
+    }
     uint32_t cnt = 0;
     int4 ti = make_int4(0, 0, 0, 1 | (1 << 16));
     int ylo0 = 0;
@@ -2657,7 +2675,7 @@ int splatct_fvr_workspace_bytes(int64_t n, int w, int h, int c, int hx, int hy, 
 
 static int fvr_bin_impl(const double* params, int64_t n, int w, int h, int c, int z0, int hx,
                         int hy, int hz, void* ws, size_t ws_bytes, const int* halt, void* stream,
-                        bool row_order) {
+                        bool row_order, AdamFuse af = AdamFuse{nullptr, nullptr, nullptr, nullptr, 0.0, 0.0}) {
     FvrLayout L = make_layout(n, w, h, c, hx, hy, hz);
     if (int e = check_args(n, w, h, c, hx, hy, hz, ws_bytes, L)) return e;
     // row order uses the key bits the radix passes sort anyway (no extra pass),
@@ -2675,7 +2693,7 @@ static int fvr_bin_impl(const double* params, int64_t n, int w, int h, int c, in
                               ybits, at<int32_t>(ws, L.o_fp), at<GRec>(ws, L.o_rec),
                               at<uint32_t>(ws, L.o_k0), at<uint32_t>(ws, L.o_v0),
                               at<uint32_t>(ws, L.o_ghist),
-                              at<unsigned long long>(ws, L.o_stat_e), tickets, halt));
+                              at<unsigned long long>(ws, L.o_stat_e), tickets, af, halt));
         SPLATCT_LAUNCH_CK();
         for (int p = 0; p < L.passes; ++p) {
             const size_t ki = p % 2 ? L.o_k1 : L.o_k0, vi = p % 2 ? L.o_v1 : L.o_v0;
@@ -2714,6 +2732,18 @@ int splatct_fvr_bin_row_ordered(const double* params, int64_t n, int w, int h, i
                                 int hx, int hy, int hz, void* ws, size_t ws_bytes,
                                 const int* halt, void* stream) {
     return fvr_bin_impl(params, n, w, h, c, z0, hx, hy, hz, ws, ws_bytes, halt, stream, true);
+}
+
+int splatct_fvr_adam_bin(double* params, const double* grads, double* m1, double* m2,
+                         const double* adam, double sigma_floor, double sigma_ceiling, int64_t n,
+                         int w, int h, int c, int z0, int hx, int hy, int hz, void* ws,
+                         size_t ws_bytes, int row_ordered, const int* halt, void* stream) {
+    SPLATCT_REQUIRE(grads && m1 && m2 && adam, "adam_bin needs grads, moments and scalars");
+    if (n == 0) return fvr_bin_impl(params, n, w, h, c, z0, hx, hy, hz, ws, ws_bytes, halt,
+                                    stream, row_ordered != 0);
+    const AdamFuse af{grads, m1, m2, adam, sigma_floor, sigma_ceiling};
+    return fvr_bin_impl(params, n, w, h, c, z0, hx, hy, hz, ws, ws_bytes, halt, stream,
+                        row_ordered != 0, af);
 }
 
 // TMA descriptor of the (h, w, c) volume for 16^3 boxes with the 64-byte

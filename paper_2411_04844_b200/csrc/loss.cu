@@ -961,17 +961,7 @@ __global__ void k_adam(double* __restrict__ P, const double* __restrict__ G,
     if (halted(halt)) return;
     const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (idx >= 5 * n) return;
-    const double lr = adam[0], bc1 = adam[1], bc2 = adam[2];
-    const double g = G[idx];
-    const double m = 0.9 * M1[idx] + (1.0 - 0.9) * g;
-    const double v = 0.999 * M2[idx] + (1.0 - 0.999) * g * g;
-    double p = P[idx] - lr * (m / bc1) / (sqrt(v / bc2) + 1e-8);
-    const int64_t row = idx / n;
-    if (row == 3) p = fmin(fmax(p, sfloor), sceil);
-    if (row == 4) p = fmax(p, 0.0);
-    M1[idx] = m;
-    M2[idx] = v;
-    P[idx] = p;
+    adam_elem(P, G, M1, M2, idx, (int)(idx / n), adam[0], adam[1], adam[2], sfloor, sceil);
 }
 
 }  // namespace splatct

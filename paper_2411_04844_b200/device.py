@@ -320,6 +320,13 @@ class FvrPlan:
 
     masks_valid = False
 
+    def adam_bin(self, params, grads, m1, m2, scalars, sigma_floor: float, sigma_ceiling: float,
+                 halt=None, row_ordered: bool = False) -> None:
+        """adam() then bin() of the updated params, in one pass (the training step)."""
+        call("splatct_fvr_adam_bin", ptr(params), ptr(grads), ptr(m1), ptr(m2), ptr(scalars),
+             float(sigma_floor), float(sigma_ceiling), *self._geo(), ptr(self.ws), self.ws_bytes,
+             int(row_ordered), ptr(halt), stream_handle())
+
     def bin(self, params: torch.Tensor, halt=None, row_ordered: bool = False) -> None:
         """row_ordered: each tile's list ordered by the Gaussians' first row
         (same pairs; the forward skips more work, its sums change order)."""

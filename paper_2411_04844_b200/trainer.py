@@ -304,9 +304,9 @@ class Trainer:
         def update_resplat():
             if sharded:
                 D.grad_norm_accum(self.grads, self.accum, halt)
-            D.adam(self.params, self.grads, self.m1, self.m2, self.adam_s, SIGMA_FLOOR,
-                   self.sigma_ceiling, halt)
-            self.fvr.bin(self.params, halt, row_ordered=ROW_ORDERED_BINS)
+            # Adam fused into the binning pass of the updated params
+            self.fvr.adam_bin(self.params, self.grads, self.m1, self.m2, self.adam_s, SIGMA_FLOOR,
+                              self.sigma_ceiling, halt, row_ordered=ROW_ORDERED_BINS)
             self.fvr.forward(self.params, self.vol, halt, masks=True)   # + empty-space masks
         st.append(("gpu", update_resplat))
         return st
