@@ -426,3 +426,32 @@ def test_row_ordered_bins_same_pairs(dims, n):
     assert reordered > 0
     assert rel_l2(vol_b, vol_a) < 1e-6
     np.testing.assert_array_equal(vol_b, vol_c)
+
+
+def test_adam_fused_into_bins_matches_separate_calls():
+    """splatct_fvr_adam_bin (the training step's fused Adam + binning pass)
+    leaves params and both moments bitwise as splatct_adam does, and bins the
+    updated params exactly as a separate bin call would."""
+    import torch
+    from paper_2411_04844_b200 import device as D, optim
+    dev = D.require_cuda()
+    dims = (64, 48, 40)
+    box = core.BoxConfig.for_dims(17, dims)
+    cloud = optim.init_cloud_random(dims, 4000, seed=6, box=box)
+    g = torch.Generator(device="cpu").manual_seed(6)
+    p0 = D.cloud_to_params(cloud, dev)
+    grads = (torch.randn(p0.shape, generator=g, dtype=torch.float64) * 0.05).to(dev)
+    m1 = (torch.randn(p0.shape, generator=g, dtype=torch.float64) * 0.01).to(dev)
+    m2 = (torch.rand(p0.shape, generator=g, dtype=torch.float64) * 0.01).to(dev)
+    scal = torch.tensor([3e-2, 0.1, 0.001], dtype=torch.float64, device=dev)
+    a = [t.clone() for t in (p0, m1, m2)]
+    b = [t.clone() for t in (p0, m1, m2)]
+    plan_a = D.FvrPlan(cloud.n, dims, box.half, 0, dev)
+    plan_b = D.FvrPlan(cloud.n, dims, box.half, 0, dev)
+    D.adam(a[0], grads, a[1], a[2], scal, 0.3, 8.0)
+    plan_a.bin(a[0], row_ordered=True)
+    plan_b.adam_bin(b[0], grads, b[1], b[2], scal, 0.3, 8.0, row_ordered=True)
+    for x, y in zip(a, b):
+        np.testing.assert_array_equal(x.cpu().numpy(), y.cpu().numpy())
+    for x, y in zip(plan_a.export_bins(), plan_b.export_bins()):
+        np.testing.assert_array_equal(x, y)
