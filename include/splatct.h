@@ -338,17 +338,20 @@ int splatct_iter_finalize(const double* sums, double lambda1, double lambda2, do
  * (32 blocks sum fixed slices, the last one to finish combines them in block
  * order: deterministic); a part with n = 0 keeps sums[f] as given.  scratch:
  * SPLATCT_FIN_SCRATCH_DOUBLES doubles, zero before the first call (the kernel
- * leaves its ticket word at zero again).  Replaces the three separate
- * reductions of the single-device training step. */
+ * leaves its ticket word at zero again).  sched (optional, sched_len rows):
+ * the Adam scalars {lr, 1-b1^t, 1-b2^t} per pre-increment step, computed on
+ * the host like the reference; steps beyond it use device pow.  Replaces the
+ * three separate reductions of the single-device training step. */
 #define SPLATCT_FIN_SCRATCH_DOUBLES 97
 int splatct_iter_finalize_partials(double* sums, const double* l1_part, int64_t n_l1,
                                    const double* ssim_part, int64_t n_ssim,
                                    const double* tv_part, int64_t n_tv, double* scratch,
-                                   double lambda1, double lambda2, double lambda3,
-                                   double l1_count, double ssim_count, double tv_count,
-                                   double lr0, double lrf, int64_t max_iters, int64_t* step,
-                                   int64_t* iter, double* trace, int64_t trace_cap, double* adam,
-                                   int* halt, void* stream);
+                                   const double* sched, int64_t sched_len, double lambda1,
+                                   double lambda2, double lambda3, double l1_count,
+                                   double ssim_count, double tv_count, double lr0, double lrf,
+                                   int64_t max_iters, int64_t* step, int64_t* iter,
+                                   double* trace, int64_t trace_cap, double* adam, int* halt,
+                                   void* stream);
 
 /* ---------------------------------------------------------------------------
  * Adam: optim.adam_step (optim.py:109-144): bias-corrected Adam on the

@@ -83,9 +83,9 @@ SIGNATURES: dict[str, list] = {
     "splatct_reduce_sum": [c_vp, c_i64, c_vp, c_vp],
     "splatct_iter_finalize": [c_vp, c_f64, c_f64, c_f64, c_f64, c_f64, c_f64, c_f64, c_f64, c_i64,
                               c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp],
-    "splatct_iter_finalize_partials": [c_vp, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_f64,
-                                       c_f64, c_f64, c_f64, c_f64, c_f64, c_f64, c_f64, c_i64,
-                                       c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp],
+    "splatct_iter_finalize_partials": [c_vp, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp,
+                                       c_i64, c_f64, c_f64, c_f64, c_f64, c_f64, c_f64, c_f64,
+                                       c_f64, c_i64, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp],
     "splatct_loss_partials": [c_i32, c_i32, c_i32, c_f64, c_vp, c_sz, c_vpp, c_i64p, c_vpp,
                               c_i64p],
     "splatct_loss_fused_prepared_deferred": [c_vp, c_vp, c_i32, c_i32, c_i32, c_f64, c_f64,

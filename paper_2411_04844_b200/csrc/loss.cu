@@ -870,6 +870,8 @@ struct FinParts {
     const double* p[3];   // l1, ssim, tv partials (or null: sums[f] is final)
     int64_t n[3];
     double* scratch;      // FIN_BLOCKS x 3 block sums, then a ticket word (zero between calls)
+    const double* sched;  // optional {lr, 1-b1^t, 1-b2^t} per pre-increment step (host-computed)
+    int64_t sched_len;
 };
 constexpr int FIN_BLOCKS = 32, FIN_NT = 256;
 
@@ -944,11 +946,19 @@ __global__ void k_iter_finalize(double* __restrict__ sums, FinParts parts, doubl
         return;
     }
     const int64_t st = *step;
-    const double T = (double)(max_iters > 1 ? max_iters : 1);
-    const double frac = (double)(st < max_iters ? st : max_iters) / T;
-    adam[0] = lr0 * pow(lrf / lr0, frac);
-    adam[1] = 1.0 - pow(0.9, (double)(st + 1));
-    adam[2] = 1.0 - pow(0.999, (double)(st + 1));
+    if (parts.sched != nullptr && st >= 0 && st < parts.sched_len) {
+        // the schedule as the reference computes it on the host (Python float
+        // powers, optim.py:88-90, 123-126), tabulated once per run
+        adam[0] = parts.sched[3 * st];
+        adam[1] = parts.sched[3 * st + 1];
+        adam[2] = parts.sched[3 * st + 2];
+    } else {
+        const double T = (double)(max_iters > 1 ? max_iters : 1);
+        const double frac = (double)(st < max_iters ? st : max_iters) / T;
+        adam[0] = lr0 * pow(lrf / lr0, frac);
+        adam[1] = 1.0 - pow(0.9, (double)(st + 1));
+        adam[2] = 1.0 - pow(0.999, (double)(st + 1));
+    }
     *step = st + 1;
     *iter = it + 1;
 }
@@ -1177,7 +1187,7 @@ int splatct_iter_finalize(const double* sums, double lambda1, double lambda2, do
                           double lrf, int64_t max_iters, int64_t* step, int64_t* iter,
                           double* trace, int64_t trace_cap, double* adam, int* halt,
                           void* stream) {
-    const FinParts none{{nullptr, nullptr, nullptr}, {0, 0, 0}, nullptr};
+    const FinParts none{{nullptr, nullptr, nullptr}, {0, 0, 0}, nullptr, nullptr, 0};
     SPLATCT_CK(launch_pdl(k_iter_finalize, dim3(1), dim3(1), 0, as_stream(stream),
                           const_cast<double*>(sums), none, lambda1, lambda2, lambda3, l1_count,
                           ssim_count, tv_count, lr0, lrf, max_iters, step, iter, trace, trace_cap,
@@ -1189,16 +1199,19 @@ int splatct_iter_finalize(const double* sums, double lambda1, double lambda2, do
 int splatct_iter_finalize_partials(double* sums, const double* l1_part, int64_t n_l1,
                                    const double* ssim_part, int64_t n_ssim,
                                    const double* tv_part, int64_t n_tv, double* scratch,
-                                   double lambda1, double lambda2, double lambda3,
-                                   double l1_count, double ssim_count, double tv_count,
-                                   double lr0, double lrf, int64_t max_iters, int64_t* step,
-                                   int64_t* iter, double* trace, int64_t trace_cap, double* adam,
-                                   int* halt, void* stream) {
+                                   const double* sched, int64_t sched_len, double lambda1,
+                                   double lambda2, double lambda3, double l1_count,
+                                   double ssim_count, double tv_count, double lr0, double lrf,
+                                   int64_t max_iters, int64_t* step, int64_t* iter,
+                                   double* trace, int64_t trace_cap, double* adam, int* halt,
+                                   void* stream) {
     SPLATCT_REQUIRE(scratch != nullptr, "finalize scratch required");
     const FinParts parts{{n_l1 > 0 ? l1_part : nullptr, n_ssim > 0 ? ssim_part : nullptr,
                           n_tv > 0 ? tv_part : nullptr},
                          {n_l1, n_ssim, n_tv},
-                         scratch};
+                         scratch,
+                         sched_len > 0 ? sched : nullptr,
+                         sched_len};
     SPLATCT_CK(launch_pdl(k_iter_finalize, dim3(FIN_BLOCKS), dim3(FIN_NT), 0, as_stream(stream), sums,
                           parts, lambda1, lambda2, lambda3, l1_count, ssim_count, tv_count, lr0,
                           lrf, max_iters, step, iter, trace, trace_cap, adam, halt));

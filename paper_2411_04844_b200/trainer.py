@@ -35,6 +35,17 @@ SIGMA_FLOOR = 0.3
 ROW_ORDERED_BINS = os.environ.get("SPLATCT_ROW_ORDER", "1") != "0"
 
 
+def adam_schedule(lr0: float, lrf: float, max_iters: int) -> list:
+    """[lr, 1 - 0.9^t, 1 - 0.999^t] for pre-increment steps 0..max_iters, with
+    Python float arithmetic as in the reference (optim.py:88-90, 123-126)."""
+    T = max(int(max_iters), 1)
+    rows = []
+    for s in range(int(max_iters) + 1):
+        rows.append([lr0 * (lrf / lr0) ** (min(s, max_iters) / T), 1.0 - 0.9 ** (s + 1),
+                     1.0 - 0.999 ** (s + 1)])
+    return rows
+
+
 @dataclass
 class Slab:
     """The z-range [z0, z0 + c_local) of a c_global-slice volume owned by a rank."""
@@ -126,6 +137,10 @@ class Trainer:
                                    device=dev)
         self.sums = torch.zeros(3, dtype=torch.float64, device=dev)
         self.fin_scratch = torch.zeros(97, dtype=torch.float64, device=dev)   # SPLATCT_FIN_SCRATCH_DOUBLES
+        # the Adam scalars per pre-increment step, computed like the reference
+        # on the host (optim.py:88-90, 123-126): the finalize looks them up
+        self.adam_sched = torch.tensor(adam_schedule(self.lr0, self.lrf, self.max_iters),
+                                       dtype=torch.float64, device=dev)
         self.adam_s = torch.zeros(3, dtype=torch.float64, device=dev)
         self.step_t = torch.tensor([int(step)], dtype=torch.int64, device=dev)
         self.iter_t = torch.zeros(1, dtype=torch.int64, device=dev)
@@ -284,7 +299,8 @@ class Trainer:
                                   else (D.VP(0), 0, D.VP(0), 0))
             tvn = D.tv_partial_len(self.w, self.h, self.slab.c_local, blocked=True)
             parts = (l1p, nl1, ssp, nss, D.ptr(self.tv_part) if defer_tv else D.VP(0),
-                     tvn if defer_tv else 0, D.ptr(self.fin_scratch))
+                     tvn if defer_tv else 0, D.ptr(self.fin_scratch), D.ptr(self.adam_sched),
+                     int(self.adam_sched.shape[0]))
 
         def finalize_backward():
             scal = (float(lw.lambda1), float(lw.lambda2), float(lw.lambda3), self.l1_count,
