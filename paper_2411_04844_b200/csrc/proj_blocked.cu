@@ -501,13 +501,12 @@ __global__ void __launch_bounds__(32 * BS_WARPS, R == 8 ? 4 : 6) k_bspmm(GroupMa
         const int tlo = max(zlo - 1, 0) / 16, thi = min(zhi + 1, c - 1) / 16;
         const unsigned long long zm =
             (thi >= 63 ? ~0ull : ((1ull << (thi + 1)) - 1ull)) & ~((1ull << tlo) - 1ull);
-        // footprint coverage of the quad's pixels and their one-pixel ring
-        const int xa = max(x0 - 1, 0), xb = min(x0 + 2, gm.w - 1);
-        const int ya = max(y0 - 1, 0), yb = min(y0 + 2, gm.h - 1);
-        unsigned long long any = 0ull;
-        for (int yy = ya; yy <= yb; ++yy)
-            for (int xx = xa; xx <= xb; ++xx) any |= oc.occ[(int64_t)yy * gm.w + xx];
-        if (!halo && (any & zm) == 0ull) {   // warp-uniform
+        // footprint coverage of the quad's pixels and their one-pixel ring: the
+        // 4 x 4 neighbourhood's words are loaded one per lane, then a vote
+        const int xx = x0 - 1 + (lane & 3), yy = y0 - 1 + ((lane >> 2) & 3);
+        const bool in = lane < 16 && xx >= 0 && xx < gm.w && yy >= 0 && yy < gm.h;
+        const bool cov = in && (oc.occ[(int64_t)yy * gm.w + xx] & zm) != 0ull;
+        if (!halo && !__any_sync(0xffffffffu, cov)) {   // warp-uniform
             if (TV && tv.partial && lane == 0) tv.partial[zch * ngr + g] = 0.0;
             return;
         }
