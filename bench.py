@@ -201,7 +201,8 @@ def cpu_reference_iters(cfg, steps, warmup, threads=None):
 
 
 def stage_profile(tr, iters):
-    """Per-stage device time of eager iterations (CUDA events on the launch stream)."""
+    """Per-stage device time of eager iterations (CUDA events on the launch stream;
+    median over the iterations)."""
     import torch
     from paper_2411_04844_b200 import device as D
     from paper_2411_04844_b200 import _lib
@@ -209,7 +210,7 @@ def stage_profile(tr, iters):
     s = torch.cuda.current_stream()
     names = ["proj_forward", "loss_fused", "proj_adjoint_tv", "finalize", "fvr_backward", "adam",
              "fvr_bin", "fvr_forward"]
-    acc = {k: 0.0 for k in names}
+    acc = {k: [] for k in names}
     lw = tr.weights
     launches = 0
     for _ in range(iters):
@@ -252,8 +253,8 @@ def stage_profile(tr, iters):
         torch.cuda.synchronize()
         launches = _lib.launch_count() - l0
         for k, nm in enumerate(names):
-            acc[nm] += ev[k].elapsed_time(ev[k + 1])
-    return {k: v / iters for k, v in acc.items()}, launches
+            acc[nm].append(ev[k].elapsed_time(ev[k + 1]))
+    return {k: float(np.median(v)) for k, v in acc.items()}, launches
 
 
 def time_config(cfg, steps, warmup, dev):
@@ -362,7 +363,7 @@ def run_b200(args, cfg):
     loss_last = float(tr.trace_rows()[-1, 0])
 
     # per-stage device times (eager, instrumented)
-    stages, _ = stage_profile(tr, 5)
+    stages, _ = stage_profile(tr, 11)
     # launches per iteration: one eager pass of exactly the stages the captured
     # graph replays
     from paper_2411_04844_b200 import _lib
@@ -386,14 +387,14 @@ def run_b200(args, cfg):
                                                 n_gaussians=cfg["n"], densify_interval=0)
         optim.run_reconstruction(meas_host, geom, settings, init_cloud=cloud)   # warm
         dts = []
-        for _ in range(3):   # median of three whole calls (host staging, page cache noise)
+        for _ in range(5):   # median of five whole calls (host staging, page cache noise)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             vol, cl_out, trace = optim.run_reconstruction(meas_host, geom, settings,
                                                           init_cloud=cloud)
             torch.cuda.synchronize()
             dts.append(time.perf_counter() - t0)
-        dt = sorted(dts)[1]
+        dt = sorted(dts)[2]
         # cold calls: no cached projector operator or captured graph (a first
         # call pays the operator build and the graph capture); median of three
         colds = []
@@ -430,7 +431,7 @@ def run_b200(args, cfg):
                   "distributed.run_reconstruction_sharded",
            "includes": "H2D of measured sinogram + cloud, operator lookup, plans, "
                        "initial splat, K iterations, D2H of volume + cloud + trace",
-           "timing": "median of 3 whole API calls after one warm call" if world == 1 else
+           "timing": "median of 5 whole API calls after one warm call" if world == 1 else
                      "one whole API call, max over ranks"}
     if dt_cold is not None:
         e2e["cold"] = {"value": args.steps / dt_cold, "unit": "iterations/s",

@@ -127,6 +127,12 @@ def pinned_output(shape) -> np.ndarray | None:
     the pool once the caller drops the array and all its views."""
     import weakref
     numel = int(np.prod(shape))
+    if not any(e.t.numel() == numel for e in _OUT_POOL):
+        # a new size: idle slots of other sizes go, and every slot of this size
+        # is page-locked now, so a caller that keeps one result while computing
+        # the next never pays cudaHostAlloc mid-run
+        _OUT_POOL[:] = [e for e in _OUT_POOL if e.busy]
+        _OUT_POOL.extend(_PinnedSlot(numel) for _ in range(_OUT_POOL_MAX))
     slot = next((e for e in _OUT_POOL if not e.busy and e.t.numel() == numel), None)
     if slot is None:
         if sum(e.busy for e in _OUT_POOL) >= _OUT_POOL_MAX:
