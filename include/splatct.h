@@ -314,6 +314,14 @@ int splatct_sum_sq_diff(const float* x, const float* y, int64_t count, double* w
 /* Sum n doubles in a fixed order into out[0] (deterministic reductions). */
 int splatct_reduce_sum(const double* in, int64_t n, double* out, void* stream);
 
+/* Host -> device upload through a page-locked staging buffer of >= bytes:
+ * nthreads host threads each copy a slice of src into pinned and queue that
+ * slice's DMA on stream (returns once every slice is queued; the DMAs run in
+ * stream order).  The measured sinogram's upload in run_reconstruction; the
+ * call releases the GIL (ctypes), so the caller overlaps it with other host work. */
+int splatct_stage_upload(void* dst, const void* src, void* pinned, size_t bytes, int nthreads,
+                         void* stream);
+
 /* TV terms across a z-slab boundary after an adjoint that ran without halo
  * planes (the halo exchange then overlaps it), loss.py:183-207: plane c-1 gets
  * -lambda/count * sign(hi - v) and |hi - v| is added to *tv_sum (this slab

@@ -81,6 +81,7 @@ SIGNATURES: dict[str, list] = {
                                     c_f64, c_vp, c_vp, c_sz, c_vp, c_vp, c_vp],
     "splatct_sum_sq_diff": [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp],
     "splatct_reduce_sum": [c_vp, c_i64, c_vp, c_vp],
+    "splatct_stage_upload": [c_vp, c_vp, c_vp, c_sz, c_i32, c_vp],
     "splatct_iter_finalize": [c_vp, c_f64, c_f64, c_f64, c_f64, c_f64, c_f64, c_f64, c_f64, c_i64,
                               c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp],
     "splatct_iter_finalize_partials": [c_vp, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp,

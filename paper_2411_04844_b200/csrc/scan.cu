@@ -5,6 +5,10 @@
 
 #include "common.cuh"
 
+#include <cstring>
+#include <thread>
+#include <vector>
+
 namespace splatct {
 
 static thread_local char g_err[1024] = "";
@@ -189,6 +193,33 @@ unsigned long long splatct_launch_count(void) { return splatct::g_launches.load(
 
 int splatct_reduce_sum(const double* in, int64_t n, double* out, void* stream) {
     return splatct::reduce_sum_f64(in, n, out, splatct::as_stream(stream));
+}
+
+int splatct_stage_upload(void* dst, const void* src, void* pinned, size_t bytes, int nthreads,
+                         void* stream) {
+    // nthreads host threads each copy one slice into the page-locked buffer
+    // and queue that slice's DMA at once, so the copies and the DMAs overlap
+    SPLATCT_REQUIRE(dst && src && pinned, "null pointer");
+    if (bytes == 0) return SPLATCT_OK;
+    const int k = nthreads < 1 ? 1 : (nthreads > 32 ? 32 : nthreads);
+    const size_t slice = ((bytes + k - 1) / k + 4095) & ~(size_t)4095;
+    cudaStream_t s = splatct::as_stream(stream);
+    std::vector<std::thread> th;
+    std::vector<cudaError_t> err(k, cudaSuccess);
+    for (int i = 0; i < k; ++i) {
+        const size_t off = (size_t)i * slice;
+        if (off >= bytes) break;
+        const size_t len = bytes - off < slice ? bytes - off : slice;
+        th.emplace_back([=, &err]() {
+            memcpy(static_cast<char*>(pinned) + off, static_cast<const char*>(src) + off, len);
+            err[i] = cudaMemcpyAsync(static_cast<char*>(dst) + off,
+                                     static_cast<const char*>(pinned) + off, len,
+                                     cudaMemcpyHostToDevice, s);
+        });
+    }
+    for (auto& t : th) t.join();
+    for (int i = 0; i < k; ++i) SPLATCT_CK(err[i]);
+    return SPLATCT_OK;
 }
 
 }  // extern "C"

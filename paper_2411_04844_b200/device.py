@@ -248,23 +248,45 @@ def yxz_to_zyx(t: torch.Tensor, out: np.ndarray | None = None) -> np.ndarray:
     return to_host(t.permute(2, 0, 1).contiguous(), out)
 
 
-class StagedHost:
-    """A host array being copied into the pinned staging buffer on a helper
-    thread (so the caller can prepare other inputs meanwhile); .to(device)
-    waits for the copy and uploads from pinned memory."""
+_UPLOAD_STREAM: dict = {}
+_UPLOAD_PIN: dict = {}
 
-    def __init__(self, views):
+
+class StagedHost:
+    """A host array uploaded by a helper thread while the caller prepares other
+    inputs: splatct_stage_upload copies it into a page-locked buffer with
+    several native threads and queues each slice's DMA as soon as the slice is
+    written (ctypes releases the GIL for the call).  .to() makes the caller's
+    stream wait for the upload and returns the device tensor."""
+
+    def __init__(self, views, device):
         import threading
-        self.a = np.asarray(views)
-        self.st = _pinned(self.a.size, torch.float32)
-        self._th = threading.Thread(target=_par_copy,
-                                    args=(self.st.numpy().reshape(self.a.shape), self.a),
-                                    daemon=True)
+        self.a = np.ascontiguousarray(views, dtype=np.float32)
+        self.dev = torch.device(device)
+        st = _UPLOAD_PIN.get(self.dev)
+        if st is None or st.numel() < self.a.size:   # its own buffer: DMAs outlive .to()
+            st = _UPLOAD_PIN[self.dev] = torch.empty(max(self.a.size, 1), dtype=torch.float32,
+                                                     pin_memory=True)
+        self.st = st
+        self.out = torch.empty(self.a.shape, dtype=torch.float32, device=self.dev)
+        side = _UPLOAD_STREAM.get(self.dev)
+        if side is None:
+            side = _UPLOAD_STREAM[self.dev] = torch.cuda.Stream(device=self.dev)
+        self.side = side
+        self.side.wait_stream(torch.cuda.current_stream(self.dev))   # out's allocation
+        self.done = torch.cuda.Event()
+        self._th = threading.Thread(target=self._run, daemon=True)
         self._th.start()
 
-    def to(self, device) -> torch.Tensor:
+    def _run(self):
+        call("splatct_stage_upload", ptr(self.out), VP(self.a.ctypes.data), ptr(self.st),
+             self.a.nbytes, 8, VP(self.side.cuda_stream))
+        self.done.record(self.side)
+
+    def to(self, device=None) -> torch.Tensor:
         self._th.join()
-        return self.st.view(self.a.shape).to(device, non_blocking=False)
+        torch.cuda.current_stream(self.dev).wait_event(self.done)
+        return self.out
 
 
 def sino_to_device(views, device) -> torch.Tensor:

@@ -18,9 +18,9 @@ orig_init, orig_to = D.StagedHost.__init__, D.StagedHost.to
 log = []
 
 
-def init(self, views):
+def init(self, views, device):
     self._t0 = time.perf_counter()
-    orig_init(self, views)
+    orig_init(self, views, device)
 
 
 def to(self, device):
