@@ -69,13 +69,22 @@ def cloud_to_params(cloud: GaussianCloud, device) -> torch.Tensor:
     return p
 
 
-def params_to_cloud(params: torch.Tensor) -> GaussianCloud:
-    """The inverse: transposed on the device, one download, host views."""
+def params_to_host(params: torch.Tensor) -> np.ndarray:
+    """The device [5, N] block as one packed host array [mu (N, 3) | sigma | I],
+    transposed on the device (one download)."""
     p = params.detach()
-    n = int(p.shape[1])
-    packed = torch.cat([p[0:3].t().reshape(-1), p[3], p[4]])
-    h = to_host(packed)
+    return to_host(torch.cat([p[0:3].t().reshape(-1), p[3], p[4]]))
+
+
+def cloud_from_host(h: np.ndarray) -> GaussianCloud:
+    """A GaussianCloud viewing a params_to_host array."""
+    n = h.size // 5
     return GaussianCloud(h[: 3 * n].reshape(n, 3), h[3 * n: 4 * n], h[4 * n:])
+
+
+def params_to_cloud(params: torch.Tensor) -> GaussianCloud:
+    """The inverse of cloud_to_params."""
+    return cloud_from_host(params_to_host(params))
 
 
 def _host_f32(arr) -> torch.Tensor:
