@@ -181,6 +181,14 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+def host_cores() -> int:
+    """Host cores this process may run on."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
 def cpu_reference_iters(cfg, steps, warmup, threads=None):
     """Time the oracle (the reference algorithm's CPU port) on the workload."""
     from oracle import oracle as O
@@ -614,7 +622,7 @@ def run_b200(args, cfg):
         out["configs"] = {name: time_config(CONFIGS[name], max(args.steps, 10), args.warmup, dev)
                           for name in args.extra.split(",") if name}
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not cone:
-        v, dt, cores = cpu_reference_iters(cfg, args.cpu_iters, 0)
+        v, dt, cores = cpu_reference_iters(cfg, args.cpu_iters, 0, threads=host_cores())
         out["cpu_baseline"] = {"value": round(v, 5), "unit": "iterations/s", "cores": cores,
                                "kind": "port",
                                "sample": f"{args.cpu_iters} full training iteration(s) of the "
@@ -633,7 +641,9 @@ def run_reference(args, cfg):
         return
     steps = max(1, min(args.steps, args.ref_max_steps))
     warm = min(args.warmup, 1)
-    v, dt, cores = cpu_reference_iters(cfg, steps, warm)
+    # every host core: torchrun exports OMP_NUM_THREADS=1 to its ranks, which
+    # would otherwise leave the OpenMP port on one thread
+    v, dt, cores = cpu_reference_iters(cfg, steps, warm, threads=host_cores())
     out = {"metric": METRIC, "value": round(v, 5), "unit": "iterations/s",
            "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": steps, "warmup": warm,
            "ms_per_step": round(1000 * dt / steps, 2), "higher_is_better": True,
