@@ -328,8 +328,12 @@ class Trainer:
         return st
 
     def iteration(self):
-        for _, fn in self._stages():
+        # NVTX ranges name every stage in an nsys / ncu timeline; a
+        # captured graph keeps only the kernels, its replay gets one range
+        for kind, fn in self._stages():
+            torch.cuda.nvtx.range_push(f"{kind}:{fn.__name__}")
             fn()
+            torch.cuda.nvtx.range_pop()
 
     def capture(self):
         """Capture one iteration as a CUDA graph (runs one real iteration first)."""
@@ -378,7 +382,9 @@ class Trainer:
 
     def step(self):
         if self.graph is not None:
+            torch.cuda.nvtx.range_push("iteration (graph)")
             self.graph.replay()
+            torch.cuda.nvtx.range_pop()
         elif getattr(self, "segments", None):
             for kind, x in self.segments:
                 if kind == "graph":
