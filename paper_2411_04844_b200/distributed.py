@@ -197,12 +197,18 @@ def init_from_env(backend: str = "nccl"):
     """Initialise torch.distributed from torchrun's env (127.0.0.1 rendezvous)."""
     if dist.is_available() and not dist.is_initialized() and int(os.environ.get("WORLD_SIZE", "1")) > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        # failure detection (SURVEY 5.3): a rank that dies or hangs in a
+        # collective surfaces as an error on the others instead of a silent hang
+        os.environ.setdefault("TORCH_NCCL_ASYNC_ERROR_HANDLING", "1")
+        import datetime
+        timeout = datetime.timedelta(seconds=int(os.environ.get("SPLATCT_PG_TIMEOUT_S", "600")))
         local = int(os.environ.get("LOCAL_RANK", "0"))
         if backend == "nccl":
             torch.cuda.set_device(local)
-            dist.init_process_group(backend, device_id=torch.device("cuda", local))
+            dist.init_process_group(backend, device_id=torch.device("cuda", local),
+                                    timeout=timeout)
         else:
-            dist.init_process_group(backend)
+            dist.init_process_group(backend, timeout=timeout)
     if dist.is_available() and dist.is_initialized():
         return dist.get_rank(), dist.get_world_size()
     return 0, 1
