@@ -38,6 +38,33 @@ def main():
     D.projector_for(geom, w, h, 0.5, dev)
     torch.cuda.synchronize()
     print(f"operator build: {1e3 * (time.perf_counter() - t0):.1f} ms")
+    # phase split of one cold call (each wrapper synchronises)
+    from paper_2411_04844_b200.trainer import Trainer
+    T = {}
+
+    def wrap(obj, name):
+        fn = getattr(obj, name)
+
+        def w_(*a, **k):
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            r = fn(*a, **k)
+            torch.cuda.synchronize()
+            T[name] = T.get(name, 0.0) + 1e3 * (time.perf_counter() - t1)
+            return r
+        setattr(obj, name, w_)
+    wrap(D, "operator_for")
+    wrap(Trainer, "__init__")
+    wrap(Trainer, "capture")
+    wrap(Trainer, "initial_volume")
+    wrap(Trainer, "step")
+    optim.clear_caches()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    optim.run_reconstruction(meas, geom, st, init_cloud=cloud)
+    torch.cuda.synchronize()
+    print(f"cold call {1e3 * (time.perf_counter() - t0):.1f} ms: " +
+          ", ".join(f"{k} {v:.2f}" for k, v in T.items()))
 
 
 if __name__ == "__main__":
