@@ -15,6 +15,9 @@
 // in the same ascending-column order for the adjoint (rows of A^T are sorted
 // by ray), so the blocked and unblocked operators agree to f32 rounding of
 // the accumulation order only.
+#include <stdlib.h>
+#include <string.h>
+
 #include "common.cuh"
 
 namespace splatct {
@@ -226,6 +229,61 @@ __global__ void __launch_bounds__(BLK_NT) k_block_build(GroupMap gm, const int64
     }
     __syncthreads();
     if (threadIdx.x == 0 && mode == 0) gcount[g] = nuniq;
+}
+
+// Count pass for the column-keyed kinds (0, 1, 2): the number of distinct
+// pixels among a group's member rows, which is the fill's unique-key count
+// (the march key is a function of the pixel).  An open-addressing set in
+// shared memory (load factor <= 1/2) replaces the fill's sort: one CAS per
+// entry instead of a bitonic network.
+constexpr int HC_BITS = 14;
+constexpr int HC_SLOTS = 1 << HC_BITS;   // 2 x BLK_CAP
+static_assert(HC_SLOTS >= 2 * BLK_CAP, "hash set load factor");
+
+__global__ void __launch_bounds__(BLK_NT) k_block_count_hash(GroupMap gm,
+                                                             const int64_t* __restrict__ ptr,
+                                                             const int32_t* __restrict__ idx,
+                                                             int64_t* __restrict__ gcount,
+                                                             int* __restrict__ overflow) {
+    extern __shared__ unsigned char smem[];
+    uint32_t* tab = reinterpret_cast<uint32_t*>(smem);   // [HC_SLOTS]
+    __shared__ int64_t beg[8], len[8];
+    __shared__ int nuniq, ok;
+    const int64_t g = blockIdx.x;
+    const int NR = gm.rows();
+    if (threadIdx.x < 8) {
+        const int64_t r = (int)threadIdx.x < NR ? gm.row(g, threadIdx.x) : -1;
+        beg[threadIdx.x] = r >= 0 ? ptr[r] : 0;
+        len[threadIdx.x] = r >= 0 ? ptr[r + 1] - ptr[r] : 0;
+    }
+    for (int i = threadIdx.x; i < HC_SLOTS; i += BLK_NT) tab[i] = 0xffffffffu;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int64_t t = 0;
+        for (int k = 0; k < NR; ++k) t += len[k];
+        ok = t <= BLK_CAP;
+        if (!ok) atomicExch(overflow, 1);
+        nuniq = 0;
+    }
+    __syncthreads();
+    if (!ok) return;   // the fill rejects the operator
+    int mine = 0;
+    for (int k = 0; k < NR; ++k) {
+        for (int64_t i = threadIdx.x; i < len[k]; i += BLK_NT) {
+            const uint32_t pix = (uint32_t)idx[beg[k] + i];
+            uint32_t s = (pix * 2654435761u) >> (32 - HC_BITS);
+            for (;;) {
+                const uint32_t old = atomicCAS(&tab[s], 0xffffffffu, pix);
+                if (old == 0xffffffffu) { ++mine; break; }
+                if (old == pix) break;
+                s = (s + 1) & (HC_SLOTS - 1);
+            }
+        }
+    }
+    mine = __reduce_add_sync(0xffffffffu, mine);
+    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&nuniq, mine);
+    __syncthreads();
+    if (threadIdx.x == 0) gcount[g] = nuniq;
 }
 
 // ---------------------------------------------------------------------------
@@ -788,11 +846,21 @@ int splatct_proj_block_count(const int64_t* ptr, const int32_t* idx, int nrows, 
     if (!attr) {
         SPLATCT_CK(cudaFuncSetAttribute(k_block_build, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)block_smem(3)));
+        SPLATCT_CK(cudaFuncSetAttribute(k_block_count_hash,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        HC_SLOTS * (int)sizeof(uint32_t)));
         attr = true;
     }
-    k_block_build<<<(unsigned)ng, BLK_NT, block_smem(kind), s>>>(
-        gm, ptr, idx, nullptr, reinterpret_cast<const float2*>(order_dir), 0, cnt, nullptr, nullptr,
-        nullptr, overflow);
+    // SPLATCT_BLOCK_COUNT=sort counts with the fill's sort (test knob)
+    const char* how = getenv("SPLATCT_BLOCK_COUNT");
+    if (!gm.band() && !(how && !strcmp(how, "sort"))) {
+        k_block_count_hash<<<(unsigned)ng, BLK_NT, HC_SLOTS * sizeof(uint32_t), s>>>(
+            gm, ptr, idx, cnt, overflow);
+    } else {
+        k_block_build<<<(unsigned)ng, BLK_NT, block_smem(kind), s>>>(
+            gm, ptr, idx, nullptr, reinterpret_cast<const float2*>(order_dir), 0, cnt, nullptr,
+            nullptr, nullptr, overflow);
+    }
     SPLATCT_LAUNCH_CK();
     if (int e = exclusive_scan_i64(cnt, gptr, ng + 1, scan_tmp, s)) return e;
     int ovf = 0;

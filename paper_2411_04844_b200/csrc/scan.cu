@@ -5,9 +5,13 @@
 
 #include "common.cuh"
 
+#include <cstdlib>
 #include <cstring>
 #include <thread>
 #include <vector>
+#if defined(__x86_64__)
+#include <emmintrin.h>
+#endif
 
 namespace splatct {
 
@@ -195,6 +199,32 @@ int splatct_reduce_sum(const double* in, int64_t n, double* out, void* stream) {
     return splatct::reduce_sum_f64(in, n, out, splatct::as_stream(stream));
 }
 
+// Host copy into page-locked staging memory with non-temporal stores: the
+// lines go to DRAM instead of staying dirty in the CPU caches, so the DMA
+// that follows reads them without snooping (SPLATCT_STAGE_NT=0: memcpy).
+static void stage_copy(char* dst, const char* src, size_t len, bool nt) {
+#if defined(__x86_64__)
+    if (nt && ((uintptr_t)dst & 15) == 0) {
+        size_t i = 0;
+        for (; i + 64 <= len; i += 64) {
+            const __m128i a = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i));
+            const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 16));
+            const __m128i c = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 32));
+            const __m128i d = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 48));
+            _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i), a);
+            _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 16), b);
+            _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 32), c);
+            _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 48), d);
+        }
+        if (i < len) memcpy(dst + i, src + i, len - i);
+        _mm_sfence();
+        return;
+    }
+#endif
+    (void)nt;
+    memcpy(dst, src, len);
+}
+
 int splatct_stage_upload(void* dst, const void* src, void* pinned, size_t bytes, int nthreads,
                          void* stream) {
     // nthreads host threads each copy one slice into the page-locked buffer
@@ -204,6 +234,8 @@ int splatct_stage_upload(void* dst, const void* src, void* pinned, size_t bytes,
     const int k = nthreads < 1 ? 1 : (nthreads > 32 ? 32 : nthreads);
     const size_t slice = ((bytes + k - 1) / k + 4095) & ~(size_t)4095;
     cudaStream_t s = splatct::as_stream(stream);
+    const char* env = getenv("SPLATCT_STAGE_NT");
+    const bool nt = !(env && !strcmp(env, "0"));
     std::vector<std::thread> th;
     std::vector<cudaError_t> err(k, cudaSuccess);
     for (int i = 0; i < k; ++i) {
@@ -211,7 +243,8 @@ int splatct_stage_upload(void* dst, const void* src, void* pinned, size_t bytes,
         if (off >= bytes) break;
         const size_t len = bytes - off < slice ? bytes - off : slice;
         th.emplace_back([=, &err]() {
-            memcpy(static_cast<char*>(pinned) + off, static_cast<const char*>(src) + off, len);
+            stage_copy(static_cast<char*>(pinned) + off, static_cast<const char*>(src) + off, len,
+                       nt);
             err[i] = cudaMemcpyAsync(static_cast<char*>(dst) + off,
                                      static_cast<const char*>(pinned) + off, len,
                                      cudaMemcpyHostToDevice, s);

@@ -386,6 +386,26 @@ def test_projector_band_groups_match_4ray_groups(groups, monkeypatch):
         D.ProjectorOperator(big, 512, 512, 0.5, dev)
 
 
+@pytest.mark.parametrize("size", [256, 512])
+def test_block_count_hash_matches_sort(size, monkeypatch):
+    """The blocked operators' count pass (a shared-memory hash set of the
+    group's pixels) gives the same group sizes as counting with the fill's
+    sort, so the built operators are identical (C2 / C4 fan geometries)."""
+    import torch
+    from paper_2411_04844_b200 import device as D
+    dev = D.require_cuda()
+    geom = (core.ScanGeometry.fan(50, 512, 1.6, 512.0, 512.0) if size == 256
+            else core.ScanGeometry.fan(100, 1024, 1.6, 1024.0, 1024.0))
+    monkeypatch.setenv("SPLATCT_BLOCK_COUNT", "sort")
+    ref = D.ProjectorOperator(geom, size, size, 0.5, dev)
+    monkeypatch.delenv("SPLATCT_BLOCK_COUNT")
+    op = D.ProjectorOperator(geom, size, size, 0.5, dev)
+    for a, b in ((ref.fb, op.fb), (ref.ab, op.ab)):
+        assert a[3] == b[3]
+        for u, v in zip(a[:3], b[:3]):
+            assert torch.equal(u, v)
+
+
 @pytest.mark.parametrize("dims,n", [((64, 48, 40), 3000), ((256, 256, 64), 20000)])
 def test_row_ordered_bins_same_pairs(dims, n):
     """splatct_fvr_bin_row_ordered (the training step's bins): every tile holds
