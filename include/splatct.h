@@ -212,7 +212,10 @@ int splatct_proj_adjoint(const int64_t* at_ptr, const int32_t* at_ray, const flo
  * (k0 << 27 | pixel, w[4]) for band rays k0..k0+3, one per window of a
  * pixel's run of rays, entries ordered by (k0, pixel); order_dir is ignored.
  * count (synchronous) -> gptr[ngroups+1] and *nb; fill -> gidx, gval
- * (float[nb][R], R = 8 for kind 2 and 4 otherwise, 16-byte aligned). */
+ * (float[nb][R], R = 8 for kind 2 and 4 otherwise, 16-byte aligned).  fill
+ * takes the scratch its count used (the count leaves the largest group's
+ * size there; a mismatch is an error, not a wrong operator).  Rows already
+ * sorted by column (A^T from splatct_proj_fill) are merged without a sort. */
 int splatct_proj_block_scratch_bytes(int nrows, int kind, int w, int h, size_t* bytes);
 int splatct_proj_block_count(const int64_t* ptr, const int32_t* idx, int nrows, int kind, int w,
                              int h, const float* order_dir, int64_t* gptr, void* scratch,

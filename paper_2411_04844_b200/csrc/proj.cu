@@ -17,30 +17,51 @@
 // vector loads of contiguous z-vectors (yxz volume / (m,n,p) sinogram), all
 // slices of the z-slab handled by one weight fetch.  The adjoint also fuses
 // the TV subgradient and TV value of loss.tv_loss (loss.py:183-207).
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "raygeom.cuh"
 
 namespace splatct {
 
-__global__ void k_proj_count(Geom g, int64_t* __restrict__ cnt) {
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= g.m * g.n_det) return;
-    int64_t c = 0;
-    march_ray(g, r, [&](int, double, double) { ++c; });
-    cnt[r] = c;
+// The march is one sequential f64 chain per ray: a thread per ray leaves
+// ~5 warps per SM at C2.  It runs as PSEG segments per ray (march_ray_seg),
+// a thread each; segment (r, s) is CSR sub-row r * PSEG + s, so a ray's
+// entries are its segments' in order (SPLATCT_MARCH_SEGMENTS=1: whole rays).
+constexpr int PSEG = 16;
+
+static int march_segments() {
+    const char* e = getenv("SPLATCT_MARCH_SEGMENTS");
+    const int n = e ? atoi(e) : PSEG;
+    return n < 1 ? 1 : (n > PSEG ? PSEG : n);
 }
 
-__global__ void k_proj_fill(Geom g, const int64_t* __restrict__ a_ptr, int32_t* __restrict__ a_col,
-                            float* __restrict__ a_val) {
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= g.m * g.n_det) return;
-    int64_t j = a_ptr[r];
+__global__ void k_proj_count(Geom g, int nseg, int64_t* __restrict__ cnt) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= (int64_t)g.m * g.n_det * nseg) return;
+    int64_t c = 0;
+    march_ray_seg(g, (int)(i / nseg), (int)(i % nseg), nseg, [&](int, double, double) { ++c; });
+    cnt[i] = c;
+}
+
+__global__ void k_proj_fill(Geom g, int nseg, const int64_t* __restrict__ sub_ptr,
+                            int32_t* __restrict__ a_col, float* __restrict__ a_val) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= (int64_t)g.m * g.n_det * nseg) return;
+    int64_t j = sub_ptr[i];
     const double step = g.step;
-    march_ray(g, r, [&](int pix, double w, double) {
+    march_ray_seg(g, (int)(i / nseg), (int)(i % nseg), nseg, [&](int pix, double w, double) {
         a_col[j] = pix;
         a_val[j] = (float)(step * w);
         ++j;
     });
+}
+
+// a_ptr[r] = sub_ptr[r * nseg] (r = 0 .. rays)
+__global__ void k_ray_ptr(const int64_t* __restrict__ sub_ptr, int rays, int nseg,
+                          int64_t* __restrict__ a_ptr) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r <= rays) a_ptr[r] = sub_ptr[(int64_t)r * nseg];
 }
 
 __global__ void k_col_count(const int32_t* __restrict__ a_col, int64_t nnz,
@@ -49,13 +70,15 @@ __global__ void k_col_count(const int32_t* __restrict__ a_col, int64_t nnz,
     if (j < nnz) atomicAdd(&cnt[a_col[j]], 1ull);
 }
 
+// warp per ray (the slot order inside a pixel row is arbitrary: k_row_sort
+// orders it by ray next)
 __global__ void k_transpose_fill(int n_rays, const int64_t* __restrict__ a_ptr,
                                  const int32_t* __restrict__ a_col, const float* __restrict__ a_val,
                                  unsigned long long* __restrict__ cursor,
                                  int32_t* __restrict__ t_ray, float* __restrict__ t_val) {
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    const int r = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
     if (r >= n_rays) return;
-    for (int64_t j = a_ptr[r]; j < a_ptr[r + 1]; ++j) {
+    for (int64_t j = a_ptr[r] + (threadIdx.x & 31); j < a_ptr[r + 1]; j += 32) {
         const unsigned long long pos = atomicAdd(&cursor[a_col[j]], 1ull);
         t_ray[pos] = r;
         t_val[pos] = a_val[j];
@@ -338,7 +361,7 @@ static Geom make_geom(const double* cos_t, const double* sin_t, int m, int n_det
 }
 
 struct ProjScratch {
-    size_t o_cnt, o_cursor, o_scan, o_tray, o_tval, total;
+    size_t o_cnt, o_cursor, o_sub, o_scan, o_tray, o_tval, total;
 };
 static ProjScratch proj_scratch(int m, int n_det, int w, int h, int64_t nnz) {
     ProjScratch S{};
@@ -346,13 +369,27 @@ static ProjScratch proj_scratch(int m, int n_det, int w, int h, int64_t nnz) {
     const int64_t big = rays > pix ? rays : pix;
     size_t off = 0;
     auto take = [&](size_t b) { size_t o = off; off += align_up(b > 0 ? b : 1); return o; };
-    S.o_cnt = take(sizeof(int64_t) * (big + 1));
+    const int64_t nsub = rays * PSEG;   // march segments (sub-rows)
+    const int64_t cnt_n = (big > nsub ? big : nsub) + 1;
+    S.o_cnt = take(sizeof(int64_t) * cnt_n);
     S.o_cursor = take(sizeof(int64_t) * (pix + 1));
-    S.o_scan = take(scan_temp_bytes(big + 1));
+    S.o_sub = take(sizeof(int64_t) * (nsub + 1));
+    S.o_scan = take(scan_temp_bytes(cnt_n));
     S.o_tray = take(sizeof(int32_t) * (size_t)nnz);
     S.o_tval = take(sizeof(float) * (size_t)nnz);
     S.total = off;
     return S;
+}
+
+// per-segment entry counts of the march -> exclusive offsets sub[0 .. rays * nseg]
+static int march_offsets(const Geom& g, int nseg, const ProjScratch& S, void* scratch,
+                         int64_t* sub, cudaStream_t s) {
+    const int64_t nsub = (int64_t)g.m * g.n_det * nseg;
+    int64_t* cnt = reinterpret_cast<int64_t*>((char*)scratch + S.o_cnt);
+    SPLATCT_CK(cudaMemsetAsync(cnt + nsub, 0, sizeof(int64_t), s));
+    k_proj_count<<<(unsigned)((nsub + 127) / 128), 128, 0, s>>>(g, nseg, cnt);
+    SPLATCT_LAUNCH_CK();
+    return exclusive_scan_i64(cnt, sub, nsub + 1, (char*)scratch + S.o_scan, s);
 }
 
 }  // namespace splatct
@@ -376,11 +413,11 @@ int splatct_proj_count(const double* cos_t, const double* sin_t, int m, int n_de
     cudaStream_t s = as_stream(stream);
     Geom g = make_geom(cos_t, sin_t, m, n_det, spacing, step, is_fan, rs, rd, w, h);
     const int rays = m * n_det;
-    int64_t* cnt = reinterpret_cast<int64_t*>((char*)scratch + S.o_cnt);
-    SPLATCT_CK(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (rays + 1), s));
-    k_proj_count<<<(rays + 127) / 128, 128, 0, s>>>(g, cnt);
+    int64_t* sub = reinterpret_cast<int64_t*>((char*)scratch + S.o_sub);
+    const int nseg = march_segments();
+    if (int e = march_offsets(g, nseg, S, scratch, sub, s)) return e;
+    k_ray_ptr<<<(rays + 1 + 255) / 256, 256, 0, s>>>(sub, rays, nseg, a_ptr);
     SPLATCT_LAUNCH_CK();
-    if (int e = exclusive_scan_i64(cnt, a_ptr, rays + 1, (char*)scratch + S.o_scan, s)) return e;
     SPLATCT_CK(cudaMemcpyAsync(nnz, a_ptr + rays, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     SPLATCT_CK(cudaStreamSynchronize(s));
     return SPLATCT_OK;
@@ -401,7 +438,12 @@ int splatct_proj_fill(const double* cos_t, const double* sin_t, int m, int n_det
     SPLATCT_REQUIRE(scratch_bytes >= S.total, "projector scratch too small (%zu < %zu)",
                     scratch_bytes, S.total);
     Geom g = make_geom(cos_t, sin_t, m, n_det, spacing, step, is_fan, rs, rd, w, h);
-    k_proj_fill<<<(rays + 127) / 128, 128, 0, s>>>(g, a_ptr, a_col, a_val);
+    // the segments' offsets again (the count's scratch is not kept), then the fill
+    int64_t* sub = reinterpret_cast<int64_t*>((char*)scratch + S.o_sub);
+    const int nseg = march_segments();
+    if (int e = march_offsets(g, nseg, S, scratch, sub, s)) return e;
+    const int64_t nsub = (int64_t)rays * nseg;
+    k_proj_fill<<<(unsigned)((nsub + 127) / 128), 128, 0, s>>>(g, nseg, sub, a_col, a_val);
     SPLATCT_LAUNCH_CK();
     // transpose: per-pixel counts -> offsets -> scatter -> per-row sort by ray
     auto* cnt = reinterpret_cast<unsigned long long*>((char*)scratch + S.o_cnt);
@@ -418,8 +460,8 @@ int splatct_proj_fill(const double* cos_t, const double* sin_t, int m, int n_det
         return e;
     SPLATCT_CK(cudaMemcpyAsync(cursor, at_ptr, sizeof(int64_t) * (pix + 1),
                                cudaMemcpyDeviceToDevice, s));
-    k_transpose_fill<<<(rays + 127) / 128, 128, 0, s>>>(rays, a_ptr, a_col, a_val, cursor, tray,
-                                                        tval);
+    k_transpose_fill<<<(unsigned)(((int64_t)rays * 32 + 255) / 256), 256, 0, s>>>(
+        rays, a_ptr, a_col, a_val, cursor, tray, tval);
     SPLATCT_LAUNCH_CK();
     k_row_sort<<<(unsigned)((pix * 32 + 255) / 256), 256, 0, s>>>(pix, at_ptr, tray, tval, at_ray,
                                                                   at_val);

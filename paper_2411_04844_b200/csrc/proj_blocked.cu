@@ -53,7 +53,7 @@ struct GroupMap {
 
 // One CTA per group: gather the member rows' entries, bitonic-sort by column,
 // merge equal columns into one (column, w[4]) entry.  mode 0 counts, mode 1
-// writes at gptr[g].
+// writes at gptr[g] (mode 2: writes, always through the sort).
 //
 // Band kinds (3, 4): a pixel of a band of B rays is crossed by a few
 // consecutive rays (its bilinear support spans ~2-3 detector bins).  Each
@@ -72,11 +72,14 @@ __global__ void __launch_bounds__(BLK_NT) k_block_build(GroupMap gm, const int64
                                                         const int64_t* __restrict__ gptr,
                                                         int32_t* __restrict__ gidx,
                                                         float4* __restrict__ gval,
-                                                        int* __restrict__ overflow) {
+                                                        int* __restrict__ overflow, int cap,
+                                                        int* __restrict__ maxlen) {
+    // cap (a power of two <= BLK_CAP): the largest group of this operator, from
+    // its count pass; it sizes the shared arrays, so small groups run more CTAs per SM
     extern __shared__ unsigned char smem[];
     uint32_t* key = reinterpret_cast<uint32_t*>(smem);            // [cap]
-    uint32_t* pay = key + BLK_CAP;                                // [cap] (k << 29 | src)
-    float* wv = reinterpret_cast<float*>(pay + BLK_CAP);          // [cap]
+    uint32_t* pay = key + cap;                                    // [cap] (k << 28 | src)
+    float* wv = reinterpret_cast<float*>(pay + cap);              // [cap]
     __shared__ int64_t beg[16], len[16];
     __shared__ int total, nuniq;
     const int64_t g = blockIdx.x;
@@ -90,10 +93,11 @@ __global__ void __launch_bounds__(BLK_NT) k_block_build(GroupMap gm, const int64
     if (threadIdx.x == 0) {
         int64_t t = 0;
         for (int k = 0; k < NR; ++k) t += len[k];
-        if (t > BLK_CAP) {
+        if (t > cap) {
             atomicExch(overflow, 1);
             t = 0;
         }
+        if (maxlen) atomicMax(maxlen, (int)t);
         total = (int)t;
     }
     __syncthreads();
@@ -124,13 +128,95 @@ __global__ void __launch_bounds__(BLK_NT) k_block_build(GroupMap gm, const int64
                 key[i] = pix;
             }
             pay[i] = ((uint32_t)k << 28) | (uint32_t)i;
-            wv[i] = mode == 1 ? val[j] : 0.f;
+            wv[i] = mode != 0 ? val[j] : 0.f;
         } else {
             key[i] = 0xffffffffu;
             pay[i] = 0xffffffffu;
         }
     }
     __syncthreads();
+    // Rows already sorted by column (the pixel quads' rows of A^T, sorted by
+    // ray): the (key, row) order the sort below builds is a merge of the rows,
+    // so each distinct key is placed by binary searches instead.  Its first
+    // occurrence (lowest row) is its head; the head's rank is the number of
+    // heads with a smaller key, summed over the rows from a prefix count.
+    if (!march && !gm.band() && mode == 1) {
+        int st[9];
+        st[0] = 0;
+        for (int k = 0; k < NR; ++k) st[k + 1] = st[k] + (int)len[k];
+        bool unsorted = false;
+        for (int i = threadIdx.x; i + 1 < L; i += BLK_NT)
+            if ((pay[i] >> 28) == (pay[i + 1] >> 28) && key[i] >= key[i + 1]) unsorted = true;
+        if (!__syncthreads_or(unsorted)) {
+            // entries of row kk with a key < x
+            auto lower = [&](int kk, uint32_t x) {
+                int lo = st[kk], hi = st[kk + 1];
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (key[mid] < x) lo = mid + 1; else hi = mid;
+                }
+                return lo - st[kk];
+            };
+            // heads, counted per contiguous chunk, then an exclusive block scan
+            const int chunk = (L + BLK_NT - 1) / BLK_NT;
+            const int c0 = min(L, (int)threadIdx.x * chunk), c1 = min(L, c0 + chunk);
+            int nh = 0;
+            for (int i = c0; i < c1; ++i) {
+                const int k = (int)(pay[i] >> 28);
+                const uint32_t x = key[i];
+                bool head = true;
+                for (int kk = 0; kk < k && head; ++kk) {
+                    const int lb = lower(kk, x);
+                    head = !(lb < st[kk + 1] - st[kk] && key[st[kk] + lb] == x);
+                }
+                nh += head;
+                pay[i] = ((uint32_t)k << 28) | (head ? 1u : 0u);
+            }
+            __shared__ int wsum[BLK_NT / 32];
+            const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+            int inc = nh;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += t;
+            }
+            if (lane == 31) wsum[wid] = inc;
+            __syncthreads();
+            int base = 0;
+            for (int q = 0; q < wid; ++q) base += wsum[q];
+            if (threadIdx.x == BLK_NT - 1) nuniq = base + inc;
+            int run = base + inc - nh;
+            for (int i = c0; i < c1; ++i) {
+                const uint32_t h = pay[i] & 1u;
+                pay[i] = (uint32_t)run;   // heads before entry i
+                run += (int)h;
+            }
+            __syncthreads();
+            const int nu = nuniq;
+            auto pre = [&](int j) { return j < L ? (int)pay[j] : nu; };
+            // every entry re-derives its row and head flag; heads write
+            for (int i = threadIdx.x; i < L; i += BLK_NT) {
+                int k = 0;
+                while (i >= st[k + 1]) ++k;
+                const uint32_t x = key[i];
+                if (pre(i + 1) == pre(i)) continue;   // not a head
+                float wr[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                int pos = 0;
+                for (int kk = 0; kk < NR; ++kk) {
+                    const int lb = kk == k ? i - st[k] : lower(kk, x);
+                    pos += pre(st[kk] + lb) - pre(st[kk]);
+                    if (kk == k) wr[kk] = wv[i];
+                    else if (kk > k && lb < st[kk + 1] - st[kk] && key[st[kk] + lb] == x)
+                        wr[kk] = wv[st[kk] + lb];
+                }
+                const int64_t o = gptr[g] + pos;
+                gidx[o] = (int32_t)x;
+                gval[o * (NR / 4)] = make_float4(wr[0], wr[1], wr[2], wr[3]);
+                if (NR == 8) gval[o * 2 + 1] = make_float4(wr[4], wr[5], wr[6], wr[7]);
+            }
+            return;
+        }
+    }
     // bitonic sort of (key, pay) pairs, ascending by key then payload
     for (int size = 2; size <= P; size <<= 1) {
         for (int stride = size >> 1; stride > 0; stride >>= 1) {
@@ -149,8 +235,8 @@ __global__ void __launch_bounds__(BLK_NT) k_block_build(GroupMap gm, const int64
         }
     }
     if (gm.band()) {   // sorted by (pixel, ray): cut each pixel's run into 4-ray windows
-        uint32_t* wkey = reinterpret_cast<uint32_t*>(wv + BLK_CAP);   // [cap] k0 << 27 | pixel
-        uint32_t* wpos = wkey + BLK_CAP;                              // [cap] first entry
+        uint32_t* wkey = reinterpret_cast<uint32_t*>(wv + cap);   // [cap] k0 << 27 | pixel
+        uint32_t* wpos = wkey + cap;                              // [cap] first entry
         if (threadIdx.x == 0) nuniq = 0;
         __syncthreads();
         for (int i = threadIdx.x; i < L; i += BLK_NT) {
@@ -212,7 +298,7 @@ __global__ void __launch_bounds__(BLK_NT) k_block_build(GroupMap gm, const int64
             const bool head = i < L && (i == 0 || key[i] != key[i - 1]);
             const unsigned m = __ballot_sync(0xffffffffu, head);
             const int pos = base + __popc(m & ((1u << threadIdx.x) - 1u));
-            if (head && mode == 1) {
+            if (head && mode != 0) {
                 float wr[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
                 for (int e = i; e < L && key[e] == key[i]; ++e) {
                     const uint32_t pl = pay[e];
@@ -244,7 +330,8 @@ __global__ void __launch_bounds__(BLK_NT) k_block_count_hash(GroupMap gm,
                                                              const int64_t* __restrict__ ptr,
                                                              const int32_t* __restrict__ idx,
                                                              int64_t* __restrict__ gcount,
-                                                             int* __restrict__ overflow) {
+                                                             int* __restrict__ overflow,
+                                                             int* __restrict__ maxlen) {
     extern __shared__ unsigned char smem[];
     uint32_t* tab = reinterpret_cast<uint32_t*>(smem);   // [HC_SLOTS]
     __shared__ int64_t beg[8], len[8];
@@ -263,6 +350,7 @@ __global__ void __launch_bounds__(BLK_NT) k_block_count_hash(GroupMap gm,
         for (int k = 0; k < NR; ++k) t += len[k];
         ok = t <= BLK_CAP;
         if (!ok) atomicExch(overflow, 1);
+        else atomicMax(maxlen, (int)t);
         nuniq = 0;
     }
     __syncthreads();
@@ -803,7 +891,9 @@ static int launch_bspmm(const GroupMap& gm, const int64_t* gptr, const int32_t* 
 }
 
 // key, payload, weight per gathered entry; band kinds add the window key and position
-static size_t block_smem(int kind) { return (size_t)BLK_CAP * (kind == 3 || kind == 4 ? 20 : 12); }
+static size_t block_smem(int kind, int cap) {
+    return (size_t)cap * (kind == 3 || kind == 4 ? 20 : 12);
+}
 
 }  // namespace splatct
 
@@ -840,12 +930,13 @@ int splatct_proj_block_count(const int64_t* ptr, const int32_t* idx, int nrows, 
     int64_t* cnt = reinterpret_cast<int64_t*>(scratch);
     char* scan_tmp = reinterpret_cast<char*>(scratch) + align_up(sizeof(int64_t) * (ng + 1));
     int* overflow = reinterpret_cast<int*>(scan_tmp + scan_temp_bytes(ng + 1));
+    int* maxlen = overflow + 1;   // the largest group's entry count, for the fill
     SPLATCT_CK(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (ng + 1), s));
-    SPLATCT_CK(cudaMemsetAsync(overflow, 0, sizeof(int), s));
+    SPLATCT_CK(cudaMemsetAsync(overflow, 0, 2 * sizeof(int), s));
     static bool attr = false;
     if (!attr) {
         SPLATCT_CK(cudaFuncSetAttribute(k_block_build, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)block_smem(3)));
+                                        (int)block_smem(3, BLK_CAP)));
         SPLATCT_CK(cudaFuncSetAttribute(k_block_count_hash,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         HC_SLOTS * (int)sizeof(uint32_t)));
@@ -855,11 +946,11 @@ int splatct_proj_block_count(const int64_t* ptr, const int32_t* idx, int nrows, 
     const char* how = getenv("SPLATCT_BLOCK_COUNT");
     if (!gm.band() && !(how && !strcmp(how, "sort"))) {
         k_block_count_hash<<<(unsigned)ng, BLK_NT, HC_SLOTS * sizeof(uint32_t), s>>>(
-            gm, ptr, idx, cnt, overflow);
+            gm, ptr, idx, cnt, overflow, maxlen);
     } else {
-        k_block_build<<<(unsigned)ng, BLK_NT, block_smem(kind), s>>>(
+        k_block_build<<<(unsigned)ng, BLK_NT, block_smem(kind, BLK_CAP), s>>>(
             gm, ptr, idx, nullptr, reinterpret_cast<const float2*>(order_dir), 0, cnt, nullptr,
-            nullptr, nullptr, overflow);
+            nullptr, nullptr, overflow, BLK_CAP, maxlen);
     }
     SPLATCT_LAUNCH_CK();
     if (int e = exclusive_scan_i64(cnt, gptr, ng + 1, scan_tmp, s)) return e;
@@ -885,11 +976,24 @@ int splatct_proj_block_fill(const int64_t* ptr, const int32_t* idx, const float*
     int* overflow = reinterpret_cast<int*>(reinterpret_cast<char*>(scratch) +
                                            align_up(sizeof(int64_t) * (ng + 1)) +
                                            scan_temp_bytes(ng + 1));
-    k_block_build<<<(unsigned)ng, BLK_NT, block_smem(kind), s>>>(
-        gm, ptr, idx, val, reinterpret_cast<const float2*>(order_dir), 1, nullptr, gptr, gidx,
-        reinterpret_cast<float4*>(gval), overflow);
-    SPLATCT_LAUNCH_CK();
+    // SPLATCT_BLOCK_FILL=sort: rows sorted by column are merged through the sort too (test knob)
+    const char* how = getenv("SPLATCT_BLOCK_FILL");
+    const int mode = how && !strcmp(how, "sort") ? 2 : 1;
+    // the shared arrays are sized for the largest group the count pass saw
+    int maxlen = 0;
+    SPLATCT_CK(cudaMemcpyAsync(&maxlen, overflow + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
     SPLATCT_CK(cudaStreamSynchronize(s));
+    int cap = 256;
+    while (cap < maxlen && cap < BLK_CAP) cap <<= 1;
+    k_block_build<<<(unsigned)ng, BLK_NT, block_smem(kind, cap), s>>>(
+        gm, ptr, idx, val, reinterpret_cast<const float2*>(order_dir), mode, nullptr, gptr, gidx,
+        reinterpret_cast<float4*>(gval), overflow, cap, nullptr);
+    SPLATCT_LAUNCH_CK();
+    int ovf = 0;
+    SPLATCT_CK(cudaMemcpyAsync(&ovf, overflow, sizeof(int), cudaMemcpyDeviceToHost, s));
+    SPLATCT_CK(cudaStreamSynchronize(s));
+    SPLATCT_REQUIRE(!ovf, "a row group has more entries than its count pass saw "
+                          "(splatct_proj_block_fill needs the scratch of splatct_proj_block_count)");
     return SPLATCT_OK;
 }
 

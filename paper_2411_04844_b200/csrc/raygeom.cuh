@@ -69,8 +69,16 @@ struct Geom {
 // A pixel's support is the open square (x-1,x+1)x(y-1,y+1); the samples
 // inside it are a contiguous k-range, so a pixel untouched by sample k is
 // final (the "open set" never holds more than 8 entries).
+//
+// Segment seg of nseg: the samples [ns*seg/nseg, ns*(seg+1)/nseg) open
+// pixels; the segment owns the pixels it opens and keeps marching past its
+// end until they are all closed, while pixels still open from the previous
+// sample at its start belong to an earlier segment and are skipped.  Every
+// pixel is therefore summed by exactly one segment, over the same samples in
+// the same order as by the whole-ray march (identical merged weights); only
+// the order of emission across segment boundaries differs.
 template <typename Emit>
-__device__ void march_ray(const Geom& g, int r, Emit emit) {
+__device__ void march_ray_seg(const Geom& g, int r, int seg, int nseg, Emit emit) {
     const int v = r / g.n_det, d = r % g.n_det;
     const double cx = 0.5 * (g.w - 1), cy = 0.5 * (g.h - 1);
     const double u = (d - 0.5 * (g.n_det - 1)) * g.spacing;
@@ -79,28 +87,57 @@ __device__ void march_ray(const Geom& g, int r, Emit emit) {
                  dy, t0, t1);
     if (!(t1 > t0)) return;
     const int64_t ns = (int64_t)((t1 - t0) / g.step);
-    int opix[8];
-    double ow[8], owt[8];
-    bool otouch[8];
-    int nopen = 0;
-    for (int64_t k = 0; k < ns; ++k) {
-        const double t = t0 + (k + 0.5) * g.step;
+    const int64_t kb = ns * seg / nseg, ke = ns * (seg + 1) / nseg;
+    if (kb >= ke) return;
+    // the 4 bilinear taps of sample k: pixel (or -1: outside / zero weight), weight
+    auto taps = [&](int64_t k, double& t, int (&px)[4], double (&tw)[4]) {
+        t = t0 + (k + 0.5) * g.step;
         const double sx = ox + t * dx, sy = oy + t * dy;
         const double fx0 = floor(sx), fy0 = floor(sy);
         const int64_t x0 = (int64_t)fx0, y0 = (int64_t)fy0;
         const double fx = sx - (double)x0, fy = sy - (double)y0;
-        for (int q = 0; q < nopen; ++q) otouch[q] = false;
         const int64_t tx[4] = {x0, x0 + 1, x0, x0 + 1};
         const int64_t ty[4] = {y0, y0, y0 + 1, y0 + 1};
-        const double tw[4] = {(1 - fx) * (1 - fy), fx * (1 - fy), (1 - fx) * fy, fx * fy};
+        tw[0] = (1 - fx) * (1 - fy);
+        tw[1] = fx * (1 - fy);
+        tw[2] = (1 - fx) * fy;
+        tw[3] = fx * fy;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            px[q] = (tx[q] < 0 || tx[q] >= g.w || ty[q] < 0 || ty[q] >= g.h || tw[q] == 0.0)
+                        ? -1 : (int)(ty[q] * g.w + tx[q]);
+    };
+    int pre[4] = {-1, -1, -1, -1};   // pixels an earlier segment still has open
+    if (kb > 0) {
+        double t, tw[4];
+        taps(kb - 1, t, pre, tw);
+    }
+    int opix[8];
+    double ow[8], owt[8];
+    bool otouch[8];
+    int nopen = 0;
+    for (int64_t k = kb; k < ns; ++k) {
+        const bool opening = k < ke;
+        if (!opening && nopen == 0) break;
+        double t, tw[4];
+        int px[4];
+        taps(k, t, px, tw);
+        for (int q = 0; q < nopen; ++q) otouch[q] = false;
+        bool ptouch[4] = {false, false, false, false};
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            if (tx[q] < 0 || tx[q] >= g.w || ty[q] < 0 || ty[q] >= g.h || tw[q] == 0.0) continue;
-            const int pix = (int)(ty[q] * g.w + tx[q]);
+            const int pix = px[q];
+            if (pix < 0) continue;
+            bool earlier = false;
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (pre[e] == pix) { ptouch[e] = true; earlier = true; }
+            if (earlier) continue;
             int f = -1;
             for (int e = 0; e < nopen; ++e)
                 if (opix[e] == pix) f = e;
             if (f < 0) {
+                if (!opening) continue;   // a later segment's pixel
                 f = nopen++;
                 opix[f] = pix;
                 ow[f] = 0.0;
@@ -110,6 +147,9 @@ __device__ void march_ray(const Geom& g, int r, Emit emit) {
             owt[f] += tw[q] * t;
             otouch[f] = true;
         }
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            if (!ptouch[e]) pre[e] = -1;   // closed: it cannot be touched again
         int keep = 0;
         for (int e = 0; e < nopen; ++e) {
             if (!otouch[e]) {
@@ -125,6 +165,11 @@ __device__ void march_ray(const Geom& g, int r, Emit emit) {
         nopen = keep;
     }
     for (int e = 0; e < nopen; ++e) emit(opix[e], ow[e], owt[e]);
+}
+
+template <typename Emit>
+__device__ void march_ray(const Geom& g, int r, Emit emit) {
+    march_ray_seg(g, r, 0, 1, emit);
 }
 
 }  // namespace splatct

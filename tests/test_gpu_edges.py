@@ -386,20 +386,57 @@ def test_projector_band_groups_match_4ray_groups(groups, monkeypatch):
         D.ProjectorOperator(big, 512, 512, 0.5, dev)
 
 
-@pytest.mark.parametrize("size", [256, 512])
-def test_block_count_hash_matches_sort(size, monkeypatch):
-    """The blocked operators' count pass (a shared-memory hash set of the
-    group's pixels) gives the same group sizes as counting with the fill's
-    sort, so the built operators are identical (C2 / C4 fan geometries)."""
+@pytest.mark.parametrize("geom,w,h", [
+    (core.ScanGeometry.fan(50, 512, 1.6, 512.0, 512.0), 256, 256),
+    (core.ScanGeometry.parallel(13, 70, 1.3), 41, 29),
+    (core.ScanGeometry.fan(7, 20, 0.9, 12.0, 9.0), 5, 7)])
+def test_march_segments_same_operator(geom, w, h, monkeypatch):
+    """The operator's ray march split into segments per ray (a thread each)
+    merges exactly the weights of the whole-ray march: every ray has the same
+    (pixel, weight) entries bitwise, only their order inside the row differs,
+    and the blocked operators built from them are identical."""
     import torch
     from paper_2411_04844_b200 import device as D
     dev = D.require_cuda()
-    geom = (core.ScanGeometry.fan(50, 512, 1.6, 512.0, 512.0) if size == 256
-            else core.ScanGeometry.fan(100, 1024, 1.6, 1024.0, 1024.0))
+    monkeypatch.setenv("SPLATCT_MARCH_SEGMENTS", "1")
+    ref = D.ProjectorOperator(geom, w, h, 0.5, dev)
+    monkeypatch.delenv("SPLATCT_MARCH_SEGMENTS")
+    op = D.ProjectorOperator(geom, w, h, 0.5, dev)
+    assert torch.equal(ref.a_ptr, op.a_ptr) and ref.nnz == op.nnz > 0
+
+    def rows_sorted(o):
+        lens = o.a_ptr[1:] - o.a_ptr[:-1]
+        row = torch.repeat_interleave(torch.arange(o.n_rays, device=dev), lens)
+        perm = torch.argsort(row * (w * h) + o.a_col.long()[:o.nnz])
+        return o.a_col[:o.nnz][perm], o.a_val[:o.nnz][perm]
+    for u, v in zip(rows_sorted(ref), rows_sorted(op)):
+        assert torch.equal(u, v)
+    for x, y in ((ref.at_ptr, op.at_ptr), (ref.at_ray, op.at_ray), (ref.at_val, op.at_val)):
+        assert torch.equal(x, y)
+    for a, b in ((ref.fb, op.fb), (ref.ab, op.ab)):
+        assert a[3] == b[3]
+        for u, v in zip(a[:3], b[:3]):
+            assert torch.equal(u, v)
+
+
+@pytest.mark.parametrize("size", [256, 512, 37])
+def test_block_build_without_sorts_matches_sort(size, monkeypatch):
+    """The blocked operators built without sorting where the rows allow it --
+    the count pass as a shared-memory hash set of the group's pixels, the
+    pixel quads' fill as a merge of their ray-sorted rows -- are identical to
+    the ones the bitonic sort builds (C2 / C4 fan geometries, a ragged one)."""
+    import torch
+    from paper_2411_04844_b200 import device as D
+    dev = D.require_cuda()
+    geom = {256: core.ScanGeometry.fan(50, 512, 1.6, 512.0, 512.0),
+            512: core.ScanGeometry.fan(100, 1024, 1.6, 1024.0, 1024.0),
+            37: core.ScanGeometry.parallel(11, 45, 1.2)}[size]
     monkeypatch.setenv("SPLATCT_BLOCK_COUNT", "sort")
-    ref = D.ProjectorOperator(geom, size, size, 0.5, dev)
+    monkeypatch.setenv("SPLATCT_BLOCK_FILL", "sort")
+    ref = D.ProjectorOperator(geom, size, size - size // 5, 0.5, dev)
     monkeypatch.delenv("SPLATCT_BLOCK_COUNT")
-    op = D.ProjectorOperator(geom, size, size, 0.5, dev)
+    monkeypatch.delenv("SPLATCT_BLOCK_FILL")
+    op = D.ProjectorOperator(geom, size, size - size // 5, 0.5, dev)
     for a, b in ((ref.fb, op.fb), (ref.ab, op.ab)):
         assert a[3] == b[3]
         for u, v in zip(a[:3], b[:3]):
