@@ -50,8 +50,10 @@ def main():
         optim.run_reconstruction(meas, geom, st, init_cloud=cloud)
         torch.cuda.synchronize()
         print(f"plain run {rep}: {1e3 * (time.perf_counter() - t0):.1f} ms")
-    for name in ("cloud_to_params", "params_to_cloud", "to_pinned_host", "pinned_output"):
+    for name in ("cloud_to_params", "params_to_cloud", "to_pinned_host", "pinned_output",
+                 "params_to_host", "cloud_from_host"):
         wrap(D, name)
+    wrap(D.StagedHost, "__init__")
     wrap(optim, "_trainer_for")
     from paper_2411_04844_b200.trainer import Trainer
     wrap(D.StagedHost, "to")
@@ -62,7 +64,8 @@ def main():
     optim.run_reconstruction(meas, geom, st, init_cloud=cloud)
     torch.cuda.synchronize()
     tot = 1e3 * (time.perf_counter() - t0)
-    print(f"instrumented run: {tot:.1f} ms; " + ", ".join(f"{k} {v:.2f}" for k, v in T.items()))
+    print(f"instrumented run: {tot:.1f} ms; " + ", ".join(f"{k} {v:.2f}" for k, v in T.items())
+          + f"; not in a wrapper {tot - sum(T.values()):.2f}")
 
 
 if __name__ == "__main__":

@@ -29,15 +29,15 @@ def main():
     truth, geom, box, cloud = bench.make_problem(cfg)
     dev = torch.device("cuda", 0)
     w, h, c = cfg["dims"]
-    op = D.projector_for(geom, w, h, 0.5, dev)
-    meas = op.forward(D.zyx_to_yxz(truth.zyx, dev))
+    op = D.operator_for(geom, w, h, c, 0.5, dev)   # per-slice or cone
+    meas = op.forward(D.zyx_to_yxz(np.ascontiguousarray(truth.zyx), dev))
     tr = Trainer(meas, geom, cfg["dims"], box, L.LossWeights(), D.cloud_to_params(cloud, dev),
                  max_iters=1000, trace_cap=a.iters + 1)
     tr.initial_volume()
     for _ in range(a.iters):
         tr.iteration()
     torch.cuda.synchronize()
-    print("loss trace", tr.trace_rows()[:, 0], "nnz", op.nnz)
+    print("loss trace", tr.trace_rows()[:, 0], "nnz", getattr(op, "nnz", None))
 
 
 if __name__ == "__main__":
