@@ -82,6 +82,23 @@ def cloud_from_host(h: np.ndarray) -> GaussianCloud:
     return GaussianCloud(h[: 3 * n].reshape(n, 3), h[3 * n: 4 * n], h[4 * n:])
 
 
+class CloudDownload:
+    """params_to_host queued on the current stream (into the cached page-locked
+    buffer) without waiting; cloud() waits for it and builds the GaussianCloud."""
+
+    def __init__(self, params: torch.Tensor):
+        p = params.detach()
+        packed = torch.cat([p[0:3].t().reshape(-1), p[3], p[4]])
+        self.st = _pinned(packed.numel(), packed.dtype)
+        self.st.copy_(packed, non_blocking=True)
+        self.ev = torch.cuda.Event()
+        self.ev.record(torch.cuda.current_stream(p.device))
+
+    def cloud(self) -> GaussianCloud:
+        self.ev.synchronize()
+        return cloud_from_host(self.st.numpy().copy())
+
+
 def params_to_cloud(params: torch.Tensor) -> GaussianCloud:
     """The inverse of cloud_to_params."""
     return cloud_from_host(params_to_host(params))
