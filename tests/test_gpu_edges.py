@@ -419,6 +419,39 @@ def test_march_segments_same_operator(geom, w, h, monkeypatch):
             assert torch.equal(u, v)
 
 
+def test_block_fill_needs_its_count_scratch():
+    """The fill sizes its shared arrays from what the count left in the
+    scratch: given a scratch its count did not fill, it fails loudly instead of
+    building a wrong operator."""
+    import ctypes
+    import torch
+    from paper_2411_04844_b200 import device as D
+    from paper_2411_04844_b200._lib import SplatctError, call, size_query
+    dev = D.require_cuda()
+    op = D.ProjectorOperator(core.ScanGeometry.fan(50, 512, 1.6, 512.0, 512.0), 256, 256, 0.5,
+                             dev)
+    sb = size_query("splatct_proj_block_scratch_bytes", op.n_rays, 0, 256, 256)
+    ng = (op.n_rays + 3) // 4
+    gptr = torch.empty(ng + 1, dtype=torch.int64, device=dev)
+    nb = ctypes.c_int64(0)
+    dirs = op._group_dirs(4)
+    scratch = torch.zeros(sb, dtype=torch.uint8, device=dev)
+    call("splatct_proj_block_count", D.ptr(op.a_ptr), D.ptr(op.a_col), op.n_rays, 0, 256, 256,
+         D.ptr(dirs), D.ptr(gptr), D.ptr(scratch), sb, ctypes.byref(nb), D.stream_handle())
+    assert torch.equal(gptr, op.fb[0]) and nb.value == op.fb[3]
+    gidx = torch.empty(nb.value, dtype=torch.int32, device=dev)
+    gval = torch.empty((nb.value, 4), dtype=torch.float32, device=dev)
+    fresh = torch.zeros(sb, dtype=torch.uint8, device=dev)
+    with pytest.raises(SplatctError):
+        call("splatct_proj_block_fill", D.ptr(op.a_ptr), D.ptr(op.a_col), D.ptr(op.a_val),
+             op.n_rays, 0, 256, 256, D.ptr(dirs), D.ptr(gptr), D.ptr(gidx), D.ptr(gval),
+             D.ptr(fresh), sb, D.stream_handle())
+    call("splatct_proj_block_fill", D.ptr(op.a_ptr), D.ptr(op.a_col), D.ptr(op.a_val),
+         op.n_rays, 0, 256, 256, D.ptr(dirs), D.ptr(gptr), D.ptr(gidx), D.ptr(gval),
+         D.ptr(scratch), sb, D.stream_handle())
+    assert torch.equal(gidx, op.fb[1]) and torch.equal(gval, op.fb[2])
+
+
 @pytest.mark.parametrize("size", [256, 512, 37])
 def test_block_build_without_sorts_matches_sort(size, monkeypatch):
     """The blocked operators built without sorting where the rows allow it --
