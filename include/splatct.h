@@ -244,6 +244,23 @@ int splatct_proj_forward_blocked(const int64_t* gptr, const int32_t* gidx, const
                                  int n_rays, int kind, const float* vol_yxz, float* sino, int c,
                                  const uint64_t* col_occ, int w, int h, const int* halt,
                                  void* stream);
+/* The forward's launch shape for a c-slice volume: *ctas CTAs over ngroups x
+ * *zsplit (group, z-chunk) warp tasks, 4 per CTA, CTA b taking tasks 4b..4b+3
+ * in group-major order; *ordered = 1 when the launch honours a CTA order
+ * (not for bands, nor in the z-chunk-major order used once the volume
+ * outgrows ~3/4 of L2). */
+int splatct_proj_forward_ctas(int n_rays, int kind, int w, int h, int c, int64_t* ctas,
+                              int* zsplit, int* ordered);
+/* splatct_proj_forward_blocked with cta_order (device int32[*ctas], a
+ * permutation, or NULL): CTA b runs CTA cta_order[b]'s tasks.  Listing the
+ * CTAs with the most entries first shortens the grid's tail; the results are
+ * bitwise those of the default order. */
+int splatct_proj_forward_blocked_ordered(const int64_t* gptr, const int32_t* gidx,
+                                         const float* gval, int n_rays, int kind,
+                                         const float* vol_yxz, float* sino, int c,
+                                         const uint64_t* col_occ, int w, int h,
+                                         const int32_t* cta_order, const int* halt,
+                                         void* stream);
 /* col_occ (optional, NULL = dense): the voxelizer's footprint coverage of
  * vol_yxz (splatct_fvr_footprint_coverage_offset).  A 2x2-pixel quad x
  * z-chunk whose one-voxel neighbourhood no footprint covers is skipped: its

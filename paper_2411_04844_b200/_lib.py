@@ -20,6 +20,7 @@ c_sz = ctypes.c_size_t
 c_vp = ctypes.c_void_p
 c_szp = ctypes.POINTER(ctypes.c_size_t)
 c_i64p = ctypes.POINTER(ctypes.c_int64)
+c_i32p = ctypes.POINTER(ctypes.c_int)
 c_vpp = ctypes.POINTER(ctypes.c_void_p)
 
 # name -> argtypes (all return int status except where noted)
@@ -64,6 +65,9 @@ SIGNATURES: dict[str, list] = {
                                 c_vp, c_sz, c_vp],
     "splatct_proj_forward_blocked": [c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_i32, c_vp,
                                      c_i32, c_i32, c_vp, c_vp],
+    "splatct_proj_forward_ctas": [c_i32, c_i32, c_i32, c_i32, c_i32, c_i64p, c_i32p, c_i32p],
+    "splatct_proj_forward_blocked_ordered": [c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_i32,
+                                             c_vp, c_i32, c_i32, c_vp, c_vp, c_vp],
     "splatct_fvr_footprint_coverage_offset": [c_i64, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32,
                                               c_szp],
     "splatct_fvr_pixel_occupancy_offset": [c_i64, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32,

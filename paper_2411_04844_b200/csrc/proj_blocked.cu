@@ -424,6 +424,7 @@ __device__ __forceinline__ int sgnf(float d) { return (d > 0.f) - (d < 0.f); }
 struct Occ {
     const unsigned long long* occ;
     int w, ntx, mode;   // mode 1: forward entry skipping, 2: adjoint quad skipping
+    const int32_t* order = nullptr;   // CTA visit order (group-major launches only)
 };
 
 constexpr int BS_WARPS = 4;
@@ -619,7 +620,9 @@ __global__ void __launch_bounds__(32 * BS_WARPS, R == 8 ? 4 : 6) k_bspmm(GroupMa
     __shared__ int s_col[BS_WARPS][32];
     __shared__ float4 s_w[BS_WARPS][32 * RW];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t gw = blockIdx.x * (int64_t)BS_WARPS + wid;
+    // CTA b runs the work of CTA order[b]: the host lists the longest first
+    const int64_t bid = oc.order ? (int64_t)oc.order[blockIdx.x] : (int64_t)blockIdx.x;
+    const int64_t gw = bid * BS_WARPS + wid;
     // zmajor (gathered operand larger than L2): z-chunk-major order, so the
     // warps in flight share one z-chunk and the L2 working set is 1/zsplit of
     // the operand (C4: 512 MB volume); otherwise a group's chunks run together
@@ -850,20 +853,22 @@ static int launch_bspmm_v(const GroupMap& gm, const int64_t* gptr, const int32_t
     // proxy for the adjoint's sinogram) outgrows ~3/4 of L2
     const int zmajor = zsplit > 1 && vol_bytes > ((int64_t)96 << 20);
     const unsigned grid = (unsigned)((warps + BS_WARPS - 1) / BS_WARPS);
+    Occ oc_ = oc;
+    if (zmajor || gm.band()) oc_.order = nullptr;   // chunk-major order is kept as it is
     const float4* gv = reinterpret_cast<const float4*>(gval);
     if (!TV && gm.band()) {
         if (gm.kind == 4)
             SPLATCT_CK(launch_pdl(k_bspmm_band<V, 16>, dim3(grid), dim3(32 * BS_WARPS), 0, s, gm,
-                                  gptr, gidx, gv, X, Y, c, zsplit, zmajor, oc, halt));
+                                  gptr, gidx, gv, X, Y, c, zsplit, zmajor, oc_, halt));
         else
             SPLATCT_CK(launch_pdl(k_bspmm_band<V, 8>, dim3(grid), dim3(32 * BS_WARPS), 0, s, gm,
-                                  gptr, gidx, gv, X, Y, c, zsplit, zmajor, oc, halt));
+                                  gptr, gidx, gv, X, Y, c, zsplit, zmajor, oc_, halt));
     } else if (!TV && gm.rows() == 8)
         SPLATCT_CK(launch_pdl(k_bspmm<V, false, 8>, dim3(grid), dim3(32 * BS_WARPS), 0, s, gm,
-                              gptr, gidx, gv, X, Y, c, zsplit, zmajor, tv, oc, halt));
+                              gptr, gidx, gv, X, Y, c, zsplit, zmajor, tv, oc_, halt));
     else
         SPLATCT_CK(launch_pdl(k_bspmm<V, TV, 4>, dim3(grid), dim3(32 * BS_WARPS), 0, s, gm, gptr,
-                              gidx, gv, X, Y, c, zsplit, zmajor, tv, oc, halt));
+                              gidx, gv, X, Y, c, zsplit, zmajor, tv, oc_, halt));
     SPLATCT_LAUNCH_CK();
     return SPLATCT_OK;
 }
@@ -997,18 +1002,41 @@ int splatct_proj_block_fill(const int64_t* ptr, const int32_t* idx, const float*
     return SPLATCT_OK;
 }
 
+int splatct_proj_forward_ctas(int n_rays, int kind, int w, int h, int c, int64_t* ctas,
+                              int* zsplit, int* ordered) {
+    SPLATCT_REQUIRE(n_rays >= 0 && c > 0 && w > 0 && h > 0, "invalid sizes");
+    GroupMap gm{kind, n_rays, 0, 0};
+    const int V = vec_width(c);
+    const int zs = (c + 32 * V - 1) / (32 * V);
+    *zsplit = zs;
+    *ctas = (gm.ngroups() * zs + BS_WARPS - 1) / BS_WARPS;
+    *ordered = !gm.band() && !(zs > 1 && (int64_t)w * h * c * 4 > ((int64_t)96 << 20));
+    return SPLATCT_OK;
+}
+
 int splatct_proj_forward_blocked(const int64_t* gptr, const int32_t* gidx, const float* gval,
                                  int n_rays, int kind, const float* vol_yxz, float* sino, int c,
                                  const uint64_t* col_occ, int w, int h, const int* halt,
                                  void* stream) {
+    return splatct_proj_forward_blocked_ordered(gptr, gidx, gval, n_rays, kind, vol_yxz, sino, c,
+                                                col_occ, w, h, nullptr, halt, stream);
+}
+
+int splatct_proj_forward_blocked_ordered(const int64_t* gptr, const int32_t* gidx,
+                                         const float* gval, int n_rays, int kind,
+                                         const float* vol_yxz, float* sino, int c,
+                                         const uint64_t* col_occ, int w, int h,
+                                         const int32_t* cta_order, const int* halt,
+                                         void* stream) {
     SPLATCT_REQUIRE(n_rays >= 0 && c > 0 && w > 0 && h > 0, "invalid sizes");
     SPLATCT_REQUIRE(kind == 0 || kind == 2 || kind == 3 || kind == 4,
                     "forward groups are kind 0, 2, 3 or 4");
     SPLATCT_REQUIRE(col_occ == nullptr || c <= 64 * 16, "occupancy needs <= 64 z tiles");
     GroupMap gm{kind, n_rays, 0, 0};
     TvB tv{};
-    const Occ oc{reinterpret_cast<const unsigned long long*>(col_occ), w, (w + 15) / 16,
-                 col_occ ? 1 : 0};
+    Occ oc{reinterpret_cast<const unsigned long long*>(col_occ), w, (w + 15) / 16,
+           col_occ ? 1 : 0};
+    oc.order = cta_order;
     return launch_bspmm<false>(gm, gptr, gidx, gval, vol_yxz, sino, c, tv, halt,
                                as_stream(stream), oc, (int64_t)w * h * c * 4);
 }

@@ -594,13 +594,40 @@ class ProjectorOperator:
         occ = _occ(occ, "pixel")
         if self.blocked if blocked is None else blocked:
             g = self.fb
-            call("splatct_proj_forward_blocked", ptr(g[0]), ptr(g[1]), ptr(g[2]), self.n_rays,
-                 self.fkind, ptr(vol), ptr(out), c, occ if occ is not None else VP(0), self.w,
-                 self.h, ptr(halt), stream_handle())
+            call("splatct_proj_forward_blocked_ordered", ptr(g[0]), ptr(g[1]), ptr(g[2]),
+                 self.n_rays, self.fkind, ptr(vol), ptr(out), c,
+                 occ if occ is not None else VP(0), self.w, self.h,
+                 ptr(self._forward_order(c)), ptr(halt), stream_handle())
         else:
             call("splatct_proj_forward", ptr(self.a_ptr), ptr(self.a_col), ptr(self.a_val),
                  self.n_rays, ptr(vol), ptr(out), c, ptr(halt), stream_handle())
         return out
+
+    def _forward_order(self, c: int):
+        """The blocked forward's CTAs, those with the longest warp task first
+        (None: default order).  A CTA lasts as long as its longest (group,
+        z-chunk) task, about its group's entry count; launching the long ones
+        first leaves short ones for the grid's tail (C2: 0.229 -> 0.200 ms).
+        Computed once per slice depth, outside any graph capture."""
+        cache = self.__dict__.setdefault("_orders", {})
+        if c in cache:
+            return cache[c]
+        if torch.cuda.is_current_stream_capturing():
+            return None
+        ctas, zs, ordered = ctypes.c_int64(0), ctypes.c_int(0), ctypes.c_int(0)
+        call("splatct_proj_forward_ctas", self.n_rays, self.fkind, self.w, self.h, c,
+             ctypes.byref(ctas), ctypes.byref(zs), ctypes.byref(ordered))
+        order = None
+        if ordered.value and ctas.value > 1:
+            gptr = self.fb[0]
+            work = gptr[1:] - gptr[:-1]
+            ng, z, n = work.numel(), zs.value, ctas.value
+            task = torch.arange(4 * n, device=self.device)   # CTA b: tasks 4b .. 4b + 3
+            wk = torch.where(task < ng * z, work[(task // z).clamp(max=ng - 1)],
+                             torch.zeros_like(task))
+            order = torch.argsort(-wk.view(n, 4).amax(1), stable=True).to(torch.int32)
+        cache[c] = order
+        return order
 
     def adjoint(self, gsino: torch.Tensor, out: torch.Tensor | None = None, vol=None,
                 halo_lo=None, halo_hi=None, lambda_tv: float = 0.0, tv_count: float = 1.0,

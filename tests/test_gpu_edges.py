@@ -419,6 +419,40 @@ def test_march_segments_same_operator(geom, w, h, monkeypatch):
             assert torch.equal(u, v)
 
 
+@pytest.mark.parametrize("c", [256, 100, 1040])
+def test_forward_cta_order_is_bitwise_neutral(c):
+    """The blocked forward launched with its CTAs longest-first gives bitwise
+    the default order's sinogram; the order covers every CTA once (the
+    z-chunk-major launch of volumes beyond ~3/4 of L2 takes no order)."""
+    import ctypes
+    import torch
+    from paper_2411_04844_b200 import device as D
+    from paper_2411_04844_b200._lib import call
+    dev = D.require_cuda()
+    w = h = 256 if c != 1040 else 160
+    op = D.ProjectorOperator(core.ScanGeometry.fan(50, 512, 1.6, 512.0, 512.0), w, h, 0.5, dev)
+    g = torch.Generator(device="cpu").manual_seed(11)
+    vol = torch.rand((h, w, c), generator=g).to(dev)
+    vol[:, :, : c // 3] = 0.0
+    order = op._forward_order(c)
+    ctas, zs, ordered = ctypes.c_int64(0), ctypes.c_int(0), ctypes.c_int(0)
+    call("splatct_proj_forward_ctas", op.n_rays, op.fkind, w, h, c, ctypes.byref(ctas),
+         ctypes.byref(zs), ctypes.byref(ordered))
+    if c == 1040:
+        assert ordered.value == 0 and order is None
+        return
+    assert order is not None and order.numel() == ctas.value
+    assert torch.equal(torch.sort(order.long()).values, torch.arange(ctas.value, device=dev))
+    a = torch.full((op.m, op.n_det, c), float("nan"), device=dev)
+    b = torch.full_like(a, float("nan"))
+    fb = op.fb
+    for dst, o in ((a, None), (b, order)):
+        call("splatct_proj_forward_blocked_ordered", D.ptr(fb[0]), D.ptr(fb[1]), D.ptr(fb[2]),
+             op.n_rays, op.fkind, D.ptr(vol), D.ptr(dst), c, D.VP(0), w, h, D.ptr(o), D.VP(0),
+             D.stream_handle())
+    assert torch.isfinite(a).all() and torch.equal(a, b)
+
+
 def test_block_fill_needs_its_count_scratch():
     """The fill sizes its shared arrays from what the count left in the
     scratch: given a scratch its count did not fill, it fails loudly instead of
