@@ -245,10 +245,12 @@ int splatct_proj_forward_blocked(const int64_t* gptr, const int32_t* gidx, const
                                  const uint64_t* col_occ, int w, int h, const int* halt,
                                  void* stream);
 /* The forward's launch shape for a c-slice volume: *ctas CTAs over ngroups x
- * *zsplit (group, z-chunk) warp tasks, 4 per CTA, CTA b taking tasks 4b..4b+3
- * in group-major order; *ordered = 1 when the launch honours a CTA order
- * (not for bands, nor in the z-chunk-major order used once the volume
- * outgrows ~3/4 of L2). */
+ * *zsplit (group, z-chunk) warp tasks, 4 per CTA, CTA b taking tasks
+ * 4b..4b+3.  *ordered: 1 = tasks are group-major (task t: group t / zsplit,
+ * chunk t % zsplit); 2 = z-chunk-major, used once the volume outgrows ~3/4 of
+ * L2 (group t % ngroups, chunk t / ngroups) -- an order should then keep each
+ * chunk's CTAs together, so the warps in flight keep sharing one chunk;
+ * 0 = bands, which take no order. */
 int splatct_proj_forward_ctas(int n_rays, int kind, int w, int h, int c, int64_t* ctas,
                               int* zsplit, int* ordered);
 /* splatct_proj_forward_blocked with cta_order (device int32[*ctas], a

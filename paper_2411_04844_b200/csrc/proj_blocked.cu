@@ -854,7 +854,7 @@ static int launch_bspmm_v(const GroupMap& gm, const int64_t* gptr, const int32_t
     const int zmajor = zsplit > 1 && vol_bytes > ((int64_t)96 << 20);
     const unsigned grid = (unsigned)((warps + BS_WARPS - 1) / BS_WARPS);
     Occ oc_ = oc;
-    if (zmajor || gm.band()) oc_.order = nullptr;   // chunk-major order is kept as it is
+    if (gm.band()) oc_.order = nullptr;
     const float4* gv = reinterpret_cast<const float4*>(gval);
     if (!TV && gm.band()) {
         if (gm.kind == 4)
@@ -1010,7 +1010,8 @@ int splatct_proj_forward_ctas(int n_rays, int kind, int w, int h, int c, int64_t
     const int zs = (c + 32 * V - 1) / (32 * V);
     *zsplit = zs;
     *ctas = (gm.ngroups() * zs + BS_WARPS - 1) / BS_WARPS;
-    *ordered = !gm.band() && !(zs > 1 && (int64_t)w * h * c * 4 > ((int64_t)96 << 20));
+    const bool zmajor = zs > 1 && (int64_t)w * h * c * 4 > ((int64_t)96 << 20);
+    *ordered = gm.band() ? 0 : (zmajor ? 2 : 1);
     return SPLATCT_OK;
 }
 

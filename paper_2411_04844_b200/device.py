@@ -623,9 +623,13 @@ class ProjectorOperator:
             work = gptr[1:] - gptr[:-1]
             ng, z, n = work.numel(), zs.value, ctas.value
             task = torch.arange(4 * n, device=self.device)   # CTA b: tasks 4b .. 4b + 3
-            wk = torch.where(task < ng * z, work[(task // z).clamp(max=ng - 1)],
-                             torch.zeros_like(task))
-            order = torch.argsort(-wk.view(n, 4).amax(1), stable=True).to(torch.int32)
+            grp = task // z if ordered.value == 1 else task % ng
+            wk = torch.where(task < ng * z, work[grp.clamp(max=ng - 1)], torch.zeros_like(task))
+            key = -wk.view(n, 4).amax(1)
+            if ordered.value == 2:   # z-chunk-major: longest first within each chunk
+                chunk = task.view(n, 4)[:, 0] // ng
+                key = key + chunk * (int(work.max().item()) + 1)
+            order = torch.argsort(key, stable=True).to(torch.int32)
         cache[c] = order
         return order
 
