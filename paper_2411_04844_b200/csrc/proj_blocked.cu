@@ -428,6 +428,9 @@ struct Occ {
 };
 
 constexpr int BS_WARPS = 4;
+#ifndef BS_MINB
+#define BS_MINB 6   // CTAs per SM (80 registers); swept 4..8, tools/jobs/bs_minb.sh
+#endif
 constexpr int UNR = 8;    // z-vector gathers in flight per warp (16 measured no faster)
 
 // Per-lane accumulators of the R group rows over the lane's V slices, held
@@ -607,7 +610,7 @@ __device__ __forceinline__ void tv_epilogue_quad(const TvB& a, const GroupMap& g
 // column load.  Entries are staged per warp in shared memory and consumed
 // UNR at a time (UNR independent vector loads in flight).
 template <int V, bool TV, int R>
-__global__ void __launch_bounds__(32 * BS_WARPS, R == 8 ? 4 : 6) k_bspmm(GroupMap gm, const int64_t* __restrict__ gptr,
+__global__ void __launch_bounds__(32 * BS_WARPS, R == 8 ? 4 : BS_MINB) k_bspmm(GroupMap gm, const int64_t* __restrict__ gptr,
                                                         const int32_t* __restrict__ gidx,
                                                         const float4* __restrict__ gval,
                                                         const float* __restrict__ X,
