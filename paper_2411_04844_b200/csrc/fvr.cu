@@ -489,11 +489,17 @@ __global__ void __launch_bounds__(SORT_NT) k_onesweep(
 // with the 3xTF32 split (a_hi b_hi + a_hi b_lo + a_lo b_hi, fp32 accumulate),
 // which keeps fp32-level accuracy (the volume target is 1e-5 relative L2).
 // The separable tables (I ey, ex, ez; zero outside box, tile and volume) are
-// built 32 Gaussians at a time in shared memory exactly as before; padding
+// built 64 Gaussians at a time (FWD_BATCH) in shared memory exactly as before; padding
 // rows are zero so partial k8 steps contribute nothing.  Accumulators go
 // through an XOR-swizzled shared-memory tile for coalesced stores.
 // --------------------------------------------------------------------------
-constexpr int FWD_BATCH = 32;   // Gaussians staged per round (8 threads each)
+#ifndef FWD_TPG
+// table-builder threads per Gaussian: 4 = 64-Gaussian batches, half the block
+// barriers per Gaussian of 32-Gaussian batches (C2 0.100 -> 0.092 ms; 2 would
+// need 53 KB of static shared memory)
+#define FWD_TPG 4
+#endif
+constexpr int FWD_BATCH = 256 / FWD_TPG;   // Gaussians staged per round
 // per Gaussian row: ex_hi[16] | ex_lo[16] (TF32 split, A operand) | I ey[16] | ez[16] | pad
 constexpr int TAB_STRIDE = 72;  // 72 mod 32 = 8: the four k rows of a fragment hit distinct banks
 
@@ -574,7 +580,7 @@ __global__ void __launch_bounds__(256, 4) k_fvr_fwd(const GRec* __restrict__ rec
     float acc[4][4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
-    const int tg = threadIdx.x >> 3, tj = threadIdx.x & 7;   // table builder: Gaussian, part
+    const int tg = threadIdx.x / FWD_TPG, tj = threadIdx.x % FWD_TPG;   // table builder: Gaussian, part
 
     // the next batch's Gaussian records are loaded while this batch's MMAs run,
     // from pair values loaded one batch earlier still (the value -> record
@@ -599,15 +605,15 @@ __global__ void __launch_bounds__(256, 4) k_fvr_fwd(const GRec* __restrict__ rec
                     if (bx0 <= bx1) {
                         const unsigned xb = ((2u << (bx1 - x0)) - 1u) & ~((1u << (bx0 - x0)) - 1u);
 #pragma unroll
-                        for (int rr = 0; rr < 2; ++rr) {
-                            const int yy = y0 + tj + 8 * rr;
-                            if (yy >= by0 && yy <= by1) atomicOr(&s_rows[tj + 8 * rr], xb);
+                        for (int rr = 0; rr < TT / FWD_TPG; ++rr) {
+                            const int yy = y0 + tj + FWD_TPG * rr;
+                            if (yy >= by0 && yy <= by1) atomicOr(&s_rows[tj + FWD_TPG * rr], xb);
                         }
                     }
                 }
 #pragma unroll
-                for (int q = 0; q < 3 * TT / 8; ++q) {
-                    const int e = tj + 8 * q, a = e / TT, l = e % TT;   // compile-time a per q
+                for (int q = 0; q < 3 * TT / FWD_TPG; ++q) {
+                    const int e = tj + FWD_TPG * q, a = e / TT, l = e % TT;   // compile-time a per q
                     if (a == 0) {
                         uint32_t hi, lo;
                         tf32_split(tab_weight(x0 + l, 0, w, r.fx, hx, r.dx, r.inv2), hi, lo);
@@ -621,7 +627,7 @@ __global__ void __launch_bounds__(256, 4) k_fvr_fwd(const GRec* __restrict__ rec
                 }
             } else {
 #pragma unroll
-                for (int q = 0; q < 4 * TT / 8; ++q) row[tj + 8 * q] = 0.f;   // k8 padding
+                for (int q = 0; q < 4 * TT / FWD_TPG; ++q) row[tj + FWD_TPG * q] = 0.f;   // k8 padding
             }
         }
         __syncthreads();
