@@ -38,7 +38,10 @@ namespace splatct {
 
 constexpr int TT = SPLATCT_TILE;   // tile edge (16)
 constexpr int SORT_NT = 256;
-constexpr int SORT_IPT = 16;
+#ifndef SORT_IPT_N
+#define SORT_IPT_N 16
+#endif
+constexpr int SORT_IPT = SORT_IPT_N;   // keys per thread of a radix pass
 constexpr int SORT_CHUNK = SORT_NT * SORT_IPT;
 constexpr int RADIX = 256;
 constexpr int MAX_PASSES = 4;     // 8-bit digits of a 32-bit tile id
