@@ -873,7 +873,10 @@ struct FinParts {
     const double* sched;  // optional {lr, 1-b1^t, 1-b2^t} per pre-increment step (host-computed)
     int64_t sched_len;
 };
-constexpr int FIN_BLOCKS = 32, FIN_NT = 256;
+#ifndef FIN_BLOCKS_N
+#define FIN_BLOCKS_N 32
+#endif
+constexpr int FIN_BLOCKS = FIN_BLOCKS_N, FIN_NT = 256;
 
 __global__ void k_iter_finalize(double* __restrict__ sums, FinParts parts, double l1w,
                                 double ssw, double tvw, double l1_count, double ssim_count,
