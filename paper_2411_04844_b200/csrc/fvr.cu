@@ -503,6 +503,9 @@ __global__ void __launch_bounds__(SORT_NT) k_onesweep(
 #define FWD_TPG 4
 #endif
 constexpr int FWD_BATCH = 256 / FWD_TPG;   // Gaussians staged per round
+#ifndef FWD_MINB
+#define FWD_MINB 4   // CTAs per SM (64 registers)
+#endif
 // per Gaussian row: ex_hi[16] | ex_lo[16] (TF32 split, A operand) | I ey[16] | ez[16] | pad
 constexpr int TAB_STRIDE = 72;  // 72 mod 32 = 8: the four k rows of a fragment hit distinct banks
 
@@ -533,7 +536,7 @@ __device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], 
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-__global__ void __launch_bounds__(256, 4) k_fvr_fwd(const GRec* __restrict__ rec, int w, int h, int c,
+__global__ void __launch_bounds__(256, FWD_MINB) k_fvr_fwd(const GRec* __restrict__ rec, int w, int h, int c,
                                                  int zoff, int hx, int hy, int hz, int ntx,
                                                  int nty, int64_t nt, int S,
                                                  const uint32_t* __restrict__ tstart,
@@ -2777,7 +2780,7 @@ static int fvr_forward_impl(const double* params, int64_t n, int w, int h, int c
     FvrLayout L = make_layout(n, w, h, c, hx, hy, hz);
     if (int e = check_args(n, w, h, c, hx, hy, hz, ws_bytes, L)) return e;
     const size_t vo = L.final_buf ? L.o_v1 : L.o_v0;
-    const int64_t grid = L.nt < 148 * 4 ? L.nt : 148 * 4;   // persistent: 4 CTAs/SM resident
+    const int64_t grid = L.nt < 148 * FWD_MINB ? L.nt : 148 * FWD_MINB;   // persistent: all resident
     int64_t fetch = L.nt / (8 * grid);                       // >= 8 claims per CTA
     fetch = fetch < 1 ? 1 : (fetch > 32 ? 32 : fetch);
     // the bins zeroed the tile counter and the masks; the default kernel
